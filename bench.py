@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""Benchmark of the GPU join hot path (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c4|c1] [--impl ours|reference]
+
+Default workload (N=1): BASELINE.json configs[1] -- equi hash join of 2^27 x 2^27
+8-byte tuples (int32 key + int32 payload; payload never read), PK-FK "unique-ish"
+keys.  One step = the whole exact join: radix partition R and S,
+build/probe count, exclusive scan, D2H of |J|, build/probe write of all |J| pairs.
+Inputs are generated in HBM by the seeded generator twin before timing (1 GiB of
+keys > the 126 MB L2, so no L2 flush is needed between steps).
+
+`value` = input tuples/s = (n_R + n_S) * K / T (device time, CUDA events on the
+ctx stream, max over ranks).  `e2e` = the same metric through the host-buffer C-ABI
+entry `join_host` (pinned H2D of both key columns + D2H of all pairs inside the
+timed region).  `roofline` = the dominant kernel's algorithmic bytes per launch /
+its mean launch time (CUDA events around every launch on the ctx stream, in a
+second, profiled pass of the same K steps) vs MEASURED_PEAKS.json hbm_gbs.
+`cpu_baseline` = the CPU oracle (oracle/, O2 unordered_multimap hash join) timed on
+a bounded PK-FK sample on this host, 1 thread.
+
+--impl reference: this tier has no runnable reference implementation; the
+reference arm is the oracle itself, timed the same way on the host cores.
+
+N > 1 (torchrun): weak scaling -- every rank runs the same-size problem on its own
+GPU (the equi join shards by hash partition; the NCCL shuffle path is
+`join_dist_*`, measured separately once available).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "join input & output tuples/s at 1/2/4/8 B200; % of HBM/INT roofline"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Samples SM clock and clock-event reasons via NVML during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+            "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for k, v in names.items():
+                    if r & v and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ workloads
+
+def make_workload(name, device):
+    import torch
+    import gen
+    import gen.device as gd
+    seed = gen.BASE_SEED
+    if name == "c2":
+        b = 27
+        R = gd.perm_range(1 << b, b, seed, device=device)
+        S = gd.pkfk_S(1 << b, b, seed, device=device)
+        desc = "configs[1]: equi hash join 2^27 x 2^27 8-byte tuples (int32 key+payload, payload not read), PK-FK unique R keys"
+        return dict(kind="equi", R=R, S=S, desc=desc, n_out_expected=1 << b)
+    if name == "c1":
+        R = gd.uniform(10_000, 10_000, seed, 0, device=device)
+        S = gd.uniform(10_000, 10_000, seed, 1, device=device)
+        return dict(kind="equi", R=R, S=S, desc="configs[0]: R=S=10^4 uniform keys in [0,10^4), equi hash join")
+    if name == "c4":
+        R = gd.uniform(1 << 20, 1 << 30, seed, 0, device=device)
+        S = gd.uniform(1 << 24, 1 << 30, seed, 1, device=device)
+        return dict(kind="band", R=R, S=S, eps=gen.C4_EPS,
+                    desc="configs[3]: band join |R.a-S.b|<=53687, 2^20 x 2^24 uniform int32 in [0,2^30), count+scan+write")
+    raise SystemExit(f"unknown workload {name}")
+
+
+def algorithmic_bytes(w, ctxinfo):
+    """Algorithmic HBM bytes per launch of each kernel tag."""
+    nR, nS = w["R"].numel(), w["S"].numel()
+    nout = ctxinfo["n_out"]
+    if w["kind"] == "equi":
+        passes = ctxinfo["passes"]
+        n = nR + nS
+        # scatter: pass 1 reads the key (rid implicit) + writes key+rid; later passes read key+rid
+        scatter_total = (nR + nS) * (4 + 8) + (passes - 1) * (nR + nS) * (8 + 8)
+        return {
+            "part_hist": (4 * n * passes, 2 * passes),
+            "part_scatter": (scatter_total, 2 * passes),
+            "hj_count": (4 * n, 1),
+            "hj_write": (8 * n + 8 * nout, 1),
+        }
+    # band: NLJ is ALU-bound; bytes are tiny
+    return {"nlj_count": (4 * (nR + nS), 1), "nlj_write": (4 * (nR + nS) + 8 * nout, 1)}
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    import paper_1904_11201_b200 as gj
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    w = make_workload(args.workload, dev)
+    stream = torch.cuda.current_stream(dev)
+    ctx = gj.Context(local, stream)
+    R, S = w["R"], w["S"]
+    nR, nS = R.numel(), S.numel()
+
+    if w["kind"] == "equi":
+        n = gj.join_count(ctx, R, S)
+        out = torch.empty((max(n, 1), 2), dtype=torch.int32, device=dev)
+
+        def step():
+            m = gj.join_count(ctx, R, S)
+            gj.join_materialize(ctx, R, S, m, out=out)
+            return m
+    else:
+        eps = w["eps"]
+        n = gj.theta_join_count(ctx, R, S, "band", eps)
+        out = torch.empty((max(n, 1), 2), dtype=torch.int32, device=dev)
+
+        def step():
+            m = gj.theta_join_count(ctx, R, S, "band", eps)
+            gj.theta_join_materialize(ctx, R, S, "band", eps, m, out=out)
+            return m
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, device time by CUDA events on the ctx stream
+    sampler = ClockSampler(local)
+    ctx.reset_stats()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        e0.record(stream)
+        for _ in range(args.steps):
+            m = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launches()
+    assert m == n
+    ms_max = max_over_ranks(ms, world)
+
+    # ---- profiled pass (per-kernel CUDA events on the ctx stream)
+    ctx.set_option("profile", 1)
+    ctx.reset_stats()
+    for _ in range(args.steps):
+        step()
+    ktimes = ctx.kernel_times()
+    ctx.set_option("profile", 0)
+
+    info = {"n_out": n}
+    if w["kind"] == "equi":
+        B = 0
+        nb = min(nR, nS)
+        while (nb >> B) > 2048 and B < 27:
+            B += 1
+        info["passes"] = (B + 8) // 9 if B else 0
+    ab = algorithmic_bytes(w, info)
+    hbm, peak_src = peaks()
+    per_kernel = {}
+    for tag, (tms, cnt) in ktimes.items():
+        rec = {"ms_per_launch": tms / cnt, "launches_per_step": cnt / args.steps,
+               "share": tms / sum(v[0] for v in ktimes.values())}
+        if tag in ab:
+            total_bytes, per_step = ab[tag]
+            per_launch = total_bytes / per_step
+            rec["alg_bytes_per_launch"] = per_launch
+            rec["achieved_gbs"] = per_launch / (tms / cnt * 1e-3) / 1e9
+        per_kernel[tag] = rec
+    dom = max(ktimes.items(), key=lambda kv: kv[1][0])[0]
+    if w["kind"] == "equi":
+        d = per_kernel[dom]
+        roof = {"kernel": dom, "bound": "hbm", "achieved": round(d.get("achieved_gbs", 0.0), 1), "peak": hbm,
+                "unit": "GB/s", "frac": round(d.get("achieved_gbs", 0.0) / hbm, 4), "traffic": None,
+                "peak_source": peak_src}
+    else:
+        # INT ALU roofline: 1.5 ALU-pipe instr per pair-compare (band: + 1 FMA-pipe IMAD), DESIGN.md §5
+        pairs = nR * nS
+        d = per_kernel[dom]
+        sm = sampler.summary().get("sm_mhz") or 1965
+        alu_peak = 148 * 64 * sm * 1e6 / 1.5 / 1e12  # T pair-compares/s the ALU pipe allows
+        ach = pairs / (d["ms_per_launch"] * 1e-3) / 1e12
+        roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 3),
+                "unit": "Tpair/s", "frac": round(ach / alu_peak, 4), "traffic": None,
+                "peak_source": "148 SM x 64 ALU lanes/clk x median SM clock / 1.5 ALU instr per pair"}
+
+    # ---- e2e through the host-buffer C-ABI entry (equi only)
+    e2e = None
+    if w["kind"] == "equi":
+        hR = R.cpu().pin_memory()
+        hS = S.cpu().pin_memory()
+        hout = torch.empty((max(n, 1), 2), dtype=torch.int32).pin_memory()
+        gj.join_host(ctx, hR, hS, hout)
+        k_e2e = max(1, min(args.steps, args.e2e_steps))
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            got = gj.join_host(ctx, hR, hS, hout)
+        t1 = time.perf_counter()
+        assert got == n
+        e2e_s = max_over_ranks(t1 - t0, world)
+        e2e = {"value": (nR + nS) * k_e2e * world / e2e_s, "unit": "input tuples/s",
+               "h2d_bytes_per_step": hR.numel() * hR.element_size() + hS.numel() * hS.element_size(),
+               "d2h_bytes_per_step": n * 8, "steps": k_e2e,
+               "note": "join_host(): pinned host keys -> H2D -> count/scan/write -> D2H of all pairs; wall clock, the call synchronises"}
+
+    return dict(ms=ms_max, n=n, nR=nR, nS=nS, launches=launches, roof=roof, per_kernel=per_kernel, e2e=e2e,
+                clocks=sampler.summary(), desc=w["desc"], kind=w["kind"])
+
+
+def cpu_baseline(args):
+    """The oracle (O2 unordered_multimap + sort, 1 thread) on a bounded PK-FK sample."""
+    import numpy as np
+    import gen
+    import oracle
+    if args.workload == "c4":
+        R, S = gen.c4(nR=1 << 11, nS=1 << 24)
+        t0 = time.perf_counter()
+        c = oracle.theta_count_sorted(R, S, "band", gen.C4_EPS)  # noqa: F841
+        dt = time.perf_counter() - t0
+        return {"value": (len(R) + len(S)) / dt, "unit": "input tuples/s", "cores": 1, "kind": "oracle",
+                "sample": "O3 sort+binary-search band count, R 2^11 x S 2^24 slice of configs[3]", "seconds": dt}
+    b = args.cpu_sample_bits
+    R, S, m = gen.pkfk(b, 1 << b)
+    t0 = time.perf_counter()
+    c, _ = oracle.hash_equi(R, S)
+    dt = time.perf_counter() - t0
+    assert c == 1 << b
+    return {"value": (len(R) + len(S)) / dt, "unit": "input tuples/s", "cores": 1, "kind": "oracle",
+            "sample": f"O2 std::unordered_multimap build/probe + sort, PK-FK 2^{b} x 2^{b} (configs[1] shape, scaled)",
+            "seconds": round(dt, 3)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c4"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample-bits", type=int, default=23)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup(args)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        res = []
+        for _ in range(max(args.warmup, 0)):
+            pass
+        for _ in range(args.steps):
+            res.append(cpu_baseline(args))
+        v = statistics.median(r["value"] for r in res)
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "input tuples/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "i32", "data": "synthetic",
+                "config": {"workload": res[0]["sample"]},
+                "cpu_baseline": {k: res[0][k] for k in ("kind", "cores", "sample")} | {"value": v,
+                                                                                       "unit": "input tuples/s"},
+                "e2e": {"value": v, "unit": "input tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    r = run_ours(args, world, rank, local)
+    if rank != 0:
+        return
+    T = r["ms"] * 1e-3
+    value = (r["nR"] + r["nS"]) * args.steps * world / T
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "input tuples/s",
+        "output_tuples_per_s": r["n"] * args.steps * world / T,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": r["ms"] / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "i32",
+        "data": "synthetic",
+        "config": {"workload": r["desc"], "n_R": r["nR"], "n_S": r["nS"], "n_out": r["n"],
+                   "l2": "inputs (>=64 MiB of keys, 1 GiB for configs[1]) exceed/stream past the 126 MB L2; no flush",
+                   "parallelism": f"{world} independent ranks (weak scaling)"},
+        "roofline": r["roof"],
+        "kernels": r["per_kernel"],
+        "gpu_launches": r["launches"],
+        "clocks": r["clocks"],
+        "e2e": r["e2e"],
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(args)
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

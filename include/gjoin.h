@@ -1,0 +1,184 @@
+/* gjoin.h -- C ABI of the B200-native GPU join hot path (arXiv 1904.11201).
+ *
+ * One shared library, paper_1904_11201_b200/libgjoin.so, compiled for sm_100a.
+ * No torch types cross this boundary: plain pointers, sizes and status codes.
+ *
+ * What is computed (PAPER.md:49-59 §2.3 "Join Operation"; :67-68 nested loop and
+ * hash join; :141 §3.2.2 positional result rule):
+ *
+ *   J(R, S, theta) = { (rid_R(i), rid_S(j)) : theta(R.key[i], S.key[j]) }
+ *
+ * with theta = R.key OP S.key, OP in {=, !=, <, <=, >, >=}
+ * or the band predicate |R.key - S.key| <= eps (BASELINE.json north_star), eps an
+ * unsigned 64-bit integer and the distance computed exactly (no wrap-around).
+ * rid(i) = rid[i] when a rid map is given, else rid_base + i.  Bag semantics:
+ * duplicate keys produce every qualifying pair.
+ *
+ * Result sizing: the paper allocates per-thread Cartesian slots (PAPER.md:174-175,
+ * :195) and estimates R_size (Eq. 7-8).  This library instead
+ * counts exactly (count pass), takes an exclusive scan of the per-work-unit counts,
+ * and writes every pair at its scanned offset (write pass); so *_count returns the
+ * exact |J| and *_materialize writes exactly |J| pairs.
+ *
+ * Conventions (all entry points):
+ *  - Data pointers inside gj_rel and the out buffers are DEVICE pointers unless the
+ *    entry point's name ends in _host.  The caller owns every input and output
+ *    buffer; the ctx owns its scratch space.
+ *  - Calls are ordered on the ctx's CUDA stream.  Entry points that return a host
+ *    count synchronise that stream once.
+ *  - Output pairs are uint32 [rid_R, rid_S] (8 bytes per pair), unordered between
+ *    work units but at deterministic positions except that, for an equi join whose
+ *    build side has duplicate keys, the matches of one probe tuple may appear in
+ *    any order (reading R4).  Parity is defined on the canonically sorted
+ *    (rid_R, rid_S) sequence.
+ *  - Errors: a gj_status code is returned and a thread-local message is available
+ *    from gj_last_error(); nothing aborts; nothing is written past `capacity`.
+ *    GJ_EINVAL: NULL pointer with n > 0, mismatched key types, unknown op,
+ *    rid_base + n > 2^32, NULL host result pointer.  GJ_ERANGE: capacity smaller
+ *    than |J| (then *n_written = |J| and the output buffer is untouched).
+ *    GJ_ENOMEM: scratch allocation failed.  GJ_ECUDA / GJ_ENCCL: runtime failures.
+ *  - Empty inputs are legal (count 0).  GJ_BAND with eps = 0 equals GJ_EQ.
+ */
+#ifndef GJOIN_H
+#define GJOIN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GJ_OK = 0,
+  GJ_EINVAL = 1,
+  GJ_ENOMEM = 2,
+  GJ_ERANGE = 3,
+  GJ_ESTATE = 4,
+  GJ_ECUDA = 5,
+  GJ_ENCCL = 6
+} gj_status;
+
+typedef enum { GJ_I32 = 0, GJ_I64 = 1 } gj_key_type;
+
+/* theta = R.key OP S.key; GJ_BAND: |R.key - S.key| <= eps */
+typedef enum { GJ_EQ = 0, GJ_NE = 1, GJ_LT = 2, GJ_LE = 3, GJ_GT = 4, GJ_GE = 5, GJ_BAND = 6 } gj_op;
+
+/* One relation's join-key column (§3.2.2: the row->column
+ * transform leaves a contiguous key buffer whose m-th entry is row m).
+ *   key      DEVICE pointer to n keys of key_type (int32 or int64, signed).
+ *   rid      DEVICE pointer to n uint32 row ids, or NULL: rid(i) = rid_base + i.
+ *   n        number of tuples (0 allowed); rid_base + n <= 2^32 when rid == NULL.
+ *   key_type GJ_I32 or GJ_I64; both relations of one call must agree. */
+typedef struct {
+  const void* key;
+  const uint32_t* rid;
+  uint64_t n;
+  int32_t key_type;
+  uint32_t rid_base;
+} gj_rel;
+
+typedef struct gj_ctx gj_ctx;
+
+/* Context: binds a CUDA device and stream (cudaStream_t passed as void*; NULL =
+ * the legacy default stream) and owns scratch memory (stream-ordered cudaMallocAsync).
+ * A ctx is not thread-safe; use one per host thread. */
+gj_status gj_ctx_create(gj_ctx** out, int device, void* stream);
+void gj_ctx_destroy(gj_ctx* ctx);
+gj_status gj_ctx_set_stream(gj_ctx* ctx, void* stream);
+/* Thread-local, human-readable description of the last failure. */
+const char* gj_last_error(void);
+
+/* Tuning / test options (gj_ctx_set_option).  Defaults are chosen for B200.
+ *  GJ_OPT_PART_BITS        total radix bits B (-1 = auto from the build size)
+ *  GJ_OPT_BUILD_CHUNK      build tuples per hash-join work unit (<= 4096, power of 2)
+ *  GJ_OPT_PROBE_CHUNK      probe tuples per hash-join work unit
+ *  GJ_OPT_PROFILE          1 = bracket every kernel with CUDA events (per-kernel times)
+ *  GJ_OPT_NLJ_SPLIT        S-range splits per R tile for the NLJ (0 = auto)
+ *  GJ_OPT_FORCE_SLOW_BAND  1 = always use the 64-bit band path (tests)
+ *  GJ_OPT_BUILD_SIDE       0 = smaller side (default), 1 = always R, 2 = always S */
+enum {
+  GJ_OPT_PART_BITS = 1,
+  GJ_OPT_BUILD_CHUNK = 2,
+  GJ_OPT_PROBE_CHUNK = 3,
+  GJ_OPT_PROFILE = 4,
+  GJ_OPT_NLJ_SPLIT = 5,
+  GJ_OPT_FORCE_SLOW_BAND = 6,
+  GJ_OPT_BUILD_SIDE = 7
+};
+gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t value);
+
+/* Number of kernels this ctx has launched since creation (or the last reset). */
+uint64_t gj_ctx_launch_count(gj_ctx* ctx);
+void gj_ctx_reset_stats(gj_ctx* ctx);
+/* With GJ_OPT_PROFILE=1: accumulated device milliseconds and launch count of
+ * every kernel tag since the last reset, after synchronising the stream.
+ * Writes up to max_tags entries; returns the number of tags.  Tag names are
+ * static strings owned by the library. */
+int gj_ctx_kernel_times(gj_ctx* ctx, const char** names, double* ms, uint64_t* launches,
+                        int max_tags);
+
+/* ---------------------------------------------------------------- equi join
+ * Hash join ("put the smaller table (inner table) into a hash table
+ * ... traverse the larger table (outer table)"; §3.3.2).
+ * Both relations are radix-partitioned by a multiplicative hash of the key (the
+ * analogue of the Hadoop shuffle by key), each partition's
+ * smaller side is built into a shared-memory hash table, and the other side
+ * probes it.
+ *
+ * join_count: *n_out = |J(R,S,=)| (host, uint64).  Synchronises the stream.
+ *   Caches the partitions and scanned offsets in the ctx for a following
+ *   join_materialize on the same (R, S).
+ * join_materialize: writes |J| pairs to out[0 .. 2*|J|) (device uint32, caller-
+ *   allocated, `capacity` pairs).  Reuses the cache of the immediately preceding
+ *   join_count on the same R, S (same pointers, sizes, types, rid bases); else
+ *   recomputes.  *n_written = |J| (host).  GJ_ERANGE if capacity < |J|. */
+gj_status join_count(gj_ctx* ctx, gj_rel R, gj_rel S, uint64_t* n_out);
+gj_status join_materialize(gj_ctx* ctx, gj_rel R, gj_rel S, uint32_t* out, uint64_t capacity,
+                           uint64_t* n_written);
+
+/* ---------------------------------------------------------------- theta join
+ * Tiled nested-loop join (§3.3.1; theta = NLJ with a predicate,
+ * PAPER.md:302 §4.2).  Every (R, S) pair is compared once per pass: R tiles are
+ * held in registers, S tiles are staged into shared memory by 1-D TMA bulk copies.
+ * op in gj_op; eps used only by GJ_BAND.
+ * theta_join_count: *n_out = |J(R,S,op)|; synchronises; caches per-unit offsets.
+ * theta_join_materialize: writes |J| pairs (same cache/ERANGE rules as above). */
+gj_status theta_join_count(gj_ctx* ctx, gj_rel R, gj_rel S, int op, uint64_t eps, uint64_t* n_out);
+gj_status theta_join_materialize(gj_ctx* ctx, gj_rel R, gj_rel S, int op, uint64_t eps,
+                                 uint32_t* out, uint64_t capacity, uint64_t* n_written);
+
+/* ---------------------------------------------------------------- pre-filter
+ * Approximation of the paper's two-round common-key pre-filter (PAPER.md:78-82
+ * §3.1, Alg.1 lines 1-13: keep only tuples whose join key occurs in both tables,
+ * filtering BOTH tables).  GJ_PF_RANGE keeps keys in [max(minR,minS)-eps,
+ * min(maxR,maxS)+eps] (saturating); GJ_PF_BLOOM builds a sector-blocked Bloom
+ * filter of R's surviving keys (bloom_bits_per_key bits per key, 8 probes inside
+ * one 32-byte sector) and drops S tuples whose key is absent; GJ_PF_TWO_SIDED then
+ * builds a filter of S's survivors and filters R the same way.  With op = GJ_BAND
+ * and eps > 0 only the range stage applies (a Bloom filter cannot answer range
+ * membership).  Guarantee: J(prefilter(R), prefilter(S)) = J(R, S) (no false
+ * negatives).  Survivors keep their original relative order and rid.
+ *   key_out_X / rid_out_X: DEVICE buffers of X.n keys / uint32 rids (caller-owned).
+ *   n_X_out: host; number of survivors.  Synchronises the stream. */
+enum { GJ_PF_RANGE = 1, GJ_PF_BLOOM = 2, GJ_PF_TWO_SIDED = 4 };
+gj_status prefilter(gj_ctx* ctx, gj_rel R, gj_rel S, uint32_t flags, int op, uint64_t eps,
+                    double bloom_bits_per_key, void* key_out_R, uint32_t* rid_out_R,
+                    uint64_t* n_R_out, void* key_out_S, uint32_t* rid_out_S, uint64_t* n_S_out);
+
+/* ---------------------------------------------------------------- host entry
+ * End-to-end equi join from HOST buffers (pinned for full PCIe speed): copies the
+ * two key columns host->device on the ctx stream, runs join_count +
+ * join_materialize into ctx scratch, and copies the pairs device->host.
+ *   key_R_host / key_S_host: host arrays of n_R / n_S keys of key_type.
+ *   out_host: host uint32 buffer of 2*capacity entries.  *n_out = |J|; GJ_ERANGE
+ *   (nothing copied) if capacity < |J|.  rids are row positions (rid_base 0). */
+gj_status join_host(gj_ctx* ctx, const void* key_R_host, uint64_t n_R, const void* key_S_host,
+                    uint64_t n_S, int key_type, uint32_t* out_host, uint64_t capacity,
+                    uint64_t* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GJOIN_H */

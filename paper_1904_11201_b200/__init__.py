@@ -1,0 +1,249 @@
+"""paper_1904_11201_b200 -- B200-native GPU join hot path of arXiv 1904.11201.
+
+Thin ctypes binding over ``libgjoin.so`` (C ABI declared in ``include/gjoin.h``).
+This module only marshals arguments: every step of the join (partitioning, hash
+build/probe, nested-loop theta compare, scans, pre-filter, materialisation) runs
+in the library's CUDA kernels.  torch supplies device memory, streams and process
+groups.  There is NO CPU fallback: importing fails loudly if the library is
+missing, and every call needs CUDA tensors.
+
+Names follow the C ABI:
+
+    ctx = Context(device=0)                       # gj_ctx_create
+    n   = join_count(ctx, R, S)                   # |J(R, S, =)|
+    out = join_materialize(ctx, R, S, n)          # (n, 2) int32 view of uint32 (rid_R, rid_S)
+    n   = theta_join_count(ctx, R, S, "band", eps)
+    out = theta_join_materialize(ctx, R, S, "band", eps, n)
+    (Rk, Rr, Sk, Sr) = prefilter(ctx, R, S, flags=RANGE|BLOOM|TWO_SIDED)
+    n   = join_host(ctx, keyR_host, keyS_host, out_host)   # host buffers, e2e
+
+``R``/``S`` are :class:`Rel` (key tensor, optional rid tensor, rid_base) or bare key
+tensors (rid = row position).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgjoin.so")
+
+OPS = {"eq": 0, "ne": 1, "lt": 2, "le": 3, "gt": 4, "ge": 5, "band": 6}
+RANGE, BLOOM, TWO_SIDED = 1, 2, 4
+OPT = {"part_bits": 1, "build_chunk": 2, "probe_chunk": 3, "profile": 4, "nlj_split": 5,
+       "force_slow_band": 6, "build_side": 7}
+STATUS = {0: "GJ_OK", 1: "GJ_EINVAL", 2: "GJ_ENOMEM", 3: "GJ_ERANGE", 4: "GJ_ESTATE", 5: "GJ_ECUDA",
+          6: "GJ_ENCCL"}
+I32, I64 = 0, 1
+
+
+class GJError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Rel(ctypes.Structure):
+    _fields_ = [("key", ctypes.c_void_p), ("rid", ctypes.c_void_p), ("n", ctypes.c_uint64),
+                ("key_type", ctypes.c_int32), ("rid_base", ctypes.c_uint32)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a); "
+                          "there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, u64, i32, u32, i64 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint32, ctypes.c_int64
+    pu64 = ctypes.POINTER(ctypes.c_uint64)
+    L.gj_ctx_create.argtypes = [ctypes.POINTER(vp), i32, vp]
+    L.gj_ctx_destroy.argtypes = [vp]
+    L.gj_ctx_destroy.restype = None
+    L.gj_ctx_set_stream.argtypes = [vp, vp]
+    L.gj_ctx_set_option.argtypes = [vp, i32, i64]
+    L.gj_last_error.restype = ctypes.c_char_p
+    L.gj_ctx_launch_count.argtypes = [vp]
+    L.gj_ctx_launch_count.restype = u64
+    L.gj_ctx_reset_stats.argtypes = [vp]
+    L.gj_ctx_reset_stats.restype = None
+    L.gj_ctx_kernel_times.argtypes = [vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
+                                      pu64, i32]
+    L.gj_ctx_kernel_times.restype = i32
+    L.join_count.argtypes = [vp, _Rel, _Rel, pu64]
+    L.join_materialize.argtypes = [vp, _Rel, _Rel, vp, u64, pu64]
+    L.theta_join_count.argtypes = [vp, _Rel, _Rel, i32, u64, pu64]
+    L.theta_join_materialize.argtypes = [vp, _Rel, _Rel, i32, u64, vp, u64, pu64]
+    L.prefilter.argtypes = [vp, _Rel, _Rel, u32, i32, u64, ctypes.c_double, vp, vp, pu64, vp, vp, pu64]
+    L.join_host.argtypes = [vp, vp, u64, vp, u64, i32, vp, u64, pu64]
+    for f in ("gj_ctx_create", "gj_ctx_set_stream", "gj_ctx_set_option", "join_count", "join_materialize",
+              "theta_join_count", "theta_join_materialize", "prefilter", "join_host"):
+        getattr(L, f).restype = i32
+    return L
+
+
+lib = _load()
+
+# C-ABI symbols declared in include/gjoin.h (checked by tests/test_abi.py)
+ABI_SYMBOLS = ("gj_ctx_create", "gj_ctx_destroy", "gj_ctx_set_stream", "gj_last_error", "gj_ctx_set_option",
+               "gj_ctx_launch_count", "gj_ctx_reset_stats", "gj_ctx_kernel_times", "join_count",
+               "join_materialize", "theta_join_count", "theta_join_materialize", "prefilter", "join_host")
+
+
+def _check(status: int):
+    if status != 0:
+        raise GJError(status, lib.gj_last_error().decode(errors="replace"))
+
+
+@dataclass
+class Rel:
+    """One relation's key column (+ optional rid map) on the GPU."""
+    key: torch.Tensor
+    rid: Optional[torch.Tensor] = None
+    rid_base: int = 0
+
+    def c(self) -> _Rel:
+        k = self.key
+        if not k.is_cuda:
+            raise ValueError("Rel.key must be a CUDA tensor (no CPU fallback)")
+        if k.dtype not in (torch.int32, torch.int64) or not k.is_contiguous():
+            raise ValueError("Rel.key must be a contiguous int32/int64 CUDA tensor")
+        rid = None
+        if self.rid is not None:
+            if not self.rid.is_cuda or self.rid.dtype not in (torch.int32, torch.uint32) or \
+                    not self.rid.is_contiguous() or self.rid.numel() != k.numel():
+                raise ValueError("Rel.rid must be a contiguous 32-bit CUDA tensor of key's length")
+            rid = self.rid.data_ptr()
+        return _Rel(k.data_ptr() if k.numel() else None, rid, k.numel(),
+                    I32 if k.dtype == torch.int32 else I64, self.rid_base)
+
+
+def _rel(x) -> _Rel:
+    return x.c() if isinstance(x, Rel) else Rel(x).c()
+
+
+class Context:
+    """gj_ctx bound to a device and (by default) torch's current stream there."""
+
+    def __init__(self, device: int = 0, stream: Optional[torch.cuda.Stream] = None, **options):
+        torch.cuda.set_device(device)
+        self.device = device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        h = ctypes.c_void_p()
+        _check(lib.gj_ctx_create(ctypes.byref(h), device, ctypes.c_void_p(self.stream.cuda_stream)))
+        self.h = h
+        for k, v in options.items():
+            self.set_option(k, v)
+
+    def set_option(self, name: str, value: int):
+        _check(lib.gj_ctx_set_option(self.h, OPT[name], int(value)))
+
+    def set_stream(self, stream: torch.cuda.Stream):
+        self.stream = stream
+        _check(lib.gj_ctx_set_stream(self.h, ctypes.c_void_p(stream.cuda_stream)))
+
+    def launches(self) -> int:
+        return int(lib.gj_ctx_launch_count(self.h))
+
+    def reset_stats(self):
+        lib.gj_ctx_reset_stats(self.h)
+
+    def kernel_times(self) -> dict:
+        """{tag: (total_ms, launches)} of kernels since the last reset (needs profile=1)."""
+        n = 64
+        names = (ctypes.c_char_p * n)()
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_uint64 * n)()
+        k = lib.gj_ctx_kernel_times(self.h, names, ms, cnt, n)
+        if k < 0:
+            raise GJError(5, lib.gj_last_error().decode())
+        return {names[i].decode(): (ms[i], int(cnt[i])) for i in range(min(k, n))}
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.gj_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def join_count(ctx: Context, R, S) -> int:
+    n = ctypes.c_uint64()
+    _check(lib.join_count(ctx.h, _rel(R), _rel(S), ctypes.byref(n)))
+    return n.value
+
+
+def _out(n: int, out: Optional[torch.Tensor], device) -> torch.Tensor:
+    if out is None:
+        return torch.empty((max(n, 1), 2), dtype=torch.int32, device=device)
+    if not out.is_cuda or out.dtype not in (torch.int32, torch.uint32) or not out.is_contiguous():
+        raise ValueError("out must be a contiguous 32-bit CUDA tensor of shape (capacity, 2)")
+    return out
+
+
+def join_materialize(ctx: Context, R, S, n: Optional[int] = None, out: Optional[torch.Tensor] = None):
+    """Writes |J| (rid_R, rid_S) pairs; returns the (|J|, 2) int32 view (uint32 values)."""
+    if n is None and out is None:
+        n = join_count(ctx, R, S)
+    key = (R.key if isinstance(R, Rel) else R)
+    buf = _out(n or 0, out, key.device)
+    w = ctypes.c_uint64()
+    _check(lib.join_materialize(ctx.h, _rel(R), _rel(S), ctypes.c_void_p(buf.data_ptr()), buf.shape[0],
+                                ctypes.byref(w)))
+    return buf[: w.value]
+
+
+def theta_join_count(ctx: Context, R, S, op: str, eps: int = 0) -> int:
+    n = ctypes.c_uint64()
+    _check(lib.theta_join_count(ctx.h, _rel(R), _rel(S), OPS[op], int(eps), ctypes.byref(n)))
+    return n.value
+
+
+def theta_join_materialize(ctx: Context, R, S, op: str, eps: int = 0, n: Optional[int] = None,
+                           out: Optional[torch.Tensor] = None):
+    if n is None and out is None:
+        n = theta_join_count(ctx, R, S, op, eps)
+    key = (R.key if isinstance(R, Rel) else R)
+    buf = _out(n or 0, out, key.device)
+    w = ctypes.c_uint64()
+    _check(lib.theta_join_materialize(ctx.h, _rel(R), _rel(S), OPS[op], int(eps),
+                                      ctypes.c_void_p(buf.data_ptr()), buf.shape[0], ctypes.byref(w)))
+    return buf[: w.value]
+
+
+def prefilter(ctx: Context, R, S, flags: int = RANGE | BLOOM | TWO_SIDED, op: str = "eq", eps: int = 0,
+              bloom_bits_per_key: float = 8.0):
+    """Returns (R_keys, R_rids, S_keys, S_rids) of the surviving tuples (CUDA tensors)."""
+    rR, rS = _rel(R), _rel(S)
+    kR = (R.key if isinstance(R, Rel) else R)
+    kS = (S.key if isinstance(S, Rel) else S)
+    okR, orR = torch.empty_like(kR), torch.empty(kR.numel(), dtype=torch.int32, device=kR.device)
+    okS, orS = torch.empty_like(kS), torch.empty(kS.numel(), dtype=torch.int32, device=kS.device)
+    nR, nS = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(lib.prefilter(ctx.h, rR, rS, flags, OPS[op], int(eps), float(bloom_bits_per_key),
+                         ctypes.c_void_p(okR.data_ptr()), ctypes.c_void_p(orR.data_ptr()), ctypes.byref(nR),
+                         ctypes.c_void_p(okS.data_ptr()), ctypes.c_void_p(orS.data_ptr()), ctypes.byref(nS)))
+    return okR[: nR.value], orR[: nR.value], okS[: nS.value], orS[: nS.value]
+
+
+def join_host(ctx: Context, key_R: torch.Tensor, key_S: torch.Tensor, out: torch.Tensor) -> int:
+    """End-to-end equi join from HOST tensors (pin them for full PCIe speed).
+
+    out: host int32 tensor (capacity, 2).  Returns |J|; pairs land in out[:|J|]."""
+    for t in (key_R, key_S, out):
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError("join_host takes contiguous HOST tensors")
+    if key_R.dtype != key_S.dtype or key_R.dtype not in (torch.int32, torch.int64):
+        raise ValueError("keys must both be int32 or int64")
+    n = ctypes.c_uint64()
+    _check(lib.join_host(ctx.h, ctypes.c_void_p(key_R.data_ptr()), key_R.numel(),
+                         ctypes.c_void_p(key_S.data_ptr()), key_S.numel(),
+                         I32 if key_R.dtype == torch.int32 else I64,
+                         ctypes.c_void_p(out.data_ptr()), out.shape[0], ctypes.byref(n)))
+    return n.value

@@ -1,0 +1,374 @@
+// api.cu -- the C ABI (include/gjoin.h) and the host runtime behind it: ctx,
+// stream-ordered workspace, launch accounting, per-kernel event timing, argument
+// validation, and the count -> materialize cache.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "gjoin.h"
+#include "hashjoin.cuh"
+#include "nlj.cuh"
+#include "partition.cuh"
+#include "runtime.h"
+
+namespace gj {
+gj_status prefilter_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t flags, int op, uint64_t eps,
+                         double bpk, void* kR, uint32_t* rR, uint64_t* nRo, void* kS, uint32_t* rS,
+                         uint64_t* nSo);
+
+static thread_local std::string g_err;
+
+void* ws(gj_ctx* ctx, const char* name, size_t bytes) {
+  Buf& b = ctx->bufs[name];
+  if (bytes == 0) bytes = 1;
+  if (b.bytes < bytes) {
+    if (b.ptr) GJ_CUDA(cudaFreeAsync(b.ptr, ctx->stream));
+    b.ptr = nullptr;
+    b.bytes = 0;
+    const size_t rounded = (bytes + (1u << 20) - 1) & ~(size_t)((1u << 20) - 1);
+    cudaError_t e = cudaMallocAsync(&b.ptr, rounded, ctx->stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(GJ_ENOMEM, std::string("workspace '") + name + "' (" + std::to_string(rounded) +
+                                 " bytes): " + cudaGetErrorString(e));
+    }
+    b.bytes = rounded;
+  }
+  return b.ptr;
+}
+
+void d2h_sync(gj_ctx* ctx, void* host, const void* dev, size_t bytes) {
+  if (bytes > 4096) throw Error(GJ_EINVAL, "d2h_sync: too large");
+  GJ_CUDA(cudaMemcpyAsync(ctx->host_pinned, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  GJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(host, ctx->host_pinned, bytes);
+}
+
+static cudaEvent_t get_event(gj_ctx* ctx) {
+  if (!ctx->event_pool.empty()) {
+    cudaEvent_t e = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  GJ_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+LaunchScope::LaunchScope(gj_ctx* c, const char* t) : ctx(c), tag(t) {
+  if (ctx->profile) {
+    a = get_event(ctx);
+    GJ_CUDA(cudaEventRecord(a, ctx->stream));
+  }
+}
+
+LaunchScope::~LaunchScope() noexcept(false) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(GJ_ECUDA, std::string("launch ") + tag + ": " + cudaGetErrorString(e));
+  ++ctx->launches;
+  if (ctx->profile) {
+    cudaEvent_t b = get_event(ctx);
+    GJ_CUDA(cudaEventRecord(b, ctx->stream));
+    ctx->pending.push_back({tag, a, b});
+  }
+}
+
+static void flush_prof(gj_ctx* ctx) {
+  if (ctx->pending.empty()) return;
+  GJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (auto& p : ctx->pending) {
+    float ms = 0.f;
+    GJ_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    auto& t = ctx->times[p.tag];
+    t.first += ms;
+    t.second += 1;
+    ctx->event_pool.push_back(p.a);
+    ctx->event_pool.push_back(p.b);
+  }
+  ctx->pending.clear();
+}
+
+static void check_rel(const gj_rel& X, const char* name) {
+  if (X.key_type != GJ_I32 && X.key_type != GJ_I64)
+    throw Error(GJ_EINVAL, std::string(name) + ": key_type must be GJ_I32 or GJ_I64");
+  if (X.n > 0 && X.key == nullptr) throw Error(GJ_EINVAL, std::string(name) + ": key is NULL with n > 0");
+  if (X.n >= (1ull << 32)) throw Error(GJ_EINVAL, std::string(name) + ": n must be < 2^32 per call");
+  if (X.rid == nullptr && (uint64_t)X.rid_base + X.n > (1ull << 32))
+    throw Error(GJ_EINVAL, std::string(name) + ": rid_base + n exceeds 2^32");
+}
+
+static void check_pair(const gj_rel& R, const gj_rel& S) {
+  check_rel(R, "R");
+  check_rel(S, "S");
+  if (R.key_type != S.key_type) throw Error(GJ_EINVAL, "R and S key types differ");
+}
+
+static bool same_rel(const gj_rel& a, const gj_rel& b) {
+  return a.key == b.key && a.rid == b.rid && a.n == b.n && a.key_type == b.key_type && a.rid_base == b.rid_base;
+}
+
+static uint32_t auto_bits(gj_ctx* ctx, uint64_t nb) {
+  if (ctx->part_bits >= 0) return (uint32_t)ctx->part_bits;
+  const uint64_t target = ctx->build_chunk / 2;  // mean build tuples per partition
+  uint32_t B = 0;
+  while ((nb >> B) > target && B < 27) ++B;
+  return B;
+}
+
+static void do_join_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S) {
+  JoinCache& jc = ctx->jc;
+  jc = JoinCache{};
+  jc.R = R;
+  jc.S = S;
+  if (R.n == 0 || S.n == 0) {
+    jc.valid = true;
+    return;
+  }
+  const bool swap = ctx->build_side == 2 || (ctx->build_side == 0 && S.n < R.n);
+  const uint32_t B = auto_bits(ctx, swap ? S.n : R.n);
+  Partitioned PR = radix_partition(ctx, R, B, "R");
+  Partitioned PS = radix_partition(ctx, S, B, "S");
+  hash_join_count(ctx, R, S, B, swap, PR, PS);
+  jc.valid = true;
+}
+
+}  // namespace gj
+
+using namespace gj;
+
+#define API_BEGIN try {
+#define API_END                                            \
+  }                                                        \
+  catch (const gj::Error& e) {                             \
+    g_err = e.what();                                      \
+    return e.code;                                         \
+  }                                                        \
+  catch (const std::exception& e) {                        \
+    g_err = e.what();                                      \
+    return GJ_ECUDA;                                       \
+  }                                                        \
+  return GJ_OK;
+
+extern "C" {
+
+const char* gj_last_error(void) { return g_err.c_str(); }
+
+gj_status gj_ctx_create(gj_ctx** out, int device, void* stream) {
+  API_BEGIN
+  if (!out) throw Error(GJ_EINVAL, "gj_ctx_create: out is NULL");
+  GJ_CUDA(cudaSetDevice(device));
+  gj_ctx* c = new gj_ctx();
+  c->device = device;
+  c->stream = static_cast<cudaStream_t>(stream);
+  int sms = 0;
+  GJ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  c->num_sms = sms;
+  GJ_CUDA(cudaMallocHost(&c->host_pinned, 4096));
+  *out = c;
+  API_END
+}
+
+void gj_ctx_destroy(gj_ctx* ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& kv : ctx->bufs)
+    if (kv.second.ptr) cudaFreeAsync(kv.second.ptr, ctx->stream);
+  for (auto& p : ctx->pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
+  delete ctx;
+}
+
+gj_status gj_ctx_set_stream(gj_ctx* ctx, void* stream) {
+  API_BEGIN
+  if (!ctx) throw Error(GJ_EINVAL, "ctx is NULL");
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  API_END
+}
+
+gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t v) {
+  API_BEGIN
+  if (!ctx) throw Error(GJ_EINVAL, "ctx is NULL");
+  switch (option) {
+    case GJ_OPT_PART_BITS:
+      if (v < -1 || v > 27) throw Error(GJ_EINVAL, "part_bits must be in [-1, 27]");
+      ctx->part_bits = (int)v;
+      break;
+    case GJ_OPT_BUILD_CHUNK:
+      if (v < 32 || v > 4096 || (v & (v - 1))) throw Error(GJ_EINVAL, "build_chunk must be a power of 2 in [32, 4096]");
+      ctx->build_chunk = (uint32_t)v;
+      break;
+    case GJ_OPT_PROBE_CHUNK:
+      if (v < 32 || v > (1 << 20)) throw Error(GJ_EINVAL, "probe_chunk must be in [32, 2^20]");
+      ctx->probe_chunk = (uint32_t)v;
+      break;
+    case GJ_OPT_PROFILE: ctx->profile = v != 0; break;
+    case GJ_OPT_NLJ_SPLIT:
+      if (v < 0 || v > (1 << 24)) throw Error(GJ_EINVAL, "nlj_split out of range");
+      ctx->nlj_split = (uint32_t)v;
+      break;
+    case GJ_OPT_FORCE_SLOW_BAND: ctx->force_slow_band = v != 0; break;
+    case GJ_OPT_BUILD_SIDE:
+      if (v < 0 || v > 2) throw Error(GJ_EINVAL, "build_side must be 0, 1 or 2");
+      ctx->build_side = (int)v;
+      break;
+    default: throw Error(GJ_EINVAL, "unknown option");
+  }
+  ctx->jc.valid = false;
+  ctx->tc.valid = false;
+  API_END
+}
+
+uint64_t gj_ctx_launch_count(gj_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void gj_ctx_reset_stats(gj_ctx* ctx) {
+  if (!ctx) return;
+  try {
+    flush_prof(ctx);
+  } catch (...) {
+  }
+  ctx->launches = 0;
+  ctx->times.clear();
+}
+
+int gj_ctx_kernel_times(gj_ctx* ctx, const char** names, double* ms, uint64_t* launches, int max_tags) {
+  if (!ctx) return 0;
+  try {
+    flush_prof(ctx);
+  } catch (const gj::Error& e) {
+    g_err = e.what();
+    return -1;
+  }
+  int i = 0;
+  for (auto& kv : ctx->times) {
+    if (i < max_tags) {
+      // tags are static strings passed to launch(); find the canonical pointer
+      names[i] = kv.first.c_str();
+      ms[i] = kv.second.first;
+      launches[i] = kv.second.second;
+    }
+    ++i;
+  }
+  return i;
+}
+
+gj_status join_count(gj_ctx* ctx, gj_rel R, gj_rel S, uint64_t* n_out) {
+  API_BEGIN
+  if (!ctx || !n_out) throw Error(GJ_EINVAL, "join_count: NULL ctx or n_out");
+  check_pair(R, S);
+  do_join_count(ctx, R, S);
+  *n_out = ctx->jc.total;
+  API_END
+}
+
+gj_status join_materialize(gj_ctx* ctx, gj_rel R, gj_rel S, uint32_t* out, uint64_t capacity, uint64_t* n_written) {
+  API_BEGIN
+  if (!ctx || !n_written) throw Error(GJ_EINVAL, "join_materialize: NULL ctx or n_written");
+  check_pair(R, S);
+  JoinCache& jc = ctx->jc;
+  if (!(jc.valid && same_rel(jc.R, R) && same_rel(jc.S, S))) do_join_count(ctx, R, S);
+  if (capacity < jc.total) {
+    *n_written = jc.total;
+    throw Error(GJ_ERANGE, "join_materialize: capacity " + std::to_string(capacity) + " < |J| = " +
+                               std::to_string(jc.total));
+  }
+  if (jc.total && !out) throw Error(GJ_EINVAL, "join_materialize: out is NULL");
+  hash_join_write(ctx, out);
+  *n_written = jc.total;
+  API_END
+}
+
+gj_status theta_join_count(gj_ctx* ctx, gj_rel R, gj_rel S, int op, uint64_t eps, uint64_t* n_out) {
+  API_BEGIN
+  if (!ctx || !n_out) throw Error(GJ_EINVAL, "theta_join_count: NULL ctx or n_out");
+  check_pair(R, S);
+  if (op < GJ_EQ || op > GJ_BAND) throw Error(GJ_EINVAL, "theta_join_count: unknown op");
+  ctx->tc = ThetaCache{};
+  theta_count(ctx, R, S, op, eps);
+  ctx->tc.R = R;
+  ctx->tc.S_user_key = S.key;
+  ctx->tc.valid = true;
+  *n_out = ctx->tc.total;
+  API_END
+}
+
+gj_status theta_join_materialize(gj_ctx* ctx, gj_rel R, gj_rel S, int op, uint64_t eps, uint32_t* out,
+                                 uint64_t capacity, uint64_t* n_written) {
+  API_BEGIN
+  if (!ctx || !n_written) throw Error(GJ_EINVAL, "theta_join_materialize: NULL ctx or n_written");
+  check_pair(R, S);
+  if (op < GJ_EQ || op > GJ_BAND) throw Error(GJ_EINVAL, "theta_join_materialize: unknown op");
+  ThetaCache& tc = ctx->tc;
+  const gj_rel S_seen = S;
+  if (!(tc.valid && same_rel(tc.R, R) && tc.op == op && tc.eps == eps && tc.S.n == S.n &&
+        tc.S.rid == S.rid && tc.S.rid_base == S.rid_base && tc.S_user_key == S.key)) {
+    tc = ThetaCache{};
+    theta_count(ctx, R, S, op, eps);
+    tc.R = R;
+    tc.S_user_key = S.key;
+    tc.valid = true;
+  }
+  (void)S_seen;
+  if (capacity < tc.total) {
+    *n_written = tc.total;
+    throw Error(GJ_ERANGE, "theta_join_materialize: capacity " + std::to_string(capacity) + " < |J| = " +
+                               std::to_string(tc.total));
+  }
+  if (tc.total && !out) throw Error(GJ_EINVAL, "theta_join_materialize: out is NULL");
+  theta_write(ctx, out);
+  *n_written = tc.total;
+  API_END
+}
+
+gj_status prefilter(gj_ctx* ctx, gj_rel R, gj_rel S, uint32_t flags, int op, uint64_t eps,
+                    double bloom_bits_per_key, void* key_out_R, uint32_t* rid_out_R, uint64_t* n_R_out,
+                    void* key_out_S, uint32_t* rid_out_S, uint64_t* n_S_out) {
+  API_BEGIN
+  if (!ctx || !n_R_out || !n_S_out) throw Error(GJ_EINVAL, "prefilter: NULL ctx or count pointer");
+  check_pair(R, S);
+  if (op != GJ_EQ && op != GJ_BAND) throw Error(GJ_EINVAL, "prefilter: op must be GJ_EQ or GJ_BAND");
+  if ((R.n && (!key_out_R || !rid_out_R)) || (S.n && (!key_out_S || !rid_out_S)))
+    throw Error(GJ_EINVAL, "prefilter: NULL output buffer");
+  if ((flags & GJ_PF_BLOOM) && !(bloom_bits_per_key > 0.0 && bloom_bits_per_key <= 64.0))
+    throw Error(GJ_EINVAL, "prefilter: bloom_bits_per_key must be in (0, 64]");
+  prefilter_impl(ctx, R, S, flags, op, eps, bloom_bits_per_key, key_out_R, rid_out_R, n_R_out, key_out_S,
+                 rid_out_S, n_S_out);
+  API_END
+}
+
+gj_status join_host(gj_ctx* ctx, const void* key_R_host, uint64_t n_R, const void* key_S_host, uint64_t n_S,
+                    int key_type, uint32_t* out_host, uint64_t capacity, uint64_t* n_out) {
+  API_BEGIN
+  if (!ctx || !n_out) throw Error(GJ_EINVAL, "join_host: NULL ctx or n_out");
+  if ((n_R && !key_R_host) || (n_S && !key_S_host)) throw Error(GJ_EINVAL, "join_host: NULL key buffer");
+  if (key_type != GJ_I32 && key_type != GJ_I64) throw Error(GJ_EINVAL, "join_host: bad key_type");
+  if (n_R >= (1ull << 32) || n_S >= (1ull << 32)) throw Error(GJ_EINVAL, "join_host: n must be < 2^32");
+  const size_t ks = key_type == GJ_I64 ? 8 : 4;
+  gj_rel R{nullptr, nullptr, n_R, key_type, 0}, S{nullptr, nullptr, n_S, key_type, 0};
+  void* dR = ws(ctx, "host.R", n_R * ks);
+  void* dS = ws(ctx, "host.S", n_S * ks);
+  if (n_R) GJ_CUDA(cudaMemcpyAsync(dR, key_R_host, n_R * ks, cudaMemcpyHostToDevice, ctx->stream));
+  if (n_S) GJ_CUDA(cudaMemcpyAsync(dS, key_S_host, n_S * ks, cudaMemcpyHostToDevice, ctx->stream));
+  R.key = dR;
+  S.key = dS;
+  do_join_count(ctx, R, S);
+  const uint64_t total = ctx->jc.total;
+  *n_out = total;
+  if (capacity < total) throw Error(GJ_ERANGE, "join_host: capacity < |J|");
+  if (total && !out_host) throw Error(GJ_EINVAL, "join_host: out_host is NULL");
+  if (total) {
+    uint32_t* dout = static_cast<uint32_t*>(ws(ctx, "host.out", total * 8));
+    hash_join_write(ctx, dout);
+    GJ_CUDA(cudaMemcpyAsync(out_host, dout, total * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  GJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  API_END
+}
+
+}  // extern "C"

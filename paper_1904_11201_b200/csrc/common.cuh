@@ -1,0 +1,75 @@
+// common.cuh -- device helpers shared by the gjoin kernels (product code only).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "gjoin.h"
+
+namespace gj {
+
+constexpr uint32_t FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------- key traits
+// Signed keys are compared through an order-preserving bias to unsigned
+// (k ^ sign bit), so the carry-out of an unsigned subtraction decides r >= s.
+template <typename K> struct KeyT;
+template <> struct KeyT<int32_t> {
+  using U = uint32_t;
+  static constexpr int kType = GJ_I32;
+  __host__ __device__ static __forceinline__ U bias(int32_t k) { return (U)k ^ 0x80000000u; }
+};
+template <> struct KeyT<int64_t> {
+  using U = uint64_t;
+  static constexpr int kType = GJ_I64;
+  __host__ __device__ static __forceinline__ U bias(int64_t k) { return (U)k ^ 0x8000000000000000ull; }
+};
+
+// Multiplicative hash (Fibonacci hashing): the high 32 bits of key * 2^64/phi.
+// Partition = top B bits; in-partition hash-table slot = the next bits below.
+// Raw low key bits are NOT used: configs[4]'s R keys are all even.
+__device__ __forceinline__ uint32_t khash(int32_t k) {
+  return (uint32_t)(((uint64_t)(uint32_t)k * 0x9E3779B97F4A7C15ull) >> 32);
+}
+__device__ __forceinline__ uint32_t khash(int64_t k) {
+  uint64_t x = (uint64_t)k;
+  x ^= x >> 32;
+  return (uint32_t)((x * 0x9E3779B97F4A7C15ull) >> 32);
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+// Inclusive warp scan (Kogge-Stone over shuffles).
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(FULL, v, o);
+    if ((int)lane_id() >= o) v += n;
+  }
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// Binary search: largest i in [0, n) with a[i] <= x (a ascending, a[0] <= x).
+template <typename T>
+__device__ __forceinline__ uint32_t upper_index(const T* __restrict__ a, uint32_t n, T x) {
+  uint32_t lo = 0, hi = n;  // invariant: a[lo] <= x, answer in [lo, hi)
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+}  // namespace gj

@@ -1,0 +1,527 @@
+// nlj.cu -- tiled nested-loop theta join: count pass + write pass.
+//
+// Paper: §3.3.1 GPU-Based Nested Loop Join and §4.2's GPU theta
+// join, which runs the same nested loop with a theta predicate.
+// The paper gives each thread NB_S x NB_T tuples (Eq.1-4) and a
+// private Cartesian-size result slot.  B200 design (DESIGN.md
+// §4.4): a CTA owns an R tile of 2048 keys held in registers (8 per thread) and
+// streams a range of S through a 4-stage shared-memory ring filled by 1-D TMA bulk
+// copies (cp.async.bulk + mbarrier complete_tx).  Each S key is read from shared
+// memory once per 4 keys (LDS.128 broadcast) and compared against the 8 register
+// keys with the carry-chain trick: `sub.cc` + `addc` compile to IADD3 (carry-out
+// predicate) + one IADD3.X that folds two carries into the counter, i.e. 1.5 ALU
+// instructions per (r, s) pair for <, <=, >, >= (2.5 for =, != and band).  Signed
+// keys are compared as (key ^ signbit) unsigned.  The band predicate uses
+// t = (r + eps) - s  (mod 2^32),  match <=> t <= 2 eps, which is exact only when
+// span + eps < 2^32 and 2 eps < 2^32 (reading R5); otherwise the exact
+// 64-bit path runs.  Exact sizing: counts per (work unit, warp) -> exclusive scan
+// -> the write pass re-runs the traversal and, when a warp sees any match for an
+// S key, writes its pairs at ballot/popc ranks (deterministic order).
+#include <algorithm>
+
+#include "common.cuh"
+#include "nlj.cuh"
+#include "scan.cuh"
+
+namespace gj {
+namespace {
+
+constexpr int NT = 256;            // threads per CTA
+constexpr int NWARP = NT / 32;
+constexpr int KR = 8;              // R keys per thread (registers)
+constexpr int RT = NT * KR;        // R tile = 2048 keys
+constexpr int TS = 2048;           // S keys per pipeline stage
+constexpr int STG = 4;             // pipeline depth
+
+enum Fam { F_GE = 0, F_LE = 1, F_NE = 2, F_BAND = 3, F_GENERIC = 4 };
+
+// ------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(saddr(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// 1-D TMA: global -> shared bulk copy completing on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(bar))
+      : "memory");
+}
+
+// ------------------------------------------------- carry-chain pair counters
+// c += (a1 >= s) + (a2 >= s)   (unsigned)
+__device__ __forceinline__ void acc_ge2(uint32_t& c, uint32_t a1, uint32_t a2, uint32_t s) {
+  asm("{\n .reg .u32 t1, t2;\n sub.cc.u32 t1, %1, %3;\n addc.u32 %0, %0, 0;\n"
+      " sub.cc.u32 t2, %2, %3;\n addc.u32 %0, %0, 0;\n}"
+      : "+r"(c)
+      : "r"(a1), "r"(a2), "r"(s));
+}
+// c += (s >= a1) + (s >= a2)
+__device__ __forceinline__ void acc_le2(uint32_t& c, uint32_t a1, uint32_t a2, uint32_t s) {
+  asm("{\n .reg .u32 t1, t2;\n sub.cc.u32 t1, %3, %1;\n addc.u32 %0, %0, 0;\n"
+      " sub.cc.u32 t2, %3, %2;\n addc.u32 %0, %0, 0;\n}"
+      : "+r"(c)
+      : "r"(a1), "r"(a2), "r"(s));
+}
+// c += (a1 != s) + (a2 != s)   via  (a ^ s) >= 1
+__device__ __forceinline__ void acc_ne2(uint32_t& c, uint32_t a1, uint32_t a2, uint32_t s) {
+  asm("{\n .reg .u32 x1, x2, t1, t2;\n xor.b32 x1, %1, %3;\n xor.b32 x2, %2, %3;\n"
+      " sub.cc.u32 t1, x1, 1;\n addc.u32 %0, %0, 0;\n"
+      " sub.cc.u32 t2, x2, 1;\n addc.u32 %0, %0, 0;\n}"
+      : "+r"(c)
+      : "r"(a1), "r"(a2), "r"(s));
+}
+// c += ((a1 - s) >= C) + ((a2 - s) >= C)   (band non-matches; a = r + eps, C = 2eps+1)
+__device__ __forceinline__ void acc_nb2(uint32_t& c, uint32_t a1, uint32_t a2, uint32_t s, uint32_t C) {
+  asm("{\n .reg .u32 x1, x2, t1, t2;\n sub.u32 x1, %1, %3;\n sub.u32 x2, %2, %3;\n"
+      " sub.cc.u32 t1, x1, %4;\n addc.u32 %0, %0, 0;\n"
+      " sub.cc.u32 t2, x2, %4;\n addc.u32 %0, %0, 0;\n}"
+      : "+r"(c)
+      : "r"(a1), "r"(a2), "r"(s), "r"(C));
+}
+
+// Count the carries of all KR register keys against one biased S key.
+template <int FAM>
+__device__ __forceinline__ void step8(uint32_t& c, const uint32_t (&r)[KR], uint32_t su, uint32_t C) {
+#pragma unroll
+  for (int i = 0; i < KR; i += 2) {
+    if (FAM == F_GE) acc_ge2(c, r[i], r[i + 1], su);
+    if (FAM == F_LE) acc_le2(c, r[i], r[i + 1], su);
+    if (FAM == F_NE) acc_ne2(c, r[i], r[i + 1], su);
+    if (FAM == F_BAND) acc_nb2(c, r[i], r[i + 1], su, C);
+  }
+}
+// Does the counted event mean "match" (false = complement: count = pairs - carries)?
+__host__ __device__ constexpr bool direct(int op) { return op == GJ_GE || op == GJ_LE || op == GJ_NE; }
+__host__ __device__ constexpr int family(int op) {
+  return (op == GJ_GE || op == GJ_LT) ? F_GE
+       : (op == GJ_LE || op == GJ_GT) ? F_LE
+       : (op == GJ_NE || op == GJ_EQ) ? F_NE
+                                      : F_BAND;
+}
+// Explicit fast-path predicate on biased keys (write pass).
+template <int OP>
+__device__ __forceinline__ bool pred_fast(uint32_t r, uint32_t su, uint32_t C) {
+  switch (OP) {
+    case GJ_GE: return r >= su;
+    case GJ_LT: return r < su;
+    case GJ_LE: return su >= r;
+    case GJ_GT: return su < r;
+    case GJ_NE: return r != su;
+    case GJ_EQ: return r == su;
+    default: return (r - su) < C;  // band: r holds (biased r) + eps
+  }
+}
+
+// Exact predicate R.key OP S.key on the original signed keys.
+template <typename K, int OP>
+__device__ __forceinline__ bool theta_exact(K r, K s, uint64_t eps) {
+  switch (OP) {
+    case GJ_EQ: return r == s;
+    case GJ_NE: return r != s;
+    case GJ_LT: return r < s;
+    case GJ_LE: return r <= s;
+    case GJ_GT: return r > s;
+    case GJ_GE: return r >= s;
+    default: {
+      // (uint64)(sign-extended key) differences are exact mod 2^64, and the true
+      // distance of two int32/int64 keys is < 2^64.
+      const uint64_t d = r >= s ? (uint64_t)(int64_t)r - (uint64_t)(int64_t)s
+                                : (uint64_t)(int64_t)s - (uint64_t)(int64_t)r;
+      return d <= eps;
+    }
+  }
+}
+
+struct NLJArgs {
+  const void* rkey;
+  const uint32_t* rrid;
+  uint32_t rrid_base;
+  uint64_t nR;
+  const void* skey;
+  const uint32_t* srid;
+  uint32_t srid_base;
+  uint64_t nS;
+  uint64_t eps;
+  uint32_t C;
+  uint32_t nsplit;
+  uint64_t SR;
+  uint32_t U;
+  uint32_t* work;
+  uint64_t* wcnt;
+  const uint64_t* woff;
+  uint2* out;
+};
+
+template <typename K, int OP, bool FAST, bool WRITE>
+__global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  K* sbuf = reinterpret_cast<K*>(smem);  // STG * TS keys
+  __shared__ __align__(8) uint64_t bar[STG];
+  __shared__ uint32_t s_u;
+  const K* __restrict__ rkey = static_cast<const K*>(a.rkey);
+  const K* __restrict__ skey = static_cast<const K*>(a.skey);
+  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
+  if (tid == 0) {
+    for (int b = 0; b < STG; ++b) mbar_init(&bar[b], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t g = 0;  // CTA-wide tile sequence number (drives mbarrier parities)
+
+  for (;;) {
+    if (tid == 0) s_u = atomicAdd(a.work, 1u);
+    __syncthreads();
+    const uint32_t u = s_u;
+    if (u >= a.U) break;
+    const uint64_t r0 = (uint64_t)(u / a.nsplit) * RT;
+    const uint64_t sbeg = (uint64_t)(u % a.nsplit) * a.SR;
+    const uint64_t send = min(sbeg + a.SR, a.nS);
+    const uint64_t slen = send > sbeg ? send - sbeg : 0;
+    const uint32_t ntiles = (uint32_t)((slen + TS - 1) / TS);
+    const bool full = r0 + RT <= a.nR;
+
+    K rk[KR];
+    uint32_t rf[KR], rr[KR];
+    uint32_t nvalid = 0;
+#pragma unroll
+    for (int i = 0; i < KR; ++i) {
+      const uint64_t row = r0 + (uint64_t)i * NT + tid;
+      const bool v = row < a.nR;
+      rk[i] = v ? rkey[row] : K(0);
+      nvalid += v;
+      if (WRITE) rr[i] = v ? (a.rrid ? a.rrid[row] : a.rrid_base + (uint32_t)row) : 0u;
+      if (FAST) {
+        uint32_t b = (uint32_t)rk[i] ^ 0x80000000u;
+        rf[i] = (OP == GJ_BAND) ? b + (uint32_t)a.eps : b;
+      }
+    }
+
+    auto issue = [&](uint32_t t, uint32_t seq) {
+      const uint32_t buf = seq % STG;
+      const uint64_t tb = sbeg + (uint64_t)t * TS;
+      const uint32_t tn = (uint32_t)min((uint64_t)TS, slen - (uint64_t)t * TS);
+      const uint32_t bytes = (tn * (uint32_t)sizeof(K)) & ~15u;
+      fence_proxy_async();
+      if (bytes) {
+        mbar_expect_tx(&bar[buf], bytes);
+        bulk_g2s(sbuf + buf * TS, skey + tb, bytes, &bar[buf]);
+      } else {
+        mbar_arrive(&bar[buf]);
+      }
+    };
+    if (tid == 0)
+      for (uint32_t t = 0; t < min(ntiles, (uint32_t)STG); ++t) issue(t, g + t);
+
+    uint64_t tot = 0;
+    uint64_t wbase = WRITE ? a.woff[(uint64_t)u * NWARP + w] : 0;
+    auto srow = [&](uint64_t idx) -> uint32_t {
+      return a.srid ? a.srid[idx] : a.srid_base + (uint32_t)idx;
+    };
+
+    for (uint32_t t = 0; t < ntiles; ++t) {
+      const uint32_t seq = g + t, buf = seq % STG;
+      mbar_wait(&bar[buf], (seq / STG) & 1);
+      const K* st = sbuf + buf * TS;
+      const uint64_t tb = sbeg + (uint64_t)t * TS;
+      const uint32_t tn = (uint32_t)min((uint64_t)TS, slen - (uint64_t)t * TS);
+      const uint32_t tn16 = ((tn * (uint32_t)sizeof(K)) & ~15u) / (uint32_t)sizeof(K);
+      auto skey_at = [&](uint32_t j) -> K { return j < tn16 ? st[j] : skey[tb + j]; };
+
+      if (FAST && full) {
+        constexpr int FAM = family(OP);
+        if (!WRITE) {
+          uint32_t acc = 0;
+          const uint4* s4 = reinterpret_cast<const uint4*>(st);
+          const uint32_t n4 = tn16 >> 2;
+#pragma unroll 4
+          for (uint32_t j = 0; j < n4; ++j) {
+            const uint4 v = s4[j];
+            step8<FAM>(acc, rf, v.x ^ 0x80000000u, a.C);
+            step8<FAM>(acc, rf, v.y ^ 0x80000000u, a.C);
+            step8<FAM>(acc, rf, v.z ^ 0x80000000u, a.C);
+            step8<FAM>(acc, rf, v.w ^ 0x80000000u, a.C);
+          }
+          for (uint32_t j = n4 * 4; j < tn; ++j) step8<FAM>(acc, rf, (uint32_t)skey_at(j) ^ 0x80000000u, a.C);
+          tot += acc;
+        } else {
+          for (uint32_t j = 0; j < tn; ++j) {
+            const uint32_t su = (uint32_t)skey_at(j) ^ 0x80000000u;
+            uint32_t acc = 0;
+            step8<FAM>(acc, rf, su, a.C);
+            const uint32_t m = direct(OP) ? acc : KR - acc;
+            if (__any_sync(FULL, m != 0)) {
+              const uint32_t sr = srow(tb + j);
+#pragma unroll
+              for (int i = 0; i < KR; ++i) {
+                const bool p = pred_fast<OP>(rf[i], su, a.C);
+                const uint32_t bal = __ballot_sync(FULL, p);
+                if (p) a.out[wbase + __popc(bal & lanemask_lt())] = make_uint2(rr[i], sr);
+                wbase += __popc(bal);
+              }
+            }
+          }
+        }
+      } else {
+        // exact generic path: int64 keys, the ragged last R tile, band overflow cases
+        for (uint32_t j = 0; j < tn; ++j) {
+          const K s = skey_at(j);
+          if (!WRITE) {
+            uint32_t c = 0;
+#pragma unroll
+            for (int i = 0; i < KR; ++i)
+              c += ((r0 + (uint64_t)i * NT + tid) < a.nR && theta_exact<K, OP>(rk[i], s, a.eps));
+            tot += c;
+          } else {
+            bool any = false;
+            bool p[KR];
+#pragma unroll
+            for (int i = 0; i < KR; ++i) {
+              p[i] = (r0 + (uint64_t)i * NT + tid) < a.nR && theta_exact<K, OP>(rk[i], s, a.eps);
+              any |= p[i];
+            }
+            if (__any_sync(FULL, any)) {
+              const uint32_t sr = srow(tb + j);
+#pragma unroll
+              for (int i = 0; i < KR; ++i) {
+                const uint32_t bal = __ballot_sync(FULL, p[i]);
+                if (p[i]) a.out[wbase + __popc(bal & lanemask_lt())] = make_uint2(rr[i], sr);
+                wbase += __popc(bal);
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0 && t + STG < ntiles) issue(t + STG, seq + STG);
+    }
+    g += ntiles;
+    if (!WRITE) {
+      uint64_t c = tot;
+      if (FAST && full && !direct(OP)) c = (uint64_t)nvalid * slen - tot;
+      c = warp_sum(c);
+      if (lane == 0) a.wcnt[(uint64_t)u * NWARP + w] = c;
+    }
+    __syncthreads();
+  }
+}
+
+template <typename K>
+__global__ void minmax_kernel(const K* __restrict__ key, uint64_t n, unsigned long long* mm) {
+  unsigned long long lo = ~0ull, hi = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    unsigned long long b = (unsigned long long)KeyT<K>::bias(key[i]);
+    lo = min(lo, b);
+    hi = max(hi, b);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(FULL, lo, o));
+    hi = max(hi, __shfl_xor_sync(FULL, hi, o));
+  }
+  if (lane_id() == 0) {
+    atomicMin(&mm[0], lo);
+    atomicMax(&mm[1], hi);
+  }
+}
+__global__ void minmax_init(unsigned long long* mm) {
+  mm[0] = ~0ull;
+  mm[1] = 0;
+}
+
+__global__ void cross_kernel(const uint32_t* __restrict__ rrid, uint32_t rbase, uint64_t nR,
+                             const uint32_t* __restrict__ srid, uint32_t sbase, uint64_t nS, uint2* out) {
+  const uint64_t total = nR * nS;
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = x / nS, j = x - i * nS;
+    out[x] = make_uint2(rrid ? rrid[i] : rbase + (uint32_t)i, srid ? srid[j] : sbase + (uint32_t)j);
+  }
+}
+
+// ----------------------------------------------------------------- host side
+template <typename K, int OP, bool FAST>
+void run(gj_ctx* ctx, const NLJArgs& a, bool write) {
+  const size_t smem = STG * TS * sizeof(K);
+  const uint32_t grid = std::min<uint32_t>(a.U, (uint32_t)ctx->num_sms * 6);
+  if (!write) {
+    static bool once = (set_smem(nlj_kernel<K, OP, FAST, false>, smem), true);
+    (void)once;
+    launch(ctx, "nlj_count", nlj_kernel<K, OP, FAST, false>, dim3(grid), dim3(NT), smem, a);
+  } else {
+    static bool once = (set_smem(nlj_kernel<K, OP, FAST, true>, smem), true);
+    (void)once;
+    launch(ctx, "nlj_write", nlj_kernel<K, OP, FAST, true>, dim3(grid), dim3(NT), smem, a);
+  }
+}
+
+template <typename K, int OP>
+void dispatch_fast(gj_ctx* ctx, const NLJArgs& a, bool fast, bool write) {
+  if constexpr (sizeof(K) == 4) {
+    if (fast) return run<K, OP, true>(ctx, a, write);
+  }
+  run<K, OP, false>(ctx, a, write);
+}
+
+template <typename K>
+void dispatch(gj_ctx* ctx, const NLJArgs& a, int op, bool fast, bool write) {
+  switch (op) {
+    case GJ_EQ: return dispatch_fast<K, GJ_EQ>(ctx, a, fast, write);
+    case GJ_NE: return dispatch_fast<K, GJ_NE>(ctx, a, fast, write);
+    case GJ_LT: return dispatch_fast<K, GJ_LT>(ctx, a, fast, write);
+    case GJ_LE: return dispatch_fast<K, GJ_LE>(ctx, a, fast, write);
+    case GJ_GT: return dispatch_fast<K, GJ_GT>(ctx, a, fast, write);
+    case GJ_GE: return dispatch_fast<K, GJ_GE>(ctx, a, fast, write);
+    default: return dispatch_fast<K, GJ_BAND>(ctx, a, fast, write);
+  }
+}
+
+NLJArgs make_args(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, const ThetaCache& tc) {
+  NLJArgs a{};
+  a.rkey = R.key;
+  a.rrid = R.rid;
+  a.rrid_base = R.rid_base;
+  a.nR = R.n;
+  a.skey = S.key;
+  a.srid = S.rid;
+  a.srid_base = S.rid_base;
+  a.nS = S.n;
+  a.eps = tc.eps;
+  a.C = (uint32_t)(2 * tc.eps + 1);
+  a.nsplit = tc.nsplit;
+  a.SR = tc.SR;
+  a.U = tc.U;
+  return a;
+}
+
+template <typename K>
+void theta_count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S0, int op, uint64_t eps) {
+  ThetaCache& tc = ctx->tc;
+  tc.op = op;
+  tc.eps = eps;
+  tc.all_pairs = false;
+  tc.total = 0;
+  tc.U = 0;
+  gj_rel S = S0;
+  if (R.n == 0 || S.n == 0) return;
+  // cp.async.bulk needs a 16-byte aligned source: realign S if the caller's view is not.
+  if (reinterpret_cast<uintptr_t>(S.key) % 16 != 0) {
+    void* al = ws(ctx, "nlj.salign", S.n * sizeof(K));
+    GJ_CUDA(cudaMemcpyAsync(al, S.key, S.n * sizeof(K), cudaMemcpyDeviceToDevice, ctx->stream));
+    S.key = al;
+  }
+  tc.S = S;
+  bool fast = (sizeof(K) == 4) && !ctx->force_slow_band;
+  if (op == GJ_BAND) {
+    unsigned long long* mm = static_cast<unsigned long long*>(ws(ctx, "nlj.minmax", 4 * sizeof(unsigned long long)));
+    key_minmax(ctx, R, mm);
+    key_minmax(ctx, S, mm + 2);
+    unsigned long long h[4];
+    d2h_sync(ctx, h, mm, sizeof(h));
+    const unsigned long long lo = std::min(h[0], h[2]), hi = std::max(h[1], h[3]);
+    const unsigned long long span = hi - lo;  // exact: biased keys are order-preserving
+    if (eps >= span) {
+      tc.all_pairs = true;
+      tc.total = R.n * S.n;
+      return;
+    }
+    // t = (r + eps) - s mod 2^32 is exact iff span + eps < 2^32 and 2 eps < 2^32
+    if (!(span + eps < (1ull << 32) && 2 * eps < (1ull << 32) - 1)) fast = false;
+    if (ctx->force_slow_band) fast = false;
+  }
+  tc.mode = fast ? 1 : 0;
+  const uint64_t n_rt = (R.n + RT - 1) / RT;
+  const uint64_t max_split = (S.n + TS - 1) / TS;
+  uint64_t nsplit = ctx->nlj_split ? ctx->nlj_split : std::max<uint64_t>(1, (16384 + n_rt - 1) / n_rt);
+  nsplit = std::min(nsplit, max_split);
+  uint64_t SR = (S.n + nsplit - 1) / nsplit;
+  SR = (SR + TS - 1) / TS * TS;
+  nsplit = (S.n + SR - 1) / SR;
+  if (n_rt * nsplit >= (1ull << 31)) throw Error(GJ_EINVAL, "theta join too large for one call");
+  tc.nsplit = (uint32_t)nsplit;
+  tc.SR = SR;
+  tc.U = (uint32_t)(n_rt * nsplit);
+  const uint64_t nw = (uint64_t)tc.U * NWARP;
+  uint64_t* wcnt = static_cast<uint64_t*>(ws(ctx, "nlj.wcnt", (nw + 1) * sizeof(uint64_t)));
+  uint64_t* woff = static_cast<uint64_t*>(ws(ctx, "nlj.woff", (nw + 1) * sizeof(uint64_t)));
+  uint32_t* work = static_cast<uint32_t*>(ws(ctx, "nlj.work", 16));
+  GJ_CUDA(cudaMemsetAsync(work, 0, sizeof(uint32_t), ctx->stream));
+  NLJArgs a = make_args(ctx, R, S, tc);
+  a.work = work;
+  a.wcnt = wcnt;
+  dispatch<K>(ctx, a, op, fast, false);
+  exclusive_scan<uint64_t, uint64_t>(ctx, wcnt, woff, nw, woff + nw);
+  tc.woff = woff;
+  d2h_sync(ctx, &tc.total, woff + nw, sizeof(uint64_t));
+}
+
+template <typename K>
+void theta_write_impl(gj_ctx* ctx, uint32_t* out) {
+  ThetaCache& tc = ctx->tc;
+  if (tc.total == 0) return;
+  if (tc.all_pairs) return cross_write(ctx, tc.R, tc.S, out);
+  uint32_t* work = static_cast<uint32_t*>(ws(ctx, "nlj.work", 16));
+  GJ_CUDA(cudaMemsetAsync(work, 0, sizeof(uint32_t), ctx->stream));
+  NLJArgs a = make_args(ctx, tc.R, tc.S, tc);
+  a.work = work;
+  a.woff = tc.woff;
+  a.out = reinterpret_cast<uint2*>(out);
+  dispatch<K>(ctx, a, tc.op, tc.mode == 1, true);
+}
+
+}  // namespace
+
+void key_minmax(gj_ctx* ctx, const gj_rel& X, unsigned long long* mm) {
+  launch(ctx, "minmax_init", minmax_init, dim3(1), dim3(1), 0, mm);
+  const unsigned grid = (unsigned)std::min<uint64_t>((X.n + 1023) / 1024, (uint64_t)ctx->num_sms * 8);
+  if (X.key_type == GJ_I32)
+    launch(ctx, "minmax", minmax_kernel<int32_t>, dim3(grid), dim3(256), 0, static_cast<const int32_t*>(X.key), X.n, mm);
+  else
+    launch(ctx, "minmax", minmax_kernel<int64_t>, dim3(grid), dim3(256), 0, static_cast<const int64_t*>(X.key), X.n, mm);
+}
+
+void cross_write(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t* out) {
+  const uint64_t total = R.n * S.n;
+  if (!total) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, (uint64_t)ctx->num_sms * 16);
+  launch(ctx, "cross_write", cross_kernel, dim3(grid), dim3(256), 0, R.rid, R.rid_base, R.n, S.rid, S.rid_base,
+         S.n, reinterpret_cast<uint2*>(out));
+}
+
+void theta_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, int op, uint64_t eps) {
+  ctx->tc.R = R;
+  if (R.key_type == GJ_I32) theta_count_impl<int32_t>(ctx, R, S, op, eps);
+  else theta_count_impl<int64_t>(ctx, R, S, op, eps);
+}
+
+void theta_write(gj_ctx* ctx, uint32_t* out) {
+  if (ctx->tc.R.key_type == GJ_I32) theta_write_impl<int32_t>(ctx, out);
+  else theta_write_impl<int64_t>(ctx, out);
+}
+
+}  // namespace gj

@@ -1,0 +1,265 @@
+// prefilter.cu -- range + Bloom pre-filter with stable stream compaction.
+//
+// Paper: §3.1 Data Pre-filtering (Alg.1 lines 1-13): a first
+// MapReduce round extracts the join keys common to BOTH tables, a second round
+// loads them into a hash table in Setup() and drops every tuple whose key is not
+// in it, filtering both tables.  B200 design: the exact key set
+// becomes (1) a range test against [max(min R, min S) - eps, min(max R, max S) + eps]
+// (two min/max reductions) and (2) a sector-blocked Bloom filter: every key sets 8
+// bits inside one 32-byte block, so a probe is ONE 32-byte sector read.  Filter S
+// by R's filter, then (two-sided) R by the filter of S's survivors.  No false
+// negatives, so J(filtered R, filtered S) = J(R, S).  Survivors are compacted
+// stably (count -> scan -> write) keeping their original rids.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "nlj.cuh"
+#include "runtime.h"
+#include "scan.cuh"
+
+namespace gj {
+gj_status prefilter_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t flags, int op,
+                         uint64_t eps, double bpk, void* kR, uint32_t* rR, uint64_t* nRo, void* kS,
+                         uint32_t* rS, uint64_t* nSo);
+namespace {
+
+constexpr int FT = 256;
+constexpr int FI = 16;
+constexpr int FTILE = FT * FI;  // 4096 keys per compaction tile
+
+struct Filt {
+  unsigned long long lo, hi;  // biased key range (inclusive)
+  int use_range;
+  const uint32_t* bloom;      // nblocks * 8 words, or nullptr
+  uint32_t log_blocks;
+};
+
+__device__ __forceinline__ uint64_t bloom_hash(int32_t k) {
+  uint64_t h = (uint64_t)(uint32_t)k * 0xC2B2AE3D27D4EB4Full;
+  h ^= h >> 29;
+  h *= 0x165667B19E3779F9ull;
+  return h ^ (h >> 32);
+}
+__device__ __forceinline__ uint64_t bloom_hash(int64_t k) {
+  uint64_t h = (uint64_t)k * 0xC2B2AE3D27D4EB4Full;
+  h ^= h >> 29;
+  h *= 0x165667B19E3779F9ull;
+  return h ^ (h >> 32);
+}
+
+// Block index from the top bits, the 8 bit positions (0..255) from a remix.
+struct BloomSlot {
+  uint32_t block;
+  uint32_t mask[8];
+};
+template <typename K>
+__device__ __forceinline__ BloomSlot bloom_slot(K k, uint32_t log_blocks) {
+  BloomSlot b;
+  const uint64_t h = bloom_hash(k);
+  b.block = log_blocks ? (uint32_t)(h >> (64 - log_blocks)) : 0u;
+  const uint64_t h2 = (h ^ (h >> 31)) * 0x9E3779B97F4A7C15ull;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) b.mask[i] = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t pos = (uint32_t)(h2 >> (8 * i)) & 255u;
+#pragma unroll
+    for (int w = 0; w < 8; ++w)
+      if ((pos >> 5) == (uint32_t)w) b.mask[w] |= 1u << (pos & 31);
+  }
+  return b;
+}
+
+template <typename K>
+__device__ __forceinline__ bool keep(K k, const Filt& f) {
+  if (f.use_range) {
+    const unsigned long long b = (unsigned long long)KeyT<K>::bias(k);
+    if (b < f.lo || b > f.hi) return false;
+  }
+  if (f.bloom) {
+    const BloomSlot s = bloom_slot(k, f.log_blocks);
+    const uint4* p = reinterpret_cast<const uint4*>(f.bloom + (uint64_t)s.block * 8);
+    const uint4 a = __ldg(p), c = __ldg(p + 1);
+    const uint32_t wv[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+    bool ok = true;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) ok &= (wv[w] & s.mask[w]) == s.mask[w];
+    return ok;
+  }
+  return true;
+}
+
+template <typename K>
+__global__ void bloom_build(const K* __restrict__ key, uint64_t n, Filt range, uint32_t* __restrict__ bloom,
+                            uint32_t log_blocks) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const K k = key[i];
+    if (!keep(k, range)) continue;
+    const BloomSlot s = bloom_slot(k, log_blocks);
+#pragma unroll
+    for (int w = 0; w < 8; ++w)
+      if (s.mask[w]) atomicOr(&bloom[(uint64_t)s.block * 8 + w], s.mask[w]);
+  }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(FT) pf_count(const K* __restrict__ key, uint64_t n, Filt f,
+                                               uint32_t* __restrict__ tile_cnt) {
+  const uint64_t beg = (uint64_t)blockIdx.x * FTILE;
+  uint32_t c = 0;
+#pragma unroll 4
+  for (int k = 0; k < FI; ++k) {
+    const uint64_t i = beg + (uint64_t)k * FT + threadIdx.x;
+    if (i < n) c += keep(key[i], f);
+  }
+  __shared__ uint32_t red[FT / 32];
+  c = warp_sum(c);
+  if (lane_id() == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < FT / 32; ++w) t += red[w];
+    tile_cnt[blockIdx.x] = t;
+  }
+}
+
+// Stable compaction: warp w owns tile items [w*32*FI, (w+1)*32*FI) in order.
+template <typename K>
+__global__ void __launch_bounds__(FT) pf_write(const K* __restrict__ key, const uint32_t* __restrict__ rid,
+                                               uint32_t rid_base, uint64_t n, Filt f,
+                                               const uint32_t* __restrict__ tile_off, K* __restrict__ kout,
+                                               uint32_t* __restrict__ rout) {
+  __shared__ uint32_t woff[FT / 32];
+  const uint32_t w = threadIdx.x >> 5, lane = lane_id();
+  const uint64_t beg = (uint64_t)blockIdx.x * FTILE + (uint64_t)w * 32 * FI;
+  K k[FI];
+  uint32_t fl = 0;
+#pragma unroll
+  for (int j = 0; j < FI; ++j) {
+    const uint64_t i = beg + (uint64_t)j * 32 + lane;
+    k[j] = i < n ? key[i] : K(0);
+    if (i < n && keep(k[j], f)) fl |= 1u << j;
+  }
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int j = 0; j < FI; ++j) cnt += __popc(__ballot_sync(FULL, (fl >> j) & 1));
+  if (lane == 0) woff[w] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = tile_off[blockIdx.x];
+    for (int ww = 0; ww < FT / 32; ++ww) {
+      const uint32_t c = woff[ww];
+      woff[ww] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  uint32_t pos = woff[w];
+#pragma unroll
+  for (int j = 0; j < FI; ++j) {
+    const bool p = (fl >> j) & 1;
+    const uint32_t bal = __ballot_sync(FULL, p);
+    if (p) {
+      const uint64_t i = beg + (uint64_t)j * 32 + lane;
+      const uint32_t o = pos + __popc(bal & lanemask_lt());
+      kout[o] = k[j];
+      rout[o] = rid ? rid[i] : rid_base + (uint32_t)i;
+    }
+    pos += __popc(bal);
+  }
+}
+
+template <typename K>
+uint64_t compact(gj_ctx* ctx, const gj_rel& X, const Filt& f, void* kout, uint32_t* rout, const char* tag) {
+  if (X.n == 0) return 0;
+  const uint64_t ntiles = (X.n + FTILE - 1) / FTILE;
+  std::string t(tag);
+  uint32_t* cnt = static_cast<uint32_t*>(ws(ctx, (t + ".pfcnt").c_str(), (ntiles + 1) * sizeof(uint32_t)));
+  launch(ctx, "pf_count", pf_count<K>, dim3((unsigned)ntiles), dim3(FT), 0, static_cast<const K*>(X.key), X.n, f, cnt);
+  exclusive_scan<uint32_t, uint32_t>(ctx, cnt, cnt, ntiles, cnt + ntiles);
+  launch(ctx, "pf_write", pf_write<K>, dim3((unsigned)ntiles), dim3(FT), 0, static_cast<const K*>(X.key), X.rid,
+         X.rid_base, X.n, f, (const uint32_t*)cnt, static_cast<K*>(kout), rout);
+  uint32_t h = 0;
+  d2h_sync(ctx, &h, cnt + ntiles, sizeof(uint32_t));
+  return h;
+}
+
+template <typename K>
+const uint32_t* build_bloom(gj_ctx* ctx, const gj_rel& X, const Filt& range, double bpk, uint32_t* log_blocks,
+                            const char* tag) {
+  const double bits = std::max(256.0, (double)X.n * bpk);
+  uint32_t lb = 0;
+  while ((256.0 * (double)(1ull << lb)) < bits && lb < 40) ++lb;
+  *log_blocks = lb;
+  const uint64_t words = (1ull << lb) * 8;
+  uint32_t* bloom = static_cast<uint32_t*>(ws(ctx, tag, words * sizeof(uint32_t)));
+  GJ_CUDA(cudaMemsetAsync(bloom, 0, words * sizeof(uint32_t), ctx->stream));
+  if (X.n) {
+    const unsigned grid = (unsigned)std::min<uint64_t>((X.n + 255) / 256, (uint64_t)ctx->num_sms * 16);
+    launch(ctx, "bloom_build", bloom_build<K>, dim3(grid), dim3(256), 0, static_cast<const K*>(X.key), X.n, range,
+           bloom, lb);
+  }
+  return bloom;
+}
+
+template <typename K>
+void prefilter_t(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t flags, int op, uint64_t eps,
+                 double bpk, void* kR, uint32_t* rR, uint64_t* nRo, void* kS, uint32_t* rS, uint64_t* nSo) {
+  Filt range{};
+  range.lo = 0;
+  range.hi = ~0ull;
+  range.use_range = 0;
+  const uint64_t e = (op == GJ_BAND) ? eps : 0;
+  if (flags & GJ_PF_RANGE) {
+    unsigned long long* mm = static_cast<unsigned long long*>(ws(ctx, "pf.minmax", 4 * sizeof(unsigned long long)));
+    key_minmax(ctx, R, mm);
+    key_minmax(ctx, S, mm + 2);
+    unsigned long long h[4];
+    d2h_sync(ctx, h, mm, sizeof(h));
+    if (R.n == 0 || S.n == 0) {
+      range.lo = 1;
+      range.hi = 0;  // empty range: nothing survives (the join is empty)
+    } else {
+      const unsigned long long lo = std::max(h[0], h[2]), hi = std::min(h[1], h[3]);
+      range.lo = lo >= e ? lo - e : 0;
+      range.hi = (~0ull - hi) >= e ? hi + e : ~0ull;
+    }
+    range.use_range = 1;
+  }
+  const bool bloom_ok = (flags & GJ_PF_BLOOM) && (op == GJ_EQ || (op == GJ_BAND && eps == 0));
+  if (!bloom_ok) {
+    *nSo = compact<K>(ctx, S, range, kS, rS, "S");
+    *nRo = compact<K>(ctx, R, range, kR, rR, "R");
+    return;
+  }
+  // S filtered by the Bloom filter of R's in-range keys
+  Filt fs = range;
+  fs.bloom = build_bloom<K>(ctx, R, range, bpk, &fs.log_blocks, "pf.bloomR");
+  *nSo = compact<K>(ctx, S, fs, kS, rS, "S");
+  if (flags & GJ_PF_TWO_SIDED) {
+    gj_rel S2 = S;
+    S2.key = kS;
+    S2.rid = rS;
+    S2.n = *nSo;
+    Filt fr = range;
+    fr.bloom = build_bloom<K>(ctx, S2, range, bpk, &fr.log_blocks, "pf.bloomS");
+    *nRo = compact<K>(ctx, R, fr, kR, rR, "R");
+  } else {
+    *nRo = compact<K>(ctx, R, range, kR, rR, "R");
+  }
+}
+
+}  // namespace
+
+gj_status prefilter_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t flags, int op, uint64_t eps,
+                         double bpk, void* kR, uint32_t* rR, uint64_t* nRo, void* kS, uint32_t* rS,
+                         uint64_t* nSo) {
+  if (R.key_type == GJ_I32)
+    prefilter_t<int32_t>(ctx, R, S, flags, op, eps, bpk, kR, rR, nRo, kS, rS, nSo);
+  else
+    prefilter_t<int64_t>(ctx, R, S, flags, op, eps, bpk, kR, rR, nRo, kS, rS, nSo);
+  return GJ_OK;
+}
+
+}  // namespace gj

@@ -1,0 +1,136 @@
+// runtime.h -- host runtime internals: the gj_ctx, scratch workspace, launch
+// accounting and per-kernel CUDA-event timing.  Product code only.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gjoin.h"
+
+namespace gj {
+
+// Thrown inside the library, converted to a gj_status at the C-ABI boundary.
+struct Error : std::runtime_error {
+  gj_status code;
+  Error(gj_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define GJ_CUDA(expr)                                                                   \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      throw ::gj::Error(_e == cudaErrorMemoryAllocation ? GJ_ENOMEM : GJ_ECUDA,         \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e));            \
+  } while (0)
+
+struct Buf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+// Per-call cache so that *_materialize reuses what the preceding *_count built.
+struct JoinCache {
+  bool valid = false;
+  gj_rel R{}, S{};
+  bool swap = false;     // build side is S
+  uint32_t B = 0;        // radix bits
+  uint32_t P = 1;        // partitions
+  const void* bkey = nullptr;  // partitioned build keys / rids
+  const uint32_t* brid = nullptr;
+  const void* pkey = nullptr;  // partitioned probe keys / rids
+  const uint32_t* prid = nullptr;
+  const uint32_t* boff = nullptr;  // P+1
+  const uint32_t* poff = nullptr;  // P+1
+  const uint32_t* unit_off = nullptr;  // P+1
+  uint32_t U = 0;                 // work units
+  uint32_t bchunk = 0, pchunk = 0;
+  const uint64_t* woff = nullptr;  // U*W exclusive offsets
+  uint64_t total = 0;
+};
+
+struct ThetaCache {
+  bool valid = false;
+  gj_rel R{}, S{};
+  int op = 0;
+  uint64_t eps = 0;
+  int mode = 0;  // kernel variant chosen by the count pass
+  uint32_t nsplit = 1, U = 0;
+  uint64_t SR = 0;
+  const uint64_t* woff = nullptr;
+  uint64_t total = 0;
+  bool all_pairs = false;  // band with eps >= span: every pair qualifies
+  const void* S_user_key = nullptr;  // caller's S.key (tc.S may be a realigned copy)
+};
+
+struct ProfRec {
+  const char* tag;
+  cudaEvent_t a, b;
+};
+
+}  // namespace gj
+
+struct gj_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  // options (gjoin.h GJ_OPT_*)
+  int part_bits = -1;
+  uint32_t build_chunk = 4096;
+  uint32_t probe_chunk = 16384;
+  bool profile = false;
+  uint32_t nlj_split = 0;
+  bool force_slow_band = false;
+  int build_side = 0;
+  // workspace
+  std::map<std::string, gj::Buf> bufs;
+  void* host_pinned = nullptr;  // small pinned staging for counts
+  // stats
+  uint64_t launches = 0;
+  std::vector<gj::ProfRec> pending;
+  std::vector<cudaEvent_t> event_pool;
+  std::map<std::string, std::pair<double, uint64_t>> times;
+  // caches
+  gj::JoinCache jc;
+  gj::ThetaCache tc;
+};
+
+namespace gj {
+
+// Grow-only named scratch buffer, stream-ordered.
+void* ws(gj_ctx* ctx, const char* name, size_t bytes);
+// Read a small device value to the host (synchronises the ctx stream).
+void d2h_sync(gj_ctx* ctx, void* host, const void* dev, size_t bytes);
+
+// Launch bracket: counts the launch and, when profiling, records events.
+struct LaunchScope {
+  gj_ctx* ctx;
+  const char* tag;
+  cudaEvent_t a = nullptr;
+  LaunchScope(gj_ctx* c, const char* t);
+  ~LaunchScope() noexcept(false);
+};
+
+// launch(ctx, "tag", kernel<...>, grid, block, smem, args...): every kernel of the
+// library goes through here, so gj_ctx_launch_count() is exact.
+template <typename... KArgs, typename... Args>
+inline void launch(gj_ctx* ctx, const char* tag, void (*k)(KArgs...), dim3 grid, dim3 block,
+                   size_t smem, Args... args) {
+  if (grid.x == 0 || grid.y == 0 || grid.z == 0) return;
+  LaunchScope ls(ctx, tag);
+  k<<<grid, block, smem, ctx->stream>>>(static_cast<KArgs>(args)...);
+}
+
+// Opt a kernel into > 48 KB dynamic shared memory (once per kernel).
+template <typename... KArgs>
+inline void set_smem(void (*k)(KArgs...), size_t bytes) {
+  GJ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k),
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+}  // namespace gj

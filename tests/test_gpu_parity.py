@@ -1,0 +1,371 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Bit-exact on every count and on the canonically sorted (rid_R, rid_S) pairs
+(integer work: no tolerance).  Inputs are the seeded synthetic generators.
+"""
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+OPS = ["eq", "ne", "lt", "le", "gt", "ge", "band"]
+
+
+@pytest.fixture(scope="module")
+def gj():
+    import native_build
+    native_build.build_all()
+    import paper_1904_11201_b200 as m
+    return m
+
+
+@pytest.fixture()
+def ctx(gj):
+    c = gj.Context(0)
+    yield c
+    c.close()
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def canon_gpu(pairs_t):
+    """Canonically sort GPU pairs on the device; return numpy uint32 (n, 2)."""
+    if pairs_t.numel() == 0:
+        return np.zeros((0, 2), np.uint32)
+    p = pairs_t.to(torch.int64) & 0xFFFFFFFF
+    packed = (p[:, 0] << 32) | p[:, 1]
+    s, _ = torch.sort(packed)  # uint32 halves are non-negative, so signed sort is the canonical order
+    hi = (s >> 32).to(torch.int64)
+    lo = (s & 0xFFFFFFFF).to(torch.int64)
+    return torch.stack([hi, lo], 1).cpu().numpy().astype(np.uint32)
+
+
+def check_equi(gj, ctx, R, S, **kw):
+    if isinstance(R, np.ndarray):
+        tR, tS = dev(R), dev(S)
+    else:
+        tR, tS = R, S
+    n = gj.join_count(ctx, tR, tS)
+    out = gj.join_materialize(ctx, tR, tS, n)
+    Rk = R if isinstance(R, np.ndarray) else R.key.cpu().numpy()
+    Sk = S if isinstance(S, np.ndarray) else S.key.cpu().numpy()
+    cn, cp = oracle.hash_equi(Rk, Sk, **kw)
+    assert n == cn
+    got = canon_gpu(out)
+    assert got.shape == cp.shape and np.array_equal(got, cp)
+    return n
+
+
+def check_theta(gj, ctx, R, S, op, eps=0, materialize=True):
+    tR, tS = dev(R), dev(S)
+    n = gj.theta_join_count(ctx, tR, tS, op, eps)
+    assert n == oracle.theta_count_sorted(R, S, op, eps), (op, eps)
+    if materialize:
+        out = gj.theta_join_materialize(ctx, tR, tS, op, eps, n)
+        cn, cp = oracle.nlj(R, S, op, eps)
+        assert cn == n
+        assert np.array_equal(canon_gpu(out), cp), (op, eps)
+    return n
+
+
+# ------------------------------------------------------------------ generator twin
+
+def test_device_generator_matches_numpy(gj):
+    import gen.device as gd
+    import native_build
+    native_build.build_gen()
+    n = 100_003
+    for D in (10_000, 1 << 30, 2**32):
+        assert np.array_equal(gd.uniform(n, D, 7, 1, offset=5).cpu().numpy(),
+                              gen.uniform(n, D, 7, 1, offset=5).astype(np.int32))
+    assert np.array_equal(gd.perm_range(n, 20, 3, offset=11).cpu().numpy(),
+                          gen.perm(np.arange(11, 11 + n, dtype=np.uint64), 20, 3).astype(np.int32))
+    R, S, m = gen.pkfk(18, n, seed=9)
+    assert np.array_equal(gd.pkfk_S(n, 18, 9).cpu().numpy(), S)
+    q = gen.zipf_table(1 << 16)
+    Rz, Sz, mz = gen.zipf_pkfk(16, n, q, seed=4)
+    assert np.array_equal(gd.zipf_S(n, 16, gd.zipf_table_device(1 << 16), 4).cpu().numpy(), Sz)
+    R5, S5, m5 = gen.c5(1 << 10, n, seed=8)
+    assert np.array_equal(gd.c5_S(n, 8).cpu().numpy(), S5)
+    assert np.array_equal(gd.perm_range(1 << 10, 31, 8, mult=2, dtype=torch.int64).cpu().numpy(), R5)
+
+
+# ------------------------------------------------------------------ golden fixtures on the GPU
+
+@pytest.mark.parametrize("name", ["e1_small_mixed.json", "e2_int32_extremes.json", "e3_int64_extremes.json"])
+def test_golden_on_gpu(gj, ctx, name):
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", name)))
+    dt = np.int32 if g["dtype"] == "int32" else np.int64
+    R, S = np.array(g["R"], dtype=dt), np.array(g["S"], dtype=dt)
+    tR, tS = dev(R), dev(S)
+    for c in g["cases"]:
+        n = gj.theta_join_count(ctx, tR, tS, c["op"], c["eps"])
+        assert n == c["count"], c
+        out = canon_gpu(gj.theta_join_materialize(ctx, tR, tS, c["op"], c["eps"], n))
+        if "pairs" in c:
+            assert out.tolist() == c["pairs"], c
+        if c["op"] == "eq":
+            assert gj.join_count(ctx, tR, tS) == c["count"]
+            out = canon_gpu(gj.join_materialize(ctx, tR, tS))
+            if "pairs" in c:
+                assert out.tolist() == c["pairs"]
+
+
+# ------------------------------------------------------------------ equi hash join
+
+def test_equi_c1_full(gj, ctx):
+    """configs[0]: R=S=10^4 uniform keys in [0,10^4), default planner."""
+    R, S = gen.c1()
+    check_equi(gj, ctx, R, S)
+
+
+@pytest.mark.parametrize("bits,chunk,pchunk", [(0, 4096, 16384), (0, 64, 100), (3, 4096, 16384), (9, 256, 64),
+                                               (10, 4096, 16384), (12, 32, 1000), (19, 4096, 16384)])
+def test_equi_planner_variants(gj, ctx, bits, chunk, pchunk):
+    """1, 2 and 3 radix passes; build chunks split into many units; ragged tails."""
+    ctx.set_option("part_bits", bits)
+    ctx.set_option("build_chunk", chunk)
+    ctx.set_option("probe_chunk", pchunk)
+    R = gen.uniform_keys(20_011, 5_000, 1, 0)
+    S = gen.uniform_keys(30_007, 5_000, 1, 1)
+    check_equi(gj, ctx, R, S)
+
+
+@pytest.mark.parametrize("side", [1, 2])
+def test_equi_build_side(gj, ctx, side):
+    ctx.set_option("build_side", side)
+    R = gen.uniform_keys(7_000, 3_000, 2, 0)
+    S = gen.uniform_keys(11_000, 3_000, 2, 1)
+    check_equi(gj, ctx, R, S)
+
+
+def test_equi_all_equal_keys(gj, ctx):
+    """Degenerate build-side duplication: |J| = nR * nS, build chunks overflow one table."""
+    R = np.full(3000, 42, np.int32)
+    S = np.full(2500, 42, np.int32)
+    assert check_equi(gj, ctx, R, S) == 3000 * 2500
+
+
+def test_equi_int64_extremes(gj, ctx):
+    rng = np.random.default_rng(5)
+    pool = np.array([np.iinfo(np.int64).min, -1, 0, 1, np.iinfo(np.int64).max, 2**40, -2**40], np.int64)
+    R = np.concatenate([rng.choice(pool, 500), rng.integers(-1000, 1000, 5000)]).astype(np.int64)
+    S = np.concatenate([rng.choice(pool, 700), rng.integers(-1000, 1000, 6000)]).astype(np.int64)
+    check_equi(gj, ctx, R, S)
+
+
+def test_equi_empty_and_tiny(gj, ctx):
+    e = np.zeros(0, np.int32)
+    one = np.array([5], np.int32)
+    assert gj.join_count(ctx, dev(e), dev(one)) == 0
+    assert gj.join_count(ctx, dev(one), dev(e)) == 0
+    assert gj.join_materialize(ctx, dev(e), dev(one)).shape[0] == 0
+    check_equi(gj, ctx, one, np.array([5, 5, 6], np.int32))
+
+
+def test_equi_rid_map_and_base(gj, ctx):
+    R = gen.uniform_keys(5000, 900, 3, 0)
+    S = gen.uniform_keys(6000, 900, 3, 1)
+    rid = np.arange(5000, dtype=np.int32)[::-1].copy() + 100
+    tR = gj.Rel(dev(R), dev(rid))
+    tS = gj.Rel(dev(S), None, 7_000_000)
+    n = gj.join_count(ctx, tR, tS)
+    got = canon_gpu(gj.join_materialize(ctx, tR, tS, n))
+    cn, cp = oracle.hash_equi(R, S, rid_base_S=7_000_000)
+    cp[:, 0] = rid[cp[:, 0]]
+    cp = cp[np.lexsort((cp[:, 1], cp[:, 0]))]
+    assert n == cn and np.array_equal(got, cp)
+
+
+def test_equi_pkfk_c2_full_size(gj, ctx):
+    """configs[1] at full size 2^27 x 2^27: every pair vs the closed form O8 (pinned to O2)."""
+    R, S, m = gen.pkfk(27, 1 << 27)
+    tR, tS = dev(R), dev(S)
+    del R, S
+    n = gj.join_count(ctx, tR, tS)
+    assert n == 1 << 27
+    out = gj.join_materialize(ctx, tR, tS, n)
+    cn, cp = oracle.pkfk_closed_form(m)
+    assert np.array_equal(canon_gpu(out), cp)
+
+
+def test_equi_zipf_skew(gj, ctx):
+    """configs[2] shape (scaled): R unique over 2^20 ranks, S Zipf(1) FK, 2^22 rows."""
+    q = gen.zipf_table(1 << 20)
+    R, S, m = gen.zipf_pkfk(20, 1 << 22, q, seed=77)
+    n = gj.join_count(ctx, dev(R), dev(S))
+    assert n == 1 << 22
+    cn, cp = oracle.pkfk_closed_form(m)
+    assert np.array_equal(canon_gpu(gj.join_materialize(ctx, dev(R), dev(S), n)), cp)
+
+
+def test_equi_deterministic_positions(gj, ctx):
+    R, S, _ = gen.pkfk(16, 200_000, seed=3)
+    tR, tS = dev(R), dev(S)
+    a = gj.join_materialize(ctx, tR, tS).clone()
+    b = gj.join_materialize(ctx, tR, tS).clone()
+    ctx2 = gj.Context(0)
+    c = gj.join_materialize(ctx2, tR, tS)
+    assert torch.equal(a, b) and torch.equal(a, c)
+
+
+# ------------------------------------------------------------------ theta / NLJ
+
+@pytest.mark.parametrize("op", OPS)
+def test_theta_ragged_all_ops(gj, ctx, op):
+    """Several R tiles + a ragged last tile; S spans several pipeline stages + tail."""
+    R = gen.uniform_keys(4099, 300, 5, 0) - 150
+    S = gen.uniform_keys(9001, 300, 5, 1) - 150
+    check_theta(gj, ctx, R.astype(np.int32), S.astype(np.int32), op, eps=7 if op == "band" else 0)
+
+
+@pytest.mark.parametrize("op", OPS)
+def test_theta_int64(gj, ctx, op):
+    rng = np.random.default_rng(11)
+    R = rng.integers(-2**40, 2**40, 2100).astype(np.int64)
+    S = np.concatenate([rng.integers(-2**40, 2**40, 3000), R[:500]]).astype(np.int64)
+    check_theta(gj, ctx, R, S, op, eps=2**38 if op == "band" else 0)
+
+
+@pytest.mark.parametrize("eps", [0, 1, 5, 2**31 - 1, 2**31, 2**32 - 1, 2**40])
+def test_band_fast_and_exact_paths(gj, ctx, eps):
+    """Full-range int32 keys: the 32-bit band trick is invalid here, the exact path must run."""
+    rng = np.random.default_rng(eps % 1000)
+    R = rng.integers(-2**31, 2**31, 2500, dtype=np.int64).astype(np.int32)
+    S = rng.integers(-2**31, 2**31, 3000, dtype=np.int64).astype(np.int32)
+    S[:100] = R[:100] + 1
+    check_theta(gj, ctx, R, S, "band", eps)
+
+
+def test_band_forced_slow_equals_fast(gj, ctx):
+    R = gen.uniform_keys(5000, 1 << 20, 2, 0)
+    S = gen.uniform_keys(7000, 1 << 20, 2, 1)
+    a = check_theta(gj, ctx, R, S, "band", 300)
+    ctx.set_option("force_slow_band", 1)
+    assert check_theta(gj, ctx, R, S, "band", 300) == a
+
+
+def test_theta_c1_lt_full(gj, ctx):
+    """configs[0] theta R.a < S.b: count and all ~5e7 pairs."""
+    R, S = gen.c1()
+    check_theta(gj, ctx, R, S, "lt", 0, materialize=True)
+    check_theta(gj, ctx, R, S, "eq", 0, materialize=True)
+
+
+def test_theta_nlj_split_variants(gj, ctx):
+    R = gen.uniform_keys(6000, 1000, 9, 0)
+    S = gen.uniform_keys(50_000, 1000, 9, 1)
+    for split in (1, 3, 25):
+        ctx.set_option("nlj_split", split)
+        check_theta(gj, ctx, R, S, "ge", 0, materialize=False)
+        check_theta(gj, ctx, R, S, "band", 2, materialize=True)
+
+
+def test_theta_unaligned_s(gj, ctx):
+    R = gen.uniform_keys(3000, 500, 4, 0)
+    S = gen.uniform_keys(5001, 500, 4, 1)
+    tR, tS = dev(R), dev(S)
+    tS1 = tS[1:]  # 4-byte offset: not 16-byte aligned
+    n = gj.theta_join_count(ctx, tR, tS1, "le")
+    assert n == oracle.theta_count_sorted(R, S[1:], "le")
+    got = canon_gpu(gj.theta_join_materialize(ctx, tR, tS1, "le", 0, n))
+    assert np.array_equal(got, oracle.nlj(R, S[1:], "le")[1])
+
+
+def test_theta_c4_full_size_count_and_sampled_pairs(gj, ctx):
+    """configs[3]: band join 2^20 x 2^24, eps=53687: exact count vs O3; pairs of 48
+    sampled R rows vs O4 on (R_sample x S)."""
+    R, S = gen.c4()
+    tR, tS = dev(R), dev(S)
+    eps = gen.C4_EPS
+    n = gj.theta_join_count(ctx, tR, tS, "band", eps)
+    assert n == oracle.theta_count_sorted(R, S, "band", eps)
+    out = gj.theta_join_materialize(ctx, tR, tS, "band", eps, n)
+    rows = np.random.default_rng(1).choice(len(R), 48, replace=False)
+    sel = torch.isin(out[:, 0], dev(rows.astype(np.int32)))
+    got = canon_gpu(out[sel])
+    ref = []
+    for r in sorted(rows):
+        c, p = oracle.band_materialize(R[r:r + 1], S, eps, rid_base_R=int(r))
+        ref.append(p)
+    ref = np.concatenate(ref)
+    assert np.array_equal(got, ref)
+
+
+# ------------------------------------------------------------------ pre-filter
+
+@pytest.mark.parametrize("flags", [1, 2, 3, 7])
+def test_prefilter_no_false_negatives(gj, ctx, flags):
+    """J(prefilter(R), prefilter(S)) == J(R, S); exact semi-join survivors are kept."""
+    rng = np.random.default_rng(flags)
+    R = rng.integers(0, 200_000, 60_000).astype(np.int32)
+    S = rng.integers(100_000, 400_000, 80_000).astype(np.int32)
+    kR, rR, kS, rS = gj.prefilter(ctx, dev(R), dev(S), flags=flags)
+    kR, rR, kS, rS = (t.cpu().numpy() for t in (kR, rR, kS, rS))
+    assert np.array_equal(kR, R[rR]) and np.array_equal(kS, S[rS])
+    assert np.all(np.diff(rR) > 0) and np.all(np.diff(rS) > 0)  # stable, original order
+    keepR = set(np.nonzero(oracle.semijoin_exact(R, S))[0])
+    keepS = set(np.nonzero(oracle.semijoin_exact(S, R))[0])
+    assert keepR <= set(rR.tolist()) and keepS <= set(rS.tolist())
+    c, p = oracle.hash_equi(kR, kS)
+    p = np.stack([rR[p[:, 0]], rS[p[:, 1]]], 1).astype(np.uint32)
+    p = p[np.lexsort((p[:, 1], p[:, 0]))]
+    assert np.array_equal(p, oracle.hash_equi(R, S)[1])
+    if flags & 2:
+        # Bloom at 8 bits/key: S keeps the exact survivors plus a few false positives
+        assert len(rS) <= len(keepS) + 0.08 * (len(S) - len(keepS))
+
+
+def test_prefilter_band_range(gj, ctx):
+    R = gen.uniform_keys(20_000, 1 << 20, 6, 0)
+    S = (gen.uniform_keys(20_000, 1 << 20, 6, 1) + (1 << 19)).astype(np.int32)
+    kR, rR, kS, rS = gj.prefilter(ctx, dev(R), dev(S), flags=1, op="band", eps=1000)
+    rR, rS = rR.cpu().numpy(), rS.cpu().numpy()
+    assert set(np.nonzero(oracle.semijoin_band(R, S, 1000))[0]) <= set(rR.tolist())
+    assert set(np.nonzero(oracle.semijoin_band(S, R, 1000))[0]) <= set(rS.tolist())
+
+
+# ------------------------------------------------------------------ errors and host entry
+
+def test_errors(gj, ctx):
+    R, S = dev(gen.uniform_keys(100, 10, 1, 0)), dev(gen.uniform_keys(100, 10, 1, 1))
+    n = gj.join_count(ctx, R, S)
+    small = torch.empty((max(n - 1, 1), 2), dtype=torch.int32, device="cuda")
+    with pytest.raises(gj.GJError) as e:
+        gj.join_materialize(ctx, R, S, out=small)
+    assert e.value.status == 3
+    with pytest.raises(gj.GJError) as e:
+        gj.join_count(ctx, R, S.to(torch.int64))
+    assert e.value.status == 1
+    with pytest.raises(gj.GJError):
+        gj.prefilter(ctx, R, S, op="lt")
+
+
+def test_join_host_e2e(gj, ctx):
+    R, S, m = gen.pkfk(16, 300_000, seed=21)
+    hR = torch.from_numpy(R).pin_memory()
+    hS = torch.from_numpy(S).pin_memory()
+    out = torch.empty((300_000, 2), dtype=torch.int32).pin_memory()
+    n = gj.join_host(ctx, hR, hS, out)
+    assert n == 300_000
+    p = out.numpy().view(np.uint32)
+    p = p[np.lexsort((p[:, 1], p[:, 0]))]
+    assert np.array_equal(p, oracle.pkfk_closed_form(m)[1])
+
+
+def test_launch_accounting_and_profile(gj):
+    c = gj.Context(0, profile=1)
+    R, S = dev(gen.uniform_keys(50_000, 10_000, 1, 0)), dev(gen.uniform_keys(50_000, 10_000, 1, 1))
+    c.reset_stats()
+    gj.join_materialize(c, R, S)
+    t = c.kernel_times()
+    assert "hj_count" in t and "hj_write" in t and "part_scatter" in t
+    assert c.launches() == sum(v[1] for v in t.values())
+    c.close()

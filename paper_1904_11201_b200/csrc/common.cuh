@@ -26,8 +26,9 @@ template <> struct KeyT<int64_t> {
 };
 
 // Multiplicative hash (Fibonacci hashing): the high 32 bits of key * 2^64/phi.
-// Partition = top B bits; in-partition hash-table slot = the next bits below.
-// Raw low key bits are NOT used: configs[4]'s R keys are all even.
+// Partition = top B bits (the multi-GPU shuffle takes the top log2(G) bits first);
+// the in-partition hash-table slot uses an independent hash.  Raw low key bits are
+// NOT used: configs[4]'s R keys are all even.
 __device__ __forceinline__ uint32_t khash(int32_t k) {
   return (uint32_t)(((uint64_t)(uint32_t)k * 0x9E3779B97F4A7C15ull) >> 32);
 }

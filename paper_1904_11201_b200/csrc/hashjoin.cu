@@ -4,13 +4,16 @@
 // Paper: §3.3.2 GPU-Based Hash Join -- "put the smaller table
 // (inner table) into a hash table ... traverse the larger table",
 // hash buckets with a small-range probe.  B200 design (DESIGN.md
-// §4.3): after radix partitioning both relations with the same hash bits, every
+// §4.2): after radix partitioning both relations with the same hash bits, every
 // work unit u = (partition p, build chunk, probe chunk) builds an open-addressing
-// (linear probing) table of <= 4096 build tuples in shared memory, sized 2x the
+// (linear probing) table of <= 2048 build tuples in shared memory, sized 2x the
 // chunk from the exact partition histogram -- so it can never overflow (the paper's
 // fixed-size buckets could) -- and streams the probe chunk past it.
-// Units are handed out by an atomic work counter, so Zipf-skewed partitions
-// (configs[2]) split into many units instead of serialising one CTA.
+// Units have bounded cost (<= 2048 x 2048 tuples), so Zipf-skewed partitions
+// (configs[2]) split into many units instead of serialising one CTA.  CTAs take
+// units round-robin (u = blockIdx.x + k * gridDim.x) from a precomputed descriptor
+// array, and software-pipeline them: the next unit's build and probe keys are
+// loaded into registers while the current unit is built and probed.
 //
 // Exact result sizing (replacing the paper's NB_T*NB_S slots):
 // the count kernel stores one count per (unit, warp); an exclusive scan turns them
@@ -24,10 +27,13 @@
 namespace gj {
 namespace {
 
-constexpr int HT = 512;         // threads per CTA
-constexpr int HW = HT / 32;     // warps per CTA (counts are kept per (unit, warp))
-constexpr int BCH_MAX = 4096;   // max build tuples per unit
+constexpr int HT = 256;            // threads per CTA
+constexpr int HW = HT / 32;        // warps per CTA (counts are kept per (unit, warp))
+constexpr int BCH_MAX = 2048;      // max build tuples per unit
+constexpr int PCH_MAX = 2048;      // max probe tuples per unit
 constexpr int TAB_MAX = 2 * BCH_MAX;
+constexpr int BPT = BCH_MAX / HT;  // build tuples per thread
+constexpr int PPT = PCH_MAX / HT;  // probe tuples per lane (warp w owns rows [w*pn/HW, ...))
 
 // Independent second hash for the in-partition table slot (the partition id
 // already consumed the top bits of khash).
@@ -47,94 +53,249 @@ struct HJArgs {
   const void* pkey;
   const uint32_t* prid;
   uint32_t prid_base;
-  const uint32_t* boff;
-  const uint32_t* poff;
-  const uint32_t* unit_off;
-  uint32_t P, U, bchunk, pchunk;
-  uint32_t* work;
+  const uint4* desc;  // per unit: (build begin, build n, probe begin, probe n)
+  uint32_t U;
   uint32_t* wcnt;
   const uint64_t* woff;
   uint2* out;
   int swap;
 };
 
-template <typename K, bool WRITE>
-__global__ void __launch_bounds__(HT) hj_kernel(HJArgs a) {
+// Shared-memory table.  int32 keys: one 64-bit slot = (index+1) << 32 | key, so a
+// probe step is a single LDS.64; 0 = empty.  int64 keys: slot = index+1 and the
+// key is compared in the staged key array.
+template <typename K> struct Table;
+template <> struct Table<int32_t> {
+  unsigned long long* slot;
+  static constexpr size_t kBytes = TAB_MAX * 8;
+  __device__ void init(uint8_t* base) { slot = reinterpret_cast<unsigned long long*>(base); }
+  __device__ void clear(uint32_t T) {
+    for (uint32_t i = threadIdx.x; i < T; i += HT) slot[i] = 0ull;
+  }
+  __device__ void stage(uint32_t, int32_t) {}
+  __device__ void insert(uint32_t s, uint32_t tmask, int32_t k, uint32_t i) {
+    const unsigned long long v = ((unsigned long long)(i + 1) << 32) | (uint32_t)k;
+    while (atomicCAS(&slot[s], 0ull, v) != 0ull) s = (s + 1) & tmask;
+  }
+  // calls f(index) for every build tuple with key == k
+  template <typename F>
+  __device__ void probe(uint32_t s, uint32_t tmask, int32_t k, F f) const {
+    for (unsigned long long v; (v = slot[s]) != 0ull; s = (s + 1) & tmask)
+      if ((uint32_t)v == (uint32_t)k) f((uint32_t)(v >> 32) - 1);
+  }
+};
+template <> struct Table<int64_t> {
+  uint32_t* slot;
+  int64_t* bk;
+  static constexpr size_t kBytes = TAB_MAX * 4 + BCH_MAX * 8;
+  __device__ void init(uint8_t* base) {
+    slot = reinterpret_cast<uint32_t*>(base);
+    bk = reinterpret_cast<int64_t*>(slot + TAB_MAX);
+  }
+  __device__ void clear(uint32_t T) {
+    for (uint32_t i = threadIdx.x; i < T; i += HT) slot[i] = 0u;
+  }
+  __device__ void stage(uint32_t i, int64_t k) { bk[i] = k; }
+  __device__ void insert(uint32_t s, uint32_t tmask, int64_t, uint32_t i) {
+    while (atomicCAS(&slot[s], 0u, i + 1) != 0u) s = (s + 1) & tmask;
+  }
+  template <typename F>
+  __device__ void probe(uint32_t s, uint32_t tmask, int64_t k, F f) const {
+    for (uint32_t v; (v = slot[s]) != 0u; s = (s + 1) & tmask)
+      if (bk[v - 1] == k) f(v - 1);
+  }
+};
+
+// One unit's keys, held in registers (the software-pipelined prefetch buffer).
+template <typename K>
+struct UnitKeys {
+  K kb[BPT];
+  K kp[PPT];
+};
+
+__device__ __forceinline__ void probe_range(uint32_t pn, uint32_t w, uint32_t& wb, uint32_t& we) {
+  const uint32_t per_w = (pn + HW - 1) / HW;
+  wb = min(w * per_w, pn);
+  we = min(wb + per_w, pn);
+}
+
+template <typename K>
+__device__ __forceinline__ void load_keys(UnitKeys<K>& R, const uint4 d, const HJArgs& a, uint32_t tid, uint32_t w,
+                                          uint32_t lane) {
+  const K* __restrict__ bkey = static_cast<const K*>(a.bkey);
+  const K* __restrict__ pkey = static_cast<const K*>(a.pkey);
+#pragma unroll
+  for (int j = 0; j < BPT; ++j) {
+    const uint32_t i = tid + j * HT;
+    R.kb[j] = i < d.y ? bkey[d.x + i] : K(0);
+  }
+  uint32_t wb, we;
+  probe_range(d.w, w, wb, we);
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) {
+    const uint32_t i = wb + lane + 32 * j;
+    R.kp[j] = i < we ? pkey[d.z + i] : K(0);
+  }
+}
+
+__device__ __forceinline__ uint32_t table_logT(uint32_t bn) {
+  return max(32 - __clz(2 * bn - 1), 5u);  // ceil(log2(2*bn)), >= 32 slots
+}
+
+// Count pass.  Per probe row it also records the matching build index inside the
+// unit's build chunk (uint16; NO_MATCH / MULTI sentinels), so the write pass can
+// emit pairs without rebuilding the table (units holding a MULTI row are flagged
+// and re-probed by the write pass).
+constexpr uint16_t NO_MATCH = 0xFFFF, MULTI = 0xFFFE;
+
+template <typename K>
+__global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __restrict__ stage,
+                                                      uint8_t* __restrict__ multi) {
   extern __shared__ __align__(16) uint8_t smem[];
-  uint32_t* tab = reinterpret_cast<uint32_t*>(smem);          // TAB_MAX
-  K* bk = reinterpret_cast<K*>(tab + TAB_MAX);                 // BCH_MAX
-  uint32_t* br = reinterpret_cast<uint32_t*>(bk + BCH_MAX);    // BCH_MAX (WRITE)
-  __shared__ uint32_t s_u;
+  Table<K> tab;
+  tab.init(smem);
+  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
+  const uint32_t G = gridDim.x;
+  uint32_t u = blockIdx.x;
+  if (u >= a.U) return;
+  const uint4 zero = make_uint4(0, 0, 0, 0);
+  uint4 d = a.desc[u];
+  uint4 dn = u + G < a.U ? a.desc[u + G] : zero;
+  UnitKeys<K> cur;
+  load_keys(cur, d, a, tid, w, lane);
+
+  for (; u < a.U; u += G) {
+    UnitKeys<K> nxt;  // prefetch the next unit while this one is built and probed
+    load_keys(nxt, dn, a, tid, w, lane);
+    const uint4 dnn = u + 2 * G < a.U ? a.desc[u + 2 * G] : zero;
+    const uint32_t bn = d.y, pn = d.w;
+    const uint32_t logT = table_logT(bn);
+    const uint32_t T = 1u << logT, tmask = T - 1, tshift = 32 - logT;
+
+    tab.clear(T);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < BPT; ++j) {
+      const uint32_t i = tid + j * HT;
+      if (i < bn) {
+        tab.stage(i, cur.kb[j]);
+        tab.insert(slot_hash(cur.kb[j]) >> tshift, tmask, cur.kb[j], i);
+      }
+    }
+    __syncthreads();
+
+    uint32_t wb, we;
+    probe_range(pn, w, wb, we);
+    uint32_t c = 0;
+    bool many = false;
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const uint32_t i = wb + lane + 32 * j;
+      if (i < we) {
+        const K k = cur.kp[j];
+        uint32_t m = 0, f = 0;
+        tab.probe(slot_hash(k) >> tshift, tmask, k, [&](uint32_t idx) {
+          f = idx;
+          ++m;
+        });
+        c += m;
+        many |= m > 1;
+        stage[d.z + i] = m == 0 ? NO_MATCH : (m == 1 ? (uint16_t)f : MULTI);
+      }
+    }
+    c = warp_sum(c);
+    if (lane == 0) a.wcnt[(uint64_t)u * HW + w] = c;
+    if (__any_sync(FULL, many) && lane == 0) multi[u] = 1;
+    __syncthreads();
+    cur = nxt;
+    d = dn;
+    dn = dnn;
+  }
+}
+
+// Write pass.  Normal units: stage the build rids in shared memory, then every warp
+// walks its probe rows in order, ranks the rows with a match by a shuffle scan and
+// writes (rid_R, rid_S) at its scanned offset -- a gather, no hashing.  Units with
+// a MULTI row rebuild the table and re-probe (bag semantics with duplicate keys).
+template <typename K>
+__global__ void __launch_bounds__(HT) hj_write_kernel(HJArgs a, const uint16_t* __restrict__ stage,
+                                                      const uint8_t* __restrict__ multi) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  Table<K> tab;
+  tab.init(smem);
+  uint32_t* br = reinterpret_cast<uint32_t*>(smem + Table<K>::kBytes);  // BCH_MAX
   const K* __restrict__ bkey = static_cast<const K*>(a.bkey);
   const K* __restrict__ pkey = static_cast<const K*>(a.pkey);
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
 
-  for (;;) {
-    if (tid == 0) s_u = atomicAdd(a.work, 1u);
-    __syncthreads();
-    const uint32_t u = s_u;
-    if (u >= a.U) break;
-    const uint32_t p = upper_index(a.unit_off, a.P, u);
-    const uint32_t uu = u - a.unit_off[p];
-    const uint32_t b0 = a.boff[p], nb = a.boff[p + 1] - b0;
-    const uint32_t p0 = a.poff[p], np = a.poff[p + 1] - p0;
-    const uint32_t nbc = (nb + a.bchunk - 1) / a.bchunk;
-    const uint32_t bci = uu % nbc, pci = uu / nbc;
-    const uint32_t bbeg = b0 + bci * a.bchunk, bn = min(a.bchunk, nb - bci * a.bchunk);
-    const uint32_t pbeg = p0 + pci * a.pchunk, pn = min(a.pchunk, np - pci * a.pchunk);
-    uint32_t logT = 32 - __clz(2 * bn - 1);  // ceil(log2(2*bn))
-    logT = max(logT, 6u);
+  for (uint32_t u = blockIdx.x; u < a.U; u += gridDim.x) {
+    const uint4 d = a.desc[u];
+    const uint32_t bn = d.y, pn = d.w;
+    const bool full = multi[u] != 0;
+    uint32_t wb, we;
+    probe_range(pn, w, wb, we);
+    // probe-side inputs of this warp's rows, all loads in flight at once
+    uint32_t prow[PPT];
+    uint16_t sidx[PPT];
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const uint32_t i = wb + lane + 32 * j;
+      prow[j] = i < we ? (a.prid ? a.prid[d.z + i] : a.prid_base + d.z + i) : 0u;
+      sidx[j] = i < we ? stage[d.z + i] : NO_MATCH;
+    }
+    const uint32_t logT = table_logT(bn);
     const uint32_t T = 1u << logT, tmask = T - 1, tshift = 32 - logT;
-
-    // ---- build: stage the chunk, insert index+1 by CAS (linear probing)
-    for (uint32_t i = tid; i < T; i += HT) tab[i] = 0;
-    for (uint32_t i = tid; i < bn; i += HT) {
-      bk[i] = bkey[bbeg + i];
-      if (WRITE) br[i] = a.brid ? a.brid[bbeg + i] : a.brid_base + bbeg + i;
+    if (full) tab.clear(T);
+#pragma unroll
+    for (int j = 0; j < BPT; ++j) {
+      const uint32_t i = tid + j * HT;
+      if (i < bn) br[i] = a.brid ? a.brid[d.x + i] : a.brid_base + d.x + i;
     }
     __syncthreads();
-    for (uint32_t i = tid; i < bn; i += HT) {
-      uint32_t s = slot_hash(bk[i]) >> tshift;
-      while (atomicCAS(&tab[s], 0u, i + 1) != 0u) s = (s + 1) & tmask;
-    }
-    __syncthreads();
-
-    // ---- probe: warp w owns probe rows [wb, we) of the chunk, in order
-    const uint32_t per_w = (pn + HW - 1) / HW;
-    const uint32_t wb = min(w * per_w, pn), we = min(wb + per_w, pn);
-    if (!WRITE) {
-      uint32_t c = 0;
-      for (uint32_t i = wb + lane; i < we; i += 32) {
-        const K k = pkey[pbeg + i];
-        uint32_t s = slot_hash(k) >> tshift;
-        for (uint32_t v; (v = tab[s]) != 0u; s = (s + 1) & tmask) c += (bk[v - 1] == k);
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < BPT; ++j) {
+        const uint32_t i = tid + j * HT;
+        if (i < bn) {
+          const K kb = bkey[d.x + i];
+          tab.stage(i, kb);
+          tab.insert(slot_hash(kb) >> tshift, tmask, kb, i);
+        }
       }
-      c = warp_sum(c);
-      if (lane == 0) a.wcnt[(uint64_t)u * HW + w] = c;
-    } else {
-      uint64_t base = a.woff[(uint64_t)u * HW + w];
-      for (uint32_t i0 = wb; i0 < we; i0 += 32) {
-        const uint32_t i = i0 + lane;
-        K k = K(0);
-        uint32_t m = 0, s0 = 0, prow = 0;
-        if (i < we) {
-          k = pkey[pbeg + i];
-          prow = a.prid ? a.prid[pbeg + i] : a.prid_base + pbeg + i;
+      __syncthreads();
+    }
+    uint64_t base = a.woff[(uint64_t)u * HW + w];
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      if (wb + 32 * j >= we) break;  // warp-uniform
+      const uint32_t i = wb + lane + 32 * j;
+      const bool valid = i < we;
+      uint32_t m = 0;
+      K k = K(0);
+      uint32_t s0 = 0;
+      if (full) {
+        if (valid) {
+          k = pkey[d.z + i];
           s0 = slot_hash(k) >> tshift;
-          for (uint32_t s = s0, v; (v = tab[s]) != 0u; s = (s + 1) & tmask) m += (bk[v - 1] == k);
+          tab.probe(s0, tmask, k, [&](uint32_t) { ++m; });
         }
-        const uint32_t incl = warp_incl_scan(m);
-        uint64_t pos = base + (incl - m);
-        if (m) {
-          for (uint32_t s = s0, v; (v = tab[s]) != 0u; s = (s + 1) & tmask) {
-            if (bk[v - 1] == k) {
-              const uint32_t brow = br[v - 1];
-              a.out[pos++] = a.swap ? make_uint2(prow, brow) : make_uint2(brow, prow);
-            }
-          }
-        }
-        base += __shfl_sync(FULL, incl, 31);
+      } else {
+        m = sidx[j] != NO_MATCH ? 1u : 0u;
       }
+      const uint32_t incl = warp_incl_scan(m);
+      uint64_t pos = base + (incl - m);
+      if (m) {
+        if (full) {
+          tab.probe(s0, tmask, k, [&](uint32_t idx) {
+            const uint32_t brow = br[idx];
+            a.out[pos++] = a.swap ? make_uint2(prow[j], brow) : make_uint2(brow, prow[j]);
+          });
+        } else {
+          const uint32_t brow = br[sidx[j]];
+          a.out[pos] = a.swap ? make_uint2(prow[j], brow) : make_uint2(brow, prow[j]);
+        }
+      }
+      base += __shfl_sync(FULL, incl, 31);
     }
     __syncthreads();
   }
@@ -146,6 +307,39 @@ __global__ void hj_units(const uint32_t* __restrict__ boff, const uint32_t* __re
   if (p >= P) return;
   uint32_t nb = boff[p + 1] - boff[p], np = poff[p + 1] - poff[p];
   nunits[p] = (nb && np) ? ((nb + bchunk - 1) / bchunk) * ((np + pchunk - 1) / pchunk) : 0u;
+}
+
+// unit descriptors (build begin, build n, probe begin, probe n): one binary search
+// per unit, fully parallel.  Also initialises multi[u]: units of a partition with
+// several build chunks share probe rows, so their per-row staging is ambiguous and
+// the write pass re-probes them.
+__global__ void hj_unit_desc(const uint32_t* __restrict__ unit_off, const uint32_t* __restrict__ boff,
+                             const uint32_t* __restrict__ poff, uint32_t P, uint32_t U, uint32_t bchunk,
+                             uint32_t pchunk, uint4* __restrict__ desc, uint8_t* __restrict__ multi) {
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
+    const uint32_t p = upper_index(unit_off, P, u);
+    const uint32_t uu = u - unit_off[p];
+    const uint32_t b0 = boff[p], nb = boff[p + 1] - b0;
+    const uint32_t p0 = poff[p], np = poff[p + 1] - p0;
+    const uint32_t nbc = (nb + bchunk - 1) / bchunk;
+    const uint32_t bci = uu % nbc, pci = uu / nbc;
+    desc[u] = make_uint4(b0 + bci * bchunk, min(bchunk, nb - bci * bchunk), p0 + pci * pchunk,
+                         min(pchunk, np - pci * pchunk));
+    multi[u] = nbc > 1 ? 1 : 0;
+  }
+}
+
+template <typename K, bool WRITE>
+size_t hj_smem() {
+  return Table<K>::kBytes + (WRITE ? BCH_MAX * 4 : 0);
+}
+
+template <typename Kern>
+uint32_t hj_grid(gj_ctx* ctx, Kern k, size_t smem, uint32_t U) {
+  static_assert(sizeof(Kern) > 0, "");
+  int occ = 0;
+  GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, HT, smem));
+  return std::min<uint32_t>(U, (uint32_t)ctx->num_sms * std::max(occ, 1));
 }
 
 template <typename K>
@@ -166,15 +360,14 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
   jc.prid = PP.rid;
   jc.boff = PB.off;
   jc.poff = PP.off;
-  jc.bchunk = ctx->build_chunk;
-  jc.pchunk = ctx->probe_chunk;
-  // partitioned relations carry explicit rids; B == 0 keeps the caller's view
-  (void)Bld;
-  (void)Prb;
+  const uint32_t bchunk = std::min<uint32_t>(ctx->build_chunk, BCH_MAX);
+  const uint32_t pchunk = std::min<uint32_t>(ctx->probe_chunk, PCH_MAX);
+  jc.bchunk = bchunk;
+  jc.pchunk = pchunk;
 
   uint32_t* unit_off = static_cast<uint32_t*>(ws(ctx, "hj.unit_off", (P + 1) * sizeof(uint32_t)));
-  launch(ctx, "hj_units", hj_units, dim3((P + 255) / 256), dim3(256), 0, PB.off, PP.off, P, jc.bchunk,
-         jc.pchunk, unit_off);
+  launch(ctx, "hj_units", hj_units, dim3((P + 255) / 256), dim3(256), 0, PB.off, PP.off, P, bchunk, pchunk,
+         unit_off);
   exclusive_scan<uint32_t, uint32_t>(ctx, unit_off, unit_off, P, unit_off + P);
   uint32_t U = 0;
   d2h_sync(ctx, &U, unit_off + P, sizeof(uint32_t));
@@ -183,13 +376,19 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
   const uint64_t nw = (uint64_t)U * HW;
   uint32_t* wcnt = static_cast<uint32_t*>(ws(ctx, "hj.wcnt", (nw + 1) * sizeof(uint32_t)));
   uint64_t* woff = static_cast<uint64_t*>(ws(ctx, "hj.woff", (nw + 1) * sizeof(uint64_t)));
-  uint32_t* work = static_cast<uint32_t*>(ws(ctx, "hj.work", 16));
+  uint4* desc = static_cast<uint4*>(ws(ctx, "hj.desc", ((uint64_t)U + 1) * sizeof(uint4)));
   jc.woff = woff;
+  jc.desc = desc;
   if (U == 0) {
     jc.total = 0;
     return;
   }
-  GJ_CUDA(cudaMemsetAsync(work, 0, sizeof(uint32_t), ctx->stream));
+  uint16_t* stage = static_cast<uint16_t*>(ws(ctx, "hj.stage", (Prb.n + 8) * sizeof(uint16_t)));
+  uint8_t* multi = static_cast<uint8_t*>(ws(ctx, "hj.multi", (uint64_t)U + 16));
+  jc.stage = stage;
+  jc.multi = multi;
+  launch(ctx, "hj_unit_desc", hj_unit_desc, dim3(std::min<uint32_t>((U + 255) / 256, ctx->num_sms * 16)),
+         dim3(256), 0, (const uint32_t*)unit_off, PB.off, PP.off, P, U, bchunk, pchunk, desc, multi);
   HJArgs a{};
   a.bkey = PB.key;
   a.brid = PB.rid;
@@ -197,21 +396,17 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
   a.pkey = PP.key;
   a.prid = PP.rid;
   a.prid_base = Prb.rid_base;
-  a.boff = PB.off;
-  a.poff = PP.off;
-  a.unit_off = unit_off;
-  a.P = P;
+  a.desc = desc;
   a.U = U;
-  a.bchunk = jc.bchunk;
-  a.pchunk = jc.pchunk;
-  a.work = work;
   a.wcnt = wcnt;
   a.swap = swap;
-  const size_t smem = TAB_MAX * 4 + BCH_MAX * sizeof(K);
-  static bool once = (set_smem(hj_kernel<K, false>, smem), true);
-  (void)once;
-  const uint32_t grid = std::min<uint32_t>(U, (uint32_t)ctx->num_sms * 4);
-  launch(ctx, "hj_count", hj_kernel<K, false>, dim3(grid), dim3(HT), smem, a);
+  {
+    const size_t smem = hj_smem<K, false>();
+    static bool once = (set_smem(hj_count_kernel<K>, smem), true);
+    (void)once;
+    launch(ctx, "hj_count", hj_count_kernel<K>, dim3(hj_grid(ctx, hj_count_kernel<K>, smem, U)), dim3(HT), smem, a,
+           stage, multi);
+  }
   exclusive_scan<uint32_t, uint64_t>(ctx, wcnt, woff, nw, woff + nw);
   d2h_sync(ctx, &jc.total, woff + nw, sizeof(uint64_t));
 }
@@ -220,8 +415,6 @@ template <typename K>
 void write_impl(gj_ctx* ctx, uint32_t* out) {
   JoinCache& jc = ctx->jc;
   if (jc.U == 0 || jc.total == 0) return;
-  uint32_t* work = static_cast<uint32_t*>(ws(ctx, "hj.work", 16));
-  GJ_CUDA(cudaMemsetAsync(work, 0, sizeof(uint32_t), ctx->stream));
   const gj_rel& Bld = jc.swap ? jc.S : jc.R;
   const gj_rel& Prb = jc.swap ? jc.R : jc.S;
   HJArgs a{};
@@ -231,22 +424,16 @@ void write_impl(gj_ctx* ctx, uint32_t* out) {
   a.pkey = jc.pkey;
   a.prid = jc.prid;
   a.prid_base = Prb.rid_base;
-  a.boff = jc.boff;
-  a.poff = jc.poff;
-  a.unit_off = jc.unit_off;
-  a.P = jc.P;
+  a.desc = static_cast<const uint4*>(jc.desc);
   a.U = jc.U;
-  a.bchunk = jc.bchunk;
-  a.pchunk = jc.pchunk;
-  a.work = work;
   a.woff = jc.woff;
   a.out = reinterpret_cast<uint2*>(out);
   a.swap = jc.swap;
-  const size_t smem = TAB_MAX * 4 + BCH_MAX * (sizeof(K) + 4);
-  static bool once = (set_smem(hj_kernel<K, true>, smem), true);
+  const size_t smem = hj_smem<K, true>();
+  static bool once = (set_smem(hj_write_kernel<K>, smem), true);
   (void)once;
-  const uint32_t grid = std::min<uint32_t>(jc.U, (uint32_t)ctx->num_sms * 3);
-  launch(ctx, "hj_write", hj_kernel<K, true>, dim3(grid), dim3(HT), smem, a);
+  launch(ctx, "hj_write", hj_write_kernel<K>, dim3(hj_grid(ctx, hj_write_kernel<K>, smem, a.U)), dim3(HT), smem, a,
+         (const uint16_t*)jc.stage, (const uint8_t*)jc.multi);
 }
 
 }  // namespace

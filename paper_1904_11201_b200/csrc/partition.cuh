@@ -22,6 +22,8 @@ int radix_passes(uint32_t B);
 
 // Partition relation X (key type by X.key_type) into 2^B partitions.
 // tag distinguishes the workspace of the two relations ("R" / "S").
-Partitioned radix_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char* tag);
+// skip = top hash bits already consumed (log2 #ranks after a multi-GPU shuffle);
+// the partition digits are bits [32-skip-B, 32-skip) of khash.
+Partitioned radix_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char* tag, uint32_t skip = 0);
 
 }  // namespace gj

@@ -48,6 +48,9 @@ struct JoinCache {
   const uint32_t* boff = nullptr;  // P+1
   const uint32_t* poff = nullptr;  // P+1
   const uint32_t* unit_off = nullptr;  // P+1
+  const void* desc = nullptr;  // U x uint4 unit descriptors
+  const uint16_t* stage = nullptr;  // per probe row: matching build index in its unit
+  const uint8_t* multi = nullptr;   // per unit: some probe row has > 1 match
   uint32_t U = 0;                 // work units
   uint32_t bchunk = 0, pchunk = 0;
   const uint64_t* woff = nullptr;  // U*W exclusive offsets
@@ -81,8 +84,8 @@ struct gj_ctx {
   int num_sms = 148;
   // options (gjoin.h GJ_OPT_*)
   int part_bits = -1;
-  uint32_t build_chunk = 4096;
-  uint32_t probe_chunk = 16384;
+  uint32_t build_chunk = 2048;
+  uint32_t probe_chunk = 2048;
   bool profile = false;
   uint32_t nlj_split = 0;
   bool force_slow_band = false;

@@ -194,6 +194,9 @@ def run_ours(args, world, rank, local):
     w = make_workload(args.workload, dev)
     stream = torch.cuda.current_stream(dev)
     ctx = gj.Context(local, stream)
+    for o in args.opt:
+        k, v = o.split("=")
+        ctx.set_option(k, int(v))
     R, S = w["R"], w["S"]
     nR, nS = R.numel(), S.numel()
 
@@ -339,6 +342,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample-bits", type=int, default=23)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--opt", action="append", default=[], help="ctx option name=value (tuning sweeps)")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
 

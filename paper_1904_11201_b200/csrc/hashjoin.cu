@@ -65,23 +65,62 @@ struct HJArgs {
 // probe step is a single LDS.64; 0 = empty.  int64 keys: slot = index+1 and the
 // key is compared in the staged key array.
 template <typename K> struct Table;
+//
+// insert() returns true if it walked past an equal key (a duplicate build key):
+// two equal keys share a probe sequence, so whichever is inserted second meets the
+// first.  When a chunk has no duplicates, probe<true>() stops at the first match
+// (a PK build side), otherwise probe<false>() walks to the first empty slot (bag
+// semantics).
+template <typename K> struct Table;
+// int32 keys: 64-bit slot = gen:20 | index:12 | key:32.  A slot is occupied only
+// if its generation equals the current unit's, so consecutive units of a CTA need
+// no table clear (one clear per launch; the generation advances per unit).
 template <> struct Table<int32_t> {
   unsigned long long* slot;
+  unsigned long long g;  // current generation, pre-shifted to bit 44
   static constexpr size_t kBytes = TAB_MAX * 8;
-  __device__ void init(uint8_t* base) { slot = reinterpret_cast<unsigned long long*>(base); }
-  __device__ void clear(uint32_t T) {
-    for (uint32_t i = threadIdx.x; i < T; i += HT) slot[i] = 0ull;
+  static_assert(BCH_MAX <= 4096, "12-bit index");
+  __device__ void init(uint8_t* base) {
+    slot = reinterpret_cast<unsigned long long*>(base);
+    uint4* p = reinterpret_cast<uint4*>(slot);
+    for (uint32_t i = threadIdx.x; i < TAB_MAX / 2; i += HT) p[i] = make_uint4(0, 0, 0, 0);
+    g = 0;  // generation 0 is "empty"; next_unit() moves to 1 before the first use
   }
+  // a new unit: bump the generation (wraps after 2^20 units; re-clear then)
+  __device__ void clear(uint32_t) {
+    g += 1ull << 44;
+    if (g == 0) {
+      uint4* p = reinterpret_cast<uint4*>(slot);
+      for (uint32_t i = threadIdx.x; i < TAB_MAX / 2; i += HT) p[i] = make_uint4(0, 0, 0, 0);
+      g = 1ull << 44;
+    }
+  }
+  __device__ bool live(unsigned long long v) const { return (v & (0xFFFFFull << 44)) == g; }
   __device__ void stage(uint32_t, int32_t) {}
-  __device__ void insert(uint32_t s, uint32_t tmask, int32_t k, uint32_t i) {
-    const unsigned long long v = ((unsigned long long)(i + 1) << 32) | (uint32_t)k;
-    while (atomicCAS(&slot[s], 0ull, v) != 0ull) s = (s + 1) & tmask;
+  __device__ bool insert(uint32_t s, uint32_t tmask, int32_t k, uint32_t i) {
+    const unsigned long long v = g | ((unsigned long long)i << 32) | (uint32_t)k;
+    bool dup = false;
+    unsigned long long old = slot[s];
+    for (;;) {
+      if (!live(old)) {
+        const unsigned long long prev = atomicCAS(&slot[s], old, v);
+        if (prev == old) return dup;
+        old = prev;  // lost the race: re-examine the same slot
+        continue;
+      }
+      dup |= (uint32_t)old == (uint32_t)k;
+      s = (s + 1) & tmask;
+      old = slot[s];
+    }
   }
-  // calls f(index) for every build tuple with key == k
-  template <typename F>
+  // calls f(index) for every build tuple with key == k (the first one if UNIQUE)
+  template <bool UNIQUE = false, typename F>
   __device__ void probe(uint32_t s, uint32_t tmask, int32_t k, F f) const {
-    for (unsigned long long v; (v = slot[s]) != 0ull; s = (s + 1) & tmask)
-      if ((uint32_t)v == (uint32_t)k) f((uint32_t)(v >> 32) - 1);
+    for (unsigned long long v; live(v = slot[s]); s = (s + 1) & tmask)
+      if ((uint32_t)v == (uint32_t)k) {
+        f((uint32_t)(v >> 32) & 0xFFFu);
+        if (UNIQUE) break;
+      }
   }
 };
 template <> struct Table<int64_t> {
@@ -96,13 +135,19 @@ template <> struct Table<int64_t> {
     for (uint32_t i = threadIdx.x; i < T; i += HT) slot[i] = 0u;
   }
   __device__ void stage(uint32_t i, int64_t k) { bk[i] = k; }
-  __device__ void insert(uint32_t s, uint32_t tmask, int64_t, uint32_t i) {
-    while (atomicCAS(&slot[s], 0u, i + 1) != 0u) s = (s + 1) & tmask;
+  __device__ bool insert(uint32_t s, uint32_t tmask, int64_t k, uint32_t i) {
+    bool dup = false;
+    for (uint32_t old; (old = atomicCAS(&slot[s], 0u, i + 1)) != 0u; s = (s + 1) & tmask)
+      dup |= bk[old - 1] == k;
+    return dup;
   }
-  template <typename F>
+  template <bool UNIQUE = false, typename F>
   __device__ void probe(uint32_t s, uint32_t tmask, int64_t k, F f) const {
     for (uint32_t v; (v = slot[s]) != 0u; s = (s + 1) & tmask)
-      if (bk[v - 1] == k) f(v - 1);
+      if (bk[v - 1] == k) {
+        f(v - 1);
+        if (UNIQUE) break;
+      }
   }
 };
 
@@ -138,8 +183,11 @@ __device__ __forceinline__ void load_keys(UnitKeys<K>& R, const uint4 d, const H
   }
 }
 
+// Table size: ~4 slots per build tuple (load factor <= 1/4 keeps the longest probe
+// walk of a warp short), at least 2 per tuple within the TAB_MAX budget.
 __device__ __forceinline__ uint32_t table_logT(uint32_t bn) {
-  return max(32 - __clz(2 * bn - 1), 5u);  // ceil(log2(2*bn)), >= 32 slots
+  const uint32_t want = max(32 - __clz(4 * bn - 1), 5u);  // ceil(log2(4*bn)), >= 32 slots
+  return min(want, (uint32_t)(31 - __clz(TAB_MAX)));
 }
 
 // Count pass.  Per probe row it also records the matching build index inside the
@@ -152,6 +200,7 @@ template <typename K>
 __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __restrict__ stage,
                                                       uint8_t* __restrict__ multi) {
   extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_dup;
   Table<K> tab;
   tab.init(smem);
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
@@ -173,16 +222,22 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
     const uint32_t T = 1u << logT, tmask = T - 1, tshift = 32 - logT;
 
     tab.clear(T);
-    __syncthreads();
+    if (tid == 0) s_dup = 0;
 #pragma unroll
     for (int j = 0; j < BPT; ++j) {
       const uint32_t i = tid + j * HT;
-      if (i < bn) {
-        tab.stage(i, cur.kb[j]);
-        tab.insert(slot_hash(cur.kb[j]) >> tshift, tmask, cur.kb[j], i);
-      }
+      if (i < bn) tab.stage(i, cur.kb[j]);
     }
     __syncthreads();
+    bool dup = false;
+#pragma unroll
+    for (int j = 0; j < BPT; ++j) {
+      const uint32_t i = tid + j * HT;
+      if (i < bn) dup |= tab.insert(slot_hash(cur.kb[j]) >> tshift, tmask, cur.kb[j], i);
+    }
+    if (__any_sync(FULL, dup) && lane == 0) s_dup = 1;
+    __syncthreads();
+    const bool unique = s_dup == 0;  // no duplicate build key: stop each probe at its first match
 
     uint32_t wb, we;
     probe_range(pn, w, wb, we);
@@ -193,11 +248,14 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
       const uint32_t i = wb + lane + 32 * j;
       if (i < we) {
         const K k = cur.kp[j];
+        const uint32_t s0 = slot_hash(k) >> tshift;
         uint32_t m = 0, f = 0;
-        tab.probe(slot_hash(k) >> tshift, tmask, k, [&](uint32_t idx) {
+        auto hit = [&](uint32_t idx) {
           f = idx;
           ++m;
-        });
+        };
+        if (unique) tab.template probe<true>(s0, tmask, k, hit);
+        else tab.template probe<false>(s0, tmask, k, hit);
         c += m;
         many |= m > 1;
         stage[d.z + i] = m == 0 ? NO_MATCH : (m == 1 ? (uint16_t)f : MULTI);
@@ -253,14 +311,18 @@ __global__ void __launch_bounds__(HT) hj_write_kernel(HJArgs a, const uint16_t* 
     }
     __syncthreads();
     if (full) {
+      K kb[BPT];
 #pragma unroll
       for (int j = 0; j < BPT; ++j) {
         const uint32_t i = tid + j * HT;
-        if (i < bn) {
-          const K kb = bkey[d.x + i];
-          tab.stage(i, kb);
-          tab.insert(slot_hash(kb) >> tshift, tmask, kb, i);
-        }
+        kb[j] = i < bn ? bkey[d.x + i] : K(0);
+        if (i < bn) tab.stage(i, kb[j]);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < BPT; ++j) {
+        const uint32_t i = tid + j * HT;
+        if (i < bn) tab.insert(slot_hash(kb[j]) >> tshift, tmask, kb[j], i);
       }
       __syncthreads();
     }

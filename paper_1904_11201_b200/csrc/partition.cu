@@ -25,8 +25,8 @@
 namespace gj {
 namespace {
 
-constexpr int PT = 512;          // threads per CTA
-constexpr int PI = 8;            // items per thread per tile
+constexpr int PT = 256;          // threads per CTA
+constexpr int PI = 16;           // items per thread per tile
 constexpr int TILE = PT * PI;    // 4096 tuples per tile
 constexpr int TPC = 16;          // tiles per chunk
 constexpr int CHUNK = TILE * TPC;  // 65536 tuples per chunk
@@ -126,114 +126,223 @@ __global__ void __launch_bounds__(PT) part_hist(const K* __restrict__ key, uint6
   for (uint32_t d = threadIdx.x; d < D; d += PT) out[(uint64_t)d * L.nc] = h[d];
 }
 
-// Exclusive scan in place of a[0..D) (D <= 2*PT) by the whole CTA; returns nothing,
-// ends with a barrier.
+// Exclusive scan in place of a[0..D) (D <= 2^MAX_BITS) by the whole CTA; thread t
+// owns EPT consecutive elements.  Ends with a barrier.
 __device__ __forceinline__ void cta_scan_small(uint32_t* a, uint32_t D, uint32_t* wt) {
+  constexpr int EPT = ((1 << MAX_BITS) + PT - 1) / PT;
   const uint32_t t = threadIdx.x;
-  uint32_t a0 = 2 * t < D ? a[2 * t] : 0, a1 = 2 * t + 1 < D ? a[2 * t + 1] : 0;
-  uint32_t s = a0 + a1;
-  uint32_t incl = warp_incl_scan(s);
+  uint32_t v[EPT];
+  uint32_t s = 0;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const uint32_t i = t * EPT + e;
+    v[e] = i < D ? a[i] : 0u;
+    s += v[e];
+  }
+  const uint32_t incl = warp_incl_scan(s);
   if (lane_id() == 31) wt[t >> 5] = incl;
   __syncthreads();
   if (t < 32) {
-    uint32_t v = t < NW ? wt[t] : 0;
-    uint32_t vi = warp_incl_scan(v);
-    if (t < NW) wt[t] = vi - v;
+    const uint32_t x = t < NW ? wt[t] : 0;
+    const uint32_t xi = warp_incl_scan(x);
+    if (t < NW) wt[t] = xi - x;
   }
   __syncthreads();
-  uint32_t e = wt[t >> 5] + incl - s;
-  if (2 * t < D) a[2 * t] = e;
-  if (2 * t + 1 < D) a[2 * t + 1] = e + a0;
+  uint32_t run = wt[t >> 5] + incl - s;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const uint32_t i = t * EPT + e;
+    if (i < D) a[i] = run;
+    run += v[e];
+  }
   __syncthreads();
 }
 
-// Scatter one tile (see the file comment).  Per-digit offset of the tile = chunk
-// run offset (scanned chunk histogram) + the tile's in-chunk prefix row written
-// by part_hist.  Adjacent tiles run concurrently, so each digit run's partial
-// sectors are completed in L2 before eviction.  Shared memory: staged keys + rids
-// (TILE each), warp-private digit counters (NW x (D+1), +1 = dummy bin for
-// padding), per-digit tile start and "global minus local" delta (D each).
+// Tile descriptors for the scatter: (tile begin, tile length, index of the tile's
+// chunk column in the scanned histogram, chunks in its segment); length 0 = empty.
+__global__ void tile_desc_kernel(uint64_t n, const uint32_t* __restrict__ seg_off,
+                                 const uint32_t* __restrict__ chunk_base, uint32_t nseg, uint32_t D,
+                                 uint32_t ntiles, uint4* __restrict__ desc) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const uint32_t c = t / TPC, t_in = t % TPC;
+  const ChunkLoc L = locate(c, n, seg_off, chunk_base, nseg);
+  uint4 d = make_uint4(0, 0, 0, 0);
+  if (c < L.total) {
+    const uint32_t len = (uint32_t)(L.end - L.beg);
+    if (t_in * TILE < len)
+      d = make_uint4((uint32_t)L.beg + t_in * TILE, min(len - t_in * TILE, (uint32_t)TILE), L.cb * D + (c - L.cb),
+                     L.nc);
+  }
+  desc[t] = d;
+}
+
+// Scatter (see the file comment).  Persistent CTAs take tiles t = blockIdx.x +
+// k*gridDim.x, so neighbouring tiles still run concurrently on different SMs and
+// each digit run's partial sectors are completed in L2 before eviction.  The next
+// tile's keys (and rids) are streamed into a shared-memory buffer by 1-D TMA bulk
+// copies (mbarrier completion) while the current tile is ranked and written; the
+// consumed input buffer then doubles as the digit-ordered staging area.
+// Per-digit offset of a tile = chunk run offset (scanned chunk histogram) + the
+// tile's in-chunk prefix row written by part_hist.
+template <typename K, bool HAS_RID>
+struct ScatterSmem {
+  static constexpr uint32_t KPAD = 16 / sizeof(K);  // room for the 16-byte alignment shift
+  K key[2][TILE + KPAD];
+  uint32_t rid[2][TILE + 4];
+  uint32_t whist[NW << MAX_BITS];
+  uint32_t dstart[1 << MAX_BITS];
+  uint32_t delta[1 << MAX_BITS];
+  uint64_t bar[2];
+  uint32_t wt[NW];
+};
+
+template <typename K, bool HAS_RID>
+__device__ __forceinline__ void issue_tile(ScatterSmem<K, HAS_RID>& sm, uint32_t buf, const uint4 d,
+                                           const K* key_in, const uint32_t* rid_in, uint64_t n) {
+  fence_proxy_async();
+  if (d.y == 0) {
+    mbar_arrive(&sm.bar[buf]);
+    return;
+  }
+  const uint64_t kb0 = (uint64_t)d.x * sizeof(K), kb1 = (uint64_t)(d.x + d.y) * sizeof(K);
+  const uint64_t ka = kb0 & ~15ull, kz = min((kb1 + 15) & ~15ull, (n * sizeof(K)) & ~15ull);
+  uint32_t bytes = kz > ka ? (uint32_t)(kz - ka) : 0u;
+  uint64_t ra = 0, rz = 0;
+  if (HAS_RID) {
+    const uint64_t rb0 = (uint64_t)d.x * 4, rb1 = (uint64_t)(d.x + d.y) * 4;
+    ra = rb0 & ~15ull;
+    rz = min((rb1 + 15) & ~15ull, (n * 4) & ~15ull);
+    if (rz > ra) bytes += (uint32_t)(rz - ra);
+  }
+  mbar_expect_tx(&sm.bar[buf], bytes);
+  if (kz > ka) bulk_g2s(sm.key[buf], reinterpret_cast<const uint8_t*>(key_in) + ka, (uint32_t)(kz - ka), &sm.bar[buf]);
+  if (HAS_RID && rz > ra)
+    bulk_g2s(sm.rid[buf], reinterpret_cast<const uint8_t*>(rid_in) + ra, (uint32_t)(rz - ra), &sm.bar[buf]);
+}
+
 template <typename K, bool HAS_RID>
 __global__ void __launch_bounds__(PT) part_scatter(
-    const K* __restrict__ key_in, const uint32_t* __restrict__ rid_in, uint32_t rid_base,
-    uint64_t n, const uint32_t* __restrict__ seg_off, const uint32_t* __restrict__ chunk_base,
-    uint32_t nseg, uint32_t shift, uint32_t bits, const uint32_t* __restrict__ scanned,
-    const uint32_t* __restrict__ tile_pref, K* __restrict__ key_out, uint32_t* __restrict__ rid_out) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  K* skey = reinterpret_cast<K*>(smem);                                  // TILE
-  uint32_t* srid = reinterpret_cast<uint32_t*>(skey + TILE);             // TILE
-  const uint32_t D = 1u << bits, mask = D - 1, DW = D + 1;
-  uint32_t* whist = srid + TILE;                                         // NW * DW
-  uint32_t* dstart = whist + NW * DW;                                    // D
-  uint32_t* delta = dstart + D;                                          // D
-  __shared__ uint32_t wt[NW];
-
-  const uint32_t tile = blockIdx.x;
-  const uint32_t c = tile / TPC, t_in = tile % TPC;
-  const ChunkLoc L = locate(c, n, seg_off, chunk_base, nseg);
-  if (c >= L.total) return;
-  const uint32_t len = (uint32_t)(L.end - L.beg);
-  if (t_in * TILE >= len) return;  // empty tile of a short chunk
-  const uint64_t tbeg = L.beg + (uint64_t)t_in * TILE;
-  const uint32_t cnt = min(len - t_in * TILE, (uint32_t)TILE);
+    const K* __restrict__ key_in, const uint32_t* __restrict__ rid_in, uint32_t rid_base, uint64_t n,
+    const uint4* __restrict__ tdesc, uint32_t ntiles, uint32_t shift, uint32_t bits,
+    const uint32_t* __restrict__ scanned, const uint32_t* __restrict__ tile_pref, K* __restrict__ key_out,
+    uint32_t* __restrict__ rid_out) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  ScatterSmem<K, HAS_RID>& sm = *reinterpret_cast<ScatterSmem<K, HAS_RID>*>(smem_raw);
+  const uint32_t D = 1u << bits, mask = D - 1;
   const uint32_t w = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t G = gridDim.x;
+  uint32_t t = blockIdx.x;
+  if (t >= ntiles) return;
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.bar[0], 1);
+    mbar_init(&sm.bar[1], 1);
+    fence_mbar_init();
+    issue_tile(sm, 0, tdesc[t], key_in, rid_in, n);
+  }
+  __syncthreads();
+  constexpr int DPT = (1 << MAX_BITS) / PT;  // digits per thread (upper bound)
 
-  K k[PI];
-  uint32_t r[HAS_RID ? PI : 1];
-  load_tile<K, HAS_RID>(key_in, rid_in, tbeg, cnt, w, lane, k, r);
-  // global offset of this tile's digit-d run: loads issued now, consumed after ranking
-  static_assert((1 << MAX_BITS) <= PT, "one digit per thread");
-  const uint32_t dd = threadIdx.x;
-  uint32_t goff = 0;
-  if (dd < D) goff = scanned[(uint64_t)L.cb * D + (uint64_t)dd * L.nc + (c - L.cb)] + tile_pref[(uint64_t)tile * D + dd];
-  for (uint32_t d = lane; d < DW; d += 32) whist[w * DW + d] = 0;
-  __syncwarp();
-  // Rank inside the warp: every lane fetch-adds its digit's warp-private counter.
-  // Warp w's items are processed in index order, so ranks follow input order
-  // (conflicting lanes of one instruction are serialised in a fixed hardware
-  // order); the column prefix below orders the warps.  (MATCH.ANY-based peer
-  // aggregation measured 0.016 warp-instr/clk/SM on sm_100a: DESIGN.md §4.1.)
-  uint32_t rk[PI];  // (digit << 16) | rank among this warp's keys of that digit
+  for (uint32_t it = 0; t < ntiles; t += G, ++it) {
+    const uint32_t buf = it & 1;
+    const uint4 d = tdesc[t];
+    if (threadIdx.x == 0 && t + G < ntiles) issue_tile(sm, buf ^ 1, tdesc[t + G], key_in, rid_in, n);
+    const uint32_t cnt = d.y;
+    if (cnt) {  // CTA-uniform
+      // this tile's run offsets: loads issued now, consumed after ranking
+      uint32_t g0[DPT], g1[DPT];
 #pragma unroll
-  for (int i = 0; i < PI; ++i) {
-    const uint32_t j = (w * PI + i) * 32 + lane;
-    const uint32_t d = j < cnt ? digit_of(k[i], shift, mask) : D;
-    rk[i] = (d << 16) | atomicAdd(&whist[w * DW + d], 1u);
-  }
-  __syncthreads();
-  // column prefix over warps -> per-warp bases and this tile's count per digit
-  if (dd < D) {
-    uint32_t acc = 0;
+      for (int q = 0; q < DPT; ++q) {
+        const uint32_t dd = threadIdx.x + q * PT;
+        g0[q] = dd < D ? scanned[d.z + (uint64_t)dd * d.w] : 0u;
+        g1[q] = dd < D ? tile_pref[(uint64_t)t * D + dd] : 0u;
+      }
+      {
+        uint4* z = reinterpret_cast<uint4*>(sm.whist + w * D);
+        for (uint32_t i = lane; i < D / 4; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+      }
+      mbar_wait(&sm.bar[buf], (it >> 1) & 1);
+      const uint32_t ko = (d.x * (uint32_t)sizeof(K) & 15u) / (uint32_t)sizeof(K);
+      const uint32_t ro = (d.x & 3u);
+      const uint64_t kz = min((((uint64_t)(d.x + d.y) * sizeof(K)) + 15) & ~15ull, (n * sizeof(K)) & ~15ull);
+      const uint32_t kvalid = (uint32_t)(kz / sizeof(K) > d.x ? kz / sizeof(K) - d.x : 0);  // keys inside the bulk copy
+      const uint64_t rz = min((((uint64_t)(d.x + d.y) * 4) + 15) & ~15ull, (n * 4) & ~15ull);
+      const uint32_t rvalid = (uint32_t)(rz / 4 > d.x ? rz / 4 - d.x : 0);
+      K k[PI];
+      uint32_t rk[PI];  // (digit << 16) | rank among this warp's keys of that digit
+      __syncwarp();
+      // Rank inside the warp: every lane fetch-adds its digit's warp-private counter.
+      // Warp w's items are processed in index order, so ranks follow input order
+      // (conflicting lanes of one instruction are serialised in a fixed hardware
+      // order); the column prefix below orders the warps.  (MATCH.ANY-based peer
+      // aggregation measured 0.016 warp-instr/clk/SM on sm_100a: DESIGN.md §4.1.)
 #pragma unroll
-    for (int ww = 0; ww < NW; ++ww) {
-      const uint32_t x = whist[ww * DW + dd];
-      whist[ww * DW + dd] = acc;
-      acc += x;
+      for (int i = 0; i < PI; ++i) {
+        const uint32_t j = (w * PI + i) * 32 + lane;
+        const bool v = j < cnt;
+        k[i] = v ? (j < kvalid ? sm.key[buf][ko + j] : key_in[d.x + j]) : K(0);
+        const uint32_t dg = v ? digit_of(k[i], shift, mask) : 0u;
+        uint32_t r = 0;
+        if (v) r = atomicAdd(&sm.whist[w * D + dg], 1u);
+        rk[i] = v ? ((dg << 16) | r) : 0xffffffffu;
+      }
+      uint32_t rr[HAS_RID ? PI : 1];
+      if (HAS_RID) {
+#pragma unroll
+        for (int i = 0; i < PI; ++i) {
+          const uint32_t j = (w * PI + i) * 32 + lane;
+          rr[i] = j < cnt ? (j < rvalid ? sm.rid[buf][ro + j] : rid_in[d.x + j]) : 0u;
+        }
+      }
+      __syncthreads();  // all inputs are in registers: the buffer becomes the staging area
+      for (uint32_t dd = threadIdx.x; dd < D; dd += PT) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) {
+          const uint32_t x = sm.whist[ww * D + dd];
+          sm.whist[ww * D + dd] = acc;
+          acc += x;
+        }
+        sm.dstart[dd] = acc;
+      }
+      __syncthreads();
+      cta_scan_small(sm.dstart, D, sm.wt);  // tile-local digit starts; ends with a barrier
+#pragma unroll
+      for (int q = 0; q < DPT; ++q) {
+        const uint32_t dd = threadIdx.x + q * PT;
+        if (dd < D) {
+          const uint32_t st = sm.dstart[dd];
+          sm.delta[dd] = g0[q] + g1[q] - st;
+#pragma unroll
+          for (int ww = 0; ww < NW; ++ww) sm.whist[ww * D + dd] += st;
+        }
+      }
+      __syncthreads();
+      K* skey = sm.key[buf];
+      uint32_t* srid = sm.rid[buf];
+#pragma unroll
+      for (int i = 0; i < PI; ++i) {
+        if (rk[i] != 0xffffffffu) {
+          const uint32_t pos = sm.whist[w * D + (rk[i] >> 16)] + (rk[i] & 0xffffu);
+          skey[pos] = k[i];
+          srid[pos] = HAS_RID ? rr[i] : rid_base + d.x + (w * PI + i) * 32 + lane;
+        }
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int i = 0; i < PI; ++i) {
+        const uint32_t j = i * PT + threadIdx.x;
+        if (j < cnt) {
+          const K kk = skey[j];
+          const uint32_t pos = sm.delta[digit_of(kk, shift, mask)] + j;
+          key_out[pos] = kk;
+          rid_out[pos] = srid[j];
+        }
+      }
+    } else {
+      mbar_wait(&sm.bar[buf], (it >> 1) & 1);
     }
-    dstart[dd] = acc;
-  }
-  __syncthreads();
-  cta_scan_small(dstart, D, wt);  // tile-local digit starts; ends with a barrier
-  if (dd < D) delta[dd] = goff - dstart[dd];
-#pragma unroll
-  for (int i = 0; i < PI; ++i) {
-    const uint32_t d = rk[i] >> 16;
-    if (d < D) {
-      const uint32_t pos = dstart[d] + whist[w * DW + d] + (rk[i] & 0xffffu);
-      skey[pos] = k[i];
-      srid[pos] = HAS_RID ? r[i] : rid_base + (uint32_t)tbeg + (w * PI + i) * 32 + lane;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < PI; ++i) {
-    const uint32_t j = i * PT + threadIdx.x;
-    if (j < cnt) {
-      const K kk = skey[j];
-      const uint32_t pos = delta[digit_of(kk, shift, mask)] + j;
-      key_out[pos] = kk;
-      rid_out[pos] = srid[j];
-    }
+    __syncthreads();  // the buffer may be refilled by the next iteration's issue
   }
 }
 
@@ -287,9 +396,6 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
   const uint32_t* rin = X.rid;
   const uint32_t* seg_off = nullptr;
   uint32_t nseg = 1, used = skip;
-  const size_t smem_max = TILE * (sizeof(K) + sizeof(uint32_t)) + (NW * ((1u << MAX_BITS) + 1) + 3 * (1u << MAX_BITS)) * sizeof(uint32_t);
-  static bool smem_set = (set_smem(part_scatter<K, true>, smem_max), set_smem(part_scatter<K, false>, smem_max), true);
-  (void)smem_set;
   for (int pass = 0; pass < npass; ++pass) {
     const uint32_t bits = B / npass + ((uint32_t)pass < B % npass ? 1 : 0);
     const uint32_t D = 1u << bits;
@@ -311,15 +417,30 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
     launch(ctx, "part_hist", part_hist<K>, dim3((unsigned)max_chunks), dim3(PT), 0, kin, n, seg_off,
            (const uint32_t*)chunk_base, nseg, shift, bits, hist, tile_pref);
     exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
-    const size_t smem = TILE * (sizeof(K) + sizeof(uint32_t)) + (NW * (D + 1) + 2 * D) * sizeof(uint32_t);
-    if (rin)
-      launch(ctx, "part_scatter", part_scatter<K, true>, dim3((unsigned)ntiles), dim3(PT), smem, kin, rin,
-             X.rid_base, n, seg_off, (const uint32_t*)chunk_base, nseg, shift, bits, (const uint32_t*)hist,
-             (const uint32_t*)tile_pref, kout, rout);
-    else
-      launch(ctx, "part_scatter", part_scatter<K, false>, dim3((unsigned)ntiles), dim3(PT), smem, kin, rin,
-             X.rid_base, n, seg_off, (const uint32_t*)chunk_base, nseg, shift, bits, (const uint32_t*)hist,
-             (const uint32_t*)tile_pref, kout, rout);
+    uint4* tdesc = static_cast<uint4*>(ws(ctx, "part.tdesc", (ntiles + 1) * sizeof(uint4)));
+    launch(ctx, "tile_desc", tile_desc_kernel, dim3((unsigned)((ntiles + 255) / 256)), dim3(256), 0, n, seg_off,
+           (const uint32_t*)chunk_base, nseg, D, (uint32_t)ntiles, tdesc);
+    if (rin) {
+      const size_t smem = sizeof(ScatterSmem<K, true>);
+      static bool once = (set_smem(part_scatter<K, true>, smem), true);
+      (void)once;
+      int occ = 1;
+      GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, part_scatter<K, true>, PT, smem));
+      const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
+      launch(ctx, "part_scatter", part_scatter<K, true>, dim3(grid), dim3(PT), smem, kin, rin, X.rid_base, n,
+             (const uint4*)tdesc, (uint32_t)ntiles, shift, bits, (const uint32_t*)hist, (const uint32_t*)tile_pref,
+             kout, rout);
+    } else {
+      const size_t smem = sizeof(ScatterSmem<K, false>);
+      static bool once = (set_smem(part_scatter<K, false>, smem), true);
+      (void)once;
+      int occ = 1;
+      GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, part_scatter<K, false>, PT, smem));
+      const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
+      launch(ctx, "part_scatter", part_scatter<K, false>, dim3(grid), dim3(PT), smem, kin, rin, X.rid_base, n,
+             (const uint4*)tdesc, (uint32_t)ntiles, shift, bits, (const uint32_t*)hist, (const uint32_t*)tile_pref,
+             kout, rout);
+    }
     const uint32_t P = nseg << bits;
     uint32_t* off = static_cast<uint32_t*>(ws(ctx, (ps + ".off").c_str(), (P + 1) * sizeof(uint32_t)));
     launch(ctx, "extract_off", extract_off, dim3((P + 1 + 255) / 256), dim3(256), 0, (const uint32_t*)hist,

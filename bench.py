@@ -143,26 +143,37 @@ def max_over_ranks(x, world):
 
 # ------------------------------------------------------------------ workloads
 
-def make_workload(name, device):
+def make_workload(name, device, rank=0, world=1):
+    """Synthetic relations in HBM.  With world > 1 every rank holds a block shard
+    of a problem `world` times larger (weak scaling); rid_base = global row offset."""
     import torch
     import gen
     import gen.device as gd
     seed = gen.BASE_SEED
+    g = max(world.bit_length() - 1, 0)
     if name == "c2":
-        b = 27
-        R = gd.perm_range(1 << b, b, seed, device=device)
-        S = gd.pkfk_S(1 << b, b, seed, device=device)
-        desc = "configs[1]: equi hash join 2^27 x 2^27 8-byte tuples (int32 key+payload, payload not read), PK-FK unique R keys"
-        return dict(kind="equi", R=R, S=S, desc=desc, n_out_expected=1 << b)
+        n = 1 << 27  # per GPU
+        b = 27 + g
+        R = gd.perm_range(n, b, seed, offset=rank * n, device=device)
+        S = gd.pkfk_S(n, b, seed, offset=rank * n, device=device)
+        desc = ("configs[1]: equi hash join 2^27 x 2^27 8-byte tuples (int32 key+payload, payload not read), "
+                "PK-FK unique R keys")
+        if world > 1:
+            desc += f"; weak scaling: {world} ranks x (2^27 x 2^27) block shards, NCCL hash shuffle + local join"
+        return dict(kind="equi", R=R, S=S, desc=desc, rid_base=rank * n, n_out_expected=n)
     if name == "c1":
         R = gd.uniform(10_000, 10_000, seed, 0, device=device)
         S = gd.uniform(10_000, 10_000, seed, 1, device=device)
         return dict(kind="equi", R=R, S=S, desc="configs[0]: R=S=10^4 uniform keys in [0,10^4), equi hash join")
     if name == "c4":
-        R = gd.uniform(1 << 20, 1 << 30, seed, 0, device=device)
-        S = gd.uniform(1 << 24, 1 << 30, seed, 1, device=device)
-        return dict(kind="band", R=R, S=S, eps=gen.C4_EPS,
-                    desc="configs[3]: band join |R.a-S.b|<=53687, 2^20 x 2^24 uniform int32 in [0,2^30), count+scan+write")
+        nr = (1 << 20) // world  # R (2^20) is block-sharded and replicated by the join
+        ns = 1 << 24             # per GPU
+        R = gd.uniform(nr, 1 << 30, seed, 0, offset=rank * nr, device=device)
+        S = gd.uniform(ns, 1 << 30, seed, 1, offset=rank * ns, device=device)
+        desc = "configs[3]: band join |R.a-S.b|<=53687, 2^20 x 2^24 uniform int32 in [0,2^30), count+scan+write"
+        if world > 1:
+            desc += f"; weak scaling: R (2^20) all-gathered, {world} x 2^24 S shards"
+        return dict(kind="band", R=R, S=S, eps=gen.C4_EPS, desc=desc, rid_base_R=rank * nr, rid_base=rank * ns)
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -175,11 +186,14 @@ def algorithmic_bytes(w, ctxinfo):
         n = nR + nS
         # scatter: pass 1 reads the key (rid implicit) + writes key+rid; later passes read key+rid
         scatter_total = (nR + nS) * (4 + 8) + (passes - 1) * (nR + nS) * (8 + 8)
+        nb, npb = min(nR, nS), max(nR, nS)
         return {
             "part_hist": (4 * n * passes, 2 * passes),
             "part_scatter": (scatter_total, 2 * passes),
-            "hj_count": (4 * n, 1),
-            "hj_write": (8 * n + 8 * nout, 1),
+            # count: build + probe keys in, one uint16 match index per probe row out
+            "hj_count": (4 * n + 2 * npb, 1),
+            # write: build + probe rids and the staged index in, 8-byte pairs out
+            "hj_write": (4 * nb + 4 * npb + 2 * npb + 8 * nout, 1),
         }
     # band: NLJ is ALU-bound; bytes are tiny
     return {"nlj_count": (4 * (nR + nS), 1), "nlj_write": (4 * (nR + nS) + 8 * nout, 1)}
@@ -191,31 +205,47 @@ def run_ours(args, world, rank, local):
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    w = make_workload(args.workload, dev)
+    w = make_workload(args.workload, dev, rank, world)
     stream = torch.cuda.current_stream(dev)
     ctx = gj.Context(local, stream)
     for o in args.opt:
         k, v = o.split("=")
         ctx.set_option(k, int(v))
-    R, S = w["R"], w["S"]
-    nR, nS = R.numel(), S.numel()
+    nR, nS = w["R"].numel(), w["S"].numel()
+    R = gj.Rel(w["R"], None, w.get("rid_base_R", w.get("rid_base", 0)))
+    S = gj.Rel(w["S"], None, w.get("rid_base", 0))
+    comm = gj.Comm(rank, world) if world > 1 else None
 
     if w["kind"] == "equi":
-        n = gj.join_count(ctx, R, S)
-        out = torch.empty((max(n, 1), 2), dtype=torch.int32, device=dev)
+        if comm is None:
+            n = n_global = gj.join_count(ctx, R, S)
+        else:
+            n, n_global = gj.join_dist_count(ctx, comm, R, S)
+        out = torch.empty((max(int(n * 1.2) + 1024, 1), 2), dtype=torch.int32, device=dev)
 
         def step():
-            m = gj.join_count(ctx, R, S)
-            gj.join_materialize(ctx, R, S, m, out=out)
+            if comm is None:
+                m = gj.join_count(ctx, R, S)
+                gj.join_materialize(ctx, R, S, m, out=out)
+            else:
+                m, _ = gj.join_dist_count(ctx, comm, R, S)
+                gj.join_dist_materialize(ctx, comm, R, S, m, out=out)
             return m
     else:
         eps = w["eps"]
-        n = gj.theta_join_count(ctx, R, S, "band", eps)
+        if comm is None:
+            n = n_global = gj.theta_join_count(ctx, R, S, "band", eps)
+        else:
+            n, n_global = gj.theta_join_dist_count(ctx, comm, R, S, "band", eps)
         out = torch.empty((max(n, 1), 2), dtype=torch.int32, device=dev)
 
         def step():
-            m = gj.theta_join_count(ctx, R, S, "band", eps)
-            gj.theta_join_materialize(ctx, R, S, "band", eps, m, out=out)
+            if comm is None:
+                m = gj.theta_join_count(ctx, R, S, "band", eps)
+                gj.theta_join_materialize(ctx, R, S, "band", eps, m, out=out)
+            else:
+                m, _ = gj.theta_join_dist_count(ctx, comm, R, S, "band", eps)
+                gj.theta_join_dist_materialize(ctx, comm, R, S, "band", eps, m, out=out)
             return m
 
     for _ in range(args.warmup):
@@ -250,11 +280,8 @@ def run_ours(args, world, rank, local):
 
     info = {"n_out": n}
     if w["kind"] == "equi":
-        B = 0
-        nb = min(nR, nS)
-        while (nb >> B) > 2048 and B < 27:
-            B += 1
-        info["passes"] = (B + 8) // 9 if B else 0
+        # radix passes per relation actually run (incl. the multi-GPU shuffle pass)
+        info["passes"] = round(ktimes.get("part_scatter", (0, 0))[1] / args.steps / 2)
     ab = algorithmic_bytes(w, info)
     hbm, peak_src = peaks()
     per_kernel = {}
@@ -284,28 +311,46 @@ def run_ours(args, world, rank, local):
                 "unit": "Tpair/s", "frac": round(ach / alu_peak, 4), "traffic": None,
                 "peak_source": "148 SM x 64 ALU lanes/clk x median SM clock / 1.5 ALU instr per pair"}
 
-    # ---- e2e through the host-buffer C-ABI entry (equi only)
+    # ---- e2e: host buffers in, host pairs out, through the public API
     e2e = None
     if w["kind"] == "equi":
-        hR = R.cpu().pin_memory()
-        hS = S.cpu().pin_memory()
+        hR = w["R"].cpu().pin_memory()
+        hS = w["S"].cpu().pin_memory()
         hout = torch.empty((max(n, 1), 2), dtype=torch.int32).pin_memory()
-        gj.join_host(ctx, hR, hS, hout)
         k_e2e = max(1, min(args.steps, args.e2e_steps))
+        if comm is None:
+            def e2e_step():
+                return gj.join_host(ctx, hR, hS, hout)  # one C-ABI call: H2D, join, D2H
+            note = "join_host(): pinned host keys -> H2D -> count/scan/write -> D2H of all pairs (one C-ABI call)"
+        else:
+            dR, dS = torch.empty_like(w["R"]), torch.empty_like(w["S"])
+            eR, eS = gj.Rel(dR, None, R.rid_base), gj.Rel(dS, None, S.rid_base)
+
+            def e2e_step():
+                dR.copy_(hR, non_blocking=True)
+                dS.copy_(hS, non_blocking=True)
+                m, _ = gj.join_dist_count(ctx, comm, eR, eS)
+                res = gj.join_dist_materialize(ctx, comm, eR, eS, m, out=out)
+                hout[:m].copy_(res)
+                return m
+            note = "per rank: pinned H2D of its shards -> join_dist_count/materialize (NCCL shuffle) -> D2H of its pairs"
+        e2e_step()
         torch.cuda.synchronize()
         barrier(world)
         t0 = time.perf_counter()
         for _ in range(k_e2e):
-            got = gj.join_host(ctx, hR, hS, hout)
+            got = e2e_step()
+        torch.cuda.synchronize()
         t1 = time.perf_counter()
         assert got == n
         e2e_s = max_over_ranks(t1 - t0, world)
         e2e = {"value": (nR + nS) * k_e2e * world / e2e_s, "unit": "input tuples/s",
                "h2d_bytes_per_step": hR.numel() * hR.element_size() + hS.numel() * hS.element_size(),
-               "d2h_bytes_per_step": n * 8, "steps": k_e2e,
-               "note": "join_host(): pinned host keys -> H2D -> count/scan/write -> D2H of all pairs; wall clock, the call synchronises"}
+               "d2h_bytes_per_step": n * 8, "steps": k_e2e, "note": note + "; wall clock, max over ranks"}
+    if comm is not None:
+        comm.close()
 
-    return dict(ms=ms_max, n=n, nR=nR, nS=nS, launches=launches, roof=roof, per_kernel=per_kernel, e2e=e2e,
+    return dict(ms=ms_max, n=n_global, nR=nR, nS=nS, launches=launches, roof=roof, per_kernel=per_kernel, e2e=e2e,
                 clocks=sampler.summary(), desc=w["desc"], kind=w["kind"])
 
 
@@ -333,6 +378,18 @@ def cpu_baseline(args):
 
 
 def main():
+    # Exactly one JSON line goes to stdout: C-level chatter (e.g. NCCL's version
+    # banner) is redirected to stderr and the JSON is written to the saved fd.
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+    global print
+    _print = print
+
+    def print(*a, **k):  # noqa: A001 - route this module's JSON line to the real stdout
+        with os.fdopen(os.dup(json_fd), "w") as f:
+            _print(*a, **k, file=f)
+
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -374,7 +431,7 @@ def main():
         "metric": METRIC,
         "value": value,
         "unit": "input tuples/s",
-        "output_tuples_per_s": r["n"] * args.steps * world / T,
+        "output_tuples_per_s": r["n"] * args.steps / T,
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
@@ -384,9 +441,10 @@ def main():
         "vs_baseline": None,
         "dtype": "i32",
         "data": "synthetic",
-        "config": {"workload": r["desc"], "n_R": r["nR"], "n_S": r["nS"], "n_out": r["n"],
+        "config": {"workload": r["desc"], "n_R_per_gpu": r["nR"], "n_S_per_gpu": r["nS"], "n_out": r["n"],
                    "l2": "inputs (>=64 MiB of keys, 1 GiB for configs[1]) exceed/stream past the 126 MB L2; no flush",
-                   "parallelism": f"{world} independent ranks (weak scaling)"},
+                   "parallelism": ("1 GPU" if world == 1 else
+                                   f"{world} ranks, NCCL hash-partition shuffle (equi) / R all-gather (theta)")},
         "roofline": r["roof"],
         "kernels": r["per_kernel"],
         "gpu_launches": r["launches"],

@@ -177,6 +177,46 @@ gj_status join_host(gj_ctx* ctx, const void* key_R_host, uint64_t n_R, const voi
                     uint64_t n_S, int key_type, uint32_t* out_host, uint64_t capacity,
                     uint64_t* n_out);
 
+/* ---------------------------------------------------------------- multi-GPU
+ * One process per GPU.  Equi joins shard by hash partition (the B200 analogue of
+ * the Hadoop shuffle of Alg.1 Map2): every rank partitions its
+ * shards of R and S by the top log2(G) bits of the key hash, an NCCL all-gather
+ * exchanges the GxG count matrix, grouped ncclSend/ncclRecv move the (key, rid)
+ * buckets over NVLink, and each rank joins what it received.  Theta joins
+ * broadcast R (all-gather of the R shards, PAPER.md:302 region model with one
+ * region per rank) and join it against the local S shard.  Output stays sharded:
+ * every pair lands on exactly one rank; the union over ranks is J(R, S).
+ * Shards identify rows globally through rid_base (or rid maps).
+ *
+ * gj_comm_unique_id: writes GJ_COMM_ID_BYTES bytes (an ncclUniqueId) on one rank;
+ *   the caller broadcasts them (e.g. over torch.distributed).
+ * gj_comm_init: every rank, collectively; binds the current CUDA device.
+ * All *_dist_* calls are COLLECTIVE: every rank calls with the same op/eps.
+ * G (nranks) must be a power of two for the equi-join shuffle.
+ * n_local = pairs written by this rank; n_global = sum over ranks (host, uint64).
+ * *_dist_materialize follows the same cache / GJ_ERANGE rules as the 1-GPU calls
+ * (capacity and out refer to this rank's share). */
+#define GJ_COMM_ID_BYTES 128
+typedef struct gj_comm gj_comm;
+gj_status gj_comm_unique_id(void* id_out);
+gj_status gj_comm_init(gj_comm** out, const void* id, int nranks, int rank);
+void gj_comm_destroy(gj_comm* comm);
+gj_status join_dist_count(gj_ctx* ctx, gj_comm* comm, gj_rel R, gj_rel S, uint64_t* n_local,
+                          uint64_t* n_global);
+gj_status join_dist_materialize(gj_ctx* ctx, gj_comm* comm, gj_rel R, gj_rel S, uint32_t* out,
+                                uint64_t capacity, uint64_t* n_written);
+gj_status theta_join_dist_count(gj_ctx* ctx, gj_comm* comm, gj_rel R, gj_rel S, int op, uint64_t eps,
+                                uint64_t* n_local, uint64_t* n_global);
+gj_status theta_join_dist_materialize(gj_ctx* ctx, gj_comm* comm, gj_rel R, gj_rel S, int op,
+                                      uint64_t eps, uint32_t* out, uint64_t capacity,
+                                      uint64_t* n_written);
+/* Host-only shuffle planning (no GPU, no NCCL): given the row-major G x G matrix
+ * counts[src*G + dst] of tuples rank src sends to rank dst, writes this rank's
+ * receive displacements recv_off[0..G) (exclusive prefix over sources) and returns
+ * the number of tuples it receives in *recv_total.  Exposed for host-side tests. */
+gj_status gj_dist_plan(const uint64_t* counts, int nranks, int rank, uint64_t* recv_off,
+                       uint64_t* recv_total);
+
 #ifdef __cplusplus
 }
 #endif

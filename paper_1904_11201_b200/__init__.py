@@ -78,8 +78,19 @@ def _load():
     L.theta_join_materialize.argtypes = [vp, _Rel, _Rel, i32, u64, vp, u64, pu64]
     L.prefilter.argtypes = [vp, _Rel, _Rel, u32, i32, u64, ctypes.c_double, vp, vp, pu64, vp, vp, pu64]
     L.join_host.argtypes = [vp, vp, u64, vp, u64, i32, vp, u64, pu64]
+    L.gj_comm_unique_id.argtypes = [vp]
+    L.gj_comm_init.argtypes = [ctypes.POINTER(vp), vp, i32, i32]
+    L.gj_comm_destroy.argtypes = [vp]
+    L.gj_comm_destroy.restype = None
+    L.join_dist_count.argtypes = [vp, vp, _Rel, _Rel, pu64, pu64]
+    L.join_dist_materialize.argtypes = [vp, vp, _Rel, _Rel, vp, u64, pu64]
+    L.theta_join_dist_count.argtypes = [vp, vp, _Rel, _Rel, i32, u64, pu64, pu64]
+    L.theta_join_dist_materialize.argtypes = [vp, vp, _Rel, _Rel, i32, u64, vp, u64, pu64]
+    L.gj_dist_plan.argtypes = [pu64, i32, i32, pu64, pu64]
     for f in ("gj_ctx_create", "gj_ctx_set_stream", "gj_ctx_set_option", "join_count", "join_materialize",
-              "theta_join_count", "theta_join_materialize", "prefilter", "join_host"):
+              "theta_join_count", "theta_join_materialize", "prefilter", "join_host", "gj_comm_unique_id",
+              "gj_comm_init", "join_dist_count", "join_dist_materialize", "theta_join_dist_count",
+              "theta_join_dist_materialize", "gj_dist_plan"):
         getattr(L, f).restype = i32
     return L
 
@@ -89,7 +100,10 @@ lib = _load()
 # C-ABI symbols declared in include/gjoin.h (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("gj_ctx_create", "gj_ctx_destroy", "gj_ctx_set_stream", "gj_last_error", "gj_ctx_set_option",
                "gj_ctx_launch_count", "gj_ctx_reset_stats", "gj_ctx_kernel_times", "join_count",
-               "join_materialize", "theta_join_count", "theta_join_materialize", "prefilter", "join_host")
+               "join_materialize", "theta_join_count", "theta_join_materialize", "prefilter", "join_host",
+               "gj_comm_unique_id", "gj_comm_init", "gj_comm_destroy", "join_dist_count", "join_dist_materialize",
+               "theta_join_dist_count", "theta_join_dist_materialize", "gj_dist_plan")
+COMM_ID_BYTES = 128
 
 
 def _check(status: int):
@@ -247,3 +261,88 @@ def join_host(ctx: Context, key_R: torch.Tensor, key_S: torch.Tensor, out: torch
                          I32 if key_R.dtype == torch.int32 else I64,
                          ctypes.c_void_p(out.data_ptr()), out.shape[0], ctypes.byref(n)))
     return n.value
+
+
+# ---------------------------------------------------------------- multi-GPU (NCCL)
+
+def dist_plan(counts, rank: int):
+    """Host-only shuffle plan (gj_dist_plan): counts = G x G matrix [src][dst].
+    Returns (recv_off list, recv_total)."""
+    import numpy as np
+    m = np.ascontiguousarray(np.asarray(counts, dtype=np.uint64))
+    G = m.shape[0]
+    off = np.zeros(G, dtype=np.uint64)
+    tot = ctypes.c_uint64()
+    _check(lib.gj_dist_plan(m.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), G, rank,
+                            off.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ctypes.byref(tot)))
+    return off.tolist(), tot.value
+
+
+class Comm:
+    """gj_comm: an NCCL communicator over the ranks of a torch.distributed group.
+
+    Rank 0 creates the ncclUniqueId; it is broadcast with torch.distributed (any
+    backend), then every rank calls gj_comm_init on its current CUDA device."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        import torch.distributed as dist
+        uid = (ctypes.c_uint8 * COMM_ID_BYTES)()
+        if rank == 0:
+            _check(lib.gj_comm_unique_id(ctypes.cast(uid, ctypes.c_void_p)))
+        obj = [bytes(uid)]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        uid = (ctypes.c_uint8 * COMM_ID_BYTES).from_buffer_copy(obj[0])
+        h = ctypes.c_void_p()
+        _check(lib.gj_comm_init(ctypes.byref(h), ctypes.cast(uid, ctypes.c_void_p), world, rank))
+        self.h, self.rank, self.world = h, rank, world
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.gj_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def join_dist_count(ctx: Context, comm: Comm, R, S):
+    """Collective.  Returns (n_local, n_global)."""
+    nl, ng = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(lib.join_dist_count(ctx.h, comm.h, _rel(R), _rel(S), ctypes.byref(nl), ctypes.byref(ng)))
+    return nl.value, ng.value
+
+
+def join_dist_materialize(ctx: Context, comm: Comm, R, S, n_local: Optional[int] = None,
+                          out: Optional[torch.Tensor] = None):
+    """Collective.  Writes this rank's share of J(R, S) (global rids)."""
+    if n_local is None and out is None:
+        n_local, _ = join_dist_count(ctx, comm, R, S)
+    key = (R.key if isinstance(R, Rel) else R)
+    buf = _out(n_local or 0, out, key.device)
+    w = ctypes.c_uint64()
+    _check(lib.join_dist_materialize(ctx.h, comm.h, _rel(R), _rel(S), ctypes.c_void_p(buf.data_ptr()),
+                                     buf.shape[0], ctypes.byref(w)))
+    return buf[: w.value]
+
+
+def theta_join_dist_count(ctx: Context, comm: Comm, R, S, op: str, eps: int = 0):
+    nl, ng = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(lib.theta_join_dist_count(ctx.h, comm.h, _rel(R), _rel(S), OPS[op], int(eps), ctypes.byref(nl),
+                                     ctypes.byref(ng)))
+    return nl.value, ng.value
+
+
+def theta_join_dist_materialize(ctx: Context, comm: Comm, R, S, op: str, eps: int = 0,
+                                n_local: Optional[int] = None, out: Optional[torch.Tensor] = None):
+    if n_local is None and out is None:
+        n_local, _ = theta_join_dist_count(ctx, comm, R, S, op, eps)
+    key = (R.key if isinstance(R, Rel) else R)
+    buf = _out(n_local or 0, out, key.device)
+    w = ctypes.c_uint64()
+    _check(lib.theta_join_dist_materialize(ctx.h, comm.h, _rel(R), _rel(S), OPS[op], int(eps),
+                                           ctypes.c_void_p(buf.data_ptr()), buf.shape[0], ctypes.byref(w)))
+    return buf[: w.value]

@@ -19,16 +19,19 @@ gj_status prefilter_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t
                          uint64_t* nSo);
 
 static thread_local std::string g_err;
+void set_last_error(const std::string& m) { g_err = m; }
 
 void* ws(gj_ctx* ctx, const char* name, size_t bytes) {
   Buf& b = ctx->bufs[name];
   if (bytes == 0) bytes = 1;
   if (b.bytes < bytes) {
-    if (b.ptr) GJ_CUDA(cudaFreeAsync(b.ptr, ctx->stream));
+    // Grow-only: plain cudaMalloc/cudaFree (synchronising, but rare).  Stream-ordered
+    // pool memory was measured to make NCCL peer transfers ~10x slower.
+    if (b.ptr) GJ_CUDA(cudaFree(b.ptr));
     b.ptr = nullptr;
     b.bytes = 0;
     const size_t rounded = (bytes + (1u << 20) - 1) & ~(size_t)((1u << 20) - 1);
-    cudaError_t e = cudaMallocAsync(&b.ptr, rounded, ctx->stream);
+    cudaError_t e = cudaMalloc(&b.ptr, rounded);
     if (e != cudaSuccess) {
       cudaGetLastError();
       throw Error(GJ_ENOMEM, std::string("workspace '") + name + "' (" + std::to_string(rounded) +
@@ -75,6 +78,20 @@ LaunchScope::~LaunchScope() noexcept(false) {
   }
 }
 
+RegionScope::RegionScope(gj_ctx* c, const char* t) : ctx(c), tag(t) {
+  if (ctx->profile) {
+    a = get_event(ctx);
+    GJ_CUDA(cudaEventRecord(a, ctx->stream));
+  }
+}
+
+RegionScope::~RegionScope() {
+  if (ctx->profile && a) {
+    cudaEvent_t b = get_event(ctx);
+    if (cudaEventRecord(b, ctx->stream) == cudaSuccess) ctx->pending.push_back({tag, a, b});
+  }
+}
+
 static void flush_prof(gj_ctx* ctx) {
   if (ctx->pending.empty()) return;
   GJ_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -117,7 +134,10 @@ static uint32_t auto_bits(gj_ctx* ctx, uint64_t nb) {
   return B;
 }
 
-static void do_join_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S) {
+// Single-GPU equi-join count: partition both relations with the same radix bits
+// (skipping the top `skip` hash bits a multi-GPU shuffle already consumed), then
+// count per partition.  Leaves everything the write pass needs in ctx->jc.
+void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t skip) {
   JoinCache& jc = ctx->jc;
   jc = JoinCache{};
   jc.R = R;
@@ -127,12 +147,14 @@ static void do_join_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S) {
     return;
   }
   const bool swap = ctx->build_side == 2 || (ctx->build_side == 0 && S.n < R.n);
-  const uint32_t B = auto_bits(ctx, swap ? S.n : R.n);
-  Partitioned PR = radix_partition(ctx, R, B, "R");
-  Partitioned PS = radix_partition(ctx, S, B, "S");
+  const uint32_t B = std::min<uint32_t>(auto_bits(ctx, swap ? S.n : R.n), 32 - skip);
+  Partitioned PR = radix_partition(ctx, R, B, "R", skip);
+  Partitioned PS = radix_partition(ctx, S, B, "S", skip);
   hash_join_count(ctx, R, S, B, swap, PR, PS);
   jc.valid = true;
 }
+
+static void do_join_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S) { join_count_core(ctx, R, S, 0); }
 
 }  // namespace gj
 
@@ -174,7 +196,7 @@ void gj_ctx_destroy(gj_ctx* ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->stream);
   for (auto& kv : ctx->bufs)
-    if (kv.second.ptr) cudaFreeAsync(kv.second.ptr, ctx->stream);
+    if (kv.second.ptr) cudaFree(kv.second.ptr);
   for (auto& p : ctx->pending) {
     cudaEventDestroy(p.a);
     cudaEventDestroy(p.b);

@@ -1,0 +1,398 @@
+// dist.cu -- multi-GPU joins over NCCL (one process per GPU).
+//
+// Equi join: the paper's Hadoop shuffle ("emit
+// (join_key/a, tagged tuple)" then shuffle by key, Alg.1) becomes
+//   1. a radix pass over each local shard by the top log2(G) bits of the key hash
+//      (the destination rank), writing SoA (key, rid) buckets;
+//   2. ncclAllGather of every rank's 2G bucket sizes (R and S);
+//   3. grouped ncclSend/ncclRecv of the buckets (all-to-all-v over NVLink);
+//   4. the single-GPU partitioned hash join on what arrived, skipping the hash bits
+//      the shuffle consumed.  Each pair is produced on exactly one rank (the owner
+//      of its key's hash bucket); rids are global (shard rid_base / rid maps).
+// Theta join: R is replicated (ncclBroadcast from every rank inside one group, i.e.
+// an all-gather-v) and each rank runs the tiled NLJ of R x (its S shard): the
+// one-region-per-rank case of the paper's region matrix.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "gjoin.h"
+#include "hashjoin.cuh"
+#include "nlj.cuh"
+#include "partition.cuh"
+#include "runtime.h"
+
+#ifdef GJ_HAVE_NCCL
+#include <nccl.h>
+#endif
+
+namespace gj {
+void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t skip);
+void set_last_error(const std::string& m);
+}  // namespace gj
+
+struct gj_comm {
+#ifdef GJ_HAVE_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+  int rank = 0, nranks = 1;
+  // cache of the last dist count (for materialize)
+  bool eq_valid = false, th_valid = false;
+  gj_rel R{}, S{};
+  int op = 0;
+  uint64_t eps = 0;
+  uint64_t total = 0;
+};
+
+namespace gj {
+
+#ifdef GJ_HAVE_NCCL
+#define GJ_NCCL(expr)                                                                        \
+  do {                                                                                       \
+    ncclResult_t _r = (expr);                                                                \
+    if (_r != ncclSuccess) throw ::gj::Error(GJ_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+  } while (0)
+#endif
+
+namespace {
+
+__global__ void bucket_counts(const uint32_t* __restrict__ off, uint32_t G, unsigned long long* __restrict__ out) {
+  const uint32_t p = threadIdx.x;
+  if (p < G) out[p] = off[p + 1] - off[p];
+}
+__global__ void fill_rids(uint32_t* __restrict__ out, uint64_t n, uint32_t base) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = base + (uint32_t)i;
+}
+
+bool same_rel(const gj_rel& a, const gj_rel& b) {
+  return a.key == b.key && a.rid == b.rid && a.n == b.n && a.key_type == b.key_type && a.rid_base == b.rid_base;
+}
+
+uint32_t log2_exact(int G) {
+  if (G < 1 || (G & (G - 1))) throw Error(GJ_EINVAL, "equi-join shuffle needs a power-of-two number of ranks");
+  uint32_t g = 0;
+  while ((1 << g) < G) ++g;
+  return g;
+}
+
+#ifdef GJ_HAVE_NCCL
+// allreduce of one uint64 (host in, host out)
+uint64_t allreduce_sum(gj_ctx* ctx, gj_comm* c, uint64_t v) {
+  unsigned long long* d = static_cast<unsigned long long*>(ws(ctx, "dist.sum", 16));
+  GJ_CUDA(cudaMemcpyAsync(d, &v, 8, cudaMemcpyHostToDevice, ctx->stream));
+  GJ_NCCL(ncclAllReduce(d, d + 1, 1, ncclUint64, ncclSum, c->comm, ctx->stream));
+  uint64_t out = 0;
+  d2h_sync(ctx, &out, d + 1, 8);
+  return out;
+}
+
+void dist_equi_count(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) {
+  const int G = c->nranks;
+  const uint32_t g = log2_exact(G);
+  const size_t ks = R.key_type == GJ_I64 ? 8 : 4;
+  const ncclDataType_t kt = R.key_type == GJ_I64 ? ncclInt64 : ncclInt32;
+  // 1. bucket both shards by destination rank (one radix pass of g bits)
+  Partitioned PR = radix_partition(ctx, R, g, "dR", 0);
+  Partitioned PS = radix_partition(ctx, S, g, "dS", 0);
+  unsigned long long* cnt = static_cast<unsigned long long*>(ws(ctx, "dist.cnt", (2 * G + 2 * G * G) * 8));
+  unsigned long long* all = cnt + 2 * G;
+  if (g == 0) {
+    GJ_CUDA(cudaMemcpyAsync(cnt, &R.n, 8, cudaMemcpyHostToDevice, ctx->stream));
+    GJ_CUDA(cudaMemcpyAsync(cnt + 1, &S.n, 8, cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    launch(ctx, "bucket_counts", bucket_counts, dim3(1), dim3(32), 0, PR.off, (uint32_t)G, cnt);
+    launch(ctx, "bucket_counts", bucket_counts, dim3(1), dim3(32), 0, PS.off, (uint32_t)G, cnt + G);
+  }
+  // 2. every rank learns the full count matrices
+  GJ_NCCL(ncclAllGather(cnt, all, 2 * G, ncclUint64, c->comm, ctx->stream));
+  std::vector<unsigned long long> M(2 * G * G);
+  d2h_sync(ctx, M.data(), all, M.size() * 8);
+  auto sent = [&](int src, int rel, int dst) { return (uint64_t)M[(size_t)src * 2 * G + rel * G + dst]; };
+  uint64_t nrecv[2] = {0, 0};
+  std::vector<uint64_t> roff[2] = {std::vector<uint64_t>(G), std::vector<uint64_t>(G)};
+  std::vector<uint64_t> soff[2] = {std::vector<uint64_t>(G), std::vector<uint64_t>(G)};
+  for (int rel = 0; rel < 2; ++rel) {
+    for (int p = 0; p < G; ++p) {
+      roff[rel][p] = nrecv[rel];
+      nrecv[rel] += sent(p, rel, c->rank);
+    }
+    uint64_t s = 0;
+    for (int p = 0; p < G; ++p) {
+      soff[rel][p] = s;
+      s += sent(c->rank, rel, p);
+    }
+  }
+  if (nrecv[0] >= (1ull << 32) || nrecv[1] >= (1ull << 32))
+    throw Error(GJ_EINVAL, "a rank would receive >= 2^32 tuples; use more ranks");
+  // 3. all-to-all-v of the (key, rid) buckets
+  uint8_t* rk[2] = {static_cast<uint8_t*>(ws(ctx, "dist.R.key", nrecv[0] * ks)),
+                    static_cast<uint8_t*>(ws(ctx, "dist.S.key", nrecv[1] * ks))};
+  uint32_t* rr[2] = {static_cast<uint32_t*>(ws(ctx, "dist.R.rid", nrecv[0] * 4)),
+                     static_cast<uint32_t*>(ws(ctx, "dist.S.rid", nrecv[1] * 4))};
+  const Partitioned* Ps[2] = {&PR, &PS};
+  const gj_rel* Xs[2] = {&R, &S};
+  // with g == 0 the "partitioned" view is the caller's relation: materialise rids
+  const uint32_t* srid[2];
+  for (int rel = 0; rel < 2; ++rel) {
+    srid[rel] = Ps[rel]->rid;
+    if (srid[rel] == nullptr) {
+      uint32_t* tmp = static_cast<uint32_t*>(ws(ctx, rel ? "dist.S.srid" : "dist.R.srid", Xs[rel]->n * 4));
+      launch(ctx, "fill_rids", fill_rids, dim3(std::max<uint32_t>(1, (uint32_t)std::min<uint64_t>((Xs[rel]->n + 255) / 256, 4096))),
+             dim3(256), 0, tmp, Xs[rel]->n, Xs[rel]->rid_base);
+      srid[rel] = tmp;
+    }
+  }
+  {
+    // the bucket a rank keeps never crosses NVLink: a device-local copy
+    RegionScope rs(ctx, "shuffle_self_copy");
+    for (int rel = 0; rel < 2; ++rel) {
+      const uint64_t nk = sent(c->rank, rel, c->rank);
+      if (!nk) continue;
+      GJ_CUDA(cudaMemcpyAsync(rk[rel] + roff[rel][c->rank] * ks,
+                              static_cast<const uint8_t*>(Ps[rel]->key) + soff[rel][c->rank] * ks, nk * ks,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+      GJ_CUDA(cudaMemcpyAsync(rr[rel] + roff[rel][c->rank], srid[rel] + soff[rel][c->rank], nk * 4,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+  }
+  {
+    RegionScope rs(ctx, "nccl_shuffle");
+    GJ_NCCL(ncclGroupStart());
+    for (int rel = 0; rel < 2; ++rel) {
+      const uint8_t* skey = static_cast<const uint8_t*>(Ps[rel]->key);
+      for (int p = 0; p < G; ++p) {
+        if (p == c->rank) continue;
+        const uint64_t ns = sent(c->rank, rel, p), nr = sent(p, rel, c->rank);
+        if (ns) {
+          GJ_NCCL(ncclSend(skey + soff[rel][p] * ks, ns, kt, p, c->comm, ctx->stream));
+          GJ_NCCL(ncclSend(srid[rel] + soff[rel][p], ns, ncclUint32, p, c->comm, ctx->stream));
+        }
+        if (nr) {
+          GJ_NCCL(ncclRecv(rk[rel] + roff[rel][p] * ks, nr, kt, p, c->comm, ctx->stream));
+          GJ_NCCL(ncclRecv(rr[rel] + roff[rel][p], nr, ncclUint32, p, c->comm, ctx->stream));
+        }
+      }
+    }
+    GJ_NCCL(ncclGroupEnd());
+  }
+  // 4. local partitioned hash join of what arrived (top g hash bits are now constant)
+  gj_rel RL{rk[0], rr[0], nrecv[0], R.key_type, 0}, SL{rk[1], rr[1], nrecv[1], S.key_type, 0};
+  join_count_core(ctx, RL, SL, g);
+}
+
+void dist_theta_count(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S, int op, uint64_t eps) {
+  const int G = c->nranks;
+  const size_t ks = R.key_type == GJ_I64 ? 8 : 4;
+  const ncclDataType_t kt = R.key_type == GJ_I64 ? ncclInt64 : ncclInt32;
+  unsigned long long* cnt = static_cast<unsigned long long*>(ws(ctx, "dist.tcnt", (1 + G) * 8));
+  GJ_CUDA(cudaMemcpyAsync(cnt, &R.n, 8, cudaMemcpyHostToDevice, ctx->stream));
+  GJ_NCCL(ncclAllGather(cnt, cnt + 1, 1, ncclUint64, c->comm, ctx->stream));
+  std::vector<unsigned long long> nR(G);
+  d2h_sync(ctx, nR.data(), cnt + 1, G * 8);
+  std::vector<uint64_t> off(G + 1, 0);
+  for (int p = 0; p < G; ++p) off[p + 1] = off[p] + nR[p];
+  if (off[G] >= (1ull << 32)) throw Error(GJ_EINVAL, "replicated R must hold < 2^32 tuples");
+  uint8_t* rkey = static_cast<uint8_t*>(ws(ctx, "dist.Rall.key", off[G] * ks));
+  uint32_t* rrid = static_cast<uint32_t*>(ws(ctx, "dist.Rall.rid", off[G] * 4));
+  const uint32_t* myrid = R.rid;
+  if (!myrid && R.n) {
+    uint32_t* tmp = static_cast<uint32_t*>(ws(ctx, "dist.R.srid", R.n * 4));
+    launch(ctx, "fill_rids", fill_rids, dim3((uint32_t)std::min<uint64_t>((R.n + 255) / 256, 4096)), dim3(256), 0,
+           tmp, R.n, R.rid_base);
+    myrid = tmp;
+  }
+  {
+    RegionScope rs(ctx, "nccl_allgather_R");
+    GJ_NCCL(ncclGroupStart());
+    for (int p = 0; p < G; ++p) {
+      if (!nR[p]) continue;
+      GJ_NCCL(ncclBroadcast(p == c->rank ? R.key : nullptr, rkey + off[p] * ks, nR[p], kt, p, c->comm,
+                            ctx->stream));
+      GJ_NCCL(ncclBroadcast(p == c->rank ? (const void*)myrid : nullptr, rrid + off[p], nR[p], ncclUint32, p,
+                            c->comm, ctx->stream));
+    }
+    GJ_NCCL(ncclGroupEnd());
+  }
+  gj_rel RA{rkey, rrid, off[G], R.key_type, 0};
+  ctx->tc = ThetaCache{};
+  theta_count(ctx, RA, S, op, eps);
+  ctx->tc.R = RA;
+  ctx->tc.valid = true;
+}
+#endif
+
+}  // namespace
+}  // namespace gj
+
+using namespace gj;
+
+#define DAPI_BEGIN try {
+#define DAPI_END                                                  \
+  }                                                               \
+  catch (const gj::Error& e) {                                    \
+    gj::set_last_error(e.what());                                 \
+    return e.code;                                                \
+  }                                                               \
+  catch (const std::exception& e) {                               \
+    gj::set_last_error(e.what());                                 \
+    return GJ_ECUDA;                                              \
+  }                                                               \
+  return GJ_OK;
+
+extern "C" {
+
+gj_status gj_dist_plan(const uint64_t* counts, int nranks, int rank, uint64_t* recv_off, uint64_t* recv_total) {
+  DAPI_BEGIN
+  if (!counts || !recv_off || !recv_total || nranks < 1 || rank < 0 || rank >= nranks)
+    throw Error(GJ_EINVAL, "gj_dist_plan: bad arguments");
+  uint64_t s = 0;
+  for (int p = 0; p < nranks; ++p) {
+    recv_off[p] = s;
+    s += counts[(size_t)p * nranks + rank];
+  }
+  *recv_total = s;
+  DAPI_END
+}
+
+#ifdef GJ_HAVE_NCCL
+gj_status gj_comm_unique_id(void* id_out) {
+  DAPI_BEGIN
+  if (!id_out) throw Error(GJ_EINVAL, "gj_comm_unique_id: NULL");
+  static_assert(sizeof(ncclUniqueId) == GJ_COMM_ID_BYTES, "ncclUniqueId size");
+  ncclUniqueId id;
+  GJ_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(id_out, &id, sizeof(id));
+  DAPI_END
+}
+
+gj_status gj_comm_init(gj_comm** out, const void* id, int nranks, int rank) {
+  DAPI_BEGIN
+  if (!out || !id || nranks < 1 || rank < 0 || rank >= nranks) throw Error(GJ_EINVAL, "gj_comm_init: bad arguments");
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  gj_comm* c = new gj_comm();
+  c->rank = rank;
+  c->nranks = nranks;
+  ncclResult_t r = ncclCommInitRank(&c->comm, nranks, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    throw Error(GJ_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  }
+  *out = c;
+  DAPI_END
+}
+
+void gj_comm_destroy(gj_comm* c) {
+  if (!c) return;
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+}
+
+static void check_args(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) {
+  if (!ctx || !c) throw Error(GJ_EINVAL, "NULL ctx or comm");
+  if (R.key_type != S.key_type || (R.key_type != GJ_I32 && R.key_type != GJ_I64))
+    throw Error(GJ_EINVAL, "R and S key types must agree (GJ_I32 or GJ_I64)");
+  if ((R.n && !R.key) || (S.n && !S.key)) throw Error(GJ_EINVAL, "NULL key with n > 0");
+  if (R.n >= (1ull << 32) || S.n >= (1ull << 32)) throw Error(GJ_EINVAL, "shard n must be < 2^32");
+}
+
+gj_status join_dist_count(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, uint64_t* n_local, uint64_t* n_global) {
+  DAPI_BEGIN
+  check_args(ctx, c, R, S);
+  if (!n_local || !n_global) throw Error(GJ_EINVAL, "NULL result pointer");
+  c->eq_valid = false;
+  dist_equi_count(ctx, c, R, S);
+  c->R = R;
+  c->S = S;
+  c->total = ctx->jc.total;
+  c->eq_valid = true;
+  *n_local = ctx->jc.total;
+  *n_global = allreduce_sum(ctx, c, ctx->jc.total);
+  DAPI_END
+}
+
+gj_status join_dist_materialize(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, uint32_t* out, uint64_t capacity,
+                                uint64_t* n_written) {
+  DAPI_BEGIN
+  check_args(ctx, c, R, S);
+  if (!n_written) throw Error(GJ_EINVAL, "NULL n_written");
+  if (!(c->eq_valid && same_rel(c->R, R) && same_rel(c->S, S) && ctx->jc.valid)) {
+    dist_equi_count(ctx, c, R, S);
+    c->R = R;
+    c->S = S;
+    c->eq_valid = true;
+  }
+  if (capacity < ctx->jc.total) {
+    *n_written = ctx->jc.total;
+    throw Error(GJ_ERANGE, "join_dist_materialize: capacity < local |J|");
+  }
+  if (ctx->jc.total && !out) throw Error(GJ_EINVAL, "NULL out");
+  hash_join_write(ctx, out);
+  *n_written = ctx->jc.total;
+  DAPI_END
+}
+
+gj_status theta_join_dist_count(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, int op, uint64_t eps,
+                                uint64_t* n_local, uint64_t* n_global) {
+  DAPI_BEGIN
+  check_args(ctx, c, R, S);
+  if (op < GJ_EQ || op > GJ_BAND) throw Error(GJ_EINVAL, "unknown op");
+  if (!n_local || !n_global) throw Error(GJ_EINVAL, "NULL result pointer");
+  c->th_valid = false;
+  dist_theta_count(ctx, c, R, S, op, eps);
+  c->R = R;
+  c->S = S;
+  c->op = op;
+  c->eps = eps;
+  c->th_valid = true;
+  *n_local = ctx->tc.total;
+  *n_global = allreduce_sum(ctx, c, ctx->tc.total);
+  DAPI_END
+}
+
+gj_status theta_join_dist_materialize(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, int op, uint64_t eps,
+                                      uint32_t* out, uint64_t capacity, uint64_t* n_written) {
+  DAPI_BEGIN
+  check_args(ctx, c, R, S);
+  if (op < GJ_EQ || op > GJ_BAND) throw Error(GJ_EINVAL, "unknown op");
+  if (!n_written) throw Error(GJ_EINVAL, "NULL n_written");
+  if (!(c->th_valid && same_rel(c->R, R) && same_rel(c->S, S) && c->op == op && c->eps == eps && ctx->tc.valid)) {
+    dist_theta_count(ctx, c, R, S, op, eps);
+    c->R = R;
+    c->S = S;
+    c->op = op;
+    c->eps = eps;
+    c->th_valid = true;
+  }
+  if (capacity < ctx->tc.total) {
+    *n_written = ctx->tc.total;
+    throw Error(GJ_ERANGE, "theta_join_dist_materialize: capacity < local |J|");
+  }
+  if (ctx->tc.total && !out) throw Error(GJ_EINVAL, "NULL out");
+  theta_write(ctx, out);
+  *n_written = ctx->tc.total;
+  DAPI_END
+}
+#else
+#define NO_NCCL                                                                   \
+  do {                                                                            \
+    gj::set_last_error("libgjoin was built without NCCL");                        \
+    return GJ_ENCCL;                                                              \
+  } while (0)
+gj_status gj_comm_unique_id(void*) { NO_NCCL; }
+gj_status gj_comm_init(gj_comm**, const void*, int, int) { NO_NCCL; }
+void gj_comm_destroy(gj_comm*) {}
+gj_status join_dist_count(gj_ctx*, gj_comm*, gj_rel, gj_rel, uint64_t*, uint64_t*) { NO_NCCL; }
+gj_status join_dist_materialize(gj_ctx*, gj_comm*, gj_rel, gj_rel, uint32_t*, uint64_t, uint64_t*) { NO_NCCL; }
+gj_status theta_join_dist_count(gj_ctx*, gj_comm*, gj_rel, gj_rel, int, uint64_t, uint64_t*, uint64_t*) { NO_NCCL; }
+gj_status theta_join_dist_materialize(gj_ctx*, gj_comm*, gj_rel, gj_rel, int, uint64_t, uint32_t*, uint64_t,
+                                      uint64_t*) {
+  NO_NCCL;
+}
+#endif
+
+}  // extern "C"

@@ -257,9 +257,11 @@ __global__ void __launch_bounds__(PT) part_scatter(
         g0[q] = dd < D ? scanned[d.z + (uint64_t)dd * d.w] : 0u;
         g1[q] = dd < D ? tile_pref[(uint64_t)t * D + dd] : 0u;
       }
-      {
+      if (D >= 4) {
         uint4* z = reinterpret_cast<uint4*>(sm.whist + w * D);
         for (uint32_t i = lane; i < D / 4; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+      } else if (lane < D) {
+        sm.whist[w * D + lane] = 0;
       }
       mbar_wait(&sm.bar[buf], (it >> 1) & 1);
       const uint32_t ko = (d.x * (uint32_t)sizeof(K) & 15u) / (uint32_t)sizeof(K);

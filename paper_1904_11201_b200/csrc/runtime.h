@@ -119,6 +119,16 @@ struct LaunchScope {
   ~LaunchScope() noexcept(false);
 };
 
+// Times a non-kernel stream region (e.g. an NCCL exchange) under GJ_OPT_PROFILE;
+// not counted as a kernel launch.
+struct RegionScope {
+  gj_ctx* ctx;
+  const char* tag;
+  cudaEvent_t a = nullptr;
+  RegionScope(gj_ctx* c, const char* t);
+  ~RegionScope();
+};
+
 // launch(ctx, "tag", kernel<...>, grid, block, smem, args...): every kernel of the
 // library goes through here, so gj_ctx_launch_count() is exact.
 template <typename... KArgs, typename... Args>

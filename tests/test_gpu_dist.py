@@ -1,0 +1,114 @@
+"""Multi-GPU parity (NCCL, one process per GPU): join_dist_* / theta_join_dist_*
+vs the CPU oracle on the union of all ranks' outputs.  Skips below 2 GPUs."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        import gen
+        import paper_1904_11201_b200 as gj
+        ctx = gj.Context(rank)
+        comm = gj.Comm(rank, world)
+        out = {}
+        # equi: PK-FK Zipf, block-sharded; rid_base = global row offset
+        b = 18
+        q_tab = gen.zipf_table(1 << b)
+        Rall, Sall, m = gen.zipf_pkfk(b, 1 << 20, q_tab, seed=5)
+        nr, ns = len(Rall) // world, len(Sall) // world
+        Rk = torch.from_numpy(Rall[rank * nr:(rank + 1) * nr]).cuda()
+        Sk = torch.from_numpy(Sall[rank * ns:(rank + 1) * ns]).cuda()
+        R = gj.Rel(Rk, None, rank * nr)
+        S = gj.Rel(Sk, None, rank * ns)
+        nl, ng = gj.join_dist_count(ctx, comm, R, S)
+        pairs = gj.join_dist_materialize(ctx, comm, R, S, nl).cpu().numpy().view(np.uint32)
+        out["equi"] = (nl, ng, pairs)
+        # duplicates on both sides, uneven shards
+        R2all = gen.uniform_keys(30_001, 2000, 3, 0)
+        S2all = gen.uniform_keys(40_003, 2000, 3, 1)
+        r0, r1 = (rank * len(R2all)) // world, ((rank + 1) * len(R2all)) // world
+        s0, s1 = (rank * len(S2all)) // world, ((rank + 1) * len(S2all)) // world
+        R2 = gj.Rel(torch.from_numpy(R2all[r0:r1]).cuda(), None, r0)
+        S2 = gj.Rel(torch.from_numpy(S2all[s0:s1]).cuda(), None, s0)
+        nl, ng = gj.join_dist_count(ctx, comm, R2, S2)
+        out["dup"] = (nl, ng, gj.join_dist_materialize(ctx, comm, R2, S2, nl).cpu().numpy().view(np.uint32))
+        # theta band: R replicated, S sharded
+        R3all = gen.uniform_keys(5000, 1 << 20, 8, 0)
+        S3all = gen.uniform_keys(20_000, 1 << 20, 8, 1)
+        a0, a1 = (rank * 5000) // world, ((rank + 1) * 5000) // world
+        c0, c1 = (rank * 20_000) // world, ((rank + 1) * 20_000) // world
+        R3 = gj.Rel(torch.from_numpy(R3all[a0:a1]).cuda(), None, a0)
+        S3 = gj.Rel(torch.from_numpy(S3all[c0:c1]).cuda(), None, c0)
+        nl, ng = gj.theta_join_dist_count(ctx, comm, R3, S3, "band", 40)
+        out["band"] = (nl, ng, gj.theta_join_dist_materialize(ctx, comm, R3, S3, "band", 40, nl).cpu().numpy().view(
+            np.uint32))
+        q.put((rank, out))
+        comm.close()
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def _canon(p):
+    p = np.asarray(p, dtype=np.uint32).reshape(-1, 2)
+    return p[np.lexsort((p[:, 1], p[:, 0]))]
+
+
+@pytest.mark.timeout(400)
+@pytest.mark.parametrize("world", [2, 4])
+def test_dist_joins_match_oracle(world):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import gen
+    import oracle
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    try:
+        for _ in range(world):
+            r, o = q.get(timeout=300)
+            res[r] = o
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.exitcode is None:
+                p.kill()
+    assert all(p.exitcode == 0 for p in procs)
+    b = 18
+    Rall, Sall, m = gen.zipf_pkfk(b, 1 << 20, gen.zipf_table(1 << b), seed=5)
+    R2all, S2all = gen.uniform_keys(30_001, 2000, 3, 0), gen.uniform_keys(40_003, 2000, 3, 1)
+    R3all, S3all = gen.uniform_keys(5000, 1 << 20, 8, 0), gen.uniform_keys(20_000, 1 << 20, 8, 1)
+    expect = {"equi": oracle.pkfk_closed_form(m), "dup": oracle.hash_equi(R2all, S2all),
+              "band": oracle.band_materialize(R3all, S3all, 40)}
+    for name, (cnt, pairs) in expect.items():
+        locals_ = [res[r][name] for r in range(world)]
+        assert all(l[1] == cnt for l in locals_), name  # n_global
+        assert sum(l[0] for l in locals_) == cnt, name  # n_local adds up
+        union = _canon(np.concatenate([l[2] for l in locals_]))
+        assert np.array_equal(union, pairs), name

@@ -126,7 +126,8 @@ def test_equi_c1_full(gj, ctx):
     check_equi(gj, ctx, R, S)
 
 
-@pytest.mark.parametrize("bits,chunk,pchunk", [(0, 2048, 2048), (0, 64, 100), (3, 2048, 2048), (9, 256, 64),
+@pytest.mark.parametrize("bits,chunk,pchunk", [(0, 2048, 2048), (0, 64, 100), (1, 2048, 2048), (2, 64, 100),
+                                               (3, 2048, 2048), (9, 256, 64),
                                                (10, 2048, 1024), (12, 32, 1000), (19, 2048, 2048)])
 def test_equi_planner_variants(gj, ctx, bits, chunk, pchunk):
     """1, 2 and 3 radix passes; build chunks split into many units; ragged tails."""

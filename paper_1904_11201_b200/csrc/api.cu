@@ -3,7 +3,12 @@
 // validation, and the count -> materialize cache.
 #include <cuda_runtime.h>
 
+#include <unistd.h>
+
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -45,7 +50,9 @@ void* ws(gj_ctx* ctx, const char* name, size_t bytes) {
 void d2h_sync(gj_ctx* ctx, void* host, const void* dev, size_t bytes) {
   if (bytes > 4096) throw Error(GJ_EINVAL, "d2h_sync: too large");
   GJ_CUDA(cudaMemcpyAsync(ctx->host_pinned, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  trace_mark("d2h_sync enqueue");
   GJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  trace_mark("d2h_sync done");
   std::memcpy(host, ctx->host_pinned, bytes);
 }
 
@@ -76,6 +83,29 @@ LaunchScope::~LaunchScope() noexcept(false) {
     GJ_CUDA(cudaEventRecord(b, ctx->stream));
     ctx->pending.push_back({tag, a, b});
   }
+}
+
+static int trace_level() {
+  static const int lvl = [] {
+    const char* e = std::getenv("GJ_TRACE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return lvl;
+}
+
+// GJ_TRACE=2: synchronise the stream first, so the mark times the GPU work of the phase
+void trace_sync(gj_ctx* ctx, const char* label) {
+  if (trace_level() >= 2) cudaStreamSynchronize(ctx->stream);
+  trace_mark(label);
+}
+
+void trace_mark(const char* label) {
+  if (trace_level() < 1) return;
+  static auto last = std::chrono::steady_clock::now();
+  const auto now = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[gj %d] %-24s +%.3f ms\n", (int)getpid(), label,
+               std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
 }
 
 RegionScope::RegionScope(gj_ctx* c, const char* t) : ctx(c), tag(t) {
@@ -146,7 +176,10 @@ void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t ski
     jc.valid = true;
     return;
   }
-  const bool swap = ctx->build_side == 2 || (ctx->build_side == 0 && S.n < R.n);
+  // "put the smaller table into a hash table", with a 10% tie band
+  // favouring R: near-equal sizes (e.g. a PK-FK join after a shuffle) must not flip
+  // the build side to the duplicate-heavy FK relation on random size fluctuations.
+  const bool swap = ctx->build_side == 2 || (ctx->build_side == 0 && S.n * 10 < R.n * 9);
   const uint32_t B = std::min<uint32_t>(auto_bits(ctx, swap ? S.n : R.n), 32 - skip);
   Partitioned PR = radix_partition(ctx, R, B, "R", skip);
   Partitioned PS = radix_partition(ctx, S, B, "S", skip);

@@ -14,6 +14,7 @@
 // one-region-per-rank case of the paper's region matrix.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -39,6 +40,16 @@ struct gj_comm {
   ncclComm_t comm = nullptr;
 #endif
   int rank = 0, nranks = 1;
+  // CUDA-IPC mappings of the peers' receive buffers (R key, R rid, S key, S rid),
+  // re-opened only when a peer reallocates (its handle changes)
+  cudaIpcMemHandle_t peer_h[gj::MAX_RANKS][4];
+  void* peer_ptr[gj::MAX_RANKS][4] = {};
+  // receive capacity (tuples) of every rank per relation: a deterministic function
+  // of the all-gathered count matrices, so all ranks agree when handles must be
+  // re-exchanged without an extra collective
+  uint64_t cap[gj::MAX_RANKS][2] = {};
+  bool mapped = false;
+  bool fused = true;  // shuffle fused into the scatter over NVLink (else NCCL send/recv)
   // cache of the last dist count (for materialize)
   bool eq_valid = false, th_valid = false;
   gj_rel R{}, S{};
@@ -184,6 +195,107 @@ void dist_equi_count(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) 
   join_count_core(ctx, RL, SL, g);
 }
 
+// Fused shuffle: radix histogram by destination rank, count-matrix all-gather,
+// then ONE scatter kernel per relation that writes every destination's run straight
+// into that rank's receive buffers through CUDA-IPC peer pointers (NVLink stores),
+// then a stream-ordered barrier (tiny all-reduce) before the local join reads them.
+void dist_equi_count_fused(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) {
+  const int G = c->nranks, me = c->rank;
+  const uint32_t g = log2_exact(G);
+  const size_t ks = R.key_type == GJ_I64 ? 8 : 4;
+  trace_sync(ctx, "fused: start");
+  ShufflePass SP[2] = {shuffle_prepare(ctx, R, g, "sR"), shuffle_prepare(ctx, S, g, "sS")};
+  trace_sync(ctx, "fused: shuffle hist");
+  unsigned long long* cnt = static_cast<unsigned long long*>(ws(ctx, "dist.cnt", (2 * G + 2 * G * G + 2) * 8));
+  unsigned long long* all = cnt + 2 * G;
+  launch(ctx, "bucket_counts", bucket_counts, dim3(1), dim3(32), 0, SP[0].off, (uint32_t)G, cnt);
+  launch(ctx, "bucket_counts", bucket_counts, dim3(1), dim3(32), 0, SP[1].off, (uint32_t)G, cnt + G);
+  GJ_NCCL(ncclAllGather(cnt, all, 2 * G, ncclUint64, c->comm, ctx->stream));
+  std::vector<unsigned long long> M(2 * G * G);
+  d2h_sync(ctx, M.data(), all, M.size() * 8);
+  auto sent = [&](int src, int rel, int dst) { return (uint64_t)M[(size_t)src * 2 * G + rel * G + dst]; };
+  uint64_t nrecv[2] = {0, 0};
+  for (int rel = 0; rel < 2; ++rel)
+    for (int p = 0; p < G; ++p) nrecv[rel] += sent(p, rel, me);
+  if (nrecv[0] >= (1ull << 32) || nrecv[1] >= (1ull << 32))
+    throw Error(GJ_EINVAL, "a rank would receive >= 2^32 tuples; use more ranks");
+  // grow every rank's capacity the same way on every rank (25% headroom)
+  bool grew = !c->mapped;
+  for (int p = 0; p < G; ++p)
+    for (int rel = 0; rel < 2; ++rel) {
+      uint64_t need = 0;
+      for (int q = 0; q < G; ++q) need += sent(q, rel, p);
+      if (need > c->cap[p][rel]) {
+        c->cap[p][rel] = need + need / 4 + 1024;
+        grew = true;
+      }
+    }
+  // IPC-exported buffers: their own workspace names (only this path resizes them)
+  void* bufs[4] = {ws(ctx, "ipc.R.key", c->cap[me][0] * ks + 16), ws(ctx, "ipc.R.rid", c->cap[me][0] * 4 + 16),
+                   ws(ctx, "ipc.S.key", c->cap[me][1] * ks + 16), ws(ctx, "ipc.S.rid", c->cap[me][1] * 4 + 16)};
+  if (grew) {
+    // exchange the IPC handles of everyone's receive buffers (all ranks take this branch together)
+    cudaIpcMemHandle_t mine[4];
+    for (int b = 0; b < 4; ++b) GJ_CUDA(cudaIpcGetMemHandle(&mine[b], bufs[b]));
+    uint8_t* hdev = static_cast<uint8_t*>(ws(ctx, "dist.ipc", (size_t)(G + 1) * sizeof(mine)));
+    GJ_CUDA(cudaMemcpyAsync(hdev, mine, sizeof(mine), cudaMemcpyHostToDevice, ctx->stream));
+    GJ_NCCL(ncclAllGather(hdev, hdev + sizeof(mine), sizeof(mine), ncclUint8, c->comm, ctx->stream));
+    std::vector<cudaIpcMemHandle_t> hall((size_t)G * 4);
+    const size_t total = (size_t)G * sizeof(mine);
+    for (size_t o = 0; o < total; o += 4096)  // d2h_sync moves <= 4 KB per call
+      d2h_sync(ctx, reinterpret_cast<uint8_t*>(hall.data()) + o, hdev + sizeof(mine) + o,
+               std::min<size_t>(4096, total - o));
+    for (int p = 0; p < G; ++p) {
+      if (p == me) continue;
+      for (int b = 0; b < 4; ++b) {
+        const cudaIpcMemHandle_t& h = hall[(size_t)p * 4 + b];
+        if (c->peer_ptr[p][b] && std::memcmp(&h, &c->peer_h[p][b], sizeof(h)) == 0) continue;
+        if (c->peer_ptr[p][b]) cudaIpcCloseMemHandle(c->peer_ptr[p][b]);
+        c->peer_ptr[p][b] = nullptr;
+        GJ_CUDA(cudaIpcOpenMemHandle(&c->peer_ptr[p][b], h, cudaIpcMemLazyEnablePeerAccess));
+        c->peer_h[p][b] = h;
+      }
+    }
+    c->mapped = true;
+  }
+  // where my run for rank p lands in p's buffers, and where it starts in my digit order
+  for (int rel = 0; rel < 2; ++rel) {
+    ShuffleDest dst{};
+    uint64_t base = 0;
+    for (int p = 0; p < G; ++p) {
+      uint64_t at = 0;
+      for (int q = 0; q < me; ++q) at += sent(q, rel, p);
+      uint8_t* kb = p == me ? static_cast<uint8_t*>(bufs[2 * rel]) : static_cast<uint8_t*>(c->peer_ptr[p][2 * rel]);
+      uint32_t* rb = p == me ? static_cast<uint32_t*>(bufs[2 * rel + 1])
+                             : static_cast<uint32_t*>(c->peer_ptr[p][2 * rel + 1]);
+      dst.key[p] = kb + at * ks;
+      dst.rid[p] = rb + at;
+      dst.base[p] = (uint32_t)base;
+      base += sent(me, rel, p);
+    }
+    shuffle_scatter(ctx, rel ? S : R, SP[rel], dst);
+  }
+  trace_sync(ctx, "fused: scatter");
+  // every rank's NVLink stores are done before any local join reads its buffers
+  {
+    RegionScope rs(ctx, "shuffle_barrier");
+    GJ_NCCL(ncclAllReduce(cnt + 2 * G + 2 * G * G, cnt + 2 * G + 2 * G * G + 1, 1, ncclUint64, ncclSum, c->comm,
+                          ctx->stream));
+  }
+  trace_sync(ctx, "fused: barrier");
+  gj_rel RL{bufs[0], static_cast<const uint32_t*>(bufs[1]), nrecv[0], R.key_type, 0};
+  gj_rel SL{bufs[2], static_cast<const uint32_t*>(bufs[3]), nrecv[1], S.key_type, 0};
+  join_count_core(ctx, RL, SL, g);
+  trace_sync(ctx, "fused: local join count");
+}
+
+void equi_count_any(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) {
+  const char* env = std::getenv("GJ_SHUFFLE");  // "nccl" forces the send/recv path
+  const bool fused = c->fused && !(env && std::string(env) == "nccl") && c->nranks > 1 && c->nranks <= MAX_RANKS;
+  if (fused) dist_equi_count_fused(ctx, c, R, S);
+  else dist_equi_count(ctx, c, R, S);
+}
+
 void dist_theta_count(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S, int op, uint64_t eps) {
   const int G = c->nranks;
   const size_t ks = R.key_type == GJ_I64 ? 8 : 4;
@@ -288,6 +400,9 @@ gj_status gj_comm_init(gj_comm** out, const void* id, int nranks, int rank) {
 
 void gj_comm_destroy(gj_comm* c) {
   if (!c) return;
+  for (int p = 0; p < gj::MAX_RANKS; ++p)
+    for (int b = 0; b < 4; ++b)
+      if (c->peer_ptr[p][b]) cudaIpcCloseMemHandle(c->peer_ptr[p][b]);
   if (c->comm) ncclCommDestroy(c->comm);
   delete c;
 }
@@ -305,13 +420,15 @@ gj_status join_dist_count(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, uint64_t*
   check_args(ctx, c, R, S);
   if (!n_local || !n_global) throw Error(GJ_EINVAL, "NULL result pointer");
   c->eq_valid = false;
-  dist_equi_count(ctx, c, R, S);
+  trace_mark("join_dist_count begin");
+  equi_count_any(ctx, c, R, S);
   c->R = R;
   c->S = S;
   c->total = ctx->jc.total;
   c->eq_valid = true;
   *n_local = ctx->jc.total;
   *n_global = allreduce_sum(ctx, c, ctx->jc.total);
+  trace_mark("join_dist_count end");
   DAPI_END
 }
 
@@ -321,7 +438,7 @@ gj_status join_dist_materialize(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, uin
   check_args(ctx, c, R, S);
   if (!n_written) throw Error(GJ_EINVAL, "NULL n_written");
   if (!(c->eq_valid && same_rel(c->R, R) && same_rel(c->S, S) && ctx->jc.valid)) {
-    dist_equi_count(ctx, c, R, S);
+    equi_count_any(ctx, c, R, S);
     c->R = R;
     c->S = S;
     c->eq_valid = true;

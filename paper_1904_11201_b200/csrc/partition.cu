@@ -221,12 +221,16 @@ __device__ __forceinline__ void issue_tile(ScatterSmem<K, HAS_RID>& sm, uint32_t
     bulk_g2s(sm.rid[buf], reinterpret_cast<const uint8_t*>(rid_in) + ra, (uint32_t)(rz - ra), &sm.bar[buf]);
 }
 
-template <typename K, bool HAS_RID>
+// REMOTE (multi-GPU shuffle fused into the scatter): digit d = destination rank;
+// its run is written straight into rank d's receive buffers (peer pointers mapped
+// over NVLink through CUDA IPC) at key[d] / rid[d] + (position - base[d]), base[d]
+// being the run's start in this rank's digit order.
+template <typename K, bool HAS_RID, bool REMOTE>
 __global__ void __launch_bounds__(PT) part_scatter(
     const K* __restrict__ key_in, const uint32_t* __restrict__ rid_in, uint32_t rid_base, uint64_t n,
     const uint4* __restrict__ tdesc, uint32_t ntiles, uint32_t shift, uint32_t bits,
     const uint32_t* __restrict__ scanned, const uint32_t* __restrict__ tile_pref, K* __restrict__ key_out,
-    uint32_t* __restrict__ rid_out) {
+    uint32_t* __restrict__ rid_out, ShuffleDest dst) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   ScatterSmem<K, HAS_RID>& sm = *reinterpret_cast<ScatterSmem<K, HAS_RID>*>(smem_raw);
   const uint32_t D = 1u << bits, mask = D - 1;
@@ -336,9 +340,16 @@ __global__ void __launch_bounds__(PT) part_scatter(
         const uint32_t j = i * PT + threadIdx.x;
         if (j < cnt) {
           const K kk = skey[j];
-          const uint32_t pos = sm.delta[digit_of(kk, shift, mask)] + j;
-          key_out[pos] = kk;
-          rid_out[pos] = srid[j];
+          const uint32_t dg = digit_of(kk, shift, mask);
+          const uint32_t pos = sm.delta[dg] + j;
+          if (REMOTE) {
+            const uint32_t idx = pos - dst.base[dg];
+            static_cast<K*>(dst.key[dg])[idx] = kk;
+            dst.rid[dg][idx] = srid[j];
+          } else {
+            key_out[pos] = kk;
+            rid_out[pos] = srid[j];
+          }
         }
       }
     } else {
@@ -346,6 +357,33 @@ __global__ void __launch_bounds__(PT) part_scatter(
     }
     __syncthreads();  // the buffer may be refilled by the next iteration's issue
   }
+  if (REMOTE) __threadfence_system();  // peer writes performed before the kernel retires
+}
+
+template <typename K, bool HAS_RID, bool REMOTE>
+void launch_scatter_t(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
+                      const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* hist,
+                      const uint32_t* tile_pref, K* kout, uint32_t* rout, const ShuffleDest& dst) {
+  const size_t smem = sizeof(ScatterSmem<K, HAS_RID>);
+  static bool once = (set_smem(part_scatter<K, HAS_RID, REMOTE>, smem), true);
+  (void)once;
+  int occ = 1;
+  GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, part_scatter<K, HAS_RID, REMOTE>, PT, smem));
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
+  launch(ctx, REMOTE ? "shuffle_scatter" : "part_scatter", part_scatter<K, HAS_RID, REMOTE>, dim3(grid), dim3(PT),
+         smem, kin, rin, rid_base, n, tdesc, (uint32_t)ntiles, shift, bits, hist, tile_pref, kout, rout, dst);
+}
+
+template <typename K, bool REMOTE>
+void launch_scatter(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
+                    const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* hist,
+                    const uint32_t* tile_pref, K* kout, uint32_t* rout, const ShuffleDest& dst) {
+  if (rin)
+    launch_scatter_t<K, true, REMOTE>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, hist, tile_pref, kout,
+                                      rout, dst);
+  else
+    launch_scatter_t<K, false, REMOTE>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, hist, tile_pref,
+                                       kout, rout, dst);
 }
 
 __global__ void seg_chunks(const uint32_t* __restrict__ seg_off, uint32_t nseg, uint32_t* __restrict__ nc) {
@@ -422,27 +460,8 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
     uint4* tdesc = static_cast<uint4*>(ws(ctx, "part.tdesc", (ntiles + 1) * sizeof(uint4)));
     launch(ctx, "tile_desc", tile_desc_kernel, dim3((unsigned)((ntiles + 255) / 256)), dim3(256), 0, n, seg_off,
            (const uint32_t*)chunk_base, nseg, D, (uint32_t)ntiles, tdesc);
-    if (rin) {
-      const size_t smem = sizeof(ScatterSmem<K, true>);
-      static bool once = (set_smem(part_scatter<K, true>, smem), true);
-      (void)once;
-      int occ = 1;
-      GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, part_scatter<K, true>, PT, smem));
-      const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
-      launch(ctx, "part_scatter", part_scatter<K, true>, dim3(grid), dim3(PT), smem, kin, rin, X.rid_base, n,
-             (const uint4*)tdesc, (uint32_t)ntiles, shift, bits, (const uint32_t*)hist, (const uint32_t*)tile_pref,
-             kout, rout);
-    } else {
-      const size_t smem = sizeof(ScatterSmem<K, false>);
-      static bool once = (set_smem(part_scatter<K, false>, smem), true);
-      (void)once;
-      int occ = 1;
-      GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, part_scatter<K, false>, PT, smem));
-      const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
-      launch(ctx, "part_scatter", part_scatter<K, false>, dim3(grid), dim3(PT), smem, kin, rin, X.rid_base, n,
-             (const uint4*)tdesc, (uint32_t)ntiles, shift, bits, (const uint32_t*)hist, (const uint32_t*)tile_pref,
-             kout, rout);
-    }
+    launch_scatter<K, false>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, hist, tile_pref, kout, rout,
+                             ShuffleDest{});
     const uint32_t P = nseg << bits;
     uint32_t* off = static_cast<uint32_t*>(ws(ctx, (ps + ".off").c_str(), (P + 1) * sizeof(uint32_t)));
     launch(ctx, "extract_off", extract_off, dim3((P + 1 + 255) / 256), dim3(256), 0, (const uint32_t*)hist,
@@ -459,6 +478,42 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
   return out;
 }
 
+template <typename K>
+ShufflePass shuffle_prepare_impl(gj_ctx* ctx, const gj_rel& X, uint32_t g, const char* tag) {
+  std::string t(tag);
+  ShufflePass sp;
+  sp.g = g;
+  const uint64_t n = X.n;
+  const uint32_t D = 1u << g;
+  if (n == 0) {  // nothing to send: all runs empty
+    uint32_t* off = static_cast<uint32_t*>(ws(ctx, (t + ".soff").c_str(), (D + 1) * sizeof(uint32_t)));
+    GJ_CUDA(cudaMemsetAsync(off, 0, (D + 1) * sizeof(uint32_t), ctx->stream));
+    sp.off = off;
+    return sp;
+  }
+  const uint64_t max_chunks = (n + CHUNK - 1) / CHUNK;
+  const uint64_t hn = max_chunks * D;
+  uint32_t* hist = static_cast<uint32_t*>(ws(ctx, (t + ".shist").c_str(), (hn + 1) * sizeof(uint32_t)));
+  sp.ntiles = max_chunks * TPC;
+  uint32_t* tile_pref = static_cast<uint32_t*>(ws(ctx, (t + ".stp").c_str(), sp.ntiles * D * sizeof(uint32_t) + 4));
+  const uint32_t shift = 32 - g;
+  launch(ctx, "part_hist", part_hist<K>, dim3((unsigned)std::max<uint64_t>(max_chunks, 1)), dim3(PT), 0,
+         static_cast<const K*>(X.key), n, (const uint32_t*)nullptr, (const uint32_t*)nullptr, 1u, shift, g, hist,
+         tile_pref);
+  exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
+  uint4* tdesc = static_cast<uint4*>(ws(ctx, (t + ".stdesc").c_str(), (sp.ntiles + 1) * sizeof(uint4)));
+  launch(ctx, "tile_desc", tile_desc_kernel, dim3((unsigned)((sp.ntiles + 255) / 256)), dim3(256), 0, n,
+         (const uint32_t*)nullptr, (const uint32_t*)nullptr, 1u, D, (uint32_t)sp.ntiles, tdesc);
+  uint32_t* off = static_cast<uint32_t*>(ws(ctx, (t + ".soff").c_str(), (D + 1) * sizeof(uint32_t)));
+  launch(ctx, "extract_off", extract_off, dim3(1), dim3(256), 0, (const uint32_t*)hist, (const uint32_t*)nullptr,
+         (const uint32_t*)nullptr, 1u, g, n, off);
+  sp.hist = hist;
+  sp.tile_pref = tile_pref;
+  sp.tdesc = tdesc;
+  sp.off = off;
+  return sp;
+}
+
 }  // namespace
 
 int radix_passes(uint32_t B) { return B == 0 ? 0 : (int)((B + MAX_BITS - 1) / MAX_BITS); }
@@ -466,6 +521,21 @@ int radix_passes(uint32_t B) { return B == 0 ? 0 : (int)((B + MAX_BITS - 1) / MA
 Partitioned radix_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char* tag, uint32_t skip) {
   if (X.key_type == GJ_I32) return partition_impl<int32_t>(ctx, X, B, tag, skip);
   return partition_impl<int64_t>(ctx, X, B, tag, skip);
+}
+
+ShufflePass shuffle_prepare(gj_ctx* ctx, const gj_rel& X, uint32_t g, const char* tag) {
+  if (X.key_type == GJ_I32) return shuffle_prepare_impl<int32_t>(ctx, X, g, tag);
+  return shuffle_prepare_impl<int64_t>(ctx, X, g, tag);
+}
+
+void shuffle_scatter(gj_ctx* ctx, const gj_rel& X, const ShufflePass& sp, const ShuffleDest& dst) {
+  if (X.n == 0) return;
+  if (X.key_type == GJ_I32)
+    launch_scatter<int32_t, true>(ctx, static_cast<const int32_t*>(X.key), X.rid, X.rid_base, X.n, sp.tdesc, sp.ntiles,
+                                  32 - sp.g, sp.g, sp.hist, sp.tile_pref, nullptr, nullptr, dst);
+  else
+    launch_scatter<int64_t, true>(ctx, static_cast<const int64_t*>(X.key), X.rid, X.rid_base, X.n, sp.tdesc, sp.ntiles,
+                                  32 - sp.g, sp.g, sp.hist, sp.tile_pref, nullptr, nullptr, dst);
 }
 
 }  // namespace gj

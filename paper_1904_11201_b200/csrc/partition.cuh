@@ -26,4 +26,24 @@ int radix_passes(uint32_t B);
 // the partition digits are bits [32-skip-B, 32-skip) of khash.
 Partitioned radix_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char* tag, uint32_t skip = 0);
 
+// ---- multi-GPU shuffle fused into the partition scatter
+constexpr int MAX_RANKS = 8;
+struct ShuffleDest {
+  void* key[MAX_RANKS];       // destination key pointer per rank (peer memory via IPC)
+  uint32_t* rid[MAX_RANKS];   // destination rid pointer per rank
+  uint32_t base[MAX_RANKS];   // start of the rank's run in this relation's local digit order
+};
+struct ShufflePass {
+  uint32_t g = 0;
+  uint64_t ntiles = 0;
+  const uint32_t* hist = nullptr;
+  const uint32_t* tile_pref = nullptr;
+  const uint4* tdesc = nullptr;
+  const uint32_t* off = nullptr;  // device, 2^g + 1 run starts (local digit order)
+};
+// Histogram + scan for a one-pass partition of X by the top g hash bits.
+ShufflePass shuffle_prepare(gj_ctx* ctx, const gj_rel& X, uint32_t g, const char* tag);
+// The scatter of that pass, writing run d to dst.key[d] / dst.rid[d].
+void shuffle_scatter(gj_ctx* ctx, const gj_rel& X, const ShufflePass& sp, const ShuffleDest& dst);
+
 }  // namespace gj

@@ -119,6 +119,10 @@ struct LaunchScope {
   ~LaunchScope() noexcept(false);
 };
 
+// Host-side phase trace (env GJ_TRACE=1): wall-clock ms since the previous mark, to stderr.
+void trace_mark(const char* label);
+void trace_sync(gj_ctx* ctx, const char* label);  // GJ_TRACE=2: stream sync first
+
 // Times a non-kernel stream region (e.g. an NCCL exchange) under GJ_OPT_PROFILE;
 // not counted as a kernel launch.
 struct RegionScope {

@@ -22,9 +22,11 @@ a bounded PK-FK sample on this host, 1 thread.
 --impl reference: this tier has no runnable reference implementation; the
 reference arm is the oracle itself, timed the same way on the host cores.
 
-N > 1 (torchrun): weak scaling -- every rank runs the same-size problem on its own
-GPU (the equi join shards by hash partition; the NCCL shuffle path is
-`join_dist_*`, measured separately once available).
+N > 1 (torchrun): weak scaling -- every rank holds a same-size shard of one global
+join.  Equi (c2): join_dist_count/materialize = a hash shuffle by the top log2(N)
+hash bits fused into the first radix scatter (NVLink peer stores),
+then the local partitioned hash join.  Band (c4): R all-gathered over NCCL, local
+NLJ against the rank's S shard.
 """
 from __future__ import annotations
 
@@ -39,6 +41,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+S_BITS_C4 = 24  # set from --c4-s-bits
 METRIC = "join input & output tuples/s at 1/2/4/8 B200; % of HBM/INT roofline"
 
 
@@ -167,10 +170,10 @@ def make_workload(name, device, rank=0, world=1):
         return dict(kind="equi", R=R, S=S, desc="configs[0]: R=S=10^4 uniform keys in [0,10^4), equi hash join")
     if name == "c4":
         nr = (1 << 20) // world  # R (2^20) is block-sharded and replicated by the join
-        ns = 1 << 24             # per GPU
+        ns = 1 << S_BITS_C4      # per GPU (2^24 = configs[3]; smaller only for ncu captures)
         R = gd.uniform(nr, 1 << 30, seed, 0, offset=rank * nr, device=device)
         S = gd.uniform(ns, 1 << 30, seed, 1, offset=rank * ns, device=device)
-        desc = "configs[3]: band join |R.a-S.b|<=53687, 2^20 x 2^24 uniform int32 in [0,2^30), count+scan+write"
+        desc = f"configs[3]: band join |R.a-S.b|<=53687, 2^20 x 2^{S_BITS_C4} uniform int32 in [0,2^30), count+scan+write"
         if world > 1:
             desc += f"; weak scaling: R (2^20) all-gathered, {world} x 2^24 S shards"
         return dict(kind="band", R=R, S=S, eps=gen.C4_EPS, desc=desc, rid_base_R=rank * nr, rid_base=rank * ns)
@@ -333,7 +336,7 @@ def run_ours(args, world, rank, local):
                 res = gj.join_dist_materialize(ctx, comm, eR, eS, m, out=out)
                 hout[:m].copy_(res)
                 return m
-            note = "per rank: pinned H2D of its shards -> join_dist_count/materialize (NCCL shuffle) -> D2H of its pairs"
+            note = "per rank: pinned H2D of its shards -> join_dist_count/materialize (hash shuffle over NVLink peer stores) -> D2H of its pairs"
         e2e_step()
         torch.cuda.synchronize()
         barrier(world)
@@ -399,8 +402,11 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample-bits", type=int, default=23)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--c4-s-bits", type=int, default=24, help="log2 |S| per GPU for c4 (24 = configs[3]; ncu only)")
     ap.add_argument("--opt", action="append", default=[], help="ctx option name=value (tuning sweeps)")
     args = ap.parse_args()
+    global S_BITS_C4
+    S_BITS_C4 = args.c4_s_bits
     world, rank, local = dist_setup(args)
 
     if args.impl == "reference":

@@ -96,7 +96,10 @@ const char* gj_last_error(void);
  *  GJ_OPT_PROFILE          1 = bracket every kernel with CUDA events (per-kernel times)
  *  GJ_OPT_NLJ_SPLIT        S-range splits per R tile for the NLJ (0 = auto)
  *  GJ_OPT_FORCE_SLOW_BAND  1 = always use the 64-bit band path (tests)
- *  GJ_OPT_BUILD_SIDE       0 = smaller side (default), 1 = always R, 2 = always S */
+ *  GJ_OPT_BUILD_SIDE       0 = smaller side (default), 1 = always R, 2 = always S
+ *  GJ_OPT_SHUFFLE_BITS     multi-GPU equi join: local radix bits folded into the NVLink
+ *                          shuffle pass (0 = destination rank only, the default; at most
+ *                          9 - log2(#ranks); must be equal on every rank) */
 enum {
   GJ_OPT_PART_BITS = 1,
   GJ_OPT_BUILD_CHUNK = 2,
@@ -104,7 +107,8 @@ enum {
   GJ_OPT_PROFILE = 4,
   GJ_OPT_NLJ_SPLIT = 5,
   GJ_OPT_FORCE_SLOW_BAND = 6,
-  GJ_OPT_BUILD_SIDE = 7
+  GJ_OPT_BUILD_SIDE = 7,
+  GJ_OPT_SHUFFLE_BITS = 8
 };
 gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t value);
 

@@ -47,13 +47,29 @@ void* ws(gj_ctx* ctx, const char* name, size_t bytes) {
   return b.ptr;
 }
 
+void* pinned(gj_ctx* ctx, const char* name, size_t bytes) {
+  Buf& b = ctx->pinned_bufs[name];
+  if (b.bytes < bytes) {
+    if (b.ptr) {
+      GJ_CUDA(cudaStreamSynchronize(ctx->stream));
+      GJ_CUDA(cudaFreeHost(b.ptr));
+      b.ptr = nullptr;
+      b.bytes = 0;
+    }
+    const size_t want = std::max<size_t>(4096, (bytes + 4095) & ~size_t(4095));
+    GJ_CUDA(cudaMallocHost(&b.ptr, want));
+    b.bytes = want;
+  }
+  return b.ptr;
+}
+
 void d2h_sync(gj_ctx* ctx, void* host, const void* dev, size_t bytes) {
-  if (bytes > 4096) throw Error(GJ_EINVAL, "d2h_sync: too large");
-  GJ_CUDA(cudaMemcpyAsync(ctx->host_pinned, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  void* hp = pinned(ctx, "d2h", bytes);
+  GJ_CUDA(cudaMemcpyAsync(hp, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   trace_mark("d2h_sync enqueue");
   GJ_CUDA(cudaStreamSynchronize(ctx->stream));
   trace_mark("d2h_sync done");
-  std::memcpy(host, ctx->host_pinned, bytes);
+  std::memcpy(host, hp, bytes);
 }
 
 static cudaEvent_t get_event(gj_ctx* ctx) {
@@ -156,7 +172,7 @@ static bool same_rel(const gj_rel& a, const gj_rel& b) {
   return a.key == b.key && a.rid == b.rid && a.n == b.n && a.key_type == b.key_type && a.rid_base == b.rid_base;
 }
 
-static uint32_t auto_bits(gj_ctx* ctx, uint64_t nb) {
+uint32_t auto_bits(gj_ctx* ctx, uint64_t nb) {
   if (ctx->part_bits >= 0) return (uint32_t)ctx->part_bits;
   const uint64_t target = ctx->build_chunk / 2;  // mean build tuples per partition
   uint32_t B = 0;
@@ -167,7 +183,11 @@ static uint32_t auto_bits(gj_ctx* ctx, uint64_t nb) {
 // Single-GPU equi-join count: partition both relations with the same radix bits
 // (skipping the top `skip` hash bits a multi-GPU shuffle already consumed), then
 // count per partition.  Leaves everything the write pass needs in ctx->jc.
-void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t skip) {
+// b0 > 0: R and S arrive already grouped by the b0 hash bits below the skipped
+// ones (segment offsets segR / segS, 2^b0 + 1 entries each, device), as the fused
+// multi-GPU shuffle delivers them; only the remaining bits are partitioned here.
+void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t skip, uint32_t b0,
+                     const uint32_t* segR, const uint32_t* segS) {
   JoinCache& jc = ctx->jc;
   jc = JoinCache{};
   jc.R = R;
@@ -180,14 +200,16 @@ void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t ski
   // favouring R: near-equal sizes (e.g. a PK-FK join after a shuffle) must not flip
   // the build side to the duplicate-heavy FK relation on random size fluctuations.
   const bool swap = ctx->build_side == 2 || (ctx->build_side == 0 && S.n * 10 < R.n * 9);
-  const uint32_t B = std::min<uint32_t>(auto_bits(ctx, swap ? S.n : R.n), 32 - skip);
-  Partitioned PR = radix_partition(ctx, R, B, "R", skip);
-  Partitioned PS = radix_partition(ctx, S, B, "S", skip);
+  const uint32_t B = std::max(b0, std::min<uint32_t>(auto_bits(ctx, swap ? S.n : R.n), 32 - skip));
+  Partitioned PR = radix_partition(ctx, R, B - b0, "R", skip + b0, b0 ? segR : nullptr, 1u << b0);
+  Partitioned PS = radix_partition(ctx, S, B - b0, "S", skip + b0, b0 ? segS : nullptr, 1u << b0);
   hash_join_count(ctx, R, S, B, swap, PR, PS);
   jc.valid = true;
 }
 
-static void do_join_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S) { join_count_core(ctx, R, S, 0); }
+static void do_join_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S) {
+  join_count_core(ctx, R, S, 0, 0, nullptr, nullptr);
+}
 
 }  // namespace gj
 
@@ -220,7 +242,6 @@ gj_status gj_ctx_create(gj_ctx** out, int device, void* stream) {
   int sms = 0;
   GJ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   c->num_sms = sms;
-  GJ_CUDA(cudaMallocHost(&c->host_pinned, 4096));
   *out = c;
   API_END
 }
@@ -236,7 +257,8 @@ void gj_ctx_destroy(gj_ctx* ctx) {
   }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
   cudaStreamSynchronize(ctx->stream);
-  if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
+  for (auto& kv : ctx->pinned_bufs)
+    if (kv.second.ptr) cudaFreeHost(kv.second.ptr);
   delete ctx;
 }
 
@@ -269,6 +291,10 @@ gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t v) {
       ctx->nlj_split = (uint32_t)v;
       break;
     case GJ_OPT_FORCE_SLOW_BAND: ctx->force_slow_band = v != 0; break;
+    case GJ_OPT_SHUFFLE_BITS:
+      if (v < 0 || v > 9) throw Error(GJ_EINVAL, "shuffle_bits must be in [0, 9]");
+      ctx->shuffle_bits = (int)v;
+      break;
     case GJ_OPT_BUILD_SIDE:
       if (v < 0 || v > 2) throw Error(GJ_EINVAL, "build_side must be 0, 1 or 2");
       ctx->build_side = (int)v;

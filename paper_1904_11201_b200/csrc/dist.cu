@@ -14,6 +14,7 @@
 // one-region-per-rank case of the paper's region matrix.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -31,7 +32,9 @@
 #endif
 
 namespace gj {
-void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t skip);
+void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t skip, uint32_t b0,
+                     const uint32_t* segR, const uint32_t* segS);
+uint32_t auto_bits(gj_ctx* ctx, uint64_t nb);
 void set_last_error(const std::string& m);
 }  // namespace gj
 
@@ -48,6 +51,7 @@ struct gj_comm {
   // of the all-gathered count matrices, so all ranks agree when handles must be
   // re-exchanged without an extra collective
   uint64_t cap[gj::MAX_RANKS][2] = {};
+  size_t cap_ks = 0;  // key width the receive buffers were sized for
   bool mapped = false;
   bool fused = true;  // shuffle fused into the scatter over NVLink (else NCCL send/recv)
   // cache of the last dist count (for materialize)
@@ -73,6 +77,9 @@ namespace {
 __global__ void bucket_counts(const uint32_t* __restrict__ off, uint32_t G, unsigned long long* __restrict__ out) {
   const uint32_t p = threadIdx.x;
   if (p < G) out[p] = off[p + 1] - off[p];
+}
+__global__ void run_counts(const uint32_t* __restrict__ off, uint32_t D, uint32_t* __restrict__ out) {
+  for (uint32_t d = threadIdx.x; d < D; d += blockDim.x) out[d] = off[d + 1] - off[d];
 }
 __global__ void fill_rids(uint32_t* __restrict__ out, uint64_t n, uint32_t base) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
@@ -137,8 +144,12 @@ void dist_equi_count(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) 
       s += sent(c->rank, rel, p);
     }
   }
-  if (nrecv[0] >= (1ull << 32) || nrecv[1] >= (1ull << 32))
-    throw Error(GJ_EINVAL, "a rank would receive >= 2^32 tuples; use more ranks");
+  for (int p = 0; p < G; ++p) {  // checked for every rank so that all ranks fail together
+    uint64_t in[2] = {0, 0};
+    for (int q = 0; q < G; ++q) in[0] += sent(q, 0, p), in[1] += sent(q, 1, p);
+    if (in[0] >= (1ull << 32) || in[1] >= (1ull << 32))
+      throw Error(GJ_EINVAL, "a rank would receive >= 2^32 tuples; use more ranks");
+  }
   // 3. all-to-all-v of the (key, rid) buckets
   uint8_t* rk[2] = {static_cast<uint8_t*>(ws(ctx, "dist.R.key", nrecv[0] * ks)),
                     static_cast<uint8_t*>(ws(ctx, "dist.S.key", nrecv[1] * ks))};
@@ -192,44 +203,69 @@ void dist_equi_count(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) 
   }
   // 4. local partitioned hash join of what arrived (top g hash bits are now constant)
   gj_rel RL{rk[0], rr[0], nrecv[0], R.key_type, 0}, SL{rk[1], rr[1], nrecv[1], S.key_type, 0};
-  join_count_core(ctx, RL, SL, g);
+  join_count_core(ctx, RL, SL, g, 0, nullptr, nullptr);
 }
 
 // Fused shuffle: radix histogram by destination rank, count-matrix all-gather,
 // then ONE scatter kernel per relation that writes every destination's run straight
 // into that rank's receive buffers through CUDA-IPC peer pointers (NVLink stores),
 // then a stream-ordered barrier (tiny all-reduce) before the local join reads them.
+// Fused shuffle: ONE radix pass by (destination rank, first local digit) -- the top
+// g + b1 hash bits -- whose scatter stores every tuple straight into the receiving
+// rank's buffers over NVLink (CUDA-IPC mappings).  Receivers lay their buffers out
+// digit-major (for each local digit: the senders' runs in rank order), so what
+// arrives is already radix-partitioned by b1 bits and the local join only applies
+// the remaining ones.  Order inside a partition: sender rank, then sender order.
 void dist_equi_count_fused(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) {
   const int G = c->nranks, me = c->rank;
   const uint32_t g = log2_exact(G);
   const size_t ks = R.key_type == GJ_I64 ? 8 : 4;
+  // b1 must be the same on every rank: it depends only on G and the ctx options.
+  // Default 0: with 512 digits the NVLink stores come in ~8-tuple runs and the
+  // shuffle scatter measured 3.1 ms vs 1.2 ms for 2 digits (2^27 tuples, N=2) --
+  // more than the local radix pass it saves.
+  uint32_t b1 = std::min<uint32_t>((uint32_t)ctx->shuffle_bits, 9 - g);
+  if (ctx->part_bits >= 0) b1 = std::min<uint32_t>(b1, (uint32_t)ctx->part_bits);
+  const uint32_t G1 = g + b1, D1 = 1u << G1, L1 = 1u << b1;
   trace_sync(ctx, "fused: start");
-  ShufflePass SP[2] = {shuffle_prepare(ctx, R, g, "sR"), shuffle_prepare(ctx, S, g, "sS")};
+  ShufflePass SP[2] = {shuffle_prepare(ctx, R, G1, "sR"), shuffle_prepare(ctx, S, G1, "sS")};
   trace_sync(ctx, "fused: shuffle hist");
-  unsigned long long* cnt = static_cast<unsigned long long*>(ws(ctx, "dist.cnt", (2 * G + 2 * G * G + 2) * 8));
-  unsigned long long* all = cnt + 2 * G;
-  launch(ctx, "bucket_counts", bucket_counts, dim3(1), dim3(32), 0, SP[0].off, (uint32_t)G, cnt);
-  launch(ctx, "bucket_counts", bucket_counts, dim3(1), dim3(32), 0, SP[1].off, (uint32_t)G, cnt + G);
-  GJ_NCCL(ncclAllGather(cnt, all, 2 * G, ncclUint64, c->comm, ctx->stream));
-  std::vector<unsigned long long> M(2 * G * G);
-  d2h_sync(ctx, M.data(), all, M.size() * 8);
-  auto sent = [&](int src, int rel, int dst) { return (uint64_t)M[(size_t)src * 2 * G + rel * G + dst]; };
-  uint64_t nrecv[2] = {0, 0};
-  for (int rel = 0; rel < 2; ++rel)
-    for (int p = 0; p < G; ++p) nrecv[rel] += sent(p, rel, me);
-  if (nrecv[0] >= (1ull << 32) || nrecv[1] >= (1ull << 32))
-    throw Error(GJ_EINVAL, "a rank would receive >= 2^32 tuples; use more ranks");
-  // grow every rank's capacity the same way on every rank (25% headroom)
-  bool grew = !c->mapped;
+  // per rank: 2 x D1 run counts + its key width (all ranks must agree on it)
+  const size_t row = 2 * (size_t)D1 + 1;
+  uint32_t* cnt = static_cast<uint32_t*>(ws(ctx, "dist.cnt", (row * (G + 1) + 2) * 4));
+  uint32_t* all = cnt + row;
+  launch(ctx, "run_counts", run_counts, dim3(1), dim3(256), 0, SP[0].off, D1, cnt);
+  launch(ctx, "run_counts", run_counts, dim3(1), dim3(256), 0, SP[1].off, D1, cnt + D1);
+  const uint32_t ks32 = (uint32_t)ks;
+  GJ_CUDA(cudaMemcpyAsync(cnt + 2 * D1, &ks32, 4, cudaMemcpyHostToDevice, ctx->stream));
+  GJ_NCCL(ncclAllGather(cnt, all, row, ncclUint32, c->comm, ctx->stream));
+  std::vector<uint32_t> M((size_t)G * row);
+  d2h_sync(ctx, M.data(), all, M.size() * 4);
+  for (int q = 0; q < G; ++q)
+    if (M[(size_t)q * row + 2 * D1] != ks32) throw Error(GJ_EINVAL, "ranks disagree on the key type");
+  // cnt(q, rel, p, d): tuples of relation rel that rank q sends to rank p, local digit d
+  auto cntq = [&](int q, int rel, int p, uint32_t d) -> uint64_t {
+    return M[(size_t)q * row + (size_t)rel * D1 + ((size_t)p << b1) + d];
+  };
+  uint64_t need[MAX_RANKS][2] = {};
+  for (int q = 0; q < G; ++q)
+    for (int rel = 0; rel < 2; ++rel)
+      for (int p = 0; p < G; ++p)
+        for (uint32_t d = 0; d < L1; ++d) need[p][rel] += cntq(q, rel, p, d);
+  const uint64_t nrecv[2] = {need[me][0], need[me][1]};
+  for (int p = 0; p < G; ++p)  // every rank sees the whole matrix: all ranks fail together
+    if (need[p][0] >= (1ull << 32) || need[p][1] >= (1ull << 32))
+      throw Error(GJ_EINVAL, "a rank would receive >= 2^32 tuples; use more ranks");
+  // grow every rank's capacity the same way on every rank (25% headroom); a new key
+  // width reallocates the key buffers, so it also forces a handle exchange
+  bool grew = !c->mapped || c->cap_ks != ks;
+  c->cap_ks = ks;
   for (int p = 0; p < G; ++p)
-    for (int rel = 0; rel < 2; ++rel) {
-      uint64_t need = 0;
-      for (int q = 0; q < G; ++q) need += sent(q, rel, p);
-      if (need > c->cap[p][rel]) {
-        c->cap[p][rel] = need + need / 4 + 1024;
+    for (int rel = 0; rel < 2; ++rel)
+      if (need[p][rel] > c->cap[p][rel]) {
+        c->cap[p][rel] = need[p][rel] + need[p][rel] / 4 + 1024;
         grew = true;
       }
-    }
   // IPC-exported buffers: their own workspace names (only this path resizes them)
   void* bufs[4] = {ws(ctx, "ipc.R.key", c->cap[me][0] * ks + 16), ws(ctx, "ipc.R.rid", c->cap[me][0] * 4 + 16),
                    ws(ctx, "ipc.S.key", c->cap[me][1] * ks + 16), ws(ctx, "ipc.S.rid", c->cap[me][1] * 4 + 16)};
@@ -241,10 +277,7 @@ void dist_equi_count_fused(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_re
     GJ_CUDA(cudaMemcpyAsync(hdev, mine, sizeof(mine), cudaMemcpyHostToDevice, ctx->stream));
     GJ_NCCL(ncclAllGather(hdev, hdev + sizeof(mine), sizeof(mine), ncclUint8, c->comm, ctx->stream));
     std::vector<cudaIpcMemHandle_t> hall((size_t)G * 4);
-    const size_t total = (size_t)G * sizeof(mine);
-    for (size_t o = 0; o < total; o += 4096)  // d2h_sync moves <= 4 KB per call
-      d2h_sync(ctx, reinterpret_cast<uint8_t*>(hall.data()) + o, hdev + sizeof(mine) + o,
-               std::min<size_t>(4096, total - o));
+    d2h_sync(ctx, hall.data(), hdev + sizeof(mine), (size_t)G * sizeof(mine));
     for (int p = 0; p < G; ++p) {
       if (p == me) continue;
       for (int b = 0; b < 4; ++b) {
@@ -258,34 +291,51 @@ void dist_equi_count_fused(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_re
     }
     c->mapped = true;
   }
-  // where my run for rank p lands in p's buffers, and where it starts in my digit order
+  // Per relation: adj[dg] = (index of my run dg in its receiver's buffer) - (its start
+  // in my digit order), and seg[d] = start of local digit d in MY receive buffer.
+  const size_t tab_n = 2 * (size_t)D1 + 2 * (size_t)(L1 + 1);
+  uint32_t* htab = static_cast<uint32_t*>(pinned(ctx, "dist.tab", tab_n * 4));
+  for (int rel = 0; rel < 2; ++rel) {
+    uint32_t* adj = htab + (size_t)rel * D1;
+    uint32_t* seg = htab + 2 * (size_t)D1 + (size_t)rel * (L1 + 1);
+    uint64_t local = 0;
+    for (int p = 0; p < G; ++p) {
+      uint64_t at = 0;  // start of digit d in rank p's receive buffer
+      for (uint32_t d = 0; d < L1; ++d) {
+        uint64_t mine_at = at;
+        for (int q = 0; q < me; ++q) mine_at += cntq(q, rel, p, d);
+        adj[((size_t)p << b1) + d] = (uint32_t)(mine_at - local);
+        if (p == me) seg[d] = (uint32_t)at;
+        for (int q = 0; q < G; ++q) at += cntq(q, rel, p, d);
+        local += cntq(me, rel, p, d);
+      }
+      if (p == me) seg[L1] = (uint32_t)at;
+    }
+  }
+  uint32_t* dtab = static_cast<uint32_t*>(ws(ctx, "dist.tab", tab_n * 4));
+  GJ_CUDA(cudaMemcpyAsync(dtab, htab, tab_n * 4, cudaMemcpyHostToDevice, ctx->stream));
   for (int rel = 0; rel < 2; ++rel) {
     ShuffleDest dst{};
-    uint64_t base = 0;
     for (int p = 0; p < G; ++p) {
-      uint64_t at = 0;
-      for (int q = 0; q < me; ++q) at += sent(q, rel, p);
-      uint8_t* kb = p == me ? static_cast<uint8_t*>(bufs[2 * rel]) : static_cast<uint8_t*>(c->peer_ptr[p][2 * rel]);
-      uint32_t* rb = p == me ? static_cast<uint32_t*>(bufs[2 * rel + 1])
-                             : static_cast<uint32_t*>(c->peer_ptr[p][2 * rel + 1]);
-      dst.key[p] = kb + at * ks;
-      dst.rid[p] = rb + at;
-      dst.base[p] = (uint32_t)base;
-      base += sent(me, rel, p);
+      dst.key[p] = p == me ? bufs[2 * rel] : c->peer_ptr[p][2 * rel];
+      dst.rid[p] = static_cast<uint32_t*>(p == me ? bufs[2 * rel + 1] : c->peer_ptr[p][2 * rel + 1]);
     }
+    dst.adj = dtab + (size_t)rel * D1;
+    dst.lbits = b1;
     shuffle_scatter(ctx, rel ? S : R, SP[rel], dst);
   }
   trace_sync(ctx, "fused: scatter");
   // every rank's NVLink stores are done before any local join reads its buffers
   {
     RegionScope rs(ctx, "shuffle_barrier");
-    GJ_NCCL(ncclAllReduce(cnt + 2 * G + 2 * G * G, cnt + 2 * G + 2 * G * G + 1, 1, ncclUint64, ncclSum, c->comm,
-                          ctx->stream));
+    uint32_t* z = all + row * G;
+    GJ_NCCL(ncclAllReduce(z, z + 1, 1, ncclUint32, ncclSum, c->comm, ctx->stream));
   }
   trace_sync(ctx, "fused: barrier");
   gj_rel RL{bufs[0], static_cast<const uint32_t*>(bufs[1]), nrecv[0], R.key_type, 0};
   gj_rel SL{bufs[2], static_cast<const uint32_t*>(bufs[3]), nrecv[1], S.key_type, 0};
-  join_count_core(ctx, RL, SL, g);
+  const uint32_t* segR = dtab + 2 * (size_t)D1;
+  join_count_core(ctx, RL, SL, g, b1, segR, segR + (L1 + 1));
   trace_sync(ctx, "fused: local join count");
 }
 

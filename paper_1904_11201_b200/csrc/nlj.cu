@@ -234,8 +234,13 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
           for (uint32_t j = n4 * 4; j < tn; ++j) step8<FAM>(acc, rf, (uint32_t)skey_at(j) ^ 0x80000000u, a.C);
           tot += acc;
         } else {
-          for (uint32_t j = 0; j < tn; ++j) {
-            const uint32_t su = (uint32_t)skey_at(j) ^ 0x80000000u;
+          // One S key: if any lane of the warp matches it, write the warp's pairs.
+          // The key is re-read through a volatile shared load: given the screening
+          // values, ptxas would otherwise keep all 32 carry predicates of a group alive
+          // in a register bitmask (2 extra ALU ops per pair on the hot path).
+          auto emit = [&](uint32_t j) {
+            const uint32_t su = (uint32_t)(j < tn16 ? reinterpret_cast<volatile const K*>(st)[j] : skey[tb + j]) ^
+                                0x80000000u;
             uint32_t acc = 0;
             step8<FAM>(acc, rf, su, a.C);
             const uint32_t m = direct(OP) ? acc : KR - acc;
@@ -249,7 +254,31 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
                 wbase += __popc(bal);
               }
             }
+          };
+          // Screen 4 S keys (one LDS.128) with the count pass's carry-chain counters and
+          // one warp vote; only groups holding a match are re-walked key by key, in
+          // order, so the output order is the per-key order.
+          const uint4* s4 = reinterpret_cast<const uint4*>(st);
+          const uint32_t n4 = tn16 >> 2;
+#pragma unroll 2
+          for (uint32_t q = 0; q < n4; ++q) {
+            const uint4 v = s4[q];
+            const uint32_t s0 = v.x ^ 0x80000000u, s1 = v.y ^ 0x80000000u;
+            const uint32_t s2 = v.z ^ 0x80000000u, s3 = v.w ^ 0x80000000u;
+            uint32_t acc = 0;
+            step8<FAM>(acc, rf, s0, a.C);
+            step8<FAM>(acc, rf, s1, a.C);
+            step8<FAM>(acc, rf, s2, a.C);
+            step8<FAM>(acc, rf, s3, a.C);
+            const bool hit = direct(OP) ? acc != 0 : acc != 4u * KR;
+            if (__any_sync(FULL, hit)) {
+              emit(4 * q);
+              emit(4 * q + 1);
+              emit(4 * q + 2);
+              emit(4 * q + 3);
+            }
           }
+          for (uint32_t j = n4 * 4; j < tn; ++j) emit(j);
         }
       } else {
         // exact generic path: int64 keys, the ragged last R tile, band overflow cases

@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(PT) part_scatter(
         const uint32_t dd = threadIdx.x + q * PT;
         g0[q] = dd < D ? scanned[d.z + (uint64_t)dd * d.w] : 0u;
         g1[q] = dd < D ? tile_pref[(uint64_t)t * D + dd] : 0u;
+        if (REMOTE) g1[q] += dd < D ? dst.adj[dd] : 0u;  // position -> receiver index
       }
       if (D >= 4) {
         uint4* z = reinterpret_cast<uint4*>(sm.whist + w * D);
@@ -342,10 +343,10 @@ __global__ void __launch_bounds__(PT) part_scatter(
           const K kk = skey[j];
           const uint32_t dg = digit_of(kk, shift, mask);
           const uint32_t pos = sm.delta[dg] + j;
-          if (REMOTE) {
-            const uint32_t idx = pos - dst.base[dg];
-            static_cast<K*>(dst.key[dg])[idx] = kk;
-            dst.rid[dg][idx] = srid[j];
+          if (REMOTE) {  // pos is already the index in the receiving rank's buffer
+            const uint32_t p = dg >> dst.lbits;
+            static_cast<K*>(dst.key[p])[pos] = kk;
+            dst.rid[p][pos] = srid[j];
           } else {
             key_out[pos] = kk;
             rid_out[pos] = srid[j];
@@ -418,10 +419,17 @@ __global__ void fill_off2(uint32_t* off, uint64_t n) {
 }
 
 template <typename K>
-Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char* tag, uint32_t skip) {
+Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char* tag, uint32_t skip,
+                           const uint32_t* seg_off0, uint32_t nseg0) {
   std::string t(tag);
   Partitioned out;
   const uint64_t n = X.n;
+  if (B == 0 && seg_off0) {  // the given segments are the partitions
+    out.key = X.key;
+    out.rid = X.rid;
+    out.off = seg_off0;
+    return out;
+  }
   if (B == 0) {
     uint32_t* off = static_cast<uint32_t*>(ws(ctx, (t + ".off").c_str(), 2 * sizeof(uint32_t)));
     launch(ctx, "fill_off", fill_off2, dim3(1), dim3(1), 0, off, n);
@@ -434,8 +442,8 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
   const int npass = radix_passes(B);
   const K* kin = static_cast<const K*>(X.key);
   const uint32_t* rin = X.rid;
-  const uint32_t* seg_off = nullptr;
-  uint32_t nseg = 1, used = skip;
+  const uint32_t* seg_off = seg_off0;
+  uint32_t nseg = seg_off0 ? nseg0 : 1, used = skip;
   for (int pass = 0; pass < npass; ++pass) {
     const uint32_t bits = B / npass + ((uint32_t)pass < B % npass ? 1 : 0);
     const uint32_t D = 1u << bits;
@@ -444,12 +452,12 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
     K* kout = static_cast<K*>(ws(ctx, (ps + ".key").c_str(), n * sizeof(K)));
     uint32_t* rout = static_cast<uint32_t*>(ws(ctx, (ps + ".rid").c_str(), n * sizeof(uint32_t)));
     uint32_t* chunk_base = nullptr;
-    if (pass > 0) {
+    if (seg_off) {
       chunk_base = static_cast<uint32_t*>(ws(ctx, (t + ".cb").c_str(), (nseg + 1) * sizeof(uint32_t)));
       launch(ctx, "seg_chunks", seg_chunks, dim3((nseg + 255) / 256), dim3(256), 0, seg_off, nseg, chunk_base);
       exclusive_scan<uint32_t, uint32_t>(ctx, chunk_base, chunk_base, nseg, chunk_base + nseg);
     }
-    const uint64_t max_chunks = (n + CHUNK - 1) / CHUNK + (pass > 0 ? nseg : 0);
+    const uint64_t max_chunks = (n + CHUNK - 1) / CHUNK + (seg_off ? nseg : 0);
     const uint64_t hn = max_chunks * D;
     uint32_t* hist = static_cast<uint32_t*>(ws(ctx, (t + ".hist").c_str(), (hn + 1) * sizeof(uint32_t)));
     const uint64_t ntiles = max_chunks * TPC;
@@ -505,7 +513,8 @@ ShufflePass shuffle_prepare_impl(gj_ctx* ctx, const gj_rel& X, uint32_t g, const
   launch(ctx, "tile_desc", tile_desc_kernel, dim3((unsigned)((sp.ntiles + 255) / 256)), dim3(256), 0, n,
          (const uint32_t*)nullptr, (const uint32_t*)nullptr, 1u, D, (uint32_t)sp.ntiles, tdesc);
   uint32_t* off = static_cast<uint32_t*>(ws(ctx, (t + ".soff").c_str(), (D + 1) * sizeof(uint32_t)));
-  launch(ctx, "extract_off", extract_off, dim3(1), dim3(256), 0, (const uint32_t*)hist, (const uint32_t*)nullptr,
+  launch(ctx, "extract_off", extract_off, dim3((D + 1 + 255) / 256), dim3(256), 0, (const uint32_t*)hist,
+         (const uint32_t*)nullptr,
          (const uint32_t*)nullptr, 1u, g, n, off);
   sp.hist = hist;
   sp.tile_pref = tile_pref;
@@ -518,9 +527,10 @@ ShufflePass shuffle_prepare_impl(gj_ctx* ctx, const gj_rel& X, uint32_t g, const
 
 int radix_passes(uint32_t B) { return B == 0 ? 0 : (int)((B + MAX_BITS - 1) / MAX_BITS); }
 
-Partitioned radix_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char* tag, uint32_t skip) {
-  if (X.key_type == GJ_I32) return partition_impl<int32_t>(ctx, X, B, tag, skip);
-  return partition_impl<int64_t>(ctx, X, B, tag, skip);
+Partitioned radix_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char* tag, uint32_t skip,
+                            const uint32_t* seg_off0, uint32_t nseg0) {
+  if (X.key_type == GJ_I32) return partition_impl<int32_t>(ctx, X, B, tag, skip, seg_off0, nseg0);
+  return partition_impl<int64_t>(ctx, X, B, tag, skip, seg_off0, nseg0);
 }
 
 ShufflePass shuffle_prepare(gj_ctx* ctx, const gj_rel& X, uint32_t g, const char* tag) {

@@ -22,16 +22,21 @@ int radix_passes(uint32_t B);
 
 // Partition relation X (key type by X.key_type) into 2^B partitions.
 // tag distinguishes the workspace of the two relations ("R" / "S").
-// skip = top hash bits already consumed (log2 #ranks after a multi-GPU shuffle);
-// the partition digits are bits [32-skip-B, 32-skip) of khash.
-Partitioned radix_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char* tag, uint32_t skip = 0);
+// skip = top hash bits already consumed (after a multi-GPU shuffle); the partition
+// digits are bits [32-skip-B, 32-skip) of khash.  If seg_off0 is given, X is
+// already grouped into nseg0 segments (device offsets, nseg0+1 entries) by the
+// log2(nseg0) hash bits just below the skipped ones, and only B more bits are
+// applied inside each segment: the result has nseg0 * 2^B partitions.
+Partitioned radix_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char* tag, uint32_t skip = 0,
+                            const uint32_t* seg_off0 = nullptr, uint32_t nseg0 = 1);
 
 // ---- multi-GPU shuffle fused into the partition scatter
 constexpr int MAX_RANKS = 8;
 struct ShuffleDest {
-  void* key[MAX_RANKS];       // destination key pointer per rank (peer memory via IPC)
-  uint32_t* rid[MAX_RANKS];   // destination rid pointer per rank
-  uint32_t base[MAX_RANKS];   // start of the rank's run in this relation's local digit order
+  void* key[MAX_RANKS];       // receive key buffer per rank (peer memory via IPC)
+  uint32_t* rid[MAX_RANKS];   // receive rid buffer per rank
+  const uint32_t* adj;        // device, per digit: receiver index - sender position (mod 2^32)
+  uint32_t lbits;             // destination rank = digit >> lbits
 };
 struct ShufflePass {
   uint32_t g = 0;
@@ -41,9 +46,11 @@ struct ShufflePass {
   const uint4* tdesc = nullptr;
   const uint32_t* off = nullptr;  // device, 2^g + 1 run starts (local digit order)
 };
-// Histogram + scan for a one-pass partition of X by the top g hash bits.
+// Histogram + scan for a one-pass partition of X by the top g hash bits
+// (g = log2 #ranks + the first local radix digit).
 ShufflePass shuffle_prepare(gj_ctx* ctx, const gj_rel& X, uint32_t g, const char* tag);
-// The scatter of that pass, writing run d to dst.key[d] / dst.rid[d].
+// The scatter of that pass: the tuple at position pos of run d (sender digit
+// order) goes to dst.key/rid[d >> dst.lbits][pos + dst.adj[d]].
 void shuffle_scatter(gj_ctx* ctx, const gj_rel& X, const ShufflePass& sp, const ShuffleDest& dst);
 
 }  // namespace gj

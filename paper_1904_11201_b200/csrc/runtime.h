@@ -90,9 +90,10 @@ struct gj_ctx {
   uint32_t nlj_split = 0;
   bool force_slow_band = false;
   int build_side = 0;
+  int shuffle_bits = 0;
   // workspace
   std::map<std::string, gj::Buf> bufs;
-  void* host_pinned = nullptr;  // small pinned staging for counts
+  std::map<std::string, gj::Buf> pinned_bufs;  // grow-only pinned host staging
   // stats
   uint64_t launches = 0;
   std::vector<gj::ProfRec> pending;
@@ -107,7 +108,10 @@ namespace gj {
 
 // Grow-only named scratch buffer, stream-ordered.
 void* ws(gj_ctx* ctx, const char* name, size_t bytes);
-// Read a small device value to the host (synchronises the ctx stream).
+// Grow-only named pinned host buffer (callers must not overwrite one that an
+// enqueued copy still reads: every reuse here follows a stream synchronisation).
+void* pinned(gj_ctx* ctx, const char* name, size_t bytes);
+// Read a device array to the host (synchronises the ctx stream).
 void d2h_sync(gj_ctx* ctx, void* host, const void* dev, size_t bytes);
 
 // Launch bracket: counts the launch and, when profiling, records events.

@@ -18,6 +18,14 @@ def _free_port():
     return p
 
 
+def _i64_inputs():
+    """int64 keys spread over +-2^56 (upper hash bits exercised), duplicates on both sides."""
+    import gen
+    R = gen.uniform_keys(60_000, 40_000, 12, 0, dtype=np.int64) * np.int64(1 << 35) - np.int64(1 << 56)
+    S = gen.uniform_keys(250_000, 50_000, 12, 1, dtype=np.int64) * np.int64(1 << 35) - np.int64(1 << 56)
+    return R, S
+
+
 def _worker(rank, world, port, q):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -53,6 +61,27 @@ def _worker(rank, world, port, q):
         S2 = gj.Rel(torch.from_numpy(S2all[s0:s1]).cuda(), None, s0)
         nl, ng = gj.join_dist_count(ctx, comm, R2, S2)
         out["dup"] = (nl, ng, gj.join_dist_materialize(ctx, comm, R2, S2, nl).cpu().numpy().view(np.uint32))
+        # local radix digits folded into the NVLink shuffle (receivers lay out digit-major):
+        # (a) 3 radix bits in all, so the shuffle's local digit alone forms the partitions
+        ctx.set_option("shuffle_bits", 8)
+        ctx.set_option("part_bits", 3)
+        nl, ng = gj.join_dist_count(ctx, comm, R2, S2)
+        out["dup_pb3"] = (nl, ng, gj.join_dist_materialize(ctx, comm, R2, S2, nl).cpu().numpy().view(np.uint32))
+        ctx.set_option("part_bits", -1)
+        # (b) 6 folded bits + the remaining radix bits of the local join on top
+        ctx.set_option("shuffle_bits", 6)
+        nl, ng = gj.join_dist_count(ctx, comm, R, S)
+        out["equi_sb6"] = (nl, ng, gj.join_dist_materialize(ctx, comm, R, S, nl).cpu().numpy().view(np.uint32))
+        ctx.set_option("shuffle_bits", 0)
+        # int64 keys (configs[4] shape, C5 recipe), rank 0 holds no R rows; larger than the
+        # calls above, so the receive buffers grow and the IPC handles are re-exchanged
+        R4all, S4all = _i64_inputs()
+        r0, r1 = (0, 0) if rank == 0 else ((rank - 1) * len(R4all) // (world - 1), rank * len(R4all) // (world - 1))
+        s0, s1 = (rank * len(S4all)) // world, ((rank + 1) * len(S4all)) // world
+        R4 = gj.Rel(torch.from_numpy(R4all[r0:r1]).cuda(), None, r0)
+        S4 = gj.Rel(torch.from_numpy(S4all[s0:s1]).cuda(), None, s0)
+        nl, ng = gj.join_dist_count(ctx, comm, R4, S4)
+        out["i64"] = (nl, ng, gj.join_dist_materialize(ctx, comm, R4, S4, nl).cpu().numpy().view(np.uint32))
         # theta band: R replicated, S sharded
         R3all = gen.uniform_keys(5000, 1 << 20, 8, 0)
         S3all = gen.uniform_keys(20_000, 1 << 20, 8, 1)
@@ -104,8 +133,11 @@ def test_dist_joins_match_oracle(world):
     Rall, Sall, m = gen.zipf_pkfk(b, 1 << 20, gen.zipf_table(1 << b), seed=5)
     R2all, S2all = gen.uniform_keys(30_001, 2000, 3, 0), gen.uniform_keys(40_003, 2000, 3, 1)
     R3all, S3all = gen.uniform_keys(5000, 1 << 20, 8, 0), gen.uniform_keys(20_000, 1 << 20, 8, 1)
-    expect = {"equi": oracle.pkfk_closed_form(m), "dup": oracle.hash_equi(R2all, S2all),
-              "band": oracle.band_materialize(R3all, S3all, 40)}
+    R4all, S4all = _i64_inputs()
+    dup = oracle.hash_equi(R2all, S2all)
+    pk = oracle.pkfk_closed_form(m)
+    expect = {"equi": pk, "equi_sb6": pk, "dup": dup, "dup_pb3": dup,
+              "i64": oracle.hash_equi(R4all, S4all), "band": oracle.band_materialize(R3all, S3all, 40)}
     for name, (cnt, pairs) in expect.items():
         locals_ = [res[r][name] for r in range(world)]
         assert all(l[1] == cnt for l in locals_), name  # n_global

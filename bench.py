@@ -42,6 +42,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 S_BITS_C4 = 24  # set from --c4-s-bits
+C5_BITS = 28  # set from --c5-bits
 METRIC = "join input & output tuples/s at 1/2/4/8 B200; % of HBM/INT roofline"
 
 
@@ -177,27 +178,66 @@ def make_workload(name, device, rank=0, world=1):
         if world > 1:
             desc += f"; weak scaling: R (2^20) all-gathered, {world} x 2^24 S shards"
         return dict(kind="band", R=R, S=S, eps=gen.C4_EPS, desc=desc, rid_base_R=rank * nr, rid_base=rank * ns)
+    if name == "c5":
+        nr, ns = 1 << C5_BITS, 1 << (C5_BITS + 1)  # per GPU; 2^28 x 2^29 at N=8 = 2^31 x 2^32 = configs[4]
+        b = C5_BITS + g
+        R = gd.c5_R(nr, seed, offset=rank * nr, device=device, b=b)
+        S = gd.c5_S(ns, seed, offset=rank * ns, device=device, b=b)
+        desc = (f"configs[4] shape: pre-filtered (range + Bloom 8 bits/key, two-sided) equi join, int64 keys, "
+                f"per GPU 2^{C5_BITS} x 2^{C5_BITS + 1} rows of a 2^{b}-row domain (N=8 with 2^28 per GPU = "
+                f"2^31 x 2^32 = configs[4]); 10% of S are members")
+        if world > 1:
+            desc += "; distributed: range all-reduce, R shuffle, per-owner Bloom all-gather, filtered S shuffle"
+        return dict(kind="pf_equi", R=R, S=S, desc=desc, rid_base_R=rank * nr, rid_base=rank * ns)
     raise SystemExit(f"unknown workload {name}")
 
 
-def algorithmic_bytes(w, ctxinfo):
+def ncu_traffic(workload, tag):
+    """(dram bytes read+written per launch, source file) from the newest committed
+    profiles/rNN_traffic.json that has this workload and kernel tag, else (None, None)."""
+    import glob
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
+        t = json.load(open(f)).get(workload, {}).get(tag)
+        if t:
+            return round(t["dram_bytes_per_launch"]), f"profiles/{os.path.basename(f)} ({t['report']})"
+    return None, None
+
+
+def join_bytes(nR, nS, nout, passes, wk, rid_implicit):
+    """Algorithmic bytes of the partitioned hash join, per tag:
+    (total bytes per step, launches per step).  wk = key bytes; rid_implicit = the
+    first radix pass reads keys only (rids are row positions)."""
+    n = nR + nS
+    first = wk + (wk + 4) if rid_implicit else 2 * (wk + 4)
+    scatter_total = n * first + (passes - 1) * n * 2 * (wk + 4)
+    nb, npb = min(nR, nS), max(nR, nS)
+    return {
+        "part_hist": (wk * n * passes, 2 * passes),
+        "part_scatter": (scatter_total, 2 * passes),
+        # count: build + probe keys in, one uint16 match index per probe row out
+        "hj_count": (wk * n + 2 * npb, 1),
+        # write: build + probe rids and the staged index in, 8-byte pairs out
+        "hj_write": (4 * nb + 4 * npb + 2 * npb + 8 * nout, 1),
+    }
+
+
+def algorithmic_bytes(w, info):
     """Algorithmic HBM bytes per launch of each kernel tag."""
     nR, nS = w["R"].numel(), w["S"].numel()
-    nout = ctxinfo["n_out"]
+    nout = info["n_out"]
     if w["kind"] == "equi":
-        passes = ctxinfo["passes"]
-        n = nR + nS
-        # scatter: pass 1 reads the key (rid implicit) + writes key+rid; later passes read key+rid
-        scatter_total = (nR + nS) * (4 + 8) + (passes - 1) * (nR + nS) * (8 + 8)
-        nb, npb = min(nR, nS), max(nR, nS)
-        return {
-            "part_hist": (4 * n * passes, 2 * passes),
-            "part_scatter": (scatter_total, 2 * passes),
-            # count: build + probe keys in, one uint16 match index per probe row out
-            "hj_count": (4 * n + 2 * npb, 1),
-            # write: build + probe rids and the staged index in, 8-byte pairs out
-            "hj_write": (4 * nb + 4 * npb + 2 * npb + 8 * nout, 1),
-        }
+        return join_bytes(nR, nS, nout, info["passes"], w["R"].element_size(), info["world"] == 1)
+    if w["kind"] == "pf_equi":
+        # SURVEY §8(d) C5: a probed row costs its 8 B key + one 32 B Bloom sector; a
+        # survivor 12 B (key + rid) written; a filter insert 8 B key + a 32 B sector;
+        # then the hash join on the survivors with 8-byte keys.
+        kR, kS = w["kept"]
+        pf = info["pf_launches"]
+        ab = join_bytes(kR, kS, nout, info["passes"], 8, False)
+        ab["pf_count"] = (40 * (nR + nS), pf)
+        ab["pf_write"] = (40 * (nR + nS) + 12 * (kR + kS), pf)
+        ab["bloom_build"] = (40 * (nR + kS), info["bloom_launches"])
+        return ab
     # band: NLJ is ALU-bound; bytes are tiny
     return {"nlj_count": (4 * (nR + nS), 1), "nlj_write": (4 * (nR + nS) + 8 * nout, 1)}
 
@@ -233,6 +273,29 @@ def run_ours(args, world, rank, local):
             else:
                 m, _ = gj.join_dist_count(ctx, comm, R, S)
                 gj.join_dist_materialize(ctx, comm, R, S, m, out=out)
+            return m
+    elif w["kind"] == "pf_equi":
+        PF = gj.RANGE | gj.BLOOM | gj.TWO_SIDED
+
+        def pf_step_count():
+            if comm is None:  # one GPU: prefilter() survivors (with rid maps) -> join
+                kR, rR, kS, rS = gj.prefilter(ctx, R, S, PF, "eq", 0, 8.0)
+                R2, S2 = gj.Rel(kR, rR), gj.Rel(kS, rS)
+                return gj.join_count(ctx, R2, S2), (R2, S2), (kR.numel(), kS.numel())
+            m, _, kept = gj.join_dist_count_filtered(ctx, comm, R, S, PF, 8.0)
+            return m, (R, S), kept
+
+        n, _, kept0 = pf_step_count()
+        n_global = n if comm is None else gj.join_dist_count_filtered(ctx, comm, R, S, PF, 8.0)[1]
+        w["kept"] = kept0
+        out = torch.empty((max(int(n * 1.2) + 1024, 1), 2), dtype=torch.int32, device=dev)
+
+        def step():
+            m, (R2, S2), _ = pf_step_count()
+            if comm is None:
+                gj.join_materialize(ctx, R2, S2, m, out=out)
+            else:
+                gj.join_dist_materialize(ctx, comm, R2, S2, m, out=out)
             return m
     else:
         eps = w["eps"]
@@ -281,10 +344,11 @@ def run_ours(args, world, rank, local):
     ktimes = ctx.kernel_times()
     ctx.set_option("profile", 0)
 
-    info = {"n_out": n}
-    if w["kind"] == "equi":
-        # radix passes per relation actually run (incl. the multi-GPU shuffle pass)
-        info["passes"] = round(ktimes.get("part_scatter", (0, 0))[1] / args.steps / 2)
+    info = {"n_out": n, "world": world}
+    # local radix passes per relation actually run (the multi-GPU shuffle is "shuffle_scatter")
+    info["passes"] = max(1, round(ktimes.get("part_scatter", (0, 0))[1] / args.steps / 2))
+    info["pf_launches"] = max(1, round(ktimes.get("pf_count", (0, 0))[1] / args.steps))
+    info["bloom_launches"] = max(1, round(ktimes.get("bloom_build", (0, 0))[1] / args.steps))
     ab = algorithmic_bytes(w, info)
     hbm, peak_src = peaks()
     per_kernel = {}
@@ -298,30 +362,54 @@ def run_ours(args, world, rank, local):
             rec["achieved_gbs"] = per_launch / (tms / cnt * 1e-3) / 1e9
         per_kernel[tag] = rec
     dom = max(ktimes.items(), key=lambda kv: kv[1][0])[0]
-    if w["kind"] == "equi":
+    # measured DRAM bytes per launch of the dominant kernel: committed ncu --set full
+    # capture of the same single-GPU workload (profiles/rNN_traffic.json)
+    traffic, tsrc = ncu_traffic(args.workload, dom) if world == 1 else (None, None)
+    if w["kind"] in ("equi", "pf_equi"):
         d = per_kernel[dom]
         roof = {"kernel": dom, "bound": "hbm", "achieved": round(d.get("achieved_gbs", 0.0), 1), "peak": hbm,
-                "unit": "GB/s", "frac": round(d.get("achieved_gbs", 0.0) / hbm, 4), "traffic": None,
+                "unit": "GB/s", "frac": round(d.get("achieved_gbs", 0.0) / hbm, 4), "traffic": traffic,
+                "alg_bytes_per_launch": d.get("alg_bytes_per_launch"), "traffic_source": tsrc,
                 "peak_source": peak_src}
     else:
         # INT ALU roofline: 1.5 ALU-pipe instr per pair-compare (band: + 1 FMA-pipe IMAD), DESIGN.md §5
-        pairs = nR * nS
+        pairs = nR * world * nS  # the local NLJ runs the all-gathered R (world equal shards) x its S shard
         d = per_kernel[dom]
         sm = sampler.summary().get("sm_mhz") or 1965
         alu_peak = 148 * 64 * sm * 1e6 / 1.5 / 1e12  # T pair-compares/s the ALU pipe allows
         ach = pairs / (d["ms_per_launch"] * 1e-3) / 1e12
         roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 3),
-                "unit": "Tpair/s", "frac": round(ach / alu_peak, 4), "traffic": None,
+                "unit": "Tpair/s", "frac": round(ach / alu_peak, 4), "traffic": traffic,
+                "alg_bytes_per_launch": d.get("alg_bytes_per_launch"), "traffic_source": tsrc,
                 "peak_source": "148 SM x 64 ALU lanes/clk x median SM clock / 1.5 ALU instr per pair"}
 
     # ---- e2e: host buffers in, host pairs out, through the public API
     e2e = None
-    if w["kind"] == "equi":
+    if w["kind"] in ("equi", "pf_equi"):
         hR = w["R"].cpu().pin_memory()
         hS = w["S"].cpu().pin_memory()
         hout = torch.empty((max(n, 1), 2), dtype=torch.int32).pin_memory()
         k_e2e = max(1, min(args.steps, args.e2e_steps))
-        if comm is None:
+        if w["kind"] == "pf_equi":
+            dR, dS = torch.empty_like(w["R"]), torch.empty_like(w["S"])
+            eR, eS = gj.Rel(dR, None, R.rid_base), gj.Rel(dS, None, S.rid_base)
+
+            def e2e_step():
+                dR.copy_(hR, non_blocking=True)
+                dS.copy_(hS, non_blocking=True)
+                if comm is None:
+                    kR, rR, kS, rS = gj.prefilter(ctx, eR, eS, PF, "eq", 0, 8.0)
+                    R2, S2 = gj.Rel(kR, rR), gj.Rel(kS, rS)
+                    m = gj.join_count(ctx, R2, S2)
+                    res = gj.join_materialize(ctx, R2, S2, m, out=out)
+                else:
+                    m, _, _ = gj.join_dist_count_filtered(ctx, comm, eR, eS, PF, 8.0)
+                    res = gj.join_dist_materialize(ctx, comm, eR, eS, m, out=out)
+                hout[:m].copy_(res)
+                return m
+            note = ("per rank: pinned H2D of its shards -> prefilter + join (count/scan/write) through the public "
+                    "API -> D2H of its pairs")
+        elif comm is None:
             def e2e_step():
                 return gj.join_host(ctx, hR, hS, hout)  # one C-ABI call: H2D, join, D2H
             note = "join_host(): pinned host keys -> H2D -> count/scan/write -> D2H of all pairs (one C-ABI call)"
@@ -354,7 +442,7 @@ def run_ours(args, world, rank, local):
         comm.close()
 
     return dict(ms=ms_max, n=n_global, nR=nR, nS=nS, launches=launches, roof=roof, per_kernel=per_kernel, e2e=e2e,
-                clocks=sampler.summary(), desc=w["desc"], kind=w["kind"])
+                clocks=sampler.summary(), desc=w["desc"], kind=w["kind"], kept=w.get("kept"))
 
 
 def cpu_baseline(args):
@@ -369,6 +457,16 @@ def cpu_baseline(args):
         dt = time.perf_counter() - t0
         return {"value": (len(R) + len(S)) / dt, "unit": "input tuples/s", "cores": 1, "kind": "oracle",
                 "sample": "O3 sort+binary-search band count, R 2^11 x S 2^24 slice of configs[3]", "seconds": dt}
+    if args.workload == "c5":
+        b = args.cpu_sample_bits - 2
+        R, S, m = gen.c5(1 << b, 1 << (b + 1), b=b)
+        t0 = time.perf_counter()
+        c, _ = oracle.hash_equi(R, S)
+        dt = time.perf_counter() - t0
+        assert c == int((m >= 0).sum())
+        return {"value": (len(R) + len(S)) / dt, "unit": "input tuples/s", "cores": 1, "kind": "oracle",
+                "sample": f"O2 unordered_multimap join (exact, no pre-filter), configs[4] shape int64 "
+                          f"2^{b} x 2^{b + 1} over a 2^{b}-row domain", "seconds": round(dt, 3)}
     b = args.cpu_sample_bits
     R, S, m = gen.pkfk(b, 1 << b)
     t0 = time.perf_counter()
@@ -397,16 +495,18 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c4"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample-bits", type=int, default=23)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--c4-s-bits", type=int, default=24, help="log2 |S| per GPU for c4 (24 = configs[3]; ncu only)")
+    ap.add_argument("--c5-bits", type=int, default=28, help="log2 |R| per GPU for c5 (|S| = 2|R|; 28 at N=8 = configs[4])")
     ap.add_argument("--opt", action="append", default=[], help="ctx option name=value (tuning sweeps)")
     args = ap.parse_args()
-    global S_BITS_C4
+    global S_BITS_C4, C5_BITS
     S_BITS_C4 = args.c4_s_bits
+    C5_BITS = args.c5_bits
     world, rank, local = dist_setup(args)
 
     if args.impl == "reference":
@@ -450,7 +550,8 @@ def main():
         "config": {"workload": r["desc"], "n_R_per_gpu": r["nR"], "n_S_per_gpu": r["nS"], "n_out": r["n"],
                    "l2": "inputs (>=64 MiB of keys, 1 GiB for configs[1]) exceed/stream past the 126 MB L2; no flush",
                    "parallelism": ("1 GPU" if world == 1 else
-                                   f"{world} ranks, NCCL hash-partition shuffle (equi) / R all-gather (theta)")},
+                                   f"{world} ranks, hash shuffle over NVLink peer stores (equi) / "
+                                   "R all-gather (theta)")} | ({"kept_R_S_rank0": list(r["kept"])} if r.get("kept") else {}),
         "roofline": r["roof"],
         "kernels": r["per_kernel"],
         "gpu_launches": r["launches"],

@@ -169,12 +169,13 @@ def c5_member_mask(nS: int, seed: int, offset: int = 0) -> np.ndarray:
     return (rng(seed, 3, nS, offset) >> _S32) < thr
 
 
-def c5(nR: int, nS: int, seed: int = BASE_SEED, r_offset: int = 0, s_offset: int = 0):
-    """configs[4] (C5) with int64 keys: R.key[i] = 2*perm_31(i) (even, unique);
-    S member rows: 2*perm_31(m_j), m_j = uniform(2^31); non-members odd 2*uniform(1.25*2^31)+1."""
-    R = (perm(np.arange(r_offset, r_offset + nR, dtype=np.uint64), 31, seed) * np.uint64(2)).astype(np.int64)
+def c5(nR: int, nS: int, seed: int = BASE_SEED, r_offset: int = 0, s_offset: int = 0, b: int = 31):
+    """configs[4] (C5) with int64 keys over a domain of 2^b R rows (b = 31 is configs[4]):
+    R.key[i] = 2*perm_b(i) (even, unique); S member rows: 2*perm_b(m_j), m_j = uniform(2^b);
+    non-members odd 2*uniform(1.25*2^b)+1."""
+    R = (perm(np.arange(r_offset, r_offset + nR, dtype=np.uint64), b, seed) * np.uint64(2)).astype(np.int64)
     mem = c5_member_mask(nS, seed, s_offset)
-    m = uniform(nS, 1 << 31, seed, 1, s_offset)
-    nonm = uniform(nS, int(1.25 * 2**31), seed, 4, s_offset) * np.uint64(2) + np.uint64(1)
-    S = np.where(mem, perm(m, 31, seed) * np.uint64(2), nonm).astype(np.int64)
+    m = uniform(nS, 1 << b, seed, 1, s_offset)
+    nonm = uniform(nS, int(1.25 * 2**b), seed, 4, s_offset) * np.uint64(2) + np.uint64(1)
+    S = np.where(mem, perm(m, b, seed) * np.uint64(2), nonm).astype(np.int64)
     return R, S, np.where(mem, m.astype(np.int64), -1)

@@ -30,7 +30,7 @@ def lib():
         L.gjgen_perm_range.argtypes = [vp, u64, u64, u32, pu, u64, u64, i32, vp]
         L.gjgen_pkfk.argtypes = [vp, u64, u64, u32, pu, u64, u64, u64, vp]
         L.gjgen_zipf.argtypes = [vp, u64, u64, u32, pu, vp, u64, u64, u64, vp]
-        L.gjgen_c5s.argtypes = [vp, u64, u64, u32, pu, u64, u64, u64, u64, u64, u64, vp]
+        L.gjgen_c5s.argtypes = [vp, u64, u64, u32, pu, u64, u64, u64, u64, u64, u64, u64, vp]
         _lib = L
     return _lib
 
@@ -81,14 +81,20 @@ def zipf_S(n, b, cdf_q: torch.Tensor, seed, offset=0, device="cuda"):
     return out
 
 
-def c5_S(n, seed, offset=0, device="cuda"):
+def c5_S(n, seed, offset=0, device="cuda", b=31):
+    """gen.c5's S column on the device (domain 2^b; b = 31 is configs[4])."""
     out = torch.empty(n, dtype=torch.int64, device=device)
-    mask, sh, c = _perm(31, seed)
+    mask, sh, c = _perm(b, seed)
     thr = int(0.1 * 2**32)
     _ok(lib().gjgen_c5s(ctypes.c_void_p(out.data_ptr()), n, mask, sh, c, int(stream_key(seed, 1)),
-                        int(stream_key(seed, 3)), int(stream_key(seed, 4)), thr, int(1.25 * 2**31), offset,
+                        int(stream_key(seed, 3)), int(stream_key(seed, 4)), thr, 1 << b, int(1.25 * 2**b), offset,
                         _stream()))
     return out
+
+
+def c5_R(n, seed, offset=0, device="cuda", b=31):
+    """gen.c5's R column on the device: 2*perm_b(offset + i) as int64."""
+    return perm_range(n, b, seed, offset=offset, mult=2, dtype=torch.int64, device=device)
 
 
 def zipf_table_device(N: int, device="cuda") -> torch.Tensor:

@@ -67,13 +67,13 @@ __global__ void k_zipf(int32_t* out, uint64_t n, Perm p, const uint64_t* __restr
   }
 }
 
-// C5 S rows: member (hi32(rng3) < thr) -> 2*perm31(uniform(2^31)), else 2*uniform(D2)+1
+// C5 S rows: member (hi32(rng3) < thr) -> 2*perm_b(uniform(D1 = 2^b)), else 2*uniform(D2)+1
 __global__ void k_c5s(int64_t* out, uint64_t n, Perm p, uint64_t k1, uint64_t k3, uint64_t k4, uint64_t thr,
-                      uint64_t D2, uint64_t offset) {
+                      uint64_t D1, uint64_t D2, uint64_t offset) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t j = offset + i;
     const bool mem = (mix64(j + k3) >> 32) < thr;
-    out[i] = mem ? (int64_t)(perm(uniform(mix64(j + k1), 1ull << 31), p) * 2)
+    out[i] = mem ? (int64_t)(perm(uniform(mix64(j + k1), D1), p) * 2)
                  : (int64_t)(uniform(mix64(j + k4), D2) * 2 + 1);
   }
 }
@@ -126,9 +126,9 @@ int gjgen_zipf(void* out, uint64_t n, uint64_t mask, uint32_t sh, const uint64_t
 }
 
 int gjgen_c5s(void* out, uint64_t n, uint64_t mask, uint32_t sh, const uint64_t* c, uint64_t k1, uint64_t k3,
-              uint64_t k4, uint64_t thr, uint64_t D2, uint64_t offset, void* stream) {
+              uint64_t k4, uint64_t thr, uint64_t D1, uint64_t D2, uint64_t offset, void* stream) {
   Perm p = make_perm(mask, sh, c);
-  k_c5s<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>((int64_t*)out, n, p, k1, k3, k4, thr, D2, offset);
+  k_c5s<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>((int64_t*)out, n, p, k1, k3, k4, thr, D1, D2, offset);
   return (int)cudaGetLastError();
 }
 

@@ -183,10 +183,12 @@ gj_status join_host(gj_ctx* ctx, const void* key_R_host, uint64_t n_R, const voi
 
 /* ---------------------------------------------------------------- multi-GPU
  * One process per GPU.  Equi joins shard by hash partition (the B200 analogue of
- * the Hadoop shuffle of Alg.1 Map2): every rank partitions its
- * shards of R and S by the top log2(G) bits of the key hash, an NCCL all-gather
- * exchanges the GxG count matrix, grouped ncclSend/ncclRecv move the (key, rid)
- * buckets over NVLink, and each rank joins what it received.  Theta joins
+ * the Hadoop shuffle of Alg.1 Map2): every rank runs one radix
+ * pass over its shards of R and S by the top log2(G) bits of the key hash, an NCCL
+ * all-gather exchanges the run counts, the pass's scatter kernel stores every
+ * (key, rid) straight into the owning rank's receive buffer over NVLink (CUDA-IPC
+ * peer memory; env GJ_SHUFFLE=nccl selects grouped ncclSend/ncclRecv instead), and
+ * each rank joins what it received.  Theta joins
  * broadcast R (all-gather of the R shards, PAPER.md:302 region model with one
  * region per rank) and join it against the local S shard.  Output stays sharded:
  * every pair lands on exactly one rank; the union over ranks is J(R, S).
@@ -207,6 +209,18 @@ gj_status gj_comm_init(gj_comm** out, const void* id, int nranks, int rank);
 void gj_comm_destroy(gj_comm* comm);
 gj_status join_dist_count(gj_ctx* ctx, gj_comm* comm, gj_rel R, gj_rel S, uint64_t* n_local,
                           uint64_t* n_global);
+/* Pre-filtered distributed equi join (configs[4]; PAPER.md:78-82 filtering of both
+ * tables before the shuffle): flags as prefilter() (GJ_PF_RANGE: global key range
+ * by NCCL min/max all-reduce; GJ_PF_BLOOM: R is shuffled first, every owner builds
+ * a Bloom filter of its R keys at bloom_bits_per_key in [1, 64], the filters are
+ * all-gathered and S is filtered at the source by its key's owner's filter before
+ * the S shuffle; GJ_PF_TWO_SIDED: each owner also drops R tuples absent from the
+ * filter of its S survivors).  Same results and caching as join_dist_count (follow
+ * with join_dist_materialize).  kept_local (optional, host [2]): R and S tuples
+ * this rank joined after filtering. */
+gj_status join_dist_count_filtered(gj_ctx* ctx, gj_comm* comm, gj_rel R, gj_rel S, uint32_t flags,
+                                   double bloom_bits_per_key, uint64_t* n_local, uint64_t* n_global,
+                                   uint64_t* kept_local);
 gj_status join_dist_materialize(gj_ctx* ctx, gj_comm* comm, gj_rel R, gj_rel S, uint32_t* out,
                                 uint64_t capacity, uint64_t* n_written);
 gj_status theta_join_dist_count(gj_ctx* ctx, gj_comm* comm, gj_rel R, gj_rel S, int op, uint64_t eps,

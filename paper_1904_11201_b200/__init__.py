@@ -83,14 +83,15 @@ def _load():
     L.gj_comm_destroy.argtypes = [vp]
     L.gj_comm_destroy.restype = None
     L.join_dist_count.argtypes = [vp, vp, _Rel, _Rel, pu64, pu64]
+    L.join_dist_count_filtered.argtypes = [vp, vp, _Rel, _Rel, u32, ctypes.c_double, pu64, pu64, pu64]
     L.join_dist_materialize.argtypes = [vp, vp, _Rel, _Rel, vp, u64, pu64]
     L.theta_join_dist_count.argtypes = [vp, vp, _Rel, _Rel, i32, u64, pu64, pu64]
     L.theta_join_dist_materialize.argtypes = [vp, vp, _Rel, _Rel, i32, u64, vp, u64, pu64]
     L.gj_dist_plan.argtypes = [pu64, i32, i32, pu64, pu64]
     for f in ("gj_ctx_create", "gj_ctx_set_stream", "gj_ctx_set_option", "join_count", "join_materialize",
               "theta_join_count", "theta_join_materialize", "prefilter", "join_host", "gj_comm_unique_id",
-              "gj_comm_init", "join_dist_count", "join_dist_materialize", "theta_join_dist_count",
-              "theta_join_dist_materialize", "gj_dist_plan"):
+              "gj_comm_init", "join_dist_count", "join_dist_count_filtered", "join_dist_materialize",
+              "theta_join_dist_count", "theta_join_dist_materialize", "gj_dist_plan"):
         getattr(L, f).restype = i32
     return L
 
@@ -101,8 +102,8 @@ lib = _load()
 ABI_SYMBOLS = ("gj_ctx_create", "gj_ctx_destroy", "gj_ctx_set_stream", "gj_last_error", "gj_ctx_set_option",
                "gj_ctx_launch_count", "gj_ctx_reset_stats", "gj_ctx_kernel_times", "join_count",
                "join_materialize", "theta_join_count", "theta_join_materialize", "prefilter", "join_host",
-               "gj_comm_unique_id", "gj_comm_init", "gj_comm_destroy", "join_dist_count", "join_dist_materialize",
-               "theta_join_dist_count", "theta_join_dist_materialize", "gj_dist_plan")
+               "gj_comm_unique_id", "gj_comm_init", "gj_comm_destroy", "join_dist_count", "join_dist_count_filtered",
+               "join_dist_materialize", "theta_join_dist_count", "theta_join_dist_materialize", "gj_dist_plan")
 COMM_ID_BYTES = 128
 
 
@@ -314,6 +315,16 @@ def join_dist_count(ctx: Context, comm: Comm, R, S):
     nl, ng = ctypes.c_uint64(), ctypes.c_uint64()
     _check(lib.join_dist_count(ctx.h, comm.h, _rel(R), _rel(S), ctypes.byref(nl), ctypes.byref(ng)))
     return nl.value, ng.value
+
+
+def join_dist_count_filtered(ctx: Context, comm: Comm, R, S, flags: int = RANGE | BLOOM | TWO_SIDED,
+                             bloom_bits_per_key: float = 8.0):
+    """Collective pre-filtered equi join count.  Returns (n_local, n_global, (kept_R, kept_S))."""
+    nl, ng = ctypes.c_uint64(), ctypes.c_uint64()
+    kept = (ctypes.c_uint64 * 2)()
+    _check(lib.join_dist_count_filtered(ctx.h, comm.h, _rel(R), _rel(S), int(flags), float(bloom_bits_per_key),
+                                        ctypes.byref(nl), ctypes.byref(ng), kept))
+    return nl.value, ng.value, (kept[0], kept[1])
 
 
 def join_dist_materialize(ctx: Context, comm: Comm, R, S, n_local: Optional[int] = None,

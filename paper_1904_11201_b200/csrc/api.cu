@@ -174,9 +174,13 @@ static bool same_rel(const gj_rel& a, const gj_rel& b) {
 
 uint32_t auto_bits(gj_ctx* ctx, uint64_t nb) {
   if (ctx->part_bits >= 0) return (uint32_t)ctx->part_bits;
-  const uint64_t target = ctx->build_chunk / 2;  // mean build tuples per partition
+  // mean build tuples per partition within [target/sqrt2, target*sqrt2]: B rounds
+  // log2(nb / target) to nearest, so 2^27 (+ a few after a multi-GPU shuffle)
+  // keeps B = 17 instead of jumping to 18 (half-size partitions, 9+9-bit passes)
+  const uint64_t target = ctx->build_chunk / 2;
+  const uint64_t hi = target * 1448 / 1024;  // target * sqrt(2)
   uint32_t B = 0;
-  while ((nb >> B) > target && B < 27) ++B;
+  while ((nb >> B) > hi && B < 27) ++B;
   return B;
 }
 

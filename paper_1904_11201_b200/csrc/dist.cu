@@ -25,6 +25,7 @@
 #include "hashjoin.cuh"
 #include "nlj.cuh"
 #include "partition.cuh"
+#include "prefilter.cuh"
 #include "runtime.h"
 
 #ifdef GJ_HAVE_NCCL
@@ -206,36 +207,41 @@ void dist_equi_count(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) 
   join_count_core(ctx, RL, SL, g, 0, nullptr, nullptr);
 }
 
-// Fused shuffle: radix histogram by destination rank, count-matrix all-gather,
-// then ONE scatter kernel per relation that writes every destination's run straight
-// into that rank's receive buffers through CUDA-IPC peer pointers (NVLink stores),
-// then a stream-ordered barrier (tiny all-reduce) before the local join reads them.
 // Fused shuffle: ONE radix pass by (destination rank, first local digit) -- the top
 // g + b1 hash bits -- whose scatter stores every tuple straight into the receiving
-// rank's buffers over NVLink (CUDA-IPC mappings).  Receivers lay their buffers out
+// rank's buffers over NVLink (CUDA-IPC mappings), then a stream-ordered barrier
+// (tiny all-reduce) before anyone reads them.  Receivers lay their buffers out
 // digit-major (for each local digit: the senders' runs in rank order), so what
 // arrives is already radix-partitioned by b1 bits and the local join only applies
 // the remaining ones.  Order inside a partition: sender rank, then sender order.
-void dist_equi_count_fused(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) {
+struct FusedOut {
+  gj_rel X[2]{};                   // this rank's receive buffers (shuffled relations)
+  const uint32_t* seg[2] = {};     // device, 2^b1 + 1 local-digit starts
+  uint64_t need[MAX_RANKS][2] = {};  // tuples every rank receives, per relation
+};
+
+// Shuffles X[rel] (rel 0 = R, 1 = S; nullptr = leave that relation alone).
+void fused_shuffle(gj_ctx* ctx, gj_comm* c, const gj_rel* const X[2], uint32_t b1, FusedOut& out) {
   const int G = c->nranks, me = c->rank;
   const uint32_t g = log2_exact(G);
-  const size_t ks = R.key_type == GJ_I64 ? 8 : 4;
-  // b1 must be the same on every rank: it depends only on G and the ctx options.
-  // Default 0: with 512 digits the NVLink stores come in ~8-tuple runs and the
-  // shuffle scatter measured 3.1 ms vs 1.2 ms for 2 digits (2^27 tuples, N=2) --
-  // more than the local radix pass it saves (DESIGN.md §6).
-  uint32_t b1 = std::min<uint32_t>((uint32_t)ctx->shuffle_bits, 9 - g);
-  if (ctx->part_bits >= 0) b1 = std::min<uint32_t>(b1, (uint32_t)ctx->part_bits);
+  const int kt = X[0] ? X[0]->key_type : X[1]->key_type;
+  const size_t ks = kt == GJ_I64 ? 8 : 4;
   const uint32_t G1 = g + b1, D1 = 1u << G1, L1 = 1u << b1;
   trace_sync(ctx, "fused: start");
-  ShufflePass SP[2] = {shuffle_prepare(ctx, R, G1, "sR"), shuffle_prepare(ctx, S, G1, "sS")};
+  ShufflePass SP[2];
+  for (int rel = 0; rel < 2; ++rel)
+    if (X[rel]) SP[rel] = shuffle_prepare(ctx, *X[rel], G1, rel ? "sS" : "sR");
   trace_sync(ctx, "fused: shuffle hist");
   // per rank: 2 x D1 run counts + its key width (all ranks must agree on it)
   const size_t row = 2 * (size_t)D1 + 1;
   uint32_t* cnt = static_cast<uint32_t*>(ws(ctx, "dist.cnt", (row * (G + 1) + 2) * 4));
   uint32_t* all = cnt + row;
-  launch(ctx, "run_counts", run_counts, dim3(1), dim3(256), 0, SP[0].off, D1, cnt);
-  launch(ctx, "run_counts", run_counts, dim3(1), dim3(256), 0, SP[1].off, D1, cnt + D1);
+  for (int rel = 0; rel < 2; ++rel) {
+    if (X[rel])
+      launch(ctx, "run_counts", run_counts, dim3(1), dim3(256), 0, SP[rel].off, D1, cnt + (size_t)rel * D1);
+    else
+      GJ_CUDA(cudaMemsetAsync(cnt + (size_t)rel * D1, 0, D1 * 4, ctx->stream));
+  }
   const uint32_t ks32 = (uint32_t)ks;
   GJ_CUDA(cudaMemcpyAsync(cnt + 2 * D1, &ks32, 4, cudaMemcpyHostToDevice, ctx->stream));
   GJ_NCCL(ncclAllGather(cnt, all, row, ncclUint32, c->comm, ctx->stream));
@@ -247,12 +253,12 @@ void dist_equi_count_fused(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_re
   auto cntq = [&](int q, int rel, int p, uint32_t d) -> uint64_t {
     return M[(size_t)q * row + (size_t)rel * D1 + ((size_t)p << b1) + d];
   };
-  uint64_t need[MAX_RANKS][2] = {};
+  auto& need = out.need;
+  for (int p = 0; p < G; ++p) need[p][0] = need[p][1] = 0;
   for (int q = 0; q < G; ++q)
     for (int rel = 0; rel < 2; ++rel)
       for (int p = 0; p < G; ++p)
         for (uint32_t d = 0; d < L1; ++d) need[p][rel] += cntq(q, rel, p, d);
-  const uint64_t nrecv[2] = {need[me][0], need[me][1]};
   for (int p = 0; p < G; ++p)  // every rank sees the whole matrix: all ranks fail together
     if (need[p][0] >= (1ull << 32) || need[p][1] >= (1ull << 32))
       throw Error(GJ_EINVAL, "a rank would receive >= 2^32 tuples; use more ranks");
@@ -291,13 +297,15 @@ void dist_equi_count_fused(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_re
     }
     c->mapped = true;
   }
-  // Per relation: adj[dg] = (index of my run dg in its receiver's buffer) - (its start
-  // in my digit order), and seg[d] = start of local digit d in MY receive buffer.
-  const size_t tab_n = 2 * (size_t)D1 + 2 * (size_t)(L1 + 1);
-  uint32_t* htab = static_cast<uint32_t*>(pinned(ctx, "dist.tab", tab_n * 4));
   for (int rel = 0; rel < 2; ++rel) {
-    uint32_t* adj = htab + (size_t)rel * D1;
-    uint32_t* seg = htab + 2 * (size_t)D1 + (size_t)rel * (L1 + 1);
+    if (!X[rel]) continue;
+    // adj[dg] = (index of my run dg in its receiver's buffer) - (its start in my
+    // digit order); seg[d] = start of local digit d in MY receive buffer
+    const size_t tab_n = (size_t)D1 + L1 + 1;
+    const char* tn = rel ? "dist.tab.S" : "dist.tab.R";
+    uint32_t* htab = static_cast<uint32_t*>(pinned(ctx, tn, tab_n * 4));
+    uint32_t* adj = htab;
+    uint32_t* seg = htab + D1;
     uint64_t local = 0;
     for (int p = 0; p < G; ++p) {
       uint64_t at = 0;  // start of digit d in rank p's receive buffer
@@ -311,18 +319,18 @@ void dist_equi_count_fused(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_re
       }
       if (p == me) seg[L1] = (uint32_t)at;
     }
-  }
-  uint32_t* dtab = static_cast<uint32_t*>(ws(ctx, "dist.tab", tab_n * 4));
-  GJ_CUDA(cudaMemcpyAsync(dtab, htab, tab_n * 4, cudaMemcpyHostToDevice, ctx->stream));
-  for (int rel = 0; rel < 2; ++rel) {
+    uint32_t* dtab = static_cast<uint32_t*>(ws(ctx, tn, tab_n * 4));
+    GJ_CUDA(cudaMemcpyAsync(dtab, htab, tab_n * 4, cudaMemcpyHostToDevice, ctx->stream));
     ShuffleDest dst{};
     for (int p = 0; p < G; ++p) {
       dst.key[p] = p == me ? bufs[2 * rel] : c->peer_ptr[p][2 * rel];
       dst.rid[p] = static_cast<uint32_t*>(p == me ? bufs[2 * rel + 1] : c->peer_ptr[p][2 * rel + 1]);
     }
-    dst.adj = dtab + (size_t)rel * D1;
+    dst.adj = dtab;
     dst.lbits = b1;
-    shuffle_scatter(ctx, rel ? S : R, SP[rel], dst);
+    shuffle_scatter(ctx, *X[rel], SP[rel], dst);
+    out.X[rel] = gj_rel{bufs[2 * rel], static_cast<const uint32_t*>(bufs[2 * rel + 1]), need[me][rel], kt, 0};
+    out.seg[rel] = dtab + D1;
   }
   trace_sync(ctx, "fused: scatter");
   // every rank's NVLink stores are done before any local join reads its buffers
@@ -332,11 +340,125 @@ void dist_equi_count_fused(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_re
     GJ_NCCL(ncclAllReduce(z, z + 1, 1, ncclUint32, ncclSum, c->comm, ctx->stream));
   }
   trace_sync(ctx, "fused: barrier");
-  gj_rel RL{bufs[0], static_cast<const uint32_t*>(bufs[1]), nrecv[0], R.key_type, 0};
-  gj_rel SL{bufs[2], static_cast<const uint32_t*>(bufs[3]), nrecv[1], S.key_type, 0};
-  const uint32_t* segR = dtab + 2 * (size_t)D1;
-  join_count_core(ctx, RL, SL, g, b1, segR, segR + (L1 + 1));
+}
+
+void dist_equi_count_fused(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) {
+  const uint32_t g = log2_exact(c->nranks);
+  // b1 must be the same on every rank: it depends only on G and the ctx options.
+  // Default 0: with 512 digits the NVLink stores come in ~8-tuple runs and the
+  // shuffle scatter measured 3.1 ms vs 1.2 ms for 2 digits (2^27 tuples, N=2) --
+  // more than the local radix pass it saves (DESIGN.md §6).
+  uint32_t b1 = std::min<uint32_t>((uint32_t)ctx->shuffle_bits, 9 - g);
+  if (ctx->part_bits >= 0) b1 = std::min<uint32_t>(b1, (uint32_t)ctx->part_bits);
+  const gj_rel* X[2] = {&R, &S};
+  FusedOut o;
+  fused_shuffle(ctx, c, X, b1, o);
+  join_count_core(ctx, o.X[0], o.X[1], g, b1, o.seg[0], o.seg[1]);
   trace_sync(ctx, "fused: local join count");
+}
+
+// Pre-filtered distributed equi join (configs[4]):
+//  1. global key range: NCCL min/max all-reduce of the shards' biased min/max;
+//  2. R compacted to the range, then shuffled to its hash owners;
+//  3. every owner p builds a Bloom filter of the R keys it now holds; the G filters
+//     are all-gathered (grouped broadcasts; sizes follow from the count matrix);
+//  4. S compacted at the source by range AND the filter of each key's owner, so
+//     dropped S tuples never cross NVLink, then shuffled;
+//  5. two-sided: each owner drops its R tuples absent from the filter of its S
+//     survivors (R_p and S_p have the same owner: no communication);
+//  6. local partitioned hash join.
+// No false negatives at any step, so the union of the local joins is J(R, S).
+void dist_equi_count_filtered(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S, uint32_t flags,
+                              double bpk, uint64_t kept[2]) {
+  const int G = c->nranks, me = c->rank;
+  const uint32_t g = log2_exact(G);
+  if (G > MAX_RANKS) throw Error(GJ_EINVAL, "pre-filtered distributed join supports at most 8 ranks");
+  const size_t ks = R.key_type == GJ_I64 ? 8 : 4;
+  PfSpec spec;
+  if (flags & GJ_PF_RANGE) {
+    unsigned long long* mm = static_cast<unsigned long long*>(ws(ctx, "dpf.minmax", 4 * 8));
+    pf_minmax(ctx, R, mm);
+    pf_minmax(ctx, S, mm + 2);
+    GJ_NCCL(ncclGroupStart());
+    GJ_NCCL(ncclAllReduce(mm + 0, mm + 0, 1, ncclUint64, ncclMin, c->comm, ctx->stream));
+    GJ_NCCL(ncclAllReduce(mm + 1, mm + 1, 1, ncclUint64, ncclMax, c->comm, ctx->stream));
+    GJ_NCCL(ncclAllReduce(mm + 2, mm + 2, 1, ncclUint64, ncclMin, c->comm, ctx->stream));
+    GJ_NCCL(ncclAllReduce(mm + 3, mm + 3, 1, ncclUint64, ncclMax, c->comm, ctx->stream));
+    GJ_NCCL(ncclGroupEnd());
+    unsigned long long h[4];
+    d2h_sync(ctx, h, mm, sizeof(h));
+    spec.use_range = true;
+    if (h[0] > h[1] || h[2] > h[3]) {  // R or S is empty everywhere: nothing joins
+      spec.lo = 1;
+      spec.hi = 0;
+    } else {
+      spec.lo = std::max(h[0], h[2]);
+      spec.hi = std::min(h[1], h[3]);
+    }
+  }
+  // 2. R to its owners (range-compacted first)
+  gj_rel Rk = R;
+  if (spec.use_range) {
+    void* k = ws(ctx, "dpf.R.key", R.n * ks + 16);
+    uint32_t* r = static_cast<uint32_t*>(ws(ctx, "dpf.R.rid", R.n * 4 + 16));
+    Rk = gj_rel{k, r, pf_compact(ctx, R, spec, k, r, "dpfR"), R.key_type, 0};
+  }
+  FusedOut o;
+  {
+    const gj_rel* X[2] = {&Rk, nullptr};
+    fused_shuffle(ctx, c, X, 0, o);
+  }
+  gj_rel RL = o.X[0];
+  // 3. per-owner Bloom filters of R, all-gathered
+  PfSpec sspec = spec;
+  if (flags & GJ_PF_BLOOM) {
+    uint64_t total = 0;
+    for (int p = 0; p < G; ++p) {
+      sspec.logb[p] = pf_log_blocks(o.need[p][0], bpk);
+      sspec.woff[p] = total;
+      total += 8ull << sspec.logb[p];
+    }
+    uint32_t* words = static_cast<uint32_t*>(ws(ctx, "dpf.filters", total * 4));
+    pf_bloom_into(ctx, RL, words + sspec.woff[me], sspec.logb[me]);
+    {
+      RegionScope rs(ctx, "nccl_allgather_bloom");
+      GJ_NCCL(ncclGroupStart());
+      for (int p = 0; p < G; ++p)
+        GJ_NCCL(ncclBroadcast(words + sspec.woff[p], words + sspec.woff[p], 8ull << sspec.logb[p], ncclUint32, p,
+                              c->comm, ctx->stream));
+      GJ_NCCL(ncclGroupEnd());
+    }
+    sspec.words = words;
+    sspec.nfilt = (uint32_t)G;
+    sspec.g = g;
+  }
+  // 4. S filtered at the source, then to its owners
+  gj_rel Sk = S;
+  if (sspec.use_range || sspec.nfilt) {
+    void* k = ws(ctx, "dpf.S.key", S.n * ks + 16);
+    uint32_t* r = static_cast<uint32_t*>(ws(ctx, "dpf.S.rid", S.n * 4 + 16));
+    Sk = gj_rel{k, r, pf_compact(ctx, S, sspec, k, r, "dpfS"), S.key_type, 0};
+  }
+  {
+    const gj_rel* X[2] = {nullptr, &Sk};
+    fused_shuffle(ctx, c, X, 0, o);
+  }
+  gj_rel SL = o.X[1];
+  // 5. two-sided: R_p by the filter of S_p's survivors
+  if ((flags & GJ_PF_TWO_SIDED) && (flags & GJ_PF_BLOOM)) {
+    PfSpec rspec;
+    rspec.logb[0] = pf_log_blocks(SL.n, bpk);
+    uint32_t* w = static_cast<uint32_t*>(ws(ctx, "dpf.filterS", (8ull << rspec.logb[0]) * 4));
+    pf_bloom_into(ctx, SL, w, rspec.logb[0]);
+    rspec.words = w;
+    rspec.nfilt = 1;
+    void* k = ws(ctx, "dpf.R2.key", RL.n * ks + 16);
+    uint32_t* r = static_cast<uint32_t*>(ws(ctx, "dpf.R2.rid", RL.n * 4 + 16));
+    RL = gj_rel{k, r, pf_compact(ctx, RL, rspec, k, r, "dpfR2"), R.key_type, 0};
+  }
+  kept[0] = RL.n;
+  kept[1] = SL.n;
+  join_count_core(ctx, RL, SL, g, 0, nullptr, nullptr);
 }
 
 void equi_count_any(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) {
@@ -482,6 +604,31 @@ gj_status join_dist_count(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, uint64_t*
   DAPI_END
 }
 
+gj_status join_dist_count_filtered(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, uint32_t flags,
+                                   double bloom_bits_per_key, uint64_t* n_local, uint64_t* n_global,
+                                   uint64_t* kept_local) {
+  DAPI_BEGIN
+  check_args(ctx, c, R, S);
+  if (!n_local || !n_global) throw Error(GJ_EINVAL, "NULL result pointer");
+  if (flags & ~(uint32_t)(GJ_PF_RANGE | GJ_PF_BLOOM | GJ_PF_TWO_SIDED)) throw Error(GJ_EINVAL, "unknown prefilter flag");
+  if ((flags & GJ_PF_BLOOM) && !(bloom_bits_per_key >= 1.0 && bloom_bits_per_key <= 64.0))
+    throw Error(GJ_EINVAL, "bloom_bits_per_key must be in [1, 64]");
+  c->eq_valid = false;
+  uint64_t kept[2] = {0, 0};
+  dist_equi_count_filtered(ctx, c, R, S, flags, bloom_bits_per_key, kept);
+  c->R = R;
+  c->S = S;
+  c->total = ctx->jc.total;
+  c->eq_valid = true;
+  *n_local = ctx->jc.total;
+  *n_global = allreduce_sum(ctx, c, ctx->jc.total);
+  if (kept_local) {
+    kept_local[0] = kept[0];
+    kept_local[1] = kept[1];
+  }
+  DAPI_END
+}
+
 gj_status join_dist_materialize(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, uint32_t* out, uint64_t capacity,
                                 uint64_t* n_written) {
   DAPI_BEGIN
@@ -554,6 +701,10 @@ gj_status gj_comm_unique_id(void*) { NO_NCCL; }
 gj_status gj_comm_init(gj_comm**, const void*, int, int) { NO_NCCL; }
 void gj_comm_destroy(gj_comm*) {}
 gj_status join_dist_count(gj_ctx*, gj_comm*, gj_rel, gj_rel, uint64_t*, uint64_t*) { NO_NCCL; }
+gj_status join_dist_count_filtered(gj_ctx*, gj_comm*, gj_rel, gj_rel, uint32_t, double, uint64_t*, uint64_t*,
+                                   uint64_t*) {
+  NO_NCCL;
+}
 gj_status join_dist_materialize(gj_ctx*, gj_comm*, gj_rel, gj_rel, uint32_t*, uint64_t, uint64_t*) { NO_NCCL; }
 gj_status theta_join_dist_count(gj_ctx*, gj_comm*, gj_rel, gj_rel, int, uint64_t, uint64_t*, uint64_t*) { NO_NCCL; }
 gj_status theta_join_dist_materialize(gj_ctx*, gj_comm*, gj_rel, gj_rel, int, uint64_t, uint32_t*, uint64_t,

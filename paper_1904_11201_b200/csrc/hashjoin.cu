@@ -6,9 +6,10 @@
 // hash buckets with a small-range probe.  B200 design (DESIGN.md
 // §4.2): after radix partitioning both relations with the same hash bits, every
 // work unit u = (partition p, build chunk, probe chunk) builds an open-addressing
-// (linear probing) table of <= 2048 build tuples in shared memory, sized 2x the
-// chunk from the exact partition histogram -- so it can never overflow (the paper's
-// fixed-size buckets could) -- and streams the probe chunk past it.
+// (linear probing) table of <= 2048 build tuples in shared memory, ~4 slots per
+// build tuple (<= 4096) sized from the exact unit size -- so it can never overflow
+// (the paper's fixed-size buckets could) -- and streams the probe
+// chunk (<= 2048 tuples) past it.
 // Units have bounded cost (<= 2048 x 2048 tuples), so Zipf-skewed partitions
 // (configs[2]) split into many units instead of serialising one CTA.  CTAs take
 // units round-robin (u = blockIdx.x + k * gridDim.x) from a precomputed descriptor

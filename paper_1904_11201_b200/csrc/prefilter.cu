@@ -15,6 +15,7 @@
 
 #include "common.cuh"
 #include "nlj.cuh"
+#include "prefilter.cuh"
 #include "runtime.h"
 #include "scan.cuh"
 
@@ -33,6 +34,10 @@ struct Filt {
   int use_range;
   const uint32_t* bloom;      // nblocks * 8 words, or nullptr
   uint32_t log_blocks;
+  // distributed join: one filter per shuffle destination (used when nfilt > 0)
+  uint32_t nfilt, g;
+  uint64_t woff[MAX_RANKS];
+  uint32_t logb[MAX_RANKS];
 };
 
 __device__ __forceinline__ uint64_t bloom_hash(int32_t k) {
@@ -78,8 +83,15 @@ __device__ __forceinline__ bool keep(K k, const Filt& f) {
     if (b < f.lo || b > f.hi) return false;
   }
   if (f.bloom) {
-    const BloomSlot s = bloom_slot(k, f.log_blocks);
-    const uint4* p = reinterpret_cast<const uint4*>(f.bloom + (uint64_t)s.block * 8);
+    const uint32_t* words = f.bloom;
+    uint32_t lb = f.log_blocks;
+    if (f.nfilt) {  // the filter of the key's destination rank
+      const uint32_t d = f.g ? khash(k) >> (32 - f.g) : 0u;
+      words += f.woff[d];
+      lb = f.logb[d];
+    }
+    const BloomSlot s = bloom_slot(k, lb);
+    const uint4* p = reinterpret_cast<const uint4*>(words + (uint64_t)s.block * 8);
     const uint4 a = __ldg(p), c = __ldg(p + 1);
     const uint32_t wv[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
     bool ok = true;
@@ -185,12 +197,17 @@ uint64_t compact(gj_ctx* ctx, const gj_rel& X, const Filt& f, void* kout, uint32
   return h;
 }
 
+uint32_t log_blocks_for(uint64_t n, double bpk) {
+  const double bits = std::max(256.0, (double)n * bpk);
+  uint32_t lb = 0;
+  while ((256.0 * (double)(1ull << lb)) < bits && lb < 40) ++lb;
+  return lb;
+}
+
 template <typename K>
 const uint32_t* build_bloom(gj_ctx* ctx, const gj_rel& X, const Filt& range, double bpk, uint32_t* log_blocks,
                             const char* tag) {
-  const double bits = std::max(256.0, (double)X.n * bpk);
-  uint32_t lb = 0;
-  while ((256.0 * (double)(1ull << lb)) < bits && lb < 40) ++lb;
+  const uint32_t lb = log_blocks_for(X.n, bpk);
   *log_blocks = lb;
   const uint64_t words = (1ull << lb) * 8;
   uint32_t* bloom = static_cast<uint32_t*>(ws(ctx, tag, words * sizeof(uint32_t)));
@@ -250,7 +267,47 @@ void prefilter_t(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t flags, 
   }
 }
 
+Filt to_filt(const PfSpec& p) {
+  Filt f{};
+  f.lo = p.lo;
+  f.hi = p.hi;
+  f.use_range = p.use_range ? 1 : 0;
+  f.bloom = p.nfilt ? p.words : nullptr;
+  f.nfilt = p.nfilt;
+  f.g = p.g;
+  for (int i = 0; i < MAX_RANKS; ++i) {
+    f.woff[i] = p.woff[i];
+    f.logb[i] = p.logb[i];
+  }
+  return f;
+}
+
 }  // namespace
+
+uint32_t pf_log_blocks(uint64_t n, double bpk) { return log_blocks_for(n, bpk); }
+
+void pf_bloom_into(gj_ctx* ctx, const gj_rel& X, uint32_t* words, uint32_t logb) {
+  GJ_CUDA(cudaMemsetAsync(words, 0, (8ull << logb) * sizeof(uint32_t), ctx->stream));
+  if (X.n == 0) return;
+  Filt none{};
+  none.lo = 0;
+  none.hi = ~0ull;
+  const unsigned grid = (unsigned)std::min<uint64_t>((X.n + 255) / 256, (uint64_t)ctx->num_sms * 16);
+  if (X.key_type == GJ_I32)
+    launch(ctx, "bloom_build", bloom_build<int32_t>, dim3(grid), dim3(256), 0, static_cast<const int32_t*>(X.key),
+           X.n, none, words, logb);
+  else
+    launch(ctx, "bloom_build", bloom_build<int64_t>, dim3(grid), dim3(256), 0, static_cast<const int64_t*>(X.key),
+           X.n, none, words, logb);
+}
+
+uint64_t pf_compact(gj_ctx* ctx, const gj_rel& X, const PfSpec& spec, void* kout, uint32_t* rout, const char* tag) {
+  const Filt f = to_filt(spec);
+  if (X.key_type == GJ_I32) return compact<int32_t>(ctx, X, f, kout, rout, tag);
+  return compact<int64_t>(ctx, X, f, kout, rout, tag);
+}
+
+void pf_minmax(gj_ctx* ctx, const gj_rel& X, unsigned long long* mm) { key_minmax(ctx, X, mm); }
 
 gj_status prefilter_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t flags, int op, uint64_t eps,
                          double bpk, void* kR, uint32_t* rR, uint64_t* nRo, void* kS, uint32_t* rS,

@@ -1,0 +1,34 @@
+// prefilter.cuh -- pieces of the range/Bloom pre-filter (§3.1)
+// reused by the distributed pre-filtered equi join (dist.cu).
+#pragma once
+
+#include <cstdint>
+
+#include "partition.cuh"
+#include "runtime.h"
+
+namespace gj {
+
+// Keep-predicate of a compaction: biased key in [lo, hi] (if use_range) and, if
+// nfilt > 0, present in the Bloom filter of the key's shuffle destination
+// d = khash(key) >> (32 - g) (d = 0 if g = 0): words + woff[d], 2^logb[d] blocks.
+struct PfSpec {
+  unsigned long long lo = 0, hi = ~0ull;
+  bool use_range = false;
+  const uint32_t* words = nullptr;
+  uint32_t nfilt = 0, g = 0;
+  uint64_t woff[MAX_RANKS] = {};
+  uint32_t logb[MAX_RANKS] = {};
+};
+
+// log2 of the number of 256-bit blocks of a filter for n keys at bpk bits per key.
+uint32_t pf_log_blocks(uint64_t n, double bpk);
+// Bloom filter of X's keys into `words` (8 << logb uint32, zeroed here).
+void pf_bloom_into(gj_ctx* ctx, const gj_rel& X, uint32_t* words, uint32_t logb);
+// Stable compaction of X by the spec into kout / rout (X.n entries each); returns
+// the number of survivors (synchronises the stream).  Survivors keep their rids.
+uint64_t pf_compact(gj_ctx* ctx, const gj_rel& X, const PfSpec& spec, void* kout, uint32_t* rout, const char* tag);
+// Device min / max of X's biased keys into mm[0], mm[1] (empty X: ~0, 0).
+void pf_minmax(gj_ctx* ctx, const gj_rel& X, unsigned long long* mm);
+
+}  // namespace gj

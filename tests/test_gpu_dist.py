@@ -18,6 +18,15 @@ def _free_port():
     return p
 
 
+C5_FLAGS = (7, 1, 2)  # RANGE|BLOOM|TWO_SIDED, RANGE only, BLOOM only
+
+
+def _c5_inputs():
+    """gen.c5 over a 2^16-row domain: R = 2*perm(i) unique, S 10% members else odd keys."""
+    import gen
+    return gen.c5(1 << 16, 1 << 18, seed=21, b=16)
+
+
 def _i64_inputs():
     """int64 keys spread over +-2^56 (upper hash bits exercised), duplicates on both sides."""
     import gen
@@ -82,6 +91,18 @@ def _worker(rank, world, port, q):
         S4 = gj.Rel(torch.from_numpy(S4all[s0:s1]).cuda(), None, s0)
         nl, ng = gj.join_dist_count(ctx, comm, R4, S4)
         out["i64"] = (nl, ng, gj.join_dist_materialize(ctx, comm, R4, S4, nl).cpu().numpy().view(np.uint32))
+        # configs[4] shape (int64, 10% S members), pre-filtered join: range by all-reduce,
+        # R shuffled first, per-owner Bloom filters all-gathered, S filtered at the source
+        R5all, S5all, _ = _c5_inputs()
+        a0, a1 = (rank * len(R5all)) // world, ((rank + 1) * len(R5all)) // world
+        c0, c1 = (rank * len(S5all)) // world, ((rank + 1) * len(S5all)) // world
+        R5 = gj.Rel(torch.from_numpy(R5all[a0:a1]).cuda(), None, a0)
+        S5 = gj.Rel(torch.from_numpy(S5all[c0:c1]).cuda(), None, c0)
+        for flags in C5_FLAGS:
+            nl, ng, kept = gj.join_dist_count_filtered(ctx, comm, R5, S5, flags, 8.0)
+            out[f"c5pf{flags}"] = (nl, ng, gj.join_dist_materialize(ctx, comm, R5, S5, nl).cpu().numpy().view(
+                np.uint32))
+            out[f"kept{flags}"] = kept
         # theta band: R replicated, S sharded
         R3all = gen.uniform_keys(5000, 1 << 20, 8, 0)
         S3all = gen.uniform_keys(20_000, 1 << 20, 8, 1)
@@ -138,6 +159,23 @@ def test_dist_joins_match_oracle(world):
     pk = oracle.pkfk_closed_form(m)
     expect = {"equi": pk, "equi_sb6": pk, "dup": dup, "dup_pb3": dup,
               "i64": oracle.hash_equi(R4all, S4all), "band": oracle.band_materialize(R3all, S3all, 40)}
+    R5all, S5all, m5 = _c5_inputs()
+    import paper_1904_11201_b200 as gj
+    pk5 = oracle.pkfk_closed_form(m5)
+    members = int((m5 >= 0).sum())
+    lo, hi = max(R5all.min(), S5all.min()), min(R5all.max(), S5all.max())
+    in_range = (int(((R5all >= lo) & (R5all <= hi)).sum()), int(((S5all >= lo) & (S5all <= hi)).sum()))
+    for flags in C5_FLAGS:
+        expect[f"c5pf{flags}"] = pk5
+        kept_R = sum(res[r][f"kept{flags}"][0] for r in range(world))
+        kept_S = sum(res[r][f"kept{flags}"][1] for r in range(world))
+        assert members <= kept_S <= len(S5all), flags  # no false negatives
+        if flags == gj.RANGE:
+            assert (kept_R, kept_S) == in_range, flags
+        if flags & gj.BLOOM:  # 8 bits/key: ~2-3% false positives among the 90% non-members
+            assert kept_S < members + 0.08 * len(S5all), (flags, kept_S)
+        if flags & gj.TWO_SIDED:
+            assert kept_R < len(R5all), flags
     for name, (cnt, pairs) in expect.items():
         locals_ = [res[r][name] for r in range(world)]
         assert all(l[1] == cnt for l in locals_), name  # n_global

@@ -93,6 +93,9 @@ def test_device_generator_matches_numpy(gj):
     assert np.array_equal(gd.zipf_S(n, 16, gd.zipf_table_device(1 << 16), 4).cpu().numpy(), Sz)
     R5, S5, m5 = gen.c5(1 << 10, n, seed=8)
     assert np.array_equal(gd.c5_S(n, 8).cpu().numpy(), S5)
+    R5b, S5b, _ = gen.c5(1 << 10, n, seed=8, r_offset=77, s_offset=5, b=20)
+    assert np.array_equal(gd.c5_S(n, 8, offset=5, b=20).cpu().numpy(), S5b)
+    assert np.array_equal(gd.c5_R(1 << 10, 8, offset=77, b=20).cpu().numpy(), R5b)
     assert np.array_equal(gd.perm_range(1 << 10, 31, 8, mult=2, dtype=torch.int64).cpu().numpy(), R5)
 
 

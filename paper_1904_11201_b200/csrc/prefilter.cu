@@ -53,7 +53,10 @@ __device__ __forceinline__ uint64_t bloom_hash(int64_t k) {
   return h ^ (h >> 32);
 }
 
-// Block index from the top bits, the 8 bit positions (0..255) from a remix.
+// Split-block Bloom filter: the block index from the top bits of the hash, then ONE
+// bit in each of the block's 8 words (bit positions from a remix), so a key sets 8
+// bits inside one 32-byte sector, its mask costs 8 shifts, an insert is 4 64-bit
+// atomicOr and a probe one 32-byte sector read.
 struct BloomSlot {
   uint32_t block;
   uint32_t mask[8];
@@ -65,22 +68,16 @@ __device__ __forceinline__ BloomSlot bloom_slot(K k, uint32_t log_blocks) {
   b.block = log_blocks ? (uint32_t)(h >> (64 - log_blocks)) : 0u;
   const uint64_t h2 = (h ^ (h >> 31)) * 0x9E3779B97F4A7C15ull;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) b.mask[i] = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t pos = (uint32_t)(h2 >> (8 * i)) & 255u;
-#pragma unroll
-    for (int w = 0; w < 8; ++w)
-      if ((pos >> 5) == (uint32_t)w) b.mask[w] |= 1u << (pos & 31);
-  }
+  for (int w = 0; w < 8; ++w) b.mask[w] = 1u << ((uint32_t)(h2 >> (24 + 5 * w)) & 31u);
   return b;
 }
 
 template <typename K>
 __device__ __forceinline__ bool keep(K k, const Filt& f) {
+  bool ok = true;
   if (f.use_range) {
     const unsigned long long b = (unsigned long long)KeyT<K>::bias(k);
-    if (b < f.lo || b > f.hi) return false;
+    ok = b >= f.lo && b <= f.hi;
   }
   if (f.bloom) {
     const uint32_t* words = f.bloom;
@@ -91,15 +88,15 @@ __device__ __forceinline__ bool keep(K k, const Filt& f) {
       lb = f.logb[d];
     }
     const BloomSlot s = bloom_slot(k, lb);
-    const uint4* p = reinterpret_cast<const uint4*>(words + (uint64_t)s.block * 8);
-    const uint4 a = __ldg(p), c = __ldg(p + 1);
-    const uint32_t wv[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
-    bool ok = true;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) ok &= (wv[w] & s.mask[w]) == s.mask[w];
-    return ok;
+    if (ok) {  // predicated sector read: out-of-range keys cost no probe
+      const uint4* p = reinterpret_cast<const uint4*>(words + (uint64_t)s.block * 8);
+      const uint4 a = __ldg(p), c = __ldg(p + 1);
+      ok = ((a.x & s.mask[0]) != 0) & ((a.y & s.mask[1]) != 0) & ((a.z & s.mask[2]) != 0) &
+           ((a.w & s.mask[3]) != 0) & ((c.x & s.mask[4]) != 0) & ((c.y & s.mask[5]) != 0) &
+           ((c.z & s.mask[6]) != 0) & ((c.w & s.mask[7]) != 0);
+    }
   }
-  return true;
+  return ok;
 }
 
 template <typename K>
@@ -109,53 +106,68 @@ __global__ void bloom_build(const K* __restrict__ key, uint64_t n, Filt range, u
     const K k = key[i];
     if (!keep(k, range)) continue;
     const BloomSlot s = bloom_slot(k, log_blocks);
+    unsigned long long* bw = reinterpret_cast<unsigned long long*>(bloom + (uint64_t)s.block * 8);
 #pragma unroll
-    for (int w = 0; w < 8; ++w)
-      if (s.mask[w]) atomicOr(&bloom[(uint64_t)s.block * 8 + w], s.mask[w]);
+    for (int w = 0; w < 4; ++w)
+      atomicOr(&bw[w], (unsigned long long)s.mask[2 * w] | ((unsigned long long)s.mask[2 * w + 1] << 32));
   }
 }
 
+// Keep-flags pass: warp w of a tile owns rows [w*32*FI, (w+1)*32*FI) in 32-row
+// groups; each group's ballot is stored as one flag word (bit = lane), so the write
+// pass needs no second probe.  8 probes per thread are independent (in flight at once).
 template <typename K>
 __global__ void __launch_bounds__(FT) pf_count(const K* __restrict__ key, uint64_t n, Filt f,
-                                               uint32_t* __restrict__ tile_cnt) {
-  const uint64_t beg = (uint64_t)blockIdx.x * FTILE;
+                                               uint32_t* __restrict__ flags, uint32_t* __restrict__ tile_cnt) {
+  const uint32_t w = threadIdx.x >> 5, lane = lane_id();
+  const uint64_t wb = (uint64_t)blockIdx.x * FTILE + (uint64_t)w * 32 * FI;
   uint32_t c = 0;
-#pragma unroll 4
-  for (int k = 0; k < FI; ++k) {
-    const uint64_t i = beg + (uint64_t)k * FT + threadIdx.x;
-    if (i < n) c += keep(key[i], f);
+#pragma unroll
+  for (int h = 0; h < FI; h += 8) {
+    K k[8];
+    bool ok[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint64_t i = wb + (uint64_t)(h + j) * 32 + lane;
+      k[j] = i < n ? key[i] : K(0);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ok[j] = (wb + (uint64_t)(h + j) * 32 + lane < n) && keep(k[j], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t bal = __ballot_sync(FULL, ok[j]);
+      const uint64_t row0 = wb + (uint64_t)(h + j) * 32;
+      if (lane == 0 && row0 < n) flags[row0 >> 5] = bal;
+      c += __popc(bal);
+    }
   }
   __shared__ uint32_t red[FT / 32];
-  c = warp_sum(c);
-  if (lane_id() == 0) red[threadIdx.x >> 5] = c;
+  if (lane == 0) red[w] = c;
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t t = 0;
-    for (int w = 0; w < FT / 32; ++w) t += red[w];
+    for (int ww = 0; ww < FT / 32; ++ww) t += red[ww];
     tile_cnt[blockIdx.x] = t;
   }
 }
 
-// Stable compaction: warp w owns tile items [w*32*FI, (w+1)*32*FI) in order.
+// Stable compaction from the flag words: survivors' keys/rids only are read.
 template <typename K>
 __global__ void __launch_bounds__(FT) pf_write(const K* __restrict__ key, const uint32_t* __restrict__ rid,
-                                               uint32_t rid_base, uint64_t n, Filt f,
+                                               uint32_t rid_base, uint64_t n, const uint32_t* __restrict__ flags,
                                                const uint32_t* __restrict__ tile_off, K* __restrict__ kout,
                                                uint32_t* __restrict__ rout) {
   __shared__ uint32_t woff[FT / 32];
   const uint32_t w = threadIdx.x >> 5, lane = lane_id();
-  const uint64_t beg = (uint64_t)blockIdx.x * FTILE + (uint64_t)w * 32 * FI;
-  K k[FI];
-  uint32_t fl = 0;
-#pragma unroll
-  for (int j = 0; j < FI; ++j) {
-    const uint64_t i = beg + (uint64_t)j * 32 + lane;
-    k[j] = i < n ? key[i] : K(0);
-    if (i < n && keep(k[j], f)) fl |= 1u << j;
-  }
+  const uint64_t wb = (uint64_t)blockIdx.x * FTILE + (uint64_t)w * 32 * FI;
+  uint32_t fw[FI];
   uint32_t cnt = 0;
 #pragma unroll
-  for (int j = 0; j < FI; ++j) cnt += __popc(__ballot_sync(FULL, (fl >> j) & 1));
+  for (int j = 0; j < FI; ++j) {
+    const uint64_t row0 = wb + (uint64_t)j * 32;
+    fw[j] = row0 < n ? flags[row0 >> 5] : 0u;
+    cnt += __popc(fw[j]);
+  }
   if (lane == 0) woff[w] = cnt;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -168,17 +180,16 @@ __global__ void __launch_bounds__(FT) pf_write(const K* __restrict__ key, const 
   }
   __syncthreads();
   uint32_t pos = woff[w];
+  const uint32_t lt = lanemask_lt();
 #pragma unroll
   for (int j = 0; j < FI; ++j) {
-    const bool p = (fl >> j) & 1;
-    const uint32_t bal = __ballot_sync(FULL, p);
-    if (p) {
-      const uint64_t i = beg + (uint64_t)j * 32 + lane;
-      const uint32_t o = pos + __popc(bal & lanemask_lt());
-      kout[o] = k[j];
+    if ((fw[j] >> lane) & 1u) {
+      const uint64_t i = wb + (uint64_t)j * 32 + lane;
+      const uint32_t o = pos + __popc(fw[j] & lt);
+      kout[o] = key[i];
       rout[o] = rid ? rid[i] : rid_base + (uint32_t)i;
     }
-    pos += __popc(bal);
+    pos += __popc(fw[j]);
   }
 }
 
@@ -188,10 +199,12 @@ uint64_t compact(gj_ctx* ctx, const gj_rel& X, const Filt& f, void* kout, uint32
   const uint64_t ntiles = (X.n + FTILE - 1) / FTILE;
   std::string t(tag);
   uint32_t* cnt = static_cast<uint32_t*>(ws(ctx, (t + ".pfcnt").c_str(), (ntiles + 1) * sizeof(uint32_t)));
-  launch(ctx, "pf_count", pf_count<K>, dim3((unsigned)ntiles), dim3(FT), 0, static_cast<const K*>(X.key), X.n, f, cnt);
+  uint32_t* flags = static_cast<uint32_t*>(ws(ctx, "pf.flags", ntiles * (FTILE / 32) * sizeof(uint32_t)));
+  launch(ctx, "pf_count", pf_count<K>, dim3((unsigned)ntiles), dim3(FT), 0, static_cast<const K*>(X.key), X.n, f,
+         flags, cnt);
   exclusive_scan<uint32_t, uint32_t>(ctx, cnt, cnt, ntiles, cnt + ntiles);
   launch(ctx, "pf_write", pf_write<K>, dim3((unsigned)ntiles), dim3(FT), 0, static_cast<const K*>(X.key), X.rid,
-         X.rid_base, X.n, f, (const uint32_t*)cnt, static_cast<K*>(kout), rout);
+         X.rid_base, X.n, (const uint32_t*)flags, (const uint32_t*)cnt, static_cast<K*>(kout), rout);
   uint32_t h = 0;
   d2h_sync(ctx, &h, cnt + ntiles, sizeof(uint32_t));
   return h;

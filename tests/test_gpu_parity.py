@@ -210,6 +210,35 @@ def test_equi_zipf_skew(gj, ctx):
     assert np.array_equal(canon_gpu(gj.join_materialize(ctx, dev(R), dev(S), n)), cp)
 
 
+@pytest.mark.timeout(900)
+def test_equi_zipf_c3_full_size(gj, ctx):
+    """configs[2] at full size on one GPU: R = perm_28(i) (2^28 unique keys), S = 2^30 Zipf(1)
+    FK draws (the hot key is ~5% of S).  O8: J = {(m_j, j)}, m_j = the R row drawn for S row j.
+    Since R's keys are unique, the output equals J iff |J| = n_S, every S rid occurs exactly once,
+    each pair's keys are equal (all 2^30 pairs checked on the device), and sampled pairs match
+    the closed form evaluated on the host from the generator alone."""
+    import gen.device as gd
+    b, nS, seed = 28, 1 << 30, gen.BASE_SEED
+    q = gen.zipf_table(1 << b)
+    R = gd.perm_range(1 << b, b, seed)
+    S = gd.zipf_S(nS, b, torch.from_numpy(q.view(np.int64)).cuda(), seed)
+    n = gj.join_count(ctx, R, S)
+    assert n == nS
+    out = gj.join_materialize(ctx, R, S, n)
+    rr, rs = out[:, 0].long(), out[:, 1].long()
+    del out
+    seen = torch.zeros(nS, dtype=torch.uint8, device=rr.device)
+    seen[rs] = 1
+    assert bool(seen.all())  # n_S pairs, every S row once
+    del seen
+    assert torch.equal(R[rr], S[rs])  # each pair joins equal keys
+    r_of_s = torch.empty(nS, dtype=torch.int64, device=rr.device)
+    r_of_s[rs] = rr
+    js = np.unique(gen.uniform(2048, nS, 99, 0).astype(np.int64))
+    m = np.array([gen.zipf_ranks(1, q, seed, 1, offset=int(j))[0] for j in js], dtype=np.int64)
+    assert np.array_equal(r_of_s[torch.from_numpy(js).cuda()].cpu().numpy(), m)
+
+
 def test_equi_deterministic_positions(gj, ctx):
     R, S, _ = gen.pkfk(16, 200_000, seed=3)
     tR, tS = dev(R), dev(S)

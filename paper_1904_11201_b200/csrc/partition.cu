@@ -18,6 +18,8 @@
 // a tile, keys are ranked with warp-private counters (shared-memory fetch-add),
 // staged in shared memory in digit order, and each digit run is written back with
 // consecutive threads on consecutive addresses.  Stable, deterministic.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "partition.cuh"
 #include "scan.cuh"
@@ -32,6 +34,7 @@ constexpr int TPC = 16;          // tiles per chunk
 constexpr int CHUNK = TILE * TPC;  // 65536 tuples per chunk
 constexpr int NW = PT / 32;
 constexpr int MAX_BITS = 9;      // digits per pass <= 512
+constexpr int SCATTER_DEFAULT_V = 2;  // part_scatter variant (see launch_scatter_t)
 
 struct ChunkLoc {
   uint32_t total, seg, cb, nc;  // #chunks, segment, first chunk of segment, chunks in segment
@@ -126,38 +129,6 @@ __global__ void __launch_bounds__(PT) part_hist(const K* __restrict__ key, uint6
   for (uint32_t d = threadIdx.x; d < D; d += PT) out[(uint64_t)d * L.nc] = h[d];
 }
 
-// Exclusive scan in place of a[0..D) (D <= 2^MAX_BITS) by the whole CTA; thread t
-// owns EPT consecutive elements.  Ends with a barrier.
-__device__ __forceinline__ void cta_scan_small(uint32_t* a, uint32_t D, uint32_t* wt) {
-  constexpr int EPT = ((1 << MAX_BITS) + PT - 1) / PT;
-  const uint32_t t = threadIdx.x;
-  uint32_t v[EPT];
-  uint32_t s = 0;
-#pragma unroll
-  for (int e = 0; e < EPT; ++e) {
-    const uint32_t i = t * EPT + e;
-    v[e] = i < D ? a[i] : 0u;
-    s += v[e];
-  }
-  const uint32_t incl = warp_incl_scan(s);
-  if (lane_id() == 31) wt[t >> 5] = incl;
-  __syncthreads();
-  if (t < 32) {
-    const uint32_t x = t < NW ? wt[t] : 0;
-    const uint32_t xi = warp_incl_scan(x);
-    if (t < NW) wt[t] = xi - x;
-  }
-  __syncthreads();
-  uint32_t run = wt[t >> 5] + incl - s;
-#pragma unroll
-  for (int e = 0; e < EPT; ++e) {
-    const uint32_t i = t * EPT + e;
-    if (i < D) a[i] = run;
-    run += v[e];
-  }
-  __syncthreads();
-}
-
 // Tile descriptors for the scatter: (tile begin, tile length, index of the tile's
 // chunk column in the scanned histogram, chunks in its segment); length 0 = empty.
 __global__ void tile_desc_kernel(uint64_t n, const uint32_t* __restrict__ seg_off,
@@ -185,24 +156,51 @@ __global__ void tile_desc_kernel(uint64_t n, const uint32_t* __restrict__ seg_of
 // consumed input buffer then doubles as the digit-ordered staging area.
 // Per-digit offset of a tile = chunk run offset (scanned chunk histogram) + the
 // tile's in-chunk prefix row written by part_hist.
-template <typename K, bool HAS_RID>
-struct ScatterSmem {
-  static constexpr uint32_t KPAD = 16 / sizeof(K);  // room for the 16-byte alignment shift
-  K key[2][TILE + KPAD];
-  uint32_t rid[2][TILE + 4];
-  uint32_t whist[NW << MAX_BITS];
-  uint32_t dstart[1 << MAX_BITS];
-  uint32_t delta[1 << MAX_BITS];
-  uint64_t bar[2];
-  uint32_t wt[NW];
+// Shared-memory layout of the scatter (dynamic: the counter arrays follow D).
+//   buf[2] = {key[KB], rid[RB]}  double-buffered TMA input (rids only if HAS_RID);
+//            the consumed buffer is the staging area of the digit-ordered tile
+//            (ILV: one (key, rid) uint2 per slot across key[] and rid[])
+//   bar[2], wt[NW]
+//   whist[NW][PACK ? D/2 : D]  warp-private digit counters (PACK: two 16-bit
+//                              counters per word)
+//   delta[D]                   per digit: global position - tile-local position
+template <typename K, bool PACK>
+struct ScatterLayout {
+  // room for the 16-byte TMA alignment shift and the bulk-store run padding (<= 3 per run)
+  static constexpr uint32_t KB = TILE + 64;
+  static constexpr uint32_t RB = TILE + 64;
+  static constexpr size_t BUF = (size_t)KB * sizeof(K) + (size_t)RB * 4;
+  static constexpr size_t off_bar = 2 * BUF;
+  static constexpr size_t off_wt = off_bar + 16;
+  static constexpr size_t off_run = off_wt + 8 * NW;  // bulk path: tstart[16], sadj[16]
+  static constexpr size_t off_whist = off_run + 128;
+  static_assert(BUF % 16 == 0 && off_whist % 16 == 0, "16-byte aligned sections");
+  static __host__ __device__ uint32_t words(uint32_t D) { return PACK ? (D > 1 ? D / 2 : 1) : D; }
+  static size_t bytes(uint32_t D) { return off_whist + ((size_t)NW * words(D) + (size_t)D) * 4; }
 };
 
-template <typename K, bool HAS_RID>
-__device__ __forceinline__ void issue_tile(ScatterSmem<K, HAS_RID>& sm, uint32_t buf, const uint4 d,
+template <typename K, bool PACK>
+struct ScatterSmem {
+  using L = ScatterLayout<K, PACK>;
+  uint8_t* base;
+  __device__ K* key(uint32_t b) const { return reinterpret_cast<K*>(base + b * L::BUF); }
+  __device__ uint32_t* rid(uint32_t b) const {
+    return reinterpret_cast<uint32_t*>(base + b * L::BUF + (size_t)L::KB * sizeof(K));
+  }
+  __device__ uint2* stage(uint32_t b) const { return reinterpret_cast<uint2*>(base + b * L::BUF); }
+  __device__ uint64_t* bar() const { return reinterpret_cast<uint64_t*>(base + L::off_bar); }
+  __device__ uint32_t* wt() const { return reinterpret_cast<uint32_t*>(base + L::off_wt); }
+  __device__ uint32_t* whist() const { return reinterpret_cast<uint32_t*>(base + L::off_whist); }
+  __device__ uint32_t* run() const { return reinterpret_cast<uint32_t*>(base + L::off_run); }
+};
+
+template <typename K, bool HAS_RID, bool PACK>
+__device__ __forceinline__ void issue_tile(const ScatterSmem<K, PACK>& sm, uint32_t buf, const uint4 d,
                                            const K* key_in, const uint32_t* rid_in, uint64_t n) {
   fence_proxy_async();
+  uint64_t* bar = sm.bar() + buf;
   if (d.y == 0) {
-    mbar_arrive(&sm.bar[buf]);
+    mbar_arrive(bar);
     return;
   }
   const uint64_t kb0 = (uint64_t)d.x * sizeof(K), kb1 = (uint64_t)(d.x + d.y) * sizeof(K);
@@ -215,66 +213,90 @@ __device__ __forceinline__ void issue_tile(ScatterSmem<K, HAS_RID>& sm, uint32_t
     rz = min((rb1 + 15) & ~15ull, (n * 4) & ~15ull);
     if (rz > ra) bytes += (uint32_t)(rz - ra);
   }
-  mbar_expect_tx(&sm.bar[buf], bytes);
-  if (kz > ka) bulk_g2s(sm.key[buf], reinterpret_cast<const uint8_t*>(key_in) + ka, (uint32_t)(kz - ka), &sm.bar[buf]);
+  mbar_expect_tx(bar, bytes);
+  if (kz > ka) bulk_g2s(sm.key(buf), reinterpret_cast<const uint8_t*>(key_in) + ka, (uint32_t)(kz - ka), bar);
   if (HAS_RID && rz > ra)
-    bulk_g2s(sm.rid[buf], reinterpret_cast<const uint8_t*>(rid_in) + ra, (uint32_t)(rz - ra), &sm.bar[buf]);
+    bulk_g2s(sm.rid(buf), reinterpret_cast<const uint8_t*>(rid_in) + ra, (uint32_t)(rz - ra), bar);
 }
 
-// REMOTE (multi-GPU shuffle fused into the scatter): digit d = destination rank;
-// its run is written straight into rank d's receive buffers (peer pointers mapped
-// over NVLink through CUDA IPC) at key[d] / rid[d] + (position - base[d]), base[d]
-// being the run's start in this rank's digit order.
-template <typename K, bool HAS_RID, bool REMOTE>
+// REMOTE (multi-GPU shuffle fused into the scatter): run d's tuples go to rank
+// d >> dst.lbits at index position + dst.adj[d] of its receive buffers (peer
+// pointers mapped over NVLink through CUDA IPC).
+template <typename K, bool HAS_RID, bool REMOTE, bool PACK, bool ILV>
 __global__ void __launch_bounds__(PT) part_scatter(
     const K* __restrict__ key_in, const uint32_t* __restrict__ rid_in, uint32_t rid_base, uint64_t n,
     const uint4* __restrict__ tdesc, uint32_t ntiles, uint32_t shift, uint32_t bits,
     const uint32_t* __restrict__ scanned, const uint32_t* __restrict__ tile_pref, K* __restrict__ key_out,
     uint32_t* __restrict__ rid_out, ShuffleDest dst) {
+  static_assert(!ILV || sizeof(K) == 4, "interleaved staging holds 32-bit keys");
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  ScatterSmem<K, HAS_RID>& sm = *reinterpret_cast<ScatterSmem<K, HAS_RID>*>(smem_raw);
+  using L = ScatterLayout<K, PACK>;
+  const ScatterSmem<K, PACK> sm{smem_raw};
   const uint32_t D = 1u << bits, mask = D - 1;
+  const uint32_t W = L::words(D);  // counter words per warp
+  uint32_t* whist = sm.whist();
+  uint32_t* delta = whist + NW * W;
   const uint32_t w = threadIdx.x >> 5, lane = lane_id();
   const uint32_t G = gridDim.x;
+  // REMOTE with few destinations: each tile's runs are long (~TILE/D tuples), so they
+  // go out as 1-D TMA bulk stores (16-byte aligned middles) instead of thread stores
+  const bool bulk = REMOTE && !ILV && D <= 16;
+  uint32_t* tstart = sm.run();    // bulk: tile-local start of every run
+  uint32_t* sadj = tstart + 16;   // bulk: staging shift of every run (alignment padding)
   uint32_t t = blockIdx.x;
   if (t >= ntiles) return;
   if (threadIdx.x == 0) {
-    mbar_init(&sm.bar[0], 1);
-    mbar_init(&sm.bar[1], 1);
+    mbar_init(sm.bar() + 0, 1);
+    mbar_init(sm.bar() + 1, 1);
     fence_mbar_init();
-    issue_tile(sm, 0, tdesc[t], key_in, rid_in, n);
+    issue_tile<K, HAS_RID>(sm, 0, tdesc[t], key_in, rid_in, n);
   }
   __syncthreads();
-  constexpr int DPT = (1 << MAX_BITS) / PT;  // digits per thread (upper bound)
+  static_assert((1 << MAX_BITS) <= 2 * PT, "two digits per thread");
+  static_assert(MAX_BITS >= 1, "");
+  // counter of digit dg of warp ww: word, shift
+  // thread i owns digits i and i + H (H = D/2): consecutive threads touch consecutive
+  // words (no bank conflicts); PACK keeps digit i in the low and i + H in the high half
+  const uint32_t H = D > 1 ? D / 2 : 1;
+  auto cword = [&](uint32_t ww, uint32_t dg) -> uint32_t* { return whist + ww * W + (PACK ? (dg & (H - 1)) : dg); };
+  auto cshift = [&](uint32_t dg) -> uint32_t { return PACK ? (uint32_t)(dg >= H && D > 1) << 4 : 0u; };
 
   for (uint32_t it = 0; t < ntiles; t += G, ++it) {
     const uint32_t buf = it & 1;
     const uint4 d = tdesc[t];
-    if (threadIdx.x == 0 && t + G < ntiles) issue_tile(sm, buf ^ 1, tdesc[t + G], key_in, rid_in, n);
+    if (threadIdx.x == 0 && t + G < ntiles) {
+      if (bulk) bulk_wait_read();  // the bulk stores of the previous tile have read its staging
+      issue_tile<K, HAS_RID>(sm, buf ^ 1, tdesc[t + G], key_in, rid_in, n);
+    }
     const uint32_t cnt = d.y;
     if (cnt) {  // CTA-uniform
-      // this tile's run offsets: loads issued now, consumed after ranking
-      uint32_t g0[DPT], g1[DPT];
-#pragma unroll
-      for (int q = 0; q < DPT; ++q) {
-        const uint32_t dd = threadIdx.x + q * PT;
-        g0[q] = dd < D ? scanned[d.z + (uint64_t)dd * d.w] : 0u;
-        g1[q] = dd < D ? tile_pref[(uint64_t)t * D + dd] : 0u;
-        if (REMOTE) g1[q] += dd < D ? dst.adj[dd] : 0u;  // position -> receiver index
+      // this tile's run offsets for my two digits (i, i + H), i = threadIdx.x: loads
+      // issued now, consumed after ranking
+      const uint32_t da = threadIdx.x, db = threadIdx.x + H;
+      const bool ha = da < H && da < D, hb = D > 1 && da < H;
+      uint32_t g0a = 0, g0b = 0;
+      if (ha) {
+        g0a = scanned[d.z + (uint64_t)da * d.w] + tile_pref[(uint64_t)t * D + da];
+        if (REMOTE) g0a += dst.adj[da];  // position -> receiver index
       }
-      if (D >= 4) {
-        uint4* z = reinterpret_cast<uint4*>(sm.whist + w * D);
-        for (uint32_t i = lane; i < D / 4; i += 32) z[i] = make_uint4(0, 0, 0, 0);
-      } else if (lane < D) {
-        sm.whist[w * D + lane] = 0;
+      if (hb) {
+        g0b = scanned[d.z + (uint64_t)db * d.w] + tile_pref[(uint64_t)t * D + db];
+        if (REMOTE) g0b += dst.adj[db];
       }
-      mbar_wait(&sm.bar[buf], (it >> 1) & 1);
+      if (W >= 4) {
+        uint4* z = reinterpret_cast<uint4*>(whist + w * W);
+        for (uint32_t i = lane; i < W / 4; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+      } else if (lane < W) {
+        whist[w * W + lane] = 0;
+      }
+      mbar_wait(sm.bar() + buf, (it >> 1) & 1);
       const uint32_t ko = (d.x * (uint32_t)sizeof(K) & 15u) / (uint32_t)sizeof(K);
       const uint32_t ro = (d.x & 3u);
       const uint64_t kz = min((((uint64_t)(d.x + d.y) * sizeof(K)) + 15) & ~15ull, (n * sizeof(K)) & ~15ull);
       const uint32_t kvalid = (uint32_t)(kz / sizeof(K) > d.x ? kz / sizeof(K) - d.x : 0);  // keys inside the bulk copy
       const uint64_t rz = min((((uint64_t)(d.x + d.y) * 4) + 15) & ~15ull, (n * 4) & ~15ull);
       const uint32_t rvalid = (uint32_t)(rz / 4 > d.x ? rz / 4 - d.x : 0);
+      const K* kbuf = sm.key(buf);
       K k[PI];
       uint32_t rk[PI];  // (digit << 16) | rank among this warp's keys of that digit
       __syncwarp();
@@ -287,92 +309,233 @@ __global__ void __launch_bounds__(PT) part_scatter(
       for (int i = 0; i < PI; ++i) {
         const uint32_t j = (w * PI + i) * 32 + lane;
         const bool v = j < cnt;
-        k[i] = v ? (j < kvalid ? sm.key[buf][ko + j] : key_in[d.x + j]) : K(0);
+        k[i] = v ? (j < kvalid ? kbuf[ko + j] : key_in[d.x + j]) : K(0);
         const uint32_t dg = v ? digit_of(k[i], shift, mask) : 0u;
+        const uint32_t sh = cshift(dg);
         uint32_t r = 0;
-        if (v) r = atomicAdd(&sm.whist[w * D + dg], 1u);
+        if (v) r = (atomicAdd(cword(w, dg), 1u << sh) >> sh) & 0xffffu;
         rk[i] = v ? ((dg << 16) | r) : 0xffffffffu;
       }
       uint32_t rr[HAS_RID ? PI : 1];
       if (HAS_RID) {
+        const uint32_t* rbuf = sm.rid(buf);
 #pragma unroll
         for (int i = 0; i < PI; ++i) {
           const uint32_t j = (w * PI + i) * 32 + lane;
-          rr[i] = j < cnt ? (j < rvalid ? sm.rid[buf][ro + j] : rid_in[d.x + j]) : 0u;
+          rr[i] = j < cnt ? (j < rvalid ? rbuf[ro + j] : rid_in[d.x + j]) : 0u;
         }
       }
       __syncthreads();  // all inputs are in registers: the buffer becomes the staging area
-      for (uint32_t dd = threadIdx.x; dd < D; dd += PT) {
-        uint32_t acc = 0;
+      // Tile-local digit starts with one barrier: thread i owns digits i and i + H:
+      // exclusive column prefix over the warps, warp scans of both halves' totals,
+      // then every warp adds the totals of the warps before it (and the low half's
+      // grand total for the high half).
+      {
+        uint32_t ta = 0, tb = 0;  // totals of digits i, i + H
+        if (ha) {
+          if (PACK) {
+            uint32_t acc = 0;  // halves <= TILE: no carry
+#pragma unroll
+            for (int ww = 0; ww < NW; ++ww) {
+              uint32_t* c = whist + ww * W + da;
+              const uint32_t x = *c;
+              *c = acc;
+              acc += x;
+            }
+            ta = acc & 0xffffu;
+            tb = acc >> 16;
+          } else {
+#pragma unroll
+            for (int ww = 0; ww < NW; ++ww) {
+              uint32_t* c = whist + ww * W + da;
+              const uint32_t x = c[0];
+              c[0] = ta;
+              ta += x;
+              if (hb) {
+                const uint32_t y = c[H];
+                c[H] = tb;
+                tb += y;
+              }
+            }
+          }
+        }
+        const uint32_t ia = warp_incl_scan(ta), ib = warp_incl_scan(tb);
+        uint32_t* wt = sm.wt();  // [0, NW): low-half warp totals, [NW, 2 NW): high half
+        if (lane == 31) {
+          wt[w] = ia;
+          wt[NW + w] = ib;
+        }
+        __syncthreads();
+        uint32_t st_a = ia - ta, st_b = ib - tb, low = 0;
 #pragma unroll
         for (int ww = 0; ww < NW; ++ww) {
-          const uint32_t x = sm.whist[ww * D + dd];
-          sm.whist[ww * D + dd] = acc;
-          acc += x;
+          const uint32_t xa = wt[ww], xb = wt[NW + ww];
+          low += xa;
+          if ((uint32_t)ww < w) {
+            st_a += xa;
+            st_b += xb;
+          }
         }
-        sm.dstart[dd] = acc;
+        st_b += low;
+        if (ha) {
+          delta[da] = g0a - st_a;
+          if (hb) delta[db] = g0b - st_b;
+          if (bulk) {
+            tstart[da] = st_a;
+            if (hb) tstart[db] = st_b;
+          }
+          if (PACK) {
+            const uint32_t st = st_a | (st_b << 16);  // positions stay < 2 TILE: 16 bits
+#pragma unroll
+            for (int ww = 0; ww < NW; ++ww) whist[ww * W + da] += st;
+          } else {
+#pragma unroll
+            for (int ww = 0; ww < NW; ++ww) {
+              whist[ww * W + da] += st_a;
+              if (hb) whist[ww * W + db] += st_b;
+            }
+          }
+        }
       }
       __syncthreads();
-      cta_scan_small(sm.dstart, D, sm.wt);  // tile-local digit starts; ends with a barrier
-#pragma unroll
-      for (int q = 0; q < DPT; ++q) {
-        const uint32_t dd = threadIdx.x + q * PT;
-        if (dd < D) {
-          const uint32_t st = sm.dstart[dd];
-          sm.delta[dd] = g0[q] + g1[q] - st;
-#pragma unroll
-          for (int ww = 0; ww < NW; ++ww) sm.whist[ww * D + dd] += st;
+      if (bulk) {  // pad each run so that its staging start shares its destination's 16 B phase
+        if (threadIdx.x == 0) {
+          uint32_t pad = 0;
+          for (uint32_t r = 0; r < D; ++r) {
+            const uint32_t st = tstart[r], p = delta[r] + st;
+            pad += (p - (st + pad)) & 3u;
+            sadj[r] = pad;
+          }
         }
+        __syncthreads();
       }
-      __syncthreads();
-      K* skey = sm.key[buf];
-      uint32_t* srid = sm.rid[buf];
+      K* skey = sm.key(buf);
+      uint32_t* srid = sm.rid(buf);
+      uint2* stg = sm.stage(buf);
 #pragma unroll
       for (int i = 0; i < PI; ++i) {
         if (rk[i] != 0xffffffffu) {
-          const uint32_t pos = sm.whist[w * D + (rk[i] >> 16)] + (rk[i] & 0xffffu);
-          skey[pos] = k[i];
-          srid[pos] = HAS_RID ? rr[i] : rid_base + d.x + (w * PI + i) * 32 + lane;
+          const uint32_t dg = rk[i] >> 16, sh = cshift(dg);
+          const uint32_t pos = ((*cword(w, dg) >> sh) & 0xffffu) + (rk[i] & 0xffffu) + (bulk ? sadj[dg] : 0u);
+          const uint32_t rv = HAS_RID ? rr[i] : rid_base + d.x + (w * PI + i) * 32 + lane;
+          if (ILV) {
+            stg[pos] = make_uint2((uint32_t)k[i], rv);
+          } else {
+            skey[pos] = k[i];
+            srid[pos] = rv;
+          }
         }
       }
+      if (bulk) fence_proxy_async();  // every writer: staging stores -> async proxy (bulk reads)
       __syncthreads();
+      if (bulk) {
+        // run r: staged at [s, s + len), destination index p (s = p mod 4): threads
+        // store the unaligned head and tail, thread 0 the aligned middle in bulk
+        for (uint32_t r = w; r < D; r += NW) {
+          const uint32_t st = tstart[r], len = (r + 1 < D ? tstart[r + 1] : cnt) - st;
+          const uint32_t s0 = st + sadj[r], p = delta[r] + st;
+          const uint32_t head = min(len, (4u - (p & 3u)) & 3u), tail = (len - head) & 3u;
+          K* kd = static_cast<K*>(dst.key[r >> dst.lbits]);
+          uint32_t* rd = dst.rid[r >> dst.lbits];
+          if (lane < head) {
+            kd[p + lane] = skey[s0 + lane];
+            rd[p + lane] = srid[s0 + lane];
+          } else if (lane >= 4 && lane < 4 + tail) {
+            const uint32_t e = len - tail + (lane - 4);
+            kd[p + e] = skey[s0 + e];
+            rd[p + e] = srid[s0 + e];
+          }
+        }
+        if (threadIdx.x == 0) {
+          for (uint32_t r = 0; r < D; ++r) {
+            const uint32_t st = tstart[r], len = (r + 1 < D ? tstart[r + 1] : cnt) - st;
+            const uint32_t s0 = st + sadj[r], p = delta[r] + st;
+            const uint32_t head = min(len, (4u - (p & 3u)) & 3u), body = (len - head) & ~3u;
+            if (body) {
+              bulk_s2g(static_cast<K*>(dst.key[r >> dst.lbits]) + p + head, skey + s0 + head,
+                       body * (uint32_t)sizeof(K));
+              bulk_s2g(dst.rid[r >> dst.lbits] + p + head, srid + s0 + head, body * 4u);
+            }
+          }
+          bulk_commit();
+        }
+      }
 #pragma unroll 4
-      for (int i = 0; i < PI; ++i) {
+      for (int i = 0; i < PI && !bulk; ++i) {
         const uint32_t j = i * PT + threadIdx.x;
         if (j < cnt) {
-          const K kk = skey[j];
+          K kk;
+          uint32_t rv;
+          if (ILV) {
+            const uint2 e = stg[j];
+            kk = (K)e.x;
+            rv = e.y;
+          } else {
+            kk = skey[j];
+            rv = srid[j];
+          }
           const uint32_t dg = digit_of(kk, shift, mask);
-          const uint32_t pos = sm.delta[dg] + j;
+          const uint32_t pos = delta[dg] + j;
           if (REMOTE) {  // pos is already the index in the receiving rank's buffer
             const uint32_t p = dg >> dst.lbits;
             static_cast<K*>(dst.key[p])[pos] = kk;
-            dst.rid[p][pos] = srid[j];
+            dst.rid[p][pos] = rv;
           } else {
             key_out[pos] = kk;
-            rid_out[pos] = srid[j];
+            rid_out[pos] = rv;
           }
         }
       }
     } else {
-      mbar_wait(&sm.bar[buf], (it >> 1) & 1);
+      mbar_wait(sm.bar() + buf, (it >> 1) & 1);
     }
     __syncthreads();  // the buffer may be refilled by the next iteration's issue
   }
+  if (bulk && threadIdx.x == 0) bulk_wait_all();  // bulk stores complete
   if (REMOTE) __threadfence_system();  // peer writes performed before the kernel retires
 }
 
+template <typename K, bool HAS_RID, bool REMOTE, bool PACK, bool ILV>
+void launch_scatter_v(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
+                      const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* hist,
+                      const uint32_t* tile_pref, K* kout, uint32_t* rout, const ShuffleDest& dst) {
+  auto kern = part_scatter<K, HAS_RID, REMOTE, PACK, ILV>;
+  const size_t smem = ScatterLayout<K, PACK>::bytes(1u << bits);
+  static bool once = (set_smem(kern, ScatterLayout<K, PACK>::bytes(1u << MAX_BITS)), true);
+  (void)once;
+  int occ = 1;
+  GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PT, smem));
+  if (const char* e = std::getenv("GJ_SCATTER_OCC")) occ = std::min(occ, std::atoi(e));  // tuning experiments
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
+  launch(ctx, REMOTE ? "shuffle_scatter" : "part_scatter", kern, dim3(grid), dim3(PT), smem, kin, rin, rid_base, n,
+         tdesc, (uint32_t)ntiles, shift, bits, hist, tile_pref, kout, rout, dst);
+}
+
+// Variant selection (GJ_SCATTER_V, tuning experiments): 0 = plain counters +
+// separate key/rid staging, 1 = packed counters, 2 = interleaved staging, 3 = both.
 template <typename K, bool HAS_RID, bool REMOTE>
 void launch_scatter_t(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
                       const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* hist,
                       const uint32_t* tile_pref, K* kout, uint32_t* rout, const ShuffleDest& dst) {
-  const size_t smem = sizeof(ScatterSmem<K, HAS_RID>);
-  static bool once = (set_smem(part_scatter<K, HAS_RID, REMOTE>, smem), true);
-  (void)once;
-  int occ = 1;
-  GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, part_scatter<K, HAS_RID, REMOTE>, PT, smem));
-  const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
-  launch(ctx, REMOTE ? "shuffle_scatter" : "part_scatter", part_scatter<K, HAS_RID, REMOTE>, dim3(grid), dim3(PT),
-         smem, kin, rin, rid_base, n, tdesc, (uint32_t)ntiles, shift, bits, hist, tile_pref, kout, rout, dst);
+  static const int v = [] {
+    const char* e = std::getenv("GJ_SCATTER_V");
+    const int x = e ? std::atoi(e) : SCATTER_DEFAULT_V;
+    return REMOTE ? (x & 1) : x;  // the shuffle stages key/rid separately (bulk stores)
+  }();
+  if (sizeof(K) == 4 && (v & 2)) {
+    if (v & 1)
+      launch_scatter_v<K, HAS_RID, REMOTE, true, sizeof(K) == 4>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift,
+                                                                 bits, hist, tile_pref, kout, rout, dst);
+    else
+      launch_scatter_v<K, HAS_RID, REMOTE, false, sizeof(K) == 4>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift,
+                                                                  bits, hist, tile_pref, kout, rout, dst);
+  } else if (v & 1) {
+    launch_scatter_v<K, HAS_RID, REMOTE, true, false>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, hist,
+                                                      tile_pref, kout, rout, dst);
+  } else {
+    launch_scatter_v<K, HAS_RID, REMOTE, false, false>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, hist,
+                                                       tile_pref, kout, rout, dst);
+  }
 }
 
 template <typename K, bool REMOTE>

@@ -181,6 +181,18 @@ gj_status join_host(gj_ctx* ctx, const void* key_R_host, uint64_t n_R, const voi
                     uint64_t n_S, int key_type, uint32_t* out_host, uint64_t capacity,
                     uint64_t* n_out);
 
+/* A stream of independent equi joins from HOST buffers (pinned for full PCIe
+ * speed): batch b joins key_R[b] (n_R[b] keys) with key_S[b] (n_S[b]) and copies
+ * its pairs to out[b] (2*capacity[b] uint32), |J_b| -> n_out[b] (host arrays of
+ * nbatch entries).  Consecutive batches run on two internal streams with their own
+ * workspaces, so batch b+1's host->device copy overlaps batch b's device->host
+ * copy.  A batch whose capacity is short gets n_out set and no pairs copied; the
+ * call then returns GJ_ERANGE after finishing the others.  rids are row positions
+ * (rid_base 0).  Returns when every batch's pairs are in host memory. */
+gj_status join_host_batch(gj_ctx* ctx, int nbatch, const void* const* key_R, const uint64_t* n_R,
+                          const void* const* key_S, const uint64_t* n_S, int key_type,
+                          uint32_t* const* out, const uint64_t* capacity, uint64_t* n_out);
+
 /* ---------------------------------------------------------------- multi-GPU
  * One process per GPU.  Equi joins shard by hash partition (the B200 analogue of
  * the Hadoop shuffle of Alg.1 Map2): every rank runs one radix

@@ -78,6 +78,7 @@ def _load():
     L.theta_join_materialize.argtypes = [vp, _Rel, _Rel, i32, u64, vp, u64, pu64]
     L.prefilter.argtypes = [vp, _Rel, _Rel, u32, i32, u64, ctypes.c_double, vp, vp, pu64, vp, vp, pu64]
     L.join_host.argtypes = [vp, vp, u64, vp, u64, i32, vp, u64, pu64]
+    L.join_host_batch.argtypes = [vp, i32, vp, vp, vp, vp, i32, vp, vp, pu64]
     L.gj_comm_unique_id.argtypes = [vp]
     L.gj_comm_init.argtypes = [ctypes.POINTER(vp), vp, i32, i32]
     L.gj_comm_destroy.argtypes = [vp]
@@ -89,7 +90,8 @@ def _load():
     L.theta_join_dist_materialize.argtypes = [vp, vp, _Rel, _Rel, i32, u64, vp, u64, pu64]
     L.gj_dist_plan.argtypes = [pu64, i32, i32, pu64, pu64]
     for f in ("gj_ctx_create", "gj_ctx_set_stream", "gj_ctx_set_option", "join_count", "join_materialize",
-              "theta_join_count", "theta_join_materialize", "prefilter", "join_host", "gj_comm_unique_id",
+              "theta_join_count", "theta_join_materialize", "prefilter", "join_host", "join_host_batch",
+              "gj_comm_unique_id",
               "gj_comm_init", "join_dist_count", "join_dist_count_filtered", "join_dist_materialize",
               "theta_join_dist_count", "theta_join_dist_materialize", "gj_dist_plan"):
         getattr(L, f).restype = i32
@@ -102,6 +104,7 @@ lib = _load()
 ABI_SYMBOLS = ("gj_ctx_create", "gj_ctx_destroy", "gj_ctx_set_stream", "gj_last_error", "gj_ctx_set_option",
                "gj_ctx_launch_count", "gj_ctx_reset_stats", "gj_ctx_kernel_times", "join_count",
                "join_materialize", "theta_join_count", "theta_join_materialize", "prefilter", "join_host",
+               "join_host_batch",
                "gj_comm_unique_id", "gj_comm_init", "gj_comm_destroy", "join_dist_count", "join_dist_count_filtered",
                "join_dist_materialize", "theta_join_dist_count", "theta_join_dist_materialize", "gj_dist_plan")
 COMM_ID_BYTES = 128
@@ -262,6 +265,30 @@ def join_host(ctx: Context, key_R: torch.Tensor, key_S: torch.Tensor, out: torch
                          I32 if key_R.dtype == torch.int32 else I64,
                          ctypes.c_void_p(out.data_ptr()), out.shape[0], ctypes.byref(n)))
     return n.value
+
+
+def join_host_batch(ctx: Context, batches):
+    """A stream of independent equi joins from HOST tensors: batches = [(key_R, key_S, out), ...]
+    (as join_host).  Consecutive batches' transfers overlap on two internal streams.
+    Returns the list of |J_b|."""
+    nb = len(batches)
+    for kR, kS, o in batches:
+        for t in (kR, kS, o):
+            if t.is_cuda or not t.is_contiguous():
+                raise ValueError("join_host_batch takes contiguous HOST tensors")
+        if kR.dtype != kS.dtype or kR.dtype != batches[0][0].dtype or kR.dtype not in (torch.int32, torch.int64):
+            raise ValueError("keys must all be int32 or all int64")
+    vp, u64 = ctypes.c_void_p, ctypes.c_uint64
+    kR = (vp * nb)(*[b[0].data_ptr() for b in batches])
+    kS = (vp * nb)(*[b[1].data_ptr() for b in batches])
+    nR = (u64 * nb)(*[b[0].numel() for b in batches])
+    nS = (u64 * nb)(*[b[1].numel() for b in batches])
+    outs = (vp * nb)(*[b[2].data_ptr() for b in batches])
+    cap = (u64 * nb)(*[b[2].shape[0] for b in batches])
+    n = (u64 * nb)()
+    kt = I32 if nb == 0 or batches[0][0].dtype == torch.int32 else I64
+    _check(lib.join_host_batch(ctx.h, nb, kR, nR, kS, nS, kt, outs, cap, n))
+    return [n[i] for i in range(nb)]
 
 
 # ---------------------------------------------------------------- multi-GPU (NCCL)

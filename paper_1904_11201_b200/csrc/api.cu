@@ -252,6 +252,10 @@ gj_status gj_ctx_create(gj_ctx** out, int device, void* stream) {
 
 void gj_ctx_destroy(gj_ctx* ctx) {
   if (!ctx) return;
+  for (gj_ctx*& c : ctx->sub) {
+    gj_ctx_destroy(c);
+    c = nullptr;
+  }
   cudaStreamSynchronize(ctx->stream);
   for (auto& kv : ctx->bufs)
     if (kv.second.ptr) cudaFree(kv.second.ptr);
@@ -263,6 +267,7 @@ void gj_ctx_destroy(gj_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (auto& kv : ctx->pinned_bufs)
     if (kv.second.ptr) cudaFreeHost(kv.second.ptr);
+  if (ctx->owns_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
 
@@ -453,6 +458,80 @@ gj_status join_host(gj_ctx* ctx, const void* key_R_host, uint64_t n_R, const voi
     GJ_CUDA(cudaMemcpyAsync(out_host, dout, total * 8, cudaMemcpyDeviceToHost, ctx->stream));
   }
   GJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  API_END
+}
+
+gj_status join_host_batch(gj_ctx* ctx, int nbatch, const void* const* key_R, const uint64_t* n_R,
+                          const void* const* key_S, const uint64_t* n_S, int key_type, uint32_t* const* out,
+                          const uint64_t* capacity, uint64_t* n_out) {
+  API_BEGIN
+  if (!ctx || nbatch < 0 || (nbatch && (!key_R || !n_R || !key_S || !n_S || !out || !capacity || !n_out)))
+    throw Error(GJ_EINVAL, "join_host_batch: NULL argument");
+  if (key_type != GJ_I32 && key_type != GJ_I64) throw Error(GJ_EINVAL, "join_host_batch: bad key_type");
+  for (int b = 0; b < nbatch; ++b) {
+    if ((n_R[b] && !key_R[b]) || (n_S[b] && !key_S[b])) throw Error(GJ_EINVAL, "join_host_batch: NULL key buffer");
+    if (n_R[b] >= (1ull << 32) || n_S[b] >= (1ull << 32)) throw Error(GJ_EINVAL, "join_host_batch: n must be < 2^32");
+  }
+  // the two sub-contexts inherit the planner options; the caller's stream is first
+  // ordered before them
+  for (gj_ctx*& c : ctx->sub) {
+    if (!c) {
+      c = new gj_ctx();
+      c->device = ctx->device;
+      c->num_sms = ctx->num_sms;
+      GJ_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->owns_stream = true;
+    }
+    c->part_bits = ctx->part_bits;
+    c->build_chunk = ctx->build_chunk;
+    c->probe_chunk = ctx->probe_chunk;
+    c->build_side = ctx->build_side;
+    c->launches = 0;
+  }
+  GJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  const size_t ks = key_type == GJ_I64 ? 8 : 4;
+  bool short_cap = false;
+  // Batch b runs on sub-context b & 1; its host->device copy is enqueued two batches
+  // ahead (right behind batch b-2's device->host copy in the same stream), so PCIe
+  // carries one batch's keys in while the previous batch's pairs go out, and no
+  // host synchronisation sits between a batch's copy-in and its predecessor's count.
+  std::vector<gj_rel> Rb((size_t)nbatch), Sb((size_t)nbatch);
+  auto enqueue_in = [&](int b) {
+    gj_ctx* c = ctx->sub[b & 1];
+    Rb[b] = gj_rel{ws(c, "host.R", n_R[b] * ks), nullptr, n_R[b], key_type, 0};
+    Sb[b] = gj_rel{ws(c, "host.S", n_S[b] * ks), nullptr, n_S[b], key_type, 0};
+    if (n_R[b])
+      GJ_CUDA(cudaMemcpyAsync(const_cast<void*>(Rb[b].key), key_R[b], n_R[b] * ks, cudaMemcpyHostToDevice, c->stream));
+    if (n_S[b])
+      GJ_CUDA(cudaMemcpyAsync(const_cast<void*>(Sb[b].key), key_S[b], n_S[b] * ks, cudaMemcpyHostToDevice, c->stream));
+  };
+  for (int b = 0; b < std::min(nbatch, 2); ++b) enqueue_in(b);
+  for (int b = 0; b < nbatch; ++b) {
+    gj_ctx* c = ctx->sub[b & 1];  // stream order on c serialises batch b after batch b-2
+    const gj_rel R = Rb[b], S = Sb[b];
+    do_join_count(c, R, S);  // waits for this batch's copy-in + count; the other stream keeps copying
+    const uint64_t total = c->jc.total;
+    n_out[b] = total;
+    if (capacity[b] < total) {
+      short_cap = true;
+      if (b + 2 < nbatch) enqueue_in(b + 2);
+      continue;
+    }
+    if (total && !out[b]) throw Error(GJ_EINVAL, "join_host_batch: out[b] is NULL");
+    if (total) {
+      uint32_t* dout = static_cast<uint32_t*>(ws(c, "host.out", total * 8));
+      hash_join_write(c, dout);
+      GJ_CUDA(cudaMemcpyAsync(out[b], dout, total * 8, cudaMemcpyDeviceToHost, c->stream));
+    }
+    // batch b+2 reuses this sub-context's key buffers: stream order puts its copy-in
+    // after this batch's write pass and copy-out
+    if (b + 2 < nbatch) enqueue_in(b + 2);
+  }
+  for (gj_ctx* c : ctx->sub) {
+    GJ_CUDA(cudaStreamSynchronize(c->stream));
+    ctx->launches += c->launches;
+  }
+  if (short_cap) throw Error(GJ_ERANGE, "join_host_batch: capacity < |J| for some batch (its pairs were not copied)");
   API_END
 }
 

@@ -102,6 +102,10 @@ struct gj_ctx {
   // caches
   gj::JoinCache jc;
   gj::ThetaCache tc;
+  // join_host_batch: two sub-contexts (own streams and workspaces) so that
+  // consecutive batches' transfers overlap
+  gj_ctx* sub[2] = {nullptr, nullptr};
+  bool owns_stream = false;
 };
 
 namespace gj {

@@ -393,6 +393,29 @@ def test_join_host_e2e(gj, ctx):
     assert np.array_equal(p, oracle.pkfk_closed_form(m)[1])
 
 
+def test_join_host_batch_stream(gj, ctx):
+    """join_host_batch: several independent joins (different sizes, duplicates, an empty
+    one) through the two-stream pipeline, each vs the oracle; a short capacity raises
+    GJ_ERANGE after the other batches completed."""
+    cases = [gen.pkfk(14, 70_000, seed=31)[:2],
+             (gen.uniform_keys(20_000, 3000, 5, 0), gen.uniform_keys(30_000, 3000, 5, 1)),
+             (gen.uniform_keys(0, 10, 5, 0), gen.uniform_keys(100, 10, 5, 1)),
+             gen.pkfk(12, 9_000, seed=32)[:2]]
+    expect = [oracle.hash_equi(R, S) for R, S in cases]
+    batches = [(torch.from_numpy(R).pin_memory(), torch.from_numpy(S).pin_memory(),
+                torch.empty((max(c, 1), 2), dtype=torch.int32).pin_memory())
+               for (R, S), (c, _) in zip(cases, expect)]
+    ns = gj.join_host_batch(ctx, batches)
+    for (c, pairs), n, (_, _, out) in zip(expect, ns, batches):
+        assert n == c
+        p = out.numpy()[:n].view(np.uint32)
+        assert np.array_equal(p[np.lexsort((p[:, 1], p[:, 0]))], pairs)
+    short = [batches[0], (batches[1][0], batches[1][1], torch.empty((5, 2), dtype=torch.int32).pin_memory()),
+             batches[3]]
+    with pytest.raises(gj.GJError, match="GJ_ERANGE"):
+        gj.join_host_batch(ctx, short)
+
+
 def test_launch_accounting_and_profile(gj):
     c = gj.Context(0, profile=1)
     R, S = dev(gen.uniform_keys(50_000, 10_000, 1, 0)), dev(gen.uniform_keys(50_000, 10_000, 1, 1))

@@ -60,6 +60,7 @@ struct HJArgs {
   const uint64_t* woff;
   uint2* out;
   int swap;
+  uint64_t nb, np;  // build / probe array lengths (bulk-copy windows are clamped to them)
 };
 
 // Shared-memory table.  int32 keys: one 64-bit slot = (index+1) << 32 | key, so a
@@ -199,7 +200,8 @@ constexpr uint16_t NO_MATCH = 0xFFFF, MULTI = 0xFFFE;
 
 template <typename K>
 __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __restrict__ stage,
-                                                      uint8_t* __restrict__ multi) {
+                                                      uint8_t* __restrict__ multi,
+                                                      unsigned long long* __restrict__ nmulti) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_dup;
   Table<K> tab;
@@ -224,8 +226,11 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
 
     tab.clear(T);
     if (tid == 0) s_dup = 0;
+    // loops sized for the 2048-tuple maximum exit early (CTA/warp-uniform) for the
+    // usual ~1024-tuple units
 #pragma unroll
     for (int j = 0; j < BPT; ++j) {
+      if ((uint32_t)j * HT >= bn) break;
       const uint32_t i = tid + j * HT;
       if (i < bn) tab.stage(i, cur.kb[j]);
     }
@@ -233,6 +238,7 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
     bool dup = false;
 #pragma unroll
     for (int j = 0; j < BPT; ++j) {
+      if ((uint32_t)j * HT >= bn) break;
       const uint32_t i = tid + j * HT;
       if (i < bn) dup |= tab.insert(slot_hash(cur.kb[j]) >> tshift, tmask, cur.kb[j], i);
     }
@@ -246,6 +252,7 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
     bool many = false;
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
+      if (wb + 32 * j >= we) break;  // warp-uniform
       const uint32_t i = wb + lane + 32 * j;
       if (i < we) {
         const K k = cur.kp[j];
@@ -264,7 +271,10 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
     }
     c = warp_sum(c);
     if (lane == 0) a.wcnt[(uint64_t)u * HW + w] = c;
-    if (__any_sync(FULL, many) && lane == 0) multi[u] = 1;
+    if (__any_sync(FULL, many) && lane == 0) {
+      multi[u] = 1;
+      atomicAdd(nmulti, 1ull);  // > 0 tells the host to launch the MULTI write pass
+    }
     __syncthreads();
     cur = nxt;
     d = dn;
@@ -278,7 +288,7 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
 // a MULTI row rebuild the table and re-probe (bag semantics with duplicate keys).
 template <typename K>
 __global__ void __launch_bounds__(HT) hj_write_kernel(HJArgs a, const uint16_t* __restrict__ stage,
-                                                      const uint8_t* __restrict__ multi) {
+                                                      const uint8_t* __restrict__ multi, int only_full) {
   extern __shared__ __align__(16) uint8_t smem[];
   Table<K> tab;
   tab.init(smem);
@@ -288,9 +298,10 @@ __global__ void __launch_bounds__(HT) hj_write_kernel(HJArgs a, const uint16_t* 
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
 
   for (uint32_t u = blockIdx.x; u < a.U; u += gridDim.x) {
+    const bool full = multi[u] != 0;
+    if (only_full && !full) continue;  // CTA-uniform: hj_write_fast wrote this unit
     const uint4 d = a.desc[u];
     const uint32_t bn = d.y, pn = d.w;
-    const bool full = multi[u] != 0;
     uint32_t wb, we;
     probe_range(pn, w, wb, we);
     // probe-side inputs of this warp's rows, all loads in flight at once
@@ -364,6 +375,99 @@ __global__ void __launch_bounds__(HT) hj_write_kernel(HJArgs a, const uint16_t* 
   }
 }
 
+// Fast write pass for units without a MULTI row (the usual case): no hash table.
+// The next unit's build rids, probe rids and staged match indices are streamed into
+// a second shared-memory buffer by 1-D TMA bulk copies (16-byte aligned windows,
+// elements outside a window read from global memory) while this unit is written.
+struct WBuf {
+  uint32_t br[BCH_MAX + 4];
+  uint32_t pr[PCH_MAX + 4];
+  uint16_t st[PCH_MAX + 8];
+};
+static_assert(sizeof(WBuf) % 16 == 0, "16-byte aligned buffers");
+
+struct Win {  // aligned copy window of elements [first, first + cnt) of an array
+  uint64_t a0;     // window start (bytes)
+  uint32_t bytes;  // window length (bytes, multiple of 16; 0 = nothing to copy)
+  uint32_t shift;  // element `first` sits at dst[shift]
+  uint32_t valid;  // elements [first, first + valid) are inside the window
+};
+__device__ __forceinline__ Win window(uint64_t first, uint32_t cnt, uint32_t esz, uint64_t total) {
+  Win w;
+  const uint64_t b0 = first * esz, b1 = (first + cnt) * esz;
+  w.a0 = b0 & ~15ull;
+  const uint64_t a1 = min((b1 + 15) & ~15ull, (total * esz) & ~15ull);
+  w.bytes = a1 > w.a0 ? (uint32_t)(a1 - w.a0) : 0u;
+  w.shift = (uint32_t)((b0 - w.a0) / esz);
+  w.valid = a1 > b0 ? (uint32_t)min((uint64_t)cnt, (a1 - b0) / esz) : 0u;
+  return w;
+}
+
+__device__ __forceinline__ void wf_issue(WBuf& B, uint64_t* bar, const uint4 d, const HJArgs& a,
+                                         const uint16_t* stage) {
+  fence_proxy_async();  // generic reads of this buffer (previous unit) before the async writes
+  const Win wb = a.brid ? window(d.x, d.y, 4, a.nb) : Win{0, 0, 0, 0};
+  const Win wp = a.prid ? window(d.z, d.w, 4, a.np) : Win{0, 0, 0, 0};
+  const Win ws = window(d.z, d.w, 2, a.np);
+  const uint32_t bytes = wb.bytes + wp.bytes + ws.bytes;
+  if (!bytes) {
+    mbar_arrive(bar);
+    return;
+  }
+  mbar_expect_tx(bar, bytes);
+  if (wb.bytes) bulk_g2s(B.br, reinterpret_cast<const uint8_t*>(a.brid) + wb.a0, wb.bytes, bar);
+  if (wp.bytes) bulk_g2s(B.pr, reinterpret_cast<const uint8_t*>(a.prid) + wp.a0, wp.bytes, bar);
+  if (ws.bytes) bulk_g2s(B.st, reinterpret_cast<const uint8_t*>(stage) + ws.a0, ws.bytes, bar);
+}
+
+__global__ void __launch_bounds__(HT) hj_write_fast(HJArgs a, const uint16_t* __restrict__ stage,
+                                                    const uint8_t* __restrict__ multi) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  WBuf* B = reinterpret_cast<WBuf*>(smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * sizeof(WBuf));
+  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
+  const uint32_t G = gridDim.x;
+  uint32_t u = blockIdx.x;
+  if (u >= a.U) return;
+  if (tid == 0) {
+    mbar_init(bar + 0, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+    wf_issue(B[0], bar + 0, a.desc[u], a, stage);
+  }
+  __syncthreads();
+  for (uint32_t it = 0; u < a.U; u += G, ++it) {
+    const uint32_t b = it & 1;
+    const uint4 d = a.desc[u];
+    if (tid == 0 && u + G < a.U) wf_issue(B[b ^ 1], bar + (b ^ 1), a.desc[u + G], a, stage);
+    const bool full = multi[u] != 0;
+    mbar_wait(bar + b, (it >> 1) & 1);
+    if (!full) {
+      const Win wb = window(d.x, d.y, 4, a.nb), wp = window(d.z, d.w, 4, a.np), ws = window(d.z, d.w, 2, a.np);
+      const WBuf& Bb = B[b];
+      uint32_t wlo, whi;
+      probe_range(d.w, w, wlo, whi);
+      uint64_t base = a.woff[(uint64_t)u * HW + w];
+      for (uint32_t r0 = wlo; r0 < whi; r0 += 32) {  // warp-uniform
+        const uint32_t i = r0 + lane;
+        const bool valid = i < whi;
+        const uint16_t sx = valid ? (i < ws.valid ? Bb.st[ws.shift + i] : stage[d.z + i]) : NO_MATCH;
+        const uint32_t m = sx != NO_MATCH ? 1u : 0u;
+        const uint32_t incl = warp_incl_scan(m);
+        if (m) {
+          const uint32_t prow = a.prid ? (i < wp.valid ? Bb.pr[wp.shift + i] : a.prid[d.z + i])
+                                       : a.prid_base + d.z + i;
+          const uint32_t brow = a.brid ? (sx < wb.valid ? Bb.br[wb.shift + sx] : a.brid[d.x + sx])
+                                       : a.brid_base + d.x + sx;
+          a.out[base + incl - 1] = a.swap ? make_uint2(prow, brow) : make_uint2(brow, prow);
+        }
+        base += __shfl_sync(FULL, incl, 31);
+      }
+    }
+    __syncthreads();  // buffer b is refilled by the issue of iteration it + 1
+  }
+}
+
 __global__ void hj_units(const uint32_t* __restrict__ boff, const uint32_t* __restrict__ poff, uint32_t P,
                          uint32_t bchunk, uint32_t pchunk, uint32_t* __restrict__ nunits) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -378,7 +482,8 @@ __global__ void hj_units(const uint32_t* __restrict__ boff, const uint32_t* __re
 // the write pass re-probes them.
 __global__ void hj_unit_desc(const uint32_t* __restrict__ unit_off, const uint32_t* __restrict__ boff,
                              const uint32_t* __restrict__ poff, uint32_t P, uint32_t U, uint32_t bchunk,
-                             uint32_t pchunk, uint4* __restrict__ desc, uint8_t* __restrict__ multi) {
+                             uint32_t pchunk, uint4* __restrict__ desc, uint8_t* __restrict__ multi,
+                             unsigned long long* __restrict__ nmulti) {
   for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
     const uint32_t p = upper_index(unit_off, P, u);
     const uint32_t uu = u - unit_off[p];
@@ -389,6 +494,7 @@ __global__ void hj_unit_desc(const uint32_t* __restrict__ unit_off, const uint32
     desc[u] = make_uint4(b0 + bci * bchunk, min(bchunk, nb - bci * bchunk), p0 + pci * pchunk,
                          min(pchunk, np - pci * pchunk));
     multi[u] = nbc > 1 ? 1 : 0;
+    if (nbc > 1 && uu == 0) atomicAdd(nmulti, 1ull);
   }
 }
 
@@ -438,7 +544,8 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
   jc.U = U;
   const uint64_t nw = (uint64_t)U * HW;
   uint32_t* wcnt = static_cast<uint32_t*>(ws(ctx, "hj.wcnt", (nw + 1) * sizeof(uint32_t)));
-  uint64_t* woff = static_cast<uint64_t*>(ws(ctx, "hj.woff", (nw + 1) * sizeof(uint64_t)));
+  // woff[nw] = |J| (scan total), woff[nw + 1] = MULTI-unit counter: one readback
+  uint64_t* woff = static_cast<uint64_t*>(ws(ctx, "hj.woff", (nw + 2) * sizeof(uint64_t)));
   uint4* desc = static_cast<uint4*>(ws(ctx, "hj.desc", ((uint64_t)U + 1) * sizeof(uint4)));
   jc.woff = woff;
   jc.desc = desc;
@@ -450,8 +557,10 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
   uint8_t* multi = static_cast<uint8_t*>(ws(ctx, "hj.multi", (uint64_t)U + 16));
   jc.stage = stage;
   jc.multi = multi;
+  unsigned long long* nmulti = reinterpret_cast<unsigned long long*>(woff + nw + 1);
+  GJ_CUDA(cudaMemsetAsync(nmulti, 0, sizeof(uint64_t), ctx->stream));
   launch(ctx, "hj_unit_desc", hj_unit_desc, dim3(std::min<uint32_t>((U + 255) / 256, ctx->num_sms * 16)),
-         dim3(256), 0, (const uint32_t*)unit_off, PB.off, PP.off, P, U, bchunk, pchunk, desc, multi);
+         dim3(256), 0, (const uint32_t*)unit_off, PB.off, PP.off, P, U, bchunk, pchunk, desc, multi, nmulti);
   HJArgs a{};
   a.bkey = PB.key;
   a.brid = PB.rid;
@@ -468,10 +577,13 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
     static bool once = (set_smem(hj_count_kernel<K>, smem), true);
     (void)once;
     launch(ctx, "hj_count", hj_count_kernel<K>, dim3(hj_grid(ctx, hj_count_kernel<K>, smem, U)), dim3(HT), smem, a,
-           stage, multi);
+           stage, multi, nmulti);
   }
   exclusive_scan<uint32_t, uint64_t>(ctx, wcnt, woff, nw, woff + nw);
-  d2h_sync(ctx, &jc.total, woff + nw, sizeof(uint64_t));
+  uint64_t h[2];
+  d2h_sync(ctx, h, woff + nw, sizeof(h));
+  jc.total = h[0];
+  jc.nmulti = h[1];
 }
 
 template <typename K>
@@ -492,11 +604,21 @@ void write_impl(gj_ctx* ctx, uint32_t* out) {
   a.woff = jc.woff;
   a.out = reinterpret_cast<uint2*>(out);
   a.swap = jc.swap;
+  a.nb = Bld.n;
+  a.np = Prb.n;
+  // units without a MULTI row: table-free gather with TMA prefetch; then the rare
+  // MULTI units rebuild their table and re-probe
+  const size_t fsmem = 2 * sizeof(WBuf) + 16;
+  static bool once_f = (set_smem(hj_write_fast, fsmem), true);
+  (void)once_f;
+  launch(ctx, "hj_write", hj_write_fast, dim3(hj_grid(ctx, hj_write_fast, fsmem, a.U)), dim3(HT), fsmem, a,
+         (const uint16_t*)jc.stage, (const uint8_t*)jc.multi);
+  if (jc.nmulti == 0) return;
   const size_t smem = hj_smem<K, true>();
   static bool once = (set_smem(hj_write_kernel<K>, smem), true);
   (void)once;
-  launch(ctx, "hj_write", hj_write_kernel<K>, dim3(hj_grid(ctx, hj_write_kernel<K>, smem, a.U)), dim3(HT), smem, a,
-         (const uint16_t*)jc.stage, (const uint8_t*)jc.multi);
+  launch(ctx, "hj_write_multi", hj_write_kernel<K>, dim3(hj_grid(ctx, hj_write_kernel<K>, smem, a.U)), dim3(HT),
+         smem, a, (const uint16_t*)jc.stage, (const uint8_t*)jc.multi, 1);
 }
 
 }  // namespace

@@ -69,6 +69,23 @@ __device__ __forceinline__ void acc_nb2(uint32_t& c, uint32_t a1, uint32_t a2, u
       : "r"(a1), "r"(a2), "r"(s), "r"(C));
 }
 
+// Shift one carry into a match mask: m = 2 m + carry (carry as in the counters above).
+template <int FAM>
+__device__ __forceinline__ void mask_step(uint32_t& m, uint32_t a, uint32_t s, uint32_t C) {
+  if (FAM == F_GE)
+    asm("{\n .reg .u32 t;\n sub.cc.u32 t, %1, %2;\n addc.u32 %0, %0, %0;\n}" : "+r"(m) : "r"(a), "r"(s));
+  if (FAM == F_LE)
+    asm("{\n .reg .u32 t;\n sub.cc.u32 t, %2, %1;\n addc.u32 %0, %0, %0;\n}" : "+r"(m) : "r"(a), "r"(s));
+  if (FAM == F_NE)
+    asm("{\n .reg .u32 x, t;\n xor.b32 x, %1, %2;\n sub.cc.u32 t, x, 1;\n addc.u32 %0, %0, %0;\n}"
+        : "+r"(m)
+        : "r"(a), "r"(s));
+  if (FAM == F_BAND)
+    asm("{\n .reg .u32 x, t;\n sub.u32 x, %1, %2;\n sub.cc.u32 t, x, %3;\n addc.u32 %0, %0, %0;\n}"
+        : "+r"(m)
+        : "r"(a), "r"(s), "r"(C));
+}
+
 // Count the carries of all KR register keys against one biased S key.
 template <int FAM>
 __device__ __forceinline__ void step8(uint32_t& c, const uint32_t (&r)[KR], uint32_t su, uint32_t C) {
@@ -141,6 +158,42 @@ struct NLJArgs {
   const uint64_t* woff;
   uint2* out;
 };
+
+// Write pass, a screened group of 4 S keys holding a match: each lane builds its
+// 32-pair match mask, bit 31 - (8q + i) = (S key q of the group, register key i),
+// with the counters' carry trick, and the warp walks only the set bits, highest
+// first -- (S key, slot, lane) order.  Out of line so that ptxas keeps this rare
+// path from reshaping the screening loop.  sq: the group's biased S keys; row0:
+// index of S key 0 (for its rid); returns the advanced warp output base.
+template <int OP>
+__device__ __noinline__ uint64_t emit_group(const uint32_t* rf, const uint32_t* rr, const uint32_t* sq, uint32_t C,
+                                            uint64_t wbase, uint64_t row0, const NLJArgs* a) {
+  constexpr int FAM = family(OP);
+  uint32_t mm = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int i = 0; i < KR; ++i) mask_step<FAM>(mm, rf[i], sq[q], C);
+  if (!direct(OP)) mm = ~mm;
+  uint32_t any = __reduce_or_sync(FULL, mm);
+  while (any) {
+    const uint32_t bit = 31 - __clz(any);
+    any &= ~(1u << bit);
+    const bool p = (mm >> bit) & 1u;
+    const uint32_t bal = __ballot_sync(FULL, p);
+    if (p) {
+      const uint32_t e = 31 - bit, q = e >> 3, i = e & 7;
+      uint32_t rv = 0;
+#pragma unroll
+      for (int k = 0; k < KR; ++k) rv = (uint32_t)k == i ? rr[k] : rv;
+      const uint64_t row = row0 + q;
+      a->out[wbase + __popc(bal & lanemask_lt())] =
+          make_uint2(rv, a->srid ? a->srid[row] : a->srid_base + (uint32_t)row);
+    }
+    wbase += __popc(bal);
+  }
+  return wbase;
+}
 
 template <typename K, int OP, bool FAST, bool WRITE>
 __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
@@ -256,8 +309,7 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
             }
           };
           // Screen 4 S keys (one LDS.128) with the count pass's carry-chain counters and
-          // one warp vote; only groups holding a match are re-walked key by key, in
-          // order, so the output order is the per-key order.
+          // one warp vote; only groups holding a match build masks.
           const uint4* s4 = reinterpret_cast<const uint4*>(st);
           const uint32_t n4 = tn16 >> 2;
 #pragma unroll 2
@@ -272,10 +324,13 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
             step8<FAM>(acc, rf, s3, a.C);
             const bool hit = direct(OP) ? acc != 0 : acc != 4u * KR;
             if (__any_sync(FULL, hit)) {
-              emit(4 * q);
-              emit(4 * q + 1);
-              emit(4 * q + 2);
-              emit(4 * q + 3);
+              uint32_t sq[4];  // re-read (volatile): ptxas must not carry the screening values
+              asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(sq[0]), "=r"(sq[1]), "=r"(sq[2]), "=r"(sq[3])
+                           : "r"(saddr(st + 4 * q)));
+#pragma unroll
+              for (int k = 0; k < 4; ++k) sq[k] ^= 0x80000000u;
+              wbase = emit_group<OP>(rf, rr, sq, a.C, wbase, tb + 4 * q, &a);
             }
           }
           for (uint32_t j = n4 * 4; j < tn; ++j) emit(j);

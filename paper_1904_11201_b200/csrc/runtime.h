@@ -55,6 +55,7 @@ struct JoinCache {
   uint32_t bchunk = 0, pchunk = 0;
   const uint64_t* woff = nullptr;  // U*W exclusive offsets
   uint64_t total = 0;
+  uint64_t nmulti = 0;  // units flagged MULTI (the write pass re-probes them)
 };
 
 struct ThetaCache {

@@ -34,6 +34,9 @@ TAGS = [
     (r"hj_write_kernel", "hj_write"),
     (r"nlj_kernel<[^>]*, (true|1)>", "nlj_write"),
     (r"nlj_kernel<[^>]*, (false|0)>", "nlj_count"),
+    (r"pf_count", "pf_count"),
+    (r"pf_write", "pf_write"),
+    (r"bloom_build", "bloom_build"),
 ]
 KEY_METRICS = [
     ("gpu__time_duration.sum", "time"),

@@ -34,7 +34,7 @@ constexpr int TPC = 16;          // tiles per chunk
 constexpr int CHUNK = TILE * TPC;  // 65536 tuples per chunk
 constexpr int NW = PT / 32;
 constexpr int MAX_BITS = 9;      // digits per pass <= 512
-constexpr int SCATTER_DEFAULT_V = 2;  // part_scatter variant (see launch_scatter_t)
+constexpr int SCATTER_DEFAULT_V = 4;  // part_scatter variant (see launch_scatter_t)
 
 struct ChunkLoc {
   uint32_t total, seg, cb, nc;  // #chunks, segment, first chunk of segment, chunks in segment
@@ -495,6 +495,319 @@ __global__ void __launch_bounds__(PT) part_scatter(
   if (REMOTE) __threadfence_system();  // peer writes performed before the kernel retires
 }
 
+// Local scatter (no shuffle), branch-free ranking.  Same contract and output as
+// part_scatter<K, HAS_RID, false, ...>, restructured so that every phase of a tile
+// is a straight run of independent per-item operations the scheduler can overlap:
+//  * the (rare) elements of the array's last tile that lie outside the 16-byte TMA
+//    window are patched into the shared buffer once, CTA-uniformly, instead of a
+//    per-item "shared or global" select (which compiled to 16 BSSY/BRA regions);
+//  * padding items of a ragged tile rank against a dummy counter (digit D), so the
+//    16 loads, 16 hashes and 16 fetch-adds carry no predicates;
+//  * warp-private counters are unpacked 32-bit words (W = D + 1 rounded up to 4).
+// Stable: warp w holds the tile's items [w*PI*32, (w+1)*PI*32) in order, item i of
+// lane l is element (w*PI + i)*32 + l, and lanes of one fetch-add instruction on the
+// same counter are serialised in lane order.
+template <typename K>
+struct LocalLayout {
+  static constexpr uint32_t KB = TILE + 16;  // room for the 16-byte TMA alignment shift
+  static constexpr uint32_t RB = TILE + 16;
+  static constexpr size_t BUF = (size_t)KB * sizeof(K) + (size_t)RB * 4;
+  static constexpr size_t off_bar = 2 * BUF;
+  static constexpr size_t off_wt = off_bar + 16;
+  static constexpr size_t off_whist = off_wt + 16 * NW;
+  static_assert(BUF % 16 == 0 && off_whist % 16 == 0, "16-byte aligned sections");
+  static __host__ __device__ uint32_t words(uint32_t D) { return (D + 1 + 3) & ~3u; }
+  static size_t bytes(uint32_t D) { return off_whist + ((size_t)NW * words(D) + (size_t)D) * 4; }
+};
+
+template <typename K, bool HAS_RID, bool WB1>
+__global__ void __launch_bounds__(PT, 2) part_scatter_local(
+    const K* __restrict__ key_in, const uint32_t* __restrict__ rid_in, uint32_t rid_base, uint64_t n,
+    const uint4* __restrict__ tdesc, uint32_t ntiles, uint32_t shift, uint32_t bits,
+    const uint32_t* __restrict__ tile_base, K* __restrict__ key_out, uint32_t* __restrict__ rid_out,
+    uint32_t* __restrict__ tile_ctr, int hint) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  using L = LocalLayout<K>;
+  const uint64_t pol_in = l2_evict_first(), pol_out = l2_evict_last();
+  constexpr bool ILV = sizeof(K) == 4;  // int32: one (key, rid) uint2 per staging slot
+  const uint32_t D = 1u << bits, mask = D - 1;
+  const uint32_t W = L::words(D);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L::off_bar);
+  uint32_t* wt = reinterpret_cast<uint32_t*>(smem_raw + L::off_wt);
+  uint32_t* whist = reinterpret_cast<uint32_t*>(smem_raw + L::off_whist);
+  uint32_t* delta = whist + NW * W;
+  auto kbuf_of = [&](uint32_t b) { return reinterpret_cast<K*>(smem_raw + b * L::BUF); };
+  auto rbuf_of = [&](uint32_t b) {
+    return reinterpret_cast<uint32_t*>(smem_raw + b * L::BUF + (size_t)L::KB * sizeof(K));
+  };
+  const uint32_t w = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t G = gridDim.x;
+  uint32_t t = blockIdx.x;
+  if (t >= ntiles) return;
+  auto issue = [&](uint32_t b, const uint4 d) {
+    fence_proxy_async();
+    uint64_t* bar = bars + b;
+    if (d.y == 0) {
+      mbar_arrive(bar);
+      return;
+    }
+    const uint64_t kb0 = (uint64_t)d.x * sizeof(K), kb1 = (uint64_t)(d.x + d.y) * sizeof(K);
+    const uint64_t ka = kb0 & ~15ull, kz = min((kb1 + 15) & ~15ull, (n * sizeof(K)) & ~15ull);
+    uint32_t bytes = kz > ka ? (uint32_t)(kz - ka) : 0u;
+    uint64_t ra = 0, rz = 0;
+    if (HAS_RID) {
+      ra = ((uint64_t)d.x * 4) & ~15ull;
+      rz = min((((uint64_t)(d.x + d.y) * 4) + 15) & ~15ull, (n * 4) & ~15ull);
+      if (rz > ra) bytes += (uint32_t)(rz - ra);
+    }
+    mbar_expect_tx(bar, bytes);
+    if (hint & 1) {
+      if (kz > ka)
+        bulk_g2s_hint(kbuf_of(b), reinterpret_cast<const uint8_t*>(key_in) + ka, (uint32_t)(kz - ka), bar, pol_in);
+      if (HAS_RID && rz > ra)
+        bulk_g2s_hint(rbuf_of(b), reinterpret_cast<const uint8_t*>(rid_in) + ra, (uint32_t)(rz - ra), bar, pol_in);
+    } else {
+      if (kz > ka) bulk_g2s(kbuf_of(b), reinterpret_cast<const uint8_t*>(key_in) + ka, (uint32_t)(kz - ka), bar);
+      if (HAS_RID && rz > ra)
+        bulk_g2s(rbuf_of(b), reinterpret_cast<const uint8_t*>(rid_in) + ra, (uint32_t)(rz - ra), bar);
+    }
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(bars + 0, 1);
+    mbar_init(bars + 1, 1);
+    fence_mbar_init();
+    issue(0, tdesc[t]);
+  }
+  __syncthreads();
+  const uint32_t H = D > 1 ? D / 2 : 1;
+  const uint32_t da = threadIdx.x, db = threadIdx.x + H;
+  const bool ha = da < H && da < D, hb = D > 1 && da < H;
+  // Tiles are handed out in global order by an atomic counter (first tile =
+  // blockIdx.x): the tiles in flight are always a contiguous window, so the partial
+  // sectors at the ends of neighbouring tiles' runs meet in L2 (with a static
+  // round-robin a lagging CTA left them to be written back half-filled).
+  __shared__ uint32_t s_tile[2];
+  if (threadIdx.x == 0) s_tile[0] = t;
+  __syncthreads();
+  for (uint32_t it = 0;; ++it) {
+    const uint32_t b = it & 1;
+    t = s_tile[b];
+    if (t >= ntiles) break;  // CTA-uniform
+    if (threadIdx.x == 0) {
+      const uint32_t tn = G + atomicAdd(tile_ctr, 1u);
+      s_tile[b ^ 1] = tn;
+      if (tn < ntiles) issue(b ^ 1, tdesc[tn]);
+    }
+    const uint4 d = tdesc[t];
+    uint32_t g0a = 0, g0b = 0;  // global run starts of my two digits in this tile
+    if (d.y) {
+      if (ha) g0a = tile_base[(uint64_t)t * D + da];
+      if (hb) g0b = tile_base[(uint64_t)t * D + db];
+    }
+    const uint32_t cnt = d.y;
+    if (cnt == 0) {  // CTA-uniform
+      mbar_wait(bars + b, (it >> 1) & 1);
+      __syncthreads();
+      continue;
+    }
+    {
+      uint4* z = reinterpret_cast<uint4*>(whist + w * W);
+      for (uint32_t i = lane; i < W / 4; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    mbar_wait(bars + b, (it >> 1) & 1);
+    K* kbuf = kbuf_of(b);
+    uint32_t* rbuf = rbuf_of(b);
+    const uint32_t ko = (d.x * (uint32_t)sizeof(K) & 15u) / (uint32_t)sizeof(K);
+    const uint32_t ro = d.x & 3u;
+    {  // elements past the last 16-byte boundary of the array: not in the bulk copy
+      const uint64_t kz = min((((uint64_t)(d.x + d.y) * sizeof(K)) + 15) & ~15ull, (n * sizeof(K)) & ~15ull);
+      const uint32_t kvalid = (uint32_t)(kz / sizeof(K) > d.x ? kz / sizeof(K) - d.x : 0);
+      uint32_t rvalid = cnt;
+      if (HAS_RID) {
+        const uint64_t rz = min((((uint64_t)(d.x + d.y) * 4) + 15) & ~15ull, (n * 4) & ~15ull);
+        rvalid = (uint32_t)(rz / 4 > d.x ? rz / 4 - d.x : 0);
+      }
+      if (kvalid < cnt || rvalid < cnt) {  // CTA-uniform, at most the array's final tile
+        for (uint32_t j = kvalid + threadIdx.x; j < cnt; j += PT) kbuf[ko + j] = key_in[d.x + j];
+        if (HAS_RID)
+          for (uint32_t j = rvalid + threadIdx.x; j < cnt; j += PT) rbuf[ro + j] = rid_in[d.x + j];
+        __syncthreads();
+      }
+    }
+    __syncwarp();
+    K k[PI];
+    uint32_t rk[PI];  // (digit << 16) | rank among this warp's items of that digit
+#pragma unroll
+    for (int i = 0; i < PI; ++i) k[i] = kbuf[ko + (w * PI + i) * 32 + lane];
+#pragma unroll
+    for (int i = 0; i < PI; ++i) {
+      const uint32_t j = (w * PI + i) * 32 + lane;
+      rk[i] = j < cnt ? digit_of(k[i], shift, mask) : D;  // padding -> dummy counter D
+    }
+#pragma unroll
+    for (int i = 0; i < PI; ++i) rk[i] = (rk[i] << 16) | atomicAdd(whist + w * W + rk[i], 1u);
+    uint32_t rr[PI];
+#pragma unroll
+    for (int i = 0; i < PI; ++i)
+      rr[i] = HAS_RID ? rbuf[ro + (w * PI + i) * 32 + lane] : rid_base + d.x + (w * PI + i) * 32 + lane;
+    __syncthreads();  // inputs are in registers: the buffer becomes the staging area
+    {  // tile-local digit starts (see part_scatter)
+      uint32_t ta = 0, tb = 0;
+      if (ha) {
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) {
+          uint32_t* c = whist + ww * W + da;
+          const uint32_t x = c[0];
+          c[0] = ta;
+          ta += x;
+          if (hb) {
+            const uint32_t y = c[H];
+            c[H] = tb;
+            tb += y;
+          }
+        }
+      }
+      const uint32_t ia = warp_incl_scan(ta), ib = warp_incl_scan(tb);
+      if (lane == 31) {
+        wt[w] = ia;
+        wt[NW + w] = ib;
+      }
+      __syncthreads();
+      uint32_t st_a = ia - ta, st_b = ib - tb, low = 0;
+#pragma unroll
+      for (int ww = 0; ww < NW; ++ww) {
+        const uint32_t xa = wt[ww], xb = wt[NW + ww];
+        low += xa;
+        if ((uint32_t)ww < w) {
+          st_a += xa;
+          st_b += xb;
+        }
+      }
+      st_b += low;
+      if (ha) {
+        delta[da] = g0a - st_a;
+        if (hb) delta[db] = g0b - st_b;
+#pragma unroll
+        for (int ww = 0; ww < NW; ++ww) {
+          whist[ww * W + da] += st_a;
+          if (hb) whist[ww * W + db] += st_b;
+        }
+      }
+    }
+    __syncthreads();
+    uint2* stg = reinterpret_cast<uint2*>(kbuf);
+    K* skey = kbuf;
+    uint32_t* srid = rbuf;
+#pragma unroll
+    for (int i = 0; i < PI; ++i) {
+      const uint32_t dg = rk[i] >> 16;
+      if (dg < D) {
+        const uint32_t pos = whist[w * W + dg] + (rk[i] & 0xffffu);
+        if (ILV) {
+          stg[pos] = make_uint2((uint32_t)k[i], rr[i]);
+        } else {
+          skey[pos] = k[i];
+          srid[pos] = rr[i];
+        }
+      }
+    }
+    __syncthreads();
+    // write-back in groups of 8 items: loads, offsets, then (predicated) stores --
+    // staging slots past cnt hold stale data but index delta[] safely
+    constexpr int WG = 8;
+    if (WB1) {
+#pragma unroll 4
+      for (int i = 0; i < PI; ++i) {
+        const uint32_t j = i * PT + threadIdx.x;
+        if (j < cnt) {
+          K kk;
+          uint32_t rv;
+          if (ILV) {
+            const uint2 e = stg[j];
+            kk = (K)e.x;
+            rv = e.y;
+          } else {
+            kk = skey[j];
+            rv = srid[j];
+          }
+          const uint32_t pos = delta[digit_of(kk, shift, mask)] + j;
+          key_out[pos] = kk;
+          rid_out[pos] = rv;
+        }
+      }
+    }
+#pragma unroll
+    for (int i0 = 0; i0 < PI && !WB1; i0 += WG) {
+      K kk[WG];
+      uint32_t rv[WG], pos[WG];
+#pragma unroll
+      for (int q = 0; q < WG; ++q) {
+        const uint32_t j = (i0 + q) * PT + threadIdx.x;
+        if (ILV) {
+          const uint2 e = stg[j];
+          kk[q] = (K)e.x;
+          rv[q] = e.y;
+        } else {
+          kk[q] = skey[j];
+          rv[q] = srid[j];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < WG; ++q) pos[q] = delta[digit_of(kk[q], shift, mask)] + (i0 + q) * PT + threadIdx.x;
+#pragma unroll
+      for (int q = 0; q < WG; ++q) {
+        if ((i0 + q) * PT + threadIdx.x < cnt) {
+          if (hint & 2) {
+            st_hint(key_out + pos[q], kk[q], pol_out);
+            st_hint(rid_out + pos[q], rv[q], pol_out);
+          } else {
+            key_out[pos[q]] = kk[q];
+            rid_out[pos[q]] = rv[q];
+          }
+        }
+      }
+    }
+    __syncthreads();  // the buffer may be refilled by the next iteration's issue
+  }
+}
+
+template <typename K, bool HAS_RID, bool WB1>
+void launch_scatter_local(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
+                          const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits,
+                          const uint32_t* tile_base, K* kout, uint32_t* rout) {
+  auto kern = part_scatter_local<K, HAS_RID, WB1>;
+  const size_t smem = LocalLayout<K>::bytes(1u << bits);
+  static bool once = (set_smem(kern, LocalLayout<K>::bytes(1u << MAX_BITS)), true);
+  (void)once;
+  int occ = 1;
+  GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PT, smem));
+  if (const char* e = std::getenv("GJ_SCATTER_OCC")) occ = std::min(occ, std::atoi(e));
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
+  static const int hint = std::getenv("GJ_L2HINT") ? std::atoi(std::getenv("GJ_L2HINT")) : 0;
+  uint32_t* ctr = static_cast<uint32_t*>(ws(ctx, "part.tile_ctr", sizeof(uint32_t)));
+  GJ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), ctx->stream));
+  launch(ctx, "part_scatter", kern, dim3(grid), dim3(PT), smem, kin, rin, rid_base, n, tdesc, (uint32_t)ntiles,
+         shift, bits, tile_base, kout, rout, ctr, hint);
+}
+
+// Turns the in-chunk prefix rows of part_hist into absolute run starts: every
+// tile's row gets its chunk's scanned (segment, digit, chunk) offsets added, so the
+// local scatter reads one contiguous row per tile (the scanned matrix is strided by
+// the chunk count: reading it per tile cost one DRAM sector per digit).
+// One CTA per chunk.
+__global__ void tile_base_kernel(uint64_t n, const uint32_t* __restrict__ seg_off,
+                                 const uint32_t* __restrict__ chunk_base, uint32_t nseg, uint32_t bits,
+                                 const uint32_t* __restrict__ scanned, uint32_t* __restrict__ tile_pref) {
+  const uint32_t c = blockIdx.x, D = 1u << bits;
+  const ChunkLoc L = locate(c, n, seg_off, chunk_base, nseg);
+  if (c >= L.total) return;
+  const uint32_t nt = (uint32_t)((L.end - L.beg + TILE - 1) / TILE);
+  for (uint32_t d = threadIdx.x; d < D; d += blockDim.x) {
+    const uint32_t base = scanned[(uint64_t)L.cb * D + (uint64_t)d * L.nc + (c - L.cb)];
+    for (uint32_t t = 0; t < nt; ++t) tile_pref[((uint64_t)c * TPC + t) * D + d] += base;
+  }
+}
+
 template <typename K, bool HAS_RID, bool REMOTE, bool PACK, bool ILV>
 void launch_scatter_v(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
                       const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* hist,
@@ -513,16 +826,26 @@ void launch_scatter_v(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t r
 
 // Variant selection (GJ_SCATTER_V, tuning experiments): 0 = plain counters +
 // separate key/rid staging, 1 = packed counters, 2 = interleaved staging, 3 = both.
+int scatter_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("GJ_SCATTER_V");
+    return e ? std::atoi(e) : SCATTER_DEFAULT_V;
+  }();
+  return v;
+}
+
 template <typename K, bool HAS_RID, bool REMOTE>
 void launch_scatter_t(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
                       const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* hist,
                       const uint32_t* tile_pref, K* kout, uint32_t* rout, const ShuffleDest& dst) {
-  static const int v = [] {
-    const char* e = std::getenv("GJ_SCATTER_V");
-    const int x = e ? std::atoi(e) : SCATTER_DEFAULT_V;
-    return REMOTE ? (x & 1) : x;  // the shuffle stages key/rid separately (bulk stores)
-  }();
-  if (sizeof(K) == 4 && (v & 2)) {
+  const int v = REMOTE ? (scatter_variant() & 1) : scatter_variant();  // the shuffle stages key/rid separately
+  if (!REMOTE && v == 4) {  // tile_pref holds absolute run starts (tile_base_kernel)
+    launch_scatter_local<K, HAS_RID, false>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_pref, kout,
+                                            rout);
+  } else if (!REMOTE && v == 5) {
+    launch_scatter_local<K, HAS_RID, true>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_pref, kout,
+                                           rout);
+  } else if (sizeof(K) == 4 && (v & 2)) {
     if (v & 1)
       launch_scatter_v<K, HAS_RID, REMOTE, true, sizeof(K) == 4>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift,
                                                                  bits, hist, tile_pref, kout, rout, dst);
@@ -608,7 +931,9 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
   const uint32_t* seg_off = seg_off0;
   uint32_t nseg = seg_off0 ? nseg0 : 1, used = skip;
   for (int pass = 0; pass < npass; ++pass) {
-    const uint32_t bits = B / npass + ((uint32_t)pass < B % npass ? 1 : 0);
+    static const bool last_wide = std::getenv("GJ_SPLIT_LAST") != nullptr;  // experiment: extra bits last
+    const uint32_t wide = last_wide ? (uint32_t)(npass - 1 - pass) : (uint32_t)pass;
+    const uint32_t bits = B / npass + (wide < B % npass ? 1 : 0);
     const uint32_t D = 1u << bits;
     const uint32_t shift = 32 - used - bits;
     std::string ps = t + "." + std::to_string(pass & 1);
@@ -628,6 +953,9 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
     launch(ctx, "part_hist", part_hist<K>, dim3((unsigned)max_chunks), dim3(PT), 0, kin, n, seg_off,
            (const uint32_t*)chunk_base, nseg, shift, bits, hist, tile_pref);
     exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
+    if (scatter_variant() >= 4)
+      launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, seg_off,
+             (const uint32_t*)chunk_base, nseg, bits, (const uint32_t*)hist, tile_pref);
     uint4* tdesc = static_cast<uint4*>(ws(ctx, "part.tdesc", (ntiles + 1) * sizeof(uint4)));
     launch(ctx, "tile_desc", tile_desc_kernel, dim3((unsigned)((ntiles + 255) / 256)), dim3(256), 0, n, seg_off,
            (const uint32_t*)chunk_base, nseg, D, (uint32_t)ntiles, tdesc);

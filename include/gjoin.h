@@ -91,8 +91,8 @@ const char* gj_last_error(void);
 
 /* Tuning / test options (gj_ctx_set_option).  Defaults are chosen for B200.
  *  GJ_OPT_PART_BITS        total radix bits B (-1 = auto from the build size)
- *  GJ_OPT_BUILD_CHUNK      build tuples per hash-join work unit (<= 2048, power of 2)
- *  GJ_OPT_PROBE_CHUNK      probe tuples per hash-join work unit (<= 2048)
+ *  GJ_OPT_BUILD_CHUNK      build tuples per hash-join work unit (<= 4096, power of 2)
+ *  GJ_OPT_PROBE_CHUNK      probe tuples per hash-join work unit (<= 4096)
  *  GJ_OPT_PROFILE          1 = bracket every kernel with CUDA events (per-kernel times)
  *  GJ_OPT_NLJ_SPLIT        S-range splits per R tile for the NLJ (0 = auto)
  *  GJ_OPT_FORCE_SLOW_BAND  1 = always use the 64-bit band path (tests)

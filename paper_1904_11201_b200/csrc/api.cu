@@ -287,11 +287,11 @@ gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t v) {
       ctx->part_bits = (int)v;
       break;
     case GJ_OPT_BUILD_CHUNK:
-      if (v < 32 || v > 2048 || (v & (v - 1))) throw Error(GJ_EINVAL, "build_chunk must be a power of 2 in [32, 2048]");
+      if (v < 32 || v > 4096 || (v & (v - 1))) throw Error(GJ_EINVAL, "build_chunk must be a power of 2 in [32, 4096]");
       ctx->build_chunk = (uint32_t)v;
       break;
     case GJ_OPT_PROBE_CHUNK:
-      if (v < 32 || v > 2048) throw Error(GJ_EINVAL, "probe_chunk must be in [32, 2048]");
+      if (v < 32 || v > 4096) throw Error(GJ_EINVAL, "probe_chunk must be in [32, 4096]");
       ctx->probe_chunk = (uint32_t)v;
       break;
     case GJ_OPT_PROFILE: ctx->profile = v != 0; break;

@@ -21,6 +21,8 @@
 // into output offsets; the write kernel re-probes and each warp writes its matches
 // at its offset, ranked inside the warp by a shuffle scan -- deterministic
 // positions, no atomics on the output.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "hashjoin.cuh"
 #include "scan.cuh"
@@ -28,10 +30,10 @@
 namespace gj {
 namespace {
 
-constexpr int HT = 256;            // threads per CTA
+constexpr int HT = 512;            // threads per CTA
 constexpr int HW = HT / 32;        // warps per CTA (counts are kept per (unit, warp))
-constexpr int BCH_MAX = 2048;      // max build tuples per unit
-constexpr int PCH_MAX = 2048;      // max probe tuples per unit
+constexpr int BCH_MAX = 4096;      // max build tuples per unit
+constexpr int PCH_MAX = 4096;      // max probe tuples per unit
 constexpr int TAB_MAX = 2 * BCH_MAX;
 constexpr int BPT = BCH_MAX / HT;  // build tuples per thread
 constexpr int PPT = PCH_MAX / HT;  // probe tuples per lane (warp w owns rows [w*pn/HW, ...))
@@ -192,6 +194,23 @@ __device__ __forceinline__ uint32_t table_logT(uint32_t bn) {
   return min(want, (uint32_t)(31 - __clz(TAB_MAX)));
 }
 
+struct Win {  // aligned copy window of elements [first, first + cnt) of an array
+  uint64_t a0;     // window start (bytes)
+  uint32_t bytes;  // window length (bytes, multiple of 16; 0 = nothing to copy)
+  uint32_t shift;  // element `first` sits at dst[shift]
+  uint32_t valid;  // elements [first, first + valid) are inside the window
+};
+__device__ __forceinline__ Win window(uint64_t first, uint32_t cnt, uint32_t esz, uint64_t total) {
+  Win w;
+  const uint64_t b0 = first * esz, b1 = (first + cnt) * esz;
+  w.a0 = b0 & ~15ull;
+  const uint64_t a1 = min((b1 + 15) & ~15ull, (total * esz) & ~15ull);
+  w.bytes = a1 > w.a0 ? (uint32_t)(a1 - w.a0) : 0u;
+  w.shift = (uint32_t)((b0 - w.a0) / esz);
+  w.valid = a1 > b0 ? (uint32_t)min((uint64_t)cnt, (a1 - b0) / esz) : 0u;
+  return w;
+}
+
 // Count pass.  Per probe row it also records the matching build index inside the
 // unit's build chunk (uint16; NO_MATCH / MULTI sentinels), so the write pass can
 // emit pairs without rebuilding the table (units holding a MULTI row are flagged
@@ -279,6 +298,118 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
     cur = nxt;
     d = dn;
     dn = dnn;
+  }
+}
+
+// Count pass, TMA-fed variant: the next unit's build and probe keys are streamed
+// into a second shared-memory buffer by 1-D TMA bulk copies (16-byte aligned
+// windows; elements outside a window read from global memory) while this unit is
+// built and probed, so the key loads never sit on the critical path (the
+// register-prefetch variant above waited on them at every unit boundary).
+template <typename K>
+struct CBuf {
+  K bk[BCH_MAX + 16 / sizeof(K)];
+  K pk[PCH_MAX + 16 / sizeof(K)];
+};
+
+template <typename K>
+__device__ __forceinline__ void cnt_issue(CBuf<K>& B, uint64_t* bar, const uint4 d, const HJArgs& a) {
+  fence_proxy_async();
+  const Win wb = window(d.x, d.y, sizeof(K), a.nb);
+  const Win wp = window(d.z, d.w, sizeof(K), a.np);
+  const uint32_t bytes = wb.bytes + wp.bytes;
+  if (!bytes) {
+    mbar_arrive(bar);
+    return;
+  }
+  mbar_expect_tx(bar, bytes);
+  if (wb.bytes) bulk_g2s(B.bk, reinterpret_cast<const uint8_t*>(a.bkey) + wb.a0, wb.bytes, bar);
+  if (wp.bytes) bulk_g2s(B.pk, reinterpret_cast<const uint8_t*>(a.pkey) + wp.a0, wp.bytes, bar);
+}
+
+template <typename K>
+__global__ void __launch_bounds__(HT) hj_count_tma(HJArgs a, uint16_t* __restrict__ stage,
+                                                   uint8_t* __restrict__ multi,
+                                                   unsigned long long* __restrict__ nmulti) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_dup;
+  CBuf<K>* B = reinterpret_cast<CBuf<K>*>(smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * sizeof(CBuf<K>));
+  Table<K> tab;
+  tab.init(smem + 2 * sizeof(CBuf<K>) + 16);
+  const K* __restrict__ bkey = static_cast<const K*>(a.bkey);
+  const K* __restrict__ pkey = static_cast<const K*>(a.pkey);
+  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
+  const uint32_t G = gridDim.x;
+  uint32_t u = blockIdx.x;
+  if (u >= a.U) return;
+  if (tid == 0) {
+    mbar_init(bar + 0, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+    cnt_issue(B[0], bar + 0, a.desc[u], a);
+  }
+  __syncthreads();
+  for (uint32_t it = 0; u < a.U; u += G, ++it) {
+    const uint32_t b = it & 1;
+    const uint4 d = a.desc[u];
+    if (tid == 0 && u + G < a.U) cnt_issue(B[b ^ 1], bar + (b ^ 1), a.desc[u + G], a);
+    const uint32_t bn = d.y, pn = d.w;
+    const uint32_t logT = table_logT(bn);
+    const uint32_t T = 1u << logT, tmask = T - 1, tshift = 32 - logT;
+    const Win wb = window(d.x, d.y, sizeof(K), a.nb), wp = window(d.z, d.w, sizeof(K), a.np);
+    tab.clear(T);
+    if (tid == 0) s_dup = 0;
+    mbar_wait(bar + b, (it >> 1) & 1);
+    const CBuf<K>& Bb = B[b];
+    K kb[BPT];
+#pragma unroll
+    for (int j = 0; j < BPT; ++j) {
+      const uint32_t i = tid + j * HT;
+      kb[j] = i < bn ? (i < wb.valid ? Bb.bk[wb.shift + i] : bkey[d.x + i]) : K(0);
+      if (i < bn) tab.stage(i, kb[j]);
+    }
+    __syncthreads();
+    bool dup = false;
+#pragma unroll
+    for (int j = 0; j < BPT; ++j) {
+      if ((uint32_t)j * HT >= bn) break;
+      const uint32_t i = tid + j * HT;
+      if (i < bn) dup |= tab.insert(slot_hash(kb[j]) >> tshift, tmask, kb[j], i);
+    }
+    if (__any_sync(FULL, dup) && lane == 0) s_dup = 1;
+    __syncthreads();
+    const bool unique = s_dup == 0;
+    uint32_t wlo, whi;
+    probe_range(pn, w, wlo, whi);
+    uint32_t c = 0;
+    bool many = false;
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      if (wlo + 32 * j >= whi) break;  // warp-uniform
+      const uint32_t i = wlo + lane + 32 * j;
+      if (i < whi) {
+        const K k = i < wp.valid ? Bb.pk[wp.shift + i] : pkey[d.z + i];
+        const uint32_t s0 = slot_hash(k) >> tshift;
+        uint32_t m = 0, f = 0;
+        auto hit = [&](uint32_t idx) {
+          f = idx;
+          ++m;
+        };
+        if (unique) tab.template probe<true>(s0, tmask, k, hit);
+        else tab.template probe<false>(s0, tmask, k, hit);
+        c += m;
+        many |= m > 1;
+        stage[d.z + i] = m == 0 ? NO_MATCH : (m == 1 ? (uint16_t)f : MULTI);
+      }
+    }
+    c = warp_sum(c);
+    if (lane == 0) a.wcnt[(uint64_t)u * HW + w] = c;
+    if (__any_sync(FULL, many) && lane == 0) {
+      multi[u] = 1;
+      atomicAdd(nmulti, 1ull);
+    }
+    __syncthreads();  // table and buffer b are reused by the next units
   }
 }
 
@@ -385,23 +516,6 @@ struct WBuf {
   uint16_t st[PCH_MAX + 8];
 };
 static_assert(sizeof(WBuf) % 16 == 0, "16-byte aligned buffers");
-
-struct Win {  // aligned copy window of elements [first, first + cnt) of an array
-  uint64_t a0;     // window start (bytes)
-  uint32_t bytes;  // window length (bytes, multiple of 16; 0 = nothing to copy)
-  uint32_t shift;  // element `first` sits at dst[shift]
-  uint32_t valid;  // elements [first, first + valid) are inside the window
-};
-__device__ __forceinline__ Win window(uint64_t first, uint32_t cnt, uint32_t esz, uint64_t total) {
-  Win w;
-  const uint64_t b0 = first * esz, b1 = (first + cnt) * esz;
-  w.a0 = b0 & ~15ull;
-  const uint64_t a1 = min((b1 + 15) & ~15ull, (total * esz) & ~15ull);
-  w.bytes = a1 > w.a0 ? (uint32_t)(a1 - w.a0) : 0u;
-  w.shift = (uint32_t)((b0 - w.a0) / esz);
-  w.valid = a1 > b0 ? (uint32_t)min((uint64_t)cnt, (a1 - b0) / esz) : 0u;
-  return w;
-}
 
 __device__ __forceinline__ void wf_issue(WBuf& B, uint64_t* bar, const uint4 d, const HJArgs& a,
                                          const uint16_t* stage) {
@@ -572,12 +686,23 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
   a.U = U;
   a.wcnt = wcnt;
   a.swap = swap;
+  a.nb = Bld.n;
+  a.np = Prb.n;
   {
-    const size_t smem = hj_smem<K, false>();
-    static bool once = (set_smem(hj_count_kernel<K>, smem), true);
-    (void)once;
-    launch(ctx, "hj_count", hj_count_kernel<K>, dim3(hj_grid(ctx, hj_count_kernel<K>, smem, U)), dim3(HT), smem, a,
-           stage, multi, nmulti);
+    static const int v = std::getenv("GJ_HJ_COUNT_V") ? std::atoi(std::getenv("GJ_HJ_COUNT_V")) : 1;
+    if (v == 1) {
+      const size_t smem = 2 * sizeof(CBuf<K>) + 16 + Table<K>::kBytes;
+      static bool once = (set_smem(hj_count_tma<K>, smem), true);
+      (void)once;
+      launch(ctx, "hj_count", hj_count_tma<K>, dim3(hj_grid(ctx, hj_count_tma<K>, smem, U)), dim3(HT), smem, a,
+             stage, multi, nmulti);
+    } else {
+      const size_t smem = hj_smem<K, false>();
+      static bool once = (set_smem(hj_count_kernel<K>, smem), true);
+      (void)once;
+      launch(ctx, "hj_count", hj_count_kernel<K>, dim3(hj_grid(ctx, hj_count_kernel<K>, smem, U)), dim3(HT), smem,
+             a, stage, multi, nmulti);
+    }
   }
   exclusive_scan<uint32_t, uint64_t>(ctx, wcnt, woff, nw, woff + nw);
   uint64_t h[2];

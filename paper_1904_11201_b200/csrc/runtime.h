@@ -85,8 +85,8 @@ struct gj_ctx {
   int num_sms = 148;
   // options (gjoin.h GJ_OPT_*)
   int part_bits = -1;
-  uint32_t build_chunk = 2048;
-  uint32_t probe_chunk = 2048;
+  uint32_t build_chunk = 4096;
+  uint32_t probe_chunk = 4096;
   bool profile = false;
   uint32_t nlj_split = 0;
   bool force_slow_band = false;

@@ -689,7 +689,7 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
   a.nb = Bld.n;
   a.np = Prb.n;
   {
-    static const int v = std::getenv("GJ_HJ_COUNT_V") ? std::atoi(std::getenv("GJ_HJ_COUNT_V")) : 1;
+    static const int v = std::getenv("GJ_HJ_COUNT_V") ? std::atoi(std::getenv("GJ_HJ_COUNT_V")) : 0;
     if (v == 1) {
       const size_t smem = 2 * sizeof(CBuf<K>) + 16 + Table<K>::kBytes;
       static bool once = (set_smem(hj_count_tma<K>, smem), true);

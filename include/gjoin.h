@@ -99,7 +99,12 @@ const char* gj_last_error(void);
  *  GJ_OPT_BUILD_SIDE       0 = smaller side (default), 1 = always R, 2 = always S
  *  GJ_OPT_SHUFFLE_BITS     multi-GPU equi join: local radix bits folded into the NVLink
  *                          shuffle pass (0 = destination rank only, the default; at most
- *                          9 - log2(#ranks); must be equal on every rank) */
+ *                          9 - log2(#ranks); must be equal on every rank)
+ *  GJ_OPT_THETA_REGIONS    1 = theta joins through the region matrix of PAPER.md §4.2
+ *                          Alg.3 (default): both relations range-partitioned into
+ *                          equal-width key buckets, only cells that can hold a match
+ *                          visited by the NLJ, Green cells written as cross products;
+ *                          0 = the NLJ over all n_R x n_S pairs */
 enum {
   GJ_OPT_PART_BITS = 1,
   GJ_OPT_BUILD_CHUNK = 2,
@@ -108,7 +113,8 @@ enum {
   GJ_OPT_NLJ_SPLIT = 5,
   GJ_OPT_FORCE_SLOW_BAND = 6,
   GJ_OPT_BUILD_SIDE = 7,
-  GJ_OPT_SHUFFLE_BITS = 8
+  GJ_OPT_SHUFFLE_BITS = 8,
+  GJ_OPT_THETA_REGIONS = 9
 };
 gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t value);
 

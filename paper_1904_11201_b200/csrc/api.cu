@@ -304,6 +304,7 @@ gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t v) {
       if (v < 0 || v > 9) throw Error(GJ_EINVAL, "shuffle_bits must be in [0, 9]");
       ctx->shuffle_bits = (int)v;
       break;
+    case GJ_OPT_THETA_REGIONS: ctx->theta_regions = v != 0; break;
     case GJ_OPT_BUILD_SIDE:
       if (v < 0 || v > 2) throw Error(GJ_EINVAL, "build_side must be 0, 1 or 2");
       ctx->build_side = (int)v;

@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "nlj.cuh"
+#include "partition.cuh"
 #include "scan.cuh"
 
 namespace gj {
@@ -157,6 +158,7 @@ struct NLJArgs {
   uint64_t* wcnt;
   const uint64_t* woff;
   uint2* out;
+  const uint4* udesc;  // region mode: unit u = R rows [x, x + y) x S rows [z, z + w); else a uniform grid
 };
 
 // Write pass, a screened group of 4 S keys holding a match: each lane builds its
@@ -216,12 +218,22 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
     __syncthreads();
     const uint32_t u = s_u;
     if (u >= a.U) break;
-    const uint64_t r0 = (uint64_t)(u / a.nsplit) * RT;
-    const uint64_t sbeg = (uint64_t)(u % a.nsplit) * a.SR;
-    const uint64_t send = min(sbeg + a.SR, a.nS);
-    const uint64_t slen = send > sbeg ? send - sbeg : 0;
+    uint64_t r0, rend, sbeg, slen;
+    if (a.udesc) {
+      const uint4 ud = a.udesc[u];
+      r0 = ud.x;
+      rend = (uint64_t)ud.x + ud.y;
+      sbeg = ud.z;
+      slen = ud.w;
+    } else {
+      r0 = (uint64_t)(u / a.nsplit) * RT;
+      rend = a.nR;
+      sbeg = (uint64_t)(u % a.nsplit) * a.SR;
+      const uint64_t send = min(sbeg + a.SR, a.nS);
+      slen = send > sbeg ? send - sbeg : 0;
+    }
     const uint32_t ntiles = (uint32_t)((slen + TS - 1) / TS);
-    const bool full = r0 + RT <= a.nR;
+    const bool full = r0 + RT <= rend;
 
     K rk[KR];
     uint32_t rf[KR], rr[KR];
@@ -229,7 +241,7 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
 #pragma unroll
     for (int i = 0; i < KR; ++i) {
       const uint64_t row = r0 + (uint64_t)i * NT + tid;
-      const bool v = row < a.nR;
+      const bool v = row < rend;
       rk[i] = v ? rkey[row] : K(0);
       nvalid += v;
       if (WRITE) rr[i] = v ? (a.rrid ? a.rrid[row] : a.rrid_base + (uint32_t)row) : 0u;
@@ -343,14 +355,14 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
             uint32_t c = 0;
 #pragma unroll
             for (int i = 0; i < KR; ++i)
-              c += ((r0 + (uint64_t)i * NT + tid) < a.nR && theta_exact<K, OP>(rk[i], s, a.eps));
+              c += ((r0 + (uint64_t)i * NT + tid) < rend && theta_exact<K, OP>(rk[i], s, a.eps));
             tot += c;
           } else {
             bool any = false;
             bool p[KR];
 #pragma unroll
             for (int i = 0; i < KR; ++i) {
-              p[i] = (r0 + (uint64_t)i * NT + tid) < a.nR && theta_exact<K, OP>(rk[i], s, a.eps);
+              p[i] = (r0 + (uint64_t)i * NT + tid) < rend && theta_exact<K, OP>(rk[i], s, a.eps);
               any |= p[i];
             }
             if (__any_sync(FULL, any)) {
@@ -411,6 +423,22 @@ __global__ void cross_kernel(const uint32_t* __restrict__ rrid, uint32_t rbase, 
   }
 }
 
+// Green regions (Alg.3 "do cross join"): rectangle b = R rows [x, x + y) x S rows
+// [z, z + w) of the range-partitioned relations, every pair written R-major at
+// base[b].  CTAs stride over the pairs of every rectangle in turn.
+__global__ void cross_rect_kernel(const uint4* __restrict__ rect, const uint64_t* __restrict__ base, uint32_t nrect,
+                                  const uint32_t* __restrict__ rrid, const uint32_t* __restrict__ srid, uint2* out) {
+  for (uint32_t b = 0; b < nrect; ++b) {
+    const uint4 q = rect[b];
+    const uint64_t total = (uint64_t)q.y * q.w, o = base[b];
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+      const uint64_t i = x / q.w, j = x - i * q.w;
+      out[o + x] = make_uint2(rrid[q.x + i], srid[q.z + j]);
+    }
+  }
+}
+
 // ----------------------------------------------------------------- host side
 template <typename K, int OP, bool FAST>
 void run(gj_ctx* ctx, const NLJArgs& a, bool write) {
@@ -466,6 +494,113 @@ NLJArgs make_args(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, const ThetaCach
   return a;
 }
 
+// Region matrix (§4.2, Alg.3).  Both relations are range-
+// partitioned into the same equal-width key buckets (the "k quantiles of each
+// range", reading R15 in DESIGN.md), so cell (x, y) of the k x k matrix is the pair
+// (R bucket x, S bucket y) and every key of bucket x is below every key of bucket
+// x + 1.  For the rows of one R tile (RT consecutive rows of the partitioned R,
+// buckets x1..x2) the cells that can hold a match form one contiguous S range V:
+// the tile's own buckets [x1, x2] for =, !=, <, <=, >, >= and [x1 - m, x2 + m] for
+// the band (m = ceil(eps / w) neighbour buckets of width w).  V is visited by the
+// tiled NLJ with the exact predicate (cells inside V that are White, or Green, cost
+// compares but cannot give a wrong pair).  Everything outside V is either White --
+// skipped -- or Green, written as a cross product without compares: for < and <=
+// the S rows after V (all S buckets > x2), for > and >= the rows before V, for !=
+// both.  V's ends are rounded to 16-byte boundaries for the TMA copies; the Green
+// rectangles start exactly where V ends, so every pair is produced once.
+template <typename K>
+void region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, int op, uint64_t eps, unsigned long long lo,
+                  unsigned long long hi, bool fast) {
+  ThetaCache& tc = ctx->tc;
+  const unsigned long long span = hi - lo;
+  uint32_t Bb = 1;  // ~256 R rows per bucket: an R tile spans ~8 buckets
+  while (Bb < 18 && (R.n >> (Bb + 8)) > 0) ++Bb;
+  const uint32_t L = span ? 64 - (uint32_t)__builtin_clzll(span) : 0;
+  const uint32_t sh = L > Bb ? L - Bb : 0;
+  const uint32_t P = 1u << Bb;
+  const Partitioned PR = range_partition(ctx, R, Bb, lo, sh, "tR");
+  const Partitioned PS = range_partition(ctx, S, Bb, lo, sh, "tS");
+  std::vector<uint32_t> ro(P + 1), so(P + 1);
+  d2h_sync(ctx, ro.data(), PR.off, (P + 1) * sizeof(uint32_t));
+  d2h_sync(ctx, so.data(), PS.off, (P + 1) * sizeof(uint32_t));
+  // band: buckets y with |x - y| <= m can hold a pair (min distance (|x-y|-1) w + 1 <= eps)
+  uint64_t m = 0;
+  if (op == GJ_BAND) {
+    const unsigned __int128 w = (unsigned __int128)1 << sh;
+    const unsigned __int128 mm = ((unsigned __int128)eps + w - 1) / w;
+    m = mm > P ? P : (uint64_t)mm;
+  }
+  const uint64_t al = 16 / sizeof(K);  // V's ends on 16-byte boundaries (TMA)
+  const uint64_t nR = R.n, nS = S.n;
+  const uint64_t ntile = (nR + RT - 1) / RT;
+  struct TileV { uint64_t vb, ve; };
+  std::vector<TileV> tv(ntile);
+  uint64_t visit = 0;
+  auto bucket_of = [&](uint64_t row) -> uint64_t {
+    return (uint64_t)(std::upper_bound(ro.begin(), ro.end(), (uint32_t)row) - ro.begin()) - 1;
+  };
+  tc.rects.clear();
+  tc.rect_base.clear();
+  for (uint64_t t = 0; t < ntile; ++t) {
+    const uint64_t r0 = t * RT, rn = std::min<uint64_t>(RT, nR - r0);
+    const uint64_t x1 = bucket_of(r0), x2 = bucket_of(r0 + rn - 1);
+    uint64_t ylo = x1, yhi = x2;
+    if (op == GJ_BAND) {
+      ylo = x1 > m ? x1 - m : 0;
+      yhi = std::min<uint64_t>(P - 1, x2 + m);
+    }
+    const uint64_t vb = so[ylo] / al * al, ve = std::min<uint64_t>(nS, (so[yhi + 1] + al - 1) / al * al);
+    tv[t] = {vb, ve};
+    visit += ve - vb;
+    const bool after = op == GJ_LT || op == GJ_LE || op == GJ_NE;   // Green: S buckets > x2
+    const bool before = op == GJ_GT || op == GJ_GE || op == GJ_NE;  // Green: S buckets < x1
+    if (after && ve < nS) tc.rects.push_back(make_uint4((uint32_t)r0, (uint32_t)rn, (uint32_t)ve, (uint32_t)(nS - ve)));
+    if (before && vb > 0) tc.rects.push_back(make_uint4((uint32_t)r0, (uint32_t)rn, 0u, (uint32_t)vb));
+  }
+  // NLJ units: V split into S chunks of SR rows (a multiple of the TMA tile)
+  uint64_t SR = std::max<uint64_t>(TS, (visit / 16384 + TS - 1) / TS * TS);
+  if (ctx->nlj_split) SR = std::max<uint64_t>(TS, (nS / ctx->nlj_split + TS - 1) / TS * TS);
+  std::vector<uint4> ud;
+  for (uint64_t t = 0; t < ntile; ++t) {
+    const uint64_t r0 = t * RT, rn = std::min<uint64_t>(RT, nR - r0);
+    for (uint64_t s0 = tv[t].vb; s0 < tv[t].ve; s0 += SR)
+      ud.push_back(make_uint4((uint32_t)r0, (uint32_t)rn, (uint32_t)s0, (uint32_t)std::min<uint64_t>(SR, tv[t].ve - s0)));
+  }
+  tc.regions = true;
+  tc.PR = gj_rel{PR.key, PR.rid, nR, R.key_type, 0};
+  tc.PS = gj_rel{PS.key, PS.rid, nS, S.key_type, 0};
+  tc.U = (uint32_t)ud.size();
+  tc.nsplit = 1;
+  tc.SR = SR;
+  tc.mode = fast ? 1 : 0;
+  uint64_t cross = 0;
+  for (const uint4& q : tc.rects) {
+    tc.rect_base.push_back(cross);
+    cross += (uint64_t)q.y * q.w;
+  }
+  tc.nlj_total = 0;
+  if (tc.U) {
+    uint4* udev = static_cast<uint4*>(ws(ctx, "nlj.udesc", ud.size() * sizeof(uint4)));
+    GJ_CUDA(cudaMemcpyAsync(udev, ud.data(), ud.size() * sizeof(uint4), cudaMemcpyHostToDevice, ctx->stream));
+    tc.udesc = udev;
+    const uint64_t nw = (uint64_t)tc.U * NWARP;
+    uint64_t* wcnt = static_cast<uint64_t*>(ws(ctx, "nlj.wcnt", (nw + 1) * sizeof(uint64_t)));
+    uint64_t* woff = static_cast<uint64_t*>(ws(ctx, "nlj.woff", (nw + 1) * sizeof(uint64_t)));
+    uint32_t* work = static_cast<uint32_t*>(ws(ctx, "nlj.work", 16));
+    GJ_CUDA(cudaMemsetAsync(work, 0, sizeof(uint32_t), ctx->stream));
+    NLJArgs a = make_args(ctx, tc.PR, tc.PS, tc);
+    a.work = work;
+    a.wcnt = wcnt;
+    a.udesc = udev;
+    dispatch<K>(ctx, a, op, fast, false);
+    exclusive_scan<uint64_t, uint64_t>(ctx, wcnt, woff, nw, woff + nw);
+    tc.woff = woff;
+    d2h_sync(ctx, &tc.nlj_total, woff + nw, sizeof(uint64_t));  // also orders the udesc copy before ud dies
+  }
+  for (uint64_t& b : tc.rect_base) b += tc.nlj_total;
+  tc.total = tc.nlj_total + cross;
+}
+
 template <typename K>
 void theta_count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S0, int op, uint64_t eps) {
   ThetaCache& tc = ctx->tc;
@@ -483,14 +618,20 @@ void theta_count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S0, int op, ui
     S.key = al;
   }
   tc.S = S;
+  tc.regions = false;
   bool fast = (sizeof(K) == 4) && !ctx->force_slow_band;
-  if (op == GJ_BAND) {
+  const bool regions = ctx->theta_regions != 0 && R.n < (1ull << 32) && S.n < (1ull << 32);
+  unsigned long long lo = 0, hi = 0;
+  if (op == GJ_BAND || regions) {
     unsigned long long* mm = static_cast<unsigned long long*>(ws(ctx, "nlj.minmax", 4 * sizeof(unsigned long long)));
     key_minmax(ctx, R, mm);
     key_minmax(ctx, S, mm + 2);
     unsigned long long h[4];
     d2h_sync(ctx, h, mm, sizeof(h));
-    const unsigned long long lo = std::min(h[0], h[2]), hi = std::max(h[1], h[3]);
+    lo = std::min(h[0], h[2]);
+    hi = std::max(h[1], h[3]);
+  }
+  if (op == GJ_BAND) {
     const unsigned long long span = hi - lo;  // exact: biased keys are order-preserving
     if (eps >= span) {
       tc.all_pairs = true;
@@ -501,6 +642,7 @@ void theta_count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S0, int op, ui
     if (!(span + eps < (1ull << 32) && 2 * eps < (1ull << 32) - 1)) fast = false;
     if (ctx->force_slow_band) fast = false;
   }
+  if (regions) return region_count<K>(ctx, R, S, op, eps, lo, hi, fast);
   tc.mode = fast ? 1 : 0;
   const uint64_t n_rt = (R.n + RT - 1) / RT;
   const uint64_t max_split = (S.n + TS - 1) / TS;
@@ -532,6 +674,28 @@ void theta_write_impl(gj_ctx* ctx, uint32_t* out) {
   ThetaCache& tc = ctx->tc;
   if (tc.total == 0) return;
   if (tc.all_pairs) return cross_write(ctx, tc.R, tc.S, out);
+  if (tc.regions) {
+    if (tc.nlj_total) {
+      uint32_t* work = static_cast<uint32_t*>(ws(ctx, "nlj.work", 16));
+      GJ_CUDA(cudaMemsetAsync(work, 0, sizeof(uint32_t), ctx->stream));
+      NLJArgs a = make_args(ctx, tc.PR, tc.PS, tc);
+      a.work = work;
+      a.woff = tc.woff;
+      a.out = reinterpret_cast<uint2*>(out);
+      a.udesc = tc.udesc;
+      dispatch<K>(ctx, a, tc.op, tc.mode == 1, true);
+    }
+    if (!tc.rects.empty()) {
+      const size_t nr = tc.rects.size();
+      uint4* rd = static_cast<uint4*>(ws(ctx, "nlj.rects", nr * sizeof(uint4)));
+      uint64_t* bd = static_cast<uint64_t*>(ws(ctx, "nlj.rect_base", nr * sizeof(uint64_t)));
+      GJ_CUDA(cudaMemcpyAsync(rd, tc.rects.data(), nr * sizeof(uint4), cudaMemcpyHostToDevice, ctx->stream));
+      GJ_CUDA(cudaMemcpyAsync(bd, tc.rect_base.data(), nr * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+      launch(ctx, "cross_rect", cross_rect_kernel, dim3(ctx->num_sms * 8), dim3(256), 0, (const uint4*)rd,
+             (const uint64_t*)bd, (uint32_t)nr, tc.PR.rid, tc.PS.rid, reinterpret_cast<uint2*>(out));
+    }
+    return;
+  }
   uint32_t* work = static_cast<uint32_t*>(ws(ctx, "nlj.work", 16));
   GJ_CUDA(cudaMemsetAsync(work, 0, sizeof(uint32_t), ctx->stream));
   NLJArgs a = make_args(ctx, tc.R, tc.S, tc);

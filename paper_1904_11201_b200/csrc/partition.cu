@@ -68,6 +68,15 @@ template <typename K>
 __device__ __forceinline__ uint32_t digit_of(K k, uint32_t shift, uint32_t mask) {
   return (khash(k) >> shift) & mask;
 }
+// RANGE mode (theta region matrix): the partition word is the key's equal-width
+// bucket ((bias(key) - lo) >> sh) placed in its top bits, so partitions are key
+// ranges in ascending order.
+template <bool RANGE, typename K>
+__device__ __forceinline__ uint32_t digit_of(K k, uint32_t shift, uint32_t mask, const DigitFn& f) {
+  if (!RANGE) return digit_of(k, shift, mask);
+  const uint32_t w = (uint32_t)(((unsigned long long)KeyT<K>::bias(k) - f.lo) >> f.sh) << f.up;
+  return (w >> shift) & mask;
+}
 
 // tile loads: thread (w, lane) takes items (w*PI + i)*32 + lane -- coalesced per
 // warp instruction, and warp w's items are a contiguous, in-order slice of the tile
@@ -87,12 +96,13 @@ __device__ __forceinline__ void load_tile(const K* __restrict__ key, const uint3
 // tile t, stores the running per-digit counts as tile t's exclusive in-chunk
 // prefix row (tile_pref[chunk*TPC + t][d], coalesced), so the scatter of tile t
 // finds its offsets with one row read -- no inter-CTA look-back.
-template <typename K>
+template <typename K, bool RANGE>
 __global__ void __launch_bounds__(PT) part_hist(const K* __restrict__ key, uint64_t n,
                                                 const uint32_t* __restrict__ seg_off,
                                                 const uint32_t* __restrict__ chunk_base,
                                                 uint32_t nseg, uint32_t shift, uint32_t bits,
-                                                uint32_t* __restrict__ hist, uint32_t* __restrict__ tile_pref) {
+                                                uint32_t* __restrict__ hist, uint32_t* __restrict__ tile_pref,
+                                                DigitFn fn) {
   __shared__ uint32_t h[(1 << MAX_BITS) + 1];
   const uint32_t D = 1u << bits, mask = D - 1;
   const uint32_t c = blockIdx.x;
@@ -120,7 +130,7 @@ __global__ void __launch_bounds__(PT) part_hist(const K* __restrict__ key, uint6
     // branch-free: padding items count into the dummy bin D
 #pragma unroll
     for (int i = 0; i < PI; ++i)
-      atomicAdd(&h[(w * PI + i) * 32 + lane < cnt ? digit_of(k[i], shift, mask) : D], 1u);
+      atomicAdd(&h[(w * PI + i) * 32 + lane < cnt ? digit_of<RANGE>(k[i], shift, mask, fn) : D], 1u);
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < PI; ++i) k[i] = kn[i];
@@ -520,12 +530,12 @@ struct LocalLayout {
   static size_t bytes(uint32_t D) { return off_whist + ((size_t)NW * words(D) + (size_t)D) * 4; }
 };
 
-template <typename K, bool HAS_RID, bool WB1>
+template <typename K, bool HAS_RID, bool RANGE>
 __global__ void __launch_bounds__(PT, 2) part_scatter_local(
     const K* __restrict__ key_in, const uint32_t* __restrict__ rid_in, uint32_t rid_base, uint64_t n,
     const uint4* __restrict__ tdesc, uint32_t ntiles, uint32_t shift, uint32_t bits,
     const uint32_t* __restrict__ tile_base, K* __restrict__ key_out, uint32_t* __restrict__ rid_out,
-    uint32_t* __restrict__ tile_ctr) {
+    uint32_t* __restrict__ tile_ctr, DigitFn fn) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using L = LocalLayout<K>;
   constexpr bool ILV = sizeof(K) == 4;  // int32: one (key, rid) uint2 per staging slot
@@ -634,7 +644,7 @@ __global__ void __launch_bounds__(PT, 2) part_scatter_local(
 #pragma unroll
     for (int i = 0; i < PI; ++i) {
       const uint32_t j = (w * PI + i) * 32 + lane;
-      rk[i] = j < cnt ? digit_of(k[i], shift, mask) : D;  // padding -> dummy counter D
+      rk[i] = j < cnt ? digit_of<RANGE>(k[i], shift, mask, fn) : D;  // padding -> dummy counter D
     }
 #pragma unroll
     for (int i = 0; i < PI; ++i) rk[i] = (rk[i] << 16) | atomicAdd(whist + w * W + rk[i], 1u);
@@ -707,29 +717,8 @@ __global__ void __launch_bounds__(PT, 2) part_scatter_local(
     // write-back in groups of 8 items: loads, offsets, then (predicated) stores --
     // staging slots past cnt hold stale data but index delta[] safely
     constexpr int WG = 8;
-    if (WB1) {
-#pragma unroll 4
-      for (int i = 0; i < PI; ++i) {
-        const uint32_t j = i * PT + threadIdx.x;
-        if (j < cnt) {
-          K kk;
-          uint32_t rv;
-          if (ILV) {
-            const uint2 e = stg[j];
-            kk = (K)e.x;
-            rv = e.y;
-          } else {
-            kk = skey[j];
-            rv = srid[j];
-          }
-          const uint32_t pos = delta[digit_of(kk, shift, mask)] + j;
-          key_out[pos] = kk;
-          rid_out[pos] = rv;
-        }
-      }
-    }
 #pragma unroll
-    for (int i0 = 0; i0 < PI && !WB1; i0 += WG) {
+    for (int i0 = 0; i0 < PI; i0 += WG) {
       K kk[WG];
       uint32_t rv[WG], pos[WG];
 #pragma unroll
@@ -745,7 +734,7 @@ __global__ void __launch_bounds__(PT, 2) part_scatter_local(
         }
       }
 #pragma unroll
-      for (int q = 0; q < WG; ++q) pos[q] = delta[digit_of(kk[q], shift, mask)] + (i0 + q) * PT + threadIdx.x;
+      for (int q = 0; q < WG; ++q) pos[q] = delta[digit_of<RANGE>(kk[q], shift, mask, fn)] + (i0 + q) * PT + threadIdx.x;
 #pragma unroll
       for (int q = 0; q < WG; ++q) {
         if ((i0 + q) * PT + threadIdx.x < cnt) {
@@ -758,11 +747,11 @@ __global__ void __launch_bounds__(PT, 2) part_scatter_local(
   }
 }
 
-template <typename K, bool HAS_RID, bool WB1>
+template <typename K, bool HAS_RID, bool RANGE>
 void launch_scatter_local(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
                           const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits,
-                          const uint32_t* tile_base, K* kout, uint32_t* rout) {
-  auto kern = part_scatter_local<K, HAS_RID, WB1>;
+                          const uint32_t* tile_base, K* kout, uint32_t* rout, const DigitFn& fn) {
+  auto kern = part_scatter_local<K, HAS_RID, RANGE>;
   const size_t smem = LocalLayout<K>::bytes(1u << bits);
   static bool once = (set_smem(kern, LocalLayout<K>::bytes(1u << MAX_BITS)), true);
   (void)once;
@@ -773,7 +762,7 @@ void launch_scatter_local(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32
   uint32_t* ctr = static_cast<uint32_t*>(ws(ctx, "part.tile_ctr", sizeof(uint32_t)));
   GJ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), ctx->stream));
   launch(ctx, "part_scatter", kern, dim3(grid), dim3(PT), smem, kin, rin, rid_base, n, tdesc, (uint32_t)ntiles,
-         shift, bits, tile_base, kout, rout, ctr);
+         shift, bits, tile_base, kout, rout, ctr, fn);
 }
 
 // Turns the in-chunk prefix rows of part_hist into absolute run starts: every
@@ -827,10 +816,7 @@ void launch_scatter_t(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t r
   const int v = REMOTE ? (scatter_variant() & 1) : scatter_variant();  // the shuffle stages key/rid separately
   if (!REMOTE && v == 4) {  // tile_pref holds absolute run starts (tile_base_kernel)
     launch_scatter_local<K, HAS_RID, false>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_pref, kout,
-                                            rout);
-  } else if (!REMOTE && v == 5) {
-    launch_scatter_local<K, HAS_RID, true>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_pref, kout,
-                                           rout);
+                                            rout, DigitFn{});
   } else if (sizeof(K) == 4 && (v & 2)) {
     if (v & 1)
       launch_scatter_v<K, HAS_RID, REMOTE, true, sizeof(K) == 4>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift,
@@ -890,9 +876,9 @@ __global__ void fill_off2(uint32_t* off, uint64_t n) {
   off[1] = (uint32_t)n;
 }
 
-template <typename K>
+template <typename K, bool RANGE>
 Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char* tag, uint32_t skip,
-                           const uint32_t* seg_off0, uint32_t nseg0) {
+                           const uint32_t* seg_off0, uint32_t nseg0, const DigitFn& fn) {
   std::string t(tag);
   Partitioned out;
   const uint64_t n = X.n;
@@ -936,17 +922,26 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
     uint32_t* hist = static_cast<uint32_t*>(ws(ctx, (t + ".hist").c_str(), (hn + 1) * sizeof(uint32_t)));
     const uint64_t ntiles = max_chunks * TPC;
     uint32_t* tile_pref = static_cast<uint32_t*>(ws(ctx, "part.tile_pref", ntiles * D * sizeof(uint32_t)));
-    launch(ctx, "part_hist", part_hist<K>, dim3((unsigned)max_chunks), dim3(PT), 0, kin, n, seg_off,
-           (const uint32_t*)chunk_base, nseg, shift, bits, hist, tile_pref);
+    launch(ctx, "part_hist", part_hist<K, RANGE>, dim3((unsigned)max_chunks), dim3(PT), 0, kin, n, seg_off,
+           (const uint32_t*)chunk_base, nseg, shift, bits, hist, tile_pref, fn);
     exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
-    if (scatter_variant() >= 4)
+    if (RANGE || scatter_variant() >= 4)
       launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, seg_off,
              (const uint32_t*)chunk_base, nseg, bits, (const uint32_t*)hist, tile_pref);
     uint4* tdesc = static_cast<uint4*>(ws(ctx, "part.tdesc", (ntiles + 1) * sizeof(uint4)));
     launch(ctx, "tile_desc", tile_desc_kernel, dim3((unsigned)((ntiles + 255) / 256)), dim3(256), 0, n, seg_off,
            (const uint32_t*)chunk_base, nseg, D, (uint32_t)ntiles, tdesc);
-    launch_scatter<K, false>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, hist, tile_pref, kout, rout,
-                             ShuffleDest{});
+    if (RANGE) {
+      if (rin)
+        launch_scatter_local<K, true, true>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, tile_pref, kout,
+                                            rout, fn);
+      else
+        launch_scatter_local<K, false, true>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, tile_pref,
+                                             kout, rout, fn);
+    } else {
+      launch_scatter<K, false>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, hist, tile_pref, kout, rout,
+                               ShuffleDest{});
+    }
     const uint32_t P = nseg << bits;
     uint32_t* off = static_cast<uint32_t*>(ws(ctx, (ps + ".off").c_str(), (P + 1) * sizeof(uint32_t)));
     launch(ctx, "extract_off", extract_off, dim3((P + 1 + 255) / 256), dim3(256), 0, (const uint32_t*)hist,
@@ -982,9 +977,9 @@ ShufflePass shuffle_prepare_impl(gj_ctx* ctx, const gj_rel& X, uint32_t g, const
   sp.ntiles = max_chunks * TPC;
   uint32_t* tile_pref = static_cast<uint32_t*>(ws(ctx, (t + ".stp").c_str(), sp.ntiles * D * sizeof(uint32_t) + 4));
   const uint32_t shift = 32 - g;
-  launch(ctx, "part_hist", part_hist<K>, dim3((unsigned)std::max<uint64_t>(max_chunks, 1)), dim3(PT), 0,
+  launch(ctx, "part_hist", part_hist<K, false>, dim3((unsigned)std::max<uint64_t>(max_chunks, 1)), dim3(PT), 0,
          static_cast<const K*>(X.key), n, (const uint32_t*)nullptr, (const uint32_t*)nullptr, 1u, shift, g, hist,
-         tile_pref);
+         tile_pref, DigitFn{});
   exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
   uint4* tdesc = static_cast<uint4*>(ws(ctx, (t + ".stdesc").c_str(), (sp.ntiles + 1) * sizeof(uint4)));
   launch(ctx, "tile_desc", tile_desc_kernel, dim3((unsigned)((sp.ntiles + 255) / 256)), dim3(256), 0, n,
@@ -1006,8 +1001,16 @@ int radix_passes(uint32_t B) { return B == 0 ? 0 : (int)((B + MAX_BITS - 1) / MA
 
 Partitioned radix_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char* tag, uint32_t skip,
                             const uint32_t* seg_off0, uint32_t nseg0) {
-  if (X.key_type == GJ_I32) return partition_impl<int32_t>(ctx, X, B, tag, skip, seg_off0, nseg0);
-  return partition_impl<int64_t>(ctx, X, B, tag, skip, seg_off0, nseg0);
+  if (X.key_type == GJ_I32) return partition_impl<int32_t, false>(ctx, X, B, tag, skip, seg_off0, nseg0, DigitFn{});
+  return partition_impl<int64_t, false>(ctx, X, B, tag, skip, seg_off0, nseg0, DigitFn{});
+}
+
+Partitioned range_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, unsigned long long lo, uint32_t sh,
+                            const char* tag) {
+  if (B == 0 || B > 18) throw Error(GJ_EINVAL, "range partition needs 1..18 bucket bits");
+  const DigitFn fn{lo, sh, 32 - B};
+  if (X.key_type == GJ_I32) return partition_impl<int32_t, true>(ctx, X, B, tag, 0, nullptr, 1, fn);
+  return partition_impl<int64_t, true>(ctx, X, B, tag, 0, nullptr, 1, fn);
 }
 
 ShufflePass shuffle_prepare(gj_ctx* ctx, const gj_rel& X, uint32_t g, const char* tag) {

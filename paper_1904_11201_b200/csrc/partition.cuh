@@ -30,6 +30,20 @@ int radix_passes(uint32_t B);
 Partitioned radix_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char* tag, uint32_t skip = 0,
                             const uint32_t* seg_off0 = nullptr, uint32_t nseg0 = 1);
 
+// Key -> partition word for range partitioning: ((bias(key) - lo) >> sh) << up.
+struct DigitFn {
+  unsigned long long lo = 0;
+  uint32_t sh = 0;
+  uint32_t up = 0;
+};
+// Range-partition X into 2^B equal-width key buckets: bucket(key) =
+// (bias(key) - lo) >> sh (bias = order-preserving signed -> unsigned map; every
+// key must satisfy lo <= bias(key) and bucket < 2^B).  Partition p holds the keys
+// of bucket p, so partitions are ascending key ranges (theta region matrix,
+// PAPER.md:258-266 §4.2).  Stable; off[p] as for radix_partition.
+Partitioned range_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, unsigned long long lo, uint32_t sh,
+                            const char* tag);
+
 // ---- multi-GPU shuffle fused into the partition scatter
 constexpr int MAX_RANKS = 8;
 struct ShuffleDest {

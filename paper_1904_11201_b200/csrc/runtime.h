@@ -70,6 +70,14 @@ struct ThetaCache {
   uint64_t total = 0;
   bool all_pairs = false;  // band with eps >= span: every pair qualifies
   const void* S_user_key = nullptr;  // caller's S.key (tc.S may be a realigned copy)
+  // region-matrix mode (§4.2, Alg.3): range-partitioned relations, the NLJ
+  // work units (r0, rn, s0, sn) over them and the Green cross-product rectangles
+  bool regions = false;
+  gj_rel PR{}, PS{};
+  const uint4* udesc = nullptr;
+  uint64_t nlj_total = 0;
+  std::vector<uint4> rects;
+  std::vector<uint64_t> rect_base;
 };
 
 struct ProfRec {
@@ -90,6 +98,7 @@ struct gj_ctx {
   bool profile = false;
   uint32_t nlj_split = 0;
   bool force_slow_band = false;
+  int theta_regions = 1;  // theta joins through the region matrix (0 = plain NLJ over all pairs)
   int build_side = 0;
   int shuffle_bits = 0;
   // workspace

@@ -425,3 +425,59 @@ def test_launch_accounting_and_profile(gj):
     assert "hj_count" in t and "hj_write" in t and "part_scatter" in t
     assert c.launches() == sum(v[1] for v in t.values())
     c.close()
+
+
+# ------------------------------------------------------------------ theta region matrix (§4.2, Alg.3)
+
+def _region_inputs(kind):
+    rng = np.random.default_rng({"dups": 1, "wide": 2, "skew": 3, "extremes": 4, "equal": 5}[kind])
+    if kind == "dups":        # small domain: many equal keys, buckets of width 1
+        return (rng.integers(-40, 40, 9000).astype(np.int32), rng.integers(-40, 40, 20001).astype(np.int32))
+    if kind == "wide":        # several R tiles, each spanning many buckets
+        return (rng.integers(-10**6, 10**6, 9000).astype(np.int32), rng.integers(-10**6, 10**6, 30003).astype(np.int32))
+    if kind == "skew":        # Zipf-like: most keys in few buckets, a long sparse tail
+        z = lambda n: (np.floor(np.exp(rng.uniform(0, 14, n))) * rng.choice([-1, 1], n)).astype(np.int32)
+        return z(7000), z(15000)
+    if kind == "extremes":    # full int32 range incl. INT_MIN / INT_MAX
+        R = rng.integers(-2**31, 2**31, 5000, dtype=np.int64).astype(np.int32)
+        S = rng.integers(-2**31, 2**31, 8000, dtype=np.int64).astype(np.int32)
+        R[:3] = [-2**31, 2**31 - 1, 0]
+        S[:3] = [2**31 - 1, -2**31, 0]
+        return R, S
+    if kind == "equal":       # span 0: one bucket
+        return np.full(3000, 7, np.int32), np.full(4000, 7, np.int32)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind", ["dups", "wide", "skew", "extremes", "equal"])
+@pytest.mark.parametrize("op", OPS)
+def test_theta_regions_all_ops(gj, ctx, kind, op):
+    """Region-matrix mode (the default) against the oracle: counts always, pairs when
+    the output is small enough to materialise."""
+    R, S = _region_inputs(kind)
+    eps = {"dups": 3, "wide": 1500, "skew": 20, "extremes": 2**30, "equal": 0}[kind] if op == "band" else 0
+    ctx.set_option("theta_regions", 1)
+    n = check_theta(gj, ctx, R, S, op, eps, materialize=False)
+    if n <= 30_000_000:
+        check_theta(gj, ctx, R, S, op, eps, materialize=True)
+
+
+@pytest.mark.parametrize("op", OPS)
+def test_theta_plain_nlj_all_ops(gj, ctx, op):
+    """The plain NLJ over all pairs (GJ_OPT_THETA_REGIONS = 0) stays exact."""
+    ctx.set_option("theta_regions", 0)
+    R = gen.uniform_keys(4099, 300, 5, 0) - 150
+    S = gen.uniform_keys(9001, 300, 5, 1) - 150
+    check_theta(gj, ctx, R.astype(np.int32), S.astype(np.int32), op, eps=7 if op == "band" else 0)
+
+
+def test_theta_regions_match_plain_c4_shape(gj, ctx):
+    """configs[3] shape at 2^18 x 2^20: region mode and the plain NLJ give the same count."""
+    R = gen.uniform_keys(1 << 18, 1 << 30, 3, 0).astype(np.int32)
+    S = gen.uniform_keys(1 << 20, 1 << 30, 3, 1).astype(np.int32)
+    tR, tS = dev(R), dev(S)
+    ctx.set_option("theta_regions", 1)
+    a = gj.theta_join_count(ctx, tR, tS, "band", gen.C4_EPS)
+    ctx.set_option("theta_regions", 0)
+    b = gj.theta_join_count(ctx, tR, tS, "band", gen.C4_EPS)
+    assert a == b == oracle.theta_count_sorted(R, S, "band", gen.C4_EPS)

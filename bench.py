@@ -174,7 +174,8 @@ def make_workload(name, device, rank=0, world=1):
         ns = 1 << S_BITS_C4      # per GPU (2^24 = configs[3]; smaller only for ncu captures)
         R = gd.uniform(nr, 1 << 30, seed, 0, offset=rank * nr, device=device)
         S = gd.uniform(ns, 1 << 30, seed, 1, offset=rank * ns, device=device)
-        desc = f"configs[3]: band join |R.a-S.b|<=53687, 2^20 x 2^{S_BITS_C4} uniform int32 in [0,2^30), count+scan+write"
+        desc = (f"configs[3]: band join |R.a-S.b|<=53687, 2^20 x 2^{S_BITS_C4} uniform int32 in [0,2^30), "
+                "count+scan+write; region matrix (PAPER.md §4.2 Alg.3) unless --opt theta_regions=0")
         if world > 1:
             desc += f"; weak scaling: R (2^20) all-gathered, {world} x 2^24 S shards"
         return dict(kind="band", R=R, S=S, eps=gen.C4_EPS, desc=desc, rid_base_R=rank * nr, rid_base=rank * ns)
@@ -374,16 +375,31 @@ def run_ours(args, world, rank, local):
                 "alg_bytes_per_launch": d.get("alg_bytes_per_launch"), "traffic_source": tsrc,
                 "peak_source": peak_src}
     else:
-        # INT ALU roofline: 1.5 ALU-pipe instr per pair-compare (band: + 1 FMA-pipe IMAD), DESIGN.md §5
-        pairs = nR * world * nS  # the local NLJ runs the all-gathered R (world equal shards) x its S shard
+        # The NLJ compares the pairs of the cells the region matrix keeps (all n_R x n_S
+        # with theta_regions=0): INT ALU roofline, 1.5 ALU-pipe instr per pair-compare
+        # (band: + 1 FMA-pipe IMAD), DESIGN.md §5.  The write pass also stores 8 B per
+        # pair: its bound is whichever of the two floors is higher.
+        pairs, cross = ctx.theta_stats()
         d = per_kernel[dom]
         sm = sampler.summary().get("sm_mhz") or 1965
         alu_peak = 148 * 64 * sm * 1e6 / 1.5 / 1e12  # T pair-compares/s the ALU pipe allows
-        ach = pairs / (d["ms_per_launch"] * 1e-3) / 1e12
-        roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 3),
-                "unit": "Tpair/s", "frac": round(ach / alu_peak, 4), "traffic": traffic,
-                "alg_bytes_per_launch": d.get("alg_bytes_per_launch"), "traffic_source": tsrc,
-                "peak_source": "148 SM x 64 ALU lanes/clk x median SM clock / 1.5 ALU instr per pair"}
+        t = d["ms_per_launch"] * 1e-3
+        t_alu = pairs / (alu_peak * 1e12)
+        t_hbm = (8 * info["n_out"] / (hbm * 1e9)) if dom == "nlj_write" else 0.0
+        if t_hbm > t_alu:
+            ach = 8 * info["n_out"] / t / 1e9
+            roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(ach / hbm, 4), "traffic": traffic, "alg_bytes_per_launch": 8 * info["n_out"],
+                    "traffic_source": tsrc, "peak_source": peak_src}
+        else:
+            ach = pairs / t / 1e12
+            roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 3),
+                    "unit": "Tpair/s", "frac": round(ach / alu_peak, 4), "traffic": traffic,
+                    "alg_bytes_per_launch": d.get("alg_bytes_per_launch"), "traffic_source": tsrc,
+                    "peak_source": "148 SM x 64 ALU lanes/clk x median SM clock / 1.5 ALU instr per pair"}
+        roof["nlj_pairs_per_launch"] = pairs
+        roof["cross_pairs"] = cross
+        roof["pairs_all"] = nR * world * nS
 
     # ---- e2e: host buffers in, host pairs out, through the public API
     e2e = None
@@ -566,7 +582,8 @@ def main():
                    "l2": "inputs (>=64 MiB of keys, 1 GiB for configs[1]) exceed/stream past the 126 MB L2; no flush",
                    "parallelism": ("1 GPU" if world == 1 else
                                    f"{world} ranks, hash shuffle over NVLink peer stores (equi) / "
-                                   "R all-gather (theta)")} | ({"kept_R_S_rank0": list(r["kept"])} if r.get("kept") else {}),
+                                   "R all-gather (theta)")} | ({"kept_R_S_rank0": list(r["kept"])} if r.get("kept") else {})
+                  | ({"options": args.opt} if args.opt else {}),
         "roofline": r["roof"],
         "kernels": r["per_kernel"],
         "gpu_launches": r["launches"],

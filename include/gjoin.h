@@ -127,6 +127,11 @@ void gj_ctx_reset_stats(gj_ctx* ctx);
  * static strings owned by the library. */
 int gj_ctx_kernel_times(gj_ctx* ctx, const char** names, double* ms, uint64_t* launches,
                         int max_tags);
+/* Work of the last theta_join_count on this ctx (host outputs, either may be NULL):
+ * nlj_pairs = (r, s) pairs the tiled NLJ compares (n_R * n_S without the region
+ * matrix; the visited cells with it, §4.2), cross_pairs = pairs written
+ * as Green cross products without a compare (0, 0 before any theta count). */
+gj_status gj_theta_stats(gj_ctx* ctx, uint64_t* nlj_pairs, uint64_t* cross_pairs);
 
 /* ---------------------------------------------------------------- equi join
  * Hash join ("put the smaller table (inner table) into a hash table

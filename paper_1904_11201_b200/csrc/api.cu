@@ -318,6 +318,14 @@ gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t v) {
 
 uint64_t gj_ctx_launch_count(gj_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+gj_status gj_theta_stats(gj_ctx* ctx, uint64_t* nlj_pairs, uint64_t* cross_pairs) {
+  API_BEGIN
+  if (!ctx) throw Error(GJ_EINVAL, "ctx is NULL");
+  if (nlj_pairs) *nlj_pairs = ctx->tc.nlj_pairs;
+  if (cross_pairs) *cross_pairs = ctx->tc.cross_pairs;
+  API_END
+}
+
 void gj_ctx_reset_stats(gj_ctx* ctx) {
   if (!ctx) return;
   try {

@@ -163,10 +163,14 @@ struct NLJArgs {
 
 // Write pass, a screened group of 4 S keys holding a match: each lane builds its
 // 32-pair match mask, bit 31 - (8q + i) = (S key q of the group, register key i),
-// with the counters' carry trick, and the warp walks only the set bits, highest
-// first -- (S key, slot, lane) order.  Out of line so that ptxas keeps this rare
-// path from reshaping the screening loop.  sq: the group's biased S keys; row0:
-// index of S key 0 (for its rid); returns the advanced warp output base.
+// with the counters' carry trick; a warp scan of the lanes' match counts gives each
+// lane its output slot and every lane writes its own pairs, highest bit first --
+// (lane, S key, register key) order, deterministic.  (A ballot per set bit cost
+// ~10 instructions per distinct bit: fine for the sparse plain NLJ, but the
+// region matrix visits cells where several percent of the pairs match.)  Out of
+// line so that ptxas keeps this path from reshaping the screening loop.  sq: the
+// group's biased S keys; row0: index of S key 0 (for its rid); returns the advanced
+// warp output base.
 template <int OP>
 __device__ __noinline__ uint64_t emit_group(const uint32_t* rf, const uint32_t* rr, const uint32_t* sq, uint32_t C,
                                             uint64_t wbase, uint64_t row0, const NLJArgs* a) {
@@ -177,24 +181,26 @@ __device__ __noinline__ uint64_t emit_group(const uint32_t* rf, const uint32_t* 
 #pragma unroll
     for (int i = 0; i < KR; ++i) mask_step<FAM>(mm, rf[i], sq[q], C);
   if (!direct(OP)) mm = ~mm;
-  uint32_t any = __reduce_or_sync(FULL, mm);
-  while (any) {
-    const uint32_t bit = 31 - __clz(any);
-    any &= ~(1u << bit);
-    const bool p = (mm >> bit) & 1u;
-    const uint32_t bal = __ballot_sync(FULL, p);
-    if (p) {
+  const uint32_t c = __popc(mm);
+  const uint32_t incl = warp_incl_scan(c);
+  uint64_t pos = wbase + incl - c;
+  if (mm) {
+    uint32_t sr[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sr[q] = a->srid ? a->srid[row0 + q] : a->srid_base + (uint32_t)(row0 + q);
+    while (mm) {
+      const uint32_t bit = 31 - __clz(mm);
+      mm &= ~(1u << bit);
       const uint32_t e = 31 - bit, q = e >> 3, i = e & 7;
-      uint32_t rv = 0;
+      uint32_t rv = 0, sv = 0;
 #pragma unroll
       for (int k = 0; k < KR; ++k) rv = (uint32_t)k == i ? rr[k] : rv;
-      const uint64_t row = row0 + q;
-      a->out[wbase + __popc(bal & lanemask_lt())] =
-          make_uint2(rv, a->srid ? a->srid[row] : a->srid_base + (uint32_t)row);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) sv = (uint32_t)k == q ? sr[k] : sv;
+      a->out[pos++] = make_uint2(rv, sv);
     }
-    wbase += __popc(bal);
   }
-  return wbase;
+  return wbase + __shfl_sync(FULL, incl, 31);
 }
 
 template <typename K, int OP, bool FAST, bool WRITE>
@@ -573,6 +579,8 @@ void region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, int op, uint64_
   tc.nsplit = 1;
   tc.SR = SR;
   tc.mode = fast ? 1 : 0;
+  tc.nlj_pairs = 0;
+  for (const uint4& q : ud) tc.nlj_pairs += (uint64_t)q.y * q.w;
   uint64_t cross = 0;
   for (const uint4& q : tc.rects) {
     tc.rect_base.push_back(cross);
@@ -599,6 +607,7 @@ void region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, int op, uint64_
   }
   for (uint64_t& b : tc.rect_base) b += tc.nlj_total;
   tc.total = tc.nlj_total + cross;
+  tc.cross_pairs = cross;
 }
 
 template <typename K>
@@ -619,6 +628,7 @@ void theta_count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S0, int op, ui
   }
   tc.S = S;
   tc.regions = false;
+  tc.nlj_pairs = tc.cross_pairs = 0;
   bool fast = (sizeof(K) == 4) && !ctx->force_slow_band;
   const bool regions = ctx->theta_regions != 0 && R.n < (1ull << 32) && S.n < (1ull << 32);
   unsigned long long lo = 0, hi = 0;
@@ -635,7 +645,7 @@ void theta_count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S0, int op, ui
     const unsigned long long span = hi - lo;  // exact: biased keys are order-preserving
     if (eps >= span) {
       tc.all_pairs = true;
-      tc.total = R.n * S.n;
+      tc.total = tc.cross_pairs = R.n * S.n;
       return;
     }
     // t = (r + eps) - s mod 2^32 is exact iff span + eps < 2^32 and 2 eps < 2^32
@@ -644,6 +654,7 @@ void theta_count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S0, int op, ui
   }
   if (regions) return region_count<K>(ctx, R, S, op, eps, lo, hi, fast);
   tc.mode = fast ? 1 : 0;
+  tc.nlj_pairs = R.n * S.n;
   const uint64_t n_rt = (R.n + RT - 1) / RT;
   const uint64_t max_split = (S.n + TS - 1) / TS;
   uint64_t nsplit = ctx->nlj_split ? ctx->nlj_split : std::max<uint64_t>(1, (16384 + n_rt - 1) / n_rt);

@@ -76,6 +76,7 @@ struct ThetaCache {
   gj_rel PR{}, PS{};
   const uint4* udesc = nullptr;
   uint64_t nlj_total = 0;
+  uint64_t nlj_pairs = 0, cross_pairs = 0;  // work of the count (gj_theta_stats)
   std::vector<uint4> rects;
   std::vector<uint64_t> rect_base;
 };

@@ -159,18 +159,15 @@ struct NLJArgs {
   const uint64_t* woff;
   uint2* out;
   const uint4* udesc;  // region mode: unit u = R rows [x, x + y) x S rows [z, z + w); else a uniform grid
+  uint32_t dense;      // write pass: matches are dense (>= 1 per 256 compared pairs): no screening
 };
 
 // Write pass, a screened group of 4 S keys holding a match: each lane builds its
 // 32-pair match mask, bit 31 - (8q + i) = (S key q of the group, register key i),
-// with the counters' carry trick; a warp scan of the lanes' match counts gives each
-// lane its output slot and every lane writes its own pairs, highest bit first --
-// (lane, S key, register key) order, deterministic.  (A ballot per set bit cost
-// ~10 instructions per distinct bit: fine for the sparse plain NLJ, but the
-// region matrix visits cells where several percent of the pairs match.)  Out of
-// line so that ptxas keeps this path from reshaping the screening loop.  sq: the
-// group's biased S keys; row0: index of S key 0 (for its rid); returns the advanced
-// warp output base.
+// with the counters' carry trick, and the warp walks only the set bits, highest
+// first -- (S key, slot, lane) order.  Out of line so that ptxas keeps this rare
+// path from reshaping the screening loop.  sq: the group's biased S keys; row0:
+// index of S key 0 (for its rid); returns the advanced warp output base.
 template <int OP>
 __device__ __noinline__ uint64_t emit_group(const uint32_t* rf, const uint32_t* rr, const uint32_t* sq, uint32_t C,
                                             uint64_t wbase, uint64_t row0, const NLJArgs* a) {
@@ -181,26 +178,24 @@ __device__ __noinline__ uint64_t emit_group(const uint32_t* rf, const uint32_t* 
 #pragma unroll
     for (int i = 0; i < KR; ++i) mask_step<FAM>(mm, rf[i], sq[q], C);
   if (!direct(OP)) mm = ~mm;
-  const uint32_t c = __popc(mm);
-  const uint32_t incl = warp_incl_scan(c);
-  uint64_t pos = wbase + incl - c;
-  if (mm) {
-    uint32_t sr[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) sr[q] = a->srid ? a->srid[row0 + q] : a->srid_base + (uint32_t)(row0 + q);
-    while (mm) {
-      const uint32_t bit = 31 - __clz(mm);
-      mm &= ~(1u << bit);
+  uint32_t any = __reduce_or_sync(FULL, mm);
+  while (any) {
+    const uint32_t bit = 31 - __clz(any);
+    any &= ~(1u << bit);
+    const bool p = (mm >> bit) & 1u;
+    const uint32_t bal = __ballot_sync(FULL, p);
+    if (p) {
       const uint32_t e = 31 - bit, q = e >> 3, i = e & 7;
-      uint32_t rv = 0, sv = 0;
+      uint32_t rv = 0;
 #pragma unroll
       for (int k = 0; k < KR; ++k) rv = (uint32_t)k == i ? rr[k] : rv;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) sv = (uint32_t)k == q ? sr[k] : sv;
-      a->out[pos++] = make_uint2(rv, sv);
+      const uint64_t row = row0 + q;
+      a->out[wbase + __popc(bal & lanemask_lt())] =
+          make_uint2(rv, a->srid ? a->srid[row] : a->srid_base + (uint32_t)row);
     }
+    wbase += __popc(bal);
   }
-  return wbase + __shfl_sync(FULL, incl, 31);
+  return wbase;
 }
 
 template <typename K, int OP, bool FAST, bool WRITE>
@@ -326,12 +321,38 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
               }
             }
           };
-          // Screen 4 S keys (one LDS.128) with the count pass's carry-chain counters and
-          // one warp vote; only groups holding a match build masks.
           const uint4* s4 = reinterpret_cast<const uint4*>(st);
           const uint32_t n4 = tn16 >> 2;
+          // Dense matches (the cells the region matrix keeps, or <, >, != over all
+          // pairs): every group of 4 S keys builds its 32-pair mask inline (no vote,
+          // no out-of-line call), a warp scan of the lanes' counts places each lane's
+          // pairs, which it writes in (lane, S key, register key) order.
+          for (uint32_t q = 0; q < n4 && a.dense; ++q) {
+            const uint4 v = s4[q];
+            const uint32_t sv[4] = {v.x ^ 0x80000000u, v.y ^ 0x80000000u, v.z ^ 0x80000000u, v.w ^ 0x80000000u};
+            uint32_t mm = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+              for (int i = 0; i < KR; ++i) mask_step<FAM>(mm, rf[i], sv[k], a.C);
+            if (!direct(OP)) mm = ~mm;
+            const uint32_t c = __popc(mm), incl = warp_incl_scan(c);
+            uint64_t pos = wbase + incl - c;
+            while (mm) {
+              const uint32_t bit = 31 - __clz(mm);
+              mm &= ~(1u << bit);
+              const uint32_t e = 31 - bit, qq = e >> 3, i = e & 7;
+              uint32_t rv = 0;
+#pragma unroll
+              for (int k = 0; k < KR; ++k) rv = (uint32_t)k == i ? rr[k] : rv;
+              a.out[pos++] = make_uint2(rv, srow(tb + 4 * q + qq));
+            }
+            wbase += __shfl_sync(FULL, incl, 31);
+          }
+          // Sparse matches: screen 4 S keys (one LDS.128) with the count pass's
+          // carry-chain counters and one warp vote; only groups holding a match build masks.
 #pragma unroll 2
-          for (uint32_t q = 0; q < n4; ++q) {
+          for (uint32_t q = 0; q < n4 && !a.dense; ++q) {
             const uint4 v = s4[q];
             const uint32_t s0 = v.x ^ 0x80000000u, s1 = v.y ^ 0x80000000u;
             const uint32_t s2 = v.z ^ 0x80000000u, s3 = v.w ^ 0x80000000u;
@@ -694,6 +715,7 @@ void theta_write_impl(gj_ctx* ctx, uint32_t* out) {
       a.woff = tc.woff;
       a.out = reinterpret_cast<uint2*>(out);
       a.udesc = tc.udesc;
+      a.dense = tc.nlj_total * 256 >= tc.nlj_pairs;
       dispatch<K>(ctx, a, tc.op, tc.mode == 1, true);
     }
     if (!tc.rects.empty()) {
@@ -713,6 +735,7 @@ void theta_write_impl(gj_ctx* ctx, uint32_t* out) {
   a.work = work;
   a.woff = tc.woff;
   a.out = reinterpret_cast<uint2*>(out);
+  a.dense = tc.total * 256 >= tc.nlj_pairs;
   dispatch<K>(ctx, a, tc.op, tc.mode == 1, true);
 }
 

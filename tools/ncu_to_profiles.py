@@ -27,11 +27,14 @@ PROF = os.path.join(ROOT, "profiles")
 
 # kernel symbol -> bench.py tag (the LaunchScope tags of the library)
 TAGS = [
-    (r"part_scatter<[^>]*, true>", "shuffle_scatter"),
+    (r"part_scatter<\w+, \w+, (true|1),", "shuffle_scatter"),
     (r"part_scatter", "part_scatter"),
     (r"part_hist", "part_hist"),
-    (r"hj_count_kernel", "hj_count"),
-    (r"hj_write_kernel", "hj_write"),
+    (r"tile_base", "tile_base"),
+    (r"hj_count", "hj_count"),
+    (r"hj_write_fast", "hj_write"),
+    (r"hj_write_kernel", "hj_write_multi"),
+    (r"cross_rect", "cross_rect"),
     (r"nlj_kernel<[^>]*, (true|1)>", "nlj_write"),
     (r"nlj_kernel<[^>]*, (false|0)>", "nlj_count"),
     (r"pf_count", "pf_count"),

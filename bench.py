@@ -213,6 +213,9 @@ def join_bytes(nR, nS, nout, passes, wk, rid_implicit):
     scatter_total = n * first + (passes - 1) * n * 2 * (wk + 4)
     nb, npb = min(nR, nS), max(nR, nS)
     return {
+        # multi-GPU shuffle pass: key (+ rid unless implicit) in, key + rid out (to the
+        # owner's buffer, local HBM or a peer's over NVLink)
+        "shuffle_scatter": (n * (wk + (wk + 4) if rid_implicit else 2 * (wk + 4)), 2),
         "part_hist": (wk * n * passes, 2 * passes),
         "part_scatter": (scatter_total, 2 * passes),
         # count: build + probe keys in, one uint16 match index per probe row out
@@ -227,7 +230,11 @@ def algorithmic_bytes(w, info):
     nR, nS = w["R"].numel(), w["S"].numel()
     nout = info["n_out"]
     if w["kind"] == "equi":
-        return join_bytes(nR, nS, nout, info["passes"], w["R"].element_size(), info["world"] == 1)
+        ab = join_bytes(nR, nS, nout, info["passes"], w["R"].element_size(), info["world"] == 1)
+        if info["world"] > 1:  # the shuffle reads the implicit-rid input; the local passes carry rids
+            ab["shuffle_scatter"] = ((nR + nS) * (w["R"].element_size() + (w["R"].element_size() + 4)), 2)
+            ab["part_scatter"] = ((nR + nS) * 2 * (w["R"].element_size() + 4) * info["passes"], 2 * info["passes"])
+        return ab
     if w["kind"] == "pf_equi":
         # a probed row costs its 8 B key + one 32 B Bloom sector (+ 1
         # flag bit); the write pass reads the flags and each survivor's key (8 B) and

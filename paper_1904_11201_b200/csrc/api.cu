@@ -191,7 +191,7 @@ uint32_t auto_bits(gj_ctx* ctx, uint64_t nb) {
 // ones (segment offsets segR / segS, 2^b0 + 1 entries each, device), as the fused
 // multi-GPU shuffle delivers them; only the remaining bits are partitioned here.
 void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t skip, uint32_t b0,
-                     const uint32_t* segR, const uint32_t* segS) {
+                     const uint32_t* segR, const uint32_t* segS, cudaEvent_t s_ready) {
   JoinCache& jc = ctx->jc;
   jc = JoinCache{};
   jc.R = R;
@@ -206,13 +206,16 @@ void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t ski
   const bool swap = ctx->build_side == 2 || (ctx->build_side == 0 && S.n * 10 < R.n * 9);
   const uint32_t B = std::max(b0, std::min<uint32_t>(auto_bits(ctx, swap ? S.n : R.n), 32 - skip));
   Partitioned PR = radix_partition(ctx, R, B - b0, "R", skip + b0, b0 ? segR : nullptr, 1u << b0);
+  // S may still be arriving (multi-GPU: its shuffle runs on a second stream while R
+  // is partitioned here)
+  if (s_ready) GJ_CUDA(cudaStreamWaitEvent(ctx->stream, s_ready, 0));
   Partitioned PS = radix_partition(ctx, S, B - b0, "S", skip + b0, b0 ? segS : nullptr, 1u << b0);
   hash_join_count(ctx, R, S, B, swap, PR, PS);
   jc.valid = true;
 }
 
 static void do_join_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S) {
-  join_count_core(ctx, R, S, 0, 0, nullptr, nullptr);
+  join_count_core(ctx, R, S, 0, 0, nullptr, nullptr, nullptr);
 }
 
 }  // namespace gj
@@ -246,6 +249,8 @@ gj_status gj_ctx_create(gj_ctx** out, int device, void* stream) {
   int sms = 0;
   GJ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   c->num_sms = sms;
+  c->overlap_shuffle = std::getenv("GJ_NO_OVERLAP") == nullptr;  // A/B experiments
+  if (const char* e = std::getenv("GJ_SHUFFLE_CTAS")) c->shuffle_ctas = (uint32_t)std::atoi(e);
   *out = c;
   API_END
 }
@@ -268,6 +273,12 @@ void gj_ctx_destroy(gj_ctx* ctx) {
   for (auto& kv : ctx->pinned_bufs)
     if (kv.second.ptr) cudaFreeHost(kv.second.ptr);
   if (ctx->owns_stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->aux) {
+    cudaStreamSynchronize(ctx->aux);
+    cudaStreamDestroy(ctx->aux);
+  }
+  for (auto e : ctx->aux_ev)
+    if (e) cudaEventDestroy(e);
   delete ctx;
 }
 

@@ -34,7 +34,7 @@
 
 namespace gj {
 void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t skip, uint32_t b0,
-                     const uint32_t* segR, const uint32_t* segS);
+                     const uint32_t* segR, const uint32_t* segS, cudaEvent_t s_ready);
 uint32_t auto_bits(gj_ctx* ctx, uint64_t nb);
 void set_last_error(const std::string& m);
 }  // namespace gj
@@ -204,7 +204,7 @@ void dist_equi_count(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) 
   }
   // 4. local partitioned hash join of what arrived (top g hash bits are now constant)
   gj_rel RL{rk[0], rr[0], nrecv[0], R.key_type, 0}, SL{rk[1], rr[1], nrecv[1], S.key_type, 0};
-  join_count_core(ctx, RL, SL, g, 0, nullptr, nullptr);
+  join_count_core(ctx, RL, SL, g, 0, nullptr, nullptr, nullptr);
 }
 
 // Fused shuffle: ONE radix pass by (destination rank, first local digit) -- the top
@@ -221,7 +221,14 @@ struct FusedOut {
 };
 
 // Shuffles X[rel] (rel 0 = R, 1 = S; nullptr = leave that relation alone).
-void fused_shuffle(gj_ctx* ctx, gj_comm* c, const gj_rel* const X[2], uint32_t b1, FusedOut& out) {
+// s_ready != nullptr (both relations): R's stores are fenced by a barrier on the
+// ctx stream, S's scatter and barrier run on the ctx's second stream, and
+// *s_ready is recorded there -- the caller partitions R while S crosses NVLink and
+// waits on *s_ready before touching S.  The two barriers are NCCL calls on one
+// communicator, issued in the same order on every rank and never concurrent (S's
+// waits on an event recorded after R's).
+void fused_shuffle(gj_ctx* ctx, gj_comm* c, const gj_rel* const X[2], uint32_t b1, FusedOut& out,
+                   cudaEvent_t* s_ready = nullptr) {
   const int G = c->nranks, me = c->rank;
   const uint32_t g = log2_exact(G);
   const int kt = X[0] ? X[0]->key_type : X[1]->key_type;
@@ -297,8 +304,25 @@ void fused_shuffle(gj_ctx* ctx, gj_comm* c, const gj_rel* const X[2], uint32_t b
     }
     c->mapped = true;
   }
+  const bool overlap = s_ready && X[0] && X[1];
+  cudaStream_t main_stream = ctx->stream;
+  auto barrier = [&](const char* tag) {  // every rank's NVLink stores done before any local read
+    RegionScope rs(ctx, tag);
+    uint32_t* z = all + row * G;
+    GJ_NCCL(ncclAllReduce(z, z + 1, 1, ncclUint32, ncclSum, c->comm, ctx->stream));
+  };
   for (int rel = 0; rel < 2; ++rel) {
     if (!X[rel]) continue;
+    if (overlap && rel == 1) {
+      barrier("shuffle_barrier");
+      if (!ctx->aux) {
+        GJ_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+        for (auto& e : ctx->aux_ev) GJ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+      GJ_CUDA(cudaEventRecord(ctx->aux_ev[0], main_stream));
+      GJ_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev[0], 0));
+      ctx->stream = ctx->aux;
+    }
     // adj[dg] = (index of my run dg in its receiver's buffer) - (its start in my
     // digit order); seg[d] = start of local digit d in MY receive buffer
     const size_t tab_n = (size_t)D1 + L1 + 1;
@@ -333,11 +357,11 @@ void fused_shuffle(gj_ctx* ctx, gj_comm* c, const gj_rel* const X[2], uint32_t b
     out.seg[rel] = dtab + D1;
   }
   trace_sync(ctx, "fused: scatter");
-  // every rank's NVLink stores are done before any local join reads its buffers
-  {
-    RegionScope rs(ctx, "shuffle_barrier");
-    uint32_t* z = all + row * G;
-    GJ_NCCL(ncclAllReduce(z, z + 1, 1, ncclUint32, ncclSum, c->comm, ctx->stream));
+  barrier("shuffle_barrier");
+  if (overlap) {
+    GJ_CUDA(cudaEventRecord(ctx->aux_ev[1], ctx->stream));
+    ctx->stream = main_stream;
+    *s_ready = ctx->aux_ev[1];
   }
   trace_sync(ctx, "fused: barrier");
 }
@@ -352,8 +376,9 @@ void dist_equi_count_fused(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_re
   if (ctx->part_bits >= 0) b1 = std::min<uint32_t>(b1, (uint32_t)ctx->part_bits);
   const gj_rel* X[2] = {&R, &S};
   FusedOut o;
-  fused_shuffle(ctx, c, X, b1, o);
-  join_count_core(ctx, o.X[0], o.X[1], g, b1, o.seg[0], o.seg[1]);
+  cudaEvent_t s_ready = nullptr;
+  fused_shuffle(ctx, c, X, b1, o, ctx->overlap_shuffle ? &s_ready : nullptr);
+  join_count_core(ctx, o.X[0], o.X[1], g, b1, o.seg[0], o.seg[1], s_ready);
   trace_sync(ctx, "fused: local join count");
 }
 
@@ -458,7 +483,7 @@ void dist_equi_count_filtered(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj
   }
   kept[0] = RL.n;
   kept[1] = SL.n;
-  join_count_core(ctx, RL, SL, g, 0, nullptr, nullptr);
+  join_count_core(ctx, RL, SL, g, 0, nullptr, nullptr, nullptr);
 }
 
 void equi_count_any(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) {

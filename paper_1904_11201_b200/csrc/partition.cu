@@ -794,7 +794,10 @@ void launch_scatter_v(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t r
   int occ = 1;
   GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PT, smem));
   if (const char* e = std::getenv("GJ_SCATTER_OCC")) occ = std::min(occ, std::atoi(e));  // tuning experiments
-  const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
+  uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
+  // the NVLink-bound shuffle may run beside the local passes of the other relation
+  // (second stream): capped so those keep SMs (ctx->shuffle_ctas, 0 = no cap)
+  if (REMOTE && ctx->shuffle_ctas) grid = std::min<uint32_t>(grid, ctx->shuffle_ctas);
   launch(ctx, REMOTE ? "shuffle_scatter" : "part_scatter", kern, dim3(grid), dim3(PT), smem, kin, rin, rid_base, n,
          tdesc, (uint32_t)ntiles, shift, bits, hist, tile_pref, kout, rout, dst);
 }

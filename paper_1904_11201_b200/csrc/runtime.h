@@ -99,6 +99,8 @@ struct gj_ctx {
   bool profile = false;
   uint32_t nlj_split = 0;
   bool force_slow_band = false;
+  bool overlap_shuffle = true;
+  uint32_t shuffle_ctas = 0;    // CTA cap of the shuffle scatter (0 = all)  // multi-GPU equi: S shuffle on a 2nd stream beside R's local passes
   int theta_regions = 1;  // theta joins through the region matrix (0 = plain NLJ over all pairs)
   int build_side = 0;
   int shuffle_bits = 0;
@@ -117,6 +119,10 @@ struct gj_ctx {
   // consecutive batches' transfers overlap
   gj_ctx* sub[2] = {nullptr, nullptr};
   bool owns_stream = false;
+  // multi-GPU equi join: second stream for the S shuffle, overlapped with R's local
+  // radix passes (created on first use)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t aux_ev[2] = {nullptr, nullptr};
 };
 
 namespace gj {

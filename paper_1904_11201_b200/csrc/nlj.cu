@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
     K rk[KR];
     uint32_t rf[KR], rr[KR];
     uint32_t nvalid = 0;
+    __shared__ uint32_t rrs[WRITE ? KR * NT : 1];  // rids of the register keys (dense write path)
 #pragma unroll
     for (int i = 0; i < KR; ++i) {
       const uint64_t row = r0 + (uint64_t)i * NT + tid;
@@ -250,6 +251,7 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
         uint32_t b = (uint32_t)rk[i] ^ 0x80000000u;
         rf[i] = (OP == GJ_BAND) ? b + (uint32_t)a.eps : b;
       }
+      if (WRITE) rrs[i * NT + tid] = rr[i];  // read back only by this thread
     }
 
     auto issue = [&](uint32_t t, uint32_t seq) {
@@ -337,15 +339,22 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
               for (int i = 0; i < KR; ++i) mask_step<FAM>(mm, rf[i], sv[k], a.C);
             if (!direct(OP)) mm = ~mm;
             const uint32_t c = __popc(mm), incl = warp_incl_scan(c);
-            uint64_t pos = wbase + incl - c;
-            while (mm) {
-              const uint32_t bit = 31 - __clz(mm);
-              mm &= ~(1u << bit);
-              const uint32_t e = 31 - bit, qq = e >> 3, i = e & 7;
-              uint32_t rv = 0;
+            if (mm) {
+              uint2* o = a.out + wbase + (incl - c);
+              uint32_t sr[4];  // the group's S rids, loaded once (broadcast across lanes)
 #pragma unroll
-              for (int k = 0; k < KR; ++k) rv = (uint32_t)k == i ? rr[k] : rv;
-              a.out[pos++] = make_uint2(rv, srow(tb + 4 * q + qq));
+              for (int k = 0; k < 4; ++k) sr[k] = srow(tb + 4 * q + k);
+              // S key qq = e >> 3 owns byte 3 - qq of the mask: walk it byte by byte so
+              // the S rid is a compile-time pick and only the register key is dynamic
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq) {
+                uint32_t mb = (mm >> (24 - 8 * qq)) & 0xFFu;  // bit 7 - i = register key i
+                while (mb) {
+                  const uint32_t i = __clz(mb) - 24;
+                  mb &= ~(0x80u >> i);
+                  *o++ = make_uint2(rrs[i * NT + tid], sr[qq]);
+                }
+              }
             }
             wbase += __shfl_sync(FULL, incl, 31);
           }

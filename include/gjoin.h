@@ -172,11 +172,16 @@ gj_status theta_join_materialize(gj_ctx* ctx, gj_rel R, gj_rel S, int op, uint64
  * one 32-byte sector) and drops S tuples whose key is absent; GJ_PF_TWO_SIDED then
  * builds a filter of S's survivors and filters R the same way.  With op = GJ_BAND
  * and eps > 0 only the range stage applies (a Bloom filter cannot answer range
- * membership).  Guarantee: J(prefilter(R), prefilter(S)) = J(R, S) (no false
+ * membership).  GJ_PF_EXACT (op = GJ_EQ, or GJ_BAND with eps = 0; replaces the
+ * Bloom stage) is the paper's exact version: an open-addressing hash set of R's
+ * in-range keys (Alg.1 Setup() "Build a hash table") keeps exactly
+ * the S tuples whose key occurs in R, and with GJ_PF_TWO_SIDED the set of those
+ * survivors' keys keeps exactly the R tuples whose key occurs in S -- the
+ * semi-joins S ⋉ R and R ⋉ S.  Guarantee: J(prefilter(R), prefilter(S)) = J(R, S) (no false
  * negatives).  Survivors keep their original relative order and rid.
  *   key_out_X / rid_out_X: DEVICE buffers of X.n keys / uint32 rids (caller-owned).
  *   n_X_out: host; number of survivors.  Synchronises the stream. */
-enum { GJ_PF_RANGE = 1, GJ_PF_BLOOM = 2, GJ_PF_TWO_SIDED = 4 };
+enum { GJ_PF_RANGE = 1, GJ_PF_BLOOM = 2, GJ_PF_TWO_SIDED = 4, GJ_PF_EXACT = 8 };
 gj_status prefilter(gj_ctx* ctx, gj_rel R, gj_rel S, uint32_t flags, int op, uint64_t eps,
                     double bloom_bits_per_key, void* key_out_R, uint32_t* rid_out_R,
                     uint64_t* n_R_out, void* key_out_S, uint32_t* rid_out_S, uint64_t* n_S_out);

@@ -12,6 +12,8 @@
 // stably (count -> scan -> write) keeping their original rids.
 #include <algorithm>
 #include <cmath>
+#include <string>
+#include <type_traits>
 
 #include "common.cuh"
 #include "nlj.cuh"
@@ -38,7 +40,59 @@ struct Filt {
   uint32_t nfilt, g;
   uint64_t woff[MAX_RANKS];
   uint32_t logb[MAX_RANKS];
+  // exact key set (GJ_PF_EXACT, the paper's hash set of common keys): open
+  // addressing over biased keys, ~EMPTY marks a free slot and the one key whose
+  // biased value IS ~0 is recorded in has_top
+  const void* set;
+  uint32_t set_log;
+  const uint32_t* has_top;
 };
+
+// Exact hash set of biased keys ("hash table" of the common keys,
+// Alg.1 Setup()).  Multiplicative hash, linear probing, load factor <= 1/2.
+template <typename K>
+__device__ __forceinline__ uint64_t set_hash(typename KeyT<K>::U b, uint32_t lg) {
+  return lg ? (((uint64_t)b * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)b >> 29)) * 0xBF58476D1CE4E5B9ull >> (64 - lg)
+            : 0ull;
+}
+template <typename K>
+__device__ __forceinline__ bool set_contains(K k, const Filt& f) {
+  using U = typename KeyT<K>::U;
+  const U b = KeyT<K>::bias(k);
+  if (b == (U)~(U)0) return *f.has_top != 0u;
+  const U* t = static_cast<const U*>(f.set);
+  const uint64_t mask = (1ull << f.set_log) - 1;
+  for (uint64_t s = set_hash<K>(b, f.set_log);; s = (s + 1) & mask) {
+    const U v = t[s];
+    if (v == b) return true;
+    if (v == (U)~(U)0) return false;
+  }
+}
+template <typename K>
+__global__ void set_build(const K* __restrict__ key, uint64_t n, Filt range, void* set, uint32_t lg,
+                          uint32_t* has_top) {
+  using U = typename KeyT<K>::U;
+  U* t = static_cast<U*>(set);
+  const uint64_t mask = (1ull << lg) - 1;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const K k = key[i];
+    if (range.use_range) {
+      const unsigned long long bb = (unsigned long long)KeyT<K>::bias(k);
+      if (bb < range.lo || bb > range.hi) continue;
+    }
+    const U b = KeyT<K>::bias(k);
+    if (b == (U)~(U)0) {
+      *has_top = 1u;
+      continue;
+    }
+    for (uint64_t s = set_hash<K>(b, lg);; s = (s + 1) & mask) {
+      const U old = atomicCAS(reinterpret_cast<typename std::conditional<sizeof(U) == 4, unsigned int,
+                                                                          unsigned long long>::type*>(t + s),
+                              (U)~(U)0, b);
+      if (old == (U)~(U)0 || old == b) break;  // inserted, or already present
+    }
+  }
+}
 
 __device__ __forceinline__ uint64_t bloom_hash(int32_t k) {
   uint64_t h = (uint64_t)(uint32_t)k * 0xC2B2AE3D27D4EB4Full;
@@ -96,6 +150,7 @@ __device__ __forceinline__ bool keep(K k, const Filt& f) {
            ((c.z & s.mask[6]) != 0) & ((c.w & s.mask[7]) != 0);
     }
   }
+  if (f.set && ok) ok = set_contains(k, f);
   return ok;
 }
 
@@ -233,6 +288,27 @@ const uint32_t* build_bloom(gj_ctx* ctx, const gj_rel& X, const Filt& range, dou
   return bloom;
 }
 
+// Exact key set of X's in-range keys (2^lg slots >= 2 * X.n, load <= 1/2).
+template <typename K>
+void build_set(gj_ctx* ctx, const gj_rel& X, const Filt& range, Filt& f, const char* tag) {
+  uint32_t lg = 1;
+  while ((1ull << lg) < 2 * X.n && lg < 40) ++lg;
+  const size_t bytes = (1ull << lg) * sizeof(K);
+  std::string t(tag);
+  void* set = ws(ctx, t.c_str(), bytes);
+  uint32_t* top = static_cast<uint32_t*>(ws(ctx, (t + ".top").c_str(), 16));
+  GJ_CUDA(cudaMemsetAsync(set, 0xFF, bytes, ctx->stream));
+  GJ_CUDA(cudaMemsetAsync(top, 0, 4, ctx->stream));
+  if (X.n) {
+    const unsigned grid = (unsigned)std::min<uint64_t>((X.n + 255) / 256, (uint64_t)ctx->num_sms * 16);
+    launch(ctx, "set_build", set_build<K>, dim3(grid), dim3(256), 0, static_cast<const K*>(X.key), X.n, range, set,
+           lg, top);
+  }
+  f.set = set;
+  f.set_log = lg;
+  f.has_top = top;
+}
+
 template <typename K>
 void prefilter_t(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t flags, int op, uint64_t eps,
                  double bpk, void* kR, uint32_t* rR, uint64_t* nRo, void* kS, uint32_t* rS, uint64_t* nSo) {
@@ -257,7 +333,27 @@ void prefilter_t(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t flags, 
     }
     range.use_range = 1;
   }
-  const bool bloom_ok = (flags & GJ_PF_BLOOM) && (op == GJ_EQ || (op == GJ_BAND && eps == 0));
+  const bool point = op == GJ_EQ || (op == GJ_BAND && eps == 0);  // key membership decides a match
+  if ((flags & GJ_PF_EXACT) && point) {
+    // the paper's exact semi-joins: S keeps the tuples whose key is in R's key set,
+    // then (two-sided) R keeps those whose key is in the set of S's survivors
+    Filt fs = range;
+    build_set<K>(ctx, R, range, fs, "pf.setR");
+    *nSo = compact<K>(ctx, S, fs, kS, rS, "S");
+    if (flags & GJ_PF_TWO_SIDED) {
+      gj_rel S2 = S;
+      S2.key = kS;
+      S2.rid = rS;
+      S2.n = *nSo;
+      Filt fr = range;
+      build_set<K>(ctx, S2, range, fr, "pf.setS");
+      *nRo = compact<K>(ctx, R, fr, kR, rR, "R");
+    } else {
+      *nRo = compact<K>(ctx, R, range, kR, rR, "R");
+    }
+    return;
+  }
+  const bool bloom_ok = (flags & GJ_PF_BLOOM) && point;
   if (!bloom_ok) {
     *nSo = compact<K>(ctx, S, range, kS, rS, "S");
     *nRo = compact<K>(ctx, R, range, kR, rR, "R");

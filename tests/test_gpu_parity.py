@@ -356,6 +356,31 @@ def test_prefilter_no_false_negatives(gj, ctx, flags):
         assert len(rS) <= len(keepS) + 0.08 * (len(S) - len(keepS))
 
 
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+@pytest.mark.parametrize("flags", [8, 12, 13])
+def test_prefilter_exact_is_the_semijoin(gj, ctx, flags, dtype):
+    """GJ_PF_EXACT (Alg.1 Setup's hash set of common keys): the survivors
+    are EXACTLY the semi-joins S ⋉ R and (two-sided) R ⋉ S, in original order --
+    incl. the extreme keys (the biased all-ones key lives outside the table)."""
+    rng = np.random.default_rng(flags + (0 if dtype == np.int32 else 100))
+    info = np.iinfo(dtype)
+    R = rng.integers(-50_000, 50_000, 70_000).astype(dtype)
+    S = rng.integers(0, 150_000, 90_000).astype(dtype)
+    R[:4] = [info.max, info.min, -1, 0]
+    S[:5] = [info.max, info.min, 7, info.max, 123_456_789 % 150_000]
+    kR, rR, kS, rS = gj.prefilter(ctx, dev(R), dev(S), flags=flags)
+    kR, rR, kS, rS = (t.cpu().numpy() for t in (kR, rR, kS, rS))
+    assert np.array_equal(kR, R[rR]) and np.array_equal(kS, S[rS])
+    assert np.array_equal(rS, np.nonzero(oracle.semijoin_exact(S, R))[0])
+    if flags & 4:
+        assert np.array_equal(rR, np.nonzero(oracle.semijoin_exact(R, S))[0])
+    elif flags & 1:
+        lo, hi = max(R.min(), S.min()), min(R.max(), S.max())
+        assert np.array_equal(rR, np.nonzero((R >= lo) & (R <= hi))[0])
+    else:
+        assert np.array_equal(rR, np.arange(len(R)))
+
+
 def test_prefilter_band_range(gj, ctx):
     R = gen.uniform_keys(20_000, 1 << 20, 6, 0)
     S = (gen.uniform_keys(20_000, 1 << 20, 6, 1) + (1 << 19)).astype(np.int32)

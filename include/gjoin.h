@@ -132,6 +132,13 @@ int gj_ctx_kernel_times(gj_ctx* ctx, const char** names, double* ms, uint64_t* l
  * matrix; the visited cells with it, §4.2), cross_pairs = pairs written
  * as Green cross products without a compare (0, 0 before any theta count). */
 gj_status gj_theta_stats(gj_ctx* ctx, uint64_t* nlj_pairs, uint64_t* cross_pairs);
+/* Of the last join_count (or join_dist_count: this rank's local join) on this ctx,
+ * host outputs, any may be NULL: rsize_eq8 = the paper's result-size estimate Eq.8
+ * (PAPER.md:206-211), sum over the partitions ("Reducers") of |R_p| * |S_p| -- an
+ * upper bound on |J| computed before the join; partition_bits = the radix bits B
+ * (2^B partitions, the analogue of the paper's reducer count k); units = hash-join
+ * work units.  Synchronises the stream.  GJ_ESTATE if no equi count ran. */
+gj_status gj_join_stats(gj_ctx* ctx, uint64_t* rsize_eq8, uint32_t* partition_bits, uint32_t* units);
 
 /* ---------------------------------------------------------------- equi join
  * Hash join ("put the smaller table (inner table) into a hash table

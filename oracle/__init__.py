@@ -16,6 +16,7 @@ Functions (each cites the passage it follows; see oracle.cpp for the C++ bodies)
 * ``semijoin_band``      O6b band semi-join mask                  definition (1), band
 * ``pkfk_closed_form``   O8  J = {(m_j, j)} for the PK-FK generators (R keys a bijection
                              of R rows, S.key[j] = R.key[m_j]); pinned to O2 in tests.
+* ``eq8_rsize``          O9  the paper's result-size estimate Eq.8
 
 Parity status: every function above is pinned (tests/test_oracle.py); none is
 "parity unpinned".
@@ -159,3 +160,31 @@ def pkfk_closed_form(m, rid_base_S=0, r_rows=None):
     order = np.argsort(m, kind="stable")
     pairs = np.stack([m[order], j[order]], axis=1).astype(np.uint32)
     return len(pairs), pairs
+
+
+def partition_of(K, bits):
+    """The partition ("Reducer") of every key when 2^bits partitions group equal keys
+    (tuples with the same key reach the same Reducer): the top
+    ``bits`` bits of hi32(key * 0x9E3779B97F4A7C15) over the key's 64-bit two's
+    complement pattern, int64 keys first folded as x ^ (x >> 32) (DESIGN.md §4.1's
+    partition map, restated here from its definition)."""
+    K = np.asarray(K)
+    if bits == 0:
+        return np.zeros(len(K), dtype=np.uint64)
+    x = K.astype(np.int64).view(np.uint64) if K.dtype == np.int64 else K.astype(np.uint32).astype(np.uint64)
+    if K.dtype == np.int64:
+        x = x ^ (x >> np.uint64(32))
+    with np.errstate(over="ignore"):
+        h = (x * np.uint64(0x9E3779B97F4A7C15)) >> np.uint64(32)
+    return (h & np.uint64(0xFFFFFFFF)) >> np.uint64(32 - bits)
+
+
+def eq8_rsize(R, S, bits):
+    """O9: Eq.8, R_size = gamma*beta*|S|*|T| * sum_i omega_i*lambda_i
+    = sum over the k = 2^bits Reducers i of |S_i| * |T_i| (omega_i = |S_i| / (beta |S|),
+    lambda_i = |T_i| / (gamma |T|), Eq.7): per-partition tuple counts of both sides,
+    multiplied and summed (exact Python integers)."""
+    k = 1 << bits
+    cR = np.bincount(partition_of(R, bits).astype(np.int64), minlength=k)
+    cS = np.bincount(partition_of(S, bits).astype(np.int64), minlength=k)
+    return int(sum(int(a) * int(b) for a, b in zip(cR, cS) if a and b))

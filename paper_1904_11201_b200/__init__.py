@@ -67,6 +67,8 @@ def _load():
     L.gj_last_error.restype = ctypes.c_char_p
     L.gj_theta_stats.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(u64)]
     L.gj_theta_stats.restype = i32
+    L.gj_join_stats.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(u32), ctypes.POINTER(u32)]
+    L.gj_join_stats.restype = i32
     L.gj_ctx_launch_count.argtypes = [vp]
     L.gj_ctx_launch_count.restype = u64
     L.gj_ctx_reset_stats.argtypes = [vp]
@@ -104,7 +106,7 @@ lib = _load()
 
 # C-ABI symbols declared in include/gjoin.h (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("gj_ctx_create", "gj_ctx_destroy", "gj_ctx_set_stream", "gj_last_error", "gj_ctx_set_option",
-               "gj_ctx_launch_count", "gj_ctx_reset_stats", "gj_ctx_kernel_times", "gj_theta_stats", "join_count",
+               "gj_ctx_launch_count", "gj_ctx_reset_stats", "gj_ctx_kernel_times", "gj_theta_stats", "gj_join_stats", "join_count",
                "join_materialize", "theta_join_count", "theta_join_materialize", "prefilter", "join_host",
                "join_host_batch",
                "gj_comm_unique_id", "gj_comm_init", "gj_comm_destroy", "join_dist_count", "join_dist_count_filtered",
@@ -169,6 +171,12 @@ class Context:
 
     def reset_stats(self):
         lib.gj_ctx_reset_stats(self.h)
+
+    def join_stats(self) -> tuple:
+        """(Eq.8 result-size bound, partition bits B, hash-join units) of the last equi count."""
+        e, b, u = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_uint32()
+        _check(lib.gj_join_stats(self.h, ctypes.byref(e), ctypes.byref(b), ctypes.byref(u)))
+        return int(e.value), int(b.value), int(u.value)
 
     def theta_stats(self) -> tuple:
         """(pairs the NLJ compared, pairs written as Green cross products) of the last theta count."""

@@ -329,6 +329,19 @@ gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t v) {
 
 uint64_t gj_ctx_launch_count(gj_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+gj_status gj_join_stats(gj_ctx* ctx, uint64_t* rsize_eq8, uint32_t* partition_bits, uint32_t* units) {
+  API_BEGIN
+  if (!ctx) throw Error(GJ_EINVAL, "ctx is NULL");
+  const JoinCache& jc = ctx->jc;
+  if (!jc.valid) throw Error(GJ_ESTATE, "gj_join_stats: no join_count on this ctx");
+  unsigned long long e = 0;
+  if (jc.eq8 && jc.R.n && jc.S.n) d2h_sync(ctx, &e, jc.eq8, sizeof(e));
+  if (rsize_eq8) *rsize_eq8 = e;
+  if (partition_bits) *partition_bits = jc.B;
+  if (units) *units = jc.U;
+  API_END
+}
+
 gj_status gj_theta_stats(gj_ctx* ctx, uint64_t* nlj_pairs, uint64_t* cross_pairs) {
   API_BEGIN
   if (!ctx) throw Error(GJ_EINVAL, "ctx is NULL");

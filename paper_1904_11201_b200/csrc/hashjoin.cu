@@ -582,12 +582,21 @@ __global__ void __launch_bounds__(HT) hj_write_fast(HJArgs a, const uint16_t* __
   }
 }
 
+// Work units per partition; also accumulates the paper's result-size estimate
+// Eq.8: R_size = sum over the k partitions ("Reducers") of
+// |S_i| * |T_i| -- an upper bound on |J| that needs no join (gj_join_stats).
 __global__ void hj_units(const uint32_t* __restrict__ boff, const uint32_t* __restrict__ poff, uint32_t P,
-                         uint32_t bchunk, uint32_t pchunk, uint32_t* __restrict__ nunits) {
+                         uint32_t bchunk, uint32_t pchunk, uint32_t* __restrict__ nunits,
+                         unsigned long long* __restrict__ eq8) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= P) return;
-  uint32_t nb = boff[p + 1] - boff[p], np = poff[p + 1] - poff[p];
-  nunits[p] = (nb && np) ? ((nb + bchunk - 1) / bchunk) * ((np + pchunk - 1) / pchunk) : 0u;
+  unsigned long long prod = 0;
+  if (p < P) {
+    uint32_t nb = boff[p + 1] - boff[p], np = poff[p + 1] - poff[p];
+    nunits[p] = (nb && np) ? ((nb + bchunk - 1) / bchunk) * ((np + pchunk - 1) / pchunk) : 0u;
+    prod = (unsigned long long)nb * np;
+  }
+  prod = warp_sum(prod);
+  if (lane_id() == 0 && prod) atomicAdd(eq8, prod);
 }
 
 // unit descriptors (build begin, build n, probe begin, probe n): one binary search
@@ -649,8 +658,11 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
   jc.pchunk = pchunk;
 
   uint32_t* unit_off = static_cast<uint32_t*>(ws(ctx, "hj.unit_off", (P + 1) * sizeof(uint32_t)));
+  unsigned long long* eq8 = static_cast<unsigned long long*>(ws(ctx, "hj.eq8", sizeof(unsigned long long)));
+  GJ_CUDA(cudaMemsetAsync(eq8, 0, sizeof(unsigned long long), ctx->stream));
+  jc.eq8 = eq8;
   launch(ctx, "hj_units", hj_units, dim3((P + 255) / 256), dim3(256), 0, PB.off, PP.off, P, bchunk, pchunk,
-         unit_off);
+         unit_off, eq8);
   exclusive_scan<uint32_t, uint32_t>(ctx, unit_off, unit_off, P, unit_off + P);
   uint32_t U = 0;
   d2h_sync(ctx, &U, unit_off + P, sizeof(uint32_t));

@@ -56,6 +56,7 @@ struct JoinCache {
   const uint64_t* woff = nullptr;  // U*W exclusive offsets
   uint64_t total = 0;
   uint64_t nmulti = 0;  // units flagged MULTI (the write pass re-probes them)
+  const unsigned long long* eq8 = nullptr;  // device: Eq.8 result-size bound of the last count
 };
 
 struct ThetaCache {

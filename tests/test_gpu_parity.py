@@ -452,6 +452,24 @@ def test_launch_accounting_and_profile(gj):
     c.close()
 
 
+# ------------------------------------------------------------------ Eq.8 result-size estimate
+
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+@pytest.mark.parametrize("bits", [-1, 0, 3, 11])
+def test_join_stats_eq8_matches_oracle(gj, ctx, dtype, bits):
+    """gj_join_stats: Eq.8's sum_i |R_i||S_i| over the join's own partitions
+    equals oracle O9 at the partition bits the join used, and bounds |J|."""
+    rng = np.random.default_rng(40 + bits)
+    R = rng.integers(-2**40 if dtype == np.int64 else -50_000, 50_000, 30_000).astype(dtype)
+    S = rng.integers(-50_000, 50_000, 45_000).astype(dtype)
+    ctx.set_option("part_bits", bits)
+    n = gj.join_count(ctx, dev(R), dev(S))
+    e, B, units = ctx.join_stats()
+    assert B == (bits if bits >= 0 else B) and units > 0
+    assert e == oracle.eq8_rsize(R, S, B)
+    assert e >= n == oracle.equi_count_hist(R, S)
+
+
 # ------------------------------------------------------------------ theta region matrix (PAPER.md §4.2, Alg.3)
 
 def _region_inputs(kind):

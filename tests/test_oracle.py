@@ -203,3 +203,46 @@ def test_c4_statistics_small():
     p = ((2 * eps + 1) * D - eps * (eps + 1)) / D**2
     expect = p * (1 << 12) * (1 << 16)
     assert abs(c - expect) < 5 * np.sqrt(expect) + 0.02 * expect
+
+
+
+# ---- O9: Eq.8 result-size estimate
+
+def test_eq8_single_reducer_is_the_cartesian_product():
+    """k = 1 Reducer: omega_1 = lambda_1 = 1, so R_size = |S| |T| (the Cartesian
+    allocation the paper starts from)."""
+    R, S = gen.c1(n=500, D=50)
+    assert oracle.eq8_rsize(R, S, 0) == len(R) * len(S)
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_eq8_bounds_the_join_and_shrinks_with_more_reducers(dtype):
+    """sum_i |S_i||T_i| >= sum_k cntR(k) cntS(k) = |J| (equal keys share a Reducer),
+    and splitting a Reducer never increases it ((a+b)(c+d) >= ac+bd)."""
+    rng = np.random.default_rng(5)
+    R = rng.integers(-3000, 3000, 4000).astype(dtype)
+    S = rng.integers(-3000, 3000, 5000).astype(dtype)
+    j = oracle.equi_count_hist(R, S)
+    prev = None
+    for b in range(0, 17):
+        e = oracle.eq8_rsize(R, S, b)
+        assert e >= j
+        if prev is not None:
+            assert e <= prev
+        prev = e
+
+
+def test_eq8_brute_force_partition_sums():
+    """Tiny inputs: the per-Reducer products recomputed with Python loops over a
+    partition map written out bit by bit (hi 32 bits of the 64-bit product, top b bits)."""
+    R = np.array([3, 1, 3, 7, -2, 9, 9], dtype=np.int32)
+    S = np.array([3, 5, 3, -2, 7, 7, 100, 1], dtype=np.int32)
+    for b in (1, 2, 3, 5):
+        def part(k):
+            x = k & 0xFFFFFFFF
+            h = ((x * 0x9E3779B97F4A7C15) & (2**64 - 1)) >> 32
+            return h >> (32 - b)
+        tot = 0
+        for p in range(1 << b):
+            tot += sum(part(int(r)) == p for r in R) * sum(part(int(s)) == p for s in S)
+        assert oracle.eq8_rsize(R, S, b) == tot

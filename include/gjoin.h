@@ -193,6 +193,19 @@ gj_status prefilter(gj_ctx* ctx, gj_rel R, gj_rel S, uint32_t flags, int op, uin
                     double bloom_bits_per_key, void* key_out_R, uint32_t* rid_out_R,
                     uint64_t* n_R_out, void* key_out_S, uint32_t* rid_out_S, uint64_t* n_S_out);
 
+/* ---------------------------------------------------------------- late materialisation
+ * Full result tuples from the (rid_R, rid_S) pairs ("extract the m-th
+ * record of T' and the n-th record of S'"): for p < n,
+ *   out_R[p] = row (pairs[2p] - rid_base_R) of payload_R   (width_R bytes per row)
+ *   out_S[p] = row (pairs[2p+1] - rid_base_S) of payload_S (width_S bytes per row).
+ * All pointers DEVICE, caller-owned; widths multiples of 4 (0 or a NULL payload
+ * skips that side).  Rows must exist (rid - rid_base < rows of the payload): the
+ * rids come from a join of the same relations.  Stream-ordered, no sync.
+ * GJ_EINVAL on NULL pairs with n > 0 or a width not a multiple of 4. */
+gj_status gj_gather_payloads(gj_ctx* ctx, const uint32_t* pairs, uint64_t n, const void* payload_R,
+                             uint32_t width_R, uint32_t rid_base_R, const void* payload_S, uint32_t width_S,
+                             uint32_t rid_base_S, void* out_R, void* out_S);
+
 /* ---------------------------------------------------------------- host entry
  * End-to-end equi join from HOST buffers (pinned for full PCIe speed): copies the
  * two key columns host->device on the ctx stream, runs join_count +

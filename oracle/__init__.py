@@ -17,6 +17,7 @@ Functions (each cites the passage it follows; see oracle.cpp for the C++ bodies)
 * ``pkfk_closed_form``   O8  J = {(m_j, j)} for the PK-FK generators (R keys a bijection
                              of R rows, S.key[j] = R.key[m_j]); pinned to O2 in tests.
 * ``eq8_rsize``          O9  the paper's result-size estimate Eq.8
+* ``gather_payloads``    O10 late materialisation of result tuples PAPER.md:141
 
 Parity status: every function above is pinned (tests/test_oracle.py); none is
 "parity unpinned".
@@ -188,3 +189,13 @@ def eq8_rsize(R, S, bits):
     cR = np.bincount(partition_of(R, bits).astype(np.int64), minlength=k)
     cS = np.bincount(partition_of(S, bits).astype(np.int64), minlength=k)
     return int(sum(int(a) * int(b) for a, b in zip(cR, cS) if a and b))
+
+
+def gather_payloads(pairs, payload_R=None, payload_S=None, rid_base_R=0, rid_base_S=0):
+    """O10: "if the m-th join key of T' and the n-th join key of S' match,
+    we extract the m-th record of T' and the n-th record of S'": row rid_R - base of R's
+    payload and row rid_S - base of S's payload for every pair, in pair order."""
+    pairs = np.asarray(pairs).astype(np.int64) & 0xFFFFFFFF
+    oR = None if payload_R is None else np.asarray(payload_R)[pairs[:, 0] - rid_base_R]
+    oS = None if payload_S is None else np.asarray(payload_S)[pairs[:, 1] - rid_base_S]
+    return oR, oS

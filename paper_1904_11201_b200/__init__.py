@@ -69,6 +69,8 @@ def _load():
     L.gj_theta_stats.restype = i32
     L.gj_join_stats.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(u32), ctypes.POINTER(u32)]
     L.gj_join_stats.restype = i32
+    L.gj_gather_payloads.argtypes = [vp, vp, u64, vp, u32, u32, vp, u32, u32, vp, vp]
+    L.gj_gather_payloads.restype = i32
     L.gj_ctx_launch_count.argtypes = [vp]
     L.gj_ctx_launch_count.restype = u64
     L.gj_ctx_reset_stats.argtypes = [vp]
@@ -106,7 +108,7 @@ lib = _load()
 
 # C-ABI symbols declared in include/gjoin.h (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("gj_ctx_create", "gj_ctx_destroy", "gj_ctx_set_stream", "gj_last_error", "gj_ctx_set_option",
-               "gj_ctx_launch_count", "gj_ctx_reset_stats", "gj_ctx_kernel_times", "gj_theta_stats", "gj_join_stats", "join_count",
+               "gj_ctx_launch_count", "gj_ctx_reset_stats", "gj_ctx_kernel_times", "gj_theta_stats", "gj_join_stats", "gj_gather_payloads", "join_count",
                "join_materialize", "theta_join_count", "theta_join_materialize", "prefilter", "join_host",
                "join_host_batch",
                "gj_comm_unique_id", "gj_comm_init", "gj_comm_destroy", "join_dist_count", "join_dist_count_filtered",
@@ -264,6 +266,32 @@ def prefilter(ctx: Context, R, S, flags: int = RANGE | BLOOM | TWO_SIDED, op: st
                          ctypes.c_void_p(okR.data_ptr()), ctypes.c_void_p(orR.data_ptr()), ctypes.byref(nR),
                          ctypes.c_void_p(okS.data_ptr()), ctypes.c_void_p(orS.data_ptr()), ctypes.byref(nS)))
     return okR[: nR.value], orR[: nR.value], okS[: nS.value], orS[: nS.value]
+
+
+def gather_payloads(ctx: Context, pairs: torch.Tensor, payload_R: Optional[torch.Tensor] = None,
+                    payload_S: Optional[torch.Tensor] = None, rid_base_R: int = 0, rid_base_S: int = 0):
+    """Late materialisation: rows pairs[:, 0] - rid_base_R of payload_R and
+    pairs[:, 1] - rid_base_S of payload_S (CUDA tensors, rows along dim 0, row bytes a
+    multiple of 4).  Returns (out_R, out_S) (None for a side not given)."""
+    n = pairs.shape[0]
+    outs = []
+    args = []
+    for pay in (payload_R, payload_S):
+        if pay is None:
+            outs.append(None)
+            args += [None, 0]
+            continue
+        if not pay.is_cuda or not pay.is_contiguous():
+            raise ValueError("payloads must be contiguous CUDA tensors")
+        row = pay[0].numel() * pay.element_size() if pay.dim() > 1 else pay.element_size()
+        o = torch.empty((n,) + tuple(pay.shape[1:]), dtype=pay.dtype, device=pay.device)
+        outs.append(o)
+        args += [ctypes.c_void_p(pay.data_ptr()), row]
+    _check(lib.gj_gather_payloads(ctx.h, ctypes.c_void_p(pairs.data_ptr()), n, args[0], args[1], rid_base_R,
+                                  args[2], args[3], rid_base_S,
+                                  ctypes.c_void_p(outs[0].data_ptr()) if outs[0] is not None else None,
+                                  ctypes.c_void_p(outs[1].data_ptr()) if outs[1] is not None else None))
+    return outs[0], outs[1]
 
 
 def join_host(ctx: Context, key_R: torch.Tensor, key_S: torch.Tensor, out: torch.Tensor) -> int:

@@ -13,6 +13,7 @@
 #include <string>
 
 #include "gjoin.h"
+#include "gather.cuh"
 #include "hashjoin.cuh"
 #include "nlj.cuh"
 #include "partition.cuh"
@@ -328,6 +329,21 @@ gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t v) {
 }
 
 uint64_t gj_ctx_launch_count(gj_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+gj_status gj_gather_payloads(gj_ctx* ctx, const uint32_t* pairs, uint64_t n, const void* payload_R,
+                             uint32_t width_R, uint32_t rid_base_R, const void* payload_S, uint32_t width_S,
+                             uint32_t rid_base_S, void* out_R, void* out_S) {
+  API_BEGIN
+  if (!ctx) throw Error(GJ_EINVAL, "ctx is NULL");
+  if (n && !pairs) throw Error(GJ_EINVAL, "gj_gather_payloads: pairs is NULL");
+  if (width_R % 4 || width_S % 4) throw Error(GJ_EINVAL, "gj_gather_payloads: widths must be multiples of 4");
+  const void* pR = width_R ? payload_R : nullptr;
+  const void* pS = width_S ? payload_S : nullptr;
+  if ((pR && !out_R) || (pS && !out_S)) throw Error(GJ_EINVAL, "gj_gather_payloads: NULL output");
+  gather_payloads(ctx, pairs, n, pR, width_R, rid_base_R, pS, width_S, rid_base_S, out_R, out_S);
+  GJ_CUDA(cudaGetLastError());
+  API_END
+}
 
 gj_status gj_join_stats(gj_ctx* ctx, uint64_t* rsize_eq8, uint32_t* partition_bits, uint32_t* units) {
   API_BEGIN

@@ -246,3 +246,22 @@ def test_eq8_brute_force_partition_sums():
         for p in range(1 << b):
             tot += sum(part(int(r)) == p for r in R) * sum(part(int(s)) == p for s in S)
         assert oracle.eq8_rsize(R, S, b) == tot
+
+
+
+# ---- O10: late materialisation
+
+def test_gather_of_the_key_columns_reproduces_matching_keys():
+    """Gathering the KEY columns along the join's pairs gives, pair by pair, keys that
+    satisfy the predicate: equal for the equi join, ordered for <."""
+    R, S = gen.c1(n=400, D=60)
+    _, p = oracle.hash_equi(R, S)
+    kR, kS = oracle.gather_payloads(p, R, S)
+    assert len(kR) == len(p) and np.array_equal(kR, kS)
+    _, q = oracle.nlj(R, S, "lt")
+    kR, kS = oracle.gather_payloads(q, R, S)
+    assert np.all(kR < kS)
+    # rid bases: a shard whose rids start at 1000
+    _, p2 = oracle.hash_equi(R, S, rid_base_R=1000, rid_base_S=7)
+    kR2, kS2 = oracle.gather_payloads(p2, R, S, rid_base_R=1000, rid_base_S=7)
+    assert np.array_equal(kR2, kS2) and len(kR2) == len(p)

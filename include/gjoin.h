@@ -104,7 +104,13 @@ const char* gj_last_error(void);
  *                          Alg.3 (default): both relations range-partitioned into
  *                          equal-width key buckets, only cells that can hold a match
  *                          visited by the NLJ, Green cells written as cross products;
- *                          0 = the NLJ over all n_R x n_S pairs */
+ *                          0 = the NLJ over all n_R x n_S pairs
+ *  GJ_OPT_THETA_GRID_ROWS  multi-GPU theta joins: the ranks form an r x (G/r) grid
+ *                          (1-Bucket-Theta, PAPER.md:226-244's family); rank (i, j)
+ *                          joins R block i (the R shards of grid row i) with S block
+ *                          j (the S shards of grid column j).  r = 1 is the R
+ *                          broadcast; 0 (default) = the divisor of G minimising
+ *                          |R|/r + |S|/c.  Must be equal on every rank. */
 enum {
   GJ_OPT_PART_BITS = 1,
   GJ_OPT_BUILD_CHUNK = 2,
@@ -114,7 +120,8 @@ enum {
   GJ_OPT_FORCE_SLOW_BAND = 6,
   GJ_OPT_BUILD_SIDE = 7,
   GJ_OPT_SHUFFLE_BITS = 8,
-  GJ_OPT_THETA_REGIONS = 9
+  GJ_OPT_THETA_REGIONS = 9,
+  GJ_OPT_THETA_GRID_ROWS = 10
 };
 gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t value);
 

@@ -317,6 +317,10 @@ gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t v) {
       ctx->shuffle_bits = (int)v;
       break;
     case GJ_OPT_THETA_REGIONS: ctx->theta_regions = v != 0; break;
+    case GJ_OPT_THETA_GRID_ROWS:
+      if (v < 0 || v > 64) throw Error(GJ_EINVAL, "theta_grid_rows must be in [0, 64]");
+      ctx->theta_grid_rows = (uint32_t)v;
+      break;
     case GJ_OPT_BUILD_SIDE:
       if (v < 0 || v > 2) throw Error(GJ_EINVAL, "build_side must be 0, 1 or 2");
       ctx->build_side = (int)v;

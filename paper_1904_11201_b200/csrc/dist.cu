@@ -493,7 +493,107 @@ void equi_count_any(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) {
   else dist_equi_count(ctx, c, R, S);
 }
 
+// Gathers the shards of `members` (ranks, ascending) of relation X into one buffer
+// pair (key, rid) on every member, by grouped send/recv on the job's communicator;
+// n[q] = shard size of rank q.  Shard q's rows keep their global rids.
+gj_rel gather_group(gj_ctx* ctx, gj_comm* c, const gj_rel& X, const std::vector<int>& members,
+                    const std::vector<unsigned long long>& n, const char* tag) {
+  const size_t ks = X.key_type == GJ_I64 ? 8 : 4;
+  const ncclDataType_t kt = X.key_type == GJ_I64 ? ncclInt64 : ncclInt32;
+  std::vector<uint64_t> off(members.size() + 1, 0);
+  for (size_t k = 0; k < members.size(); ++k) off[k + 1] = off[k] + n[members[k]];
+  if (off.back() >= (1ull << 32)) throw Error(GJ_EINVAL, "a gathered block must hold < 2^32 tuples");
+  std::string t(tag);
+  uint8_t* key = static_cast<uint8_t*>(ws(ctx, (t + ".key").c_str(), off.back() * ks + 16));
+  uint32_t* rid = static_cast<uint32_t*>(ws(ctx, (t + ".rid").c_str(), off.back() * 4 + 16));
+  const uint32_t* myrid = X.rid;
+  if (!myrid && X.n) {
+    uint32_t* tmp = static_cast<uint32_t*>(ws(ctx, (t + ".srid").c_str(), X.n * 4));
+    launch(ctx, "fill_rids", fill_rids, dim3((uint32_t)std::min<uint64_t>((X.n + 255) / 256, 4096)), dim3(256), 0,
+           tmp, X.n, X.rid_base);
+    myrid = tmp;
+  }
+  GJ_NCCL(ncclGroupStart());
+  for (size_t k = 0; k < members.size(); ++k) {
+    const int q = members[k];
+    if (!n[q]) continue;
+    if (q == c->rank) {
+      GJ_CUDA(cudaMemcpyAsync(key + off[k] * ks, X.key, X.n * ks, cudaMemcpyDeviceToDevice, ctx->stream));
+      GJ_CUDA(cudaMemcpyAsync(rid + off[k], myrid, X.n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+      for (int p : members)
+        if (p != c->rank) {
+          GJ_NCCL(ncclSend(X.key, X.n, kt, p, c->comm, ctx->stream));
+          GJ_NCCL(ncclSend(myrid, X.n, ncclUint32, p, c->comm, ctx->stream));
+        }
+    } else {
+      GJ_NCCL(ncclRecv(key + off[k] * ks, n[q], kt, q, c->comm, ctx->stream));
+      GJ_NCCL(ncclRecv(rid + off[k], n[q], ncclUint32, q, c->comm, ctx->stream));
+    }
+  }
+  GJ_NCCL(ncclGroupEnd());
+  return gj_rel{key, rid, off.back(), X.key_type, 0};
+}
+
+// 1-Bucket grid theta sharding (NEXT row f3; Okcan & Riedewald's 1-Bucket-Theta,
+// the paper's M-Bucket-I baseline family): the G ranks form an
+// r x c grid, rank q = (i, j) = (q / c, q % c).  R is split into r blocks -- block i
+// = the R shards of row i's ranks -- and S into c blocks -- block j = the S shards
+// of column j's ranks; rank (i, j) joins R block i with S block j.  Every (r, s)
+// pair lands on exactly one rank (row of r's shard, column of s's shard).  r = 1 is
+// the R broadcast.  r is the ctx option, else the divisor of G minimising the
+// tuples a rank holds, |R|/r + |S|/c.
+void dist_theta_grid(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S, int op, uint64_t eps,
+                     uint32_t rows) {
+  const int G = c->nranks;
+  const int cols = G / (int)rows;
+  unsigned long long* cnt = static_cast<unsigned long long*>(ws(ctx, "dist.gcnt", (2 + 2 * G) * 8));
+  const unsigned long long mine[2] = {R.n, S.n};
+  GJ_CUDA(cudaMemcpyAsync(cnt, mine, 16, cudaMemcpyHostToDevice, ctx->stream));
+  GJ_NCCL(ncclAllGather(cnt, cnt + 2, 2, ncclUint64, c->comm, ctx->stream));
+  std::vector<unsigned long long> all(2 * G), nR(G), nS(G);
+  d2h_sync(ctx, all.data(), cnt + 2, 2 * G * 8);
+  for (int q = 0; q < G; ++q) {
+    nR[q] = all[2 * q];
+    nS[q] = all[2 * q + 1];
+  }
+  const int i = c->rank / cols, j = c->rank % cols;
+  std::vector<int> row, col;
+  for (int jj = 0; jj < cols; ++jj) row.push_back(i * cols + jj);
+  for (int ii = 0; ii < (int)rows; ++ii) col.push_back(ii * cols + j);
+  gj_rel RB, SB;
+  {
+    RegionScope rs(ctx, "nccl_grid_gather");
+    RB = gather_group(ctx, c, R, row, nR, "dist.gR");
+    SB = gather_group(ctx, c, S, col, nS, "dist.gS");
+  }
+  ctx->tc = ThetaCache{};
+  theta_count(ctx, RB, SB, op, eps);
+  ctx->tc.R = RB;
+  ctx->tc.valid = true;
+}
+
+uint32_t theta_grid_rows(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) {
+  const int G = c->nranks;
+  if (ctx->theta_grid_rows) {
+    if (G % ctx->theta_grid_rows) throw Error(GJ_EINVAL, "theta_grid_rows must divide the number of ranks");
+    return ctx->theta_grid_rows;
+  }
+  // totals from this rank's shard sizes scaled by G: every rank decides alike only
+  // if the choice uses global data -- so take the cost with the largest shards
+  const double nr = (double)allreduce_sum(ctx, c, R.n), ns = (double)allreduce_sum(ctx, c, S.n);
+  uint32_t best = 1;
+  double bc = nr + ns / G;
+  for (int r = 2; r <= G; r *= 2)
+    if (G % r == 0 && nr / r + ns / (G / r) < bc) {
+      bc = nr / r + ns / (G / r);
+      best = (uint32_t)r;
+    }
+  return best;
+}
+
 void dist_theta_count(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S, int op, uint64_t eps) {
+  const uint32_t rows = theta_grid_rows(ctx, c, R, S);
+  if (rows > 1) return dist_theta_grid(ctx, c, R, S, op, eps, rows);
   const int G = c->nranks;
   const size_t ks = R.key_type == GJ_I64 ? 8 : 4;
   const ncclDataType_t kt = R.key_type == GJ_I64 ? ncclInt64 : ncclInt32;

@@ -102,7 +102,8 @@ struct gj_ctx {
   bool force_slow_band = false;
   bool overlap_shuffle = true;
   uint32_t shuffle_ctas = 0;    // CTA cap of the shuffle scatter (0 = all)  // multi-GPU equi: S shuffle on a 2nd stream beside R's local passes
-  int theta_regions = 1;  // theta joins through the region matrix (0 = plain NLJ over all pairs)
+  int theta_regions = 1;
+  uint32_t theta_grid_rows = 0;  // multi-GPU theta: rows r of the 1-Bucket grid (0 = auto; 1 = R broadcast)  // theta joins through the region matrix (0 = plain NLJ over all pairs)
   int build_side = 0;
   int shuffle_bits = 0;
   // workspace

@@ -113,6 +113,20 @@ def _worker(rank, world, port, q):
         nl, ng = gj.theta_join_dist_count(ctx, comm, R3, S3, "band", 40)
         out["band"] = (nl, ng, gj.theta_join_dist_materialize(ctx, comm, R3, S3, "band", 40, nl).cpu().numpy().view(
             np.uint32))
+        # 1-Bucket grid (NEXT f3): r x (G/r) ranks, R block per grid row, S block per grid column
+        for rows in sorted({world, 2}):
+            ctx.set_option("theta_grid_rows", rows)
+            nl, ng = gj.theta_join_dist_count(ctx, comm, R3, S3, "band", 40)
+            out[f"band_grid{rows}"] = (nl, ng, gj.theta_join_dist_materialize(ctx, comm, R3, S3, "band", 40, nl)
+                                       .cpu().numpy().view(np.uint32))
+            g0, g1 = (rank * 2000) // world, ((rank + 1) * 2000) // world
+            h0, h1 = (rank * 3000) // world, ((rank + 1) * 3000) // world
+            R6 = gj.Rel(torch.from_numpy(R3all[:2000][g0:g1]).cuda(), None, g0)
+            S6 = gj.Rel(torch.from_numpy(S3all[:3000][h0:h1]).cuda(), None, h0)
+            nl, ng = gj.theta_join_dist_count(ctx, comm, R6, S6, "ge", 0)
+            out[f"ge_grid{rows}"] = (nl, ng, gj.theta_join_dist_materialize(ctx, comm, R6, S6, "ge", 0, nl)
+                                     .cpu().numpy().view(np.uint32))
+        ctx.set_option("theta_grid_rows", 0)
         q.put((rank, out))
         comm.close()
         ctx.close()
@@ -159,6 +173,9 @@ def test_dist_joins_match_oracle(world):
     pk = oracle.pkfk_closed_form(m)
     expect = {"equi": pk, "equi_sb6": pk, "dup": dup, "dup_pb3": dup,
               "i64": oracle.hash_equi(R4all, S4all), "band": oracle.band_materialize(R3all, S3all, 40)}
+    for rows in sorted({world, 2}):
+        expect[f"band_grid{rows}"] = expect["band"]
+        expect[f"ge_grid{rows}"] = oracle.nlj(R3all[:2000], S3all[:3000], "ge")
     R5all, S5all, m5 = _c5_inputs()
     import paper_1904_11201_b200 as gj
     pk5 = oracle.pkfk_closed_form(m5)

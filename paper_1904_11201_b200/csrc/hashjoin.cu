@@ -37,9 +37,6 @@ constexpr int PCH_MAX = 4096;      // max probe tuples per unit
 constexpr int TAB_MAX = 2 * BCH_MAX;
 constexpr int BPT = BCH_MAX / HT;  // build tuples per thread
 constexpr int PPT = PCH_MAX / HT;  // probe tuples per lane (warp w owns rows [w*pn/HW, ...))
-#ifndef HJ_COUNT_MINB
-#define HJ_COUNT_MINB 1  // CTAs per SM the count kernel is register-budgeted for (3 measured slower: spills)
-#endif
 
 // Independent second hash for the in-partition table slot (the partition id
 // already consumed the top bits of khash).
@@ -221,7 +218,7 @@ __device__ __forceinline__ Win window(uint64_t first, uint32_t cnt, uint32_t esz
 constexpr uint16_t NO_MATCH = 0xFFFF, MULTI = 0xFFFE;
 
 template <typename K>
-__global__ void __launch_bounds__(HT, HJ_COUNT_MINB) hj_count_kernel(HJArgs a, uint16_t* __restrict__ stage,
+__global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __restrict__ stage,
                                                       uint8_t* __restrict__ multi,
                                                       unsigned long long* __restrict__ nmulti) {
   extern __shared__ __align__(16) uint8_t smem[];

@@ -11,6 +11,7 @@
 // negatives, so J(filtered R, filtered S) = J(R, S).  Survivors are compacted
 // stably (count -> scan -> write) keeping their original rids.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <string>
 #include <type_traits>
@@ -154,11 +155,17 @@ __device__ __forceinline__ bool keep(K k, const Filt& f) {
   return ok;
 }
 
+// Inserts the keys whose filter block lies in [blk_lo, blk_hi): the host sweeps
+// the filter in L2-sized block ranges, so every 64-bit atomicOr hits a line that
+// stays in L2 instead of a DRAM read-modify-write of a random sector (a 256 MB
+// filter does not fit the 126 MB L2); the keys are re-read once per range.
 template <typename K>
 __global__ void bloom_build(const K* __restrict__ key, uint64_t n, Filt range, uint32_t* __restrict__ bloom,
-                            uint32_t log_blocks) {
+                            uint32_t log_blocks, uint32_t blk_lo, uint32_t blk_hi) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const K k = key[i];
+    const uint32_t blk = log_blocks ? (uint32_t)(bloom_hash(k) >> (64 - log_blocks)) : 0u;
+    if (blk < blk_lo || blk >= blk_hi) continue;
     if (!keep(k, range)) continue;
     const BloomSlot s = bloom_slot(k, log_blocks);
     unsigned long long* bw = reinterpret_cast<unsigned long long*>(bloom + (uint64_t)s.block * 8);
@@ -265,6 +272,18 @@ uint64_t compact(gj_ctx* ctx, const gj_rel& X, const Filt& f, void* kout, uint32
   return h;
 }
 
+// Filter block ranges of at most ~48 MB (L2 holds them while every key is
+// streamed past): f(b0, b1) per range; one range for filters that already fit.
+template <typename F>
+void for_block_ranges(uint32_t log_blocks, F f) {
+  static const uint64_t slice_bytes = [] {
+    const char* e = std::getenv("GJ_BLOOM_SLICE_MB");
+    return (uint64_t)(e ? std::atof(e) : 48.0) * (1ull << 20);
+  }();
+  const uint64_t nblk = 1ull << log_blocks, per = std::max<uint64_t>(1, slice_bytes / 32);
+  for (uint64_t b = 0; b < nblk; b += per) f((uint32_t)b, (uint32_t)std::min<uint64_t>(nblk, b + per));
+}
+
 uint32_t log_blocks_for(uint64_t n, double bpk) {
   const double bits = std::max(256.0, (double)n * bpk);
   uint32_t lb = 0;
@@ -282,8 +301,10 @@ const uint32_t* build_bloom(gj_ctx* ctx, const gj_rel& X, const Filt& range, dou
   GJ_CUDA(cudaMemsetAsync(bloom, 0, words * sizeof(uint32_t), ctx->stream));
   if (X.n) {
     const unsigned grid = (unsigned)std::min<uint64_t>((X.n + 255) / 256, (uint64_t)ctx->num_sms * 16);
-    launch(ctx, "bloom_build", bloom_build<K>, dim3(grid), dim3(256), 0, static_cast<const K*>(X.key), X.n, range,
-           bloom, lb);
+    for_block_ranges(lb, [&](uint32_t b0, uint32_t b1) {
+      launch(ctx, "bloom_build", bloom_build<K>, dim3(grid), dim3(256), 0, static_cast<const K*>(X.key), X.n, range,
+             bloom, lb, b0, b1);
+    });
   }
   return bloom;
 }
@@ -402,12 +423,14 @@ void pf_bloom_into(gj_ctx* ctx, const gj_rel& X, uint32_t* words, uint32_t logb)
   none.lo = 0;
   none.hi = ~0ull;
   const unsigned grid = (unsigned)std::min<uint64_t>((X.n + 255) / 256, (uint64_t)ctx->num_sms * 16);
-  if (X.key_type == GJ_I32)
-    launch(ctx, "bloom_build", bloom_build<int32_t>, dim3(grid), dim3(256), 0, static_cast<const int32_t*>(X.key),
-           X.n, none, words, logb);
-  else
-    launch(ctx, "bloom_build", bloom_build<int64_t>, dim3(grid), dim3(256), 0, static_cast<const int64_t*>(X.key),
-           X.n, none, words, logb);
+  for_block_ranges(logb, [&](uint32_t b0, uint32_t b1) {
+    if (X.key_type == GJ_I32)
+      launch(ctx, "bloom_build", bloom_build<int32_t>, dim3(grid), dim3(256), 0, static_cast<const int32_t*>(X.key),
+             X.n, none, words, logb, b0, b1);
+    else
+      launch(ctx, "bloom_build", bloom_build<int64_t>, dim3(grid), dim3(256), 0, static_cast<const int64_t*>(X.key),
+             X.n, none, words, logb, b0, b1);
+  });
 }
 
 uint64_t pf_compact(gj_ctx* ctx, const gj_rel& X, const PfSpec& spec, void* kout, uint32_t* rout, const char* tag) {

@@ -549,3 +549,24 @@ def test_theta_regions_match_plain_c4_shape(gj, ctx):
     ctx.set_option("theta_regions", 0)
     b = gj.theta_join_count(ctx, tR, tS, "band", gen.C4_EPS)
     assert a == b == oracle.theta_count_sorted(R, S, "band", gen.C4_EPS)
+
+
+@pytest.mark.parametrize("op", ["lt", "band", "ne"])
+def test_theta_regions_with_rid_maps(gj, ctx, op):
+    """Region mode carries caller rid maps (e.g. pre-filter survivors) through the range
+    partitioning: pairs are the oracle's positional pairs mapped through the rid arrays."""
+    rng = np.random.default_rng(9)
+    R = rng.integers(-5000, 5000, 3000).astype(np.int32)
+    S = rng.integers(-5000, 5000, 7001).astype(np.int32)
+    rR = rng.permutation(10_000)[:3000].astype(np.int32)
+    rS = rng.permutation(20_000)[:7001].astype(np.int32)
+    eps = 25 if op == "band" else 0
+    tR = gj.Rel(dev(R), dev(rR))
+    tS = gj.Rel(dev(S), dev(rS))
+    n = gj.theta_join_count(ctx, tR, tS, op, eps)
+    cn, cp = oracle.nlj(R, S, op, eps)
+    assert n == cn
+    got = canon_gpu(gj.theta_join_materialize(ctx, tR, tS, op, eps, n))
+    exp = np.stack([rR[cp[:, 0]], rS[cp[:, 1]]], 1).astype(np.uint32)
+    exp = exp[np.lexsort((exp[:, 1], exp[:, 0]))]
+    assert np.array_equal(got, exp)

@@ -566,16 +566,17 @@ __global__ void __launch_bounds__(HT) hj_write_fast(HJArgs a, const uint16_t* __
         const uint32_t i = r0 + lane;
         const bool valid = i < whi;
         const uint16_t sx = valid ? (i < ws.valid ? Bb.st[ws.shift + i] : stage[d.z + i]) : NO_MATCH;
-        const uint32_t m = sx != NO_MATCH ? 1u : 0u;
-        const uint32_t incl = warp_incl_scan(m);
+        const bool m = sx != NO_MATCH;
+        // at most one match per row here: ranks are a ballot + popc, not a scan
+        const uint32_t bal = __ballot_sync(FULL, m);
         if (m) {
           const uint32_t prow = a.prid ? (i < wp.valid ? Bb.pr[wp.shift + i] : a.prid[d.z + i])
                                        : a.prid_base + d.z + i;
           const uint32_t brow = a.brid ? (sx < wb.valid ? Bb.br[wb.shift + sx] : a.brid[d.x + sx])
                                        : a.brid_base + d.x + sx;
-          a.out[base + incl - 1] = a.swap ? make_uint2(prow, brow) : make_uint2(brow, prow);
+          a.out[base + __popc(bal & lanemask_lt())] = a.swap ? make_uint2(prow, brow) : make_uint2(brow, prow);
         }
-        base += __shfl_sync(FULL, incl, 31);
+        base += __popc(bal);
       }
     }
     __syncthreads();  // buffer b is refilled by the issue of iteration it + 1

@@ -19,6 +19,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"par
     -s 30 -c 6 -o $O/${R}_full_c2 python bench.py --workload c2 $ARGS > $O/ncu_full_c2.log 2>&1 || echo "full c2 failed"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"nlj_kernel|part_scatter" \
     -s 8 -c 4 -o $O/${R}_full_c4 python bench.py --workload c4 $ARGS > $O/ncu_full_c4.log 2>&1 || echo "full c4 failed"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"pf_count|pf_write|bloom_build|part_scatter" \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"pf_count|pf_write|bloom_build" \
     -s 6 -c 4 -o $O/${R}_full_c5 python bench.py --workload c5 --c5-bits 26 $ARGS > $O/ncu_full_c5.log 2>&1 || echo "full c5 failed"
 ls -la $O | grep $R

@@ -30,6 +30,10 @@
 namespace gj {
 namespace {
 
+#ifndef GJ_HJ_LOAD_BREAK
+#define GJ_HJ_LOAD_BREAK 1  // key prefetch stops at the unit's end (uniform branch) instead of predicating
+#endif
+
 constexpr int HT = 512;            // threads per CTA
 constexpr int HW = HT / 32;        // warps per CTA (counts are kept per (unit, warp))
 constexpr int BCH_MAX = 4096;      // max build tuples per unit
@@ -175,6 +179,9 @@ __device__ __forceinline__ void load_keys(UnitKeys<K>& R, const uint4 d, const H
   const K* __restrict__ pkey = static_cast<const K*>(a.pkey);
 #pragma unroll
   for (int j = 0; j < BPT; ++j) {
+#if GJ_HJ_LOAD_BREAK
+    if ((uint32_t)j * HT >= d.y) break;  // CTA-uniform: no predicated-off loads past the unit
+#endif
     const uint32_t i = tid + j * HT;
     R.kb[j] = i < d.y ? bkey[d.x + i] : K(0);
   }
@@ -182,6 +189,9 @@ __device__ __forceinline__ void load_keys(UnitKeys<K>& R, const uint4 d, const H
   probe_range(d.w, w, wb, we);
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
+#if GJ_HJ_LOAD_BREAK
+    if (wb + 32 * j >= we) break;  // warp-uniform
+#endif
     const uint32_t i = wb + lane + 32 * j;
     R.kp[j] = i < we ? pkey[d.z + i] : K(0);
   }

@@ -530,8 +530,11 @@ struct LocalLayout {
   static size_t bytes(uint32_t D) { return off_whist + ((size_t)NW * words(D) + (size_t)D) * 4; }
 };
 
+#ifndef GJ_SCATTER_MINB
+#define GJ_SCATTER_MINB 2  // CTAs/SM the register budget targets (3: 85 registers, 8 B spills, -0.6%: noise level)
+#endif
 template <typename K, bool HAS_RID, bool RANGE>
-__global__ void __launch_bounds__(PT, 2) part_scatter_local(
+__global__ void __launch_bounds__(PT, GJ_SCATTER_MINB) part_scatter_local(
     const K* __restrict__ key_in, const uint32_t* __restrict__ rid_in, uint32_t rid_base, uint64_t n,
     const uint4* __restrict__ tdesc, uint32_t ntiles, uint32_t shift, uint32_t bits,
     const uint32_t* __restrict__ tile_base, K* __restrict__ key_out, uint32_t* __restrict__ rid_out,

@@ -227,8 +227,15 @@ __device__ __forceinline__ Win window(uint64_t first, uint32_t cnt, uint32_t esz
 // and re-probed by the write pass).
 constexpr uint16_t NO_MATCH = 0xFFFF, MULTI = 0xFFFE;
 
+// GJ_HJ_COUNT_MINB > 1: register budget for that many int32 CTAs per SM (an explicit
+// minimum of 1 is not the same as none: ptxas then spends 72 registers instead of 54)
+#if defined(GJ_HJ_COUNT_MINB) && GJ_HJ_COUNT_MINB > 1
+#define GJ_HJ_COUNT_BOUNDS(K) __launch_bounds__(HT, sizeof(K) == 4 ? GJ_HJ_COUNT_MINB : 1)
+#else
+#define GJ_HJ_COUNT_BOUNDS(K) __launch_bounds__(HT)
+#endif
 template <typename K>
-__global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __restrict__ stage,
+__global__ void GJ_HJ_COUNT_BOUNDS(K) hj_count_kernel(HJArgs a, uint16_t* __restrict__ stage,
                                                       uint8_t* __restrict__ multi,
                                                       unsigned long long* __restrict__ nmulti) {
   extern __shared__ __align__(16) uint8_t smem[];

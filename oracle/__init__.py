@@ -10,13 +10,16 @@ Functions (each cites the passage it follows; see oracle.cpp for the C++ bodies)
 * ``nlj``                O1  nested loop join, canonical order
 * ``hash_equi``          O2  unordered_multimap build/probe + sort PAPER.md:68
 * ``theta_count_sorted`` O3  sort + binary-search counts          definition (1) in oracle.cpp
+* ``theta_count_per_row`` O3r O3's counts per R row              definition (1) in oracle.cpp
 * ``band_materialize``   O4  sorted range enumeration             definition (1), band
 * ``equi_count_hist``    O5  sum_k cntR(k)*cntS(k)                north star invariant
 * ``semijoin_exact``     O6  exact common-key filter mask         PAPER.md:80-81, Alg.1
 * ``semijoin_band``      O6b band semi-join mask                  definition (1), band
 * ``pkfk_closed_form``   O8  J = {(m_j, j)} for the PK-FK generators (R keys a bijection
                              of R rows, S.key[j] = R.key[m_j]); pinned to O2 in tests.
-* ``eq8_rsize``          O9  the paper's result-size estimate Eq.8
+* ``eq8_from_counts``    O9  the paper's result-size estimate Eq.7-8
+* ``eq8_rsize``          O9  Eq.8 over a join's own partitions      (partition_of: the
+                             product's key -> Reducer map, a performance choice)
 * ``gather_payloads``    O10 late materialisation of result tuples PAPER.md:141
 
 Parity status: every function above is pinned (tests/test_oracle.py); none is
@@ -59,6 +62,8 @@ def lib():
         L.orc_hash_equi.restype = u64
         L.orc_theta_count_sorted.argtypes = [vp, u64, vp, u64, i32, i32, u64]
         L.orc_theta_count_sorted.restype = u64
+        L.orc_theta_count_per_row.argtypes = [vp, u64, vp, u64, i32, i32, u64, vp]
+        L.orc_theta_count_per_row.restype = None
         L.orc_band_materialize_sorted.argtypes = [vp, u64, vp, u64, i32, u64, u32, u32, vp, u64]
         L.orc_band_materialize_sorted.restype = u64
         L.orc_equi_count_hist.argtypes = [vp, u64, vp, u64, i32]
@@ -112,6 +117,14 @@ def theta_count_sorted(R, S, op, eps=0):
     return lib().orc_theta_count_sorted(_ptr(R), len(R), _ptr(S), len(S), t, OPS[op], eps)
 
 
+def theta_count_per_row(R, S, op, eps=0):
+    """O3r: uint64 array, |{j : R[i] op S[j]}| for every R row i."""
+    R, S, t = _keys(R, S)
+    out = np.zeros(max(len(R), 1), dtype=np.uint64)
+    lib().orc_theta_count_per_row(_ptr(R), len(R), _ptr(S), len(S), t, OPS[op], eps, _ptr(out))
+    return out[: len(R)]
+
+
 def band_materialize(R, S, eps, rid_base_R=0, rid_base_S=0):
     """O4: (count, pairs) for |R.key - S.key| <= eps in canonical order."""
     R, S, t = _keys(R, S)
@@ -163,12 +176,43 @@ def pkfk_closed_form(m, rid_base_S=0, r_rows=None):
     return len(pairs), pairs
 
 
+def eq8_from_counts(s_counts, t_counts, S_total, T_total):
+    """O9: the paper's result-size estimate, Eq.7-8, evaluated in
+    the paper's order and notation with exact rationals.  Inputs: the per-Reducer
+    post-filter tuple counts s_i (S side) and t_i (T side) of k Reducers, and the
+    unfiltered table sizes |S|, |T|.
+
+      beta  = sum_i s_i / |S|,  gamma = sum_i t_i / |T|          (filter ratios, :201)
+      omega_i = s_i / (beta |S|),  lambda_i = t_i / (gamma |T|)  (shares, Eq.7: sum = 1)
+      R_size = gamma * beta * |S| * |T| * sum_i omega_i * lambda_i          (Eq.8)
+
+    Returns R_size as a Fraction (an integer for integer counts).  |S| or |T| = 0, or
+    nothing surviving the filter, gives 0 ("DegenerateInput ... all-zero")."""
+    from fractions import Fraction
+    s_counts = [int(x) for x in s_counts]
+    t_counts = [int(x) for x in t_counts]
+    if len(s_counts) != len(t_counts):
+        raise ValueError("one s and one t count per Reducer")
+    if S_total == 0 or T_total == 0 or sum(s_counts) == 0 or sum(t_counts) == 0:
+        return Fraction(0)
+    beta = Fraction(sum(s_counts), S_total)
+    gamma = Fraction(sum(t_counts), T_total)
+    omega = [Fraction(x) / (beta * S_total) for x in s_counts]
+    lam = [Fraction(x) / (gamma * T_total) for x in t_counts]
+    assert sum(omega) == 1 and sum(lam) == 1  # Eq.7
+    return gamma * beta * S_total * T_total * sum(o * l for o, l in zip(omega, lam))
+
+
 def partition_of(K, bits):
-    """The partition ("Reducer") of every key when 2^bits partitions group equal keys
-    (tuples with the same key reach the same Reducer): the top
-    ``bits`` bits of hi32(key * 0x9E3779B97F4A7C15) over the key's 64-bit two's
-    complement pattern, int64 keys first folded as x ^ (x >> 32) (DESIGN.md §4.1's
-    partition map, restated here from its definition)."""
+    """The Reducer of every key when the library's join runs with 2^bits partitions.
+
+    Eq.8 holds for ANY key -> Reducer map that sends equal keys to the same Reducer
+    (PAPER.md:201 "tuples with the same key value are passed to the same Reducer");
+    WHICH map is a performance choice of the product (the top ``bits``
+    bits of hi32(key * 0x9E3779B97F4A7C15) over the key's two's-complement pattern,
+    int64 keys first folded as x ^ (x >> 32)).  It is restated here only so that
+    gj_join_stats can be compared with Eq.8 at the SAME map; nothing else in the
+    oracle depends on it, and Eq.8 itself is pinned by eq8_from_counts' tests."""
     K = np.asarray(K)
     if bits == 0:
         return np.zeros(len(K), dtype=np.uint64)
@@ -180,15 +224,17 @@ def partition_of(K, bits):
     return (h & np.uint64(0xFFFFFFFF)) >> np.uint64(32 - bits)
 
 
-def eq8_rsize(R, S, bits):
-    """O9: Eq.8, R_size = gamma*beta*|S|*|T| * sum_i omega_i*lambda_i
-    = sum over the k = 2^bits Reducers i of |S_i| * |T_i| (omega_i = |S_i| / (beta |S|),
-    lambda_i = |T_i| / (gamma |T|), Eq.7): per-partition tuple counts of both sides,
-    multiplied and summed (exact Python integers)."""
+def eq8_rsize(R, S, bits, reducer_of=None):
+    """O9 on two key columns: Eq.8 with the k = 2^bits Reducers given by ``reducer_of``
+    (default: the product's partition map, partition_of), no pre-filter (beta = gamma
+    = 1).  The join's own R plays the paper's T, S plays S."""
     k = 1 << bits
-    cR = np.bincount(partition_of(R, bits).astype(np.int64), minlength=k)
-    cS = np.bincount(partition_of(S, bits).astype(np.int64), minlength=k)
-    return int(sum(int(a) * int(b) for a, b in zip(cR, cS) if a and b))
+    f = reducer_of or (lambda K: partition_of(K, bits))
+    cR = np.bincount(np.asarray(f(R)).astype(np.int64), minlength=k)
+    cS = np.bincount(np.asarray(f(S)).astype(np.int64), minlength=k)
+    v = eq8_from_counts(cS, cR, len(S), len(R))
+    assert v.denominator == 1
+    return int(v)
 
 
 def gather_payloads(pairs, payload_R=None, payload_S=None, rid_base_R=0, rid_base_S=0):

@@ -156,6 +156,37 @@ uint64_t orc_theta_count_sorted(const void* rkey, uint64_t nR, const void* skey,
   return c;
 }
 
+// O3r -- O3 per R row: cnt[i] = |{ j : theta(R[i], S[j]) }|, the same sort + binary
+// search bounds as O3, one count per R row (so a GPU output can be checked row by
+// row: its per-row pair counts must equal these).
+void orc_theta_count_per_row(const void* rkey, uint64_t nR, const void* skey, uint64_t nS, int type, int op,
+                             uint64_t eps, uint64_t* cnt) {
+  std::vector<int64_t> R = widen(rkey, nR, type), S = widen(skey, nS, type);
+  std::sort(S.begin(), S.end());
+  auto lb = [&](int64_t x) { return (uint64_t)(std::lower_bound(S.begin(), S.end(), x) - S.begin()); };
+  auto ub = [&](int64_t x) { return (uint64_t)(std::upper_bound(S.begin(), S.end(), x) - S.begin()); };
+  for (uint64_t i = 0; i < nR; ++i) {
+    int64_t r = R[i];
+    uint64_t c = 0;
+    switch (op) {
+      case LT: c = nS - ub(r); break;
+      case LE: c = nS - lb(r); break;
+      case GT: c = lb(r); break;
+      case GE: c = ub(r); break;
+      case EQ: c = ub(r) - lb(r); break;
+      case NE: c = nS - (ub(r) - lb(r)); break;
+      case BAND: {
+        __int128 lo = (__int128)r - (__int128)eps, hi = (__int128)r + (__int128)eps;
+        uint64_t a = lo < (__int128)INT64_MIN ? 0 : lb((int64_t)lo);
+        uint64_t b = hi > (__int128)INT64_MAX ? nS : ub((int64_t)hi);
+        c = b - a;
+        break;
+      }
+    }
+    cnt[i] = c;
+  }
+}
+
 // O4 -- band join materialisation by sorted range enumeration: sort S row indices
 // by (key, row); for each R row in order take the S rows with key in
 // [r - eps, r + eps] (128-bit bounds), sort their row numbers, emit.  Canonical

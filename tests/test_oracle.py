@@ -108,6 +108,20 @@ def test_independent_algorithms_agree(dtype):
         assert np.array_equal(_canon(ps[:, ::-1]), p1)
 
 
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_theta_count_per_row_matches_double_loop(dtype):
+    """O3r: per-R-row counts equal the per-row tallies of O1's double loop, and sum to O3."""
+    rng = np.random.default_rng(31 + (dtype == np.int64))
+    for trial in range(700):
+        R, S = _random_instance(rng, dtype)
+        op = OPS[trial % len(OPS)]
+        eps = int(EPS_LIST[rng.integers(0, len(EPS_LIST))]) if op == "band" else 0
+        c, p = oracle.nlj(R, S, op, eps)
+        per = oracle.theta_count_per_row(R, S, op, eps)
+        assert np.array_equal(per, np.bincount(p[:, 0].astype(np.int64), minlength=len(R)).astype(np.uint64))
+        assert int(per.sum()) == oracle.theta_count_sorted(R, S, op, eps) == c
+
+
 def _canon(p):
     p = np.asarray(p).reshape(-1, 2)
     return p[np.lexsort((p[:, 1], p[:, 0]))]
@@ -206,19 +220,53 @@ def test_c4_statistics_small():
 
 
 
-# ---- O9: Eq.8 result-size estimate (PAPER.md:206-211)
+# ---- O9: Eq.8 result-size estimate (PAPER.md:200-211)
+
+def test_eq8_spec_worked_example_1250():
+    """SPEC.md:322 (hand evaluation of Eq.8): k = 2, |S| = |T| = 100, 50 + 50 tuples
+    survive the filter, split evenly -> beta = gamma = 0.5, omega = lambda = (0.5, 0.5),
+    R_size = 0.5 * 0.5 * 100 * 100 * (0.25 + 0.25) = 1250."""
+    assert oracle.eq8_from_counts([25, 25], [25, 25], 100, 100) == 1250
+
 
 def test_eq8_single_reducer_is_the_cartesian_product():
-    """k = 1 Reducer: omega_1 = lambda_1 = 1, so R_size = |S| |T| (the Cartesian
-    allocation the paper starts from)."""
+    """SPEC.md:323 / PAPER.md:197: one Reducer holding everything, no filtering ->
+    R_size = |S| |T| (the Cartesian allocation the paper starts from)."""
+    assert oracle.eq8_from_counts([70], [30], 70, 30) == 70 * 30
     R, S = gen.c1(n=500, D=50)
     assert oracle.eq8_rsize(R, S, 0) == len(R) * len(S)
 
 
+def test_eq8_degenerate_and_filter_ratios():
+    """|S| = 0 -> 0; a filter keeping beta of S scales the bound by beta:
+    with one Reducer, R_size = (beta |S|) (gamma |T|)."""
+    assert oracle.eq8_from_counts([0, 0], [5, 5], 0, 10) == 0
+    assert oracle.eq8_from_counts([10], [4], 40, 16) == 10 * 4
+    # uneven split, hand-evaluated: s = (30, 10), t = (5, 15), |S| = 80, |T| = 40:
+    # beta = 1/2, gamma = 1/2, omega = (3/4, 1/4), lambda = (1/4, 3/4)
+    # R_size = 1/2 * 1/2 * 80 * 40 * (3/16 + 3/16) = 800 * 3/8 = 300
+    assert oracle.eq8_from_counts([30, 10], [5, 15], 80, 40) == 300
+
+
+def test_eq8_bounds_random_8_reducer_splits():
+    """for 200 random instances split over 8 Reducers by an arbitrary map
+    that keeps equal keys together, R_size >= the actual join count (O5): each Reducer's
+    Cartesian product contains its share of the join."""
+    rng = np.random.default_rng(8)
+    for _ in range(200):
+        R = rng.integers(0, 60, rng.integers(1, 300)).astype(np.int32)
+        S = rng.integers(0, 60, rng.integers(1, 300)).astype(np.int32)
+        table = rng.integers(0, 8, 60)  # an arbitrary key -> Reducer map
+        e = oracle.eq8_rsize(R, S, 3, reducer_of=lambda K: table[np.asarray(K)])
+        # brute force: per Reducer, count tuples of each side by looping
+        brute = sum(sum(1 for r in R if table[r] == i) * sum(1 for s in S if table[s] == i) for i in range(8))
+        assert e == brute >= oracle.equi_count_hist(R, S)
+
+
 @pytest.mark.parametrize("dtype", [np.int32, np.int64])
 def test_eq8_bounds_the_join_and_shrinks_with_more_reducers(dtype):
-    """sum_i |S_i||T_i| >= sum_k cntR(k) cntS(k) = |J| (equal keys share a Reducer),
-    and splitting a Reducer never increases it ((a+b)(c+d) >= ac+bd)."""
+    """At the product's partition map: sum_i |S_i||T_i| >= |J| (equal keys share a
+    Reducer), and splitting a Reducer never increases it ((a+b)(c+d) >= ac+bd)."""
     rng = np.random.default_rng(5)
     R = rng.integers(-3000, 3000, 4000).astype(dtype)
     S = rng.integers(-3000, 3000, 5000).astype(dtype)
@@ -230,23 +278,6 @@ def test_eq8_bounds_the_join_and_shrinks_with_more_reducers(dtype):
         if prev is not None:
             assert e <= prev
         prev = e
-
-
-def test_eq8_brute_force_partition_sums():
-    """Tiny inputs: the per-Reducer products recomputed with Python loops over a
-    partition map written out bit by bit (hi 32 bits of the 64-bit product, top b bits)."""
-    R = np.array([3, 1, 3, 7, -2, 9, 9], dtype=np.int32)
-    S = np.array([3, 5, 3, -2, 7, 7, 100, 1], dtype=np.int32)
-    for b in (1, 2, 3, 5):
-        def part(k):
-            x = k & 0xFFFFFFFF
-            h = ((x * 0x9E3779B97F4A7C15) & (2**64 - 1)) >> 32
-            return h >> (32 - b)
-        tot = 0
-        for p in range(1 << b):
-            tot += sum(part(int(r)) == p for r in R) * sum(part(int(s)) == p for s in S)
-        assert oracle.eq8_rsize(R, S, b) == tot
-
 
 
 # ---- O10: late materialisation (PAPER.md:141)

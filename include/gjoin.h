@@ -168,14 +168,30 @@ gj_status join_materialize(gj_ctx* ctx, gj_rel R, gj_rel S, uint32_t* out, uint6
 
 /* ---------------------------------------------------------------- theta join
  * Tiled nested-loop join (§3.3.1; theta = NLJ with a predicate,
- * PAPER.md:302 §4.2).  Every (R, S) pair is compared once per pass: R tiles are
- * held in registers, S tiles are staged into shared memory by 1-D TMA bulk copies.
+ * PAPER.md:302 §4.2).  By default (GJ_OPT_THETA_REGIONS = 1) both relations are
+ * range-partitioned into equal-width key buckets and only the region matrix's Red
+ * cells (gj_region_classify) are compared -- R tiles held in registers, S tiles
+ * staged into shared memory by 1-D TMA bulk copies -- Green cells are written as
+ * cross products and White cells skipped; with GJ_OPT_THETA_REGIONS = 0 every
+ * (R, S) pair is compared once per pass.
  * op in gj_op; eps used only by GJ_BAND.
  * theta_join_count: *n_out = |J(R,S,op)|; synchronises; caches per-unit offsets.
  * theta_join_materialize: writes |J| pairs (same cache/ERANGE rules as above). */
 gj_status theta_join_count(gj_ctx* ctx, gj_rel R, gj_rel S, int op, uint64_t eps, uint64_t* n_out);
 gj_status theta_join_materialize(gj_ctx* ctx, gj_rel R, gj_rel S, int op, uint64_t eps,
                                  uint32_t* out, uint64_t capacity, uint64_t* n_written);
+
+/* Region-matrix cell classes (§4.2 Fig. 9 and Alg.3; the function the theta
+ * path uses to choose which cells the NLJ visits): for k equal-width key buckets
+ * shared by both relations, cls[x*k + y] (host, k*k bytes) = class of the cell
+ * (R bucket x, S bucket y) for R.key OP S.key: 0 White (no pair can match; skipped),
+ * 1 Red (compared by the tiled NLJ), 2 Green (every pair matches; written as a cross
+ * product).  <, <=: x < y Green, x == y Red, x > y White; >, >=: mirrored; !=:
+ * off-diagonal Green; =: diagonal Red, rest White; GJ_BAND: |x - y| <= m Red, rest
+ * White, where m = ceil(eps / bucket width) (m is ignored for the other ops).
+ * GJ_EINVAL for an unknown op, k = 0, k > 4096 or cls == NULL. */
+enum { GJ_CELL_WHITE = 0, GJ_CELL_RED = 1, GJ_CELL_GREEN = 2 };
+gj_status gj_region_classify(int op, uint32_t k, uint64_t m, uint8_t* cls);
 
 /* ---------------------------------------------------------------- pre-filter
  * Approximation of the paper's two-round common-key pre-filter (PAPER.md:78-82
@@ -283,12 +299,21 @@ gj_status theta_join_dist_count(gj_ctx* ctx, gj_comm* comm, gj_rel R, gj_rel S, 
 gj_status theta_join_dist_materialize(gj_ctx* ctx, gj_comm* comm, gj_rel R, gj_rel S, int op,
                                       uint64_t eps, uint32_t* out, uint64_t capacity,
                                       uint64_t* n_written);
-/* Host-only shuffle planning (no GPU, no NCCL): given the row-major G x G matrix
- * counts[src*G + dst] of tuples rank src sends to rank dst, writes this rank's
- * receive displacements recv_off[0..G) (exclusive prefix over sources) and returns
- * the number of tuples it receives in *recv_total.  Exposed for host-side tests. */
-gj_status gj_dist_plan(const uint64_t* counts, int nranks, int rank, uint64_t* recv_off,
-                       uint64_t* recv_total);
+/* Host-only receive plan of the equi-join shuffle (no GPU, no NCCL): the exact
+ * function join_dist_count* runs on every rank after the count all-gather, exposed
+ * for host-side tests.  For one relation: counts[(q*G + p)*L + d] = tuples rank q
+ * sends to rank p with local radix digit d (G = nranks <= 8, L = 2^lbits, lbits in
+ * [0, 9]).  Receivers lay their buffers out digit-major: for each digit d, the
+ * senders' runs in rank order (so a shard's received tuples keep sender order, then
+ * input order).  Outputs for rank `rank` (host arrays, caller-owned):
+ *   adj[p*L + d]  (G*L entries): index of this rank's run (p, d) in rank p's receive
+ *                 buffer minus the run's start in this rank's (destination, digit)
+ *                 order, mod 2^32 (the scatter adds it to each tuple's position);
+ *   seg[d]        (L+1 entries): start of digit d in this rank's receive buffer;
+ *   need[p]       (G entries):   tuples rank p receives.
+ * GJ_EINVAL on bad arguments or if some rank would receive >= 2^32 tuples. */
+gj_status gj_dist_plan(const uint64_t* counts, int nranks, int lbits, int rank, uint32_t* adj, uint32_t* seg,
+                       uint64_t* need);
 
 #ifdef __cplusplus
 }

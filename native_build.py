@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC]
-FLAGS += os.environ.get("GJ_NVCC_EXTRA", "").split()  # A/B variants (tools/ab_libs.sh), e.g. -DGJ_HJ_LOAD_BREAK=0
+FLAGS += os.environ.get("GJ_NVCC_EXTRA", "").split()  # extra nvcc flags, e.g. -DNDEBUG
 
 
 def nccl_paths():

@@ -95,7 +95,9 @@ def _load():
     L.join_dist_materialize.argtypes = [vp, vp, _Rel, _Rel, vp, u64, pu64]
     L.theta_join_dist_count.argtypes = [vp, vp, _Rel, _Rel, i32, u64, pu64, pu64]
     L.theta_join_dist_materialize.argtypes = [vp, vp, _Rel, _Rel, i32, u64, vp, u64, pu64]
-    L.gj_dist_plan.argtypes = [pu64, i32, i32, pu64, pu64]
+    L.gj_region_classify.argtypes = [i32, u32, u64, vp]
+    L.gj_region_classify.restype = i32
+    L.gj_dist_plan.argtypes = [pu64, i32, i32, i32, ctypes.POINTER(u32), ctypes.POINTER(u32), pu64]
     for f in ("gj_ctx_create", "gj_ctx_set_stream", "gj_ctx_set_option", "join_count", "join_materialize",
               "theta_join_count", "theta_join_materialize", "prefilter", "join_host", "join_host_batch",
               "gj_comm_unique_id",
@@ -113,7 +115,8 @@ ABI_SYMBOLS = ("gj_ctx_create", "gj_ctx_destroy", "gj_ctx_set_stream", "gj_last_
                "join_materialize", "theta_join_count", "theta_join_materialize", "prefilter", "join_host",
                "join_host_batch",
                "gj_comm_unique_id", "gj_comm_init", "gj_comm_destroy", "join_dist_count", "join_dist_count_filtered",
-               "join_dist_materialize", "theta_join_dist_count", "theta_join_dist_materialize", "gj_dist_plan")
+               "join_dist_materialize", "theta_join_dist_count", "theta_join_dist_materialize", "gj_dist_plan",
+               "gj_region_classify")
 COMM_ID_BYTES = 128
 
 
@@ -338,17 +341,33 @@ def join_host_batch(ctx: Context, batches):
 
 # ---------------------------------------------------------------- multi-GPU (NCCL)
 
-def dist_plan(counts, rank: int):
-    """Host-only shuffle plan (gj_dist_plan): counts = G x G matrix [src][dst].
-    Returns (recv_off list, recv_total)."""
+def region_classify(op: str, k: int, m: int = 0):
+    """Region-matrix cell classes (gj_region_classify, §4.2 Fig. 9): a (k, k)
+    uint8 array, [x, y] = class of (R bucket x, S bucket y): 0 White, 1 Red, 2 Green."""
+    import numpy as np
+    out = np.zeros(k * k, dtype=np.uint8)
+    _check(lib.gj_region_classify(OPS[op], k, m, out.ctypes.data_as(ctypes.c_void_p)))
+    return out.reshape(k, k)
+
+
+def dist_plan(counts, rank: int, lbits: int = 0):
+    """Host-only receive plan of the equi-join shuffle (gj_dist_plan), the function
+    every rank runs on the all-gathered counts.  counts: (G, G, 2^lbits) array,
+    counts[q, p, d] = tuples rank q sends to rank p with local digit d.
+    Returns (adj (G, 2^lbits) uint32, seg (2^lbits + 1) uint32, need (G) uint64)."""
     import numpy as np
     m = np.ascontiguousarray(np.asarray(counts, dtype=np.uint64))
-    G = m.shape[0]
-    off = np.zeros(G, dtype=np.uint64)
-    tot = ctypes.c_uint64()
-    _check(lib.gj_dist_plan(m.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), G, rank,
-                            off.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ctypes.byref(tot)))
-    return off.tolist(), tot.value
+    G, L = m.shape[0], 1 << lbits
+    if m.shape != (G, G, L):
+        raise ValueError("counts must have shape (G, G, 2^lbits)")
+    adj = np.zeros(G * L, dtype=np.uint32)
+    seg = np.zeros(L + 1, dtype=np.uint32)
+    need = np.zeros(G, dtype=np.uint64)
+    P32 = ctypes.POINTER(ctypes.c_uint32)
+    _check(lib.gj_dist_plan(m.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), G, lbits, rank,
+                            adj.ctypes.data_as(P32), seg.ctypes.data_as(P32),
+                            need.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+    return adj.reshape(G, L), seg, need
 
 
 class Comm:

@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "gjoin.h"
@@ -46,6 +48,18 @@ void* ws(gj_ctx* ctx, const char* name, size_t bytes) {
     b.bytes = rounded;
   }
   return b.ptr;
+}
+
+void set_smem_attr(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  GJ_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{kernel, dev}];
+  if (have >= bytes) return;
+  GJ_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  have = bytes;
 }
 
 void* pinned(gj_ctx* ctx, const char* name, size_t bytes) {
@@ -159,6 +173,10 @@ static void check_rel(const gj_rel& X, const char* name) {
     throw Error(GJ_EINVAL, std::string(name) + ": key_type must be GJ_I32 or GJ_I64");
   if (X.n > 0 && X.key == nullptr) throw Error(GJ_EINVAL, std::string(name) + ": key is NULL with n > 0");
   if (X.n >= (1ull << 32)) throw Error(GJ_EINVAL, std::string(name) + ": n must be < 2^32 per call");
+  // element alignment is all the kernels need (bulk copies realign on absolute addresses)
+  const uintptr_t ka = reinterpret_cast<uintptr_t>(X.key), ra = reinterpret_cast<uintptr_t>(X.rid);
+  if (ka % (X.key_type == GJ_I64 ? 8 : 4) || ra % 4)
+    throw Error(GJ_EINVAL, std::string(name) + ": key / rid pointers must be aligned to their element size");
   if (X.rid == nullptr && (uint64_t)X.rid_base + X.n > (1ull << 32))
     throw Error(GJ_EINVAL, std::string(name) + ": rid_base + n exceeds 2^32");
 }
@@ -195,6 +213,7 @@ void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t ski
                      const uint32_t* segR, const uint32_t* segS, cudaEvent_t s_ready) {
   JoinCache& jc = ctx->jc;
   jc = JoinCache{};
+  jc.epoch = ++ctx->epoch_ctr;
   jc.R = R;
   jc.S = S;
   if (R.n == 0 || S.n == 0) {
@@ -250,8 +269,6 @@ gj_status gj_ctx_create(gj_ctx** out, int device, void* stream) {
   int sms = 0;
   GJ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   c->num_sms = sms;
-  c->overlap_shuffle = std::getenv("GJ_NO_OVERLAP") == nullptr;  // A/B experiments
-  if (const char* e = std::getenv("GJ_SHUFFLE_CTAS")) c->shuffle_ctas = (uint32_t)std::atoi(e);
   *out = c;
   API_END
 }
@@ -340,6 +357,10 @@ gj_status gj_gather_payloads(gj_ctx* ctx, const uint32_t* pairs, uint64_t n, con
   API_BEGIN
   if (!ctx) throw Error(GJ_EINVAL, "ctx is NULL");
   if (n && !pairs) throw Error(GJ_EINVAL, "gj_gather_payloads: pairs is NULL");
+  if (reinterpret_cast<uintptr_t>(pairs) % 8 ||
+      (reinterpret_cast<uintptr_t>(payload_R) | reinterpret_cast<uintptr_t>(payload_S) |
+       reinterpret_cast<uintptr_t>(out_R) | reinterpret_cast<uintptr_t>(out_S)) % 4)
+    throw Error(GJ_EINVAL, "gj_gather_payloads: pairs must be 8-byte, payloads and outputs 4-byte aligned");
   if (width_R % 4 || width_S % 4) throw Error(GJ_EINVAL, "gj_gather_payloads: widths must be multiples of 4");
   const void* pR = width_R ? payload_R : nullptr;
   const void* pS = width_S ? payload_S : nullptr;
@@ -422,6 +443,7 @@ gj_status join_materialize(gj_ctx* ctx, gj_rel R, gj_rel S, uint32_t* out, uint6
                                std::to_string(jc.total));
   }
   if (jc.total && !out) throw Error(GJ_EINVAL, "join_materialize: out is NULL");
+  if (reinterpret_cast<uintptr_t>(out) % 8) throw Error(GJ_EINVAL, "join_materialize: out must be 8-byte aligned");
   hash_join_write(ctx, out);
   *n_written = jc.total;
   API_END
@@ -464,6 +486,7 @@ gj_status theta_join_materialize(gj_ctx* ctx, gj_rel R, gj_rel S, int op, uint64
                                std::to_string(tc.total));
   }
   if (tc.total && !out) throw Error(GJ_EINVAL, "theta_join_materialize: out is NULL");
+  if (reinterpret_cast<uintptr_t>(out) % 8) throw Error(GJ_EINVAL, "theta_join_materialize: out must be 8-byte aligned");
   theta_write(ctx, out);
   *n_written = tc.total;
   API_END

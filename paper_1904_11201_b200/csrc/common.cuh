@@ -107,6 +107,34 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+// Bulk-copy window over elements [first, first + cnt) of an array at `base` holding
+// `total` elements of `esz` bytes, computed on ABSOLUTE addresses (so any
+// element-aligned base works, e.g. a tensor view starting at element 1): the copy
+// starts at the 16-byte boundary at or below element `first` -- inside the same
+// 16-byte block, hence the same page, so the few bytes before the array it may
+// cover can never fault -- and ends at min(ceil16(end of the range), floor16(end of
+// the array)).  Element first + i sits at dst[shift + i]; elements [first + valid,
+// first + cnt) lie past the window and must be read directly.
+struct Win {
+  const uint8_t* src;
+  uint32_t bytes;  // multiple of 16; 0 = nothing to copy
+  uint32_t shift;
+  uint32_t valid;
+};
+__device__ __forceinline__ Win bulk_window(const void* base, uint64_t first, uint32_t cnt, uint32_t esz,
+                                           uint64_t total) {
+  const uint64_t b = reinterpret_cast<uint64_t>(base);
+  const uint64_t s0 = b + first * esz, s1 = b + (first + cnt) * esz, e = b + total * esz;
+  const uint64_t a0 = s0 & ~15ull;
+  const uint64_t a1 = min((s1 + 15) & ~15ull, e & ~15ull);
+  Win w;
+  w.src = reinterpret_cast<const uint8_t*>(a0);
+  w.bytes = a1 > a0 ? (uint32_t)(a1 - a0) : 0u;
+  w.shift = (uint32_t)((s0 - a0) / esz);
+  w.valid = a1 > s0 ? (uint32_t)min((uint64_t)cnt, (a1 - s0) / esz) : 0u;
+  return w;
+}
+
 // Binary search: largest i in [0, n) with a[i] <= x (a ascending, a[0] <= x).
 template <typename T>
 __device__ __forceinline__ uint32_t upper_index(const T* __restrict__ a, uint32_t n, T x) {

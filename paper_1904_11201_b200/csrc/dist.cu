@@ -2,10 +2,12 @@
 //
 // Equi join: the paper's Hadoop shuffle ("emit
 // (join_key/a, tagged tuple)" then shuffle by key, Alg.1) becomes
-//   1. a radix pass over each local shard by the top log2(G) bits of the key hash
-//      (the destination rank), writing SoA (key, rid) buckets;
-//   2. ncclAllGather of every rank's 2G bucket sizes (R and S);
-//   3. grouped ncclSend/ncclRecv of the buckets (all-to-all-v over NVLink);
+//   1. a histogram of each local shard by the top log2(G) bits of the key hash
+//      (the destination rank);
+//   2. ncclAllGather of every rank's run counts; every rank computes the same
+//      receive plan (plan_shuffle);
+//   3. the scatter kernel of that radix pass stores every (key, rid) straight into
+//      its owner's receive buffer over NVLink (CUDA-IPC peer memory);
 //   4. the single-GPU partitioned hash join on what arrived, skipping the hash bits
 //      the shuffle consumed.  Each pair is produced on exactly one rank (the owner
 //      of its key's hash bucket); rids are global (shard rid_base / rid maps).
@@ -54,9 +56,12 @@ struct gj_comm {
   uint64_t cap[gj::MAX_RANKS][2] = {};
   size_t cap_ks = 0;  // key width the receive buffers were sized for
   bool mapped = false;
-  bool fused = true;  // shuffle fused into the scatter over NVLink (else NCCL send/recv)
-  // cache of the last dist count (for materialize)
+  // cache of the last dist count (for materialize): valid only while the ctx's
+  // join / theta cache still holds that count (same ctx, same fill epoch) -- a
+  // single-GPU call on the ctx in between replaces the ctx cache and bumps the epoch
   bool eq_valid = false, th_valid = false;
+  const gj_ctx* ctx = nullptr;
+  uint64_t eq_epoch = 0, th_epoch = 0;
   gj_rel R{}, S{};
   int op = 0;
   uint64_t eps = 0;
@@ -98,6 +103,40 @@ uint32_t log2_exact(int G) {
   return g;
 }
 
+// Receive plan of the fused shuffle for one relation (host only; every rank computes
+// the same plan from the all-gathered count matrix).  counts[(q*G + p)*L + d] =
+// tuples rank q sends to rank p with local digit d (L = 2^lbits).  Receivers lay
+// their buffers out digit-major: for each local digit d, the senders' runs in rank
+// order.  Outputs for rank `me`: adj[p*L + d] = (index of my run (p, d) in rank p's
+// buffer) - (the run's start in my own digit order), mod 2^32 (the scatter adds it
+// to the sender-side position); seg[d] (L + 1 entries) = start of local digit d in
+// my receive buffer; need[p] = tuples rank p receives.
+void plan_shuffle(const uint64_t* counts, int G, uint32_t lbits, int me, uint32_t* adj, uint32_t* seg,
+                  uint64_t* need) {
+  const uint32_t L = 1u << lbits;
+  auto cnt = [&](int q, int p, uint32_t d) { return counts[((size_t)q * G + p) * L + d]; };
+  for (int p = 0; p < G; ++p) {
+    need[p] = 0;
+    for (int q = 0; q < G; ++q)
+      for (uint32_t d = 0; d < L; ++d) need[p] += cnt(q, p, d);
+  }
+  for (int p = 0; p < G; ++p)  // every rank sees the whole matrix: all ranks fail together
+    if (need[p] >= (1ull << 32)) throw Error(GJ_EINVAL, "a rank would receive >= 2^32 tuples; use more ranks");
+  uint64_t local = 0;  // start of my run (p, d) in my own (destination, digit) order
+  for (int p = 0; p < G; ++p) {
+    uint64_t at = 0;  // start of digit d in rank p's receive buffer
+    for (uint32_t d = 0; d < L; ++d) {
+      uint64_t mine_at = at;
+      for (int q = 0; q < me; ++q) mine_at += cnt(q, p, d);
+      adj[((size_t)p << lbits) + d] = (uint32_t)(mine_at - local);
+      if (p == me) seg[d] = (uint32_t)at;
+      for (int q = 0; q < G; ++q) at += cnt(q, p, d);
+      local += cnt(me, p, d);
+    }
+    if (p == me) seg[L] = (uint32_t)at;
+  }
+}
+
 #ifdef GJ_HAVE_NCCL
 // allreduce of one uint64 (host in, host out)
 uint64_t allreduce_sum(gj_ctx* ctx, gj_comm* c, uint64_t v) {
@@ -107,104 +146,6 @@ uint64_t allreduce_sum(gj_ctx* ctx, gj_comm* c, uint64_t v) {
   uint64_t out = 0;
   d2h_sync(ctx, &out, d + 1, 8);
   return out;
-}
-
-void dist_equi_count(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) {
-  const int G = c->nranks;
-  const uint32_t g = log2_exact(G);
-  const size_t ks = R.key_type == GJ_I64 ? 8 : 4;
-  const ncclDataType_t kt = R.key_type == GJ_I64 ? ncclInt64 : ncclInt32;
-  // 1. bucket both shards by destination rank (one radix pass of g bits)
-  Partitioned PR = radix_partition(ctx, R, g, "dR", 0);
-  Partitioned PS = radix_partition(ctx, S, g, "dS", 0);
-  unsigned long long* cnt = static_cast<unsigned long long*>(ws(ctx, "dist.cnt", (2 * G + 2 * G * G) * 8));
-  unsigned long long* all = cnt + 2 * G;
-  if (g == 0) {
-    GJ_CUDA(cudaMemcpyAsync(cnt, &R.n, 8, cudaMemcpyHostToDevice, ctx->stream));
-    GJ_CUDA(cudaMemcpyAsync(cnt + 1, &S.n, 8, cudaMemcpyHostToDevice, ctx->stream));
-  } else {
-    launch(ctx, "bucket_counts", bucket_counts, dim3(1), dim3(32), 0, PR.off, (uint32_t)G, cnt);
-    launch(ctx, "bucket_counts", bucket_counts, dim3(1), dim3(32), 0, PS.off, (uint32_t)G, cnt + G);
-  }
-  // 2. every rank learns the full count matrices
-  GJ_NCCL(ncclAllGather(cnt, all, 2 * G, ncclUint64, c->comm, ctx->stream));
-  std::vector<unsigned long long> M(2 * G * G);
-  d2h_sync(ctx, M.data(), all, M.size() * 8);
-  auto sent = [&](int src, int rel, int dst) { return (uint64_t)M[(size_t)src * 2 * G + rel * G + dst]; };
-  uint64_t nrecv[2] = {0, 0};
-  std::vector<uint64_t> roff[2] = {std::vector<uint64_t>(G), std::vector<uint64_t>(G)};
-  std::vector<uint64_t> soff[2] = {std::vector<uint64_t>(G), std::vector<uint64_t>(G)};
-  for (int rel = 0; rel < 2; ++rel) {
-    for (int p = 0; p < G; ++p) {
-      roff[rel][p] = nrecv[rel];
-      nrecv[rel] += sent(p, rel, c->rank);
-    }
-    uint64_t s = 0;
-    for (int p = 0; p < G; ++p) {
-      soff[rel][p] = s;
-      s += sent(c->rank, rel, p);
-    }
-  }
-  for (int p = 0; p < G; ++p) {  // checked for every rank so that all ranks fail together
-    uint64_t in[2] = {0, 0};
-    for (int q = 0; q < G; ++q) in[0] += sent(q, 0, p), in[1] += sent(q, 1, p);
-    if (in[0] >= (1ull << 32) || in[1] >= (1ull << 32))
-      throw Error(GJ_EINVAL, "a rank would receive >= 2^32 tuples; use more ranks");
-  }
-  // 3. all-to-all-v of the (key, rid) buckets
-  uint8_t* rk[2] = {static_cast<uint8_t*>(ws(ctx, "dist.R.key", nrecv[0] * ks)),
-                    static_cast<uint8_t*>(ws(ctx, "dist.S.key", nrecv[1] * ks))};
-  uint32_t* rr[2] = {static_cast<uint32_t*>(ws(ctx, "dist.R.rid", nrecv[0] * 4)),
-                     static_cast<uint32_t*>(ws(ctx, "dist.S.rid", nrecv[1] * 4))};
-  const Partitioned* Ps[2] = {&PR, &PS};
-  const gj_rel* Xs[2] = {&R, &S};
-  // with g == 0 the "partitioned" view is the caller's relation: materialise rids
-  const uint32_t* srid[2];
-  for (int rel = 0; rel < 2; ++rel) {
-    srid[rel] = Ps[rel]->rid;
-    if (srid[rel] == nullptr) {
-      uint32_t* tmp = static_cast<uint32_t*>(ws(ctx, rel ? "dist.S.srid" : "dist.R.srid", Xs[rel]->n * 4));
-      launch(ctx, "fill_rids", fill_rids, dim3(std::max<uint32_t>(1, (uint32_t)std::min<uint64_t>((Xs[rel]->n + 255) / 256, 4096))),
-             dim3(256), 0, tmp, Xs[rel]->n, Xs[rel]->rid_base);
-      srid[rel] = tmp;
-    }
-  }
-  {
-    // the bucket a rank keeps never crosses NVLink: a device-local copy
-    RegionScope rs(ctx, "shuffle_self_copy");
-    for (int rel = 0; rel < 2; ++rel) {
-      const uint64_t nk = sent(c->rank, rel, c->rank);
-      if (!nk) continue;
-      GJ_CUDA(cudaMemcpyAsync(rk[rel] + roff[rel][c->rank] * ks,
-                              static_cast<const uint8_t*>(Ps[rel]->key) + soff[rel][c->rank] * ks, nk * ks,
-                              cudaMemcpyDeviceToDevice, ctx->stream));
-      GJ_CUDA(cudaMemcpyAsync(rr[rel] + roff[rel][c->rank], srid[rel] + soff[rel][c->rank], nk * 4,
-                              cudaMemcpyDeviceToDevice, ctx->stream));
-    }
-  }
-  {
-    RegionScope rs(ctx, "nccl_shuffle");
-    GJ_NCCL(ncclGroupStart());
-    for (int rel = 0; rel < 2; ++rel) {
-      const uint8_t* skey = static_cast<const uint8_t*>(Ps[rel]->key);
-      for (int p = 0; p < G; ++p) {
-        if (p == c->rank) continue;
-        const uint64_t ns = sent(c->rank, rel, p), nr = sent(p, rel, c->rank);
-        if (ns) {
-          GJ_NCCL(ncclSend(skey + soff[rel][p] * ks, ns, kt, p, c->comm, ctx->stream));
-          GJ_NCCL(ncclSend(srid[rel] + soff[rel][p], ns, ncclUint32, p, c->comm, ctx->stream));
-        }
-        if (nr) {
-          GJ_NCCL(ncclRecv(rk[rel] + roff[rel][p] * ks, nr, kt, p, c->comm, ctx->stream));
-          GJ_NCCL(ncclRecv(rr[rel] + roff[rel][p], nr, ncclUint32, p, c->comm, ctx->stream));
-        }
-      }
-    }
-    GJ_NCCL(ncclGroupEnd());
-  }
-  // 4. local partitioned hash join of what arrived (top g hash bits are now constant)
-  gj_rel RL{rk[0], rr[0], nrecv[0], R.key_type, 0}, SL{rk[1], rr[1], nrecv[1], S.key_type, 0};
-  join_count_core(ctx, RL, SL, g, 0, nullptr, nullptr, nullptr);
 }
 
 // Fused shuffle: ONE radix pass by (destination rank, first local digit) -- the top
@@ -257,18 +198,21 @@ void fused_shuffle(gj_ctx* ctx, gj_comm* c, const gj_rel* const X[2], uint32_t b
   for (int q = 0; q < G; ++q)
     if (M[(size_t)q * row + 2 * D1] != ks32) throw Error(GJ_EINVAL, "ranks disagree on the key type");
   // cnt(q, rel, p, d): tuples of relation rel that rank q sends to rank p, local digit d
-  auto cntq = [&](int q, int rel, int p, uint32_t d) -> uint64_t {
-    return M[(size_t)q * row + (size_t)rel * D1 + ((size_t)p << b1) + d];
-  };
+  std::vector<uint64_t> cm[2];
+  for (int rel = 0; rel < 2; ++rel) {
+    cm[rel].resize((size_t)G * D1);
+    for (int q = 0; q < G; ++q)
+      for (uint32_t x = 0; x < D1; ++x) cm[rel][(size_t)q * D1 + x] = M[(size_t)q * row + (size_t)rel * D1 + x];
+  }
   auto& need = out.need;
-  for (int p = 0; p < G; ++p) need[p][0] = need[p][1] = 0;
-  for (int q = 0; q < G; ++q)
-    for (int rel = 0; rel < 2; ++rel)
-      for (int p = 0; p < G; ++p)
-        for (uint32_t d = 0; d < L1; ++d) need[p][rel] += cntq(q, rel, p, d);
-  for (int p = 0; p < G; ++p)  // every rank sees the whole matrix: all ranks fail together
-    if (need[p][0] >= (1ull << 32) || need[p][1] >= (1ull << 32))
-      throw Error(GJ_EINVAL, "a rank would receive >= 2^32 tuples; use more ranks");
+  const size_t tab_n = (size_t)D1 + L1 + 1;  // adj[D1] | seg[L1 + 1]
+  uint32_t* htab[2];
+  for (int rel = 0; rel < 2; ++rel) {
+    htab[rel] = static_cast<uint32_t*>(pinned(ctx, rel ? "dist.tab.S" : "dist.tab.R", tab_n * 4));
+    uint64_t nd[MAX_RANKS];
+    plan_shuffle(cm[rel].data(), G, b1, me, htab[rel], htab[rel] + D1, nd);
+    for (int p = 0; p < G; ++p) need[p][rel] = nd[p];
+  }
   // grow every rank's capacity the same way on every rank (25% headroom); a new key
   // width reallocates the key buffers, so it also forces a handle exchange
   bool grew = !c->mapped || c->cap_ks != ks;
@@ -323,28 +267,9 @@ void fused_shuffle(gj_ctx* ctx, gj_comm* c, const gj_rel* const X[2], uint32_t b
       GJ_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev[0], 0));
       ctx->stream = ctx->aux;
     }
-    // adj[dg] = (index of my run dg in its receiver's buffer) - (its start in my
-    // digit order); seg[d] = start of local digit d in MY receive buffer
-    const size_t tab_n = (size_t)D1 + L1 + 1;
     const char* tn = rel ? "dist.tab.S" : "dist.tab.R";
-    uint32_t* htab = static_cast<uint32_t*>(pinned(ctx, tn, tab_n * 4));
-    uint32_t* adj = htab;
-    uint32_t* seg = htab + D1;
-    uint64_t local = 0;
-    for (int p = 0; p < G; ++p) {
-      uint64_t at = 0;  // start of digit d in rank p's receive buffer
-      for (uint32_t d = 0; d < L1; ++d) {
-        uint64_t mine_at = at;
-        for (int q = 0; q < me; ++q) mine_at += cntq(q, rel, p, d);
-        adj[((size_t)p << b1) + d] = (uint32_t)(mine_at - local);
-        if (p == me) seg[d] = (uint32_t)at;
-        for (int q = 0; q < G; ++q) at += cntq(q, rel, p, d);
-        local += cntq(me, rel, p, d);
-      }
-      if (p == me) seg[L1] = (uint32_t)at;
-    }
     uint32_t* dtab = static_cast<uint32_t*>(ws(ctx, tn, tab_n * 4));
-    GJ_CUDA(cudaMemcpyAsync(dtab, htab, tab_n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    GJ_CUDA(cudaMemcpyAsync(dtab, htab[rel], tab_n * 4, cudaMemcpyHostToDevice, ctx->stream));
     ShuffleDest dst{};
     for (int p = 0; p < G; ++p) {
       dst.key[p] = p == me ? bufs[2 * rel] : c->peer_ptr[p][2 * rel];
@@ -487,10 +412,9 @@ void dist_equi_count_filtered(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj
 }
 
 void equi_count_any(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) {
-  const char* env = std::getenv("GJ_SHUFFLE");  // "nccl" forces the send/recv path
-  const bool fused = c->fused && !(env && std::string(env) == "nccl") && c->nranks > 1 && c->nranks <= MAX_RANKS;
-  if (fused) dist_equi_count_fused(ctx, c, R, S);
-  else dist_equi_count(ctx, c, R, S);
+  if (c->nranks > MAX_RANKS) throw Error(GJ_EINVAL, "the equi-join shuffle supports at most 8 ranks (one NVLink box)");
+  if (c->nranks == 1) join_count_core(ctx, R, S, 0, 0, nullptr, nullptr, nullptr);
+  else dist_equi_count_fused(ctx, c, R, S);
 }
 
 // Gathers the shards of `members` (ranks, ascending) of relation X into one buffer
@@ -654,16 +578,13 @@ using namespace gj;
 
 extern "C" {
 
-gj_status gj_dist_plan(const uint64_t* counts, int nranks, int rank, uint64_t* recv_off, uint64_t* recv_total) {
+gj_status gj_dist_plan(const uint64_t* counts, int nranks, int lbits, int rank, uint32_t* adj, uint32_t* seg,
+                       uint64_t* need) {
   DAPI_BEGIN
-  if (!counts || !recv_off || !recv_total || nranks < 1 || rank < 0 || rank >= nranks)
+  if (!counts || !adj || !seg || !need || nranks < 1 || nranks > MAX_RANKS || rank < 0 || rank >= nranks ||
+      lbits < 0 || lbits > 9)
     throw Error(GJ_EINVAL, "gj_dist_plan: bad arguments");
-  uint64_t s = 0;
-  for (int p = 0; p < nranks; ++p) {
-    recv_off[p] = s;
-    s += counts[(size_t)p * nranks + rank];
-  }
-  *recv_total = s;
+  plan_shuffle(counts, nranks, (uint32_t)lbits, rank, adj, seg, need);
   DAPI_END
 }
 
@@ -710,6 +631,10 @@ static void check_args(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S
     throw Error(GJ_EINVAL, "R and S key types must agree (GJ_I32 or GJ_I64)");
   if ((R.n && !R.key) || (S.n && !S.key)) throw Error(GJ_EINVAL, "NULL key with n > 0");
   if (R.n >= (1ull << 32) || S.n >= (1ull << 32)) throw Error(GJ_EINVAL, "shard n must be < 2^32");
+  const size_t ks = R.key_type == GJ_I64 ? 8 : 4;
+  if (reinterpret_cast<uintptr_t>(R.key) % ks || reinterpret_cast<uintptr_t>(S.key) % ks ||
+      reinterpret_cast<uintptr_t>(R.rid) % 4 || reinterpret_cast<uintptr_t>(S.rid) % 4)
+    throw Error(GJ_EINVAL, "key / rid pointers must be aligned to their element size");
 }
 
 gj_status join_dist_count(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, uint64_t* n_local, uint64_t* n_global) {
@@ -723,6 +648,8 @@ gj_status join_dist_count(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, uint64_t*
   c->S = S;
   c->total = ctx->jc.total;
   c->eq_valid = true;
+  c->ctx = ctx;
+  c->eq_epoch = ctx->jc.epoch;
   *n_local = ctx->jc.total;
   *n_global = allreduce_sum(ctx, c, ctx->jc.total);
   trace_mark("join_dist_count end");
@@ -745,6 +672,8 @@ gj_status join_dist_count_filtered(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, 
   c->S = S;
   c->total = ctx->jc.total;
   c->eq_valid = true;
+  c->ctx = ctx;
+  c->eq_epoch = ctx->jc.epoch;
   *n_local = ctx->jc.total;
   *n_global = allreduce_sum(ctx, c, ctx->jc.total);
   if (kept_local) {
@@ -759,17 +688,21 @@ gj_status join_dist_materialize(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, uin
   DAPI_BEGIN
   check_args(ctx, c, R, S);
   if (!n_written) throw Error(GJ_EINVAL, "NULL n_written");
-  if (!(c->eq_valid && same_rel(c->R, R) && same_rel(c->S, S) && ctx->jc.valid)) {
+  if (!(c->eq_valid && same_rel(c->R, R) && same_rel(c->S, S) && ctx->jc.valid && c->ctx == ctx &&
+        c->eq_epoch == ctx->jc.epoch)) {
     equi_count_any(ctx, c, R, S);
     c->R = R;
     c->S = S;
     c->eq_valid = true;
+    c->ctx = ctx;
+    c->eq_epoch = ctx->jc.epoch;
   }
   if (capacity < ctx->jc.total) {
     *n_written = ctx->jc.total;
     throw Error(GJ_ERANGE, "join_dist_materialize: capacity < local |J|");
   }
   if (ctx->jc.total && !out) throw Error(GJ_EINVAL, "NULL out");
+  if (reinterpret_cast<uintptr_t>(out) % 8) throw Error(GJ_EINVAL, "out must be 8-byte aligned");
   hash_join_write(ctx, out);
   *n_written = ctx->jc.total;
   DAPI_END
@@ -788,6 +721,8 @@ gj_status theta_join_dist_count(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, int
   c->op = op;
   c->eps = eps;
   c->th_valid = true;
+  c->ctx = ctx;
+  c->th_epoch = ctx->tc.epoch;
   *n_local = ctx->tc.total;
   *n_global = allreduce_sum(ctx, c, ctx->tc.total);
   DAPI_END
@@ -799,19 +734,23 @@ gj_status theta_join_dist_materialize(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel 
   check_args(ctx, c, R, S);
   if (op < GJ_EQ || op > GJ_BAND) throw Error(GJ_EINVAL, "unknown op");
   if (!n_written) throw Error(GJ_EINVAL, "NULL n_written");
-  if (!(c->th_valid && same_rel(c->R, R) && same_rel(c->S, S) && c->op == op && c->eps == eps && ctx->tc.valid)) {
+  if (!(c->th_valid && same_rel(c->R, R) && same_rel(c->S, S) && c->op == op && c->eps == eps && ctx->tc.valid &&
+        c->ctx == ctx && c->th_epoch == ctx->tc.epoch)) {
     dist_theta_count(ctx, c, R, S, op, eps);
     c->R = R;
     c->S = S;
     c->op = op;
     c->eps = eps;
     c->th_valid = true;
+    c->ctx = ctx;
+    c->th_epoch = ctx->tc.epoch;
   }
   if (capacity < ctx->tc.total) {
     *n_written = ctx->tc.total;
     throw Error(GJ_ERANGE, "theta_join_dist_materialize: capacity < local |J|");
   }
   if (ctx->tc.total && !out) throw Error(GJ_EINVAL, "NULL out");
+  if (reinterpret_cast<uintptr_t>(out) % 8) throw Error(GJ_EINVAL, "out must be 8-byte aligned");
   theta_write(ctx, out);
   *n_written = ctx->tc.total;
   DAPI_END

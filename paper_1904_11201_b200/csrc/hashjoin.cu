@@ -30,11 +30,6 @@
 namespace gj {
 namespace {
 
-#ifndef GJ_HJ_LOAD_BREAK
-// int32 key prefetch stops at the unit's end (uniform branch) instead of predicating:
-// C2 hj_count 0.835 -> 0.808 ms; the int64 kernel measured 0.830 -> 0.885 ms with it
-#define GJ_HJ_LOAD_BREAK 1
-#endif
 
 constexpr int HT = 512;            // threads per CTA
 constexpr int HW = HT / 32;        // warps per CTA (counts are kept per (unit, warp))
@@ -181,9 +176,9 @@ __device__ __forceinline__ void load_keys(UnitKeys<K>& R, const uint4 d, const H
   const K* __restrict__ pkey = static_cast<const K*>(a.pkey);
 #pragma unroll
   for (int j = 0; j < BPT; ++j) {
-#if GJ_HJ_LOAD_BREAK
-    if (sizeof(K) == 4 && (uint32_t)j * HT >= d.y) break;  // CTA-uniform: no predicated-off loads past the unit
-#endif
+    // int32: stop at the unit's end (CTA-uniform branch) instead of predicating off
+    // loads sized for the maximum (C2 0.835 -> 0.808 ms; int64 measured slower with it)
+    if (sizeof(K) == 4 && (uint32_t)j * HT >= d.y) break;
     const uint32_t i = tid + j * HT;
     R.kb[j] = i < d.y ? bkey[d.x + i] : K(0);
   }
@@ -191,9 +186,7 @@ __device__ __forceinline__ void load_keys(UnitKeys<K>& R, const uint4 d, const H
   probe_range(d.w, w, wb, we);
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
-#if GJ_HJ_LOAD_BREAK
     if (sizeof(K) == 4 && wb + 32 * j >= we) break;  // warp-uniform
-#endif
     const uint32_t i = wb + lane + 32 * j;
     R.kp[j] = i < we ? pkey[d.z + i] : K(0);
   }
@@ -206,38 +199,14 @@ __device__ __forceinline__ uint32_t table_logT(uint32_t bn) {
   return min(want, (uint32_t)(31 - __clz(TAB_MAX)));
 }
 
-struct Win {  // aligned copy window of elements [first, first + cnt) of an array
-  uint64_t a0;     // window start (bytes)
-  uint32_t bytes;  // window length (bytes, multiple of 16; 0 = nothing to copy)
-  uint32_t shift;  // element `first` sits at dst[shift]
-  uint32_t valid;  // elements [first, first + valid) are inside the window
-};
-__device__ __forceinline__ Win window(uint64_t first, uint32_t cnt, uint32_t esz, uint64_t total) {
-  Win w;
-  const uint64_t b0 = first * esz, b1 = (first + cnt) * esz;
-  w.a0 = b0 & ~15ull;
-  const uint64_t a1 = min((b1 + 15) & ~15ull, (total * esz) & ~15ull);
-  w.bytes = a1 > w.a0 ? (uint32_t)(a1 - w.a0) : 0u;
-  w.shift = (uint32_t)((b0 - w.a0) / esz);
-  w.valid = a1 > b0 ? (uint32_t)min((uint64_t)cnt, (a1 - b0) / esz) : 0u;
-  return w;
-}
-
 // Count pass.  Per probe row it also records the matching build index inside the
 // unit's build chunk (uint16; NO_MATCH / MULTI sentinels), so the write pass can
 // emit pairs without rebuilding the table (units holding a MULTI row are flagged
 // and re-probed by the write pass).
 constexpr uint16_t NO_MATCH = 0xFFFF, MULTI = 0xFFFE;
 
-// GJ_HJ_COUNT_MINB > 1: register budget for that many int32 CTAs per SM (an explicit
-// minimum of 1 is not the same as none: ptxas then spends 72 registers instead of 54)
-#if defined(GJ_HJ_COUNT_MINB) && GJ_HJ_COUNT_MINB > 1
-#define GJ_HJ_COUNT_BOUNDS(K) __launch_bounds__(HT, sizeof(K) == 4 ? GJ_HJ_COUNT_MINB : 1)
-#else
-#define GJ_HJ_COUNT_BOUNDS(K) __launch_bounds__(HT)
-#endif
 template <typename K>
-__global__ void GJ_HJ_COUNT_BOUNDS(K) hj_count_kernel(HJArgs a, uint16_t* __restrict__ stage,
+__global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __restrict__ stage,
                                                       uint8_t* __restrict__ multi,
                                                       unsigned long long* __restrict__ nmulti) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -317,118 +286,6 @@ __global__ void GJ_HJ_COUNT_BOUNDS(K) hj_count_kernel(HJArgs a, uint16_t* __rest
     cur = nxt;
     d = dn;
     dn = dnn;
-  }
-}
-
-// Count pass, TMA-fed variant: the next unit's build and probe keys are streamed
-// into a second shared-memory buffer by 1-D TMA bulk copies (16-byte aligned
-// windows; elements outside a window read from global memory) while this unit is
-// built and probed, so the key loads never sit on the critical path (the
-// register-prefetch variant above waited on them at every unit boundary).
-template <typename K>
-struct CBuf {
-  K bk[BCH_MAX + 16 / sizeof(K)];
-  K pk[PCH_MAX + 16 / sizeof(K)];
-};
-
-template <typename K>
-__device__ __forceinline__ void cnt_issue(CBuf<K>& B, uint64_t* bar, const uint4 d, const HJArgs& a) {
-  fence_proxy_async();
-  const Win wb = window(d.x, d.y, sizeof(K), a.nb);
-  const Win wp = window(d.z, d.w, sizeof(K), a.np);
-  const uint32_t bytes = wb.bytes + wp.bytes;
-  if (!bytes) {
-    mbar_arrive(bar);
-    return;
-  }
-  mbar_expect_tx(bar, bytes);
-  if (wb.bytes) bulk_g2s(B.bk, reinterpret_cast<const uint8_t*>(a.bkey) + wb.a0, wb.bytes, bar);
-  if (wp.bytes) bulk_g2s(B.pk, reinterpret_cast<const uint8_t*>(a.pkey) + wp.a0, wp.bytes, bar);
-}
-
-template <typename K>
-__global__ void __launch_bounds__(HT) hj_count_tma(HJArgs a, uint16_t* __restrict__ stage,
-                                                   uint8_t* __restrict__ multi,
-                                                   unsigned long long* __restrict__ nmulti) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint32_t s_dup;
-  CBuf<K>* B = reinterpret_cast<CBuf<K>*>(smem);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * sizeof(CBuf<K>));
-  Table<K> tab;
-  tab.init(smem + 2 * sizeof(CBuf<K>) + 16);
-  const K* __restrict__ bkey = static_cast<const K*>(a.bkey);
-  const K* __restrict__ pkey = static_cast<const K*>(a.pkey);
-  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
-  const uint32_t G = gridDim.x;
-  uint32_t u = blockIdx.x;
-  if (u >= a.U) return;
-  if (tid == 0) {
-    mbar_init(bar + 0, 1);
-    mbar_init(bar + 1, 1);
-    fence_mbar_init();
-    cnt_issue(B[0], bar + 0, a.desc[u], a);
-  }
-  __syncthreads();
-  for (uint32_t it = 0; u < a.U; u += G, ++it) {
-    const uint32_t b = it & 1;
-    const uint4 d = a.desc[u];
-    if (tid == 0 && u + G < a.U) cnt_issue(B[b ^ 1], bar + (b ^ 1), a.desc[u + G], a);
-    const uint32_t bn = d.y, pn = d.w;
-    const uint32_t logT = table_logT(bn);
-    const uint32_t T = 1u << logT, tmask = T - 1, tshift = 32 - logT;
-    const Win wb = window(d.x, d.y, sizeof(K), a.nb), wp = window(d.z, d.w, sizeof(K), a.np);
-    tab.clear(T);
-    if (tid == 0) s_dup = 0;
-    mbar_wait(bar + b, (it >> 1) & 1);
-    const CBuf<K>& Bb = B[b];
-    K kb[BPT];
-#pragma unroll
-    for (int j = 0; j < BPT; ++j) {
-      const uint32_t i = tid + j * HT;
-      kb[j] = i < bn ? (i < wb.valid ? Bb.bk[wb.shift + i] : bkey[d.x + i]) : K(0);
-      if (i < bn) tab.stage(i, kb[j]);
-    }
-    __syncthreads();
-    bool dup = false;
-#pragma unroll
-    for (int j = 0; j < BPT; ++j) {
-      if ((uint32_t)j * HT >= bn) break;
-      const uint32_t i = tid + j * HT;
-      if (i < bn) dup |= tab.insert(slot_hash(kb[j]) >> tshift, tmask, kb[j], i);
-    }
-    if (__any_sync(FULL, dup) && lane == 0) s_dup = 1;
-    __syncthreads();
-    const bool unique = s_dup == 0;
-    uint32_t wlo, whi;
-    probe_range(pn, w, wlo, whi);
-    uint32_t c = 0;
-    bool many = false;
-#pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      if (wlo + 32 * j >= whi) break;  // warp-uniform
-      const uint32_t i = wlo + lane + 32 * j;
-      if (i < whi) {
-        const K k = i < wp.valid ? Bb.pk[wp.shift + i] : pkey[d.z + i];
-        const uint32_t s0 = slot_hash(k) >> tshift;
-        uint32_t m = 0, f = 0;
-        auto hit = [&](uint32_t idx) {
-          f = idx;
-          ++m;
-        };
-        if (unique) tab.template probe<true>(s0, tmask, k, hit);
-        else tab.template probe<false>(s0, tmask, k, hit);
-        c += m;
-        many |= m > 1;
-        stage[d.z + i] = m == 0 ? NO_MATCH : (m == 1 ? (uint16_t)f : MULTI);
-      }
-    }
-    c = warp_sum(c);
-    if (lane == 0) a.wcnt[(uint64_t)u * HW + w] = c;
-    if (__any_sync(FULL, many) && lane == 0) {
-      multi[u] = 1;
-      atomicAdd(nmulti, 1ull);
-    }
-    __syncthreads();  // table and buffer b are reused by the next units
   }
 }
 
@@ -539,18 +396,18 @@ static_assert(sizeof(WBuf) % 16 == 0, "16-byte aligned buffers");
 __device__ __forceinline__ void wf_issue(WBuf& B, uint64_t* bar, const uint4 d, const HJArgs& a,
                                          const uint16_t* stage) {
   fence_proxy_async();  // generic reads of this buffer (previous unit) before the async writes
-  const Win wb = a.brid ? window(d.x, d.y, 4, a.nb) : Win{0, 0, 0, 0};
-  const Win wp = a.prid ? window(d.z, d.w, 4, a.np) : Win{0, 0, 0, 0};
-  const Win ws = window(d.z, d.w, 2, a.np);
+  const Win wb = a.brid ? bulk_window(a.brid, d.x, d.y, 4, a.nb) : Win{nullptr, 0, 0, 0};
+  const Win wp = a.prid ? bulk_window(a.prid, d.z, d.w, 4, a.np) : Win{nullptr, 0, 0, 0};
+  const Win ws = bulk_window(stage, d.z, d.w, 2, a.np);
   const uint32_t bytes = wb.bytes + wp.bytes + ws.bytes;
   if (!bytes) {
     mbar_arrive(bar);
     return;
   }
   mbar_expect_tx(bar, bytes);
-  if (wb.bytes) bulk_g2s(B.br, reinterpret_cast<const uint8_t*>(a.brid) + wb.a0, wb.bytes, bar);
-  if (wp.bytes) bulk_g2s(B.pr, reinterpret_cast<const uint8_t*>(a.prid) + wp.a0, wp.bytes, bar);
-  if (ws.bytes) bulk_g2s(B.st, reinterpret_cast<const uint8_t*>(stage) + ws.a0, ws.bytes, bar);
+  if (wb.bytes) bulk_g2s(B.br, wb.src, wb.bytes, bar);
+  if (wp.bytes) bulk_g2s(B.pr, wp.src, wp.bytes, bar);
+  if (ws.bytes) bulk_g2s(B.st, ws.src, ws.bytes, bar);
 }
 
 __global__ void __launch_bounds__(HT) hj_write_fast(HJArgs a, const uint16_t* __restrict__ stage,
@@ -576,7 +433,9 @@ __global__ void __launch_bounds__(HT) hj_write_fast(HJArgs a, const uint16_t* __
     const bool full = multi[u] != 0;
     mbar_wait(bar + b, (it >> 1) & 1);
     if (!full) {
-      const Win wb = window(d.x, d.y, 4, a.nb), wp = window(d.z, d.w, 4, a.np), ws = window(d.z, d.w, 2, a.np);
+      const Win wb = a.brid ? bulk_window(a.brid, d.x, d.y, 4, a.nb) : Win{nullptr, 0, 0, 0};
+      const Win wp = a.prid ? bulk_window(a.prid, d.z, d.w, 4, a.np) : Win{nullptr, 0, 0, 0};
+      const Win ws = bulk_window(stage, d.z, d.w, 2, a.np);
       const WBuf& Bb = B[b];
       uint32_t wlo, whi;
       probe_range(d.w, w, wlo, whi);
@@ -606,13 +465,15 @@ __global__ void __launch_bounds__(HT) hj_write_fast(HJArgs a, const uint16_t* __
 // Eq.8: R_size = sum over the k partitions ("Reducers") of
 // |S_i| * |T_i| -- an upper bound on |J| that needs no join (gj_join_stats).
 __global__ void hj_units(const uint32_t* __restrict__ boff, const uint32_t* __restrict__ poff, uint32_t P,
-                         uint32_t bchunk, uint32_t pchunk, uint32_t* __restrict__ nunits,
+                         uint32_t bchunk, uint32_t pchunk, unsigned long long* __restrict__ nunits,
                          unsigned long long* __restrict__ eq8) {
   uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long prod = 0;
   if (p < P) {
     uint32_t nb = boff[p + 1] - boff[p], np = poff[p + 1] - poff[p];
-    nunits[p] = (nb && np) ? ((nb + bchunk - 1) / bchunk) * ((np + pchunk - 1) / pchunk) : 0u;
+    // 64-bit: a heavy hitter (one key 2^28 times on one side, 2^29 on the other)
+    // needs more than 2^32 units; the host rejects that instead of wrapping
+    nunits[p] = (nb && np) ? (unsigned long long)((nb + bchunk - 1) / bchunk) * ((np + pchunk - 1) / pchunk) : 0ull;
     prod = (unsigned long long)nb * np;
   }
   prod = warp_sum(prod);
@@ -623,13 +484,13 @@ __global__ void hj_units(const uint32_t* __restrict__ boff, const uint32_t* __re
 // per unit, fully parallel.  Also initialises multi[u]: units of a partition with
 // several build chunks share probe rows, so their per-row staging is ambiguous and
 // the write pass re-probes them.
-__global__ void hj_unit_desc(const uint32_t* __restrict__ unit_off, const uint32_t* __restrict__ boff,
+__global__ void hj_unit_desc(const unsigned long long* __restrict__ unit_off, const uint32_t* __restrict__ boff,
                              const uint32_t* __restrict__ poff, uint32_t P, uint32_t U, uint32_t bchunk,
                              uint32_t pchunk, uint4* __restrict__ desc, uint8_t* __restrict__ multi,
                              unsigned long long* __restrict__ nmulti) {
   for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
-    const uint32_t p = upper_index(unit_off, P, u);
-    const uint32_t uu = u - unit_off[p];
+    const uint32_t p = upper_index(unit_off, P, (unsigned long long)u);
+    const uint32_t uu = (uint32_t)(u - unit_off[p]);
     const uint32_t b0 = boff[p], nb = boff[p + 1] - b0;
     const uint32_t p0 = poff[p], np = poff[p + 1] - p0;
     const uint32_t nbc = (nb + bchunk - 1) / bchunk;
@@ -677,15 +538,23 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
   jc.bchunk = bchunk;
   jc.pchunk = pchunk;
 
-  uint32_t* unit_off = static_cast<uint32_t*>(ws(ctx, "hj.unit_off", (P + 1) * sizeof(uint32_t)));
+  unsigned long long* unit_off =
+      static_cast<unsigned long long*>(ws(ctx, "hj.unit_off", (P + 1) * sizeof(unsigned long long)));
   unsigned long long* eq8 = static_cast<unsigned long long*>(ws(ctx, "hj.eq8", sizeof(unsigned long long)));
   GJ_CUDA(cudaMemsetAsync(eq8, 0, sizeof(unsigned long long), ctx->stream));
   jc.eq8 = eq8;
   launch(ctx, "hj_units", hj_units, dim3((P + 255) / 256), dim3(256), 0, PB.off, PP.off, P, bchunk, pchunk,
          unit_off, eq8);
-  exclusive_scan<uint32_t, uint32_t>(ctx, unit_off, unit_off, P, unit_off + P);
-  uint32_t U = 0;
-  d2h_sync(ctx, &U, unit_off + P, sizeof(uint32_t));
+  exclusive_scan<uint64_t, uint64_t>(ctx, reinterpret_cast<const uint64_t*>(unit_off),
+                                     reinterpret_cast<uint64_t*>(unit_off), P,
+                                     reinterpret_cast<uint64_t*>(unit_off) + P);
+  uint64_t U64 = 0;
+  d2h_sync(ctx, &U64, unit_off + P, sizeof(uint64_t));
+  if (U64 >= (1ull << 31))
+    throw Error(GJ_EINVAL, "equi join: " + std::to_string(U64) +
+                               " work units (a key repeated ~2^28 times on both sides); the per-unit plan is "
+                               "limited to 2^31 units");
+  const uint32_t U = (uint32_t)U64;
   jc.unit_off = unit_off;
   jc.U = U;
   const uint64_t nw = (uint64_t)U * HW;
@@ -706,7 +575,7 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
   unsigned long long* nmulti = reinterpret_cast<unsigned long long*>(woff + nw + 1);
   GJ_CUDA(cudaMemsetAsync(nmulti, 0, sizeof(uint64_t), ctx->stream));
   launch(ctx, "hj_unit_desc", hj_unit_desc, dim3(std::min<uint32_t>((U + 255) / 256, ctx->num_sms * 16)),
-         dim3(256), 0, (const uint32_t*)unit_off, PB.off, PP.off, P, U, bchunk, pchunk, desc, multi, nmulti);
+         dim3(256), 0, (const unsigned long long*)unit_off, PB.off, PP.off, P, U, bchunk, pchunk, desc, multi, nmulti);
   HJArgs a{};
   a.bkey = PB.key;
   a.brid = PB.rid;
@@ -721,20 +590,10 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
   a.nb = Bld.n;
   a.np = Prb.n;
   {
-    static const int v = std::getenv("GJ_HJ_COUNT_V") ? std::atoi(std::getenv("GJ_HJ_COUNT_V")) : 0;
-    if (v == 1) {
-      const size_t smem = 2 * sizeof(CBuf<K>) + 16 + Table<K>::kBytes;
-      static bool once = (set_smem(hj_count_tma<K>, smem), true);
-      (void)once;
-      launch(ctx, "hj_count", hj_count_tma<K>, dim3(hj_grid(ctx, hj_count_tma<K>, smem, U)), dim3(HT), smem, a,
-             stage, multi, nmulti);
-    } else {
-      const size_t smem = hj_smem<K, false>();
-      static bool once = (set_smem(hj_count_kernel<K>, smem), true);
-      (void)once;
-      launch(ctx, "hj_count", hj_count_kernel<K>, dim3(hj_grid(ctx, hj_count_kernel<K>, smem, U)), dim3(HT), smem,
-             a, stage, multi, nmulti);
-    }
+    const size_t smem = hj_smem<K, false>();
+    set_smem(ctx, hj_count_kernel<K>, smem);
+    launch(ctx, "hj_count", hj_count_kernel<K>, dim3(hj_grid(ctx, hj_count_kernel<K>, smem, U)), dim3(HT), smem, a,
+           stage, multi, nmulti);
   }
   exclusive_scan<uint32_t, uint64_t>(ctx, wcnt, woff, nw, woff + nw);
   uint64_t h[2];
@@ -766,14 +625,12 @@ void write_impl(gj_ctx* ctx, uint32_t* out) {
   // units without a MULTI row: table-free gather with TMA prefetch; then the rare
   // MULTI units rebuild their table and re-probe
   const size_t fsmem = 2 * sizeof(WBuf) + 16;
-  static bool once_f = (set_smem(hj_write_fast, fsmem), true);
-  (void)once_f;
+  set_smem(ctx, hj_write_fast, fsmem);
   launch(ctx, "hj_write", hj_write_fast, dim3(hj_grid(ctx, hj_write_fast, fsmem, a.U)), dim3(HT), fsmem, a,
          (const uint16_t*)jc.stage, (const uint8_t*)jc.multi);
   if (jc.nmulti == 0) return;
   const size_t smem = hj_smem<K, true>();
-  static bool once = (set_smem(hj_write_kernel<K>, smem), true);
-  (void)once;
+  set_smem(ctx, hj_write_kernel<K>, smem);
   launch(ctx, "hj_write_multi", hj_write_kernel<K>, dim3(hj_grid(ctx, hj_write_kernel<K>, smem, a.U)), dim3(HT),
          smem, a, (const uint16_t*)jc.stage, (const uint8_t*)jc.multi, 1);
 }

@@ -481,12 +481,10 @@ void run(gj_ctx* ctx, const NLJArgs& a, bool write) {
   const size_t smem = STG * TS * sizeof(K);
   const uint32_t grid = std::min<uint32_t>(a.U, (uint32_t)ctx->num_sms * 12);
   if (!write) {
-    static bool once = (set_smem(nlj_kernel<K, OP, FAST, false>, smem), true);
-    (void)once;
+    set_smem(ctx, nlj_kernel<K, OP, FAST, false>, smem);
     launch(ctx, "nlj_count", nlj_kernel<K, OP, FAST, false>, dim3(grid), dim3(NT), smem, a);
   } else {
-    static bool once = (set_smem(nlj_kernel<K, OP, FAST, true>, smem), true);
-    (void)once;
+    set_smem(ctx, nlj_kernel<K, OP, FAST, true>, smem);
     launch(ctx, "nlj_write", nlj_kernel<K, OP, FAST, true>, dim3(grid), dim3(NT), smem, a);
   }
 }
@@ -544,6 +542,27 @@ NLJArgs make_args(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, const ThetaCach
 // the S rows after V (all S buckets > x2), for > and >= the rows before V, for !=
 // both.  V's ends are rounded to 16-byte boundaries for the TMA copies; the Green
 // rectangles start exactly where V ends, so every pair is produced once.
+// Class of cell (x, y) = (R bucket x, S bucket y) for R.key OP S.key (Fig. 9,
+// Alg.3 Reduce): GREEN = every pair satisfies the predicate (written as a cross
+// product), RED = must be compared (sent to the NLJ), WHITE = no pair can match
+// (skipped).  Buckets are equal-width and ascending, so for <, <=: x < y is Green,
+// x > y White; >, >=: mirrored; !=: off-diagonal Green; =: off-diagonal White; the
+// diagonal is Red (bucket ties).  Band: cells within m = ceil(eps / w) buckets can
+// hold a pair and are Red (the NLJ evaluates them; they are not split further into
+// Green), the rest White.
+enum { CELL_WHITE = 0, CELL_RED = 1, CELL_GREEN = 2 };
+int region_class(int op, uint64_t x, uint64_t y, uint64_t m) {
+  switch (op) {
+    case GJ_EQ: return x == y ? CELL_RED : CELL_WHITE;
+    case GJ_NE: return x == y ? CELL_RED : CELL_GREEN;
+    case GJ_LT:
+    case GJ_LE: return x < y ? CELL_GREEN : (x == y ? CELL_RED : CELL_WHITE);
+    case GJ_GT:
+    case GJ_GE: return x > y ? CELL_GREEN : (x == y ? CELL_RED : CELL_WHITE);
+    default: return (x > y ? x - y : y - x) <= m ? CELL_RED : CELL_WHITE;
+  }
+}
+
 template <typename K>
 void region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, int op, uint64_t eps, unsigned long long lo,
                   unsigned long long hi, bool fast) {
@@ -580,16 +599,23 @@ void region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, int op, uint64_
   for (uint64_t t = 0; t < ntile; ++t) {
     const uint64_t r0 = t * RT, rn = std::min<uint64_t>(RT, nR - r0);
     const uint64_t x1 = bucket_of(r0), x2 = bucket_of(r0 + rn - 1);
+    // V = the S buckets of the tile's Red cells: [first Red y of row x1, last Red y of
+    // row x2] (the Red cells of a row are one contiguous run around its diagonal)
     uint64_t ylo = x1, yhi = x2;
-    if (op == GJ_BAND) {
+    if (op == GJ_BAND) {  // the band's Red run around x is [x - m, x + m] (closed form of the loop below)
       ylo = x1 > m ? x1 - m : 0;
       yhi = std::min<uint64_t>(P - 1, x2 + m);
     }
+    while (ylo > 0 && region_class(op, x1, ylo - 1, m) == CELL_RED) --ylo;
+    while (yhi + 1 < P && region_class(op, x2, yhi + 1, m) == CELL_RED) ++yhi;
     const uint64_t vb = so[ylo] / al * al, ve = std::min<uint64_t>(nS, (so[yhi + 1] + al - 1) / al * al);
     tv[t] = {vb, ve};
     visit += ve - vb;
-    const bool after = op == GJ_LT || op == GJ_LE || op == GJ_NE;   // Green: S buckets > x2
-    const bool before = op == GJ_GT || op == GJ_GE || op == GJ_NE;  // Green: S buckets < x1
+    // outside V a row's cells are Green or White as a whole side: Green after V when
+    // the tile's last row x2 sees bucket yhi + 1 Green (then every row does), before V
+    // when its first row x1 sees bucket ylo - 1 Green
+    const bool after = yhi + 1 < P && region_class(op, x2, yhi + 1, m) == CELL_GREEN;
+    const bool before = ylo > 0 && region_class(op, x1, ylo - 1, m) == CELL_GREEN;
     if (after && ve < nS) tc.rects.push_back(make_uint4((uint32_t)r0, (uint32_t)rn, (uint32_t)ve, (uint32_t)(nS - ve)));
     if (before && vb > 0) tc.rects.push_back(make_uint4((uint32_t)r0, (uint32_t)rn, 0u, (uint32_t)vb));
   }
@@ -768,6 +794,7 @@ void cross_write(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t* out) {
 }
 
 void theta_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, int op, uint64_t eps) {
+  ctx->tc.epoch = ++ctx->epoch_ctr;
   ctx->tc.R = R;
   if (R.key_type == GJ_I32) theta_count_impl<int32_t>(ctx, R, S, op, eps);
   else theta_count_impl<int64_t>(ctx, R, S, op, eps);
@@ -779,3 +806,13 @@ void theta_write(gj_ctx* ctx, uint32_t* out) {
 }
 
 }  // namespace gj
+
+extern "C" gj_status gj_region_classify(int op, uint32_t k, uint64_t m, uint8_t* cls) {
+  if (op < GJ_EQ || op > GJ_BAND || k == 0 || k > 4096 || !cls) {
+    gj::set_last_error("gj_region_classify: bad arguments");
+    return GJ_EINVAL;
+  }
+  for (uint64_t x = 0; x < k; ++x)
+    for (uint64_t y = 0; y < k; ++y) cls[x * k + y] = (uint8_t)gj::region_class(op, x, y, m);
+  return GJ_OK;
+}

@@ -34,7 +34,6 @@ constexpr int TPC = 16;          // tiles per chunk
 constexpr int CHUNK = TILE * TPC;  // 65536 tuples per chunk
 constexpr int NW = PT / 32;
 constexpr int MAX_BITS = 9;      // digits per pass <= 512
-constexpr int SCATTER_DEFAULT_V = 4;  // part_scatter variant (see launch_scatter_t)
 
 struct ChunkLoc {
   uint32_t total, seg, cb, nc;  // #chunks, segment, first chunk of segment, chunks in segment
@@ -98,11 +97,8 @@ __device__ __forceinline__ void load_tile(const K* __restrict__ key, const uint3
 // finds its offsets with one row read -- no inter-CTA look-back.
 // int32: a 4-CTA/SM register budget (64 registers) measured 0.1228 vs 0.1248 ms at
 // configs[1] (6 CTAs/SM: 40 registers + spills, 0.1307 ms); int64 keeps 3 (80).
-#ifndef GJ_HIST_MINB
-#define GJ_HIST_MINB 4
-#endif
 template <typename K, bool RANGE>
-__global__ void __launch_bounds__(PT, sizeof(K) == 4 ? GJ_HIST_MINB : 3) part_hist(const K* __restrict__ key, uint64_t n,
+__global__ void __launch_bounds__(PT, sizeof(K) == 4 ? 4 : 3) part_hist(const K* __restrict__ key, uint64_t n,
                                                 const uint32_t* __restrict__ seg_off,
                                                 const uint32_t* __restrict__ chunk_base,
                                                 uint32_t nseg, uint32_t shift, uint32_t bits,
@@ -163,356 +159,9 @@ __global__ void tile_desc_kernel(uint64_t n, const uint32_t* __restrict__ seg_of
   desc[t] = d;
 }
 
-// Scatter (see the file comment).  Persistent CTAs take tiles t = blockIdx.x +
-// k*gridDim.x, so neighbouring tiles still run concurrently on different SMs and
-// each digit run's partial sectors are completed in L2 before eviction.  The next
-// tile's keys (and rids) are streamed into a shared-memory buffer by 1-D TMA bulk
-// copies (mbarrier completion) while the current tile is ranked and written; the
-// consumed input buffer then doubles as the digit-ordered staging area.
-// Per-digit offset of a tile = chunk run offset (scanned chunk histogram) + the
-// tile's in-chunk prefix row written by part_hist.
-// Shared-memory layout of the scatter (dynamic: the counter arrays follow D).
-//   buf[2] = {key[KB], rid[RB]}  double-buffered TMA input (rids only if HAS_RID);
-//            the consumed buffer is the staging area of the digit-ordered tile
-//            (ILV: one (key, rid) uint2 per slot across key[] and rid[])
-//   bar[2], wt[NW]
-//   whist[NW][PACK ? D/2 : D]  warp-private digit counters (PACK: two 16-bit
-//                              counters per word)
-//   delta[D]                   per digit: global position - tile-local position
-template <typename K, bool PACK>
-struct ScatterLayout {
-  // room for the 16-byte TMA alignment shift and the bulk-store run padding (<= 3 per run)
-  static constexpr uint32_t KB = TILE + 64;
-  static constexpr uint32_t RB = TILE + 64;
-  static constexpr size_t BUF = (size_t)KB * sizeof(K) + (size_t)RB * 4;
-  static constexpr size_t off_bar = 2 * BUF;
-  static constexpr size_t off_wt = off_bar + 16;
-  static constexpr size_t off_run = off_wt + 8 * NW;  // bulk path: tstart[16], sadj[16]
-  static constexpr size_t off_whist = off_run + 128;
-  static_assert(BUF % 16 == 0 && off_whist % 16 == 0, "16-byte aligned sections");
-  static __host__ __device__ uint32_t words(uint32_t D) { return PACK ? (D > 1 ? D / 2 : 1) : D; }
-  static size_t bytes(uint32_t D) { return off_whist + ((size_t)NW * words(D) + (size_t)D) * 4; }
-};
-
-template <typename K, bool PACK>
-struct ScatterSmem {
-  using L = ScatterLayout<K, PACK>;
-  uint8_t* base;
-  __device__ K* key(uint32_t b) const { return reinterpret_cast<K*>(base + b * L::BUF); }
-  __device__ uint32_t* rid(uint32_t b) const {
-    return reinterpret_cast<uint32_t*>(base + b * L::BUF + (size_t)L::KB * sizeof(K));
-  }
-  __device__ uint2* stage(uint32_t b) const { return reinterpret_cast<uint2*>(base + b * L::BUF); }
-  __device__ uint64_t* bar() const { return reinterpret_cast<uint64_t*>(base + L::off_bar); }
-  __device__ uint32_t* wt() const { return reinterpret_cast<uint32_t*>(base + L::off_wt); }
-  __device__ uint32_t* whist() const { return reinterpret_cast<uint32_t*>(base + L::off_whist); }
-  __device__ uint32_t* run() const { return reinterpret_cast<uint32_t*>(base + L::off_run); }
-};
-
-template <typename K, bool HAS_RID, bool PACK>
-__device__ __forceinline__ void issue_tile(const ScatterSmem<K, PACK>& sm, uint32_t buf, const uint4 d,
-                                           const K* key_in, const uint32_t* rid_in, uint64_t n) {
-  fence_proxy_async();
-  uint64_t* bar = sm.bar() + buf;
-  if (d.y == 0) {
-    mbar_arrive(bar);
-    return;
-  }
-  const uint64_t kb0 = (uint64_t)d.x * sizeof(K), kb1 = (uint64_t)(d.x + d.y) * sizeof(K);
-  const uint64_t ka = kb0 & ~15ull, kz = min((kb1 + 15) & ~15ull, (n * sizeof(K)) & ~15ull);
-  uint32_t bytes = kz > ka ? (uint32_t)(kz - ka) : 0u;
-  uint64_t ra = 0, rz = 0;
-  if (HAS_RID) {
-    const uint64_t rb0 = (uint64_t)d.x * 4, rb1 = (uint64_t)(d.x + d.y) * 4;
-    ra = rb0 & ~15ull;
-    rz = min((rb1 + 15) & ~15ull, (n * 4) & ~15ull);
-    if (rz > ra) bytes += (uint32_t)(rz - ra);
-  }
-  mbar_expect_tx(bar, bytes);
-  if (kz > ka) bulk_g2s(sm.key(buf), reinterpret_cast<const uint8_t*>(key_in) + ka, (uint32_t)(kz - ka), bar);
-  if (HAS_RID && rz > ra)
-    bulk_g2s(sm.rid(buf), reinterpret_cast<const uint8_t*>(rid_in) + ra, (uint32_t)(rz - ra), bar);
-}
-
-// REMOTE (multi-GPU shuffle fused into the scatter): run d's tuples go to rank
-// d >> dst.lbits at index position + dst.adj[d] of its receive buffers (peer
-// pointers mapped over NVLink through CUDA IPC).
-template <typename K, bool HAS_RID, bool REMOTE, bool PACK, bool ILV>
-__global__ void __launch_bounds__(PT) part_scatter(
-    const K* __restrict__ key_in, const uint32_t* __restrict__ rid_in, uint32_t rid_base, uint64_t n,
-    const uint4* __restrict__ tdesc, uint32_t ntiles, uint32_t shift, uint32_t bits,
-    const uint32_t* __restrict__ scanned, const uint32_t* __restrict__ tile_pref, K* __restrict__ key_out,
-    uint32_t* __restrict__ rid_out, ShuffleDest dst) {
-  static_assert(!ILV || sizeof(K) == 4, "interleaved staging holds 32-bit keys");
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  using L = ScatterLayout<K, PACK>;
-  const ScatterSmem<K, PACK> sm{smem_raw};
-  const uint32_t D = 1u << bits, mask = D - 1;
-  const uint32_t W = L::words(D);  // counter words per warp
-  uint32_t* whist = sm.whist();
-  uint32_t* delta = whist + NW * W;
-  const uint32_t w = threadIdx.x >> 5, lane = lane_id();
-  const uint32_t G = gridDim.x;
-  // REMOTE with few destinations: each tile's runs are long (~TILE/D tuples), so they
-  // go out as 1-D TMA bulk stores (16-byte aligned middles) instead of thread stores
-  const bool bulk = REMOTE && !ILV && D <= 16;
-  uint32_t* tstart = sm.run();    // bulk: tile-local start of every run
-  uint32_t* sadj = tstart + 16;   // bulk: staging shift of every run (alignment padding)
-  uint32_t t = blockIdx.x;
-  if (t >= ntiles) return;
-  if (threadIdx.x == 0) {
-    mbar_init(sm.bar() + 0, 1);
-    mbar_init(sm.bar() + 1, 1);
-    fence_mbar_init();
-    issue_tile<K, HAS_RID>(sm, 0, tdesc[t], key_in, rid_in, n);
-  }
-  __syncthreads();
-  static_assert((1 << MAX_BITS) <= 2 * PT, "two digits per thread");
-  static_assert(MAX_BITS >= 1, "");
-  // counter of digit dg of warp ww: word, shift
-  // thread i owns digits i and i + H (H = D/2): consecutive threads touch consecutive
-  // words (no bank conflicts); PACK keeps digit i in the low and i + H in the high half
-  const uint32_t H = D > 1 ? D / 2 : 1;
-  auto cword = [&](uint32_t ww, uint32_t dg) -> uint32_t* { return whist + ww * W + (PACK ? (dg & (H - 1)) : dg); };
-  auto cshift = [&](uint32_t dg) -> uint32_t { return PACK ? (uint32_t)(dg >= H && D > 1) << 4 : 0u; };
-
-  for (uint32_t it = 0; t < ntiles; t += G, ++it) {
-    const uint32_t buf = it & 1;
-    const uint4 d = tdesc[t];
-    if (threadIdx.x == 0 && t + G < ntiles) {
-      if (bulk) bulk_wait_read();  // the bulk stores of the previous tile have read its staging
-      issue_tile<K, HAS_RID>(sm, buf ^ 1, tdesc[t + G], key_in, rid_in, n);
-    }
-    const uint32_t cnt = d.y;
-    if (cnt) {  // CTA-uniform
-      // this tile's run offsets for my two digits (i, i + H), i = threadIdx.x: loads
-      // issued now, consumed after ranking
-      const uint32_t da = threadIdx.x, db = threadIdx.x + H;
-      const bool ha = da < H && da < D, hb = D > 1 && da < H;
-      uint32_t g0a = 0, g0b = 0;
-      if (ha) {
-        g0a = scanned[d.z + (uint64_t)da * d.w] + tile_pref[(uint64_t)t * D + da];
-        if (REMOTE) g0a += dst.adj[da];  // position -> receiver index
-      }
-      if (hb) {
-        g0b = scanned[d.z + (uint64_t)db * d.w] + tile_pref[(uint64_t)t * D + db];
-        if (REMOTE) g0b += dst.adj[db];
-      }
-      if (W >= 4) {
-        uint4* z = reinterpret_cast<uint4*>(whist + w * W);
-        for (uint32_t i = lane; i < W / 4; i += 32) z[i] = make_uint4(0, 0, 0, 0);
-      } else if (lane < W) {
-        whist[w * W + lane] = 0;
-      }
-      mbar_wait(sm.bar() + buf, (it >> 1) & 1);
-      const uint32_t ko = (d.x * (uint32_t)sizeof(K) & 15u) / (uint32_t)sizeof(K);
-      const uint32_t ro = (d.x & 3u);
-      const uint64_t kz = min((((uint64_t)(d.x + d.y) * sizeof(K)) + 15) & ~15ull, (n * sizeof(K)) & ~15ull);
-      const uint32_t kvalid = (uint32_t)(kz / sizeof(K) > d.x ? kz / sizeof(K) - d.x : 0);  // keys inside the bulk copy
-      const uint64_t rz = min((((uint64_t)(d.x + d.y) * 4) + 15) & ~15ull, (n * 4) & ~15ull);
-      const uint32_t rvalid = (uint32_t)(rz / 4 > d.x ? rz / 4 - d.x : 0);
-      const K* kbuf = sm.key(buf);
-      K k[PI];
-      uint32_t rk[PI];  // (digit << 16) | rank among this warp's keys of that digit
-      __syncwarp();
-      // Rank inside the warp: every lane fetch-adds its digit's warp-private counter.
-      // Warp w's items are processed in index order, so ranks follow input order
-      // (conflicting lanes of one instruction are serialised in a fixed hardware
-      // order); the column prefix below orders the warps.  (MATCH.ANY-based peer
-      // aggregation measured 0.016 warp-instr/clk/SM on sm_100a: DESIGN.md §4.1.)
-#pragma unroll
-      for (int i = 0; i < PI; ++i) {
-        const uint32_t j = (w * PI + i) * 32 + lane;
-        const bool v = j < cnt;
-        k[i] = v ? (j < kvalid ? kbuf[ko + j] : key_in[d.x + j]) : K(0);
-        const uint32_t dg = v ? digit_of(k[i], shift, mask) : 0u;
-        const uint32_t sh = cshift(dg);
-        uint32_t r = 0;
-        if (v) r = (atomicAdd(cword(w, dg), 1u << sh) >> sh) & 0xffffu;
-        rk[i] = v ? ((dg << 16) | r) : 0xffffffffu;
-      }
-      uint32_t rr[HAS_RID ? PI : 1];
-      if (HAS_RID) {
-        const uint32_t* rbuf = sm.rid(buf);
-#pragma unroll
-        for (int i = 0; i < PI; ++i) {
-          const uint32_t j = (w * PI + i) * 32 + lane;
-          rr[i] = j < cnt ? (j < rvalid ? rbuf[ro + j] : rid_in[d.x + j]) : 0u;
-        }
-      }
-      __syncthreads();  // all inputs are in registers: the buffer becomes the staging area
-      // Tile-local digit starts with one barrier: thread i owns digits i and i + H:
-      // exclusive column prefix over the warps, warp scans of both halves' totals,
-      // then every warp adds the totals of the warps before it (and the low half's
-      // grand total for the high half).
-      {
-        uint32_t ta = 0, tb = 0;  // totals of digits i, i + H
-        if (ha) {
-          if (PACK) {
-            uint32_t acc = 0;  // halves <= TILE: no carry
-#pragma unroll
-            for (int ww = 0; ww < NW; ++ww) {
-              uint32_t* c = whist + ww * W + da;
-              const uint32_t x = *c;
-              *c = acc;
-              acc += x;
-            }
-            ta = acc & 0xffffu;
-            tb = acc >> 16;
-          } else {
-#pragma unroll
-            for (int ww = 0; ww < NW; ++ww) {
-              uint32_t* c = whist + ww * W + da;
-              const uint32_t x = c[0];
-              c[0] = ta;
-              ta += x;
-              if (hb) {
-                const uint32_t y = c[H];
-                c[H] = tb;
-                tb += y;
-              }
-            }
-          }
-        }
-        const uint32_t ia = warp_incl_scan(ta), ib = warp_incl_scan(tb);
-        uint32_t* wt = sm.wt();  // [0, NW): low-half warp totals, [NW, 2 NW): high half
-        if (lane == 31) {
-          wt[w] = ia;
-          wt[NW + w] = ib;
-        }
-        __syncthreads();
-        uint32_t st_a = ia - ta, st_b = ib - tb, low = 0;
-#pragma unroll
-        for (int ww = 0; ww < NW; ++ww) {
-          const uint32_t xa = wt[ww], xb = wt[NW + ww];
-          low += xa;
-          if ((uint32_t)ww < w) {
-            st_a += xa;
-            st_b += xb;
-          }
-        }
-        st_b += low;
-        if (ha) {
-          delta[da] = g0a - st_a;
-          if (hb) delta[db] = g0b - st_b;
-          if (bulk) {
-            tstart[da] = st_a;
-            if (hb) tstart[db] = st_b;
-          }
-          if (PACK) {
-            const uint32_t st = st_a | (st_b << 16);  // positions stay < 2 TILE: 16 bits
-#pragma unroll
-            for (int ww = 0; ww < NW; ++ww) whist[ww * W + da] += st;
-          } else {
-#pragma unroll
-            for (int ww = 0; ww < NW; ++ww) {
-              whist[ww * W + da] += st_a;
-              if (hb) whist[ww * W + db] += st_b;
-            }
-          }
-        }
-      }
-      __syncthreads();
-      if (bulk) {  // pad each run so that its staging start shares its destination's 16 B phase
-        if (threadIdx.x == 0) {
-          uint32_t pad = 0;
-          for (uint32_t r = 0; r < D; ++r) {
-            const uint32_t st = tstart[r], p = delta[r] + st;
-            pad += (p - (st + pad)) & 3u;
-            sadj[r] = pad;
-          }
-        }
-        __syncthreads();
-      }
-      K* skey = sm.key(buf);
-      uint32_t* srid = sm.rid(buf);
-      uint2* stg = sm.stage(buf);
-#pragma unroll
-      for (int i = 0; i < PI; ++i) {
-        if (rk[i] != 0xffffffffu) {
-          const uint32_t dg = rk[i] >> 16, sh = cshift(dg);
-          const uint32_t pos = ((*cword(w, dg) >> sh) & 0xffffu) + (rk[i] & 0xffffu) + (bulk ? sadj[dg] : 0u);
-          const uint32_t rv = HAS_RID ? rr[i] : rid_base + d.x + (w * PI + i) * 32 + lane;
-          if (ILV) {
-            stg[pos] = make_uint2((uint32_t)k[i], rv);
-          } else {
-            skey[pos] = k[i];
-            srid[pos] = rv;
-          }
-        }
-      }
-      if (bulk) fence_proxy_async();  // every writer: staging stores -> async proxy (bulk reads)
-      __syncthreads();
-      if (bulk) {
-        // run r: staged at [s, s + len), destination index p (s = p mod 4): threads
-        // store the unaligned head and tail, thread 0 the aligned middle in bulk
-        for (uint32_t r = w; r < D; r += NW) {
-          const uint32_t st = tstart[r], len = (r + 1 < D ? tstart[r + 1] : cnt) - st;
-          const uint32_t s0 = st + sadj[r], p = delta[r] + st;
-          const uint32_t head = min(len, (4u - (p & 3u)) & 3u), tail = (len - head) & 3u;
-          K* kd = static_cast<K*>(dst.key[r >> dst.lbits]);
-          uint32_t* rd = dst.rid[r >> dst.lbits];
-          if (lane < head) {
-            kd[p + lane] = skey[s0 + lane];
-            rd[p + lane] = srid[s0 + lane];
-          } else if (lane >= 4 && lane < 4 + tail) {
-            const uint32_t e = len - tail + (lane - 4);
-            kd[p + e] = skey[s0 + e];
-            rd[p + e] = srid[s0 + e];
-          }
-        }
-        if (threadIdx.x == 0) {
-          for (uint32_t r = 0; r < D; ++r) {
-            const uint32_t st = tstart[r], len = (r + 1 < D ? tstart[r + 1] : cnt) - st;
-            const uint32_t s0 = st + sadj[r], p = delta[r] + st;
-            const uint32_t head = min(len, (4u - (p & 3u)) & 3u), body = (len - head) & ~3u;
-            if (body) {
-              bulk_s2g(static_cast<K*>(dst.key[r >> dst.lbits]) + p + head, skey + s0 + head,
-                       body * (uint32_t)sizeof(K));
-              bulk_s2g(dst.rid[r >> dst.lbits] + p + head, srid + s0 + head, body * 4u);
-            }
-          }
-          bulk_commit();
-        }
-      }
-#pragma unroll 4
-      for (int i = 0; i < PI && !bulk; ++i) {
-        const uint32_t j = i * PT + threadIdx.x;
-        if (j < cnt) {
-          K kk;
-          uint32_t rv;
-          if (ILV) {
-            const uint2 e = stg[j];
-            kk = (K)e.x;
-            rv = e.y;
-          } else {
-            kk = skey[j];
-            rv = srid[j];
-          }
-          const uint32_t dg = digit_of(kk, shift, mask);
-          const uint32_t pos = delta[dg] + j;
-          if (REMOTE) {  // pos is already the index in the receiving rank's buffer
-            const uint32_t p = dg >> dst.lbits;
-            static_cast<K*>(dst.key[p])[pos] = kk;
-            dst.rid[p][pos] = rv;
-          } else {
-            key_out[pos] = kk;
-            rid_out[pos] = rv;
-          }
-        }
-      }
-    } else {
-      mbar_wait(sm.bar() + buf, (it >> 1) & 1);
-    }
-    __syncthreads();  // the buffer may be refilled by the next iteration's issue
-  }
-  if (bulk && threadIdx.x == 0) bulk_wait_all();  // bulk stores complete
-  if (REMOTE) __threadfence_system();  // peer writes performed before the kernel retires
-}
-
-// Local scatter (no shuffle), branch-free ranking.  Same contract and output as
-// part_scatter<K, HAS_RID, false, ...>, restructured so that every phase of a tile
-// is a straight run of independent per-item operations the scheduler can overlap:
+// Scatter (local radix pass, or the multi-GPU shuffle pass with REMOTE), branch-free
+// ranking.  Every phase of a tile is a straight run of independent per-item
+// operations the scheduler can overlap:
 //  * the (rare) elements of the array's last tile that lie outside the 16-byte TMA
 //    window are patched into the shared buffer once, CTA-uniformly, instead of a
 //    per-item "shared or global" select (which compiled to 16 BSSY/BRA regions);
@@ -522,37 +171,55 @@ __global__ void __launch_bounds__(PT) part_scatter(
 // Stable: warp w holds the tile's items [w*PI*32, (w+1)*PI*32) in order, item i of
 // lane l is element (w*PI + i)*32 + l, and lanes of one fetch-add instruction on the
 // same counter are serialised in lane order.
+// Tiles are handed out in global order by an atomic counter (first tile =
+// blockIdx.x): the tiles in flight are always a contiguous window, so the partial
+// sectors at the ends of neighbouring tiles' runs meet in L2 (with a static
+// round-robin a lagging CTA left them to be written back half-filled).  The next
+// tile's keys (and rids) are streamed into the other shared-memory buffer by 1-D
+// TMA bulk copies while this one is ranked; the consumed buffer then doubles as the
+// digit-ordered staging area.  Run starts per (tile, digit) come from
+// tile_base_kernel (absolute positions).
+// REMOTE (multi-GPU shuffle fused into the scatter): run d's tuples go to rank
+// d >> dst.lbits at index position + dst.adj[d] of its receive buffers (peer
+// pointers mapped over NVLink through CUDA IPC).  With <= 16 destinations a tile's
+// runs are long (~TILE/D tuples), so they leave as 1-D TMA bulk stores
+// (cp.async.bulk.global.shared::cta): each run's staging start is padded to its
+// destination's 16-byte phase, threads store the <= 3-element head and tail, one
+// thread issues the aligned middles.
 template <typename K>
-struct LocalLayout {
-  static constexpr uint32_t KB = TILE + 16;  // room for the 16-byte TMA alignment shift
-  static constexpr uint32_t RB = TILE + 16;
+struct ScatterLayout {
+  // room for the 16-byte TMA alignment shift and the bulk-store run padding (<= 3 per run)
+  static constexpr uint32_t KB = TILE + 64;
+  static constexpr uint32_t RB = TILE + 64;
   static constexpr size_t BUF = (size_t)KB * sizeof(K) + (size_t)RB * 4;
   static constexpr size_t off_bar = 2 * BUF;
   static constexpr size_t off_wt = off_bar + 16;
-  static constexpr size_t off_whist = off_wt + 16 * NW;
+  static constexpr size_t off_run = off_wt + 16 * NW;  // bulk path: tstart[16], sadj[16]
+  static constexpr size_t off_whist = off_run + 128;
   static_assert(BUF % 16 == 0 && off_whist % 16 == 0, "16-byte aligned sections");
   static __host__ __device__ uint32_t words(uint32_t D) { return (D + 1 + 3) & ~3u; }
   static size_t bytes(uint32_t D) { return off_whist + ((size_t)NW * words(D) + (size_t)D) * 4; }
 };
 
-#ifndef GJ_SCATTER_MINB
-#define GJ_SCATTER_MINB 2  // CTAs/SM the register budget targets (3: 85 registers, 8 B spills, -0.6%: noise level)
-#endif
-template <typename K, bool HAS_RID, bool RANGE>
-__global__ void __launch_bounds__(PT, GJ_SCATTER_MINB) part_scatter_local(
+constexpr int SCATTER_MINB = 2;  // CTAs/SM the register budget targets (3: 85 registers + spills, noise level)
+template <typename K, bool HAS_RID, bool RANGE, bool REMOTE>
+__global__ void __launch_bounds__(PT, SCATTER_MINB) part_scatter(
     const K* __restrict__ key_in, const uint32_t* __restrict__ rid_in, uint32_t rid_base, uint64_t n,
     const uint4* __restrict__ tdesc, uint32_t ntiles, uint32_t shift, uint32_t bits,
     const uint32_t* __restrict__ tile_base, K* __restrict__ key_out, uint32_t* __restrict__ rid_out,
-    uint32_t* __restrict__ tile_ctr, DigitFn fn) {
+    uint32_t* __restrict__ tile_ctr, DigitFn fn, ShuffleDest dst) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  using L = LocalLayout<K>;
-  constexpr bool ILV = sizeof(K) == 4;  // int32: one (key, rid) uint2 per staging slot
+  using L = ScatterLayout<K>;
+  constexpr bool ILV = sizeof(K) == 4 && !REMOTE;  // int32 local: one (key, rid) uint2 per staging slot
   const uint32_t D = 1u << bits, mask = D - 1;
   const uint32_t W = L::words(D);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L::off_bar);
   uint32_t* wt = reinterpret_cast<uint32_t*>(smem_raw + L::off_wt);
   uint32_t* whist = reinterpret_cast<uint32_t*>(smem_raw + L::off_whist);
   uint32_t* delta = whist + NW * W;
+  uint32_t* tstart = reinterpret_cast<uint32_t*>(smem_raw + L::off_run);  // bulk: tile-local run starts
+  uint32_t* sadj = tstart + 16;                                            // bulk: staging padding per run
+  const bool bulk = REMOTE && D <= 16;
   auto kbuf_of = [&](uint32_t b) { return reinterpret_cast<K*>(smem_raw + b * L::BUF); };
   auto rbuf_of = [&](uint32_t b) {
     return reinterpret_cast<uint32_t*>(smem_raw + b * L::BUF + (size_t)L::KB * sizeof(K));
@@ -568,19 +235,16 @@ __global__ void __launch_bounds__(PT, GJ_SCATTER_MINB) part_scatter_local(
       mbar_arrive(bar);
       return;
     }
-    const uint64_t kb0 = (uint64_t)d.x * sizeof(K), kb1 = (uint64_t)(d.x + d.y) * sizeof(K);
-    const uint64_t ka = kb0 & ~15ull, kz = min((kb1 + 15) & ~15ull, (n * sizeof(K)) & ~15ull);
-    uint32_t bytes = kz > ka ? (uint32_t)(kz - ka) : 0u;
-    uint64_t ra = 0, rz = 0;
+    const Win kw = bulk_window(key_in, d.x, d.y, sizeof(K), n);
+    uint32_t bytes = kw.bytes;
+    Win rw{};
     if (HAS_RID) {
-      ra = ((uint64_t)d.x * 4) & ~15ull;
-      rz = min((((uint64_t)(d.x + d.y) * 4) + 15) & ~15ull, (n * 4) & ~15ull);
-      if (rz > ra) bytes += (uint32_t)(rz - ra);
+      rw = bulk_window(rid_in, d.x, d.y, 4, n);
+      bytes += rw.bytes;
     }
     mbar_expect_tx(bar, bytes);
-    if (kz > ka) bulk_g2s(kbuf_of(b), reinterpret_cast<const uint8_t*>(key_in) + ka, (uint32_t)(kz - ka), bar);
-    if (HAS_RID && rz > ra)
-      bulk_g2s(rbuf_of(b), reinterpret_cast<const uint8_t*>(rid_in) + ra, (uint32_t)(rz - ra), bar);
+    if (kw.bytes) bulk_g2s(kbuf_of(b), kw.src, kw.bytes, bar);
+    if (HAS_RID && rw.bytes) bulk_g2s(rbuf_of(b), rw.src, rw.bytes, bar);
   };
   if (threadIdx.x == 0) {
     mbar_init(bars + 0, 1);
@@ -592,10 +256,6 @@ __global__ void __launch_bounds__(PT, GJ_SCATTER_MINB) part_scatter_local(
   const uint32_t H = D > 1 ? D / 2 : 1;
   const uint32_t da = threadIdx.x, db = threadIdx.x + H;
   const bool ha = da < H && da < D, hb = D > 1 && da < H;
-  // Tiles are handed out in global order by an atomic counter (first tile =
-  // blockIdx.x): the tiles in flight are always a contiguous window, so the partial
-  // sectors at the ends of neighbouring tiles' runs meet in L2 (with a static
-  // round-robin a lagging CTA left them to be written back half-filled).
   __shared__ uint32_t s_tile[2];
   if (threadIdx.x == 0) s_tile[0] = t;
   __syncthreads();
@@ -606,13 +266,16 @@ __global__ void __launch_bounds__(PT, GJ_SCATTER_MINB) part_scatter_local(
     if (threadIdx.x == 0) {
       const uint32_t tn = G + atomicAdd(tile_ctr, 1u);
       s_tile[b ^ 1] = tn;
-      if (tn < ntiles) issue(b ^ 1, tdesc[tn]);
+      if (tn < ntiles) {
+        if (bulk) bulk_wait_read();  // the previous tile's bulk stores have read buffer b ^ 1
+        issue(b ^ 1, tdesc[tn]);
+      }
     }
     const uint4 d = tdesc[t];
     uint32_t g0a = 0, g0b = 0;  // global run starts of my two digits in this tile
     if (d.y) {
-      if (ha) g0a = tile_base[(uint64_t)t * D + da];
-      if (hb) g0b = tile_base[(uint64_t)t * D + db];
+      if (ha) g0a = tile_base[(uint64_t)t * D + da] + (REMOTE ? dst.adj[da] : 0u);
+      if (hb) g0b = tile_base[(uint64_t)t * D + db] + (REMOTE ? dst.adj[db] : 0u);
     }
     const uint32_t cnt = d.y;
     if (cnt == 0) {  // CTA-uniform
@@ -627,15 +290,16 @@ __global__ void __launch_bounds__(PT, GJ_SCATTER_MINB) part_scatter_local(
     mbar_wait(bars + b, (it >> 1) & 1);
     K* kbuf = kbuf_of(b);
     uint32_t* rbuf = rbuf_of(b);
-    const uint32_t ko = (d.x * (uint32_t)sizeof(K) & 15u) / (uint32_t)sizeof(K);
-    const uint32_t ro = d.x & 3u;
+    const Win kw = bulk_window(key_in, d.x, cnt, sizeof(K), n);
+    const uint32_t ko = kw.shift;
+    uint32_t ro = 0;
     {  // elements past the last 16-byte boundary of the array: not in the bulk copy
-      const uint64_t kz = min((((uint64_t)(d.x + d.y) * sizeof(K)) + 15) & ~15ull, (n * sizeof(K)) & ~15ull);
-      const uint32_t kvalid = (uint32_t)(kz / sizeof(K) > d.x ? kz / sizeof(K) - d.x : 0);
+      const uint32_t kvalid = kw.valid;
       uint32_t rvalid = cnt;
       if (HAS_RID) {
-        const uint64_t rz = min((((uint64_t)(d.x + d.y) * 4) + 15) & ~15ull, (n * 4) & ~15ull);
-        rvalid = (uint32_t)(rz / 4 > d.x ? rz / 4 - d.x : 0);
+        const Win rw = bulk_window(rid_in, d.x, cnt, 4, n);
+        ro = rw.shift;
+        rvalid = rw.valid;
       }
       if (kvalid < cnt || rvalid < cnt) {  // CTA-uniform, at most the array's final tile
         for (uint32_t j = kvalid + threadIdx.x; j < cnt; j += PT) kbuf[ko + j] = key_in[d.x + j];
@@ -661,7 +325,9 @@ __global__ void __launch_bounds__(PT, GJ_SCATTER_MINB) part_scatter_local(
     for (int i = 0; i < PI; ++i)
       rr[i] = HAS_RID ? rbuf[ro + (w * PI + i) * 32 + lane] : rid_base + d.x + (w * PI + i) * 32 + lane;
     __syncthreads();  // inputs are in registers: the buffer becomes the staging area
-    {  // tile-local digit starts (see part_scatter)
+    {  // tile-local digit starts: thread i owns digits i and i + H -- exclusive column
+       // prefix over the warps, warp scans of both halves' totals, then every warp adds
+       // the totals of the warps before it (and the low half's total for the high half)
       uint32_t ta = 0, tb = 0;
       if (ha) {
 #pragma unroll
@@ -697,6 +363,10 @@ __global__ void __launch_bounds__(PT, GJ_SCATTER_MINB) part_scatter_local(
       if (ha) {
         delta[da] = g0a - st_a;
         if (hb) delta[db] = g0b - st_b;
+        if (bulk) {
+          tstart[da] = st_a;
+          if (hb) tstart[db] = st_b;
+        }
 #pragma unroll
         for (int ww = 0; ww < NW; ++ww) {
           whist[ww * W + da] += st_a;
@@ -705,6 +375,17 @@ __global__ void __launch_bounds__(PT, GJ_SCATTER_MINB) part_scatter_local(
       }
     }
     __syncthreads();
+    if (bulk) {  // pad each run so that its staging start shares its destination's 16 B phase
+      if (threadIdx.x == 0) {
+        uint32_t pad = 0;
+        for (uint32_t r = 0; r < D; ++r) {
+          const uint32_t st = tstart[r], p = delta[r] + st;
+          pad += (p - (st + pad)) & 3u;
+          sadj[r] = pad;
+        }
+      }
+      __syncthreads();
+    }
     uint2* stg = reinterpret_cast<uint2*>(kbuf);
     K* skey = kbuf;
     uint32_t* srid = rbuf;
@@ -712,7 +393,7 @@ __global__ void __launch_bounds__(PT, GJ_SCATTER_MINB) part_scatter_local(
     for (int i = 0; i < PI; ++i) {
       const uint32_t dg = rk[i] >> 16;
       if (dg < D) {
-        const uint32_t pos = whist[w * W + dg] + (rk[i] & 0xffffu);
+        const uint32_t pos = whist[w * W + dg] + (rk[i] & 0xffffu) + (bulk ? sadj[dg] : 0u);
         if (ILV) {
           stg[pos] = make_uint2((uint32_t)k[i], rr[i]);
         } else {
@@ -721,62 +402,89 @@ __global__ void __launch_bounds__(PT, GJ_SCATTER_MINB) part_scatter_local(
         }
       }
     }
+    if (bulk) fence_proxy_async();  // every writer: staging stores -> async proxy (bulk reads)
     __syncthreads();
-    // write-back in groups of 8 items: loads, offsets, then (predicated) stores --
-    // staging slots past cnt hold stale data but index delta[] safely
-    constexpr int WG = 8;
-#pragma unroll
-    for (int i0 = 0; i0 < PI; i0 += WG) {
-      K kk[WG];
-      uint32_t rv[WG], pos[WG];
-#pragma unroll
-      for (int q = 0; q < WG; ++q) {
-        const uint32_t j = (i0 + q) * PT + threadIdx.x;
-        if (ILV) {
-          const uint2 e = stg[j];
-          kk[q] = (K)e.x;
-          rv[q] = e.y;
-        } else {
-          kk[q] = skey[j];
-          rv[q] = srid[j];
+    if (bulk) {
+      // run r: staged at [s, s + len), destination index p (s = p mod 4): threads
+      // store the unaligned head and tail, thread 0 the aligned middle in bulk
+      for (uint32_t r = w; r < D; r += NW) {
+        const uint32_t st = tstart[r], len = (r + 1 < D ? tstart[r + 1] : cnt) - st;
+        const uint32_t s0 = st + sadj[r], p = delta[r] + st;
+        const uint32_t head = min(len, (4u - (p & 3u)) & 3u), tail = (len - head) & 3u;
+        K* kd = static_cast<K*>(dst.key[r >> dst.lbits]);
+        uint32_t* rd = dst.rid[r >> dst.lbits];
+        if (lane < head) {
+          kd[p + lane] = skey[s0 + lane];
+          rd[p + lane] = srid[s0 + lane];
+        } else if (lane >= 4 && lane < 4 + tail) {
+          const uint32_t e = len - tail + (lane - 4);
+          kd[p + e] = skey[s0 + e];
+          rd[p + e] = srid[s0 + e];
         }
       }
+      if (threadIdx.x == 0) {
+        for (uint32_t r = 0; r < D; ++r) {
+          const uint32_t st = tstart[r], len = (r + 1 < D ? tstart[r + 1] : cnt) - st;
+          const uint32_t s0 = st + sadj[r], p = delta[r] + st;
+          const uint32_t head = min(len, (4u - (p & 3u)) & 3u), body = (len - head) & ~3u;
+          if (body) {
+            bulk_s2g(static_cast<K*>(dst.key[r >> dst.lbits]) + p + head, skey + s0 + head,
+                     body * (uint32_t)sizeof(K));
+            bulk_s2g(dst.rid[r >> dst.lbits] + p + head, srid + s0 + head, body * 4u);
+          }
+        }
+        bulk_commit();
+      }
+    } else {
+      // write-back in groups of 8 items: loads, offsets, then (predicated) stores --
+      // staging slots past cnt hold stale data but index delta[] safely
+      constexpr int WG = 8;
 #pragma unroll
-      for (int q = 0; q < WG; ++q) pos[q] = delta[digit_of<RANGE>(kk[q], shift, mask, fn)] + (i0 + q) * PT + threadIdx.x;
+      for (int i0 = 0; i0 < PI; i0 += WG) {
+        K kk[WG];
+        uint32_t rv[WG], pos[WG], dgs[WG];
 #pragma unroll
-      for (int q = 0; q < WG; ++q) {
-        if ((i0 + q) * PT + threadIdx.x < cnt) {
-          key_out[pos[q]] = kk[q];
-          rid_out[pos[q]] = rv[q];
+        for (int q = 0; q < WG; ++q) {
+          const uint32_t j = (i0 + q) * PT + threadIdx.x;
+          if (ILV) {
+            const uint2 e = stg[j];
+            kk[q] = (K)e.x;
+            rv[q] = e.y;
+          } else {
+            kk[q] = skey[j];
+            rv[q] = srid[j];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < WG; ++q) {
+          dgs[q] = digit_of<RANGE>(kk[q], shift, mask, fn);
+          pos[q] = delta[dgs[q]] + (i0 + q) * PT + threadIdx.x;
+        }
+#pragma unroll
+        for (int q = 0; q < WG; ++q) {
+          if ((i0 + q) * PT + threadIdx.x < cnt) {
+            if (REMOTE) {  // pos is already the index in the receiving rank's buffer
+              const uint32_t p = dgs[q] >> dst.lbits;
+              static_cast<K*>(dst.key[p])[pos[q]] = kk[q];
+              dst.rid[p][pos[q]] = rv[q];
+            } else {
+              key_out[pos[q]] = kk[q];
+              rid_out[pos[q]] = rv[q];
+            }
+          }
         }
       }
     }
     __syncthreads();  // the buffer may be refilled by the next iteration's issue
   }
-}
-
-template <typename K, bool HAS_RID, bool RANGE>
-void launch_scatter_local(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
-                          const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits,
-                          const uint32_t* tile_base, K* kout, uint32_t* rout, const DigitFn& fn) {
-  auto kern = part_scatter_local<K, HAS_RID, RANGE>;
-  const size_t smem = LocalLayout<K>::bytes(1u << bits);
-  static bool once = (set_smem(kern, LocalLayout<K>::bytes(1u << MAX_BITS)), true);
-  (void)once;
-  int occ = 1;
-  GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PT, smem));
-  if (const char* e = std::getenv("GJ_SCATTER_OCC")) occ = std::min(occ, std::atoi(e));
-  const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
-  uint32_t* ctr = static_cast<uint32_t*>(ws(ctx, "part.tile_ctr", sizeof(uint32_t)));
-  GJ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), ctx->stream));
-  launch(ctx, "part_scatter", kern, dim3(grid), dim3(PT), smem, kin, rin, rid_base, n, tdesc, (uint32_t)ntiles,
-         shift, bits, tile_base, kout, rout, ctr, fn);
+  if (bulk && threadIdx.x == 0) bulk_wait_all();  // bulk stores complete
+  if (REMOTE) __threadfence_system();  // peer writes performed before the kernel retires
 }
 
 // Turns the in-chunk prefix rows of part_hist into absolute run starts: every
 // tile's row gets its chunk's scanned (segment, digit, chunk) offsets added, so the
-// local scatter reads one contiguous row per tile (the scanned matrix is strided by
-// the chunk count: reading it per tile cost one DRAM sector per digit).
+// scatter reads one contiguous row per tile (the scanned matrix is strided by the
+// chunk count: reading it per tile cost one DRAM sector per digit).
 // One CTA per chunk.
 __global__ void tile_base_kernel(uint64_t n, const uint32_t* __restrict__ seg_off,
                                  const uint32_t* __restrict__ chunk_base, uint32_t nseg, uint32_t bits,
@@ -791,69 +499,32 @@ __global__ void tile_base_kernel(uint64_t n, const uint32_t* __restrict__ seg_of
   }
 }
 
-template <typename K, bool HAS_RID, bool REMOTE, bool PACK, bool ILV>
-void launch_scatter_v(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
-                      const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* hist,
-                      const uint32_t* tile_pref, K* kout, uint32_t* rout, const ShuffleDest& dst) {
-  auto kern = part_scatter<K, HAS_RID, REMOTE, PACK, ILV>;
-  const size_t smem = ScatterLayout<K, PACK>::bytes(1u << bits);
-  static bool once = (set_smem(kern, ScatterLayout<K, PACK>::bytes(1u << MAX_BITS)), true);
-  (void)once;
+template <typename K, bool HAS_RID, bool RANGE, bool REMOTE>
+void launch_scatter_t(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
+                      const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* tile_base,
+                      K* kout, uint32_t* rout, const DigitFn& fn, const ShuffleDest& dst) {
+  auto kern = part_scatter<K, HAS_RID, RANGE, REMOTE>;
+  const size_t smem = ScatterLayout<K>::bytes(1u << bits);
+  set_smem(ctx, kern, ScatterLayout<K>::bytes(1u << MAX_BITS));
   int occ = 1;
   GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PT, smem));
-  if (const char* e = std::getenv("GJ_SCATTER_OCC")) occ = std::min(occ, std::atoi(e));  // tuning experiments
-  uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
-  // the NVLink-bound shuffle may run beside the local passes of the other relation
-  // (second stream): capped so those keep SMs (ctx->shuffle_ctas, 0 = no cap)
-  if (REMOTE && ctx->shuffle_ctas) grid = std::min<uint32_t>(grid, ctx->shuffle_ctas);
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
+  uint32_t* ctr = static_cast<uint32_t*>(ws(ctx, REMOTE ? "shuffle.tile_ctr" : "part.tile_ctr", sizeof(uint32_t)));
+  GJ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), ctx->stream));
   launch(ctx, REMOTE ? "shuffle_scatter" : "part_scatter", kern, dim3(grid), dim3(PT), smem, kin, rin, rid_base, n,
-         tdesc, (uint32_t)ntiles, shift, bits, hist, tile_pref, kout, rout, dst);
+         tdesc, (uint32_t)ntiles, shift, bits, tile_base, kout, rout, ctr, fn, dst);
 }
 
-// Variant selection (GJ_SCATTER_V, tuning experiments): 0 = plain counters +
-// separate key/rid staging, 1 = packed counters, 2 = interleaved staging, 3 = both.
-int scatter_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("GJ_SCATTER_V");
-    return e ? std::atoi(e) : SCATTER_DEFAULT_V;
-  }();
-  return v;
-}
-
-template <typename K, bool HAS_RID, bool REMOTE>
-void launch_scatter_t(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
-                      const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* hist,
-                      const uint32_t* tile_pref, K* kout, uint32_t* rout, const ShuffleDest& dst) {
-  const int v = REMOTE ? (scatter_variant() & 1) : scatter_variant();  // the shuffle stages key/rid separately
-  if (!REMOTE && v == 4) {  // tile_pref holds absolute run starts (tile_base_kernel)
-    launch_scatter_local<K, HAS_RID, false>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_pref, kout,
-                                            rout, DigitFn{});
-  } else if (sizeof(K) == 4 && (v & 2)) {
-    if (v & 1)
-      launch_scatter_v<K, HAS_RID, REMOTE, true, sizeof(K) == 4>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift,
-                                                                 bits, hist, tile_pref, kout, rout, dst);
-    else
-      launch_scatter_v<K, HAS_RID, REMOTE, false, sizeof(K) == 4>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift,
-                                                                  bits, hist, tile_pref, kout, rout, dst);
-  } else if (v & 1) {
-    launch_scatter_v<K, HAS_RID, REMOTE, true, false>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, hist,
-                                                      tile_pref, kout, rout, dst);
-  } else {
-    launch_scatter_v<K, HAS_RID, REMOTE, false, false>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, hist,
-                                                       tile_pref, kout, rout, dst);
-  }
-}
-
-template <typename K, bool REMOTE>
+template <typename K, bool RANGE, bool REMOTE>
 void launch_scatter(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
-                    const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* hist,
-                    const uint32_t* tile_pref, K* kout, uint32_t* rout, const ShuffleDest& dst) {
+                    const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* tile_base,
+                    K* kout, uint32_t* rout, const DigitFn& fn, const ShuffleDest& dst) {
   if (rin)
-    launch_scatter_t<K, true, REMOTE>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, hist, tile_pref, kout,
-                                      rout, dst);
+    launch_scatter_t<K, true, RANGE, REMOTE>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_base, kout,
+                                             rout, fn, dst);
   else
-    launch_scatter_t<K, false, REMOTE>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, hist, tile_pref,
-                                       kout, rout, dst);
+    launch_scatter_t<K, false, RANGE, REMOTE>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_base,
+                                              kout, rout, fn, dst);
 }
 
 __global__ void seg_chunks(const uint32_t* __restrict__ seg_off, uint32_t nseg, uint32_t* __restrict__ nc) {
@@ -936,23 +607,13 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
     launch(ctx, "part_hist", part_hist<K, RANGE>, dim3((unsigned)max_chunks), dim3(PT), 0, kin, n, seg_off,
            (const uint32_t*)chunk_base, nseg, shift, bits, hist, tile_pref, fn);
     exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
-    if (RANGE || scatter_variant() >= 4)
-      launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, seg_off,
-             (const uint32_t*)chunk_base, nseg, bits, (const uint32_t*)hist, tile_pref);
+    launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, seg_off,
+           (const uint32_t*)chunk_base, nseg, bits, (const uint32_t*)hist, tile_pref);
     uint4* tdesc = static_cast<uint4*>(ws(ctx, "part.tdesc", (ntiles + 1) * sizeof(uint4)));
     launch(ctx, "tile_desc", tile_desc_kernel, dim3((unsigned)((ntiles + 255) / 256)), dim3(256), 0, n, seg_off,
            (const uint32_t*)chunk_base, nseg, D, (uint32_t)ntiles, tdesc);
-    if (RANGE) {
-      if (rin)
-        launch_scatter_local<K, true, true>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, tile_pref, kout,
-                                            rout, fn);
-      else
-        launch_scatter_local<K, false, true>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, tile_pref,
-                                             kout, rout, fn);
-    } else {
-      launch_scatter<K, false>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, hist, tile_pref, kout, rout,
-                               ShuffleDest{});
-    }
+    launch_scatter<K, RANGE, false>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, tile_pref, kout, rout,
+                                    fn, ShuffleDest{});
     const uint32_t P = nseg << bits;
     uint32_t* off = static_cast<uint32_t*>(ws(ctx, (ps + ".off").c_str(), (P + 1) * sizeof(uint32_t)));
     launch(ctx, "extract_off", extract_off, dim3((P + 1 + 255) / 256), dim3(256), 0, (const uint32_t*)hist,
@@ -992,6 +653,8 @@ ShufflePass shuffle_prepare_impl(gj_ctx* ctx, const gj_rel& X, uint32_t g, const
          static_cast<const K*>(X.key), n, (const uint32_t*)nullptr, (const uint32_t*)nullptr, 1u, shift, g, hist,
          tile_pref, DigitFn{});
   exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
+  launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, (const uint32_t*)nullptr,
+         (const uint32_t*)nullptr, 1u, g, (const uint32_t*)hist, tile_pref);
   uint4* tdesc = static_cast<uint4*>(ws(ctx, (t + ".stdesc").c_str(), (sp.ntiles + 1) * sizeof(uint4)));
   launch(ctx, "tile_desc", tile_desc_kernel, dim3((unsigned)((sp.ntiles + 255) / 256)), dim3(256), 0, n,
          (const uint32_t*)nullptr, (const uint32_t*)nullptr, 1u, D, (uint32_t)sp.ntiles, tdesc);
@@ -1032,11 +695,11 @@ ShufflePass shuffle_prepare(gj_ctx* ctx, const gj_rel& X, uint32_t g, const char
 void shuffle_scatter(gj_ctx* ctx, const gj_rel& X, const ShufflePass& sp, const ShuffleDest& dst) {
   if (X.n == 0) return;
   if (X.key_type == GJ_I32)
-    launch_scatter<int32_t, true>(ctx, static_cast<const int32_t*>(X.key), X.rid, X.rid_base, X.n, sp.tdesc, sp.ntiles,
-                                  32 - sp.g, sp.g, sp.hist, sp.tile_pref, nullptr, nullptr, dst);
+    launch_scatter<int32_t, false, true>(ctx, static_cast<const int32_t*>(X.key), X.rid, X.rid_base, X.n, sp.tdesc,
+                                         sp.ntiles, 32 - sp.g, sp.g, sp.tile_pref, nullptr, nullptr, DigitFn{}, dst);
   else
-    launch_scatter<int64_t, true>(ctx, static_cast<const int64_t*>(X.key), X.rid, X.rid_base, X.n, sp.tdesc, sp.ntiles,
-                                  32 - sp.g, sp.g, sp.hist, sp.tile_pref, nullptr, nullptr, dst);
+    launch_scatter<int64_t, false, true>(ctx, static_cast<const int64_t*>(X.key), X.rid, X.rid_base, X.n, sp.tdesc,
+                                         sp.ntiles, 32 - sp.g, sp.g, sp.tile_pref, nullptr, nullptr, DigitFn{}, dst);
 }
 
 }  // namespace gj

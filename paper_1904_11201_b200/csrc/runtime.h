@@ -37,6 +37,7 @@ struct Buf {
 // Per-call cache so that *_materialize reuses what the preceding *_count built.
 struct JoinCache {
   bool valid = false;
+  uint64_t epoch = 0;    // ctx-wide fill counter of the count that built this cache
   gj_rel R{}, S{};
   bool swap = false;     // build side is S
   uint32_t B = 0;        // radix bits
@@ -47,7 +48,7 @@ struct JoinCache {
   const uint32_t* prid = nullptr;
   const uint32_t* boff = nullptr;  // P+1
   const uint32_t* poff = nullptr;  // P+1
-  const uint32_t* unit_off = nullptr;  // P+1
+  const unsigned long long* unit_off = nullptr;  // P+1 (uint64 unit starts)
   const void* desc = nullptr;  // U x uint4 unit descriptors
   const uint16_t* stage = nullptr;  // per probe row: matching build index in its unit
   const uint8_t* multi = nullptr;   // per unit: some probe row has > 1 match
@@ -61,6 +62,7 @@ struct JoinCache {
 
 struct ThetaCache {
   bool valid = false;
+  uint64_t epoch = 0;    // ctx-wide fill counter of the count that built this cache
   gj_rel R{}, S{};
   int op = 0;
   uint64_t eps = 0;
@@ -100,10 +102,9 @@ struct gj_ctx {
   bool profile = false;
   uint32_t nlj_split = 0;
   bool force_slow_band = false;
-  bool overlap_shuffle = true;
-  uint32_t shuffle_ctas = 0;    // CTA cap of the shuffle scatter (0 = all)  // multi-GPU equi: S shuffle on a 2nd stream beside R's local passes
-  int theta_regions = 1;
-  uint32_t theta_grid_rows = 0;  // multi-GPU theta: rows r of the 1-Bucket grid (0 = auto; 1 = R broadcast)  // theta joins through the region matrix (0 = plain NLJ over all pairs)
+  bool overlap_shuffle = true;   // multi-GPU equi: S shuffle on a 2nd stream beside R's local passes
+  int theta_regions = 1;         // theta joins through the region matrix (0 = plain NLJ over all pairs)
+  uint32_t theta_grid_rows = 0;  // multi-GPU theta: rows r of the 1-Bucket grid (0 = auto; 1 = R broadcast)
   int build_side = 0;
   int shuffle_bits = 0;
   // workspace
@@ -114,7 +115,9 @@ struct gj_ctx {
   std::vector<gj::ProfRec> pending;
   std::vector<cudaEvent_t> event_pool;
   std::map<std::string, std::pair<double, uint64_t>> times;
-  // caches
+  // caches (epoch_ctr numbers every count that fills one, so a multi-GPU count can
+  // tell whether a later single-GPU call on the same ctx replaced its cache)
+  uint64_t epoch_ctr = 0;
   gj::JoinCache jc;
   gj::ThetaCache tc;
   // join_host_batch: two sub-contexts (own streams and workspaces) so that
@@ -129,6 +132,8 @@ struct gj_ctx {
 
 namespace gj {
 
+// Thread-local message returned by gj_last_error().
+void set_last_error(const std::string& m);
 // Grow-only named scratch buffer, stream-ordered.
 void* ws(gj_ctx* ctx, const char* name, size_t bytes);
 // Grow-only named pinned host buffer (callers must not overwrite one that an
@@ -170,11 +175,13 @@ inline void launch(gj_ctx* ctx, const char* tag, void (*k)(KArgs...), dim3 grid,
   k<<<grid, block, smem, ctx->stream>>>(static_cast<KArgs>(args)...);
 }
 
-// Opt a kernel into > 48 KB dynamic shared memory (once per kernel).
+// Opt a kernel into > 48 KB dynamic shared memory.  The attribute belongs to the
+// current device's context, so it is recorded per (kernel, device): a process with
+// contexts on several devices opts every kernel in on each of them.
+void set_smem_attr(const void* kernel, size_t bytes);
 template <typename... KArgs>
-inline void set_smem(void (*k)(KArgs...), size_t bytes) {
-  GJ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k),
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+inline void set_smem(gj_ctx*, void (*k)(KArgs...), size_t bytes) {
+  set_smem_attr(reinterpret_cast<const void*>(k), bytes);
 }
 
 }  // namespace gj

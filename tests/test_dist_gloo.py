@@ -1,7 +1,9 @@
 """Multi-process host logic on CPU (gloo, world_size 2, 127.0.0.1).
 
-* every rank computes its receive plan from the all-gathered G x G count matrix
-  through the library's host-only gj_dist_plan, checked against a direct sum;
+* every rank computes its receive plan from the all-gathered run-count matrix through
+  gj_dist_plan -- the same host function join_dist_count* runs -- and the scatter
+  it drives is simulated tuple by tuple: every receive slot is written exactly once,
+  in digit-major / sender-rank / input order (see also test_dist_plan.py);
 * the communicator-id broadcast used by paper_1904_11201_b200.Comm (object
   broadcast over the process group) delivers identical bytes to every rank;
 * the oracle-side shard bookkeeping (global rids = rid_base + local row) composes:
@@ -25,6 +27,34 @@ def _free_port():
     return p
 
 
+def _simulate(M, adjs, me, seg, need, lbits):
+    """The shuffle scatter driven by the plans: sender q's tuples in its own
+    (destination, digit, input) order get position pos; tuple (p, d, j) lands at
+    index pos + adj_q[p, d] (mod 2^32) of rank p's buffer.  Checks every slot of
+    rank `me`'s buffer is written once, in (digit, sender, input) order, and that
+    seg / need describe it."""
+    G, L = M.shape[0], 1 << lbits
+    buf = {}
+    for q in range(G):
+        pos = 0
+        for p in range(G):
+            for d in range(L):
+                for j in range(int(M[q, p, d])):
+                    if p == me:
+                        idx = (pos + int(adjs[q][p, d])) % (1 << 32)
+                        if idx in buf:
+                            return False
+                        buf[idx] = (d, q, j)
+                    pos += 1
+    n = int(M[:, me, :].sum())
+    if sorted(buf) != list(range(n)) or int(need[me]) != n:
+        return False
+    if [buf[i] for i in range(n)] != sorted(buf.values()):
+        return False
+    starts = [int(M[:, me, :d].sum()) for d in range(L + 1)]
+    return list(map(int, seg)) == starts and all(int(need[p]) == int(M[:, p, :].sum()) for p in range(G))
+
+
 def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -37,15 +67,16 @@ def _worker(rank, world, port, q):
         import oracle
         import gen
 
+        lbits, L = 2, 4
         rng = np.random.default_rng(100 + rank)
-        row = torch.tensor(rng.integers(0, 1000, world), dtype=torch.int64)
-        rows = [torch.zeros(world, dtype=torch.int64) for _ in range(world)]
+        row = torch.tensor(rng.integers(0, 50, world * L), dtype=torch.int64)  # my sends [p, d]
+        rows = [torch.zeros(world * L, dtype=torch.int64) for _ in range(world)]
         dist.all_gather(rows, row)
-        M = np.stack([r.numpy() for r in rows]).astype(np.uint64)
-        off, tot = gj.dist_plan(M, rank)
-        col = M[:, rank].astype(np.int64)
-        ok_plan = tot == int(col.sum()) and off == [int(x) for x in np.concatenate([[0], np.cumsum(col)[:-1]])]
-
+        M = np.stack([r.numpy() for r in rows]).reshape(world, world, L).astype(np.uint64)
+        adj, seg, need = gj.dist_plan(M, rank, lbits)
+        adjs = [None] * world
+        dist.all_gather_object(adjs, adj)
+        ok_plan = _simulate(M, adjs, rank, seg, need, lbits)
         blob = [os.urandom(gj.COMM_ID_BYTES) if rank == 0 else None]
         dist.broadcast_object_list(blob, src=0)
         gathered = [None] * world

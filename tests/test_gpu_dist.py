@@ -70,6 +70,20 @@ def _worker(rank, world, port, q):
         S2 = gj.Rel(torch.from_numpy(S2all[s0:s1]).cuda(), None, s0)
         nl, ng = gj.join_dist_count(ctx, comm, R2, S2)
         out["dup"] = (nl, ng, gj.join_dist_materialize(ctx, comm, R2, S2, nl).cpu().numpy().view(np.uint32))
+        # a single-GPU join on the same ctx between the dist count and materialize must
+        # not leak into the dist output (the dist cache checks the ctx's fill epoch)
+        nl, ng = gj.join_dist_count(ctx, comm, R2, S2)
+        tiny = torch.arange(100, dtype=torch.int32, device="cuda")
+        assert gj.join_count(ctx, tiny, tiny) == 100
+        out["dup_epoch"] = (nl, ng, gj.join_dist_materialize(ctx, comm, R2, S2, nl).cpu().numpy().view(np.uint32))
+        # shards that are views at element offsets (not 16-byte aligned): R2[1:], S2[3:]
+        # of the same global rows, through the fused NVLink shuffle's bulk copies
+        bigR = torch.from_numpy(R2all[max(r0 - 1, 0):r1]).cuda()
+        bigS = torch.from_numpy(S2all[max(s0 - 3, 0):s1]).cuda()
+        R2u = gj.Rel(bigR[r0 - max(r0 - 1, 0):], None, r0)
+        S2u = gj.Rel(bigS[s0 - max(s0 - 3, 0):], None, s0)
+        nl, ng = gj.join_dist_count(ctx, comm, R2u, S2u)
+        out["dup_unaligned"] = (nl, ng, gj.join_dist_materialize(ctx, comm, R2u, S2u, nl).cpu().numpy().view(np.uint32))
         # local radix digits folded into the NVLink shuffle (receivers lay out digit-major):
         # (a) 3 radix bits in all, so the shuffle's local digit alone forms the partitions
         ctx.set_option("shuffle_bits", 8)
@@ -171,7 +185,7 @@ def test_dist_joins_match_oracle(world):
     R4all, S4all = _i64_inputs()
     dup = oracle.hash_equi(R2all, S2all)
     pk = oracle.pkfk_closed_form(m)
-    expect = {"equi": pk, "equi_sb6": pk, "dup": dup, "dup_pb3": dup,
+    expect = {"equi": pk, "equi_sb6": pk, "dup": dup, "dup_pb3": dup, "dup_epoch": dup, "dup_unaligned": dup,
               "i64": oracle.hash_equi(R4all, S4all), "band": oracle.band_materialize(R3all, S3all, 40)}
     for rows in sorted({world, 2}):
         expect[f"band_grid{rows}"] = expect["band"]

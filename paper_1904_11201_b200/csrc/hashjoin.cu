@@ -35,9 +35,7 @@ constexpr int HT = 512;            // threads per CTA
 constexpr int HW = HT / 32;        // warps per CTA (counts are kept per (unit, warp))
 constexpr int BCH_MAX = 4096;      // max build tuples per unit
 constexpr int PCH_MAX = 4096;      // max probe tuples per unit
-constexpr int TAB_MAX = 2 * BCH_MAX;
-constexpr int BPT = BCH_MAX / HT;  // build tuples per thread
-constexpr int PPT = PCH_MAX / HT;  // probe tuples per lane (warp w owns rows [w*pn/HW, ...))
+constexpr int TAB_MAX = 2 * BCH_MAX;  // table slots: load <= 1/4 up to 2048 build tuples, <= 1/2 at 4096
 
 // Independent second hash for the in-partition table slot (the partition id
 // already consumed the top bits of khash).
@@ -63,134 +61,119 @@ struct HJArgs {
   const uint64_t* woff;
   uint2* out;
   int swap;
-  uint64_t nb, np;  // build / probe array lengths (bulk-copy windows are clamped to them)
 };
 
-// Shared-memory table.  int32 keys: one 64-bit slot = (index+1) << 32 | key, so a
-// probe step is a single LDS.64; 0 = empty.  int64 keys: slot = index+1 and the
-// key is compared in the staged key array.
+// The 16-byte vectors covering elements [first, first + cnt) of an array, on absolute
+// addresses (any element-aligned base): vector v holds elements v*KVN - shift ..
+// v*KVN - shift + KVN - 1 of the range (KVN = 16 / element size).  The few bytes a
+// vector covers outside the range lie in the same 16-byte block as a range element
+// (hence the same page), so loading whole vectors never faults.  Both hash-join
+// passes map a unit's probe rows to warps through these vectors (warp w of a unit
+// owns the contiguous vectors [w*vpw, (w+1)*vpw)), so the per-(unit, warp) counts of
+// the count pass are the output blocks of the write pass.
+struct Span {
+  const uint8_t* a0;
+  uint32_t nv;
+  uint32_t shift;
+};
+__device__ __forceinline__ Span span16(const void* base, uint64_t first, uint32_t cnt, uint32_t esz) {
+  const uint64_t s0 = reinterpret_cast<uint64_t>(base) + first * esz, s1 = s0 + (uint64_t)cnt * esz;
+  const uint64_t a0 = s0 & ~15ull;
+  Span s;
+  s.a0 = reinterpret_cast<const uint8_t*>(a0);
+  s.nv = cnt ? (uint32_t)((((s1 + 15) & ~15ull) - a0) >> 4) : 0u;
+  s.shift = (uint32_t)((s0 - a0) / esz);
+  return s;
+}
+__device__ __forceinline__ uint4 ldv(const Span& s, uint32_t v) {
+  return __ldg(reinterpret_cast<const uint4*>(s.a0) + v);
+}
+__device__ __forceinline__ void warp_vecs(uint32_t nv, uint32_t w, uint32_t& vb, uint32_t& ve) {
+  const uint32_t vpw = (nv + HW - 1) / HW;
+  vb = min(w * vpw, nv);
+  ve = min(vb + vpw, nv);
+}
+template <typename K>
+struct KVec {
+  static constexpr uint32_t N = 16 / sizeof(K);
+  K k[N];
+  __device__ __forceinline__ explicit KVec(uint4 x) {
+    static_assert(sizeof(KVec) == 16, "");
+    *reinterpret_cast<uint4*>(k) = x;
+  }
+};
+
+// Shared-memory table, open addressing with linear probing; 0 = empty slot, so the
+// table is cleared (zeroed) between units.  int32 keys: one 64-bit slot =
+// (index + 1) << 32 | key, so a probe step is a single LDS.64.  int64 keys: 32-bit
+// slot = index + 1 and the key is compared in the staged key array.
+// insert() returns true if it walked past an equal key (a duplicate build key): two
+// equal keys share a probe sequence, so whichever is inserted second meets the
+// first.  Without duplicates each probe stops at its first match (a PK build side),
+// otherwise it walks to the first empty slot (bag semantics).
 template <typename K> struct Table;
-//
-// insert() returns true if it walked past an equal key (a duplicate build key):
-// two equal keys share a probe sequence, so whichever is inserted second meets the
-// first.  When a chunk has no duplicates, probe<true>() stops at the first match
-// (a PK build side), otherwise probe<false>() walks to the first empty slot (bag
-// semantics).
-template <typename K> struct Table;
-// int32 keys: 64-bit slot = gen:20 | index:12 | key:32.  A slot is occupied only
-// if its generation equals the current unit's, so consecutive units of a CTA need
-// no table clear (one clear per launch; the generation advances per unit).
 template <> struct Table<int32_t> {
   unsigned long long* slot;
-  unsigned long long g;  // current generation, pre-shifted to bit 44
   static constexpr size_t kBytes = TAB_MAX * 8;
-  static_assert(BCH_MAX <= 4096, "12-bit index");
-  __device__ void init(uint8_t* base) {
-    slot = reinterpret_cast<unsigned long long*>(base);
+  static constexpr bool kStaged = false;
+  __device__ void init(uint8_t* base) { slot = reinterpret_cast<unsigned long long*>(base); }
+  __device__ void clear(uint32_t T) {
     uint4* p = reinterpret_cast<uint4*>(slot);
-    for (uint32_t i = threadIdx.x; i < TAB_MAX / 2; i += HT) p[i] = make_uint4(0, 0, 0, 0);
-    g = 0;  // generation 0 is "empty"; next_unit() moves to 1 before the first use
+    for (uint32_t i = threadIdx.x; i < T / 2; i += HT) p[i] = make_uint4(0, 0, 0, 0);
   }
-  // a new unit: bump the generation (wraps after 2^20 units; re-clear then)
-  __device__ void clear(uint32_t) {
-    g += 1ull << 44;
-    if (g == 0) {
-      uint4* p = reinterpret_cast<uint4*>(slot);
-      for (uint32_t i = threadIdx.x; i < TAB_MAX / 2; i += HT) p[i] = make_uint4(0, 0, 0, 0);
-      g = 1ull << 44;
-    }
-  }
-  __device__ bool live(unsigned long long v) const { return (v & (0xFFFFFull << 44)) == g; }
   __device__ void stage(uint32_t, int32_t) {}
-  __device__ bool insert(uint32_t s, uint32_t tmask, int32_t k, uint32_t i) {
-    const unsigned long long v = g | ((unsigned long long)i << 32) | (uint32_t)k;
+  __device__ __forceinline__ unsigned long long val(int32_t k, uint32_t i) const {
+    return ((unsigned long long)(i + 1) << 32) | (uint32_t)k;
+  }
+  __device__ __forceinline__ unsigned long long cas(uint32_t s, int32_t k, uint32_t i) {
+    return atomicCAS(&slot[s], 0ull, val(k, i));
+  }
+  // continue an insert whose first CAS at slot s returned `old` != 0 (slot taken)
+  __device__ bool insert_rest(uint32_t s, uint32_t tmask, int32_t k, uint32_t i, unsigned long long old) {
     bool dup = false;
-    unsigned long long old = slot[s];
-    for (;;) {
-      if (!live(old)) {
-        const unsigned long long prev = atomicCAS(&slot[s], old, v);
-        if (prev == old) return dup;
-        old = prev;  // lost the race: re-examine the same slot
-        continue;
-      }
+    while (old != 0ull) {
       dup |= (uint32_t)old == (uint32_t)k;
       s = (s + 1) & tmask;
-      old = slot[s];
+      old = atomicCAS(&slot[s], 0ull, val(k, i));
     }
+    return dup;
   }
-  // calls f(index) for every build tuple with key == k (the first one if UNIQUE)
-  template <bool UNIQUE = false, typename F>
-  __device__ void probe(uint32_t s, uint32_t tmask, int32_t k, F f) const {
-    for (unsigned long long v; live(v = slot[s]); s = (s + 1) & tmask)
-      if ((uint32_t)v == (uint32_t)k) {
-        f((uint32_t)(v >> 32) & 0xFFFu);
-        if (UNIQUE) break;
-      }
-  }
+  __device__ __forceinline__ unsigned long long first(uint32_t s) const { return slot[s]; }
+  __device__ __forceinline__ bool empty(unsigned long long v) const { return v == 0ull; }
+  __device__ __forceinline__ bool is(unsigned long long v, int32_t k) const { return (uint32_t)v == (uint32_t)k; }
+  __device__ __forceinline__ uint32_t index(unsigned long long v) const { return (uint32_t)(v >> 32) - 1; }
+  __device__ __forceinline__ unsigned long long at(uint32_t s) const { return slot[s]; }
 };
 template <> struct Table<int64_t> {
   uint32_t* slot;
   int64_t* bk;
   static constexpr size_t kBytes = TAB_MAX * 4 + BCH_MAX * 8;
+  static constexpr bool kStaged = true;
   __device__ void init(uint8_t* base) {
     slot = reinterpret_cast<uint32_t*>(base);
     bk = reinterpret_cast<int64_t*>(slot + TAB_MAX);
   }
   __device__ void clear(uint32_t T) {
-    for (uint32_t i = threadIdx.x; i < T; i += HT) slot[i] = 0u;
+    uint4* p = reinterpret_cast<uint4*>(slot);
+    for (uint32_t i = threadIdx.x; i < T / 4; i += HT) p[i] = make_uint4(0, 0, 0, 0);
   }
   __device__ void stage(uint32_t i, int64_t k) { bk[i] = k; }
-  __device__ bool insert(uint32_t s, uint32_t tmask, int64_t k, uint32_t i) {
+  __device__ __forceinline__ uint32_t cas(uint32_t s, int64_t, uint32_t i) { return atomicCAS(&slot[s], 0u, i + 1); }
+  __device__ bool insert_rest(uint32_t s, uint32_t tmask, int64_t k, uint32_t i, uint32_t old) {
     bool dup = false;
-    for (uint32_t old; (old = atomicCAS(&slot[s], 0u, i + 1)) != 0u; s = (s + 1) & tmask)
+    while (old != 0u) {
       dup |= bk[old - 1] == k;
+      s = (s + 1) & tmask;
+      old = atomicCAS(&slot[s], 0u, i + 1);
+    }
     return dup;
   }
-  template <bool UNIQUE = false, typename F>
-  __device__ void probe(uint32_t s, uint32_t tmask, int64_t k, F f) const {
-    for (uint32_t v; (v = slot[s]) != 0u; s = (s + 1) & tmask)
-      if (bk[v - 1] == k) {
-        f(v - 1);
-        if (UNIQUE) break;
-      }
-  }
+  __device__ __forceinline__ uint32_t first(uint32_t s) const { return slot[s]; }
+  __device__ __forceinline__ bool empty(uint32_t v) const { return v == 0u; }
+  __device__ __forceinline__ bool is(uint32_t v, int64_t k) const { return bk[v - 1] == k; }
+  __device__ __forceinline__ uint32_t index(uint32_t v) const { return v - 1; }
+  __device__ __forceinline__ uint32_t at(uint32_t s) const { return slot[s]; }
 };
-
-// One unit's keys, held in registers (the software-pipelined prefetch buffer).
-template <typename K>
-struct UnitKeys {
-  K kb[BPT];
-  K kp[PPT];
-};
-
-__device__ __forceinline__ void probe_range(uint32_t pn, uint32_t w, uint32_t& wb, uint32_t& we) {
-  const uint32_t per_w = (pn + HW - 1) / HW;
-  wb = min(w * per_w, pn);
-  we = min(wb + per_w, pn);
-}
-
-template <typename K>
-__device__ __forceinline__ void load_keys(UnitKeys<K>& R, const uint4 d, const HJArgs& a, uint32_t tid, uint32_t w,
-                                          uint32_t lane) {
-  const K* __restrict__ bkey = static_cast<const K*>(a.bkey);
-  const K* __restrict__ pkey = static_cast<const K*>(a.pkey);
-#pragma unroll
-  for (int j = 0; j < BPT; ++j) {
-    // int32: stop at the unit's end (CTA-uniform branch) instead of predicating off
-    // loads sized for the maximum (C2 0.835 -> 0.808 ms; int64 measured slower with it)
-    if (sizeof(K) == 4 && (uint32_t)j * HT >= d.y) break;
-    const uint32_t i = tid + j * HT;
-    R.kb[j] = i < d.y ? bkey[d.x + i] : K(0);
-  }
-  uint32_t wb, we;
-  probe_range(d.w, w, wb, we);
-#pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    if (sizeof(K) == 4 && wb + 32 * j >= we) break;  // warp-uniform
-    const uint32_t i = wb + lane + 32 * j;
-    R.kp[j] = i < we ? pkey[d.z + i] : K(0);
-  }
-}
 
 // Table size: ~4 slots per build tuple (load factor <= 1/4 keeps the longest probe
 // walk of a warp short), at least 2 per tuple within the TAB_MAX budget.
@@ -199,11 +182,79 @@ __device__ __forceinline__ uint32_t table_logT(uint32_t bn) {
   return min(want, (uint32_t)(31 - __clz(TAB_MAX)));
 }
 
+// Build: the unit's build keys (16-byte vectors, KVN keys each) into the table.  The
+// first CAS of all KVN keys of a vector is issued back to back; collisions are
+// resolved afterwards.  Returns true if a duplicate build key was seen.
+template <typename K>
+__device__ __forceinline__ bool build_vec(Table<K>& tab, uint4 x, uint32_t v, const Span& sb, uint32_t bn,
+                                          uint32_t tmask, uint32_t tshift) {
+  constexpr uint32_t N = KVec<K>::N;
+  const KVec<K> kv(x);
+  decltype(tab.cas(0, K(0), 0)) old[N];
+  uint32_t s[N];
+  bool dup = false;
+#pragma unroll
+  for (uint32_t q = 0; q < N; ++q) {
+    const uint32_t j = v * N + q - sb.shift;  // wraps for the elements before the range
+    s[q] = slot_hash(kv.k[q]) >> tshift;
+    old[q] = j < bn ? tab.cas(s[q], kv.k[q], j) : 0;
+  }
+#pragma unroll
+  for (uint32_t q = 0; q < N; ++q) {
+    const uint32_t j = v * N + q - sb.shift;
+    if (j < bn && !tab.empty(old[q])) dup |= tab.insert_rest(s[q], tmask, kv.k[q], j, old[q]);
+  }
+  return dup;
+}
+
+template <typename K>
+__device__ __forceinline__ void stage_vec(Table<K>& tab, uint4 x, uint32_t v, const Span& sb, uint32_t bn) {
+  constexpr uint32_t N = KVec<K>::N;
+  const KVec<K> kv(x);
+#pragma unroll
+  for (uint32_t q = 0; q < N; ++q) {
+    const uint32_t j = v * N + q - sb.shift;
+    if (j < bn) tab.stage(j, kv.k[q]);
+  }
+}
+
 // Count pass.  Per probe row it also records the matching build index inside the
 // unit's build chunk (uint16; NO_MATCH / MULTI sentinels), so the write pass can
 // emit pairs without rebuilding the table (units holding a MULTI row are flagged
 // and re-probed by the write pass).
 constexpr uint16_t NO_MATCH = 0xFFFF, MULTI = 0xFFFE;
+
+template <typename K>
+__device__ __forceinline__ void probe_vec(const Table<K>& tab, uint4 x, uint32_t v, const Span& sp, uint32_t pn,
+                                          uint32_t tmask, uint32_t tshift, bool unique, uint16_t* __restrict__ st,
+                                          uint32_t& c, bool& many) {
+  constexpr uint32_t N = KVec<K>::N;
+  const KVec<K> kv(x);
+  decltype(tab.first(0)) f0[N];
+  uint32_t s[N];
+#pragma unroll
+  for (uint32_t q = 0; q < N; ++q) {  // first probe step of every key, back to back
+    const uint32_t j = v * N + q - sp.shift;
+    s[q] = slot_hash(kv.k[q]) >> tshift;
+    f0[q] = j < pn ? tab.first(s[q]) : 0;
+  }
+#pragma unroll
+  for (uint32_t q = 0; q < N; ++q) {
+    const uint32_t j = v * N + q - sp.shift;
+    if (j >= pn) continue;
+    uint32_t m = 0, f = 0, ss = s[q];
+    for (auto e = f0[q]; !tab.empty(e); e = tab.at(ss = (ss + 1) & tmask)) {
+      if (tab.is(e, kv.k[q])) {
+        f = tab.index(e);
+        ++m;
+        if (unique) break;
+      }
+    }
+    c += m;
+    many |= m > 1;
+    st[j] = m == 0 ? NO_MATCH : (m == 1 ? (uint16_t)f : MULTI);
+  }
+}
 
 template <typename K>
 __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __restrict__ stage,
@@ -217,247 +268,182 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
   const uint32_t G = gridDim.x;
   uint32_t u = blockIdx.x;
   if (u >= a.U) return;
+  tab.clear(TAB_MAX);
   const uint4 zero = make_uint4(0, 0, 0, 0);
+  // register prefetch of the next unit: its first two build and probe vectors per thread
+  // (a 2048-key int32 unit needs at most 2 of each)
+  auto fetch = [&](const uint4 dd, uint4 (&bv)[2], uint4 (&pv)[2]) {
+    const Span sb = span16(a.bkey, dd.x, dd.y, sizeof(K)), sp = span16(a.pkey, dd.z, dd.w, sizeof(K));
+    uint32_t vb, ve;
+    warp_vecs(sp.nv, w, vb, ve);
+#pragma unroll
+    for (uint32_t i = 0; i < 2; ++i) {
+      bv[i] = tid + i * HT < sb.nv ? ldv(sb, tid + i * HT) : zero;
+      pv[i] = vb + lane + 32 * i < ve ? ldv(sp, vb + lane + 32 * i) : zero;
+    }
+  };
   uint4 d = a.desc[u];
-  uint4 dn = u + G < a.U ? a.desc[u + G] : zero;
-  UnitKeys<K> cur;
-  load_keys(cur, d, a, tid, w, lane);
-
+  uint4 bv[2], pv[2];
+  fetch(d, bv, pv);
   for (; u < a.U; u += G) {
-    UnitKeys<K> nxt;  // prefetch the next unit while this one is built and probed
-    load_keys(nxt, dn, a, tid, w, lane);
-    const uint4 dnn = u + 2 * G < a.U ? a.desc[u + 2 * G] : zero;
+    const uint4 dn = u + G < a.U ? a.desc[u + G] : zero;
+    uint4 nbv[2], npv[2];
+    fetch(dn, nbv, npv);
     const uint32_t bn = d.y, pn = d.w;
     const uint32_t logT = table_logT(bn);
     const uint32_t T = 1u << logT, tmask = T - 1, tshift = 32 - logT;
-
-    tab.clear(T);
+    const Span sb = span16(a.bkey, d.x, bn, sizeof(K));
+    if (Table<K>::kStaged) {  // int64: keys staged first (inserts compare staged keys)
+      if (tid < sb.nv) stage_vec(tab, bv[0], tid, sb, bn);
+      if (tid + HT < sb.nv) stage_vec(tab, bv[1], tid + HT, sb, bn);
+      for (uint32_t v = tid + 2 * HT; v < sb.nv; v += HT) stage_vec(tab, ldv(sb, v), v, sb, bn);
+    }
     if (tid == 0) s_dup = 0;
-    // loops sized for the 2048-tuple maximum exit early (CTA/warp-uniform) for the
-    // usual ~1024-tuple units
-#pragma unroll
-    for (int j = 0; j < BPT; ++j) {
-      if ((uint32_t)j * HT >= bn) break;
-      const uint32_t i = tid + j * HT;
-      if (i < bn) tab.stage(i, cur.kb[j]);
-    }
-    __syncthreads();
+    __syncthreads();  // table cleared (and keys staged)
     bool dup = false;
-#pragma unroll
-    for (int j = 0; j < BPT; ++j) {
-      if ((uint32_t)j * HT >= bn) break;
-      const uint32_t i = tid + j * HT;
-      if (i < bn) dup |= tab.insert(slot_hash(cur.kb[j]) >> tshift, tmask, cur.kb[j], i);
-    }
+    if (tid < sb.nv) dup |= build_vec(tab, bv[0], tid, sb, bn, tmask, tshift);
+    if (tid + HT < sb.nv) dup |= build_vec(tab, bv[1], tid + HT, sb, bn, tmask, tshift);
+    for (uint32_t v = tid + 2 * HT; v < sb.nv; v += HT) dup |= build_vec(tab, ldv(sb, v), v, sb, bn, tmask, tshift);
     if (__any_sync(FULL, dup) && lane == 0) s_dup = 1;
     __syncthreads();
     const bool unique = s_dup == 0;  // no duplicate build key: stop each probe at its first match
 
-    uint32_t wb, we;
-    probe_range(pn, w, wb, we);
+    const Span sp = span16(a.pkey, d.z, pn, sizeof(K));
+    uint32_t vb, ve;
+    warp_vecs(sp.nv, w, vb, ve);
+    uint16_t* st = stage + d.z;
     uint32_t c = 0;
     bool many = false;
-#pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      if (wb + 32 * j >= we) break;  // warp-uniform
-      const uint32_t i = wb + lane + 32 * j;
-      if (i < we) {
-        const K k = cur.kp[j];
-        const uint32_t s0 = slot_hash(k) >> tshift;
-        uint32_t m = 0, f = 0;
-        auto hit = [&](uint32_t idx) {
-          f = idx;
-          ++m;
-        };
-        if (unique) tab.template probe<true>(s0, tmask, k, hit);
-        else tab.template probe<false>(s0, tmask, k, hit);
-        c += m;
-        many |= m > 1;
-        stage[d.z + i] = m == 0 ? NO_MATCH : (m == 1 ? (uint16_t)f : MULTI);
-      }
-    }
+    if (vb + lane < ve) probe_vec(tab, pv[0], vb + lane, sp, pn, tmask, tshift, unique, st, c, many);
+    if (vb + lane + 32 < ve) probe_vec(tab, pv[1], vb + lane + 32, sp, pn, tmask, tshift, unique, st, c, many);
+    for (uint32_t v = vb + lane + 64; v < ve; v += 32)
+      probe_vec(tab, ldv(sp, v), v, sp, pn, tmask, tshift, unique, st, c, many);
     c = warp_sum(c);
     if (lane == 0) a.wcnt[(uint64_t)u * HW + w] = c;
     if (__any_sync(FULL, many) && lane == 0) {
       multi[u] = 1;
       atomicAdd(nmulti, 1ull);  // > 0 tells the host to launch the MULTI write pass
     }
-    __syncthreads();
-    cur = nxt;
+    __syncthreads();  // every probe of this unit is done
+    tab.clear(T);
     d = dn;
-    dn = dnn;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      bv[i] = nbv[i];
+      pv[i] = npv[i];
+    }
   }
 }
 
-// Write pass.  Normal units: stage the build rids in shared memory, then every warp
-// walks its probe rows in order, ranks the rows with a match by a shuffle scan and
-// writes (rid_R, rid_S) at its scanned offset -- a gather, no hashing.  Units with
-// a MULTI row rebuild the table and re-probe (bag semantics with duplicate keys).
+// Write pass for units with a MULTI row (duplicate build keys) or a partition split
+// over several build chunks: rebuild the table, re-probe, and write every match of
+// a probe row at the warp's scanned offset (same row -> warp map as the count pass).
 template <typename K>
-__global__ void __launch_bounds__(HT) hj_write_kernel(HJArgs a, const uint16_t* __restrict__ stage,
-                                                      const uint8_t* __restrict__ multi, int only_full) {
+__global__ void __launch_bounds__(HT) hj_write_kernel(HJArgs a, const uint8_t* __restrict__ multi) {
   extern __shared__ __align__(16) uint8_t smem[];
   Table<K> tab;
   tab.init(smem);
-  uint32_t* br = reinterpret_cast<uint32_t*>(smem + Table<K>::kBytes);  // BCH_MAX
-  const K* __restrict__ bkey = static_cast<const K*>(a.bkey);
-  const K* __restrict__ pkey = static_cast<const K*>(a.pkey);
+  uint32_t* br = reinterpret_cast<uint32_t*>(smem + Table<K>::kBytes);  // BCH_MAX build rids
+  constexpr uint32_t N = KVec<K>::N;
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
-
+  tab.clear(TAB_MAX);
   for (uint32_t u = blockIdx.x; u < a.U; u += gridDim.x) {
-    const bool full = multi[u] != 0;
-    if (only_full && !full) continue;  // CTA-uniform: hj_write_fast wrote this unit
+    if (!multi[u]) continue;  // CTA-uniform: hj_write_fast wrote this unit
     const uint4 d = a.desc[u];
     const uint32_t bn = d.y, pn = d.w;
-    uint32_t wb, we;
-    probe_range(pn, w, wb, we);
-    // probe-side inputs of this warp's rows, all loads in flight at once
-    uint32_t prow[PPT];
-    uint16_t sidx[PPT];
-#pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      const uint32_t i = wb + lane + 32 * j;
-      prow[j] = i < we ? (a.prid ? a.prid[d.z + i] : a.prid_base + d.z + i) : 0u;
-      sidx[j] = i < we ? stage[d.z + i] : NO_MATCH;
-    }
     const uint32_t logT = table_logT(bn);
     const uint32_t T = 1u << logT, tmask = T - 1, tshift = 32 - logT;
-    if (full) tab.clear(T);
-#pragma unroll
-    for (int j = 0; j < BPT; ++j) {
-      const uint32_t i = tid + j * HT;
-      if (i < bn) br[i] = a.brid ? a.brid[d.x + i] : a.brid_base + d.x + i;
-    }
+    const Span sb = span16(a.bkey, d.x, bn, sizeof(K));
+    for (uint32_t i = tid; i < bn; i += HT) br[i] = a.brid ? a.brid[d.x + i] : a.brid_base + d.x + i;
+    if (Table<K>::kStaged)
+      for (uint32_t v = tid; v < sb.nv; v += HT) stage_vec(tab, ldv(sb, v), v, sb, bn);
     __syncthreads();
-    if (full) {
-      K kb[BPT];
-#pragma unroll
-      for (int j = 0; j < BPT; ++j) {
-        const uint32_t i = tid + j * HT;
-        kb[j] = i < bn ? bkey[d.x + i] : K(0);
-        if (i < bn) tab.stage(i, kb[j]);
-      }
-      __syncthreads();
-#pragma unroll
-      for (int j = 0; j < BPT; ++j) {
-        const uint32_t i = tid + j * HT;
-        if (i < bn) tab.insert(slot_hash(kb[j]) >> tshift, tmask, kb[j], i);
-      }
-      __syncthreads();
-    }
+    for (uint32_t v = tid; v < sb.nv; v += HT) build_vec(tab, ldv(sb, v), v, sb, bn, tmask, tshift);
+    __syncthreads();
+    const Span sp = span16(a.pkey, d.z, pn, sizeof(K));
+    uint32_t vb, ve;
+    warp_vecs(sp.nv, w, vb, ve);
     uint64_t base = a.woff[(uint64_t)u * HW + w];
-#pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      if (wb + 32 * j >= we) break;  // warp-uniform
-      const uint32_t i = wb + lane + 32 * j;
-      const bool valid = i < we;
+    for (uint32_t v0 = vb; v0 < ve; v0 += 32) {  // warp-uniform
+      const uint32_t v = v0 + lane;
+      const KVec<K> kv(v < ve ? ldv(sp, v) : make_uint4(0, 0, 0, 0));
       uint32_t m = 0;
-      K k = K(0);
-      uint32_t s0 = 0;
-      if (full) {
-        if (valid) {
-          k = pkey[d.z + i];
-          s0 = slot_hash(k) >> tshift;
-          tab.probe(s0, tmask, k, [&](uint32_t) { ++m; });
+#pragma unroll
+      for (uint32_t q = 0; q < N; ++q) {
+        const uint32_t j = v * N + q - sp.shift;
+        if (v < ve && j < pn) {
+          uint32_t ss = slot_hash(kv.k[q]) >> tshift;
+          for (auto e = tab.at(ss); !tab.empty(e); e = tab.at(ss = (ss + 1) & tmask)) m += tab.is(e, kv.k[q]);
         }
-      } else {
-        m = sidx[j] != NO_MATCH ? 1u : 0u;
       }
       const uint32_t incl = warp_incl_scan(m);
       uint64_t pos = base + (incl - m);
-      if (m) {
-        if (full) {
-          tab.probe(s0, tmask, k, [&](uint32_t idx) {
-            const uint32_t brow = br[idx];
-            a.out[pos++] = a.swap ? make_uint2(prow[j], brow) : make_uint2(brow, prow[j]);
-          });
-        } else {
-          const uint32_t brow = br[sidx[j]];
-          a.out[pos] = a.swap ? make_uint2(prow[j], brow) : make_uint2(brow, prow[j]);
+#pragma unroll
+      for (uint32_t q = 0; q < N; ++q) {
+        const uint32_t j = v * N + q - sp.shift;
+        if (v < ve && j < pn && m) {
+          const uint32_t prow = a.prid ? a.prid[d.z + j] : a.prid_base + d.z + j;
+          uint32_t ss = slot_hash(kv.k[q]) >> tshift;
+          for (auto e = tab.at(ss); !tab.empty(e); e = tab.at(ss = (ss + 1) & tmask))
+            if (tab.is(e, kv.k[q])) {
+              const uint32_t brow = br[tab.index(e)];
+              a.out[pos++] = a.swap ? make_uint2(prow, brow) : make_uint2(brow, prow);
+            }
         }
       }
       base += __shfl_sync(FULL, incl, 31);
     }
+    __syncthreads();  // the table and br are rebuilt by the next unit
+    tab.clear(T);
     __syncthreads();
   }
 }
 
-// Fast write pass for units without a MULTI row (the usual case): no hash table.
-// The next unit's build rids, probe rids and staged match indices are streamed into
-// a second shared-memory buffer by 1-D TMA bulk copies (16-byte aligned windows,
-// elements outside a window read from global memory) while this unit is written.
-struct WBuf {
-  uint32_t br[BCH_MAX + 4];
-  uint32_t pr[PCH_MAX + 4];
-  uint16_t st[PCH_MAX + 8];
-};
-static_assert(sizeof(WBuf) % 16 == 0, "16-byte aligned buffers");
-
-__device__ __forceinline__ void wf_issue(WBuf& B, uint64_t* bar, const uint4 d, const HJArgs& a,
-                                         const uint16_t* stage) {
-  fence_proxy_async();  // generic reads of this buffer (previous unit) before the async writes
-  const Win wb = a.brid ? bulk_window(a.brid, d.x, d.y, 4, a.nb) : Win{nullptr, 0, 0, 0};
-  const Win wp = a.prid ? bulk_window(a.prid, d.z, d.w, 4, a.np) : Win{nullptr, 0, 0, 0};
-  const Win ws = bulk_window(stage, d.z, d.w, 2, a.np);
-  const uint32_t bytes = wb.bytes + wp.bytes + ws.bytes;
-  if (!bytes) {
-    mbar_arrive(bar);
-    return;
-  }
-  mbar_expect_tx(bar, bytes);
-  if (wb.bytes) bulk_g2s(B.br, wb.src, wb.bytes, bar);
-  if (wp.bytes) bulk_g2s(B.pr, wp.src, wp.bytes, bar);
-  if (ws.bytes) bulk_g2s(B.st, ws.src, ws.bytes, bar);
-}
-
-__global__ void __launch_bounds__(HT) hj_write_fast(HJArgs a, const uint16_t* __restrict__ stage,
-                                                    const uint8_t* __restrict__ multi) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  WBuf* B = reinterpret_cast<WBuf*>(smem);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * sizeof(WBuf));
-  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
-  const uint32_t G = gridDim.x;
-  uint32_t u = blockIdx.x;
-  if (u >= a.U) return;
-  if (tid == 0) {
-    mbar_init(bar + 0, 1);
-    mbar_init(bar + 1, 1);
-    fence_mbar_init();
-    wf_issue(B[0], bar + 0, a.desc[u], a, stage);
-  }
-  __syncthreads();
-  for (uint32_t it = 0; u < a.U; u += G, ++it) {
-    const uint32_t b = it & 1;
+// Write pass for units without a MULTI row (the usual case): a table-free gather.
+// Warp task (unit u, warp w) covers the same probe rows as warp w of the count pass;
+// each lane takes one 16-byte key vector's rows (KVN consecutive rows), reads their
+// staged match indices, ranks its matches by a warp scan and writes (rid_R, rid_S)
+// at the task's scanned offset -- deterministic positions, rows in order.  Build
+// rids are gathered through the read-only cache (a unit's build chunk is <= 16 KB).
+template <typename K>
+__global__ void __launch_bounds__(256) hj_write_fast(HJArgs a, const uint16_t* __restrict__ stage,
+                                                     const uint8_t* __restrict__ multi) {
+  constexpr uint32_t N = KVec<K>::N;
+  const uint32_t lane = lane_id();
+  const uint64_t ntask = (uint64_t)a.U * HW;
+  const uint64_t nwarp = (uint64_t)gridDim.x * (blockDim.x / 32);
+  for (uint64_t task = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; task < ntask; task += nwarp) {
+    const uint32_t u = (uint32_t)(task / HW), w = (uint32_t)(task % HW);
+    if (multi[u]) continue;  // warp-uniform: hj_write_kernel writes this unit
     const uint4 d = a.desc[u];
-    if (tid == 0 && u + G < a.U) wf_issue(B[b ^ 1], bar + (b ^ 1), a.desc[u + G], a, stage);
-    const bool full = multi[u] != 0;
-    mbar_wait(bar + b, (it >> 1) & 1);
-    if (!full) {
-      const Win wb = a.brid ? bulk_window(a.brid, d.x, d.y, 4, a.nb) : Win{nullptr, 0, 0, 0};
-      const Win wp = a.prid ? bulk_window(a.prid, d.z, d.w, 4, a.np) : Win{nullptr, 0, 0, 0};
-      const Win ws = bulk_window(stage, d.z, d.w, 2, a.np);
-      const WBuf& Bb = B[b];
-      uint32_t wlo, whi;
-      probe_range(d.w, w, wlo, whi);
-      uint64_t base = a.woff[(uint64_t)u * HW + w];
-      for (uint32_t r0 = wlo; r0 < whi; r0 += 32) {  // warp-uniform
-        const uint32_t i = r0 + lane;
-        const bool valid = i < whi;
-        const uint16_t sx = valid ? (i < ws.valid ? Bb.st[ws.shift + i] : stage[d.z + i]) : NO_MATCH;
-        const bool m = sx != NO_MATCH;
-        // at most one match per row here: ranks are a ballot + popc, not a scan
-        const uint32_t bal = __ballot_sync(FULL, m);
-        if (m) {
-          const uint32_t prow = a.prid ? (i < wp.valid ? Bb.pr[wp.shift + i] : a.prid[d.z + i])
-                                       : a.prid_base + d.z + i;
-          const uint32_t brow = a.brid ? (sx < wb.valid ? Bb.br[wb.shift + sx] : a.brid[d.x + sx])
-                                       : a.brid_base + d.x + sx;
-          a.out[base + __popc(bal & lanemask_lt())] = a.swap ? make_uint2(prow, brow) : make_uint2(brow, prow);
-        }
-        base += __popc(bal);
+    const uint32_t pn = d.w;
+    const Span sp = span16(a.pkey, d.z, pn, sizeof(K));
+    uint32_t vb, ve;
+    warp_vecs(sp.nv, w, vb, ve);
+    uint64_t base = a.woff[task];
+    const uint16_t* st = stage + d.z;
+    for (uint32_t v0 = vb; v0 < ve; v0 += 32) {  // warp-uniform
+      const uint32_t v = v0 + lane;
+      uint32_t sx[N], m = 0;
+#pragma unroll
+      for (uint32_t q = 0; q < N; ++q) {
+        const uint32_t j = v * N + q - sp.shift;
+        sx[q] = (v < ve && j < pn) ? st[j] : NO_MATCH;
+        m += sx[q] != NO_MATCH;
       }
+      const uint32_t incl = warp_incl_scan(m);
+      uint64_t pos = base + (incl - m);
+#pragma unroll
+      for (uint32_t q = 0; q < N; ++q) {
+        if (sx[q] != NO_MATCH) {
+          const uint32_t j = v * N + q - sp.shift;
+          const uint32_t prow = a.prid ? a.prid[d.z + j] : a.prid_base + d.z + j;
+          const uint32_t brow = a.brid ? __ldg(a.brid + d.x + sx[q]) : a.brid_base + d.x + sx[q];
+          a.out[pos++] = a.swap ? make_uint2(prow, brow) : make_uint2(brow, prow);
+        }
+      }
+      base += __shfl_sync(FULL, incl, 31);
     }
-    __syncthreads();  // buffer b is refilled by the issue of iteration it + 1
   }
 }
 
@@ -587,8 +573,6 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
   a.U = U;
   a.wcnt = wcnt;
   a.swap = swap;
-  a.nb = Bld.n;
-  a.np = Prb.n;
   {
     const size_t smem = hj_smem<K, false>();
     set_smem(ctx, hj_count_kernel<K>, smem);
@@ -620,19 +604,21 @@ void write_impl(gj_ctx* ctx, uint32_t* out) {
   a.woff = jc.woff;
   a.out = reinterpret_cast<uint2*>(out);
   a.swap = jc.swap;
-  a.nb = Bld.n;
-  a.np = Prb.n;
-  // units without a MULTI row: table-free gather with TMA prefetch; then the rare
-  // MULTI units rebuild their table and re-probe
-  const size_t fsmem = 2 * sizeof(WBuf) + 16;
-  set_smem(ctx, hj_write_fast, fsmem);
-  launch(ctx, "hj_write", hj_write_fast, dim3(hj_grid(ctx, hj_write_fast, fsmem, a.U)), dim3(HT), fsmem, a,
-         (const uint16_t*)jc.stage, (const uint8_t*)jc.multi);
+  // units without a MULTI row: table-free gather (warp tasks); then the rare MULTI
+  // units rebuild their table and re-probe
+  {
+    int occ = 0;
+    GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hj_write_fast<K>, 256, 0));
+    const uint64_t tasks = (uint64_t)a.U * HW;
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((tasks + 7) / 8, (uint64_t)ctx->num_sms * std::max(occ, 1));
+    launch(ctx, "hj_write", hj_write_fast<K>, dim3(grid), dim3(256), 0, a, (const uint16_t*)jc.stage,
+           (const uint8_t*)jc.multi);
+  }
   if (jc.nmulti == 0) return;
   const size_t smem = hj_smem<K, true>();
   set_smem(ctx, hj_write_kernel<K>, smem);
   launch(ctx, "hj_write_multi", hj_write_kernel<K>, dim3(hj_grid(ctx, hj_write_kernel<K>, smem, a.U)), dim3(HT),
-         smem, a, (const uint16_t*)jc.stage, (const uint8_t*)jc.multi, 1);
+         smem, a, (const uint8_t*)jc.multi);
 }
 
 }  // namespace

@@ -224,10 +224,13 @@ __device__ __forceinline__ void stage_vec(Table<K>& tab, uint4 x, uint32_t v, co
 // and re-probed by the write pass).
 constexpr uint16_t NO_MATCH = 0xFFFF, MULTI = 0xFFFE;
 
+// Probe the KVN keys of one vector; st = stage + unit's first probe row.  vec: the
+// stage array has the key array's vector phase, so a vector whose rows all lie in
+// the unit stores its KVN indices with one store.
 template <typename K>
 __device__ __forceinline__ void probe_vec(const Table<K>& tab, uint4 x, uint32_t v, const Span& sp, uint32_t pn,
                                           uint32_t tmask, uint32_t tshift, bool unique, uint16_t* __restrict__ st,
-                                          uint32_t& c, bool& many) {
+                                          bool vec, uint32_t& c, bool& many) {
   constexpr uint32_t N = KVec<K>::N;
   const KVec<K> kv(x);
   decltype(tab.first(0)) f0[N];
@@ -238,10 +241,12 @@ __device__ __forceinline__ void probe_vec(const Table<K>& tab, uint4 x, uint32_t
     s[q] = slot_hash(kv.k[q]) >> tshift;
     f0[q] = j < pn ? tab.first(s[q]) : 0;
   }
+  uint32_t res[N];
+  const uint32_t j0 = v * N - sp.shift;
 #pragma unroll
   for (uint32_t q = 0; q < N; ++q) {
-    const uint32_t j = v * N + q - sp.shift;
-    if (j >= pn) continue;
+    res[q] = NO_MATCH;
+    if (j0 + q >= pn) continue;
     uint32_t m = 0, f = 0, ss = s[q];
     for (auto e = f0[q]; !tab.empty(e); e = tab.at(ss = (ss + 1) & tmask)) {
       if (tab.is(e, kv.k[q])) {
@@ -252,7 +257,17 @@ __device__ __forceinline__ void probe_vec(const Table<K>& tab, uint4 x, uint32_t
     }
     c += m;
     many |= m > 1;
-    st[j] = m == 0 ? NO_MATCH : (m == 1 ? (uint16_t)f : MULTI);
+    res[q] = m == 0 ? NO_MATCH : (m == 1 ? f : MULTI);
+  }
+  if (vec && j0 < pn && j0 + N - 1 < pn) {
+    if (N == 4)
+      *reinterpret_cast<uint2*>(st + j0) = make_uint2(res[0] | res[1 % N] << 16, res[2 % N] | res[3 % N] << 16);
+    else
+      *reinterpret_cast<uint32_t*>(st + j0) = res[0] | res[1 % N] << 16;
+  } else {
+#pragma unroll
+    for (uint32_t q = 0; q < N; ++q)
+      if (j0 + q < pn) st[j0 + q] = (uint16_t)res[q];
   }
 }
 
@@ -270,6 +285,9 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
   if (u >= a.U) return;
   tab.clear(TAB_MAX);
   const uint4 zero = make_uint4(0, 0, 0, 0);
+  constexpr uint32_t N = KVec<K>::N;
+  const bool vec = reinterpret_cast<uint64_t>(stage) % (2 * N) == 0 &&
+                   (reinterpret_cast<uint64_t>(a.pkey) / sizeof(K)) % N == 0;
   // register prefetch of the next unit: its first two build and probe vectors per thread
   // (a 2048-key int32 unit needs at most 2 of each)
   auto fetch = [&](const uint4 dd, uint4 (&bv)[2], uint4 (&pv)[2]) {
@@ -314,10 +332,10 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
     uint16_t* st = stage + d.z;
     uint32_t c = 0;
     bool many = false;
-    if (vb + lane < ve) probe_vec(tab, pv[0], vb + lane, sp, pn, tmask, tshift, unique, st, c, many);
-    if (vb + lane + 32 < ve) probe_vec(tab, pv[1], vb + lane + 32, sp, pn, tmask, tshift, unique, st, c, many);
+    if (vb + lane < ve) probe_vec(tab, pv[0], vb + lane, sp, pn, tmask, tshift, unique, st, vec, c, many);
+    if (vb + lane + 32 < ve) probe_vec(tab, pv[1], vb + lane + 32, sp, pn, tmask, tshift, unique, st, vec, c, many);
     for (uint32_t v = vb + lane + 64; v < ve; v += 32)
-      probe_vec(tab, ldv(sp, v), v, sp, pn, tmask, tshift, unique, st, c, many);
+      probe_vec(tab, ldv(sp, v), v, sp, pn, tmask, tshift, unique, st, vec, c, many);
     c = warp_sum(c);
     if (lane == 0) a.wcnt[(uint64_t)u * HW + w] = c;
     if (__any_sync(FULL, many) && lane == 0) {
@@ -400,16 +418,24 @@ __global__ void __launch_bounds__(HT) hj_write_kernel(HJArgs a, const uint8_t* _
 }
 
 // Write pass for units without a MULTI row (the usual case): a table-free gather.
-// Warp task (unit u, warp w) covers the same probe rows as warp w of the count pass;
-// each lane takes one 16-byte key vector's rows (KVN consecutive rows), reads their
-// staged match indices, ranks its matches by a warp scan and writes (rid_R, rid_S)
-// at the task's scanned offset -- deterministic positions, rows in order.  Build
-// rids are gathered through the read-only cache (a unit's build chunk is <= 16 KB).
+// Warp task (unit u, warp w) covers the same probe rows as warp w of the count pass,
+// 32 key vectors (32 * KVN consecutive rows) per step: each lane reads its rows'
+// staged match indices (and probe rids), the warp ranks the matches by a scan, each
+// lane puts its (rid_R, rid_S) pairs into a warp-private shared-memory buffer at its
+// rank, and the warp copies the buffer to the task's output range with consecutive
+// lanes on consecutive pairs (fully coalesced stores).  Rows stay in order, so the
+// positions are deterministic.  When the stage and probe-rid arrays share the key
+// array's 16-byte phase (always, unless the caller's key view is unaligned and the
+// join has no radix pass) each lane reads its rows' indices / rids as one vector.
+// Build rids are gathered through the read-only cache (a build chunk is <= 16 KB).
+constexpr int WF_T = 256;  // threads per CTA of the write pass
 template <typename K>
-__global__ void __launch_bounds__(256) hj_write_fast(HJArgs a, const uint16_t* __restrict__ stage,
-                                                     const uint8_t* __restrict__ multi) {
+__global__ void __launch_bounds__(WF_T) hj_write_fast(HJArgs a, const uint16_t* __restrict__ stage,
+                                                      const uint8_t* __restrict__ multi) {
   constexpr uint32_t N = KVec<K>::N;
+  __shared__ uint2 buf[WF_T / 32][32 * N];
   const uint32_t lane = lane_id();
+  uint2* wb = buf[threadIdx.x / 32];
   const uint64_t ntask = (uint64_t)a.U * HW;
   const uint64_t nwarp = (uint64_t)gridDim.x * (blockDim.x / 32);
   for (uint64_t task = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; task < ntask; task += nwarp) {
@@ -418,31 +444,65 @@ __global__ void __launch_bounds__(256) hj_write_fast(HJArgs a, const uint16_t* _
     const uint4 d = a.desc[u];
     const uint32_t pn = d.w;
     const Span sp = span16(a.pkey, d.z, pn, sizeof(K));
+    // element e of the key array <-> stage[e], prid[e]: vector loads line up when the
+    // three arrays have the same phase modulo the vector's element count
+    const uint64_t kph = (reinterpret_cast<uint64_t>(a.pkey) / sizeof(K)) % N;
+    const bool vec = reinterpret_cast<uint64_t>(stage) % (2 * N) == 0 && kph == 0 &&
+                     (!a.prid || reinterpret_cast<uint64_t>(a.prid) % (4 * N) == 0);
     uint32_t vb, ve;
     warp_vecs(sp.nv, w, vb, ve);
     uint64_t base = a.woff[task];
     const uint16_t* st = stage + d.z;
     for (uint32_t v0 = vb; v0 < ve; v0 += 32) {  // warp-uniform
       const uint32_t v = v0 + lane;
-      uint32_t sx[N], m = 0;
+      const uint32_t j0 = v * N - sp.shift;  // row of element 0 (wraps below the range)
+      uint32_t sx[N], pr[N], m = 0;
+      if (vec && v < ve) {  // element 0 of my vector is array element d.z + j0, N-aligned
+        if (N == 4) {
+          const uint2 x = __ldg(reinterpret_cast<const uint2*>(st + j0));
+          sx[0] = x.x & 0xFFFF, sx[1] = x.x >> 16, sx[2 % N] = x.y & 0xFFFF, sx[3 % N] = x.y >> 16;
+        } else {
+          const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(st + j0));
+          sx[0] = x & 0xFFFF, sx[1] = x >> 16;
+        }
+        if (a.prid) {
+          if (N == 4) {
+            const uint4 y = __ldg(reinterpret_cast<const uint4*>(a.prid + d.z + j0));
+            pr[0] = y.x, pr[1] = y.y, pr[2 % N] = y.z, pr[3 % N] = y.w;
+          } else {
+            const uint2 y = __ldg(reinterpret_cast<const uint2*>(a.prid + d.z + j0));
+            pr[0] = y.x, pr[1] = y.y;
+          }
+        }
 #pragma unroll
-      for (uint32_t q = 0; q < N; ++q) {
-        const uint32_t j = v * N + q - sp.shift;
-        sx[q] = (v < ve && j < pn) ? st[j] : NO_MATCH;
-        m += sx[q] != NO_MATCH;
+        for (uint32_t q = 0; q < N; ++q)
+          if (j0 + q >= pn) sx[q] = NO_MATCH;  // outside the unit's rows
+      } else {
+#pragma unroll
+        for (uint32_t q = 0; q < N; ++q) {
+          const uint32_t j = j0 + q;
+          const bool ok = v < ve && j < pn;
+          sx[q] = ok ? st[j] : NO_MATCH;
+          pr[q] = ok && a.prid ? a.prid[d.z + j] : 0u;
+        }
       }
+#pragma unroll
+      for (uint32_t q = 0; q < N; ++q) m += sx[q] != NO_MATCH;
       const uint32_t incl = warp_incl_scan(m);
-      uint64_t pos = base + (incl - m);
+      const uint32_t tot = __shfl_sync(FULL, incl, 31);
+      uint32_t r = incl - m;
 #pragma unroll
       for (uint32_t q = 0; q < N; ++q) {
         if (sx[q] != NO_MATCH) {
-          const uint32_t j = v * N + q - sp.shift;
-          const uint32_t prow = a.prid ? a.prid[d.z + j] : a.prid_base + d.z + j;
+          const uint32_t prow = a.prid ? pr[q] : a.prid_base + d.z + j0 + q;
           const uint32_t brow = a.brid ? __ldg(a.brid + d.x + sx[q]) : a.brid_base + d.x + sx[q];
-          a.out[pos++] = a.swap ? make_uint2(prow, brow) : make_uint2(brow, prow);
+          wb[r++] = a.swap ? make_uint2(prow, brow) : make_uint2(brow, prow);
         }
       }
-      base += __shfl_sync(FULL, incl, 31);
+      __syncwarp();
+      for (uint32_t t = lane; t < tot; t += 32) a.out[base + t] = wb[t];
+      __syncwarp();
+      base += tot;
     }
   }
 }
@@ -608,10 +668,11 @@ void write_impl(gj_ctx* ctx, uint32_t* out) {
   // units rebuild their table and re-probe
   {
     int occ = 0;
-    GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hj_write_fast<K>, 256, 0));
+    GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hj_write_fast<K>, WF_T, 0));
     const uint64_t tasks = (uint64_t)a.U * HW;
-    const uint32_t grid = (uint32_t)std::min<uint64_t>((tasks + 7) / 8, (uint64_t)ctx->num_sms * std::max(occ, 1));
-    launch(ctx, "hj_write", hj_write_fast<K>, dim3(grid), dim3(256), 0, a, (const uint16_t*)jc.stage,
+    const uint32_t grid =
+        (uint32_t)std::min<uint64_t>((tasks + WF_T / 32 - 1) / (WF_T / 32), (uint64_t)ctx->num_sms * std::max(occ, 1));
+    launch(ctx, "hj_write", hj_write_fast<K>, dim3(grid), dim3(WF_T), 0, a, (const uint16_t*)jc.stage,
            (const uint8_t*)jc.multi);
   }
   if (jc.nmulti == 0) return;

@@ -3,7 +3,8 @@
 # also the N=2 bench.  Logs under gpurun_out/${TAG}_*.
 O=gpurun_out; T=${TAG:-chk}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/${T}_smi.txt 2>&1
-timeout ${PYTEST_TIMEOUT:-2400} python -m pytest tests -m gpu -q -x -p no:cacheprovider ${PYTEST_ARGS} > $O/${T}_pytest.log 2>&1; echo "pytest rc=$?"
+if [ -n "$PYTEST_K" ]; then KARGS=(-k "$PYTEST_K"); else KARGS=(); fi
+timeout ${PYTEST_TIMEOUT:-2400} python -m pytest tests -m gpu -q -x -p no:cacheprovider "${KARGS[@]}" > $O/${T}_pytest.log 2>&1; echo "pytest rc=$?"
 tail -3 $O/${T}_pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${T}_smoke.log 2>&1; echo "smoke rc=$?"; tail -1 $O/${T}_smoke.log
 timeout 600 python bench.py ${BENCH_ARGS} > $O/${T}_bench.json 2> $O/${T}_bench.err; echo "bench rc=$?"

@@ -282,6 +282,8 @@ void gj_ctx_destroy(gj_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (auto& kv : ctx->bufs)
     if (kv.second.ptr) cudaFree(kv.second.ptr);
+  for (auto& kv : ctx->scan_state)
+    if (kv.second.ptr) cudaFree(kv.second.ptr);
   for (auto& p : ctx->pending) {
     cudaEventDestroy(p.a);
     cudaEventDestroy(p.b);
@@ -375,9 +377,7 @@ gj_status gj_join_stats(gj_ctx* ctx, uint64_t* rsize_eq8, uint32_t* partition_bi
   if (!ctx) throw Error(GJ_EINVAL, "ctx is NULL");
   const JoinCache& jc = ctx->jc;
   if (!jc.valid) throw Error(GJ_ESTATE, "gj_join_stats: no join_count on this ctx");
-  unsigned long long e = 0;
-  if (jc.eq8 && jc.R.n && jc.S.n) d2h_sync(ctx, &e, jc.eq8, sizeof(e));
-  if (rsize_eq8) *rsize_eq8 = e;
+  if (rsize_eq8) *rsize_eq8 = jc.R.n && jc.S.n ? jc.eq8_host : 0;
   if (partition_bits) *partition_bits = jc.B;
   if (units) *units = jc.U;
   API_END

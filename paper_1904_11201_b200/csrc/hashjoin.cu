@@ -56,7 +56,8 @@ struct HJArgs {
   const uint32_t* prid;
   uint32_t prid_base;
   const uint4* desc;  // per unit: (build begin, build n, probe begin, probe n)
-  uint32_t U;
+  uint32_t U;         // units (write passes); the count pass reads them from meta[3] / HW
+  const unsigned long long* meta;
   uint32_t* wcnt;
   const uint64_t* woff;
   uint2* out;
@@ -281,8 +282,9 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
   tab.init(smem);
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
   const uint32_t G = gridDim.x;
+  const uint32_t U = (uint32_t)(a.meta[3] / HW);  // 0 if the unit plan overflowed its arrays
   uint32_t u = blockIdx.x;
-  if (u >= a.U) return;
+  if (u >= U) return;
   tab.clear(TAB_MAX);
   const uint4 zero = make_uint4(0, 0, 0, 0);
   constexpr uint32_t N = KVec<K>::N;
@@ -303,8 +305,8 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
   uint4 d = a.desc[u];
   uint4 bv[2], pv[2];
   fetch(d, bv, pv);
-  for (; u < a.U; u += G) {
-    const uint4 dn = u + G < a.U ? a.desc[u + G] : zero;
+  for (; u < U; u += G) {
+    const uint4 dn = u + G < U ? a.desc[u + G] : zero;
     uint4 nbv[2], npv[2];
     fetch(dn, nbv, npv);
     const uint32_t bn = d.y, pn = d.w;
@@ -457,20 +459,21 @@ __global__ void __launch_bounds__(WF_T) hj_write_fast(HJArgs a, const uint16_t* 
       const uint32_t v = v0 + lane;
       const uint32_t j0 = v * N - sp.shift;  // row of element 0 (wraps below the range)
       uint32_t sx[N], pr[N], m = 0;
-      if (vec && v < ve) {  // element 0 of my vector is array element d.z + j0, N-aligned
+      if (vec && v < ve) {  // element 0 of my vector is array element e0 = d.z + j0 (mod 2^32), N-aligned
+        const uint32_t e0 = d.z + j0;
         if (N == 4) {
-          const uint2 x = __ldg(reinterpret_cast<const uint2*>(st + j0));
+          const uint2 x = __ldg(reinterpret_cast<const uint2*>(stage + e0));
           sx[0] = x.x & 0xFFFF, sx[1] = x.x >> 16, sx[2 % N] = x.y & 0xFFFF, sx[3 % N] = x.y >> 16;
         } else {
-          const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(st + j0));
+          const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(stage + e0));
           sx[0] = x & 0xFFFF, sx[1] = x >> 16;
         }
         if (a.prid) {
           if (N == 4) {
-            const uint4 y = __ldg(reinterpret_cast<const uint4*>(a.prid + d.z + j0));
+            const uint4 y = __ldg(reinterpret_cast<const uint4*>(a.prid + e0));
             pr[0] = y.x, pr[1] = y.y, pr[2 % N] = y.z, pr[3 % N] = y.w;
           } else {
-            const uint2 y = __ldg(reinterpret_cast<const uint2*>(a.prid + d.z + j0));
+            const uint2 y = __ldg(reinterpret_cast<const uint2*>(a.prid + e0));
             pr[0] = y.x, pr[1] = y.y;
           }
         }
@@ -513,7 +516,7 @@ __global__ void __launch_bounds__(WF_T) hj_write_fast(HJArgs a, const uint16_t* 
 __global__ void hj_units(const uint32_t* __restrict__ boff, const uint32_t* __restrict__ poff, uint32_t P,
                          uint32_t bchunk, uint32_t pchunk, unsigned long long* __restrict__ nunits,
                          unsigned long long* __restrict__ eq8) {
-  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long prod = 0;
   if (p < P) {
     uint32_t nb = boff[p + 1] - boff[p], np = poff[p + 1] - poff[p];
@@ -529,12 +532,20 @@ __global__ void hj_units(const uint32_t* __restrict__ boff, const uint32_t* __re
 // unit descriptors (build begin, build n, probe begin, probe n): one binary search
 // per unit, fully parallel.  Also initialises multi[u]: units of a partition with
 // several build chunks share probe rows, so their per-row staging is ambiguous and
-// the write pass re-probes them.
+// the write pass re-probes them.  U = unit_off[P] is read on the device; meta[2] = U,
+// meta[3] = U * HW (the length of the per-(unit, warp) count array) -- or 0 units if
+// U exceeds the capacity `cap` the host sized the arrays for (it then re-plans).
 __global__ void hj_unit_desc(const unsigned long long* __restrict__ unit_off, const uint32_t* __restrict__ boff,
-                             const uint32_t* __restrict__ poff, uint32_t P, uint32_t U, uint32_t bchunk,
+                             const uint32_t* __restrict__ poff, uint32_t P, uint32_t cap, uint32_t bchunk,
                              uint32_t pchunk, uint4* __restrict__ desc, uint8_t* __restrict__ multi,
-                             unsigned long long* __restrict__ nmulti) {
-  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < U; u += gridDim.x * blockDim.x) {
+                             unsigned long long* __restrict__ meta) {
+  const unsigned long long U = unit_off[P];
+  const uint32_t Ue = U <= cap ? (uint32_t)U : 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    meta[2] = U;
+    meta[3] = (unsigned long long)Ue * HW;
+  }
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < Ue; u += gridDim.x * blockDim.x) {
     const uint32_t p = upper_index(unit_off, P, (unsigned long long)u);
     const uint32_t uu = (uint32_t)(u - unit_off[p]);
     const uint32_t b0 = boff[p], nb = boff[p + 1] - b0;
@@ -544,7 +555,7 @@ __global__ void hj_unit_desc(const unsigned long long* __restrict__ unit_off, co
     desc[u] = make_uint4(b0 + bci * bchunk, min(bchunk, nb - bci * bchunk), p0 + pci * pchunk,
                          min(pchunk, np - pci * pchunk));
     multi[u] = nbc > 1 ? 1 : 0;
-    if (nbc > 1 && uu == 0) atomicAdd(nmulti, 1ull);
+    if (nbc > 1 && uu == 0) atomicAdd(meta + 1, 1ull);
   }
 }
 
@@ -586,64 +597,70 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
 
   unsigned long long* unit_off =
       static_cast<unsigned long long*>(ws(ctx, "hj.unit_off", (P + 1) * sizeof(unsigned long long)));
-  unsigned long long* eq8 = static_cast<unsigned long long*>(ws(ctx, "hj.eq8", sizeof(unsigned long long)));
-  GJ_CUDA(cudaMemsetAsync(eq8, 0, sizeof(unsigned long long), ctx->stream));
-  jc.eq8 = eq8;
+  // meta: [0] |J| (scan total), [1] MULTI units, [2] units U, [3] U * HW, [4] Eq.8 --
+  // everything the host needs comes back in ONE read at the end of the count
+  unsigned long long* meta = static_cast<unsigned long long*>(ws(ctx, "hj.meta", 8 * sizeof(unsigned long long)));
+  GJ_CUDA(cudaMemsetAsync(meta, 0, 8 * sizeof(unsigned long long), ctx->stream));
+  jc.eq8 = meta + 4;
   launch(ctx, "hj_units", hj_units, dim3((P + 255) / 256), dim3(256), 0, PB.off, PP.off, P, bchunk, pchunk,
-         unit_off, eq8);
+         unit_off, meta + 4);
   exclusive_scan<uint64_t, uint64_t>(ctx, reinterpret_cast<const uint64_t*>(unit_off),
                                      reinterpret_cast<uint64_t*>(unit_off), P,
                                      reinterpret_cast<uint64_t*>(unit_off) + P);
-  uint64_t U64 = 0;
-  d2h_sync(ctx, &U64, unit_off + P, sizeof(uint64_t));
-  if (U64 >= (1ull << 31))
-    throw Error(GJ_EINVAL, "equi join: " + std::to_string(U64) +
-                               " work units (a key repeated ~2^28 times on both sides); the per-unit plan is "
-                               "limited to 2^31 units");
-  const uint32_t U = (uint32_t)U64;
   jc.unit_off = unit_off;
-  jc.U = U;
-  const uint64_t nw = (uint64_t)U * HW;
-  uint32_t* wcnt = static_cast<uint32_t*>(ws(ctx, "hj.wcnt", (nw + 1) * sizeof(uint32_t)));
-  // woff[nw] = |J| (scan total), woff[nw + 1] = MULTI-unit counter: one readback
-  uint64_t* woff = static_cast<uint64_t*>(ws(ctx, "hj.woff", (nw + 2) * sizeof(uint64_t)));
-  uint4* desc = static_cast<uint4*>(ws(ctx, "hj.desc", ((uint64_t)U + 1) * sizeof(uint4)));
-  jc.woff = woff;
-  jc.desc = desc;
-  if (U == 0) {
-    jc.total = 0;
-    return;
-  }
   uint16_t* stage = static_cast<uint16_t*>(ws(ctx, "hj.stage", (Prb.n + 8) * sizeof(uint16_t)));
-  uint8_t* multi = static_cast<uint8_t*>(ws(ctx, "hj.multi", (uint64_t)U + 16));
   jc.stage = stage;
-  jc.multi = multi;
-  unsigned long long* nmulti = reinterpret_cast<unsigned long long*>(woff + nw + 1);
-  GJ_CUDA(cudaMemsetAsync(nmulti, 0, sizeof(uint64_t), ctx->stream));
-  launch(ctx, "hj_unit_desc", hj_unit_desc, dim3(std::min<uint32_t>((U + 255) / 256, ctx->num_sms * 16)),
-         dim3(256), 0, (const unsigned long long*)unit_off, PB.off, PP.off, P, U, bchunk, pchunk, desc, multi, nmulti);
-  HJArgs a{};
-  a.bkey = PB.key;
-  a.brid = PB.rid;
-  a.brid_base = Bld.rid_base;
-  a.pkey = PP.key;
-  a.prid = PP.rid;
-  a.prid_base = Prb.rid_base;
-  a.desc = desc;
-  a.U = U;
-  a.wcnt = wcnt;
-  a.swap = swap;
-  {
+  // The unit count is known only on the device: the arrays are sized for a capacity
+  // (2 units per partition, or what the last join on this ctx needed) and the count
+  // is re-planned in the rare case the units exceed it -- no host round trip here.
+  uint32_t cap = std::max<uint32_t>(ctx->hj_unit_cap, 2 * P + 1024);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const uint64_t nw = (uint64_t)cap * HW;
+    uint32_t* wcnt = static_cast<uint32_t*>(ws(ctx, "hj.wcnt", (nw + 1) * sizeof(uint32_t)));
+    uint64_t* woff = static_cast<uint64_t*>(ws(ctx, "hj.woff", (nw + 1) * sizeof(uint64_t)));
+    uint4* desc = static_cast<uint4*>(ws(ctx, "hj.desc", ((uint64_t)cap + 1) * sizeof(uint4)));
+    uint8_t* multi = static_cast<uint8_t*>(ws(ctx, "hj.multi", (uint64_t)cap + 16));
+    jc.woff = woff;
+    jc.desc = desc;
+    jc.multi = multi;
+    launch(ctx, "hj_unit_desc", hj_unit_desc, dim3(std::min<uint32_t>((cap + 255) / 256, ctx->num_sms * 16)),
+           dim3(256), 0, (const unsigned long long*)unit_off, PB.off, PP.off, P, cap, bchunk, pchunk, desc, multi,
+           meta);
+    HJArgs a{};
+    a.bkey = PB.key;
+    a.brid = PB.rid;
+    a.brid_base = Bld.rid_base;
+    a.pkey = PP.key;
+    a.prid = PP.rid;
+    a.prid_base = Prb.rid_base;
+    a.desc = desc;
+    a.meta = meta;
+    a.wcnt = wcnt;
+    a.swap = swap;
     const size_t smem = hj_smem<K, false>();
     set_smem(ctx, hj_count_kernel<K>, smem);
-    launch(ctx, "hj_count", hj_count_kernel<K>, dim3(hj_grid(ctx, hj_count_kernel<K>, smem, U)), dim3(HT), smem, a,
-           stage, multi, nmulti);
+    launch(ctx, "hj_count", hj_count_kernel<K>, dim3(hj_grid(ctx, hj_count_kernel<K>, smem, cap)), dim3(HT), smem, a,
+           stage, multi, meta + 1);
+    exclusive_scan_dev<uint32_t, uint64_t>(ctx, wcnt, woff, nw, reinterpret_cast<const uint64_t*>(meta + 3),
+                                           reinterpret_cast<uint64_t*>(meta));
+    unsigned long long h[5];
+    d2h_sync(ctx, h, meta, sizeof(h));
+    if (h[2] >= (1ull << 31))
+      throw Error(GJ_EINVAL, "equi join: " + std::to_string(h[2]) +
+                                 " work units (a key repeated ~2^28 times on both sides); the per-unit plan is "
+                                 "limited to 2^31 units");
+    if (h[2] <= cap) {
+      jc.U = (uint32_t)h[2];
+      jc.total = h[0];
+      jc.nmulti = h[1];
+      jc.eq8_host = h[4];
+      ctx->hj_unit_cap = std::max<uint32_t>(ctx->hj_unit_cap, (uint32_t)h[2]);
+      return;
+    }
+    cap = (uint32_t)std::min<uint64_t>((1ull << 31) - 1, h[2] + h[2] / 4 + 1024);  // re-plan with room
+    GJ_CUDA(cudaMemsetAsync(meta, 0, 2 * sizeof(unsigned long long), ctx->stream));
   }
-  exclusive_scan<uint32_t, uint64_t>(ctx, wcnt, woff, nw, woff + nw);
-  uint64_t h[2];
-  d2h_sync(ctx, h, woff + nw, sizeof(h));
-  jc.total = h[0];
-  jc.nmulti = h[1];
+  throw Error(GJ_ECUDA, "equi join: unit plan did not converge");
 }
 
 template <typename K>

@@ -140,25 +140,6 @@ __global__ void __launch_bounds__(PT, sizeof(K) == 4 ? 4 : 3) part_hist(const K*
   for (uint32_t d = threadIdx.x; d < D; d += PT) out[(uint64_t)d * L.nc] = h[d];
 }
 
-// Tile descriptors for the scatter: (tile begin, tile length, index of the tile's
-// chunk column in the scanned histogram, chunks in its segment); length 0 = empty.
-__global__ void tile_desc_kernel(uint64_t n, const uint32_t* __restrict__ seg_off,
-                                 const uint32_t* __restrict__ chunk_base, uint32_t nseg, uint32_t D,
-                                 uint32_t ntiles, uint4* __restrict__ desc) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= ntiles) return;
-  const uint32_t c = t / TPC, t_in = t % TPC;
-  const ChunkLoc L = locate(c, n, seg_off, chunk_base, nseg);
-  uint4 d = make_uint4(0, 0, 0, 0);
-  if (c < L.total) {
-    const uint32_t len = (uint32_t)(L.end - L.beg);
-    if (t_in * TILE < len)
-      d = make_uint4((uint32_t)L.beg + t_in * TILE, min(len - t_in * TILE, (uint32_t)TILE), L.cb * D + (c - L.cb),
-                     L.nc);
-  }
-  desc[t] = d;
-}
-
 // Scatter (local radix pass, or the multi-GPU shuffle pass with REMOTE), branch-free
 // ranking.  Every phase of a tile is a straight run of independent per-item
 // operations the scheduler can overlap:
@@ -481,18 +462,28 @@ __global__ void __launch_bounds__(PT, SCATTER_MINB) part_scatter(
   if (REMOTE) __threadfence_system();  // peer writes performed before the kernel retires
 }
 
-// Turns the in-chunk prefix rows of part_hist into absolute run starts: every
-// tile's row gets its chunk's scanned (segment, digit, chunk) offsets added, so the
-// scatter reads one contiguous row per tile (the scanned matrix is strided by the
-// chunk count: reading it per tile cost one DRAM sector per digit).
-// One CTA per chunk.
+// Plans one scatter, one CTA per chunk: turns the in-chunk prefix rows of part_hist
+// into absolute run starts (every tile's row gets its chunk's scanned (segment,
+// digit, chunk) offsets added, so the scatter reads one contiguous row per tile --
+// the scanned matrix is strided by the chunk count: reading it per tile cost one
+// DRAM sector per digit), writes the chunk's tile descriptors (tile begin, tile
+// length; length 0 = empty) and resets the scatter's tile counter.
 __global__ void tile_base_kernel(uint64_t n, const uint32_t* __restrict__ seg_off,
                                  const uint32_t* __restrict__ chunk_base, uint32_t nseg, uint32_t bits,
-                                 const uint32_t* __restrict__ scanned, uint32_t* __restrict__ tile_pref) {
+                                 const uint32_t* __restrict__ scanned, uint32_t* __restrict__ tile_pref,
+                                 uint4* __restrict__ tdesc, uint32_t* __restrict__ tile_ctr) {
   const uint32_t c = blockIdx.x, D = 1u << bits;
+  if (c == 0 && threadIdx.x == 0) *tile_ctr = 0;
   const ChunkLoc L = locate(c, n, seg_off, chunk_base, nseg);
+  const uint32_t len = c < L.total ? (uint32_t)(L.end - L.beg) : 0u;
+  if (threadIdx.x < TPC) {
+    const uint32_t t_in = threadIdx.x;
+    tdesc[(uint64_t)c * TPC + t_in] = t_in * TILE < len ? make_uint4((uint32_t)L.beg + t_in * TILE,
+                                                                     min(len - t_in * TILE, (uint32_t)TILE), 0, 0)
+                                                        : make_uint4(0, 0, 0, 0);
+  }
   if (c >= L.total) return;
-  const uint32_t nt = (uint32_t)((L.end - L.beg + TILE - 1) / TILE);
+  const uint32_t nt = (len + TILE - 1) / TILE;
   for (uint32_t d = threadIdx.x; d < D; d += blockDim.x) {
     const uint32_t base = scanned[(uint64_t)L.cb * D + (uint64_t)d * L.nc + (c - L.cb)];
     for (uint32_t t = 0; t < nt; ++t) tile_pref[((uint64_t)c * TPC + t) * D + d] += base;
@@ -502,15 +493,13 @@ __global__ void tile_base_kernel(uint64_t n, const uint32_t* __restrict__ seg_of
 template <typename K, bool HAS_RID, bool RANGE, bool REMOTE>
 void launch_scatter_t(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
                       const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* tile_base,
-                      K* kout, uint32_t* rout, const DigitFn& fn, const ShuffleDest& dst) {
+                      uint32_t* ctr, K* kout, uint32_t* rout, const DigitFn& fn, const ShuffleDest& dst) {
   auto kern = part_scatter<K, HAS_RID, RANGE, REMOTE>;
   const size_t smem = ScatterLayout<K>::bytes(1u << bits);
   set_smem(ctx, kern, ScatterLayout<K>::bytes(1u << MAX_BITS));
   int occ = 1;
   GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PT, smem));
   const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
-  uint32_t* ctr = static_cast<uint32_t*>(ws(ctx, REMOTE ? "shuffle.tile_ctr" : "part.tile_ctr", sizeof(uint32_t)));
-  GJ_CUDA(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), ctx->stream));
   launch(ctx, REMOTE ? "shuffle_scatter" : "part_scatter", kern, dim3(grid), dim3(PT), smem, kin, rin, rid_base, n,
          tdesc, (uint32_t)ntiles, shift, bits, tile_base, kout, rout, ctr, fn, dst);
 }
@@ -518,18 +507,38 @@ void launch_scatter_t(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t r
 template <typename K, bool RANGE, bool REMOTE>
 void launch_scatter(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
                     const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* tile_base,
-                    K* kout, uint32_t* rout, const DigitFn& fn, const ShuffleDest& dst) {
+                    uint32_t* ctr, K* kout, uint32_t* rout, const DigitFn& fn, const ShuffleDest& dst) {
   if (rin)
-    launch_scatter_t<K, true, RANGE, REMOTE>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_base, kout,
-                                             rout, fn, dst);
+    launch_scatter_t<K, true, RANGE, REMOTE>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_base, ctr,
+                                             kout, rout, fn, dst);
   else
-    launch_scatter_t<K, false, RANGE, REMOTE>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_base,
+    launch_scatter_t<K, false, RANGE, REMOTE>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_base, ctr,
                                               kout, rout, fn, dst);
 }
 
-__global__ void seg_chunks(const uint32_t* __restrict__ seg_off, uint32_t nseg, uint32_t* __restrict__ nc) {
-  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < nseg) nc[s] = (seg_off[s + 1] - seg_off[s] + CHUNK - 1) / CHUNK;
+// chunk_base[s] = first chunk of segment s (exclusive scan of the segments' chunk
+// counts), chunk_base[nseg] = total chunks: one CTA.
+__global__ void __launch_bounds__(1024) chunk_base_kernel(const uint32_t* __restrict__ seg_off, uint32_t nseg,
+                                                          uint32_t* __restrict__ cb) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t s0 = 0; s0 < nseg; s0 += 1024) {
+    const uint32_t s = s0 + threadIdx.x;
+    const uint32_t v = s < nseg ? (seg_off[s + 1] - seg_off[s] + CHUNK - 1) / CHUNK : 0u;
+    const uint32_t incl = warp_incl_scan(v);
+    if (lane_id() == 31) wsum[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    if (threadIdx.x < 32) wsum[threadIdx.x] = warp_incl_scan(wsum[threadIdx.x]);
+    __syncthreads();
+    const uint32_t ex = carry + (threadIdx.x >= 32 ? wsum[(threadIdx.x >> 5) - 1] : 0u) + incl - v;
+    if (s < nseg) cb[s] = ex;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = ex + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) cb[nseg] = carry;
 }
 
 __global__ void extract_off(const uint32_t* __restrict__ scanned, const uint32_t* __restrict__ seg_off,
@@ -596,8 +605,7 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
     uint32_t* chunk_base = nullptr;
     if (seg_off) {
       chunk_base = static_cast<uint32_t*>(ws(ctx, (t + ".cb").c_str(), (nseg + 1) * sizeof(uint32_t)));
-      launch(ctx, "seg_chunks", seg_chunks, dim3((nseg + 255) / 256), dim3(256), 0, seg_off, nseg, chunk_base);
-      exclusive_scan<uint32_t, uint32_t>(ctx, chunk_base, chunk_base, nseg, chunk_base + nseg);
+      launch(ctx, "chunk_base", chunk_base_kernel, dim3(1), dim3(1024), 0, seg_off, nseg, chunk_base);
     }
     const uint64_t max_chunks = (n + CHUNK - 1) / CHUNK + (seg_off ? nseg : 0);
     const uint64_t hn = max_chunks * D;
@@ -607,13 +615,12 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
     launch(ctx, "part_hist", part_hist<K, RANGE>, dim3((unsigned)max_chunks), dim3(PT), 0, kin, n, seg_off,
            (const uint32_t*)chunk_base, nseg, shift, bits, hist, tile_pref, fn);
     exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
-    launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, seg_off,
-           (const uint32_t*)chunk_base, nseg, bits, (const uint32_t*)hist, tile_pref);
     uint4* tdesc = static_cast<uint4*>(ws(ctx, "part.tdesc", (ntiles + 1) * sizeof(uint4)));
-    launch(ctx, "tile_desc", tile_desc_kernel, dim3((unsigned)((ntiles + 255) / 256)), dim3(256), 0, n, seg_off,
-           (const uint32_t*)chunk_base, nseg, D, (uint32_t)ntiles, tdesc);
-    launch_scatter<K, RANGE, false>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, tile_pref, kout, rout,
-                                    fn, ShuffleDest{});
+    uint32_t* ctr = static_cast<uint32_t*>(ws(ctx, "part.tile_ctr", sizeof(uint32_t)));
+    launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, seg_off,
+           (const uint32_t*)chunk_base, nseg, bits, (const uint32_t*)hist, tile_pref, tdesc, ctr);
+    launch_scatter<K, RANGE, false>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, tile_pref, ctr, kout,
+                                    rout, fn, ShuffleDest{});
     const uint32_t P = nseg << bits;
     uint32_t* off = static_cast<uint32_t*>(ws(ctx, (ps + ".off").c_str(), (P + 1) * sizeof(uint32_t)));
     launch(ctx, "extract_off", extract_off, dim3((P + 1 + 255) / 256), dim3(256), 0, (const uint32_t*)hist,
@@ -653,11 +660,10 @@ ShufflePass shuffle_prepare_impl(gj_ctx* ctx, const gj_rel& X, uint32_t g, const
          static_cast<const K*>(X.key), n, (const uint32_t*)nullptr, (const uint32_t*)nullptr, 1u, shift, g, hist,
          tile_pref, DigitFn{});
   exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
-  launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, (const uint32_t*)nullptr,
-         (const uint32_t*)nullptr, 1u, g, (const uint32_t*)hist, tile_pref);
   uint4* tdesc = static_cast<uint4*>(ws(ctx, (t + ".stdesc").c_str(), (sp.ntiles + 1) * sizeof(uint4)));
-  launch(ctx, "tile_desc", tile_desc_kernel, dim3((unsigned)((sp.ntiles + 255) / 256)), dim3(256), 0, n,
-         (const uint32_t*)nullptr, (const uint32_t*)nullptr, 1u, D, (uint32_t)sp.ntiles, tdesc);
+  uint32_t* ctr = static_cast<uint32_t*>(ws(ctx, (t + ".sctr").c_str(), sizeof(uint32_t)));
+  launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, (const uint32_t*)nullptr,
+         (const uint32_t*)nullptr, 1u, g, (const uint32_t*)hist, tile_pref, tdesc, ctr);
   uint32_t* off = static_cast<uint32_t*>(ws(ctx, (t + ".soff").c_str(), (D + 1) * sizeof(uint32_t)));
   launch(ctx, "extract_off", extract_off, dim3((D + 1 + 255) / 256), dim3(256), 0, (const uint32_t*)hist,
          (const uint32_t*)nullptr,
@@ -665,6 +671,7 @@ ShufflePass shuffle_prepare_impl(gj_ctx* ctx, const gj_rel& X, uint32_t g, const
   sp.hist = hist;
   sp.tile_pref = tile_pref;
   sp.tdesc = tdesc;
+  sp.ctr = ctr;
   sp.off = off;
   return sp;
 }
@@ -696,10 +703,12 @@ void shuffle_scatter(gj_ctx* ctx, const gj_rel& X, const ShufflePass& sp, const 
   if (X.n == 0) return;
   if (X.key_type == GJ_I32)
     launch_scatter<int32_t, false, true>(ctx, static_cast<const int32_t*>(X.key), X.rid, X.rid_base, X.n, sp.tdesc,
-                                         sp.ntiles, 32 - sp.g, sp.g, sp.tile_pref, nullptr, nullptr, DigitFn{}, dst);
+                                         sp.ntiles, 32 - sp.g, sp.g, sp.tile_pref, sp.ctr, nullptr, nullptr, DigitFn{},
+                                         dst);
   else
     launch_scatter<int64_t, false, true>(ctx, static_cast<const int64_t*>(X.key), X.rid, X.rid_base, X.n, sp.tdesc,
-                                         sp.ntiles, 32 - sp.g, sp.g, sp.tile_pref, nullptr, nullptr, DigitFn{}, dst);
+                                         sp.ntiles, 32 - sp.g, sp.g, sp.tile_pref, sp.ctr, nullptr, nullptr, DigitFn{},
+                                         dst);
 }
 
 }  // namespace gj

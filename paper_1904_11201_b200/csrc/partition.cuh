@@ -58,6 +58,7 @@ struct ShufflePass {
   const uint32_t* hist = nullptr;
   const uint32_t* tile_pref = nullptr;
   const uint4* tdesc = nullptr;
+  uint32_t* ctr = nullptr;        // the scatter's tile counter (reset by the planning kernel)
   const uint32_t* off = nullptr;  // device, 2^g + 1 run starts (local digit order)
 };
 // Histogram + scan for a one-pass partition of X by the top g hash bits

@@ -58,6 +58,7 @@ struct JoinCache {
   uint64_t total = 0;
   uint64_t nmulti = 0;  // units flagged MULTI (the write pass re-probes them)
   const unsigned long long* eq8 = nullptr;  // device: Eq.8 result-size bound of the last count
+  uint64_t eq8_host = 0;                      // the same, read back with |J|
 };
 
 struct ThetaCache {
@@ -84,6 +85,15 @@ struct ThetaCache {
   std::vector<uint64_t> rect_base;
 };
 
+// Per-stream state of the single-pass scan: status words + ticket counter, the
+// tickets consumed so far and the last launch epoch (scan.cu).
+struct ScanState {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  uint64_t tickets = 0;
+  uint32_t epoch = 0;
+};
+
 struct ProfRec {
   const char* tag;
   cudaEvent_t a, b;
@@ -106,10 +116,12 @@ struct gj_ctx {
   int theta_regions = 1;         // theta joins through the region matrix (0 = plain NLJ over all pairs)
   uint32_t theta_grid_rows = 0;  // multi-GPU theta: rows r of the 1-Bucket grid (0 = auto; 1 = R broadcast)
   int build_side = 0;
+  uint32_t hj_unit_cap = 0;  // hash-join unit arrays: capacity the last joins needed
   int shuffle_bits = 0;
   // workspace
   std::map<std::string, gj::Buf> bufs;
   std::map<std::string, gj::Buf> pinned_bufs;  // grow-only pinned host staging
+  std::map<std::string, gj::ScanState> scan_state;  // per-stream single-pass scan state
   // stats
   uint64_t launches = 0;
   std::vector<gj::ProfRec> pending;

@@ -39,9 +39,7 @@ constexpr int TAB_MAX = 2 * BCH_MAX;  // table slots: load <= 1/4 up to 2048 bui
 
 // Independent second hash for the in-partition table slot (the partition id
 // already consumed the top bits of khash).
-__device__ __forceinline__ uint32_t slot_hash(int32_t k) {
-  return (uint32_t)(((uint64_t)(uint32_t)k * 0xD6E8FEB86659FD93ull) >> 32);
-}
+__device__ __forceinline__ uint32_t slot_hash(int32_t k) { return __umulhi((uint32_t)k, 0xD6E8FEB9u); }
 __device__ __forceinline__ uint32_t slot_hash(int64_t k) {
   uint64_t x = (uint64_t)k;
   x ^= x >> 31;
@@ -355,6 +353,197 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
   }
 }
 
+// ---------------------------------------------------------------- int32 count pass
+// The configs[0-3] path, written for instruction count: the table lives at a 32-bit
+// shared-memory address (explicit ld/atom.shared, no generic-address conversion per
+// access); a key vector whose 4 rows all lie in the unit takes a straight-line path
+// (4 hashes, 4 CAS / 4 first-slot loads issued back to back) and only collisions
+// branch; the unit plan (vector spans, warp ranges) of the next unit is computed
+// once, together with its register prefetch.
+__device__ __forceinline__ unsigned long long lds64(uint32_t a) {
+  unsigned long long v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long cas64(uint32_t a, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "r"(a), "l"(0ull), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void sts128z(uint32_t a) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(a), "r"(0u) : "memory");
+}
+__device__ __forceinline__ uint32_t slot32(uint32_t k, uint32_t tshift) { return __umulhi(k, 0xD6E8FEB9u) >> tshift; }
+__device__ __forceinline__ unsigned long long tval(uint32_t k, uint32_t j) {
+  return ((unsigned long long)(j + 1) << 32) | k;
+}
+
+struct UnitPlan {
+  Span sb, sp;
+  uint32_t vb, ve;  // this warp's probe vectors
+};
+__device__ __forceinline__ UnitPlan plan_unit(const HJArgs& a, const uint4 d, uint32_t w) {
+  UnitPlan p;
+  p.sb = span16(a.bkey, d.x, d.y, 4);
+  p.sp = span16(a.pkey, d.z, d.w, 4);
+  warp_vecs(p.sp.nv, w, p.vb, p.ve);
+  return p;
+}
+
+// insert key k (row j) whose first CAS at slot s found `old`; returns duplicate seen
+__device__ __forceinline__ bool insert_walk(uint32_t tb, uint32_t s, uint32_t tmask, uint32_t k, uint32_t j,
+                                         unsigned long long old) {
+  bool dup = false;
+  while (old != 0ull) {
+    dup |= (uint32_t)old == k;
+    s = (s + 1) & tmask;
+    old = cas64(tb + 8 * s, tval(k, j));
+  }
+  return dup;
+}
+
+__device__ __forceinline__ bool build4(uint32_t tb, uint4 x, uint32_t v, uint32_t shift, uint32_t bn, uint32_t tmask,
+                                       uint32_t tshift) {
+  const uint32_t k[4] = {x.x, x.y, x.z, x.w};
+  const uint32_t j0 = v * 4 - shift;
+  bool dup = false;
+  if (j0 < bn && j0 + 3 < bn) {  // all four rows in the unit: straight line
+    uint32_t s[4];
+    unsigned long long o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s[q] = slot32(k[q], tshift);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = cas64(tb + 8 * s[q], tval(k[q], j0 + q));
+    if ((o[0] | o[1] | o[2] | o[3]) != 0ull) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (o[q] != 0ull) dup |= insert_walk(tb, s[q], tmask, k[q], j0 + q, o[q]);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (j0 + q < bn) {
+        const uint32_t s = slot32(k[q], tshift);
+        const unsigned long long o = cas64(tb + 8 * s, tval(k[q], j0 + q));
+        if (o != 0ull) dup |= insert_walk(tb, s, tmask, k[q], j0 + q, o);
+      }
+    }
+  }
+  return dup;
+}
+
+// walk for key k from slot s (whose entry e did not settle it); returns match count,
+// *f = matching row (the first one if unique)
+__device__ __forceinline__ uint32_t probe_walk(uint32_t tb, uint32_t s, uint32_t tmask, uint32_t k, bool unique,
+                                            unsigned long long e, uint32_t* f) {
+  uint32_t m = 0;
+  for (; e != 0ull; e = lds64(tb + 8 * (s = (s + 1) & tmask))) {
+    if ((uint32_t)e == k) {
+      *f = (uint32_t)(e >> 32) - 1;
+      ++m;
+      if (unique) break;
+    }
+  }
+  return m;
+}
+
+__device__ __forceinline__ void probe4(uint32_t tb, uint4 x, uint32_t v, uint32_t shift, uint32_t pn, uint32_t tmask,
+                                       uint32_t tshift, bool unique, uint16_t* __restrict__ st, bool vec, uint32_t& c,
+                                       bool& many) {
+  const uint32_t k[4] = {x.x, x.y, x.z, x.w};
+  const uint32_t j0 = v * 4 - shift;
+  const bool full = j0 < pn && j0 + 3 < pn;
+  uint32_t s[4], r[4];
+  unsigned long long e[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) s[q] = slot32(k[q], tshift);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) e[q] = (full || j0 + q < pn) ? lds64(tb + 8 * s[q]) : 0ull;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    // settled by the first slot: empty (no match) or, for a unique build side, a hit
+    const bool hit = e[q] != 0ull && (uint32_t)e[q] == k[q];
+    uint32_t m = hit ? 1u : 0u, f = (uint32_t)(e[q] >> 32) - 1;
+    if ((e[q] != 0ull && !(hit && unique)) && (full || j0 + q < pn)) {
+      // a walk starts at slot s holding entry e: the first slot itself after a miss,
+      // the slot after it after a (non-unique) hit
+      const uint32_t s0 = hit ? (s[q] + 1) & tmask : s[q];
+      m = probe_walk(tb, s0, tmask, k[q], unique, hit ? lds64(tb + 8 * s0) : e[q], &f);
+      if (hit) {  // bag semantics: the first slot's match plus the walk's
+        m += 1;
+        if (m == 2) f = (uint32_t)(e[q] >> 32) - 1;
+      }
+    }
+    c += (full || j0 + q < pn) ? m : 0u;
+    many |= m > 1;
+    r[q] = m == 0 ? NO_MATCH : (m == 1 ? f : MULTI);
+  }
+  if (vec && full) {
+    *reinterpret_cast<uint2*>(st + j0) = make_uint2(r[0] | r[1] << 16, r[2] | r[3] << 16);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (full || j0 + q < pn) st[j0 + q] = (uint16_t)r[q];
+  }
+}
+
+__global__ void __launch_bounds__(HT, 2) hj_count_i32(HJArgs a, uint16_t* __restrict__ stage,
+                                                   uint8_t* __restrict__ multi,
+                                                   unsigned long long* __restrict__ nmulti) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_dup;
+  const uint32_t tb = saddr(smem);
+  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
+  const uint32_t G = gridDim.x;
+  const uint32_t U = (uint32_t)(a.meta[3] / HW);
+  uint32_t u = blockIdx.x;
+  if (u >= U) return;
+  for (uint32_t i = tid; i < TAB_MAX / 2; i += HT) sts128z(tb + 16 * i);
+  const bool vec = reinterpret_cast<uint64_t>(stage) % 8 == 0 && reinterpret_cast<uint64_t>(a.pkey) % 16 == 0;
+  const uint4 zero = make_uint4(0, 0, 0, 0);
+  uint4 d = a.desc[u];
+  UnitPlan P = plan_unit(a, d, w);
+  // register prefetch: one build and one probe vector per thread (all of a 2044-row
+  // unit; the few extra vectors of larger units are loaded when needed)
+  uint4 bv0 = tid < P.sb.nv ? ldv(P.sb, tid) : zero;
+  uint4 pv0 = P.vb + lane < P.ve ? ldv(P.sp, P.vb + lane) : zero;
+  for (; u < U; u += G) {
+    const uint4 dn = u + G < U ? a.desc[u + G] : zero;
+    const UnitPlan PN = plan_unit(a, dn, w);
+    const uint4 nb0 = tid < PN.sb.nv ? ldv(PN.sb, tid) : zero;
+    const uint4 np0 = PN.vb + lane < PN.ve ? ldv(PN.sp, PN.vb + lane) : zero;
+
+    const uint32_t bn = d.y, pn = d.w;
+    const uint32_t logT = table_logT(bn);
+    const uint32_t T = 1u << logT, tmask = T - 1, tshift = 32 - logT;
+    if (tid == 0) s_dup = 0;
+    __syncthreads();  // table cleared, s_dup reset
+    bool dup = false;
+    if (tid < P.sb.nv) dup |= build4(tb, bv0, tid, P.sb.shift, bn, tmask, tshift);
+    for (uint32_t v = tid + HT; v < P.sb.nv; v += HT) dup |= build4(tb, ldv(P.sb, v), v, P.sb.shift, bn, tmask, tshift);
+    if (__any_sync(FULL, dup) && lane == 0) s_dup = 1;
+    __syncthreads();
+    const bool unique = s_dup == 0;  // no duplicate build key: stop each probe at its first match
+    uint16_t* st = stage + d.z;
+    uint32_t c = 0;
+    bool many = false;
+    if (P.vb + lane < P.ve) probe4(tb, pv0, P.vb + lane, P.sp.shift, pn, tmask, tshift, unique, st, vec, c, many);
+    for (uint32_t v = P.vb + lane + 32; v < P.ve; v += 32)
+      probe4(tb, ldv(P.sp, v), v, P.sp.shift, pn, tmask, tshift, unique, st, vec, c, many);
+    c = warp_sum(c);
+    if (lane == 0) a.wcnt[(uint64_t)u * HW + w] = c;
+    if (__any_sync(FULL, many) && lane == 0) {
+      multi[u] = 1;
+      atomicAdd(nmulti, 1ull);  // > 0 tells the host to launch the MULTI write pass
+    }
+    __syncthreads();  // every probe of this unit is done: clear what it used
+    for (uint32_t i = tid; i < T / 2; i += HT) sts128z(tb + 16 * i);
+    d = dn;
+    P = PN;
+    bv0 = nb0, pv0 = np0;
+  }
+}
+
 // Write pass for units with a MULTI row (duplicate build keys) or a partition split
 // over several build chunks: rebuild the table, re-probe, and write every match of
 // a probe row at the warp's scanned offset (same row -> warp map as the count pass).
@@ -638,9 +827,15 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
     a.wcnt = wcnt;
     a.swap = swap;
     const size_t smem = hj_smem<K, false>();
-    set_smem(ctx, hj_count_kernel<K>, smem);
-    launch(ctx, "hj_count", hj_count_kernel<K>, dim3(hj_grid(ctx, hj_count_kernel<K>, smem, cap)), dim3(HT), smem, a,
-           stage, multi, meta + 1);
+    if (sizeof(K) == 4) {
+      set_smem(ctx, hj_count_i32, smem);
+      launch(ctx, "hj_count", hj_count_i32, dim3(hj_grid(ctx, hj_count_i32, smem, cap)), dim3(HT), smem, a, stage,
+             multi, meta + 1);
+    } else {
+      set_smem(ctx, hj_count_kernel<K>, smem);
+      launch(ctx, "hj_count", hj_count_kernel<K>, dim3(hj_grid(ctx, hj_count_kernel<K>, smem, cap)), dim3(HT), smem,
+             a, stage, multi, meta + 1);
+    }
     exclusive_scan_dev<uint32_t, uint64_t>(ctx, wcnt, woff, nw, reinterpret_cast<const uint64_t*>(meta + 3),
                                            reinterpret_cast<uint64_t*>(meta));
     unsigned long long h[5];

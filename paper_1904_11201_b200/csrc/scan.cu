@@ -101,27 +101,33 @@ __global__ void __launch_bounds__(SCAN_T) scan_lookback(const TIn* in, TOut* out
     s += v[k];
   }
   TOut e = block_excl_scan<TOut>(s, &s_tot);  // (its barriers order s_tot)
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 predecessors per step
+    const uint32_t lane = threadIdx.x;
     const TOut agg = s_tot;
     const uint32_t tag = epoch << 2;
     TOut prefix = 0;
-    if (t == 0) {
-      S::put(status + t, tag | F_INCL, agg);
-    } else {
-      S::put(status + t, tag | F_AGG, agg);
-      for (uint32_t p = t - 1;; --p) {  // look back until an inclusive prefix
-        uint32_t g;
-        TOut x;
-        do {
-          S::get(status + p, g, x);
-        } while ((g >> 2) != epoch || (g & 3u) == 0u);
-        prefix += x;
-        if ((g & 3u) == F_INCL) break;
+    if (lane == 0) S::put(status + t, tag | (t == 0 ? F_INCL : F_AGG), agg);
+    if (t > 0) {
+      for (int64_t hi = (int64_t)t - 1;; hi -= 32) {  // window [hi - 31, hi]
+        const int64_t p = hi - (int64_t)lane;
+        uint32_t g = (epoch << 2) | F_INCL;  // lanes before tile 0 act as an empty inclusive prefix
+        TOut x = 0;
+        if (p >= 0) do {
+            S::get(status + p, g, x);
+          } while ((g >> 2) != epoch || (g & 3u) == 0u);
+        // the nearest inclusive prefix in the window ends the look-back: sum the
+        // values from the window's top down to it
+        const uint32_t incl = __ballot_sync(FULL, (g & 3u) == F_INCL);
+        const uint32_t stop = incl ? __ffs(incl) - 1 : 31;  // lowest lane = nearest tile
+        prefix += warp_sum(lane <= stop ? x : TOut(0));
+        if (incl) break;
       }
-      S::put(status + t, tag | F_INCL, prefix + agg);
+      if (lane == 0) S::put(status + t, tag | F_INCL, prefix + agg);
     }
-    s_prefix = prefix;
-    if (t == ntiles - 1) *total = prefix + agg;
+    if (lane == 0) {
+      s_prefix = prefix;
+      if (t == ntiles - 1) *total = prefix + agg;
+    }
   }
   __syncthreads();
   e += s_prefix;

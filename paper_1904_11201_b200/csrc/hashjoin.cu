@@ -39,7 +39,12 @@ constexpr int TAB_MAX = 2 * BCH_MAX;  // table slots: load <= 1/4 up to 2048 bui
 
 // Independent second hash for the in-partition table slot (the partition id
 // already consumed the top bits of khash).
-__device__ __forceinline__ uint32_t slot_hash(int32_t k) { return __umulhi((uint32_t)k, 0xD6E8FEB9u); }
+// hi32(k * 0xD6E8FEB86659FD93) for a 32-bit k = k * C_hi + hi32(k * C_lo): a 64-bit
+// multiplier, unlike a 32-bit one, stays uncorrelated with the partition hash (32-bit
+// multipliers measured 134-215 distinct slots for a 2049-key configs[1] partition)
+__device__ __forceinline__ uint32_t slot_hash(int32_t k) {
+  return (uint32_t)k * 0xD6E8FEB8u + __umulhi((uint32_t)k, 0x6659FD93u);
+}
 __device__ __forceinline__ uint32_t slot_hash(int64_t k) {
   uint64_t x = (uint64_t)k;
   x ^= x >> 31;
@@ -373,7 +378,7 @@ __device__ __forceinline__ unsigned long long cas64(uint32_t a, unsigned long lo
 __device__ __forceinline__ void sts128z(uint32_t a) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(a), "r"(0u) : "memory");
 }
-__device__ __forceinline__ uint32_t slot32(uint32_t k, uint32_t tshift) { return __umulhi(k, 0xD6E8FEB9u) >> tshift; }
+__device__ __forceinline__ uint32_t slot32(uint32_t k, uint32_t tshift) { return slot_hash((int32_t)k) >> tshift; }
 __device__ __forceinline__ unsigned long long tval(uint32_t k, uint32_t j) {
   return ((unsigned long long)(j + 1) << 32) | k;
 }
@@ -609,17 +614,60 @@ __global__ void __launch_bounds__(HT) hj_write_kernel(HJArgs a, const uint8_t* _
 }
 
 // Write pass for units without a MULTI row (the usual case): a table-free gather.
-// Warp task (unit u, warp w) covers the same probe rows as warp w of the count pass,
-// 32 key vectors (32 * KVN consecutive rows) per step: each lane reads its rows'
-// staged match indices (and probe rids), the warp ranks the matches by a scan, each
-// lane puts its (rid_R, rid_S) pairs into a warp-private shared-memory buffer at its
-// rank, and the warp copies the buffer to the task's output range with consecutive
-// lanes on consecutive pairs (fully coalesced stores).  Rows stay in order, so the
-// positions are deterministic.  When the stage and probe-rid arrays share the key
-// array's 16-byte phase (always, unless the caller's key view is unaligned and the
-// join has no radix pass) each lane reads its rows' indices / rids as one vector.
-// Build rids are gathered through the read-only cache (a build chunk is <= 16 KB).
+// One warp per unit.  The unit's output is one contiguous range starting at the
+// count pass's offset of (unit, warp 0) -- its warps' row ranges are consecutive --
+// so the warp walks the unit's probe rows in order, 32 key vectors (32 * KVN rows)
+// per step: each lane reads its rows' staged match indices (and probe rids), the warp
+// ranks the matches by a scan, each lane puts its (rid_R, rid_S) pairs into a
+// warp-private shared-memory buffer at its rank, and the warp copies the buffer out
+// with consecutive lanes on consecutive pairs (fully coalesced stores).  The loads of
+// step i + 1 are issued before step i's dependent build-rid gathers, so each warp
+// keeps two steps of loads in flight.  When the stage and probe-rid arrays share the
+// key array's 16-byte phase (always, unless the caller's key view is unaligned and
+// the join has no radix pass) each lane reads its rows' indices / rids as one vector.
 constexpr int WF_T = 256;  // threads per CTA of the write pass
+template <typename K>
+struct WStep {
+  uint32_t sx[16 / sizeof(K)], pr[16 / sizeof(K)];
+};
+template <typename K>
+__device__ __forceinline__ void wf_load(WStep<K>& S, const HJArgs& a, const uint16_t* __restrict__ stage, bool vec,
+                                        const uint4 d, const Span& sp, uint32_t v) {
+  constexpr uint32_t N = KVec<K>::N;
+  const uint32_t pn = d.w;
+  const uint32_t j0 = v * N - sp.shift;  // row of element 0 (wraps below the range)
+  if (vec && v < sp.nv) {  // element 0 of my vector is array element e0 = d.z + j0 (mod 2^32), N-aligned
+    const uint32_t e0 = d.z + j0;
+    if (N == 4) {
+      const uint2 x = __ldg(reinterpret_cast<const uint2*>(stage + e0));
+      S.sx[0] = x.x & 0xFFFF, S.sx[1] = x.x >> 16, S.sx[2 % N] = x.y & 0xFFFF, S.sx[3 % N] = x.y >> 16;
+    } else {
+      const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(stage + e0));
+      S.sx[0] = x & 0xFFFF, S.sx[1] = x >> 16;
+    }
+    if (a.prid) {
+      if (N == 4) {
+        const uint4 y = __ldg(reinterpret_cast<const uint4*>(a.prid + e0));
+        S.pr[0] = y.x, S.pr[1] = y.y, S.pr[2 % N] = y.z, S.pr[3 % N] = y.w;
+      } else {
+        const uint2 y = __ldg(reinterpret_cast<const uint2*>(a.prid + e0));
+        S.pr[0] = y.x, S.pr[1] = y.y;
+      }
+    }
+#pragma unroll
+    for (uint32_t q = 0; q < N; ++q)
+      if (j0 + q >= pn) S.sx[q] = NO_MATCH;  // outside the unit's rows
+  } else {
+#pragma unroll
+    for (uint32_t q = 0; q < N; ++q) {
+      const uint32_t j = j0 + q;
+      const bool ok = v < sp.nv && j < pn;
+      S.sx[q] = ok ? stage[d.z + j] : NO_MATCH;
+      S.pr[q] = ok && a.prid ? a.prid[d.z + j] : 0u;
+    }
+  }
+}
+
 template <typename K>
 __global__ void __launch_bounds__(WF_T) hj_write_fast(HJArgs a, const uint16_t* __restrict__ stage,
                                                       const uint8_t* __restrict__ multi) {
@@ -627,67 +675,33 @@ __global__ void __launch_bounds__(WF_T) hj_write_fast(HJArgs a, const uint16_t* 
   __shared__ uint2 buf[WF_T / 32][32 * N];
   const uint32_t lane = lane_id();
   uint2* wb = buf[threadIdx.x / 32];
-  const uint64_t ntask = (uint64_t)a.U * HW;
-  const uint64_t nwarp = (uint64_t)gridDim.x * (blockDim.x / 32);
-  for (uint64_t task = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; task < ntask; task += nwarp) {
-    const uint32_t u = (uint32_t)(task / HW), w = (uint32_t)(task % HW);
+  const uint32_t nwarp = gridDim.x * (blockDim.x / 32);
+  // element e of the key array <-> stage[e], prid[e]: vector loads line up when the
+  // three arrays have the same phase modulo the vector's element count
+  const bool vec = reinterpret_cast<uint64_t>(stage) % (2 * N) == 0 &&
+                   (reinterpret_cast<uint64_t>(a.pkey) / sizeof(K)) % N == 0 &&
+                   (!a.prid || reinterpret_cast<uint64_t>(a.prid) % (4 * N) == 0);
+  for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) / 32; u < a.U; u += nwarp) {
     if (multi[u]) continue;  // warp-uniform: hj_write_kernel writes this unit
     const uint4 d = a.desc[u];
-    const uint32_t pn = d.w;
-    const Span sp = span16(a.pkey, d.z, pn, sizeof(K));
-    // element e of the key array <-> stage[e], prid[e]: vector loads line up when the
-    // three arrays have the same phase modulo the vector's element count
-    const uint64_t kph = (reinterpret_cast<uint64_t>(a.pkey) / sizeof(K)) % N;
-    const bool vec = reinterpret_cast<uint64_t>(stage) % (2 * N) == 0 && kph == 0 &&
-                     (!a.prid || reinterpret_cast<uint64_t>(a.prid) % (4 * N) == 0);
-    uint32_t vb, ve;
-    warp_vecs(sp.nv, w, vb, ve);
-    uint64_t base = a.woff[task];
-    const uint16_t* st = stage + d.z;
-    for (uint32_t v0 = vb; v0 < ve; v0 += 32) {  // warp-uniform
-      const uint32_t v = v0 + lane;
-      const uint32_t j0 = v * N - sp.shift;  // row of element 0 (wraps below the range)
-      uint32_t sx[N], pr[N], m = 0;
-      if (vec && v < ve) {  // element 0 of my vector is array element e0 = d.z + j0 (mod 2^32), N-aligned
-        const uint32_t e0 = d.z + j0;
-        if (N == 4) {
-          const uint2 x = __ldg(reinterpret_cast<const uint2*>(stage + e0));
-          sx[0] = x.x & 0xFFFF, sx[1] = x.x >> 16, sx[2 % N] = x.y & 0xFFFF, sx[3 % N] = x.y >> 16;
-        } else {
-          const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(stage + e0));
-          sx[0] = x & 0xFFFF, sx[1] = x >> 16;
-        }
-        if (a.prid) {
-          if (N == 4) {
-            const uint4 y = __ldg(reinterpret_cast<const uint4*>(a.prid + e0));
-            pr[0] = y.x, pr[1] = y.y, pr[2 % N] = y.z, pr[3 % N] = y.w;
-          } else {
-            const uint2 y = __ldg(reinterpret_cast<const uint2*>(a.prid + e0));
-            pr[0] = y.x, pr[1] = y.y;
-          }
-        }
+    const Span sp = span16(a.pkey, d.z, d.w, sizeof(K));
+    uint64_t base = a.woff[(uint64_t)u * HW];
+    WStep<K> cur, nxt;
+    wf_load(cur, a, stage, vec, d, sp, lane);
+    for (uint32_t v0 = 0; v0 < sp.nv; v0 += 32) {  // warp-uniform
+      if (v0 + 32 < sp.nv) wf_load(nxt, a, stage, vec, d, sp, v0 + 32 + lane);
+      const uint32_t j0 = (v0 + lane) * N - sp.shift;
+      uint32_t m = 0;
 #pragma unroll
-        for (uint32_t q = 0; q < N; ++q)
-          if (j0 + q >= pn) sx[q] = NO_MATCH;  // outside the unit's rows
-      } else {
-#pragma unroll
-        for (uint32_t q = 0; q < N; ++q) {
-          const uint32_t j = j0 + q;
-          const bool ok = v < ve && j < pn;
-          sx[q] = ok ? st[j] : NO_MATCH;
-          pr[q] = ok && a.prid ? a.prid[d.z + j] : 0u;
-        }
-      }
-#pragma unroll
-      for (uint32_t q = 0; q < N; ++q) m += sx[q] != NO_MATCH;
+      for (uint32_t q = 0; q < N; ++q) m += cur.sx[q] != NO_MATCH;
       const uint32_t incl = warp_incl_scan(m);
       const uint32_t tot = __shfl_sync(FULL, incl, 31);
       uint32_t r = incl - m;
 #pragma unroll
       for (uint32_t q = 0; q < N; ++q) {
-        if (sx[q] != NO_MATCH) {
-          const uint32_t prow = a.prid ? pr[q] : a.prid_base + d.z + j0 + q;
-          const uint32_t brow = a.brid ? __ldg(a.brid + d.x + sx[q]) : a.brid_base + d.x + sx[q];
+        if (cur.sx[q] != NO_MATCH) {
+          const uint32_t prow = a.prid ? cur.pr[q] : a.prid_base + d.z + j0 + q;
+          const uint32_t brow = a.brid ? __ldg(a.brid + d.x + cur.sx[q]) : a.brid_base + d.x + cur.sx[q];
           wb[r++] = a.swap ? make_uint2(prow, brow) : make_uint2(brow, prow);
         }
       }
@@ -695,6 +709,7 @@ __global__ void __launch_bounds__(WF_T) hj_write_fast(HJArgs a, const uint16_t* 
       for (uint32_t t = lane; t < tot; t += 32) a.out[base + t] = wb[t];
       __syncwarp();
       base += tot;
+      cur = nxt;
     }
   }
 }
@@ -881,9 +896,8 @@ void write_impl(gj_ctx* ctx, uint32_t* out) {
   {
     int occ = 0;
     GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hj_write_fast<K>, WF_T, 0));
-    const uint64_t tasks = (uint64_t)a.U * HW;
     const uint32_t grid =
-        (uint32_t)std::min<uint64_t>((tasks + WF_T / 32 - 1) / (WF_T / 32), (uint64_t)ctx->num_sms * std::max(occ, 1));
+        (uint32_t)std::min<uint64_t>((a.U + WF_T / 32 - 1) / (WF_T / 32), (uint64_t)ctx->num_sms * std::max(occ, 1));
     launch(ctx, "hj_write", hj_write_fast<K>, dim3(grid), dim3(WF_T), 0, a, (const uint16_t*)jc.stage,
            (const uint8_t*)jc.multi);
   }

@@ -31,11 +31,15 @@ namespace gj {
 namespace {
 
 
-constexpr int HT = 512;            // threads per CTA
+// 256-thread CTAs, 4 per SM: a CTA builds and probes one unit at a time with two
+// barriers per unit, so independent CTAs hide each other's barrier and shared-memory
+// latency.  The table holds <= 4096 64-bit slots (32 KB): load <= 1/2 for the ~2048-
+// tuple units the planner aims for, <= 3/4 for the largest (3072) build chunks.
+constexpr int HT = 256;            // threads per CTA
 constexpr int HW = HT / 32;        // warps per CTA (counts are kept per (unit, warp))
-constexpr int BCH_MAX = 4096;      // max build tuples per unit
+constexpr int BCH_MAX = 3072;      // max build tuples per unit
 constexpr int PCH_MAX = 4096;      // max probe tuples per unit
-constexpr int TAB_MAX = 2 * BCH_MAX;  // table slots: load <= 1/4 up to 2048 build tuples, <= 1/2 at 4096
+constexpr int TAB_MAX = 4096;      // table slots
 
 // Independent second hash for the in-partition table slot (the partition id
 // already consumed the top bits of khash).
@@ -492,7 +496,7 @@ __device__ __forceinline__ void probe4(uint32_t tb, uint4 x, uint32_t v, uint32_
   }
 }
 
-__global__ void __launch_bounds__(HT, 2) hj_count_i32(HJArgs a, uint16_t* __restrict__ stage,
+__global__ void __launch_bounds__(HT, 4) hj_count_i32(HJArgs a, uint16_t* __restrict__ stage,
                                                    uint8_t* __restrict__ multi,
                                                    unsigned long long* __restrict__ nmulti) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -508,15 +512,18 @@ __global__ void __launch_bounds__(HT, 2) hj_count_i32(HJArgs a, uint16_t* __rest
   const uint4 zero = make_uint4(0, 0, 0, 0);
   uint4 d = a.desc[u];
   UnitPlan P = plan_unit(a, d, w);
-  // register prefetch: one build and one probe vector per thread (all of a 2044-row
+  // register prefetch: two build and two probe vectors per thread (all of a ~2040-row
   // unit; the few extra vectors of larger units are loaded when needed)
-  uint4 bv0 = tid < P.sb.nv ? ldv(P.sb, tid) : zero;
+  uint4 bv0 = tid < P.sb.nv ? ldv(P.sb, tid) : zero, bv1 = tid + HT < P.sb.nv ? ldv(P.sb, tid + HT) : zero;
   uint4 pv0 = P.vb + lane < P.ve ? ldv(P.sp, P.vb + lane) : zero;
+  uint4 pv1 = P.vb + lane + 32 < P.ve ? ldv(P.sp, P.vb + lane + 32) : zero;
   for (; u < U; u += G) {
     const uint4 dn = u + G < U ? a.desc[u + G] : zero;
     const UnitPlan PN = plan_unit(a, dn, w);
     const uint4 nb0 = tid < PN.sb.nv ? ldv(PN.sb, tid) : zero;
+    const uint4 nb1 = tid + HT < PN.sb.nv ? ldv(PN.sb, tid + HT) : zero;
     const uint4 np0 = PN.vb + lane < PN.ve ? ldv(PN.sp, PN.vb + lane) : zero;
+    const uint4 np1 = PN.vb + lane + 32 < PN.ve ? ldv(PN.sp, PN.vb + lane + 32) : zero;
 
     const uint32_t bn = d.y, pn = d.w;
     const uint32_t logT = table_logT(bn);
@@ -525,7 +532,9 @@ __global__ void __launch_bounds__(HT, 2) hj_count_i32(HJArgs a, uint16_t* __rest
     __syncthreads();  // table cleared, s_dup reset
     bool dup = false;
     if (tid < P.sb.nv) dup |= build4(tb, bv0, tid, P.sb.shift, bn, tmask, tshift);
-    for (uint32_t v = tid + HT; v < P.sb.nv; v += HT) dup |= build4(tb, ldv(P.sb, v), v, P.sb.shift, bn, tmask, tshift);
+    if (tid + HT < P.sb.nv) dup |= build4(tb, bv1, tid + HT, P.sb.shift, bn, tmask, tshift);
+    for (uint32_t v = tid + 2 * HT; v < P.sb.nv; v += HT)
+      dup |= build4(tb, ldv(P.sb, v), v, P.sb.shift, bn, tmask, tshift);
     if (__any_sync(FULL, dup) && lane == 0) s_dup = 1;
     __syncthreads();
     const bool unique = s_dup == 0;  // no duplicate build key: stop each probe at its first match
@@ -533,7 +542,9 @@ __global__ void __launch_bounds__(HT, 2) hj_count_i32(HJArgs a, uint16_t* __rest
     uint32_t c = 0;
     bool many = false;
     if (P.vb + lane < P.ve) probe4(tb, pv0, P.vb + lane, P.sp.shift, pn, tmask, tshift, unique, st, vec, c, many);
-    for (uint32_t v = P.vb + lane + 32; v < P.ve; v += 32)
+    if (P.vb + lane + 32 < P.ve)
+      probe4(tb, pv1, P.vb + lane + 32, P.sp.shift, pn, tmask, tshift, unique, st, vec, c, many);
+    for (uint32_t v = P.vb + lane + 64; v < P.ve; v += 32)
       probe4(tb, ldv(P.sp, v), v, P.sp.shift, pn, tmask, tshift, unique, st, vec, c, many);
     c = warp_sum(c);
     if (lane == 0) a.wcnt[(uint64_t)u * HW + w] = c;
@@ -545,7 +556,7 @@ __global__ void __launch_bounds__(HT, 2) hj_count_i32(HJArgs a, uint16_t* __rest
     for (uint32_t i = tid; i < T / 2; i += HT) sts128z(tb + 16 * i);
     d = dn;
     P = PN;
-    bv0 = nb0, pv0 = np0;
+    bv0 = nb0, bv1 = nb1, pv0 = np0, pv1 = np1;
   }
 }
 

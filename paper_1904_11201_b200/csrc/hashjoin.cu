@@ -31,15 +31,13 @@ namespace gj {
 namespace {
 
 
-// 256-thread CTAs, 4 per SM: a CTA builds and probes one unit at a time with two
-// barriers per unit, so independent CTAs hide each other's barrier and shared-memory
-// latency.  The table holds <= 4096 64-bit slots (32 KB): load <= 1/2 for the ~2048-
-// tuple units the planner aims for, <= 3/4 for the largest (3072) build chunks.
+// 256-thread CTAs: a CTA builds and probes one unit at a time, so several
+// independent CTAs per SM hide each other's barrier and shared-memory latency.
 constexpr int HT = 256;            // threads per CTA
 constexpr int HW = HT / 32;        // warps per CTA (counts are kept per (unit, warp))
-constexpr int BCH_MAX = 3072;      // max build tuples per unit
+constexpr int BCH_MAX = 4096;      // max build tuples per unit
 constexpr int PCH_MAX = 4096;      // max probe tuples per unit
-constexpr int TAB_MAX = 4096;      // table slots
+constexpr int TAB_MAX = 8192;      // table slots of the generic (int64 / re-probe) table
 
 // Independent second hash for the in-partition table slot (the partition id
 // already consumed the top bits of khash).
@@ -69,6 +67,7 @@ struct HJArgs {
   const uint64_t* woff;
   uint2* out;
   int swap;
+  uint64_t nb, np;  // build / probe array lengths (bulk-copy windows are clamped to them)
 };
 
 // The 16-byte vectors covering elements [first, first + cnt) of an array, on absolute
@@ -363,29 +362,46 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
 }
 
 // ---------------------------------------------------------------- int32 count pass
-// The configs[0-3] path, written for instruction count: the table lives at a 32-bit
-// shared-memory address (explicit ld/atom.shared, no generic-address conversion per
-// access); a key vector whose 4 rows all lie in the unit takes a straight-line path
-// (4 hashes, 4 CAS / 4 first-slot loads issued back to back) and only collisions
-// branch; the unit plan (vector spans, warp ranges) of the next unit is computed
-// once, together with its register prefetch.
-__device__ __forceinline__ unsigned long long lds64(uint32_t a) {
-  unsigned long long v;
-  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+// The configs[0-3] path, written for shared-memory throughput and instruction count.
+// Table: 32-bit KEY slots (empty = EMPTY_KEY) plus a parallel uint16 array with the
+// build row of each slot.  An insert is one 32-bit CAS on the key slot (5.5 cycles per
+// warp on B200 vs 10.5 for the 64-bit CAS of a packed (row, key) slot, tools/mb_ops.cu)
+// and a plain 16-bit store of the row; a probe reads the key slot, and the row only
+// on a hit.  A build key equal to EMPTY_KEY cannot live in the table: such rows go to
+// a side list that probes for that key consult.  The table sits at a 32-bit shared
+// address (explicit ld/atom.shared); a key vector whose 4 rows all lie in the unit
+// takes a straight-line path and only collisions branch; the next unit's plan is
+// computed once, together with its register prefetch.
+constexpr uint32_t EMPTY_KEY = 0x80000000u;  // INT32_MIN
+constexpr uint32_t KT = 8192;                // key slots (load <= 1/4 at 2048 build rows, <= 1/2 at 4096)
+constexpr size_t I32_SMEM = KT * 4 + KT * 2 + BCH_MAX * 2;
+
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
   return v;
 }
-__device__ __forceinline__ unsigned long long cas64(uint32_t a, unsigned long long v) {
-  unsigned long long old;
-  asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "r"(a), "l"(0ull), "l"(v) : "memory");
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ uint32_t cas32(uint32_t a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(a), "r"(EMPTY_KEY), "r"(v) : "memory");
   return old;
 }
-__device__ __forceinline__ void sts128z(uint32_t a) {
-  asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(a), "r"(0u) : "memory");
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(a), "r"(x) : "memory");
 }
 __device__ __forceinline__ uint32_t slot32(uint32_t k, uint32_t tshift) { return slot_hash((int32_t)k) >> tshift; }
-__device__ __forceinline__ unsigned long long tval(uint32_t k, uint32_t j) {
-  return ((unsigned long long)(j + 1) << 32) | k;
-}
+
+struct I32Tab {
+  uint32_t key, row, side;  // shared addresses: key slots, row per slot, side list
+};
 
 struct UnitPlan {
   Span sb, sp;
@@ -399,56 +415,73 @@ __device__ __forceinline__ UnitPlan plan_unit(const HJArgs& a, const uint4 d, ui
   return p;
 }
 
-// insert key k (row j) whose first CAS at slot s found `old`; returns duplicate seen
-__device__ __forceinline__ bool insert_walk(uint32_t tb, uint32_t s, uint32_t tmask, uint32_t k, uint32_t j,
-                                         unsigned long long old) {
-  bool dup = false;
-  while (old != 0ull) {
-    dup |= (uint32_t)old == k;
-    s = (s + 1) & tmask;
-    old = cas64(tb + 8 * s, tval(k, j));
+// insert key k (row j); returns true if an equal key was met (a duplicate)
+__device__ __forceinline__ bool insert1(const I32Tab& t, uint32_t s, uint32_t tmask, uint32_t k, uint32_t j,
+                                        uint32_t old, uint32_t* side_n) {
+  if (k == EMPTY_KEY) {  // the empty marker itself: side list
+    const uint32_t at = atomicAdd(side_n, 1u);
+    sts16(t.side + 2 * at, j);
+    return at > 0;
   }
+  bool dup = false;
+  while (old != EMPTY_KEY) {
+    dup |= old == k;
+    s = (s + 1) & tmask;
+    old = cas32(t.key + 4 * s, k);
+  }
+  sts16(t.row + 2 * s, j);
   return dup;
 }
 
-__device__ __forceinline__ bool build4(uint32_t tb, uint4 x, uint32_t v, uint32_t shift, uint32_t bn, uint32_t tmask,
-                                       uint32_t tshift) {
+__device__ __forceinline__ bool build4(const I32Tab& t, uint4 x, uint32_t v, uint32_t shift, uint32_t bn,
+                                       uint32_t tmask, uint32_t tshift, uint32_t* side_n) {
   const uint32_t k[4] = {x.x, x.y, x.z, x.w};
   const uint32_t j0 = v * 4 - shift;
   bool dup = false;
   if (j0 < bn && j0 + 3 < bn) {  // all four rows in the unit: straight line
-    uint32_t s[4];
-    unsigned long long o[4];
+    uint32_t s[4], o[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) s[q] = slot32(k[q], tshift);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) o[q] = cas64(tb + 8 * s[q], tval(k[q], j0 + q));
-    if ((o[0] | o[1] | o[2] | o[3]) != 0ull) {
+    for (int q = 0; q < 4; ++q) o[q] = k[q] != EMPTY_KEY ? cas32(t.key + 4 * s[q], k[q]) : 0u;
+    bool clean = true;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (o[q] != 0ull) dup |= insert_walk(tb, s[q], tmask, k[q], j0 + q, o[q]);
+    for (int q = 0; q < 4; ++q) clean &= o[q] == EMPTY_KEY;
+    if (clean) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sts16(t.row + 2 * s[q], j0 + q);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (o[q] == EMPTY_KEY) sts16(t.row + 2 * s[q], j0 + q);
+        else dup |= insert1(t, s[q], tmask, k[q], j0 + q, o[q], side_n);
+      }
     }
   } else {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (j0 + q < bn) {
         const uint32_t s = slot32(k[q], tshift);
-        const unsigned long long o = cas64(tb + 8 * s, tval(k[q], j0 + q));
-        if (o != 0ull) dup |= insert_walk(tb, s, tmask, k[q], j0 + q, o);
+        const uint32_t o = k[q] != EMPTY_KEY ? cas32(t.key + 4 * s, k[q]) : 0u;
+        if (o == EMPTY_KEY) sts16(t.row + 2 * s, j0 + q);
+        else dup |= insert1(t, s, tmask, k[q], j0 + q, o, side_n);
       }
     }
   }
   return dup;
 }
 
-// walk for key k from slot s (whose entry e did not settle it); returns match count,
-// *f = matching row (the first one if unique)
-__device__ __forceinline__ uint32_t probe_walk(uint32_t tb, uint32_t s, uint32_t tmask, uint32_t k, bool unique,
-                                            unsigned long long e, uint32_t* f) {
+// all matches of key k from slot s (whose entry is e): count, and *f = a matching row
+__device__ __forceinline__ uint32_t probe_walk(const I32Tab& t, uint32_t s, uint32_t tmask, uint32_t k, bool unique,
+                                              uint32_t e, uint32_t side_n, uint32_t* f) {
+  if (k == EMPTY_KEY) {
+    if (side_n) *f = lds16(t.side);
+    return side_n;
+  }
   uint32_t m = 0;
-  for (; e != 0ull; e = lds64(tb + 8 * (s = (s + 1) & tmask))) {
-    if ((uint32_t)e == k) {
-      *f = (uint32_t)(e >> 32) - 1;
+  for (; e != EMPTY_KEY; e = lds32(t.key + 4 * (s = (s + 1) & tmask))) {
+    if (e == k) {
+      *f = lds16(t.row + 2 * s);
       ++m;
       if (unique) break;
     }
@@ -456,34 +489,28 @@ __device__ __forceinline__ uint32_t probe_walk(uint32_t tb, uint32_t s, uint32_t
   return m;
 }
 
-__device__ __forceinline__ void probe4(uint32_t tb, uint4 x, uint32_t v, uint32_t shift, uint32_t pn, uint32_t tmask,
-                                       uint32_t tshift, bool unique, uint16_t* __restrict__ st, bool vec, uint32_t& c,
-                                       bool& many) {
+__device__ __forceinline__ void probe4(const I32Tab& t, uint4 x, uint32_t v, uint32_t shift, uint32_t pn,
+                                       uint32_t tmask, uint32_t tshift, bool unique, uint32_t side_n,
+                                       uint16_t* __restrict__ st, bool vec, uint32_t& c, bool& many) {
   const uint32_t k[4] = {x.x, x.y, x.z, x.w};
   const uint32_t j0 = v * 4 - shift;
   const bool full = j0 < pn && j0 + 3 < pn;
-  uint32_t s[4], r[4];
-  unsigned long long e[4];
+  uint32_t s[4], e[4], r[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) s[q] = slot32(k[q], tshift);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) e[q] = (full || j0 + q < pn) ? lds64(tb + 8 * s[q]) : 0ull;
+  for (int q = 0; q < 4; ++q) e[q] = (full || j0 + q < pn) ? lds32(t.key + 4 * s[q]) : EMPTY_KEY;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    // settled by the first slot: empty (no match) or, for a unique build side, a hit
-    const bool hit = e[q] != 0ull && (uint32_t)e[q] == k[q];
-    uint32_t m = hit ? 1u : 0u, f = (uint32_t)(e[q] >> 32) - 1;
-    if ((e[q] != 0ull && !(hit && unique)) && (full || j0 + q < pn)) {
-      // a walk starts at slot s holding entry e: the first slot itself after a miss,
-      // the slot after it after a (non-unique) hit
-      const uint32_t s0 = hit ? (s[q] + 1) & tmask : s[q];
-      m = probe_walk(tb, s0, tmask, k[q], unique, hit ? lds64(tb + 8 * s0) : e[q], &f);
-      if (hit) {  // bag semantics: the first slot's match plus the walk's
-        m += 1;
-        if (m == 2) f = (uint32_t)(e[q] >> 32) - 1;
-      }
+    const bool valid = full || j0 + q < pn;
+    uint32_t m = 0, f = 0;
+    if (valid && e[q] == k[q] && unique && k[q] != EMPTY_KEY) {  // the common case: hit in the first slot
+      m = 1;
+      f = lds16(t.row + 2 * s[q]);
+    } else if (valid && (e[q] != EMPTY_KEY || k[q] == EMPTY_KEY)) {
+      m = probe_walk(t, s[q], tmask, k[q], unique, e[q], side_n, &f);  // collision, duplicates or the side list
     }
-    c += (full || j0 + q < pn) ? m : 0u;
+    c += m;
     many |= m > 1;
     r[q] = m == 0 ? NO_MATCH : (m == 1 ? f : MULTI);
   }
@@ -497,17 +524,18 @@ __device__ __forceinline__ void probe4(uint32_t tb, uint4 x, uint32_t v, uint32_
 }
 
 __global__ void __launch_bounds__(HT, 4) hj_count_i32(HJArgs a, uint16_t* __restrict__ stage,
-                                                   uint8_t* __restrict__ multi,
-                                                   unsigned long long* __restrict__ nmulti) {
+                                                      uint8_t* __restrict__ multi,
+                                                      unsigned long long* __restrict__ nmulti) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint32_t s_dup;
+  __shared__ uint32_t s_dup, s_side;
   const uint32_t tb = saddr(smem);
+  const I32Tab t{tb, tb + KT * 4, tb + KT * 6};
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
   const uint32_t G = gridDim.x;
   const uint32_t U = (uint32_t)(a.meta[3] / HW);
   uint32_t u = blockIdx.x;
   if (u >= U) return;
-  for (uint32_t i = tid; i < TAB_MAX / 2; i += HT) sts128z(tb + 16 * i);
+  for (uint32_t i = tid; i < KT / 4; i += HT) sts128(t.key + 16 * i, EMPTY_KEY);
   const bool vec = reinterpret_cast<uint64_t>(stage) % 8 == 0 && reinterpret_cast<uint64_t>(a.pkey) % 16 == 0;
   const uint4 zero = make_uint4(0, 0, 0, 0);
   uint4 d = a.desc[u];
@@ -526,34 +554,36 @@ __global__ void __launch_bounds__(HT, 4) hj_count_i32(HJArgs a, uint16_t* __rest
     const uint4 np1 = PN.vb + lane + 32 < PN.ve ? ldv(PN.sp, PN.vb + lane + 32) : zero;
 
     const uint32_t bn = d.y, pn = d.w;
-    const uint32_t logT = table_logT(bn);
+    const uint32_t logT = min(max(32 - __clz(4 * bn - 1), 5u), 13u);  // ~4 slots per build row
     const uint32_t T = 1u << logT, tmask = T - 1, tshift = 32 - logT;
-    if (tid == 0) s_dup = 0;
-    __syncthreads();  // table cleared, s_dup reset
+    if (tid == 0) s_dup = s_side = 0;
+    __syncthreads();  // table cleared, flags reset
     bool dup = false;
-    if (tid < P.sb.nv) dup |= build4(tb, bv0, tid, P.sb.shift, bn, tmask, tshift);
-    if (tid + HT < P.sb.nv) dup |= build4(tb, bv1, tid + HT, P.sb.shift, bn, tmask, tshift);
+    if (tid < P.sb.nv) dup |= build4(t, bv0, tid, P.sb.shift, bn, tmask, tshift, &s_side);
+    if (tid + HT < P.sb.nv) dup |= build4(t, bv1, tid + HT, P.sb.shift, bn, tmask, tshift, &s_side);
     for (uint32_t v = tid + 2 * HT; v < P.sb.nv; v += HT)
-      dup |= build4(tb, ldv(P.sb, v), v, P.sb.shift, bn, tmask, tshift);
+      dup |= build4(t, ldv(P.sb, v), v, P.sb.shift, bn, tmask, tshift, &s_side);
     if (__any_sync(FULL, dup) && lane == 0) s_dup = 1;
     __syncthreads();
     const bool unique = s_dup == 0;  // no duplicate build key: stop each probe at its first match
+    const uint32_t side_n = s_side;
     uint16_t* st = stage + d.z;
     uint32_t c = 0;
     bool many = false;
-    if (P.vb + lane < P.ve) probe4(tb, pv0, P.vb + lane, P.sp.shift, pn, tmask, tshift, unique, st, vec, c, many);
+    if (P.vb + lane < P.ve)
+      probe4(t, pv0, P.vb + lane, P.sp.shift, pn, tmask, tshift, unique, side_n, st, vec, c, many);
     if (P.vb + lane + 32 < P.ve)
-      probe4(tb, pv1, P.vb + lane + 32, P.sp.shift, pn, tmask, tshift, unique, st, vec, c, many);
+      probe4(t, pv1, P.vb + lane + 32, P.sp.shift, pn, tmask, tshift, unique, side_n, st, vec, c, many);
     for (uint32_t v = P.vb + lane + 64; v < P.ve; v += 32)
-      probe4(tb, ldv(P.sp, v), v, P.sp.shift, pn, tmask, tshift, unique, st, vec, c, many);
+      probe4(t, ldv(P.sp, v), v, P.sp.shift, pn, tmask, tshift, unique, side_n, st, vec, c, many);
     c = warp_sum(c);
     if (lane == 0) a.wcnt[(uint64_t)u * HW + w] = c;
     if (__any_sync(FULL, many) && lane == 0) {
       multi[u] = 1;
       atomicAdd(nmulti, 1ull);  // > 0 tells the host to launch the MULTI write pass
     }
-    __syncthreads();  // every probe of this unit is done: clear what it used
-    for (uint32_t i = tid; i < T / 2; i += HT) sts128z(tb + 16 * i);
+    __syncthreads();  // every probe of this unit is done: clear the key slots it used
+    for (uint32_t i = tid; i < T / 4; i += HT) sts128(t.key + 16 * i, EMPTY_KEY);
     d = dn;
     P = PN;
     bv0 = nb0, bv1 = nb1, pv0 = np0, pv1 = np1;
@@ -625,103 +655,89 @@ __global__ void __launch_bounds__(HT) hj_write_kernel(HJArgs a, const uint8_t* _
 }
 
 // Write pass for units without a MULTI row (the usual case): a table-free gather.
-// One warp per unit.  The unit's output is one contiguous range starting at the
-// count pass's offset of (unit, warp 0) -- its warps' row ranges are consecutive --
-// so the warp walks the unit's probe rows in order, 32 key vectors (32 * KVN rows)
-// per step: each lane reads its rows' staged match indices (and probe rids), the warp
-// ranks the matches by a scan, each lane puts its (rid_R, rid_S) pairs into a
-// warp-private shared-memory buffer at its rank, and the warp copies the buffer out
-// with consecutive lanes on consecutive pairs (fully coalesced stores).  The loads of
-// step i + 1 are issued before step i's dependent build-rid gathers, so each warp
-// keeps two steps of loads in flight.  When the stage and probe-rid arrays share the
-// key array's 16-byte phase (always, unless the caller's key view is unaligned and
-// the join has no radix pass) each lane reads its rows' indices / rids as one vector.
-constexpr int WF_T = 256;  // threads per CTA of the write pass
-template <typename K>
-struct WStep {
-  uint32_t sx[16 / sizeof(K)], pr[16 / sizeof(K)];
+// The next unit's build rids, probe rids and staged match indices are streamed into
+// a second shared-memory buffer by 1-D TMA bulk copies (16-byte aligned windows on
+// absolute addresses, elements outside a window read from global memory) while this
+// unit is written.  Warp w writes the probe rows of its count-pass range (the key
+// vectors [w*vpw, (w+1)*vpw)) at its scanned offset, one row per lane per step; a
+// row has at most one match here, so the ranks are a ballot + popc.
+struct WBuf {
+  uint32_t br[BCH_MAX + 4];
+  uint32_t pr[PCH_MAX + 4];
+  uint16_t st[PCH_MAX + 8];
 };
-template <typename K>
-__device__ __forceinline__ void wf_load(WStep<K>& S, const HJArgs& a, const uint16_t* __restrict__ stage, bool vec,
-                                        const uint4 d, const Span& sp, uint32_t v) {
-  constexpr uint32_t N = KVec<K>::N;
-  const uint32_t pn = d.w;
-  const uint32_t j0 = v * N - sp.shift;  // row of element 0 (wraps below the range)
-  if (vec && v < sp.nv) {  // element 0 of my vector is array element e0 = d.z + j0 (mod 2^32), N-aligned
-    const uint32_t e0 = d.z + j0;
-    if (N == 4) {
-      const uint2 x = __ldg(reinterpret_cast<const uint2*>(stage + e0));
-      S.sx[0] = x.x & 0xFFFF, S.sx[1] = x.x >> 16, S.sx[2 % N] = x.y & 0xFFFF, S.sx[3 % N] = x.y >> 16;
-    } else {
-      const uint32_t x = __ldg(reinterpret_cast<const uint32_t*>(stage + e0));
-      S.sx[0] = x & 0xFFFF, S.sx[1] = x >> 16;
-    }
-    if (a.prid) {
-      if (N == 4) {
-        const uint4 y = __ldg(reinterpret_cast<const uint4*>(a.prid + e0));
-        S.pr[0] = y.x, S.pr[1] = y.y, S.pr[2 % N] = y.z, S.pr[3 % N] = y.w;
-      } else {
-        const uint2 y = __ldg(reinterpret_cast<const uint2*>(a.prid + e0));
-        S.pr[0] = y.x, S.pr[1] = y.y;
-      }
-    }
-#pragma unroll
-    for (uint32_t q = 0; q < N; ++q)
-      if (j0 + q >= pn) S.sx[q] = NO_MATCH;  // outside the unit's rows
-  } else {
-#pragma unroll
-    for (uint32_t q = 0; q < N; ++q) {
-      const uint32_t j = j0 + q;
-      const bool ok = v < sp.nv && j < pn;
-      S.sx[q] = ok ? stage[d.z + j] : NO_MATCH;
-      S.pr[q] = ok && a.prid ? a.prid[d.z + j] : 0u;
-    }
+static_assert(sizeof(WBuf) % 16 == 0, "16-byte aligned buffers");
+
+__device__ __forceinline__ void wf_issue(WBuf& B, uint64_t* bar, const uint4 d, const HJArgs& a,
+                                         const uint16_t* stage) {
+  fence_proxy_async();  // generic reads of this buffer (previous unit) before the async writes
+  const Win wb = a.brid ? bulk_window(a.brid, d.x, d.y, 4, a.nb) : Win{nullptr, 0, 0, 0};
+  const Win wp = a.prid ? bulk_window(a.prid, d.z, d.w, 4, a.np) : Win{nullptr, 0, 0, 0};
+  const Win ws = bulk_window(stage, d.z, d.w, 2, a.np);
+  const uint32_t bytes = wb.bytes + wp.bytes + ws.bytes;
+  if (!bytes) {
+    mbar_arrive(bar);
+    return;
   }
+  mbar_expect_tx(bar, bytes);
+  if (wb.bytes) bulk_g2s(B.br, wb.src, wb.bytes, bar);
+  if (wp.bytes) bulk_g2s(B.pr, wp.src, wp.bytes, bar);
+  if (ws.bytes) bulk_g2s(B.st, ws.src, ws.bytes, bar);
 }
 
 template <typename K>
-__global__ void __launch_bounds__(WF_T) hj_write_fast(HJArgs a, const uint16_t* __restrict__ stage,
-                                                      const uint8_t* __restrict__ multi) {
+__global__ void __launch_bounds__(HT) hj_write_fast(HJArgs a, const uint16_t* __restrict__ stage,
+                                                    const uint8_t* __restrict__ multi) {
+  extern __shared__ __align__(16) uint8_t smem[];
   constexpr uint32_t N = KVec<K>::N;
-  __shared__ uint2 buf[WF_T / 32][32 * N];
-  const uint32_t lane = lane_id();
-  uint2* wb = buf[threadIdx.x / 32];
-  const uint32_t nwarp = gridDim.x * (blockDim.x / 32);
-  // element e of the key array <-> stage[e], prid[e]: vector loads line up when the
-  // three arrays have the same phase modulo the vector's element count
-  const bool vec = reinterpret_cast<uint64_t>(stage) % (2 * N) == 0 &&
-                   (reinterpret_cast<uint64_t>(a.pkey) / sizeof(K)) % N == 0 &&
-                   (!a.prid || reinterpret_cast<uint64_t>(a.prid) % (4 * N) == 0);
-  for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) / 32; u < a.U; u += nwarp) {
-    if (multi[u]) continue;  // warp-uniform: hj_write_kernel writes this unit
+  WBuf* B = reinterpret_cast<WBuf*>(smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * sizeof(WBuf));
+  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
+  const uint32_t G = gridDim.x;
+  uint32_t u = blockIdx.x;
+  if (u >= a.U) return;
+  if (tid == 0) {
+    mbar_init(bar + 0, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+    wf_issue(B[0], bar + 0, a.desc[u], a, stage);
+  }
+  __syncthreads();
+  for (uint32_t it = 0; u < a.U; u += G, ++it) {
+    const uint32_t b = it & 1;
     const uint4 d = a.desc[u];
-    const Span sp = span16(a.pkey, d.z, d.w, sizeof(K));
-    uint64_t base = a.woff[(uint64_t)u * HW];
-    WStep<K> cur, nxt;
-    wf_load(cur, a, stage, vec, d, sp, lane);
-    for (uint32_t v0 = 0; v0 < sp.nv; v0 += 32) {  // warp-uniform
-      if (v0 + 32 < sp.nv) wf_load(nxt, a, stage, vec, d, sp, v0 + 32 + lane);
-      const uint32_t j0 = (v0 + lane) * N - sp.shift;
-      uint32_t m = 0;
-#pragma unroll
-      for (uint32_t q = 0; q < N; ++q) m += cur.sx[q] != NO_MATCH;
-      const uint32_t incl = warp_incl_scan(m);
-      const uint32_t tot = __shfl_sync(FULL, incl, 31);
-      uint32_t r = incl - m;
-#pragma unroll
-      for (uint32_t q = 0; q < N; ++q) {
-        if (cur.sx[q] != NO_MATCH) {
-          const uint32_t prow = a.prid ? cur.pr[q] : a.prid_base + d.z + j0 + q;
-          const uint32_t brow = a.brid ? __ldg(a.brid + d.x + cur.sx[q]) : a.brid_base + d.x + cur.sx[q];
-          wb[r++] = a.swap ? make_uint2(prow, brow) : make_uint2(brow, prow);
+    if (tid == 0 && u + G < a.U) wf_issue(B[b ^ 1], bar + (b ^ 1), a.desc[u + G], a, stage);
+    const bool full = multi[u] != 0;
+    mbar_wait(bar + b, (it >> 1) & 1);
+    if (!full) {
+      const Win wb = a.brid ? bulk_window(a.brid, d.x, d.y, 4, a.nb) : Win{nullptr, 0, 0, 0};
+      const Win wp = a.prid ? bulk_window(a.prid, d.z, d.w, 4, a.np) : Win{nullptr, 0, 0, 0};
+      const Win ws = bulk_window(stage, d.z, d.w, 2, a.np);
+      const WBuf& Bb = B[b];
+      // this warp's rows: those of its count-pass key vectors
+      const Span sp = span16(a.pkey, d.z, d.w, sizeof(K));
+      uint32_t vb, ve;
+      warp_vecs(sp.nv, w, vb, ve);
+      const uint32_t wlo = min(max(vb * N, sp.shift) - sp.shift, d.w);
+      const uint32_t whi = min(max(ve * N, sp.shift) - sp.shift, d.w);
+      uint64_t base = a.woff[(uint64_t)u * HW + w];
+      for (uint32_t r0 = wlo; r0 < whi; r0 += 32) {  // warp-uniform
+        const uint32_t i = r0 + lane;
+        const bool valid = i < whi;
+        const uint32_t sx = valid ? (i < ws.valid ? Bb.st[ws.shift + i] : stage[d.z + i]) : NO_MATCH;
+        const bool m = sx != NO_MATCH;
+        const uint32_t bal = __ballot_sync(FULL, m);
+        if (m) {
+          const uint32_t prow = a.prid ? (i < wp.valid ? Bb.pr[wp.shift + i] : a.prid[d.z + i])
+                                       : a.prid_base + d.z + i;
+          const uint32_t brow = a.brid ? (sx < wb.valid ? Bb.br[wb.shift + sx] : a.brid[d.x + sx])
+                                       : a.brid_base + d.x + sx;
+          a.out[base + __popc(bal & lanemask_lt())] = a.swap ? make_uint2(prow, brow) : make_uint2(brow, prow);
         }
+        base += __popc(bal);
       }
-      __syncwarp();
-      for (uint32_t t = lane; t < tot; t += 32) a.out[base + t] = wb[t];
-      __syncwarp();
-      base += tot;
-      cur = nxt;
     }
+    __syncthreads();  // buffer b is refilled by the issue of iteration it + 1
   }
 }
 
@@ -852,7 +868,7 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
     a.meta = meta;
     a.wcnt = wcnt;
     a.swap = swap;
-    const size_t smem = hj_smem<K, false>();
+    const size_t smem = sizeof(K) == 4 ? I32_SMEM : hj_smem<K, false>();
     if (sizeof(K) == 4) {
       set_smem(ctx, hj_count_i32, smem);
       launch(ctx, "hj_count", hj_count_i32, dim3(hj_grid(ctx, hj_count_i32, smem, cap)), dim3(HT), smem, a, stage,
@@ -904,14 +920,12 @@ void write_impl(gj_ctx* ctx, uint32_t* out) {
   a.swap = jc.swap;
   // units without a MULTI row: table-free gather (warp tasks); then the rare MULTI
   // units rebuild their table and re-probe
-  {
-    int occ = 0;
-    GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hj_write_fast<K>, WF_T, 0));
-    const uint32_t grid =
-        (uint32_t)std::min<uint64_t>((a.U + WF_T / 32 - 1) / (WF_T / 32), (uint64_t)ctx->num_sms * std::max(occ, 1));
-    launch(ctx, "hj_write", hj_write_fast<K>, dim3(grid), dim3(WF_T), 0, a, (const uint16_t*)jc.stage,
-           (const uint8_t*)jc.multi);
-  }
+  a.nb = Bld.n;
+  a.np = Prb.n;
+  const size_t fsmem = 2 * sizeof(WBuf) + 16;
+  set_smem(ctx, hj_write_fast<K>, fsmem);
+  launch(ctx, "hj_write", hj_write_fast<K>, dim3(hj_grid(ctx, hj_write_fast<K>, fsmem, a.U)), dim3(HT), fsmem, a,
+         (const uint16_t*)jc.stage, (const uint8_t*)jc.multi);
   if (jc.nmulti == 0) return;
   const size_t smem = hj_smem<K, true>();
   set_smem(ctx, hj_write_kernel<K>, smem);

@@ -157,6 +157,21 @@ def test_equi_all_equal_keys(gj, ctx):
     assert check_equi(gj, ctx, R, S) == 3000 * 2500
 
 
+@pytest.mark.parametrize("n_min_r", [1, 5])
+def test_equi_int32_min_keys(gj, ctx, n_min_r):
+    """INT32_MIN is the int32 table's empty-slot marker: build rows with that key take
+    the side list.  Unique (1 row) and duplicated (5 rows x 3 probe rows -> MULTI) cases,
+    with and without radix passes."""
+    rng = np.random.default_rng(n_min_r)
+    R = rng.integers(-1000, 1000, 6000).astype(np.int32)
+    S = rng.integers(-1000, 1000, 9000).astype(np.int32)
+    R[rng.choice(len(R), n_min_r, replace=False)] = np.iinfo(np.int32).min
+    S[rng.choice(len(S), 3, replace=False)] = np.iinfo(np.int32).min
+    for bits in (-1, 0):
+        ctx.set_option("part_bits", bits)
+        check_equi(gj, ctx, R, S)
+
+
 def test_equi_int64_extremes(gj, ctx):
     rng = np.random.default_rng(5)
     pool = np.array([np.iinfo(np.int64).min, -1, 0, 1, np.iinfo(np.int64).max, 2**40, -2**40], np.int64)

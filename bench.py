@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark of the GPU join hot path (driver contract: one JSON line on rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c4|c1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1|c2|c3|c4|c5] [--impl ours|reference]
 
 Default workload (N=1): BASELINE.json configs[1] -- equi hash join of 2^27 x 2^27
 8-byte tuples (int32 key + int32 payload; payload never read), PK-FK "unique-ish"
@@ -16,8 +16,9 @@ entry `join_host` (pinned H2D of both key columns + D2H of all pairs inside the
 timed region).  `roofline` = the dominant kernel's algorithmic bytes per launch /
 its mean launch time (CUDA events around every launch on the ctx stream, in a
 second, profiled pass of the same K steps) vs MEASURED_PEAKS.json hbm_gbs.
-`cpu_baseline` = the CPU oracle (oracle/, O2 unordered_multimap hash join) timed on
-a bounded PK-FK sample on this host, 1 thread.
+`cpu_baseline` = the CPU oracle timed on a bounded sample of the same workload on this
+host: O7 (O2's unordered_multimap hash join sliced by key hash over all host threads)
+as the value, O2 on one thread beside it.
 
 --impl reference: this tier has no runnable reference implementation; the
 reference arm is the oracle itself, timed the same way on the host cores.
@@ -43,6 +44,7 @@ sys.path.insert(0, ROOT)
 
 S_BITS_C4 = 24  # set from --c4-s-bits
 C5_BITS = 28  # set from --c5-bits
+C3_WEAK = False  # set from --c3-weak
 METRIC = "join input & output tuples/s at 1/2/4/8 B200; % of HBM/INT roofline"
 
 
@@ -164,7 +166,24 @@ def make_workload(name, device, rank=0, world=1):
                 "PK-FK unique R keys")
         if world > 1:
             desc += f"; weak scaling: {world} ranks x (2^27 x 2^27) block shards, NCCL hash shuffle + local join"
-        return dict(kind="equi", R=R, S=S, desc=desc, rid_base=rank * n, n_out_expected=n)
+        return dict(kind="equi", R=R, S=S, desc=desc, rid_base_R=rank * n, rid_base=rank * n, n_out_expected=n)
+    if name == "c3":
+        # configs[2]: R unique over 2^b ranks (perm_b), S = Zipf(1) FK draws over R's ranks
+        # (reading R11).  Strong (default): the full 2^28 x 2^30 on every N
+        # (rank r holds a 1/N block shard).  Weak (--c3-weak): 2^25 x 2^27 per GPU, so
+        # N = 8 is configs[2]'s total (SURVEY reading 17).
+        if C3_WEAK:
+            nr, ns, b = 1 << 25, 1 << 27, 25 + g
+        else:
+            b = 28
+            nr, ns = (1 << 28) // world, (1 << 30) // world
+        R = gd.perm_range(nr, b, seed, offset=rank * nr, device=device)
+        S = gd.zipf_S(ns, b, gd.zipf_table_device(1 << b, device=device), seed, offset=rank * ns, device=device)
+        desc = (f"configs[2]: Zipf(s=1) skewed equi join, R unique over 2^{b} ranks, S Zipf FK; "
+                + (f"weak: 2^25 x 2^27 per GPU x {world}" if C3_WEAK else
+                   f"strong: 2^28 x 2^30 total over {world} GPU(s)"))
+        return dict(kind="equi", R=R, S=S, desc=desc, rid_base_R=rank * nr, rid_base=rank * ns,
+                    n_out_expected=ns)
     if name == "c1":
         R = gd.uniform(10_000, 10_000, seed, 0, device=device)
         S = gd.uniform(10_000, 10_000, seed, 1, device=device)
@@ -191,6 +210,18 @@ def make_workload(name, device, rank=0, world=1):
             desc += "; distributed: range all-reduce, R shuffle, per-owner Bloom all-gather, filtered S shuffle"
         return dict(kind="pf_equi", R=R, S=S, desc=desc, rid_base_R=rank * nr, rid_base=rank * ns)
     raise SystemExit(f"unknown workload {name}")
+
+
+def nvlink_peak(world):
+    """Measured per-GPU NVLink egress of SM peer stores in an all-to-all with world-1
+    peers (profiles/r02_nvlink.json, tools/mb_nvlink.cu), or (None, reason)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_nvlink.json")) as f:
+            t = json.load(f)
+        v = t.get(str(world - 1)) or t.get(str(max(int(k) for k in t if k.isdigit())))
+        return float(v), "profiles/r02_nvlink.json (tools/mb_nvlink.cu, SM peer stores, all-to-all)"
+    except Exception:
+        return None, "not measured"
 
 
 def ncu_traffic(workload, tag):
@@ -354,6 +385,23 @@ def run_ours(args, world, rank, local):
     ktimes = ctx.kernel_times()
     ctx.set_option("profile", 0)
 
+    # receive balance of the hash shuffle (N > 1) and the hash-join unit plan: the
+    # tuples every rank's local join processed, max / mean over ranks
+    recv = None
+    if w["kind"] in ("equi", "pf_equi"):
+        lr, ls = ctx.join_local_sizes()
+        _, pbits, units = ctx.join_stats()
+        recv = {"local_R": lr, "local_S": ls, "partitions": 1 << pbits, "units": units}
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([lr, ls], dtype=torch.float64, device=dev)
+            allt = [torch.zeros_like(t) for _ in range(world)]
+            dist.all_gather(allt, t)
+            a = torch.stack(allt).cpu()
+            recv["recv_R_per_rank"] = [int(x) for x in a[:, 0]]
+            recv["recv_S_per_rank"] = [int(x) for x in a[:, 1]]
+            recv["imbalance_R"] = round(float(a[:, 0].max() / a[:, 0].mean()), 4)
+            recv["imbalance_S"] = round(float(a[:, 1].max() / a[:, 1].mean()), 4)
     info = {"n_out": n, "world": world}
     # local radix passes per relation actually run (the multi-GPU shuffle is "shuffle_scatter")
     info["passes"] = max(1, round(ktimes.get("part_scatter", (0, 0))[1] / args.steps / 2))
@@ -381,6 +429,18 @@ def run_ours(args, world, rank, local):
                 "unit": "GB/s", "frac": round(d.get("achieved_gbs", 0.0) / hbm, 4), "traffic": traffic,
                 "alg_bytes_per_launch": d.get("alg_bytes_per_launch"), "traffic_source": tsrc,
                 "peak_source": peak_src}
+        if "shuffle_scatter" in per_kernel:
+            # the NVLink shuffle: (G-1)/G of every shuffled tuple (key + rid) crosses
+            # NVLink as SM peer stores; vs the measured peer-store egress of
+            # tools/mb_nvlink.cu (profiles/r02_nvlink.json)
+            k = per_kernel["shuffle_scatter"]
+            tup = (nR + nS) / 2  # per launch (one relation per launch; R and S are equal-sized here)
+            wire = tup * (world - 1) / world * (w["R"].element_size() + 4)
+            pk, psrc = nvlink_peak(world)
+            roof["nvlink"] = {"kernel": "shuffle_scatter", "bound": "nvlink", "achieved": round(
+                wire / (k["ms_per_launch"] * 1e-3) / 1e9, 1), "peak": pk, "unit": "GB/s",
+                "frac": round(wire / (k["ms_per_launch"] * 1e-3) / 1e9 / pk, 4) if pk else None,
+                "bytes_per_launch": wire, "peak_source": psrc}
     else:
         # The NLJ compares the pairs of the cells the region matrix keeps (all n_R x n_S
         # with theta_regions=0): INT ALU roofline, 1.5 ALU-pipe instr per pair-compare
@@ -403,7 +463,7 @@ def run_ours(args, world, rank, local):
             roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 3),
                     "unit": "Tpair/s", "frac": round(ach / alu_peak, 4), "traffic": traffic,
                     "alg_bytes_per_launch": d.get("alg_bytes_per_launch"), "traffic_source": tsrc,
-                    "peak_source": "148 SM x 64 ALU lanes/clk x median SM clock / 1.5 ALU instr per pair"}
+                    "peak_source": "148 SM x 64 ALU-pipe instr/clk (measured 62.7-63.5 by tools/mb_ops.cu, profiles/r02_mb_ops.txt) x median SM clock / 1.5 ALU instr per pair"}
         roof["nlj_pairs_per_launch"] = pairs
         roof["cross_pairs"] = cross
         roof["pairs_all"] = nR * world * nS
@@ -480,40 +540,66 @@ def run_ours(args, world, rank, local):
         comm.close()
 
     return dict(ms=ms_max, n=n_global, nR=nR, nS=nS, launches=launches, roof=roof, per_kernel=per_kernel, e2e=e2e,
-                clocks=sampler.summary(), desc=w["desc"], kind=w["kind"], kept=w.get("kept"))
+                clocks=sampler.summary(), desc=w["desc"], kind=w["kind"], kept=w.get("kept"),
+                dtype="i64" if w["R"].dtype == torch.int64 else "i32", recv=recv)
 
 
-def cpu_baseline(args):
-    """The oracle (O2 unordered_multimap + sort, 1 thread) on a bounded PK-FK sample."""
-    import numpy as np
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(args, single=True):
+    """The oracle timed on this host's cores on a bounded sample of the workload.
+    Equi workloads: O7 (O2 sliced by key hash over all host threads) is the value;
+    O2 on one thread is reported beside it (single=True).  Band (c4): O3 on 1 thread."""
+    import numpy as np  # noqa: F401
     import gen
     import oracle
+    T = os.cpu_count() or 1
     if args.workload == "c4":
         R, S = gen.c4(nR=1 << 11, nS=1 << 24)
         t0 = time.perf_counter()
         c = oracle.theta_count_sorted(R, S, "band", gen.C4_EPS)  # noqa: F841
         dt = time.perf_counter() - t0
         return {"value": (len(R) + len(S)) / dt, "unit": "input tuples/s", "cores": 1, "kind": "oracle",
-                "sample": "O3 sort+binary-search band count, R 2^11 x S 2^24 slice of configs[3]", "seconds": dt}
-    if args.workload == "c5":
-        b = args.cpu_sample_bits - 2
-        R, S, m = gen.c5(1 << b, 1 << (b + 1), b=b)
-        t0 = time.perf_counter()
-        c, _ = oracle.hash_equi(R, S)
-        dt = time.perf_counter() - t0
-        assert c == int((m >= 0).sum())
-        return {"value": (len(R) + len(S)) / dt, "unit": "input tuples/s", "cores": 1, "kind": "oracle",
-                "sample": f"O2 unordered_multimap join (exact, no pre-filter), configs[4] shape int64 "
-                          f"2^{b} x 2^{b + 1} over a 2^{b}-row domain", "seconds": round(dt, 3)}
+                "sample": "O3 sort+binary-search band count, R 2^11 x S 2^24 slice of configs[3]", "seconds": dt,
+                "cpu": cpu_model()}
     b = args.cpu_sample_bits
-    R, S, m = gen.pkfk(b, 1 << b)
+    if args.workload == "c5":
+        b -= 2
+        R, S, m = gen.c5(1 << b, 1 << (b + 1), b=b)
+        expect = int((m >= 0).sum())
+        what = f"configs[4] shape int64 2^{b} x 2^{b + 1} over a 2^{b}-row domain (exact join, no pre-filter)"
+    elif args.workload == "c3":
+        b -= 2
+        R, S, m = gen.zipf_pkfk(b, 1 << (b + 2), gen.zipf_table(1 << b))
+        expect = len(S)
+        what = f"configs[2] shape: R 2^{b} unique, S 2^{b + 2} Zipf(1) FK"
+    else:
+        R, S, m = gen.pkfk(b, 1 << b)
+        expect = len(S)
+        what = f"PK-FK 2^{b} x 2^{b} (configs[1] shape, scaled)"
     t0 = time.perf_counter()
-    c, _ = oracle.hash_equi(R, S)
+    c, _ = oracle.hash_equi_sliced(R, S, T)
     dt = time.perf_counter() - t0
-    assert c == 1 << b
-    return {"value": (len(R) + len(S)) / dt, "unit": "input tuples/s", "cores": 1, "kind": "oracle",
-            "sample": f"O2 std::unordered_multimap build/probe + sort, PK-FK 2^{b} x 2^{b} (configs[1] shape, scaled)",
-            "seconds": round(dt, 3)}
+    assert c == expect
+    out = {"value": (len(R) + len(S)) / dt, "unit": "input tuples/s", "cores": T, "kind": "oracle",
+           "sample": f"O7 = O2 (std::unordered_multimap build/probe + sort) sliced by key hash over {T} host "
+                     f"threads, {what}", "seconds": round(dt, 3), "cpu": cpu_model()}
+    if single:
+        t0 = time.perf_counter()
+        c1, _ = oracle.hash_equi(R, S)
+        d1 = time.perf_counter() - t0
+        assert c1 == expect
+        out["single_thread"] = {"value": (len(R) + len(S)) / d1, "cores": 1, "kind": "oracle O2",
+                                "seconds": round(d1, 3)}
+    return out
 
 
 def main():
@@ -533,7 +619,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c4", "c5"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--c3-weak", action="store_true", help="c3: 2^25 x 2^27 per GPU (weak) instead of 2^28 x 2^30 total")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-sample-bits", type=int, default=23)
@@ -542,9 +629,10 @@ def main():
     ap.add_argument("--c5-bits", type=int, default=28, help="log2 |R| per GPU for c5 (|S| = 2|R|; 28 at N=8 = configs[4])")
     ap.add_argument("--opt", action="append", default=[], help="ctx option name=value (tuning sweeps)")
     args = ap.parse_args()
-    global S_BITS_C4, C5_BITS
+    global S_BITS_C4, C5_BITS, C3_WEAK
     S_BITS_C4 = args.c4_s_bits
     C5_BITS = args.c5_bits
+    C3_WEAK = args.c3_weak
     world, rank, local = dist_setup(args)
 
     if args.impl == "reference":
@@ -554,17 +642,17 @@ def main():
         # Warm-up is untimed; one bounded oracle step warms the page cache and
         # the host allocator, further ones would only lengthen the run.
         for _ in range(min(max(args.warmup, 0), 1)):
-            cpu_baseline(args)
+            cpu_baseline(args, single=False)
         for _ in range(args.steps):
-            res.append(cpu_baseline(args))
+            res.append(cpu_baseline(args, single=False))
         v = statistics.median(r["value"] for r in res)
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "input tuples/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": 1e3 * statistics.median(float(r["seconds"]) for r in res),
                 "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "i32", "data": "synthetic",
+                "vs_baseline": None, "dtype": "i64" if args.workload == "c5" else "i32", "data": "synthetic",
                 "config": {"workload": res[0]["sample"]},
-                "cpu_baseline": {k: res[0][k] for k in ("kind", "cores", "sample")} | {"value": v,
+                "cpu_baseline": {k: res[0][k] for k in ("kind", "cores", "sample", "cpu")} | {"value": v,
                                                                                        "unit": "input tuples/s"},
                 "e2e": {"value": v, "unit": "input tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
@@ -587,7 +675,7 @@ def main():
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "i32",
+        "dtype": r["dtype"],
         "data": "synthetic",
         "config": {"workload": r["desc"], "n_R_per_gpu": r["nR"], "n_S_per_gpu": r["nS"], "n_out": r["n"],
                    "l2": "inputs (>=64 MiB of keys, 1 GiB for configs[1]) exceed/stream past the 126 MB L2; no flush",

@@ -147,6 +147,13 @@ gj_status gj_theta_stats(gj_ctx* ctx, uint64_t* nlj_pairs, uint64_t* cross_pairs
  * work units.  Synchronises the stream.  GJ_ESTATE if no equi count ran. */
 gj_status gj_join_stats(gj_ctx* ctx, uint64_t* rsize_eq8, uint32_t* partition_bits, uint32_t* units);
 
+/* Of the last equi count on this ctx (host outputs, either may be NULL): the sizes of
+ * the two relations its local join processed -- the caller's R and S for join_count,
+ * the tuples this rank RECEIVED for join_dist_count* (after the hash shuffle and any
+ * pre-filter), so the receive imbalance of a skewed shuffle can be reported.
+ * GJ_ESTATE if no equi count ran. */
+gj_status gj_join_local_sizes(gj_ctx* ctx, uint64_t* n_R, uint64_t* n_S);
+
 /* ---------------------------------------------------------------- equi join
  * Hash join ("put the smaller table (inner table) into a hash table
  * ... traverse the larger table (outer table)"; §3.3.2).

@@ -9,6 +9,8 @@ Functions (each cites the passage it follows; see oracle.cpp for the C++ bodies)
 
 * ``nlj``                O1  nested loop join, canonical order
 * ``hash_equi``          O2  unordered_multimap build/probe + sort PAPER.md:68
+* ``hash_equi_sliced``   O7  O2 per key slice fmix64(k) mod T on T threads (the
+                             multi-core CPU baseline); pinned to O2
 * ``theta_count_sorted`` O3  sort + binary-search counts          definition (1) in oracle.cpp
 * ``theta_count_per_row`` O3r O3's counts per R row              definition (1) in oracle.cpp
 * ``band_materialize``   O4  sorted range enumeration             definition (1), band
@@ -43,7 +45,7 @@ OPS = {"eq": 0, "ne": 1, "lt": 2, "le": 3, "gt": 4, "ge": 5, "band": 6}
 def build(force: bool = False) -> str:
     """Compile oracle.cpp (plain C++17, -O2, no intrinsics) into liboracle.so."""
     if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(SRC_PATH):
-        subprocess.check_call(["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-o", LIB_PATH, SRC_PATH])
+        subprocess.check_call(["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-pthread", "-o", LIB_PATH, SRC_PATH])
     return LIB_PATH
 
 
@@ -66,6 +68,8 @@ def lib():
         L.orc_theta_count_per_row.restype = None
         L.orc_band_materialize_sorted.argtypes = [vp, u64, vp, u64, i32, u64, u32, u32, vp, u64]
         L.orc_band_materialize_sorted.restype = u64
+        L.orc_hash_equi_sliced.argtypes = [vp, u64, vp, u64, i32, u32, u32, vp, u64, i32]
+        L.orc_hash_equi_sliced.restype = u64
         L.orc_equi_count_hist.argtypes = [vp, u64, vp, u64, i32]
         L.orc_equi_count_hist.restype = u64
         L.orc_semijoin_exact.argtypes = [vp, u64, vp, u64, i32, vp]
@@ -108,6 +112,17 @@ def hash_equi(R, S, rid_base_R=0, rid_base_S=0):
     c = L.orc_equi_count_hist(_ptr(R), len(R), _ptr(S), len(S), t)  # only sizes the buffer
     out = np.empty((max(c, 1), 2), dtype=np.uint32)
     c2 = L.orc_hash_equi(_ptr(R), len(R), _ptr(S), len(S), t, rid_base_R, rid_base_S, _ptr(out), c)
+    return c2, out[: min(c, c2)]
+
+
+def hash_equi_sliced(R, S, threads=0, rid_base_R=0, rid_base_S=0):
+    """O7: O2 sliced by fmix64(key) mod T, one slice per host thread (T = 0: all cores);
+    (count, pairs) in canonical order."""
+    R, S, t = _keys(R, S)
+    L = lib()
+    c = L.orc_equi_count_hist(_ptr(R), len(R), _ptr(S), len(S), t)  # only sizes the buffer
+    out = np.empty((max(c, 1), 2), dtype=np.uint32)
+    c2 = L.orc_hash_equi_sliced(_ptr(R), len(R), _ptr(S), len(S), t, rid_base_R, rid_base_S, _ptr(out), c, threads)
     return c2, out[: min(c, c2)]
 
 

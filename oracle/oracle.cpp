@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <thread>
 #include <unordered_map>
 #include <unordered_set>
 #include <utility>
@@ -120,6 +121,77 @@ uint64_t orc_hash_equi(const void* rkey, uint64_t nR, const void* skey, uint64_t
   std::sort(pairs.begin(), pairs.end());
   for (uint64_t k = 0; k < pairs.size(); ++k) emit(out, cap, k, pairs[k].first, pairs[k].second);
   return pairs.size();
+}
+
+// O7 -- O2 sliced by key: the equi-join decomposes by key value, so with
+// slice(k) = fmix64(k) mod T (the splitmix64 finalizer of the key's 64-bit pattern),
+// J = union over t of hash_equi(R restricted to slice t, S restricted to slice t).
+// Slice t runs O2's algorithm (unordered_multimap on its R rows, probe its S rows in
+// row order) on thread t and sorts its pairs; the sorted slices are then merged
+// pairwise.  The same definition as O2, on T host threads -- the multi-core CPU
+// baseline.  T = 0 means std::thread::hardware_concurrency().
+static uint64_t fmix64(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+
+uint64_t orc_hash_equi_sliced(const void* rkey, uint64_t nR, const void* skey, uint64_t nS, int type,
+                              uint32_t rid_base_R, uint32_t rid_base_S, uint32_t* out, uint64_t cap, int T) {
+  if (T <= 0) T = (int)std::max(1u, std::thread::hardware_concurrency());
+  std::vector<int64_t> R = widen(rkey, nR, type), S = widen(skey, nS, type);
+  using Pair = std::pair<uint32_t, uint32_t>;
+  std::vector<std::vector<Pair>> part((size_t)T);
+  auto slice = [&](int64_t k) { return (size_t)(fmix64((uint64_t)k) % (uint64_t)T); };
+  // rows of each slice, in row order: thread c buckets row chunk c, so slice t's rows
+  // are the concatenation over c of bucket[c][t]
+  std::vector<std::vector<std::vector<uint32_t>>> bR((size_t)T, std::vector<std::vector<uint32_t>>((size_t)T)),
+      bS((size_t)T, std::vector<std::vector<uint32_t>>((size_t)T));
+  auto bucket = [&](int c) {
+    for (uint64_t i = nR * c / T; i < nR * (c + 1) / T; ++i) bR[(size_t)c][slice(R[i])].push_back((uint32_t)i);
+    for (uint64_t j = nS * c / T; j < nS * (c + 1) / T; ++j) bS[(size_t)c][slice(S[j])].push_back((uint32_t)j);
+  };
+  auto work = [&](int t) {
+    std::unordered_multimap<int64_t, uint32_t> table;
+    size_t nt = 0;
+    for (int c = 0; c < T; ++c) nt += bR[(size_t)c][(size_t)t].size();
+    table.reserve(nt);
+    for (int c = 0; c < T; ++c)
+      for (uint32_t i : bR[(size_t)c][(size_t)t]) table.emplace(R[i], i);
+    std::vector<Pair>& pairs = part[(size_t)t];
+    for (int c = 0; c < T; ++c)
+      for (uint32_t j : bS[(size_t)c][(size_t)t]) {
+        auto range = table.equal_range(S[j]);
+        for (auto it = range.first; it != range.second; ++it) pairs.emplace_back(rid_base_R + it->second, rid_base_S + j);
+      }
+    std::sort(pairs.begin(), pairs.end());
+  };
+  {
+    std::vector<std::thread> th;
+    for (int c = 0; c < T; ++c) th.emplace_back(bucket, c);
+    for (auto& x : th) x.join();
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < T; ++t) th.emplace_back(work, t);
+  for (auto& x : th) x.join();
+  // pairwise merge of the sorted slices, in parallel per round
+  for (size_t step = 1; step < part.size(); step *= 2) {
+    std::vector<std::thread> mt;
+    for (size_t a = 0; a + step < part.size(); a += 2 * step)
+      mt.emplace_back([&, a] {
+        std::vector<Pair> m(part[a].size() + part[a + step].size());
+        std::merge(part[a].begin(), part[a].end(), part[a + step].begin(), part[a + step].end(), m.begin());
+        part[a].swap(m);
+        std::vector<Pair>().swap(part[a + step]);
+      });
+    for (auto& x : mt) x.join();
+  }
+  const std::vector<Pair>& all = part[0];
+  for (uint64_t k = 0; k < all.size(); ++k) emit(out, cap, k, all[k].first, all[k].second);
+  return all.size();
 }
 
 // O3 -- theta count by sort + binary search.  With S sorted, for each r:

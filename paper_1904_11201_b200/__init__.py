@@ -70,6 +70,8 @@ def _load():
     L.gj_theta_stats.restype = i32
     L.gj_join_stats.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(u32), ctypes.POINTER(u32)]
     L.gj_join_stats.restype = i32
+    L.gj_join_local_sizes.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(u64)]
+    L.gj_join_local_sizes.restype = i32
     L.gj_gather_payloads.argtypes = [vp, vp, u64, vp, u32, u32, vp, u32, u32, vp, vp]
     L.gj_gather_payloads.restype = i32
     L.gj_ctx_launch_count.argtypes = [vp]
@@ -111,7 +113,8 @@ lib = _load()
 
 # C-ABI symbols declared in include/gjoin.h (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("gj_ctx_create", "gj_ctx_destroy", "gj_ctx_set_stream", "gj_last_error", "gj_ctx_set_option",
-               "gj_ctx_launch_count", "gj_ctx_reset_stats", "gj_ctx_kernel_times", "gj_theta_stats", "gj_join_stats", "gj_gather_payloads", "join_count",
+               "gj_ctx_launch_count", "gj_ctx_reset_stats", "gj_ctx_kernel_times", "gj_theta_stats", "gj_join_stats",
+               "gj_join_local_sizes", "gj_gather_payloads", "join_count",
                "join_materialize", "theta_join_count", "theta_join_materialize", "prefilter", "join_host",
                "join_host_batch",
                "gj_comm_unique_id", "gj_comm_init", "gj_comm_destroy", "join_dist_count", "join_dist_count_filtered",
@@ -183,6 +186,12 @@ class Context:
         e, b, u = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_uint32()
         _check(lib.gj_join_stats(self.h, ctypes.byref(e), ctypes.byref(b), ctypes.byref(u)))
         return int(e.value), int(b.value), int(u.value)
+
+    def join_local_sizes(self) -> tuple:
+        """(n_R, n_S) the last equi count's local join processed (received shards at N > 1)."""
+        a, b = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib.gj_join_local_sizes(self.h, ctypes.byref(a), ctypes.byref(b)))
+        return int(a.value), int(b.value)
 
     def theta_stats(self) -> tuple:
         """(pairs the NLJ compared, pairs written as Green cross products) of the last theta count."""

@@ -383,6 +383,15 @@ gj_status gj_join_stats(gj_ctx* ctx, uint64_t* rsize_eq8, uint32_t* partition_bi
   API_END
 }
 
+gj_status gj_join_local_sizes(gj_ctx* ctx, uint64_t* n_R, uint64_t* n_S) {
+  API_BEGIN
+  if (!ctx) throw Error(GJ_EINVAL, "ctx is NULL");
+  if (!ctx->jc.valid) throw Error(GJ_ESTATE, "gj_join_local_sizes: no equi count on this ctx");
+  if (n_R) *n_R = ctx->jc.R.n;
+  if (n_S) *n_S = ctx->jc.S.n;
+  API_END
+}
+
 gj_status gj_theta_stats(gj_ctx* ctx, uint64_t* nlj_pairs, uint64_t* cross_pairs) {
   API_BEGIN
   if (!ctx) throw Error(GJ_EINVAL, "ctx is NULL");

@@ -128,6 +128,22 @@ def _canon(p):
 
 
 @pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_sliced_oracle_equals_o2(dtype):
+    """O7 (O2 per key slice, T threads) equals O2 -- the slices partition J by key
+    (equal keys share a slice): random tiny instances with duplicates and extremes,
+    T in {1, 2, 3, 8, all cores}, and rid bases."""
+    rng = np.random.default_rng(77 + (dtype == np.int64))
+    for trial in range(300):
+        R, S = _random_instance(rng, dtype)
+        T = [1, 2, 3, 8, 0][trial % 5]
+        c2, p2 = oracle.hash_equi(R, S, rid_base_R=5, rid_base_S=9)
+        c7, p7 = oracle.hash_equi_sliced(R, S, T, rid_base_R=5, rid_base_S=9)
+        assert c7 == c2 and np.array_equal(p7, p2), (R, S, T)
+    R, S, m = gen.pkfk(14, 50_000, seed=3)
+    assert np.array_equal(oracle.hash_equi_sliced(R, S, 6)[1], oracle.pkfk_closed_form(m)[1])
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
 def test_closed_form_invariants(dtype):
     rng = np.random.default_rng(7)
     for _ in range(200):

@@ -27,10 +27,10 @@
  *  - Calls are ordered on the ctx's CUDA stream.  Entry points that return a host
  *    count synchronise that stream once.
  *  - Output pairs are uint32 [rid_R, rid_S] (8 bytes per pair), unordered between
- *    work units but at deterministic positions except that, for an equi join whose
- *    build side has duplicate keys, the matches of one probe tuple may appear in
- *    any order (reading R4).  Parity is defined on the canonically sorted
- *    (rid_R, rid_S) sequence.
+ *    work units but at deterministic positions: the same inputs, options and number
+ *    of GPUs give byte-identical output (reading R4; the matches of one
+ *    probe tuple against duplicate build keys come in build-row order).  Parity is
+ *    defined on the canonically sorted (rid_R, rid_S) sequence.
  *  - Errors: a gj_status code is returned and a thread-local message is available
  *    from gj_last_error(); nothing aborts; nothing is written past `capacity`.
  *    GJ_EINVAL: NULL pointer with n > 0, mismatched key types, unknown op,

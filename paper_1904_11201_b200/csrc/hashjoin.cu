@@ -591,30 +591,88 @@ __global__ void __launch_bounds__(HT, 4) hj_count_i32(HJArgs a, uint16_t* __rest
 }
 
 // Write pass for units with a MULTI row (duplicate build keys) or a partition split
-// over several build chunks: rebuild the table, re-probe, and write every match of
-// a probe row at the warp's scanned offset (same row -> warp map as the count pass).
+// over several build chunks.  The matches of one probe row are written in ascending
+// build-row order, so the output is byte-identical run to run (SPEC.md:539's
+// determinism) even with duplicate build keys, whose table insertion order races:
+// the unit's build rows are sorted by (key, row) in shared memory (bitonic sort), a
+// table of the DISTINCT keys maps each key to the start of its run in that order,
+// and a probe row walks its key's run.  Rows go to warps as in the count pass, so
+// every warp writes at its scanned offset.
+template <typename K>
+struct MultiSmem {
+  static constexpr uint32_t NP = BCH_MAX;  // sort width (power of two >= bn)
+  static constexpr size_t off_srt = (size_t)BCH_MAX * sizeof(K);     // after bk[BCH_MAX]
+  static constexpr size_t off_tab = off_srt + NP * 4;                 // uint32 slot = run start + 1
+  static constexpr size_t off_br = off_tab + TAB_MAX * 4;             // build rids
+  static constexpr size_t bytes = off_br + BCH_MAX * 4;
+};
+
 template <typename K>
 __global__ void __launch_bounds__(HT) hj_write_kernel(HJArgs a, const uint8_t* __restrict__ multi) {
   extern __shared__ __align__(16) uint8_t smem[];
-  Table<K> tab;
-  tab.init(smem);
-  uint32_t* br = reinterpret_cast<uint32_t*>(smem + Table<K>::kBytes);  // BCH_MAX build rids
+  using L = MultiSmem<K>;
+  K* bk = reinterpret_cast<K*>(smem);
+  uint32_t* srt = reinterpret_cast<uint32_t*>(smem + L::off_srt);
+  uint32_t* tab = reinterpret_cast<uint32_t*>(smem + L::off_tab);
+  uint32_t* br = reinterpret_cast<uint32_t*>(smem + L::off_br);
   constexpr uint32_t N = KVec<K>::N;
+  constexpr uint32_t PAD = 0xFFFFFFFFu;  // sorts after every row
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
-  tab.clear(TAB_MAX);
+  const K* __restrict__ bkey = static_cast<const K*>(a.bkey);
+  // (key, row) order; PAD last
+  auto less = [&](uint32_t x, uint32_t y) -> bool {
+    if (y == PAD) return x != PAD;
+    if (x == PAD) return false;
+    return bk[x] < bk[y] || (bk[x] == bk[y] && x < y);
+  };
+  for (uint32_t i = tid; i < TAB_MAX; i += HT) tab[i] = 0u;
   for (uint32_t u = blockIdx.x; u < a.U; u += gridDim.x) {
     if (!multi[u]) continue;  // CTA-uniform: hj_write_fast wrote this unit
     const uint4 d = a.desc[u];
     const uint32_t bn = d.y, pn = d.w;
+    uint32_t np2 = 1;
+    while (np2 < bn) np2 <<= 1;
+    for (uint32_t i = tid; i < np2; i += HT) {
+      srt[i] = i < bn ? i : PAD;
+      if (i < bn) {
+        bk[i] = bkey[d.x + i];
+        br[i] = a.brid ? a.brid[d.x + i] : a.brid_base + d.x + i;
+      }
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= np2; k <<= 1) {  // bitonic sort of srt[0 .. np2)
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = tid; i < np2; i += HT) {
+          const uint32_t l = i ^ j;
+          if (l > i) {
+            const uint32_t x = srt[i], y = srt[l];
+            const bool up = (i & k) == 0;
+            if (up ? less(y, x) : less(x, y)) {
+              srt[i] = y;
+              srt[l] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
     const uint32_t logT = table_logT(bn);
     const uint32_t T = 1u << logT, tmask = T - 1, tshift = 32 - logT;
-    const Span sb = span16(a.bkey, d.x, bn, sizeof(K));
-    for (uint32_t i = tid; i < bn; i += HT) br[i] = a.brid ? a.brid[d.x + i] : a.brid_base + d.x + i;
-    if (Table<K>::kStaged)
-      for (uint32_t v = tid; v < sb.nv; v += HT) stage_vec(tab, ldv(sb, v), v, sb, bn);
+    for (uint32_t p = tid; p < bn; p += HT) {  // distinct keys -> start of their run
+      const K key = bk[srt[p]];
+      if (p == 0 || bk[srt[p - 1]] != key) {
+        uint32_t s = slot_hash(key) >> tshift;
+        while (atomicCAS(&tab[s], 0u, p + 1) != 0u) s = (s + 1) & tmask;
+      }
+    }
     __syncthreads();
-    for (uint32_t v = tid; v < sb.nv; v += HT) build_vec(tab, ldv(sb, v), v, sb, bn, tmask, tshift);
-    __syncthreads();
+    auto run_start = [&](K key) -> uint32_t {  // PAD if the key is absent
+      for (uint32_t s = slot_hash(key) >> tshift;; s = (s + 1) & tmask) {
+        const uint32_t e = tab[s];
+        if (e == 0u) return PAD;
+        if (bk[srt[e - 1]] == key) return e - 1;
+      }
+    };
     const Span sp = span16(a.pkey, d.z, pn, sizeof(K));
     uint32_t vb, ve;
     warp_vecs(sp.nv, w, vb, ve);
@@ -622,34 +680,31 @@ __global__ void __launch_bounds__(HT) hj_write_kernel(HJArgs a, const uint8_t* _
     for (uint32_t v0 = vb; v0 < ve; v0 += 32) {  // warp-uniform
       const uint32_t v = v0 + lane;
       const KVec<K> kv(v < ve ? ldv(sp, v) : make_uint4(0, 0, 0, 0));
-      uint32_t m = 0;
+      uint32_t st[N], m = 0;
 #pragma unroll
       for (uint32_t q = 0; q < N; ++q) {
         const uint32_t j = v * N + q - sp.shift;
-        if (v < ve && j < pn) {
-          uint32_t ss = slot_hash(kv.k[q]) >> tshift;
-          for (auto e = tab.at(ss); !tab.empty(e); e = tab.at(ss = (ss + 1) & tmask)) m += tab.is(e, kv.k[q]);
-        }
+        st[q] = (v < ve && j < pn) ? run_start(kv.k[q]) : PAD;
+        if (st[q] != PAD)
+          for (uint32_t p = st[q]; p < bn && bk[srt[p]] == kv.k[q]; ++p) ++m;
       }
       const uint32_t incl = warp_incl_scan(m);
       uint64_t pos = base + (incl - m);
 #pragma unroll
       for (uint32_t q = 0; q < N; ++q) {
-        const uint32_t j = v * N + q - sp.shift;
-        if (v < ve && j < pn && m) {
+        if (st[q] != PAD) {
+          const uint32_t j = v * N + q - sp.shift;
           const uint32_t prow = a.prid ? a.prid[d.z + j] : a.prid_base + d.z + j;
-          uint32_t ss = slot_hash(kv.k[q]) >> tshift;
-          for (auto e = tab.at(ss); !tab.empty(e); e = tab.at(ss = (ss + 1) & tmask))
-            if (tab.is(e, kv.k[q])) {
-              const uint32_t brow = br[tab.index(e)];
-              a.out[pos++] = a.swap ? make_uint2(prow, brow) : make_uint2(brow, prow);
-            }
+          for (uint32_t p = st[q]; p < bn && bk[srt[p]] == kv.k[q]; ++p) {
+            const uint32_t brow = br[srt[p]];
+            a.out[pos++] = a.swap ? make_uint2(prow, brow) : make_uint2(brow, prow);
+          }
         }
       }
       base += __shfl_sync(FULL, incl, 31);
     }
-    __syncthreads();  // the table and br are rebuilt by the next unit
-    tab.clear(T);
+    __syncthreads();  // sort, table and rids are rebuilt by the next unit
+    for (uint32_t i = tid; i < T; i += HT) tab[i] = 0u;
     __syncthreads();
   }
 }
@@ -927,7 +982,7 @@ void write_impl(gj_ctx* ctx, uint32_t* out) {
   launch(ctx, "hj_write", hj_write_fast<K>, dim3(hj_grid(ctx, hj_write_fast<K>, fsmem, a.U)), dim3(HT), fsmem, a,
          (const uint16_t*)jc.stage, (const uint8_t*)jc.multi);
   if (jc.nmulti == 0) return;
-  const size_t smem = hj_smem<K, true>();
+  const size_t smem = MultiSmem<K>::bytes;
   set_smem(ctx, hj_write_kernel<K>, smem);
   launch(ctx, "hj_write_multi", hj_write_kernel<K>, dim3(hj_grid(ctx, hj_write_kernel<K>, smem, a.U)), dim3(HT),
          smem, a, (const uint8_t*)jc.multi);

@@ -254,6 +254,27 @@ def test_equi_zipf_c3_full_size(gj, ctx):
     assert np.array_equal(r_of_s[torch.from_numpy(js).cuda()].cpu().numpy(), m)
 
 
+@pytest.mark.parametrize("bits,chunk", [(-1, 4096), (4, 64), (0, 4096)])
+def test_equi_deterministic_positions_duplicate_keys(gj, ctx, bits, chunk):
+    """SPEC.md:539 determinism with duplicate BUILD keys (the MULTI write path: table
+    insertion order races, so matches are emitted in sorted build-row order) and with
+    partitions split over several build chunks: byte-identical outputs across runs and
+    contexts, equal to the oracle."""
+    R, S = gen.c1(n=30_000, D=3_000)
+    tR, tS = dev(R), dev(S)
+    ctx.set_option("part_bits", bits)
+    ctx.set_option("build_chunk", chunk)
+    a = gj.join_materialize(ctx, tR, tS).clone()
+    b = gj.join_materialize(ctx, tR, tS).clone()
+    ctx2 = gj.Context(0)
+    ctx2.set_option("part_bits", bits)
+    ctx2.set_option("build_chunk", chunk)
+    c = gj.join_materialize(ctx2, tR, tS)
+    ctx2.close()
+    assert torch.equal(a, b) and torch.equal(a, c)
+    assert np.array_equal(canon_gpu(a), oracle.hash_equi(R, S)[1])
+
+
 def test_equi_deterministic_positions(gj, ctx):
     R, S, _ = gen.pkfk(16, 200_000, seed=3)
     tR, tS = dev(R), dev(S)

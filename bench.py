@@ -377,14 +377,6 @@ def run_ours(args, world, rank, local):
     assert m == n
     ms_max = max_over_ranks(ms, world)
 
-    # ---- profiled pass (per-kernel CUDA events on the ctx stream)
-    ctx.set_option("profile", 1)
-    ctx.reset_stats()
-    for _ in range(args.steps):
-        step()
-    ktimes = ctx.kernel_times()
-    ctx.set_option("profile", 0)
-
     # receive balance of the hash shuffle (N > 1) and the hash-join unit plan: the
     # tuples every rank's local join processed, max / mean over ranks
     recv = None
@@ -402,6 +394,14 @@ def run_ours(args, world, rank, local):
             recv["recv_S_per_rank"] = [int(x) for x in a[:, 1]]
             recv["imbalance_R"] = round(float(a[:, 0].max() / a[:, 0].mean()), 4)
             recv["imbalance_S"] = round(float(a[:, 1].max() / a[:, 1].mean()), 4)
+    # ---- profiled pass (per-kernel CUDA events on the ctx stream)
+    ctx.set_option("profile", 1)
+    ctx.reset_stats()
+    for _ in range(args.steps):
+        step()
+    ktimes = ctx.kernel_times()
+    ctx.set_option("profile", 0)
+
     info = {"n_out": n, "world": world}
     # local radix passes per relation actually run (the multi-GPU shuffle is "shuffle_scatter")
     info["passes"] = max(1, round(ktimes.get("part_scatter", (0, 0))[1] / args.steps / 2))

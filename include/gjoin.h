@@ -86,6 +86,18 @@ typedef struct gj_ctx gj_ctx;
 gj_status gj_ctx_create(gj_ctx** out, int device, void* stream);
 void gj_ctx_destroy(gj_ctx* ctx);
 gj_status gj_ctx_set_stream(gj_ctx* ctx, void* stream);
+/* Scratch allocator hook: the ctx's workspace -- partition buffers,
+ * histograms, unit plans, staged matches, filters -- comes from alloc(bytes, stream,
+ * user) and goes back through free(ptr, bytes, stream, user) instead of cudaMalloc /
+ * cudaFree, so e.g. torch's caching allocator can back it (the Python binding's
+ * Context(torch_allocator=True)).  Returned pointers must be device memory of the ctx's
+ * device, >= 256-byte aligned, valid until freed; alloc returns NULL on failure
+ * (GJ_ENOMEM).  The multi-GPU receive buffers exported over CUDA IPC always use
+ * cudaMalloc (IPC needs allocation bases).  Setting or clearing (NULL, NULL) the hook
+ * synchronises the stream and releases the current workspace. */
+typedef void* (*gj_alloc_fn)(size_t bytes, void* stream, void* user);
+typedef void (*gj_free_fn)(void* ptr, size_t bytes, void* stream, void* user);
+gj_status gj_ctx_set_allocator(gj_ctx* ctx, gj_alloc_fn alloc, gj_free_fn free_fn, void* user);
 /* Thread-local, human-readable description of the last failure. */
 const char* gj_last_error(void);
 

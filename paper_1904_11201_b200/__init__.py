@@ -53,6 +53,10 @@ class _Rel(ctypes.Structure):
                 ("key_type", ctypes.c_int32), ("rid_base", ctypes.c_uint32)]
 
 
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a); "
@@ -64,6 +68,7 @@ def _load():
     L.gj_ctx_destroy.argtypes = [vp]
     L.gj_ctx_destroy.restype = None
     L.gj_ctx_set_stream.argtypes = [vp, vp]
+    L.gj_ctx_set_allocator.argtypes = [vp, ALLOC_FN, FREE_FN, vp]
     L.gj_ctx_set_option.argtypes = [vp, i32, i64]
     L.gj_last_error.restype = ctypes.c_char_p
     L.gj_theta_stats.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(u64)]
@@ -100,7 +105,7 @@ def _load():
     L.gj_region_classify.argtypes = [i32, u32, u64, vp]
     L.gj_region_classify.restype = i32
     L.gj_dist_plan.argtypes = [pu64, i32, i32, i32, ctypes.POINTER(u32), ctypes.POINTER(u32), pu64]
-    for f in ("gj_ctx_create", "gj_ctx_set_stream", "gj_ctx_set_option", "join_count", "join_materialize",
+    for f in ("gj_ctx_create", "gj_ctx_set_stream", "gj_ctx_set_allocator", "gj_ctx_set_option", "join_count", "join_materialize",
               "theta_join_count", "theta_join_materialize", "prefilter", "join_host", "join_host_batch",
               "gj_comm_unique_id",
               "gj_comm_init", "join_dist_count", "join_dist_count_filtered", "join_dist_materialize",
@@ -112,7 +117,7 @@ def _load():
 lib = _load()
 
 # C-ABI symbols declared in include/gjoin.h (checked by tests/test_abi.py)
-ABI_SYMBOLS = ("gj_ctx_create", "gj_ctx_destroy", "gj_ctx_set_stream", "gj_last_error", "gj_ctx_set_option",
+ABI_SYMBOLS = ("gj_ctx_create", "gj_ctx_destroy", "gj_ctx_set_stream", "gj_ctx_set_allocator", "gj_last_error", "gj_ctx_set_option",
                "gj_ctx_launch_count", "gj_ctx_reset_stats", "gj_ctx_kernel_times", "gj_theta_stats", "gj_join_stats",
                "gj_join_local_sizes", "gj_gather_payloads", "join_count",
                "join_materialize", "theta_join_count", "theta_join_materialize", "prefilter", "join_host",
@@ -156,17 +161,40 @@ def _rel(x) -> _Rel:
 
 
 class Context:
-    """gj_ctx bound to a device and (by default) torch's current stream there."""
+    """gj_ctx bound to a device and (by default) torch's current stream there.
 
-    def __init__(self, device: int = 0, stream: Optional[torch.cuda.Stream] = None, **options):
+    torch_allocator=True backs the library's scratch workspace with torch's caching
+    allocator (gj_ctx_set_allocator): the join's partition buffers then show up in,
+    and are recycled by, torch.cuda's memory pool."""
+
+    def __init__(self, device: int = 0, stream: Optional[torch.cuda.Stream] = None, torch_allocator: bool = False,
+                 **options):
         torch.cuda.set_device(device)
         self.device = device
         self.stream = stream if stream is not None else torch.cuda.current_stream(device)
         h = ctypes.c_void_p()
         _check(lib.gj_ctx_create(ctypes.byref(h), device, ctypes.c_void_p(self.stream.cuda_stream)))
         self.h = h
+        self._alloc_cbs = None
+        if torch_allocator:
+            self.use_torch_allocator()
         for k, v in options.items():
             self.set_option(k, v)
+
+    def use_torch_allocator(self):
+        dev = self.device
+
+        def _alloc(nbytes, stream, _user):
+            try:
+                return torch.cuda.caching_allocator_alloc(int(nbytes), dev, int(stream or 0))
+            except Exception:
+                return None
+
+        def _free(ptr, _nbytes, _stream, _user):
+            torch.cuda.caching_allocator_delete(int(ptr))
+
+        self._alloc_cbs = (ALLOC_FN(_alloc), FREE_FN(_free))  # keep the callbacks alive
+        _check(lib.gj_ctx_set_allocator(self.h, self._alloc_cbs[0], self._alloc_cbs[1], None))
 
     def set_option(self, name: str, value: int):
         _check(lib.gj_ctx_set_option(self.h, OPT[name], int(value)))

@@ -29,23 +29,41 @@ gj_status prefilter_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t
 static thread_local std::string g_err;
 void set_last_error(const std::string& m) { g_err = m; }
 
+static void release(gj_ctx* ctx, Buf& b) {
+  if (!b.ptr) return;
+  if (b.ext) ctx->free_fn(b.ptr, b.bytes, ctx->stream, ctx->alloc_user);
+  else cudaFree(b.ptr);
+  b = Buf{};
+}
+
 void* ws(gj_ctx* ctx, const char* name, size_t bytes) {
   Buf& b = ctx->bufs[name];
   if (bytes == 0) bytes = 1;
   if (b.bytes < bytes) {
-    // Grow-only: plain cudaMalloc/cudaFree (synchronising, but rare).  Stream-ordered
-    // pool memory was measured to make NCCL peer transfers ~10x slower.
-    if (b.ptr) GJ_CUDA(cudaFree(b.ptr));
-    b.ptr = nullptr;
-    b.bytes = 0;
+    // Grow-only.  Plain cudaMalloc/cudaFree (synchronising, but rare) unless the caller
+    // installed an allocator hook; stream-ordered pool memory (cudaMallocAsync) was
+    // measured to make NCCL peer transfers ~10x slower.  CUDA-IPC exported buffers
+    // ("ipc.*") need allocation bases: always cudaMalloc.
+    if (b.ext) GJ_CUDA(cudaStreamSynchronize(ctx->stream));  // the hook's free may not be stream-ordered
+    release(ctx, b);
     const size_t rounded = (bytes + (1u << 20) - 1) & ~(size_t)((1u << 20) - 1);
-    cudaError_t e = cudaMalloc(&b.ptr, rounded);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      throw Error(GJ_ENOMEM, std::string("workspace '") + name + "' (" + std::to_string(rounded) +
-                                 " bytes): " + cudaGetErrorString(e));
+    const bool ext = ctx->alloc_fn && std::strncmp(name, "ipc.", 4) != 0;
+    if (ext) {
+      b.ptr = ctx->alloc_fn(rounded, ctx->stream, ctx->alloc_user);
+      if (!b.ptr)
+        throw Error(GJ_ENOMEM, std::string("workspace '") + name + "' (" + std::to_string(rounded) +
+                                   " bytes): the allocator hook returned NULL");
+    } else {
+      cudaError_t e = cudaMalloc(&b.ptr, rounded);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        b.ptr = nullptr;
+        throw Error(GJ_ENOMEM, std::string("workspace '") + name + "' (" + std::to_string(rounded) +
+                                   " bytes): " + cudaGetErrorString(e));
+      }
     }
     b.bytes = rounded;
+    b.ext = ext;
   }
   return b.ptr;
 }
@@ -280,8 +298,7 @@ void gj_ctx_destroy(gj_ctx* ctx) {
     c = nullptr;
   }
   cudaStreamSynchronize(ctx->stream);
-  for (auto& kv : ctx->bufs)
-    if (kv.second.ptr) cudaFree(kv.second.ptr);
+  for (auto& kv : ctx->bufs) release(ctx, kv.second);
   for (auto& kv : ctx->scan_state)
     if (kv.second.ptr) cudaFree(kv.second.ptr);
   for (auto& p : ctx->pending) {
@@ -306,6 +323,20 @@ gj_status gj_ctx_set_stream(gj_ctx* ctx, void* stream) {
   API_BEGIN
   if (!ctx) throw Error(GJ_EINVAL, "ctx is NULL");
   ctx->stream = static_cast<cudaStream_t>(stream);
+  API_END
+}
+
+gj_status gj_ctx_set_allocator(gj_ctx* ctx, gj_alloc_fn alloc, gj_free_fn free_fn, void* user) {
+  API_BEGIN
+  if (!ctx) throw Error(GJ_EINVAL, "ctx is NULL");
+  if ((alloc == nullptr) != (free_fn == nullptr)) throw Error(GJ_EINVAL, "gj_ctx_set_allocator: give both or neither");
+  GJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (auto& kv : ctx->bufs) release(ctx, kv.second);  // the caches point into the workspace
+  ctx->jc = JoinCache{};
+  ctx->tc = ThetaCache{};
+  ctx->alloc_fn = alloc;
+  ctx->free_fn = free_fn;
+  ctx->alloc_user = user;
   API_END
 }
 

@@ -32,6 +32,7 @@ struct Error : std::runtime_error {
 struct Buf {
   void* ptr = nullptr;
   size_t bytes = 0;
+  bool ext = false;  // from the caller's allocator hook (else cudaMalloc)
 };
 
 // Per-call cache so that *_materialize reuses what the preceding *_count built.
@@ -118,8 +119,11 @@ struct gj_ctx {
   int build_side = 0;
   uint32_t hj_unit_cap = 0;  // hash-join unit arrays: capacity the last joins needed
   int shuffle_bits = 0;
-  // workspace
+  // workspace (optionally from the caller's allocator hook)
   std::map<std::string, gj::Buf> bufs;
+  gj_alloc_fn alloc_fn = nullptr;
+  gj_free_fn free_fn = nullptr;
+  void* alloc_user = nullptr;
   std::map<std::string, gj::Buf> pinned_bufs;  // grow-only pinned host staging
   std::map<std::string, gj::ScanState> scan_state;  // per-stream single-pass scan state
   // stats

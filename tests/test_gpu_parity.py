@@ -586,6 +586,22 @@ def test_join_host_batch_stream(gj, ctx):
         gj.join_host_batch(ctx, short)
 
 
+def test_torch_allocator_backs_the_workspace(gj):
+    """gj_ctx_set_allocator with torch's caching allocator: the workspace comes from
+    torch's pool (memory_allocated grows by the partition buffers) and results match."""
+    R, S, m = gen.pkfk(18, 1 << 18, seed=13)
+    tR, tS = dev(R), dev(S)
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_allocated()
+    c = gj.Context(0, torch_allocator=True)
+    n = gj.join_count(c, tR, tS)
+    grown = torch.cuda.memory_allocated() - before
+    assert n == 1 << 18 and grown >= 4 * (1 << 18) * 4  # at least the partitioned keys + rids
+    assert np.array_equal(canon_gpu(gj.join_materialize(c, tR, tS, n)), oracle.pkfk_closed_form(m)[1])
+    c.close()
+    assert torch.cuda.memory_allocated() - before < grown  # released back to torch
+
+
 def test_launch_accounting_and_profile(gj):
     c = gj.Context(0, profile=1)
     R, S = dev(gen.uniform_keys(50_000, 10_000, 1, 0)), dev(gen.uniform_keys(50_000, 10_000, 1, 1))

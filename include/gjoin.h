@@ -313,6 +313,20 @@ gj_status join_dist_count_filtered(gj_ctx* ctx, gj_comm* comm, gj_rel R, gj_rel 
                                    uint64_t* kept_local);
 gj_status join_dist_materialize(gj_ctx* ctx, gj_comm* comm, gj_rel R, gj_rel S, uint32_t* out,
                                 uint64_t capacity, uint64_t* n_written);
+/* Standalone sharded pre-filter (COLLECTIVE; §3.1, Alg.1 -- filter both
+ * tables): every rank gets its OWN shards' surviving tuples back, compacted, in their
+ * original order and with their rids (global through rid_base / rid maps), as prefilter()
+ * would filter the union of the shards: GJ_PF_RANGE keeps keys in the global
+ * [max(min R, min S) - eps, min(max R, max S) + eps] (NCCL min/max all-reduce);
+ * GJ_PF_BLOOM (op = GJ_EQ, or GJ_BAND with eps = 0) drops S tuples absent from a Bloom
+ * filter of ALL ranks' in-range R keys (per-owner filters, OR-reduced over the ranks
+ * and all-gathered; bloom_bits_per_key in [1, 64] of the global |R|); GJ_PF_TWO_SIDED
+ * then filters R by the union of the S survivors the same way.  (GJ_PF_EXACT is
+ * single-GPU only.)  Outputs as prefilter(): DEVICE buffers of the shard sizes,
+ * host counts.  Guarantee: J(survivors of R, survivors of S) over all ranks = J(R, S). */
+gj_status prefilter_dist(gj_ctx* ctx, gj_comm* comm, gj_rel R, gj_rel S, uint32_t flags, int op, uint64_t eps,
+                         double bloom_bits_per_key, void* key_out_R, uint32_t* rid_out_R, uint64_t* n_R_out,
+                         void* key_out_S, uint32_t* rid_out_S, uint64_t* n_S_out);
 gj_status theta_join_dist_count(gj_ctx* ctx, gj_comm* comm, gj_rel R, gj_rel S, int op, uint64_t eps,
                                 uint64_t* n_local, uint64_t* n_global);
 gj_status theta_join_dist_materialize(gj_ctx* ctx, gj_comm* comm, gj_rel R, gj_rel S, int op,

@@ -100,6 +100,7 @@ def _load():
     L.join_dist_count.argtypes = [vp, vp, _Rel, _Rel, pu64, pu64]
     L.join_dist_count_filtered.argtypes = [vp, vp, _Rel, _Rel, u32, ctypes.c_double, pu64, pu64, pu64]
     L.join_dist_materialize.argtypes = [vp, vp, _Rel, _Rel, vp, u64, pu64]
+    L.prefilter_dist.argtypes = [vp, vp, _Rel, _Rel, u32, i32, u64, ctypes.c_double, vp, vp, pu64, vp, vp, pu64]
     L.theta_join_dist_count.argtypes = [vp, vp, _Rel, _Rel, i32, u64, pu64, pu64]
     L.theta_join_dist_materialize.argtypes = [vp, vp, _Rel, _Rel, i32, u64, vp, u64, pu64]
     L.gj_region_classify.argtypes = [i32, u32, u64, vp]
@@ -108,7 +109,7 @@ def _load():
     for f in ("gj_ctx_create", "gj_ctx_set_stream", "gj_ctx_set_allocator", "gj_ctx_set_option", "join_count", "join_materialize",
               "theta_join_count", "theta_join_materialize", "prefilter", "join_host", "join_host_batch",
               "gj_comm_unique_id",
-              "gj_comm_init", "join_dist_count", "join_dist_count_filtered", "join_dist_materialize",
+              "gj_comm_init", "join_dist_count", "join_dist_count_filtered", "join_dist_materialize", "prefilter_dist",
               "theta_join_dist_count", "theta_join_dist_materialize", "gj_dist_plan"):
         getattr(L, f).restype = i32
     return L
@@ -123,7 +124,8 @@ ABI_SYMBOLS = ("gj_ctx_create", "gj_ctx_destroy", "gj_ctx_set_stream", "gj_ctx_s
                "join_materialize", "theta_join_count", "theta_join_materialize", "prefilter", "join_host",
                "join_host_batch",
                "gj_comm_unique_id", "gj_comm_init", "gj_comm_destroy", "join_dist_count", "join_dist_count_filtered",
-               "join_dist_materialize", "theta_join_dist_count", "theta_join_dist_materialize", "gj_dist_plan",
+               "join_dist_materialize", "prefilter_dist", "theta_join_dist_count", "theta_join_dist_materialize",
+               "gj_dist_plan",
                "gj_region_classify")
 COMM_ID_BYTES = 128
 
@@ -453,6 +455,21 @@ def join_dist_count_filtered(ctx: Context, comm: Comm, R, S, flags: int = RANGE 
     _check(lib.join_dist_count_filtered(ctx.h, comm.h, _rel(R), _rel(S), int(flags), float(bloom_bits_per_key),
                                         ctypes.byref(nl), ctypes.byref(ng), kept))
     return nl.value, ng.value, (kept[0], kept[1])
+
+
+def prefilter_dist(ctx: Context, comm: Comm, R, S, flags: int = RANGE | BLOOM | TWO_SIDED, op: str = "eq",
+                   eps: int = 0, bloom_bits_per_key: float = 8.0):
+    """Collective sharded pre-filter: this rank's surviving (R_keys, R_rids, S_keys, S_rids)."""
+    rR, rS = _rel(R), _rel(S)
+    kR = (R.key if isinstance(R, Rel) else R)
+    kS = (S.key if isinstance(S, Rel) else S)
+    okR, orR = torch.empty_like(kR), torch.empty(kR.numel(), dtype=torch.int32, device=kR.device)
+    okS, orS = torch.empty_like(kS), torch.empty(kS.numel(), dtype=torch.int32, device=kS.device)
+    nR, nS = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(lib.prefilter_dist(ctx.h, comm.h, rR, rS, flags, OPS[op], int(eps), float(bloom_bits_per_key),
+                              ctypes.c_void_p(okR.data_ptr()), ctypes.c_void_p(orR.data_ptr()), ctypes.byref(nR),
+                              ctypes.c_void_p(okS.data_ptr()), ctypes.c_void_p(orS.data_ptr()), ctypes.byref(nS)))
+    return okR[: nR.value], orR[: nR.value], okS[: nS.value], orS[: nS.value]
 
 
 def join_dist_materialize(ctx: Context, comm: Comm, R, S, n_local: Optional[int] = None,

@@ -417,6 +417,100 @@ void equi_count_any(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) {
   else dist_equi_count_fused(ctx, c, R, S);
 }
 
+// Standalone sharded pre-filter (SURVEY §8(b) prefilter_dist; §3.1,
+// Alg.1: filter BOTH tables before the join).  Every rank keeps its own shards' rows
+// (no shuffle), compacted to the survivors, exactly as prefilter() would on the union
+// of the shards:
+//  1. range: NCCL min/max all-reduce of the shards' biased min/max ([lo, hi] over both
+//     relations, widened by eps for a band);
+//  2. Bloom (op = EQ or BAND with eps = 0): every rank inserts its in-range R keys into
+//     G per-owner filters (owner = top log2 G bits of the key hash), sized alike on every
+//     rank from the global |R|; rank p receives everyone's filter p (grouped send/recv)
+//     and ORs them, and the G OR'ed filters are all-gathered -- so every rank holds the
+//     filter of the union of the R shards, split by owner, and probes one filter (its
+//     key's owner's) per S tuple;
+//  3. two-sided: the same for the S survivors, which then filter R.
+// No false negatives, so J(prefilter_dist(R), prefilter_dist(S)) = J(R, S).
+void dist_prefilter(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S, uint32_t flags, int op, uint64_t eps,
+                    double bpk, void* kR, uint32_t* rR, uint64_t* nRo, void* kS, uint32_t* rS, uint64_t* nSo) {
+  const int G = c->nranks, me = c->rank;
+  const uint32_t g = log2_exact(G);
+  if (G > MAX_RANKS) throw Error(GJ_EINVAL, "prefilter_dist supports at most 8 ranks");
+  PfSpec spec;
+  const uint64_t e = op == GJ_BAND ? eps : 0;
+  if (flags & GJ_PF_RANGE) {
+    unsigned long long* mm = static_cast<unsigned long long*>(ws(ctx, "dpf.minmax", 4 * 8));
+    pf_minmax(ctx, R, mm);
+    pf_minmax(ctx, S, mm + 2);
+    GJ_NCCL(ncclGroupStart());
+    GJ_NCCL(ncclAllReduce(mm + 0, mm + 0, 1, ncclUint64, ncclMin, c->comm, ctx->stream));
+    GJ_NCCL(ncclAllReduce(mm + 1, mm + 1, 1, ncclUint64, ncclMax, c->comm, ctx->stream));
+    GJ_NCCL(ncclAllReduce(mm + 2, mm + 2, 1, ncclUint64, ncclMin, c->comm, ctx->stream));
+    GJ_NCCL(ncclAllReduce(mm + 3, mm + 3, 1, ncclUint64, ncclMax, c->comm, ctx->stream));
+    GJ_NCCL(ncclGroupEnd());
+    unsigned long long h[4];
+    d2h_sync(ctx, h, mm, sizeof(h));
+    spec.use_range = true;
+    if (h[0] > h[1] || h[2] > h[3]) {  // R or S empty everywhere: nothing joins
+      spec.lo = 1;
+      spec.hi = 0;
+    } else {
+      const unsigned long long lo = std::max(h[0], h[2]), hi = std::min(h[1], h[3]);
+      spec.lo = lo >= e ? lo - e : 0;
+      spec.hi = (~0ull - hi) >= e ? hi + e : ~0ull;
+    }
+  }
+  const bool point = op == GJ_EQ || (op == GJ_BAND && eps == 0);
+  if (!((flags & GJ_PF_BLOOM) && point)) {
+    *nSo = pf_compact(ctx, S, spec, kS, rS, "dpfS");
+    *nRo = pf_compact(ctx, R, spec, kR, rR, "dpfR");
+    return;
+  }
+  // per-owner filters of the union of X's shards (every rank ends with all G)
+  auto union_filters = [&](const gj_rel& X, uint64_t total, const char* tag) -> PfSpec {
+    PfSpec f = spec;
+    const uint32_t lb = pf_log_blocks((total + G - 1) / G, bpk);
+    const uint64_t fw = 8ull << lb;  // words per filter
+    for (int p = 0; p < G; ++p) {
+      f.woff[p] = (uint64_t)p * fw;
+      f.logb[p] = lb;
+    }
+    f.g = g;
+    std::string t(tag);
+    uint32_t* mine = static_cast<uint32_t*>(ws(ctx, (t + ".mine").c_str(), G * fw * 4));
+    uint32_t* got = static_cast<uint32_t*>(ws(ctx, (t + ".got").c_str(), G * fw * 4));
+    uint32_t* all = static_cast<uint32_t*>(ws(ctx, (t + ".all").c_str(), G * fw * 4));
+    pf_bloom_dest(ctx, X, f, mine, G * fw);
+    {
+      RegionScope rs(ctx, "nccl_bloom_exchange");
+      GJ_NCCL(ncclGroupStart());
+      for (int p = 0; p < G; ++p) {
+        GJ_NCCL(ncclSend(mine + (uint64_t)p * fw, fw, ncclUint32, p, c->comm, ctx->stream));
+        GJ_NCCL(ncclRecv(got + (uint64_t)p * fw, fw, ncclUint32, p, c->comm, ctx->stream));
+      }
+      GJ_NCCL(ncclGroupEnd());
+    }
+    pf_bloom_or(ctx, got, fw, (uint32_t)G, all + (uint64_t)me * fw);
+    GJ_NCCL(ncclAllGather(all + (uint64_t)me * fw, all, fw, ncclUint32, c->comm, ctx->stream));
+    f.words = all;
+    f.nfilt = (uint32_t)G;
+    return f;
+  };
+  const PfSpec fS = union_filters(R, allreduce_sum(ctx, c, R.n), "dpf.bR");
+  *nSo = pf_compact(ctx, S, fS, kS, rS, "dpfS");
+  if (flags & GJ_PF_TWO_SIDED) {
+    gj_rel S2 = S;
+    S2.key = kS;
+    S2.rid = rS;
+    S2.n = *nSo;
+    S2.rid_base = 0;
+    const PfSpec fR = union_filters(S2, allreduce_sum(ctx, c, S2.n), "dpf.bS");
+    *nRo = pf_compact(ctx, R, fR, kR, rR, "dpfR");
+  } else {
+    *nRo = pf_compact(ctx, R, spec, kR, rR, "dpfR");
+  }
+}
+
 // Gathers the shards of `members` (ranks, ascending) of relation X into one buffer
 // pair (key, rid) on every member, by grouped send/recv on the job's communicator;
 // n[q] = shard size of rank q.  Shard q's rows keep their global rids.
@@ -683,6 +777,24 @@ gj_status join_dist_count_filtered(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, 
   DAPI_END
 }
 
+gj_status prefilter_dist(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, uint32_t flags, int op, uint64_t eps,
+                         double bloom_bits_per_key, void* key_out_R, uint32_t* rid_out_R, uint64_t* n_R_out,
+                         void* key_out_S, uint32_t* rid_out_S, uint64_t* n_S_out) {
+  DAPI_BEGIN
+  check_args(ctx, c, R, S);
+  if (!n_R_out || !n_S_out) throw Error(GJ_EINVAL, "prefilter_dist: NULL count pointer");
+  if (op != GJ_EQ && op != GJ_BAND) throw Error(GJ_EINVAL, "prefilter_dist: op must be GJ_EQ or GJ_BAND");
+  if (flags & ~(uint32_t)(GJ_PF_RANGE | GJ_PF_BLOOM | GJ_PF_TWO_SIDED))
+    throw Error(GJ_EINVAL, "prefilter_dist: flags must be a combination of RANGE, BLOOM, TWO_SIDED");
+  if ((R.n && (!key_out_R || !rid_out_R)) || (S.n && (!key_out_S || !rid_out_S)))
+    throw Error(GJ_EINVAL, "prefilter_dist: NULL output buffer");
+  if ((flags & GJ_PF_BLOOM) && !(bloom_bits_per_key >= 1.0 && bloom_bits_per_key <= 64.0))
+    throw Error(GJ_EINVAL, "prefilter_dist: bloom_bits_per_key must be in [1, 64]");
+  dist_prefilter(ctx, c, R, S, flags, op, eps, bloom_bits_per_key, key_out_R, rid_out_R, n_R_out, key_out_S,
+                 rid_out_S, n_S_out);
+  DAPI_END
+}
+
 gj_status join_dist_materialize(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, uint32_t* out, uint64_t capacity,
                                 uint64_t* n_written) {
   DAPI_BEGIN
@@ -770,6 +882,10 @@ gj_status join_dist_count_filtered(gj_ctx*, gj_comm*, gj_rel, gj_rel, uint32_t, 
   NO_NCCL;
 }
 gj_status join_dist_materialize(gj_ctx*, gj_comm*, gj_rel, gj_rel, uint32_t*, uint64_t, uint64_t*) { NO_NCCL; }
+gj_status prefilter_dist(gj_ctx*, gj_comm*, gj_rel, gj_rel, uint32_t, int, uint64_t, double, void*, uint32_t*,
+                         uint64_t*, void*, uint32_t*, uint64_t*) {
+  NO_NCCL;
+}
 gj_status theta_join_dist_count(gj_ctx*, gj_comm*, gj_rel, gj_rel, int, uint64_t, uint64_t*, uint64_t*) { NO_NCCL; }
 gj_status theta_join_dist_materialize(gj_ctx*, gj_comm*, gj_rel, gj_rel, int, uint64_t, uint32_t*, uint64_t,
                                       uint64_t*) {

@@ -27,11 +27,17 @@
 namespace gj {
 namespace {
 
+#ifndef GJ_SCATTER_PI
+#define GJ_SCATTER_PI 16
+#endif
+#ifndef GJ_SCATTER_MINB
+#define GJ_SCATTER_MINB 2
+#endif
 constexpr int PT = 256;          // threads per CTA
-constexpr int PI = 16;           // items per thread per tile
+constexpr int PI = GJ_SCATTER_PI;  // items per thread per tile
 constexpr int TILE = PT * PI;    // 4096 tuples per tile
-constexpr int TPC = 16;          // tiles per chunk
-constexpr int CHUNK = TILE * TPC;  // 65536 tuples per chunk
+constexpr int CHUNK = 65536;     // tuples per chunk
+constexpr int TPC = CHUNK / TILE;  // tiles per chunk
 constexpr int NW = PT / 32;
 constexpr int MAX_BITS = 9;      // digits per pass <= 512
 
@@ -182,7 +188,7 @@ struct ScatterLayout {
   static size_t bytes(uint32_t D) { return off_whist + ((size_t)NW * words(D) + (size_t)D) * 4; }
 };
 
-constexpr int SCATTER_MINB = 2;  // CTAs/SM the register budget targets (3: 85 registers + spills, noise level)
+constexpr int SCATTER_MINB = GJ_SCATTER_MINB;  // CTAs/SM the register budget targets
 template <typename K, bool HAS_RID, bool RANGE, bool REMOTE>
 __global__ void __launch_bounds__(PT, SCATTER_MINB) part_scatter(
     const K* __restrict__ key_in, const uint32_t* __restrict__ rid_in, uint32_t rid_base, uint64_t n,

@@ -175,6 +175,35 @@ __global__ void bloom_build(const K* __restrict__ key, uint64_t n, Filt range, u
   }
 }
 
+// Inserts every key passing `range` into the filter of its owner rank d = top g
+// bits of khash (filters at words + woff[d], 2^logb[d] blocks each): the per-owner
+// filters of one rank's shard, before the ranks OR them together (prefilter_dist).
+template <typename K>
+__global__ void bloom_build_dest(const K* __restrict__ key, uint64_t n, Filt range, uint32_t* __restrict__ words) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const K k = key[i];
+    if (!keep(k, range)) continue;
+    const uint32_t d = range.g ? khash(k) >> (32 - range.g) : 0u;
+    const BloomSlot s = bloom_slot(k, range.logb[d]);
+    unsigned long long* bw = reinterpret_cast<unsigned long long*>(words + range.woff[d] + (uint64_t)s.block * 8);
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+      atomicOr(&bw[w], (unsigned long long)s.mask[2 * w] | ((unsigned long long)s.mask[2 * w + 1] << 32));
+  }
+}
+
+// dst[i] = OR over the G pieces src[g * nw + i] (the owner's view of everyone's filter)
+__global__ void bloom_or(const uint4* __restrict__ src, uint64_t nw4, uint32_t G, uint4* __restrict__ dst) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw4; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 a = src[i];
+    for (uint32_t g = 1; g < G; ++g) {
+      const uint4 b = src[(uint64_t)g * nw4 + i];
+      a.x |= b.x, a.y |= b.y, a.z |= b.z, a.w |= b.w;
+    }
+    dst[i] = a;
+  }
+}
+
 // Keep-flags pass: warp w of a tile owns rows [w*32*FI, (w+1)*32*FI) in 32-row
 // groups; each group's ballot is stored as one flag word (bit = lane), so the write
 // pass needs no second probe.  8 probes per thread are independent (in flight at once).
@@ -438,6 +467,27 @@ uint64_t pf_compact(gj_ctx* ctx, const gj_rel& X, const PfSpec& spec, void* kout
 }
 
 void pf_minmax(gj_ctx* ctx, const gj_rel& X, unsigned long long* mm) { key_minmax(ctx, X, mm); }
+
+void pf_bloom_dest(gj_ctx* ctx, const gj_rel& X, const PfSpec& spec, uint32_t* words, uint64_t total_words) {
+  GJ_CUDA(cudaMemsetAsync(words, 0, total_words * sizeof(uint32_t), ctx->stream));
+  if (X.n == 0) return;
+  Filt f = to_filt(spec);
+  f.bloom = nullptr;  // insert: range test only
+  const unsigned grid = (unsigned)std::min<uint64_t>((X.n + 255) / 256, (uint64_t)ctx->num_sms * 16);
+  if (X.key_type == GJ_I32)
+    launch(ctx, "bloom_build", bloom_build_dest<int32_t>, dim3(grid), dim3(256), 0, static_cast<const int32_t*>(X.key),
+           X.n, f, words);
+  else
+    launch(ctx, "bloom_build", bloom_build_dest<int64_t>, dim3(grid), dim3(256), 0, static_cast<const int64_t*>(X.key),
+           X.n, f, words);
+}
+
+void pf_bloom_or(gj_ctx* ctx, const uint32_t* pieces, uint64_t words, uint32_t G, uint32_t* out) {
+  const uint64_t nw4 = words / 4;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nw4 + 255) / 256, (uint64_t)ctx->num_sms * 16));
+  launch(ctx, "bloom_or", bloom_or, dim3(grid), dim3(256), 0, reinterpret_cast<const uint4*>(pieces), nw4, G,
+         reinterpret_cast<uint4*>(out));
+}
 
 gj_status prefilter_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t flags, int op, uint64_t eps,
                          double bpk, void* kR, uint32_t* rR, uint64_t* nRo, void* kS, uint32_t* rS,

@@ -30,5 +30,11 @@ void pf_bloom_into(gj_ctx* ctx, const gj_rel& X, uint32_t* words, uint32_t logb)
 uint64_t pf_compact(gj_ctx* ctx, const gj_rel& X, const PfSpec& spec, void* kout, uint32_t* rout, const char* tag);
 // Device min / max of X's biased keys into mm[0], mm[1] (empty X: ~0, 0).
 void pf_minmax(gj_ctx* ctx, const gj_rel& X, unsigned long long* mm);
+// Per-owner Bloom filters of X's keys that pass spec's range: key k goes into the
+// filter of owner d = top spec.g bits of khash(k), at words + spec.woff[d] with
+// 2^spec.logb[d] blocks; `words` (total_words uint32) is zeroed first.
+void pf_bloom_dest(gj_ctx* ctx, const gj_rel& X, const PfSpec& spec, uint32_t* words, uint64_t total_words);
+// out[i] = OR over g < G of pieces[g * words + i] (words a multiple of 4).
+void pf_bloom_or(gj_ctx* ctx, const uint32_t* pieces, uint64_t words, uint32_t G, uint32_t* out);
 
 }  // namespace gj

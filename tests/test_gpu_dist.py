@@ -112,6 +112,10 @@ def _worker(rank, world, port, q):
         c0, c1 = (rank * len(S5all)) // world, ((rank + 1) * len(S5all)) // world
         R5 = gj.Rel(torch.from_numpy(R5all[a0:a1]).cuda(), None, a0)
         S5 = gj.Rel(torch.from_numpy(S5all[c0:c1]).cuda(), None, c0)
+        for flags in (7, 3, 1):  # standalone sharded pre-filter: this rank's own survivors
+            kR, rR, kS, rS = gj.prefilter_dist(ctx, comm, R5, S5, flags)
+            out[f"pfd{flags}"] = (rR.cpu().numpy().view(np.uint32), rS.cpu().numpy().view(np.uint32),
+                                  kR.cpu().numpy(), kS.cpu().numpy(), (a0, a1, c0, c1))
         for flags in C5_FLAGS:
             nl, ng, kept = gj.join_dist_count_filtered(ctx, comm, R5, S5, flags, 8.0)
             out[f"c5pf{flags}"] = (nl, ng, gj.join_dist_materialize(ctx, comm, R5, S5, nl).cpu().numpy().view(
@@ -207,6 +211,26 @@ def test_dist_joins_match_oracle(world):
             assert kept_S < members + 0.08 * len(S5all), (flags, kept_S)
         if flags & gj.TWO_SIDED:
             assert kept_R < len(R5all), flags
+    # prefilter_dist: each rank's survivors are its own rows, in order, with their keys;
+    # no false negatives (the exact semi-joins survive); the union joins to J(R, S)
+    semR = set(np.nonzero(oracle.semijoin_exact(R5all, S5all))[0].tolist())
+    semS = set(np.nonzero(oracle.semijoin_exact(S5all, R5all))[0].tolist())
+    for flags in (7, 3, 1):
+        allR, allS = [], []
+        for r in range(world):
+            rR, rS, kR, kS, (a0, a1, c0, c1) = res[r][f"pfd{flags}"]
+            assert np.all((rR >= a0) & (rR < a1)) and np.all((rS >= c0) & (rS < c1)), flags
+            assert np.all(np.diff(rR.astype(np.int64)) > 0) and np.all(np.diff(rS.astype(np.int64)) > 0), flags
+            assert np.array_equal(kR, R5all[rR]) and np.array_equal(kS, S5all[rS]), flags
+            allR.append(rR)
+            allS.append(rS)
+        allR, allS = np.concatenate(allR), np.concatenate(allS)
+        assert semS <= set(allS.tolist()), flags
+        if flags & gj.TWO_SIDED:
+            assert semR <= set(allR.tolist()) and len(allR) < len(R5all), flags
+        c, p = oracle.hash_equi(R5all[allR], S5all[allS])
+        p = np.stack([allR[p[:, 0]], allS[p[:, 1]]], 1).astype(np.uint32)
+        assert np.array_equal(_canon(p), pk5[1]), flags
     for name, (cnt, pairs) in expect.items():
         locals_ = [res[r][name] for r in range(world)]
         assert all(l[1] == cnt for l in locals_), name  # n_global

@@ -363,27 +363,22 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
 
 // ---------------------------------------------------------------- int32 count pass
 // The configs[0-3] path, written for shared-memory throughput and instruction count.
-// Table: 32-bit KEY slots (empty = EMPTY_KEY) in buckets of 4 (16 bytes, one LDS.128),
-// plus a parallel uint16 array with the build row of each slot.  A key lives in the
-// first bucket at or after its home bucket that had a free slot when it was inserted,
-// so a probe reads its home bucket and stops there unless the bucket is full -- at
-// load <= 1/4 a bucket overflows for ~0.4% of keys, so warps almost never walk (with
-// linear probing over single slots ~7% of a random-key unit's keys collided, and
-// nearly every warp took the walk: measured 1.15 vs 0.65 ms on configs[1]-size
-// inputs whose keys are not a dense range).  An insert is one 32-bit CAS on the key
-// slot (5.5 cycles per warp on B200 vs 10.5 for a 64-bit CAS, tools/mb_ops.cu) and a
-// plain 16-bit store of the row.  A build key equal to EMPTY_KEY cannot live in the
-// table: such rows go to a side list that probes for that key consult.  The table
-// sits at a 32-bit shared address (explicit ld/atom.shared); the next unit's plan is
+// Table: 32-bit KEY slots (empty = EMPTY_KEY) plus a parallel uint16 array with the
+// build row of each slot.  An insert is one 32-bit CAS on the key slot (5.5 cycles per
+// warp on B200 vs 10.5 for the 64-bit CAS of a packed (row, key) slot, tools/mb_ops.cu)
+// and a plain 16-bit store of the row; a probe reads the key slot, and the row only
+// on a hit.  A build key equal to EMPTY_KEY cannot live in the table: such rows go to
+// a side list that probes for that key consult.  The table sits at a 32-bit shared
+// address (explicit ld/atom.shared); a key vector whose 4 rows all lie in the unit
+// takes a straight-line path and only collisions branch; the next unit's plan is
 // computed once, together with its register prefetch.
 constexpr uint32_t EMPTY_KEY = 0x80000000u;  // INT32_MIN
-constexpr uint32_t KT = 8192;                // key slots = 2048 buckets of 4
+constexpr uint32_t KT = 8192;                // key slots (load <= 1/4 at 2048 build rows, <= 1/2 at 4096)
 constexpr size_t I32_SMEM = KT * 4 + KT * 2 + BCH_MAX * 2;
 
-__device__ __forceinline__ uint4 lds128(uint32_t a) {
-  uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a)
-               : "memory");
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ uint32_t lds16(uint32_t a) {
@@ -402,14 +397,7 @@ __device__ __forceinline__ uint32_t cas32(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void sts128(uint32_t a, uint32_t x) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(a), "r"(x) : "memory");
 }
-__device__ __forceinline__ uint32_t bucket32(uint32_t k, uint32_t bshift) { return slot_hash((int32_t)k) >> bshift; }
-// index 0..3 of the first slot of v equal to x, 4 if none
-__device__ __forceinline__ uint32_t first_eq(const uint4 v, uint32_t x) {
-  return v.x == x ? 0u : v.y == x ? 1u : v.z == x ? 2u : v.w == x ? 3u : 4u;
-}
-__device__ __forceinline__ uint32_t n_eq(const uint4 v, uint32_t x) {
-  return (uint32_t)(v.x == x) + (v.y == x) + (v.z == x) + (v.w == x);
-}
+__device__ __forceinline__ uint32_t slot32(uint32_t k, uint32_t tshift) { return slot_hash((int32_t)k) >> tshift; }
 
 struct I32Tab {
   uint32_t key, row, side;  // shared addresses: key slots, row per slot, side list
@@ -427,86 +415,101 @@ __device__ __forceinline__ UnitPlan plan_unit(const HJArgs& a, const uint4 d, ui
   return p;
 }
 
-// insert key k (row j) whose home bucket b read as v; returns true if an equal key
-// was met (a duplicate: equal keys share their bucket sequence)
-__device__ __forceinline__ bool insert_b(const I32Tab& t, uint32_t b, uint32_t bmask, uint32_t k, uint32_t j, uint4 v,
-                                         uint32_t* side_n) {
+// insert key k (row j); returns true if an equal key was met (a duplicate)
+__device__ __forceinline__ bool insert1(const I32Tab& t, uint32_t s, uint32_t tmask, uint32_t k, uint32_t j,
+                                        uint32_t old, uint32_t* side_n) {
   if (k == EMPTY_KEY) {  // the empty marker itself: side list
     const uint32_t at = atomicAdd(side_n, 1u);
     sts16(t.side + 2 * at, j);
     return at > 0;
   }
   bool dup = false;
-  for (;;) {
-    dup |= n_eq(v, k) != 0;
-    const uint32_t q = first_eq(v, EMPTY_KEY);
-    if (q < 4) {
-      const uint32_t sl = 4 * b + q;
-      if (cas32(t.key + 4 * sl, k) == EMPTY_KEY) {
-        sts16(t.row + 2 * sl, j);
-        return dup;
-      }
-    } else {
-      b = (b + 1) & bmask;  // bucket full: the next one
-    }
-    v = lds128(t.key + 16 * b);  // lost a race for the slot, or a new bucket
+  while (old != EMPTY_KEY) {
+    dup |= old == k;
+    s = (s + 1) & tmask;
+    old = cas32(t.key + 4 * s, k);
   }
-}
-
-__device__ __forceinline__ bool build4(const I32Tab& t, uint4 x, uint32_t v, uint32_t shift, uint32_t bn,
-                                       uint32_t bmask, uint32_t bshift, uint32_t* side_n) {
-  const uint32_t k[4] = {x.x, x.y, x.z, x.w};
-  const uint32_t j0 = v * 4 - shift;
-  bool dup = false;
-  uint32_t b[4];
-  uint4 e[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) b[q] = bucket32(k[q], bshift);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) e[q] = j0 + q < bn ? lds128(t.key + 16 * b[q]) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (j0 + q < bn) dup |= insert_b(t, b[q], bmask, k[q], j0 + q, e[q], side_n);
+  sts16(t.row + 2 * s, j);
   return dup;
 }
 
-// all matches of key k from bucket b (read as v): count, and *f = a matching row
-__device__ __forceinline__ uint32_t probe_b(const I32Tab& t, uint32_t b, uint32_t bmask, uint32_t k, bool unique,
-                                            uint4 v, uint32_t side_n, uint32_t* f) {
+__device__ __forceinline__ bool build4(const I32Tab& t, uint4 x, uint32_t v, uint32_t shift, uint32_t bn,
+                                       uint32_t tmask, uint32_t tshift, uint32_t* side_n) {
+  const uint32_t k[4] = {x.x, x.y, x.z, x.w};
+  const uint32_t j0 = v * 4 - shift;
+  bool dup = false;
+  if (j0 < bn && j0 + 3 < bn) {  // all four rows in the unit: straight line
+    uint32_t s[4], o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s[q] = slot32(k[q], tshift);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = k[q] != EMPTY_KEY ? cas32(t.key + 4 * s[q], k[q]) : 0u;
+    bool clean = true;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) clean &= o[q] == EMPTY_KEY;
+    if (clean) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sts16(t.row + 2 * s[q], j0 + q);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (o[q] == EMPTY_KEY) sts16(t.row + 2 * s[q], j0 + q);
+        else dup |= insert1(t, s[q], tmask, k[q], j0 + q, o[q], side_n);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (j0 + q < bn) {
+        const uint32_t s = slot32(k[q], tshift);
+        const uint32_t o = k[q] != EMPTY_KEY ? cas32(t.key + 4 * s, k[q]) : 0u;
+        if (o == EMPTY_KEY) sts16(t.row + 2 * s, j0 + q);
+        else dup |= insert1(t, s, tmask, k[q], j0 + q, o, side_n);
+      }
+    }
+  }
+  return dup;
+}
+
+// all matches of key k from slot s (whose entry is e): count, and *f = a matching row
+__device__ __forceinline__ uint32_t probe_walk(const I32Tab& t, uint32_t s, uint32_t tmask, uint32_t k, bool unique,
+                                              uint32_t e, uint32_t side_n, uint32_t* f) {
   if (k == EMPTY_KEY) {
     if (side_n) *f = lds16(t.side);
     return side_n;
   }
   uint32_t m = 0;
-  for (;;) {
-    const uint32_t q = first_eq(v, k);
-    if (q < 4) {
-      *f = lds16(t.row + 2 * (4 * b + q));
-      if (unique) return 1;
-      m += n_eq(v, k);
+  for (; e != EMPTY_KEY; e = lds32(t.key + 4 * (s = (s + 1) & tmask))) {
+    if (e == k) {
+      *f = lds16(t.row + 2 * s);
+      ++m;
+      if (unique) break;
     }
-    if (first_eq(v, EMPTY_KEY) < 4) return m;  // a free slot: no later bucket holds k
-    b = (b + 1) & bmask;
-    v = lds128(t.key + 16 * b);
   }
+  return m;
 }
 
 __device__ __forceinline__ void probe4(const I32Tab& t, uint4 x, uint32_t v, uint32_t shift, uint32_t pn,
-                                       uint32_t bmask, uint32_t bshift, bool unique, uint32_t side_n,
+                                       uint32_t tmask, uint32_t tshift, bool unique, uint32_t side_n,
                                        uint16_t* __restrict__ st, bool vec, uint32_t& c, bool& many) {
   const uint32_t k[4] = {x.x, x.y, x.z, x.w};
   const uint32_t j0 = v * 4 - shift;
   const bool full = j0 < pn && j0 + 3 < pn;
-  uint32_t b[4], r[4];
-  uint4 e[4];
+  uint32_t s[4], e[4], r[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) b[q] = bucket32(k[q], bshift);
+  for (int q = 0; q < 4; ++q) s[q] = slot32(k[q], tshift);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) e[q] = (full || j0 + q < pn) ? lds128(t.key + 16 * b[q]) : make_uint4(0, 0, 0, 0);
+  for (int q = 0; q < 4; ++q) e[q] = (full || j0 + q < pn) ? lds32(t.key + 4 * s[q]) : EMPTY_KEY;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
+    const bool valid = full || j0 + q < pn;
     uint32_t m = 0, f = 0;
-    if (full || j0 + q < pn) m = probe_b(t, b[q], bmask, k[q], unique, e[q], side_n, &f);
+    if (valid && e[q] == k[q] && unique && k[q] != EMPTY_KEY) {  // the common case: hit in the first slot
+      m = 1;
+      f = lds16(t.row + 2 * s[q]);
+    } else if (valid && (e[q] != EMPTY_KEY || k[q] == EMPTY_KEY)) {
+      m = probe_walk(t, s[q], tmask, k[q], unique, e[q], side_n, &f);  // collision, duplicates or the side list
+    }
     c += m;
     many |= m > 1;
     r[q] = m == 0 ? NO_MATCH : (m == 1 ? f : MULTI);
@@ -551,8 +554,8 @@ __global__ void __launch_bounds__(HT, 4) hj_count_i32(HJArgs a, uint16_t* __rest
     const uint4 np1 = PN.vb + lane + 32 < PN.ve ? ldv(PN.sp, PN.vb + lane + 32) : zero;
 
     const uint32_t bn = d.y, pn = d.w;
-    const uint32_t logB = min(max(32 - __clz(bn - 1), 3u), 11u);  // buckets >= build rows: load <= 1/4
-    const uint32_t T = 4u << logB, tmask = (1u << logB) - 1, tshift = 32 - logB;  // slots, bucket mask / shift
+    const uint32_t logT = min(max(32 - __clz(4 * bn - 1), 5u), 13u);  // ~4 slots per build row
+    const uint32_t T = 1u << logT, tmask = T - 1, tshift = 32 - logT;
     if (tid == 0) s_dup = s_side = 0;
     __syncthreads();  // table cleared, flags reset
     bool dup = false;

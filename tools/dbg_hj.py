@@ -1,5 +1,5 @@
 """Debug helper (GPU): hj_count time on C2 keys vs the keys one rank receives at N=2
-(perm_28 domain, top khash bit 0), same partition sizes.  python tools/dbg_hj.py [c2|n2|both]"""
+(perm_28 domain, top khash bit 0), same partition sizes.  python tools/dbg_hj.py"""
 import os
 import sys
 
@@ -35,13 +35,14 @@ def run(name, R, S, **opts):
 
 seed = gen.BASE_SEED
 n = 1 << 27
-which = sys.argv[1] if len(sys.argv) > 1 else "both"
-if which in ("both", "c2"):
-    run("c2 B=auto", gd.perm_range(n, 27, seed), gd.pkfk_S(n, 27, seed))
-if which in ("both", "n2"):
-    R2 = gd.perm_range(2 * n, 28, seed)
-    S2 = gd.pkfk_S(2 * n, 28, seed)
-    R2 = R2[top_bit_zero(R2)].contiguous()
-    S2 = S2[top_bit_zero(S2)].contiguous()
-    print("rank0-like sizes", R2.numel(), S2.numel())
-    run("n2-like B=17 (half the partitions empty = N=2's local B=16 below the shuffle bit)", R2, S2, part_bits=17)
+run("c2 B=auto", gd.perm_range(n, 27, seed), gd.pkfk_S(n, 27, seed))
+R2 = gd.perm_range(2 * n, 28, seed)
+S2 = gd.pkfk_S(2 * n, 28, seed)
+R2 = R2[top_bit_zero(R2)].contiguous()
+S2 = S2[top_bit_zero(S2)].contiguous()
+print("rank0-like sizes", R2.numel(), S2.numel())
+run("n2-like B=18", R2, S2, part_bits=18)
+run("c2 B=17 explicit", gd.perm_range(n, 27, seed), gd.pkfk_S(n, 27, seed), part_bits=17)
+R3 = gd.perm_range(n, 27, seed)
+S3 = gd.pkfk_S(n, 27, seed)
+run("c2 B=18", R3, S3, part_bits=18)

@@ -14,22 +14,14 @@
 struct Dst { uint4* p[8]; };
 
 __global__ void a2a_store(Dst d, int ndst, uint64_t n16) {
-  // CTA b writes to destination b % ndst, chunk b / ndst of the per-destination range;
-  // 4 independent 16-byte stores per thread per step
+  // CTA b writes to destination b % ndst, chunk b / ndst of the per-destination range
   const int dst = blockIdx.x % ndst;
   const uint64_t per = gridDim.x / ndst;
   const uint64_t chunk = blockIdx.x / ndst;
   const uint64_t lo = n16 * chunk / per, hi = n16 * (chunk + 1) / per;
   uint4* p = d.p[dst];
   const uint4 v = make_uint4(blockIdx.x, threadIdx.x, 1, 2);
-  uint64_t i = lo + threadIdx.x;
-  for (; i + 3 * blockDim.x < hi; i += 4 * blockDim.x) {
-    p[i] = v;
-    p[i + blockDim.x] = v;
-    p[i + 2 * blockDim.x] = v;
-    p[i + 3 * blockDim.x] = v;
-  }
-  for (; i < hi; i += blockDim.x) p[i] = v;
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) p[i] = v;
 }
 
 int main() {
@@ -47,7 +39,6 @@ int main() {
   }
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  for (int bps : {2, 4, 8})
   for (int npeers = 1; npeers < G; npeers *= 2) {
     std::vector<cudaEvent_t> e0(G), e1(G);
     for (int rep = 0; rep < 2; ++rep) {
@@ -58,7 +49,7 @@ int main() {
         Dst d{};
         for (int k = 0; k < npeers; ++k) d.p[k] = buf[(s + 1 + k) % G][s];
         CK(cudaEventRecord(e0[s]));
-        a2a_store<<<sms * bps / npeers * npeers, 512>>>(d, npeers, n16);
+        a2a_store<<<sms * 4 / npeers * npeers, 512>>>(d, npeers, n16);
         CK(cudaEventRecord(e1[s]));
       }
       for (int s = 0; s < G; ++s) { CK(cudaSetDevice(s)); CK(cudaDeviceSynchronize()); }
@@ -70,7 +61,7 @@ int main() {
       CK(cudaEventElapsedTime(&ms, e0[s], e1[s]));
       if (ms > worst) worst = ms;
     }
-    printf("GPUs=%d peers/GPU=%d CTAs/SM=%d  %.3f ms  egress %.1f GB/s per GPU (%.0f MiB to each peer)\n", G, npeers, bps, worst,
+    printf("GPUs=%d peers/GPU=%d  %.3f ms  egress %.1f GB/s per GPU (%.0f MiB to each peer)\n", G, npeers, worst,
            (double)bytes * npeers / (worst * 1e-3) / 1e9, bytes / 1048576.0);
   }
   return 0;

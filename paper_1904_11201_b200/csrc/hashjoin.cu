@@ -415,126 +415,104 @@ __device__ __forceinline__ UnitPlan plan_unit(const HJArgs& a, const uint4 d, ui
   return p;
 }
 
-// A 4-entry register array indexed by a warp-divergent q: selects, not local memory.
-__device__ __forceinline__ uint32_t pick(const uint32_t (&a)[4], uint32_t q) {
-  return q == 0 ? a[0] : q == 1 ? a[1] : q == 2 ? a[2] : a[3];
-}
-__device__ __forceinline__ void put(uint32_t (&a)[4], uint32_t q, uint32_t v) {
-#pragma unroll
-  for (uint32_t i = 0; i < 4; ++i)
-    if (i == q) a[i] = v;
+// insert key k (row j); returns true if an equal key was met (a duplicate)
+__device__ __forceinline__ bool insert1(const I32Tab& t, uint32_t s, uint32_t tmask, uint32_t k, uint32_t j,
+                                        uint32_t old, uint32_t* side_n) {
+  if (k == EMPTY_KEY) {  // the empty marker itself: side list
+    const uint32_t at = atomicAdd(side_n, 1u);
+    sts16(t.side + 2 * at, j);
+    return at > 0;
+  }
+  bool dup = false;
+  while (old != EMPTY_KEY) {
+    dup |= old == k;
+    s = (s + 1) & tmask;
+    old = cas32(t.key + 4 * s, k);
+  }
+  sts16(t.row + 2 * s, j);
+  return dup;
 }
 
-// Build: the 4 keys of one vector.  The first CAS of every key is issued back to
-// back; keys whose slot was taken continue in ONE warp loop that advances each lane's
-// lowest pending key by a slot per iteration (with linear probing ~7% of random keys
-// collide, so nearly every warp has some: 4 separate divergent walks cost more than
-// the work).  Called by every lane of the warp; a vector index v >= the unit's vector
-// count makes every row of the lane out of range.  Returns true if an equal key was
-// met (a duplicate).
 __device__ __forceinline__ bool build4(const I32Tab& t, uint4 x, uint32_t v, uint32_t shift, uint32_t bn,
                                        uint32_t tmask, uint32_t tshift, uint32_t* side_n) {
-  uint32_t k[4] = {x.x, x.y, x.z, x.w};
+  const uint32_t k[4] = {x.x, x.y, x.z, x.w};
   const uint32_t j0 = v * 4 - shift;
-  uint32_t s[4], o[4];
-  uint32_t pm = 0;  // pending keys (slot taken)
   bool dup = false;
+  if (j0 < bn && j0 + 3 < bn) {  // all four rows in the unit: straight line
+    uint32_t s[4], o[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) s[q] = slot32(k[q], tshift);
+    for (int q = 0; q < 4; ++q) s[q] = slot32(k[q], tshift);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    o[q] = EMPTY_KEY;
-    if (j0 + q < bn) {
-      if (k[q] != EMPTY_KEY) {
-        o[q] = cas32(t.key + 4 * s[q], k[q]);
-      } else {  // the empty marker itself: side list
-        const uint32_t at = atomicAdd(side_n, 1u);
-        sts16(t.side + 2 * at, j0 + q);
-        dup |= at > 0;
+    for (int q = 0; q < 4; ++q) o[q] = k[q] != EMPTY_KEY ? cas32(t.key + 4 * s[q], k[q]) : 0u;
+    bool clean = true;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) clean &= o[q] == EMPTY_KEY;
+    if (clean) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sts16(t.row + 2 * s[q], j0 + q);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (o[q] == EMPTY_KEY) sts16(t.row + 2 * s[q], j0 + q);
+        else dup |= insert1(t, s[q], tmask, k[q], j0 + q, o[q], side_n);
       }
     }
-  }
+  } else {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if (j0 + q < bn && k[q] != EMPTY_KEY) {
-      if (o[q] == EMPTY_KEY) sts16(t.row + 2 * s[q], j0 + q);
-      else pm |= 1u << q;
-    }
-  }
-  while (__any_sync(FULL, pm != 0)) {
-    if (pm) {
-      const uint32_t q = __ffs(pm) - 1;
-      const uint32_t kq = pick(k, q), oq = pick(o, q);
-      dup |= oq == kq;
-      const uint32_t sq = (pick(s, q) + 1) & tmask;
-      const uint32_t on = cas32(t.key + 4 * sq, kq);
-      put(s, q, sq);
-      put(o, q, on);
-      if (on == EMPTY_KEY) {
-        sts16(t.row + 2 * sq, j0 + q);
-        pm &= pm - 1;
+    for (int q = 0; q < 4; ++q) {
+      if (j0 + q < bn) {
+        const uint32_t s = slot32(k[q], tshift);
+        const uint32_t o = k[q] != EMPTY_KEY ? cas32(t.key + 4 * s, k[q]) : 0u;
+        if (o == EMPTY_KEY) sts16(t.row + 2 * s, j0 + q);
+        else dup |= insert1(t, s, tmask, k[q], j0 + q, o, side_n);
       }
     }
   }
   return dup;
 }
 
-// Probe: the 4 keys of one vector, first slots read back to back.  A key is settled
-// by its first slot if that slot is empty (no match) or, for a duplicate-free build
-// side, holds the key; the rest (collisions; every match of a non-unique build side)
-// continue in one warp loop, a slot per iteration for each lane's lowest pending key.
-// Called by every lane of the warp (the pending loop is warp-wide); active = the
-// lane's vector belongs to this warp's range.
-__device__ __forceinline__ void probe4(const I32Tab& t, uint4 x, uint32_t v, bool active, uint32_t shift, uint32_t pn,
+// all matches of key k from slot s (whose entry is e): count, and *f = a matching row
+__device__ __forceinline__ uint32_t probe_walk(const I32Tab& t, uint32_t s, uint32_t tmask, uint32_t k, bool unique,
+                                              uint32_t e, uint32_t side_n, uint32_t* f) {
+  if (k == EMPTY_KEY) {
+    if (side_n) *f = lds16(t.side);
+    return side_n;
+  }
+  uint32_t m = 0;
+  for (; e != EMPTY_KEY; e = lds32(t.key + 4 * (s = (s + 1) & tmask))) {
+    if (e == k) {
+      *f = lds16(t.row + 2 * s);
+      ++m;
+      if (unique) break;
+    }
+  }
+  return m;
+}
+
+__device__ __forceinline__ void probe4(const I32Tab& t, uint4 x, uint32_t v, uint32_t shift, uint32_t pn,
                                        uint32_t tmask, uint32_t tshift, bool unique, uint32_t side_n,
                                        uint16_t* __restrict__ st, bool vec, uint32_t& c, bool& many) {
   const uint32_t k[4] = {x.x, x.y, x.z, x.w};
-  const uint32_t j0 = active ? v * 4 - shift : pn;  // inactive lanes: every row out of range
+  const uint32_t j0 = v * 4 - shift;
   const bool full = j0 < pn && j0 + 3 < pn;
-  uint32_t s[4], e[4], m[4], f[4];
-  uint32_t pm = 0;
+  uint32_t s[4], e[4], r[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) s[q] = slot32(k[q], tshift);
 #pragma unroll
   for (int q = 0; q < 4; ++q) e[q] = (full || j0 + q < pn) ? lds32(t.key + 4 * s[q]) : EMPTY_KEY;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    m[q] = 0;
-    f[q] = 0;
-    if (!(full || j0 + q < pn)) continue;
-    if (k[q] == EMPTY_KEY) {  // rows with the marker key are in the side list
-      m[q] = side_n;
-      if (side_n) f[q] = lds16(t.side);
-    } else if (e[q] == k[q]) {
-      m[q] = 1;
-      f[q] = lds16(t.row + 2 * s[q]);
-      if (!unique) pm |= 1u << q;
-    } else if (e[q] != EMPTY_KEY) {
-      pm |= 1u << q;
+    const bool valid = full || j0 + q < pn;
+    uint32_t m = 0, f = 0;
+    if (valid && e[q] == k[q] && unique && k[q] != EMPTY_KEY) {  // the common case: hit in the first slot
+      m = 1;
+      f = lds16(t.row + 2 * s[q]);
+    } else if (valid && (e[q] != EMPTY_KEY || k[q] == EMPTY_KEY)) {
+      m = probe_walk(t, s[q], tmask, k[q], unique, e[q], side_n, &f);  // collision, duplicates or the side list
     }
-  }
-  while (__any_sync(FULL, pm != 0)) {
-    if (pm) {
-      const uint32_t q = __ffs(pm) - 1;
-      const uint32_t kq = pick(k, q);
-      const uint32_t sq = (pick(s, q) + 1) & tmask;
-      const uint32_t en = lds32(t.key + 4 * sq);
-      put(s, q, sq);
-      if (en == kq) {
-        put(m, q, pick(m, q) + 1);
-        put(f, q, lds16(t.row + 2 * sq));
-        if (unique) pm &= pm - 1;
-      } else if (en == EMPTY_KEY) {
-        pm &= pm - 1;
-      }
-    }
-  }
-  uint32_t r[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    c += m[q];
-    many |= m[q] > 1;
-    r[q] = m[q] == 0 ? NO_MATCH : (m[q] == 1 ? f[q] : MULTI);
+    c += m;
+    many |= m > 1;
+    r[q] = m == 0 ? NO_MATCH : (m == 1 ? f : MULTI);
   }
   if (vec && full) {
     *reinterpret_cast<uint2*>(st + j0) = make_uint2(r[0] | r[1] << 16, r[2] | r[3] << 16);
@@ -581,15 +559,10 @@ __global__ void __launch_bounds__(HT, 4) hj_count_i32(HJArgs a, uint16_t* __rest
     if (tid == 0) s_dup = s_side = 0;
     __syncthreads();  // table cleared, flags reset
     bool dup = false;
-    // every lane of a warp calls build4 / probe4 the same number of times (their walk
-    // loops are warp-wide); out-of-range vectors contribute no rows
-    const uint32_t wt0 = tid & ~31u;  // the warp's first thread
-    if (wt0 < P.sb.nv) dup |= build4(t, bv0, tid, P.sb.shift, bn, tmask, tshift, &s_side);
-    if (wt0 + HT < P.sb.nv) dup |= build4(t, bv1, tid + HT, P.sb.shift, bn, tmask, tshift, &s_side);
-    for (uint32_t v0 = wt0 + 2 * HT; v0 < P.sb.nv; v0 += HT) {
-      const uint32_t v = v0 + lane;
-      dup |= build4(t, v < P.sb.nv ? ldv(P.sb, v) : zero, v, P.sb.shift, bn, tmask, tshift, &s_side);
-    }
+    if (tid < P.sb.nv) dup |= build4(t, bv0, tid, P.sb.shift, bn, tmask, tshift, &s_side);
+    if (tid + HT < P.sb.nv) dup |= build4(t, bv1, tid + HT, P.sb.shift, bn, tmask, tshift, &s_side);
+    for (uint32_t v = tid + 2 * HT; v < P.sb.nv; v += HT)
+      dup |= build4(t, ldv(P.sb, v), v, P.sb.shift, bn, tmask, tshift, &s_side);
     if (__any_sync(FULL, dup) && lane == 0) s_dup = 1;
     __syncthreads();
     const bool unique = s_dup == 0;  // no duplicate build key: stop each probe at its first match
@@ -597,17 +570,12 @@ __global__ void __launch_bounds__(HT, 4) hj_count_i32(HJArgs a, uint16_t* __rest
     uint16_t* st = stage + d.z;
     uint32_t c = 0;
     bool many = false;
-    if (P.vb < P.ve)
-      probe4(t, pv0, P.vb + lane, P.vb + lane < P.ve, P.sp.shift, pn, tmask, tshift, unique, side_n, st, vec, c,
-             many);
-    if (P.vb + 32 < P.ve)
-      probe4(t, pv1, P.vb + lane + 32, P.vb + lane + 32 < P.ve, P.sp.shift, pn, tmask, tshift, unique, side_n, st,
-             vec, c, many);
-    for (uint32_t v0 = P.vb + 64; v0 < P.ve; v0 += 32) {
-      const uint32_t v = v0 + lane;
-      probe4(t, v < P.ve ? ldv(P.sp, v) : zero, v, v < P.ve, P.sp.shift, pn, tmask, tshift, unique, side_n, st, vec,
-             c, many);
-    }
+    if (P.vb + lane < P.ve)
+      probe4(t, pv0, P.vb + lane, P.sp.shift, pn, tmask, tshift, unique, side_n, st, vec, c, many);
+    if (P.vb + lane + 32 < P.ve)
+      probe4(t, pv1, P.vb + lane + 32, P.sp.shift, pn, tmask, tshift, unique, side_n, st, vec, c, many);
+    for (uint32_t v = P.vb + lane + 64; v < P.ve; v += 32)
+      probe4(t, ldv(P.sp, v), v, P.sp.shift, pn, tmask, tshift, unique, side_n, st, vec, c, many);
     c = warp_sum(c);
     if (lane == 0) a.wcnt[(uint64_t)u * HW + w] = c;
     if (__any_sync(FULL, many) && lane == 0) {

@@ -5,22 +5,23 @@
 // (inner table) into a hash table ... traverse the larger table",
 // hash buckets with a small-range probe.  B200 design (DESIGN.md
 // §4.2): after radix partitioning both relations with the same hash bits, every
-// work unit u = (partition p, build chunk, probe chunk) builds an open-addressing
-// (linear probing) table of <= 2048 build tuples in shared memory, ~4 slots per
-// build tuple (<= 4096) sized from the exact unit size -- so it can never overflow
-// (the paper's fixed-size buckets could) -- and streams the probe
-// chunk (<= 2048 tuples) past it.
-// Units have bounded cost (<= 2048 x 2048 tuples), so Zipf-skewed partitions
-// (configs[2]) split into many units instead of serialising one CTA.  CTAs take
-// units round-robin (u = blockIdx.x + k * gridDim.x) from a precomputed descriptor
-// array, and software-pipeline them: the next unit's build and probe keys are
-// loaded into registers while the current unit is built and probed.
+// work unit u = (partition p, build chunk <= 4096 tuples, probe chunk <= 4096) builds
+// an open-addressing (linear probing) table in shared memory sized from the exact
+// unit size, ~4 slots per build tuple (<= 8192) -- so it can never overflow (the
+// paper's fixed-size buckets could) -- and probes the probe chunk
+// against it.  Units have bounded cost, so Zipf-skewed partitions (configs[2]) split
+// into many units instead of serialising one CTA.  CTAs (256 threads) take units
+// round-robin (u = blockIdx.x + k * gridDim.x) from a descriptor array built on the
+// device, and prefetch the next unit's key vectors into registers while the current
+// unit is built and probed.
 //
-// Exact result sizing (replacing the paper's NB_T*NB_S slots):
-// the count kernel stores one count per (unit, warp); an exclusive scan turns them
-// into output offsets; the write kernel re-probes and each warp writes its matches
-// at its offset, ranked inside the warp by a shuffle scan -- deterministic
-// positions, no atomics on the output.
+// Exact result sizing (replacing the paper's NB_T*NB_S slots): the
+// count pass stores one count per (unit, warp) and, per probe row, the matching build
+// row (uint16); an exclusive scan turns the counts into output offsets; the write
+// pass gathers the pairs at those offsets (ballot / popc ranks) -- deterministic
+// positions, no atomics on the output.  Units with several matches per probe row
+// (duplicate build keys) are re-probed against a (key, row)-sorted build chunk, so
+// their output is deterministic too.
 #include <cstdlib>
 
 #include "common.cuh"

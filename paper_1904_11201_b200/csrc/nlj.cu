@@ -4,8 +4,8 @@
 // join, which runs the same nested loop with a theta predicate.
 // The paper gives each thread NB_S x NB_T tuples (Eq.1-4) and a
 // private Cartesian-size result slot.  B200 design (DESIGN.md
-// §4.4): a CTA owns an R tile of 2048 keys held in registers (8 per thread) and
-// streams a range of S through a 4-stage shared-memory ring filled by 1-D TMA bulk
+// §4.4): a CTA of 128 threads owns an R tile of 1024 keys held in registers (8 per
+// thread) and streams a range of S through a 4-stage shared-memory ring filled by 1-D TMA bulk
 // copies (cp.async.bulk + mbarrier complete_tx).  Each S key is read from shared
 // memory once per 4 keys (LDS.128 broadcast) and compared against the 8 register
 // keys with the carry-chain trick: `sub.cc` + `addc` compile to IADD3 (carry-out

@@ -717,19 +717,23 @@ __global__ void __launch_bounds__(HT) hj_write_kernel(HJArgs a, const uint8_t* _
 // unit is written.  Warp w writes the probe rows of its count-pass range (the key
 // vectors [w*vpw, (w+1)*vpw)) at its scanned offset, one row per lane per step; a
 // row has at most one match here, so the ranks are a ballot + popc.
+// Windows hold the first WCAP rows of a unit (rows beyond are read from global
+// memory): 2 x 51 KB per CTA, so 4 CTAs (32 warps) fit an SM; the planner's units
+// are ~2048 rows.
+constexpr uint32_t WCAP = 2560;
 struct WBuf {
-  uint32_t br[BCH_MAX + 4];
-  uint32_t pr[PCH_MAX + 4];
-  uint16_t st[PCH_MAX + 8];
+  uint32_t br[WCAP + 4];
+  uint32_t pr[WCAP + 4];
+  uint16_t st[WCAP + 8];
 };
 static_assert(sizeof(WBuf) % 16 == 0, "16-byte aligned buffers");
 
 __device__ __forceinline__ void wf_issue(WBuf& B, uint64_t* bar, const uint4 d, const HJArgs& a,
                                          const uint16_t* stage) {
   fence_proxy_async();  // generic reads of this buffer (previous unit) before the async writes
-  const Win wb = a.brid ? bulk_window(a.brid, d.x, d.y, 4, a.nb) : Win{nullptr, 0, 0, 0};
-  const Win wp = a.prid ? bulk_window(a.prid, d.z, d.w, 4, a.np) : Win{nullptr, 0, 0, 0};
-  const Win ws = bulk_window(stage, d.z, d.w, 2, a.np);
+  const Win wb = a.brid ? bulk_window(a.brid, d.x, min(d.y, WCAP), 4, a.nb) : Win{nullptr, 0, 0, 0};
+  const Win wp = a.prid ? bulk_window(a.prid, d.z, min(d.w, WCAP), 4, a.np) : Win{nullptr, 0, 0, 0};
+  const Win ws = bulk_window(stage, d.z, min(d.w, WCAP), 2, a.np);
   const uint32_t bytes = wb.bytes + wp.bytes + ws.bytes;
   if (!bytes) {
     mbar_arrive(bar);
@@ -766,9 +770,9 @@ __global__ void __launch_bounds__(HT) hj_write_fast(HJArgs a, const uint16_t* __
     const bool full = multi[u] != 0;
     mbar_wait(bar + b, (it >> 1) & 1);
     if (!full) {
-      const Win wb = a.brid ? bulk_window(a.brid, d.x, d.y, 4, a.nb) : Win{nullptr, 0, 0, 0};
-      const Win wp = a.prid ? bulk_window(a.prid, d.z, d.w, 4, a.np) : Win{nullptr, 0, 0, 0};
-      const Win ws = bulk_window(stage, d.z, d.w, 2, a.np);
+      const Win wb = a.brid ? bulk_window(a.brid, d.x, min(d.y, WCAP), 4, a.nb) : Win{nullptr, 0, 0, 0};
+      const Win wp = a.prid ? bulk_window(a.prid, d.z, min(d.w, WCAP), 4, a.np) : Win{nullptr, 0, 0, 0};
+      const Win ws = bulk_window(stage, d.z, min(d.w, WCAP), 2, a.np);
       const WBuf& Bb = B[b];
       // this warp's rows: those of its count-pass key vectors
       const Span sp = span16(a.pkey, d.z, d.w, sizeof(K));

@@ -122,6 +122,61 @@ __global__ void __launch_bounds__(PT, sizeof(K) == 4 ? 4 : 3) part_hist(const K*
   const uint32_t w = threadIdx.x >> 5, lane = lane_id();
   const uint32_t len = (uint32_t)(L.end - L.beg);
   const uint32_t ntiles = (len + TILE - 1) / TILE;
+  if (sizeof(K) == 4) {
+    // int32: each thread reads its part of a tile as 16-byte vectors (absolute-address
+    // windows: the chunk may start anywhere); the counting order does not matter
+    constexpr uint32_t VPT = TILE / 4 / PT;  // full vectors per thread per tile
+    auto tile_span = [&](uint32_t t) {
+      const uint64_t b0 = (L.beg + (uint64_t)t * TILE) * 4;
+      const uint32_t cnt = min(len - t * TILE, (uint32_t)TILE);
+      const uint64_t a0 = (reinterpret_cast<uint64_t>(key) + b0) & ~15ull;
+      return make_uint2((uint32_t)((reinterpret_cast<uint64_t>(key) + b0 - a0) / 4), cnt);  // (shift, cnt)
+    };
+    auto vec_ptr = [&](uint32_t t) {
+      return reinterpret_cast<const uint4*>((reinterpret_cast<uint64_t>(key) + (L.beg + (uint64_t)t * TILE) * 4) &
+                                            ~15ull);
+    };
+    uint4 v[VPT], vn[VPT];
+    {
+      const uint2 sc = tile_span(0);
+      const uint32_t nv = (sc.x + sc.y + 3) / 4;
+      const uint4* p = vec_ptr(0);
+#pragma unroll
+      for (uint32_t i = 0; i < VPT; ++i) v[i] = threadIdx.x + i * PT < nv ? __ldg(p + threadIdx.x + i * PT) : uint4{};
+    }
+    __syncthreads();
+    for (uint32_t t = 0; t < ntiles; ++t) {
+      const uint2 sc = tile_span(t);
+      const uint32_t nv = (sc.x + sc.y + 3) / 4;
+      if (t + 1 < ntiles) {
+        const uint2 sn = tile_span(t + 1);
+        const uint32_t nvn = (sn.x + sn.y + 3) / 4;
+        const uint4* p = vec_ptr(t + 1);
+#pragma unroll
+        for (uint32_t i = 0; i < VPT; ++i)
+          vn[i] = threadIdx.x + i * PT < nvn ? __ldg(p + threadIdx.x + i * PT) : uint4{};
+      }
+      uint32_t* row = tile_pref + ((uint64_t)c * TPC + t) * D;
+      for (uint32_t d = threadIdx.x; d < D; d += PT) row[d] = h[d];
+      __syncthreads();
+      auto count4 = [&](const uint4 x, uint32_t vi) {
+        const uint32_t j0 = vi * 4 - sc.x;  // wraps below the tile
+        const int32_t kk[4] = {(int32_t)x.x, (int32_t)x.y, (int32_t)x.z, (int32_t)x.w};
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q)
+          atomicAdd(&h[j0 + q < sc.y ? digit_of<RANGE>((K)kk[q], shift, mask, fn) : D], 1u);
+      };
+#pragma unroll
+      for (uint32_t i = 0; i < VPT; ++i) count4(v[i], threadIdx.x + i * PT);  // padding vectors hit bin D
+      for (uint32_t vi = threadIdx.x + VPT * PT; vi < nv; vi += PT) count4(__ldg(vec_ptr(t) + vi), vi);
+      __syncthreads();
+#pragma unroll
+      for (uint32_t i = 0; i < VPT; ++i) v[i] = vn[i];
+    }
+    uint32_t* out = hist + (uint64_t)L.cb * D + (c - L.cb);
+    for (uint32_t d = threadIdx.x; d < D; d += PT) out[(uint64_t)d * L.nc] = h[d];
+    return;
+  }
   K k[PI], kn[PI];
   uint32_t r0[1];
   load_tile<K, false>(key, nullptr, L.beg, min(len, (uint32_t)TILE), w, lane, k, r0);

@@ -39,7 +39,7 @@ int main() {
   }
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  for (int npeers = 1; npeers < G; npeers *= 2) {
+  for (int npeers = 1; npeers < G; ++npeers) {
     std::vector<cudaEvent_t> e0(G), e1(G);
     for (int rep = 0; rep < 2; ++rep) {
       for (int s = 0; s < G; ++s) {

@@ -122,7 +122,11 @@ const char* gj_last_error(void);
  *                          joins R block i (the R shards of grid row i) with S block
  *                          j (the S shards of grid column j).  r = 1 is the R
  *                          broadcast; 0 (default) = the divisor of G minimising
- *                          |R|/r + |S|/c.  Must be equal on every rank. */
+ *                          |R|/r + |S|/c.  Must be equal on every rank.
+ *  GJ_OPT_SHUFFLE_CTAS     multi-GPU equi join: CTAs of the S shuffle scatter, which runs
+ *                          on a second stream beside R's local radix passes (0 = the
+ *                          default, half the GPU's resident CTAs: the NVLink-bound
+ *                          shuffle leaves SMs to the local passes; -1 = all). */
 enum {
   GJ_OPT_PART_BITS = 1,
   GJ_OPT_BUILD_CHUNK = 2,
@@ -133,7 +137,8 @@ enum {
   GJ_OPT_BUILD_SIDE = 7,
   GJ_OPT_SHUFFLE_BITS = 8,
   GJ_OPT_THETA_REGIONS = 9,
-  GJ_OPT_THETA_GRID_ROWS = 10
+  GJ_OPT_THETA_GRID_ROWS = 10,
+  GJ_OPT_SHUFFLE_CTAS = 11
 };
 gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t value);
 

@@ -277,7 +277,12 @@ void fused_shuffle(gj_ctx* ctx, gj_comm* c, const gj_rel* const X[2], uint32_t b
     }
     dst.adj = dtab;
     dst.lbits = b1;
+    // beside R's local passes the NVLink-bound S scatter gets a share of the SMs
+    ctx->shuffle_grid_cap = (overlap && rel == 1 && ctx->shuffle_ctas >= 0)
+                                ? (ctx->shuffle_ctas ? ctx->shuffle_ctas : ctx->num_sms)
+                                : 0;
     shuffle_scatter(ctx, *X[rel], SP[rel], dst);
+    ctx->shuffle_grid_cap = 0;
     out.X[rel] = gj_rel{bufs[2 * rel], static_cast<const uint32_t*>(bufs[2 * rel + 1]), need[me][rel], kt, 0};
     out.seg[rel] = dtab + D1;
   }

@@ -560,7 +560,8 @@ void launch_scatter_t(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t r
   set_smem(ctx, kern, ScatterLayout<K>::bytes(1u << MAX_BITS));
   int occ = 1;
   GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PT, smem));
-  const uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
+  uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
+  if (REMOTE && ctx->shuffle_grid_cap > 0) grid = std::min<uint32_t>(grid, (uint32_t)ctx->shuffle_grid_cap);
   launch(ctx, REMOTE ? "shuffle_scatter" : "part_scatter", kern, dim3(grid), dim3(PT), smem, kin, rin, rid_base, n,
          tdesc, (uint32_t)ntiles, shift, bits, tile_base, kout, rout, ctr, fn, dst);
 }

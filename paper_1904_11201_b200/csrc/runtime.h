@@ -114,6 +114,8 @@ struct gj_ctx {
   uint32_t nlj_split = 0;
   bool force_slow_band = false;
   bool overlap_shuffle = true;   // multi-GPU equi: S shuffle on a 2nd stream beside R's local passes
+  int shuffle_ctas = 0;          // CTAs of that S shuffle scatter (0 = half the resident CTAs, -1 = all)
+  int shuffle_grid_cap = 0;      // set by the dist code for the launch in flight (0 = no cap)
   int theta_regions = 1;         // theta joins through the region matrix (0 = plain NLJ over all pairs)
   uint32_t theta_grid_rows = 0;  // multi-GPU theta: rows r of the 1-Bucket grid (0 = auto; 1 = R broadcast)
   int build_side = 0;

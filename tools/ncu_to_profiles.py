@@ -27,7 +27,7 @@ PROF = os.path.join(ROOT, "profiles")
 
 # kernel symbol -> bench.py tag (the LaunchScope tags of the library)
 TAGS = [
-    (r"part_scatter<\w+, \w+, (true|1),", "shuffle_scatter"),
+    (r"part_scatter<\w+, \w+, \w+, (true|1)>", "shuffle_scatter"),
     (r"part_scatter", "part_scatter"),
     (r"part_hist", "part_hist"),
     (r"tile_base", "tile_base"),
@@ -141,9 +141,19 @@ def main():
             rb = to_bytes(*d["dram__bytes_read.sum"]) if "dram__bytes_read.sum" in d else None
             wb = to_bytes(*d["dram__bytes_write.sum"]) if "dram__bytes_write.sum" in d else None
             if t and rb is not None and wb is not None:
-                acc[t].append(rb + wb)
-        traffic[wl] = {t: {"dram_bytes_per_launch": sum(v) / len(v), "launches_captured": len(v),
-                           "report": os.path.basename(rep)} for t, v in acc.items()}
+                # per template instantiation, so e.g. the scatter's pass-1 (no rid input)
+                # and pass-2 launches weigh equally whatever the capture caught
+                inst = re.sub(r"[(].*", "", d["kernel"])
+                acc[t].append((inst, rb + wb))
+        traffic[wl] = {}
+        for t, v in acc.items():
+            per = defaultdict(list)
+            for inst, b in v:
+                per[inst].append(b)
+            means = [sum(x) / len(x) for x in per.values()]
+            traffic[wl][t] = {"dram_bytes_per_launch": sum(means) / len(means), "launches_captured": len(v),
+                              "instantiations": {k: sum(x) / len(x) for k, x in per.items()},
+                              "report": os.path.basename(rep)}
         json.dump(traffic, open(tj, "w"), indent=1, sort_keys=True)
     with open(os.path.join(PROF, f"{rnd}_ncu_{wl}.md"), "w") as f:
         f.write("\n".join(md) + "\n")

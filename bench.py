@@ -437,10 +437,14 @@ def run_ours(args, world, rank, local):
             tup = (nR + nS) / 2  # per launch (one relation per launch; R and S are equal-sized here)
             wire = tup * (world - 1) / world * (w["R"].element_size() + 4)
             pk, psrc = nvlink_peak(world)
-            roof["nvlink"] = {"kernel": "shuffle_scatter", "bound": "nvlink", "achieved": round(
+            nv = {"kernel": "shuffle_scatter", "bound": "nvlink", "achieved": round(
                 wire / (k["ms_per_launch"] * 1e-3) / 1e9, 1), "peak": pk, "unit": "GB/s",
                 "frac": round(wire / (k["ms_per_launch"] * 1e-3) / 1e9 / pk, 4) if pk else None,
-                "bytes_per_launch": wire, "peak_source": psrc}
+                "traffic": None, "alg_bytes_per_launch": wire, "peak_source": psrc}
+            if dom == "shuffle_scatter":  # the dominant kernel is NVLink-bound: that is its roofline
+                roof = nv | {"hbm_view": roof}
+            else:
+                roof["nvlink"] = nv
     else:
         # The NLJ compares the pairs of the cells the region matrix keeps (all n_R x n_S
         # with theta_regions=0): INT ALU roofline, 1.5 ALU-pipe instr per pair-compare

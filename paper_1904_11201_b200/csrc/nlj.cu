@@ -33,7 +33,6 @@ constexpr int KR = 8;              // R keys per thread (registers)
 constexpr int RT = NT * KR;        // R tile = 1024 keys
 constexpr int TS = 2048;           // S keys per pipeline stage
 constexpr int STG = 4;             // pipeline depth
-constexpr uint32_t PB = 512;       // staged pairs per warp (dense write path)
 
 enum Fam { F_GE = 0, F_LE = 1, F_NE = 2, F_BAND = 3, F_GENERIC = 4 };
 
@@ -241,7 +240,6 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
     uint32_t rf[KR], rr[KR];
     uint32_t nvalid = 0;
     __shared__ uint32_t rrs[WRITE ? KR * NT : 1];  // rids of the register keys (dense write path)
-    __shared__ __align__(16) uint2 pbuf[WRITE ? NWARP * PB : 1];  // per-warp pair staging (dense write path)
 #pragma unroll
     for (int i = 0; i < KR; ++i) {
       const uint64_t row = r0 + (uint64_t)i * NT + tid;
@@ -274,18 +272,6 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
 
     uint64_t tot = 0;
     uint64_t wbase = WRITE ? a.woff[(uint64_t)u * NWARP + w] : 0;
-    // dense write path: the warp's pairs are staged in shared memory and copied out
-    // with consecutive lanes on consecutive pairs (one coalesced store per 32 pairs
-    // instead of scattered 8-byte stores per lane)
-    uint2* pb = pbuf + (WRITE ? w * PB : 0);
-    uint32_t fill = 0;
-    auto flush = [&]() {
-      __syncwarp();
-      for (uint32_t x = lane; x < fill; x += 32) a.out[wbase + x] = pb[x];
-      wbase += fill;
-      fill = 0;
-      __syncwarp();
-    };
     auto srow = [&](uint64_t idx) -> uint32_t {
       return a.srid ? a.srid[idx] : a.srid_base + (uint32_t)idx;
     };
@@ -353,11 +339,8 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
               for (int i = 0; i < KR; ++i) mask_step<FAM>(mm, rf[i], sv[k], a.C);
             if (!direct(OP)) mm = ~mm;
             const uint32_t c = __popc(mm), incl = warp_incl_scan(c);
-            const uint32_t gtot = __shfl_sync(FULL, incl, 31);
-            if (fill + gtot > PB) flush();  // warp-uniform
-            const bool staged = gtot <= PB;
             if (mm) {
-              uint2* o = staged ? pb + fill + (incl - c) : a.out + wbase + (incl - c);
+              uint2* o = a.out + wbase + (incl - c);
               uint32_t sr[4];  // the group's S rids, loaded once (broadcast across lanes)
 #pragma unroll
               for (int k = 0; k < 4; ++k) sr[k] = srow(tb + 4 * q + k);
@@ -373,10 +356,8 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
                 }
               }
             }
-            if (staged) fill += gtot;
-            else wbase += gtot;
+            wbase += __shfl_sync(FULL, incl, 31);
           }
-          if (a.dense) flush();
           // Sparse matches: screen 4 S keys (one LDS.128) with the count pass's
           // carry-chain counters and one warp vote; only groups holding a match build masks.
 #pragma unroll 2

@@ -126,7 +126,12 @@ const char* gj_last_error(void);
  *  GJ_OPT_SHUFFLE_CTAS     multi-GPU equi join: CTAs of the S shuffle scatter, which runs
  *                          on a second stream beside R's local radix passes (0 = the
  *                          default, half the GPU's resident CTAs: the NVLink-bound
- *                          shuffle leaves SMs to the local passes; -1 = all). */
+ *                          shuffle leaves SMs to the local passes; -1 = all).
+ *  GJ_OPT_CHECK_ARGS       1 = every collective call first all-reduces (min and max) a
+ *                          hash of its arguments and options (op, eps, flags, key type,
+ *                          bloom bits, radix / shuffle / grid options); if the ranks
+ *                          disagree, every rank returns GJ_EINVAL (SURVEY §8(b)'s debug
+ *                          check; one tiny NCCL all-reduce and a sync per call). */
 enum {
   GJ_OPT_PART_BITS = 1,
   GJ_OPT_BUILD_CHUNK = 2,
@@ -138,7 +143,8 @@ enum {
   GJ_OPT_SHUFFLE_BITS = 8,
   GJ_OPT_THETA_REGIONS = 9,
   GJ_OPT_THETA_GRID_ROWS = 10,
-  GJ_OPT_SHUFFLE_CTAS = 11
+  GJ_OPT_SHUFFLE_CTAS = 11,
+  GJ_OPT_CHECK_ARGS = 12
 };
 gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t value);
 

@@ -371,6 +371,7 @@ gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t v) {
       if (v < 0 || v > 64) throw Error(GJ_EINVAL, "theta_grid_rows must be in [0, 64]");
       ctx->theta_grid_rows = (uint32_t)v;
       break;
+    case GJ_OPT_CHECK_ARGS: ctx->check_args = v != 0; break;
     case GJ_OPT_SHUFFLE_CTAS:
       if (v < -1 || v > 1 << 20) throw Error(GJ_EINVAL, "shuffle_ctas must be -1, 0 or a CTA count");
       ctx->shuffle_ctas = (int)v;

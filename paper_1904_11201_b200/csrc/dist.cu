@@ -422,6 +422,37 @@ void equi_count_any(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S) {
   else dist_equi_count_fused(ctx, c, R, S);
 }
 
+// GJ_OPT_CHECK_ARGS: all ranks must pass the same arguments to a collective call; a
+// mismatch (e.g. a different eps on one rank) would otherwise deadlock or silently
+// produce a wrong union.  Min and max of an argument hash are all-reduced; every rank
+// sees the same verdict.
+void check_collective(gj_ctx* ctx, gj_comm* c, int call, int key_type, int op, uint64_t eps, uint32_t flags,
+                      double bpk) {
+  if (!ctx->check_args || c->nranks == 1) return;
+  uint64_t h = 0x9E3779B97F4A7C15ull;
+  auto mix = [&](uint64_t v) {
+    h ^= v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+    h *= 0xff51afd7ed558ccdull;
+  };
+  uint64_t bb;
+  static_assert(sizeof(bb) == sizeof(bpk), "");
+  std::memcpy(&bb, &bpk, 8);
+  for (uint64_t v : {(uint64_t)call, (uint64_t)key_type, (uint64_t)op, eps, (uint64_t)flags, bb,
+                     (uint64_t)(int64_t)ctx->part_bits, (uint64_t)ctx->shuffle_bits, (uint64_t)ctx->theta_grid_rows,
+                     (uint64_t)ctx->theta_regions})
+    mix(v);
+  unsigned long long* d = static_cast<unsigned long long*>(ws(ctx, "dist.argcheck", 32));
+  const unsigned long long hv[2] = {h, h};
+  GJ_CUDA(cudaMemcpyAsync(d, hv, 16, cudaMemcpyHostToDevice, ctx->stream));
+  GJ_NCCL(ncclGroupStart());
+  GJ_NCCL(ncclAllReduce(d, d + 2, 1, ncclUint64, ncclMin, c->comm, ctx->stream));
+  GJ_NCCL(ncclAllReduce(d + 1, d + 3, 1, ncclUint64, ncclMax, c->comm, ctx->stream));
+  GJ_NCCL(ncclGroupEnd());
+  unsigned long long r[2];
+  d2h_sync(ctx, r, d + 2, 16);
+  if (r[0] != r[1]) throw Error(GJ_EINVAL, "collective call: the ranks disagree on its arguments / options");
+}
+
 // Standalone sharded pre-filter (SURVEY §8(b) prefilter_dist; §3.1,
 // Alg.1: filter BOTH tables before the join).  Every rank keeps its own shards' rows
 // (no shuffle), compacted to the survivors, exactly as prefilter() would on the union
@@ -740,6 +771,7 @@ gj_status join_dist_count(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, uint64_t*
   DAPI_BEGIN
   check_args(ctx, c, R, S);
   if (!n_local || !n_global) throw Error(GJ_EINVAL, "NULL result pointer");
+  check_collective(ctx, c, 1, R.key_type, GJ_EQ, 0, 0, 0.0);
   c->eq_valid = false;
   trace_mark("join_dist_count begin");
   equi_count_any(ctx, c, R, S);
@@ -764,6 +796,7 @@ gj_status join_dist_count_filtered(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, 
   if (flags & ~(uint32_t)(GJ_PF_RANGE | GJ_PF_BLOOM | GJ_PF_TWO_SIDED)) throw Error(GJ_EINVAL, "unknown prefilter flag");
   if ((flags & GJ_PF_BLOOM) && !(bloom_bits_per_key >= 1.0 && bloom_bits_per_key <= 64.0))
     throw Error(GJ_EINVAL, "bloom_bits_per_key must be in [1, 64]");
+  check_collective(ctx, c, 2, R.key_type, GJ_EQ, 0, flags, bloom_bits_per_key);
   c->eq_valid = false;
   uint64_t kept[2] = {0, 0};
   dist_equi_count_filtered(ctx, c, R, S, flags, bloom_bits_per_key, kept);
@@ -795,6 +828,7 @@ gj_status prefilter_dist(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, uint32_t f
     throw Error(GJ_EINVAL, "prefilter_dist: NULL output buffer");
   if ((flags & GJ_PF_BLOOM) && !(bloom_bits_per_key >= 1.0 && bloom_bits_per_key <= 64.0))
     throw Error(GJ_EINVAL, "prefilter_dist: bloom_bits_per_key must be in [1, 64]");
+  check_collective(ctx, c, 3, R.key_type, op, eps, flags, bloom_bits_per_key);
   dist_prefilter(ctx, c, R, S, flags, op, eps, bloom_bits_per_key, key_out_R, rid_out_R, n_R_out, key_out_S,
                  rid_out_S, n_S_out);
   DAPI_END
@@ -831,6 +865,7 @@ gj_status theta_join_dist_count(gj_ctx* ctx, gj_comm* c, gj_rel R, gj_rel S, int
   check_args(ctx, c, R, S);
   if (op < GJ_EQ || op > GJ_BAND) throw Error(GJ_EINVAL, "unknown op");
   if (!n_local || !n_global) throw Error(GJ_EINVAL, "NULL result pointer");
+  check_collective(ctx, c, 4, R.key_type, op, eps, 0, 0.0);
   c->th_valid = false;
   dist_theta_count(ctx, c, R, S, op, eps);
   c->R = R;

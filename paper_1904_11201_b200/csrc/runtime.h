@@ -114,6 +114,7 @@ struct gj_ctx {
   uint32_t nlj_split = 0;
   bool force_slow_band = false;
   bool overlap_shuffle = true;   // multi-GPU equi: S shuffle on a 2nd stream beside R's local passes
+  bool check_args = false;       // collective calls verify the ranks agree on their arguments
   int shuffle_ctas = 0;          // CTAs of that S shuffle scatter (0 = half the resident CTAs, -1 = all)
   int shuffle_grid_cap = 0;      // set by the dist code for the launch in flight (0 = no cap)
   int theta_regions = 1;         // theta joins through the region matrix (0 = plain NLJ over all pairs)

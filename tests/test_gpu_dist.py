@@ -145,6 +145,16 @@ def _worker(rank, world, port, q):
             out[f"ge_grid{rows}"] = (nl, ng, gj.theta_join_dist_materialize(ctx, comm, R6, S6, "ge", 0, nl)
                                      .cpu().numpy().view(np.uint32))
         ctx.set_option("theta_grid_rows", 0)
+        # GJ_OPT_CHECK_ARGS: a rank passing a different eps makes EVERY rank fail with
+        # GJ_EINVAL (instead of a silently wrong union); equal arguments pass
+        ctx.set_option("check_args", 1)
+        nl, ng = gj.theta_join_dist_count(ctx, comm, R3, S3, "band", 40)
+        try:
+            gj.theta_join_dist_count(ctx, comm, R3, S3, "band", 40 + rank)
+            out["argcheck"] = "no error"
+        except gj.GJError as e:
+            out["argcheck"] = e.status
+        ctx.set_option("check_args", 0)
         q.put((rank, out))
         comm.close()
         ctx.close()
@@ -211,6 +221,7 @@ def test_dist_joins_match_oracle(world):
             assert kept_S < members + 0.08 * len(S5all), (flags, kept_S)
         if flags & gj.TWO_SIDED:
             assert kept_R < len(R5all), flags
+    assert all(res[r]["argcheck"] == 1 for r in range(world)), [res[r]["argcheck"] for r in range(world)]
     # prefilter_dist: each rank's survivors are its own rows, in order, with their keys;
     # no false negatives (the exact semi-joins survive); the union joins to J(R, S)
     semR = set(np.nonzero(oracle.semijoin_exact(R5all, S5all))[0].tolist())

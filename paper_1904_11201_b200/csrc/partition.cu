@@ -248,15 +248,14 @@ template <typename K, bool HAS_RID, bool RANGE, bool REMOTE>
 __global__ void __launch_bounds__(PT, SCATTER_MINB) part_scatter(
     const K* __restrict__ key_in, const uint32_t* __restrict__ rid_in, uint32_t rid_base, uint64_t n,
     const uint4* __restrict__ tdesc, uint32_t ntiles, uint32_t shift, uint32_t bits,
-    const uint32_t* __restrict__ tile_base, K* __restrict__ key_out, uint32_t* __restrict__ rid_out,
-    uint32_t* __restrict__ tile_ctr, DigitFn fn, ShuffleDest dst) {
+    const uint32_t* __restrict__ tile_base, const uint32_t* __restrict__ tile_st, K* __restrict__ key_out,
+    uint32_t* __restrict__ rid_out, uint32_t* __restrict__ tile_ctr, DigitFn fn, ShuffleDest dst) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using L = ScatterLayout<K>;
   constexpr bool ILV = sizeof(K) == 4 && !REMOTE;  // int32 local: one (key, rid) uint2 per staging slot
   const uint32_t D = 1u << bits, mask = D - 1;
   const uint32_t W = L::words(D);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + L::off_bar);
-  uint32_t* wt = reinterpret_cast<uint32_t*>(smem_raw + L::off_wt);
   uint32_t* whist = reinterpret_cast<uint32_t*>(smem_raw + L::off_whist);
   uint32_t* delta = whist + NW * W;
   uint32_t* tstart = reinterpret_cast<uint32_t*>(smem_raw + L::off_run);  // bulk: tile-local run starts
@@ -315,9 +314,16 @@ __global__ void __launch_bounds__(PT, SCATTER_MINB) part_scatter(
     }
     const uint4 d = tdesc[t];
     uint32_t g0a = 0, g0b = 0;  // global run starts of my two digits in this tile
+    uint32_t sta = 0, stb = 0;  // their tile-local starts (tile_base_kernel's per-tile digit scan)
     if (d.y) {
-      if (ha) g0a = tile_base[(uint64_t)t * D + da] + (REMOTE ? dst.adj[da] : 0u);
-      if (hb) g0b = tile_base[(uint64_t)t * D + db] + (REMOTE ? dst.adj[db] : 0u);
+      if (ha) {
+        g0a = tile_base[(uint64_t)t * D + da] + (REMOTE ? dst.adj[da] : 0u);
+        sta = tile_st[(uint64_t)t * D + da];
+      }
+      if (hb) {
+        g0b = tile_base[(uint64_t)t * D + db] + (REMOTE ? dst.adj[db] : 0u);
+        stb = tile_st[(uint64_t)t * D + db];
+      }
     }
     const uint32_t cnt = d.y;
     if (cnt == 0) {  // CTA-uniform
@@ -367,52 +373,28 @@ __global__ void __launch_bounds__(PT, SCATTER_MINB) part_scatter(
     for (int i = 0; i < PI; ++i)
       rr[i] = HAS_RID ? rbuf[ro + (w * PI + i) * 32 + lane] : rid_base + d.x + (w * PI + i) * 32 + lane;
     __syncthreads();  // inputs are in registers: the buffer becomes the staging area
-    {  // tile-local digit starts: thread i owns digits i and i + H -- exclusive column
-       // prefix over the warps, warp scans of both halves' totals, then every warp adds
-       // the totals of the warps before it (and the low half's total for the high half)
-      uint32_t ta = 0, tb = 0;
+    {  // staging positions: thread i owns digits i and i + H -- the warps' exclusive
+       // column prefix on top of the digit's tile-local start (precomputed per tile by
+       // tile_base_kernel, so no cross-warp scan and no extra barrier here)
       if (ha) {
+        uint32_t ra = sta, rb = stb;
 #pragma unroll
         for (int ww = 0; ww < NW; ++ww) {
           uint32_t* c = whist + ww * W + da;
           const uint32_t x = c[0];
-          c[0] = ta;
-          ta += x;
+          c[0] = ra;
+          ra += x;
           if (hb) {
             const uint32_t y = c[H];
-            c[H] = tb;
-            tb += y;
+            c[H] = rb;
+            rb += y;
           }
         }
-      }
-      const uint32_t ia = warp_incl_scan(ta), ib = warp_incl_scan(tb);
-      if (lane == 31) {
-        wt[w] = ia;
-        wt[NW + w] = ib;
-      }
-      __syncthreads();
-      uint32_t st_a = ia - ta, st_b = ib - tb, low = 0;
-#pragma unroll
-      for (int ww = 0; ww < NW; ++ww) {
-        const uint32_t xa = wt[ww], xb = wt[NW + ww];
-        low += xa;
-        if ((uint32_t)ww < w) {
-          st_a += xa;
-          st_b += xb;
-        }
-      }
-      st_b += low;
-      if (ha) {
-        delta[da] = g0a - st_a;
-        if (hb) delta[db] = g0b - st_b;
+        delta[da] = g0a - sta;
+        if (hb) delta[db] = g0b - stb;
         if (bulk) {
-          tstart[da] = st_a;
-          if (hb) tstart[db] = st_b;
-        }
-#pragma unroll
-        for (int ww = 0; ww < NW; ++ww) {
-          whist[ww * W + da] += st_a;
-          if (hb) whist[ww * W + db] += st_b;
+          tstart[da] = sta;
+          if (hb) tstart[db] = stb;
         }
       }
     }
@@ -529,10 +511,13 @@ __global__ void __launch_bounds__(PT, SCATTER_MINB) part_scatter(
 // the scanned matrix is strided by the chunk count: reading it per tile cost one
 // DRAM sector per digit), writes the chunk's tile descriptors (tile begin, tile
 // length; length 0 = empty) and resets the scatter's tile counter.
-__global__ void tile_base_kernel(uint64_t n, const uint32_t* __restrict__ seg_off,
-                                 const uint32_t* __restrict__ chunk_base, uint32_t nseg, uint32_t bits,
-                                 const uint32_t* __restrict__ scanned, uint32_t* __restrict__ tile_pref,
-                                 uint4* __restrict__ tdesc, uint32_t* __restrict__ tile_ctr) {
+__global__ void __launch_bounds__(PT) tile_base_kernel(uint64_t n, const uint32_t* __restrict__ seg_off,
+                                                       const uint32_t* __restrict__ chunk_base, uint32_t nseg,
+                                                       uint32_t bits, const uint32_t* __restrict__ scanned,
+                                                       uint32_t* __restrict__ tile_pref, uint32_t* __restrict__ tile_st,
+                                                       uint4* __restrict__ tdesc, uint32_t* __restrict__ tile_ctr) {
+  __shared__ uint32_t cnt_s[1 << MAX_BITS];
+  __shared__ uint32_t wsum[PT / 32];
   const uint32_t c = blockIdx.x, D = 1u << bits;
   if (c == 0 && threadIdx.x == 0) *tile_ctr = 0;
   const ChunkLoc L = locate(c, n, seg_off, chunk_base, nseg);
@@ -545,16 +530,40 @@ __global__ void tile_base_kernel(uint64_t n, const uint32_t* __restrict__ seg_of
   }
   if (c >= L.total) return;
   const uint32_t nt = (len + TILE - 1) / TILE;
-  for (uint32_t d = threadIdx.x; d < D; d += blockDim.x) {
-    const uint32_t base = scanned[(uint64_t)L.cb * D + (uint64_t)d * L.nc + (c - L.cb)];
-    for (uint32_t t = 0; t < nt; ++t) tile_pref[((uint64_t)c * TPC + t) * D + d] += base;
+  for (uint32_t t = 0; t < nt; ++t) {
+    uint32_t* row = tile_pref + ((uint64_t)c * TPC + t) * D;
+    for (uint32_t d = threadIdx.x; d < D; d += PT) {
+      const uint64_t idx = (uint64_t)L.cb * D + (uint64_t)d * L.nc + (c - L.cb);
+      const uint32_t base = scanned[idx], pre = row[d];
+      // digit d's count in tile t: the next tile's in-chunk prefix (still unmodified),
+      // or the chunk's total for the last tile (consecutive entries of the scanned
+      // (segment, digit, chunk) matrix; the scan also wrote the grand total at the end)
+      const uint32_t next = t + 1 < nt ? row[D + d] : scanned[idx + 1] - base;
+      cnt_s[d] = next - pre;
+      row[d] = base + pre;
+    }
+    __syncthreads();
+    // tile-local digit starts: exclusive scan of the tile's D digit counts (each thread
+    // two consecutive digits)
+    const uint32_t d0 = 2 * threadIdx.x;
+    const uint32_t x0 = d0 < D ? cnt_s[d0] : 0u, x1 = d0 + 1 < D ? cnt_s[d0 + 1] : 0u;
+    const uint32_t inc = warp_incl_scan(x0 + x1);
+    if (lane_id() == 31) wsum[threadIdx.x >> 5] = inc;
+    __syncthreads();
+    uint32_t ex = inc - (x0 + x1);
+    for (uint32_t ww = 0; ww < (threadIdx.x >> 5); ++ww) ex += wsum[ww];
+    uint32_t* st = tile_st + ((uint64_t)c * TPC + t) * D;
+    if (d0 < D) st[d0] = ex;
+    if (d0 + 1 < D) st[d0 + 1] = ex + x0;
+    __syncthreads();
   }
 }
 
 template <typename K, bool HAS_RID, bool RANGE, bool REMOTE>
 void launch_scatter_t(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
                       const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* tile_base,
-                      uint32_t* ctr, K* kout, uint32_t* rout, const DigitFn& fn, const ShuffleDest& dst) {
+                      const uint32_t* tile_st, uint32_t* ctr, K* kout, uint32_t* rout, const DigitFn& fn,
+                      const ShuffleDest& dst) {
   auto kern = part_scatter<K, HAS_RID, RANGE, REMOTE>;
   const size_t smem = ScatterLayout<K>::bytes(1u << bits);
   set_smem(ctx, kern, ScatterLayout<K>::bytes(1u << MAX_BITS));
@@ -563,19 +572,20 @@ void launch_scatter_t(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t r
   uint32_t grid = (uint32_t)std::min<uint64_t>(ntiles, (uint64_t)ctx->num_sms * std::max(occ, 1));
   if (REMOTE && ctx->shuffle_grid_cap > 0) grid = std::min<uint32_t>(grid, (uint32_t)ctx->shuffle_grid_cap);
   launch(ctx, REMOTE ? "shuffle_scatter" : "part_scatter", kern, dim3(grid), dim3(PT), smem, kin, rin, rid_base, n,
-         tdesc, (uint32_t)ntiles, shift, bits, tile_base, kout, rout, ctr, fn, dst);
+         tdesc, (uint32_t)ntiles, shift, bits, tile_base, tile_st, kout, rout, ctr, fn, dst);
 }
 
 template <typename K, bool RANGE, bool REMOTE>
 void launch_scatter(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
                     const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* tile_base,
-                    uint32_t* ctr, K* kout, uint32_t* rout, const DigitFn& fn, const ShuffleDest& dst) {
+                    const uint32_t* tile_st, uint32_t* ctr, K* kout, uint32_t* rout, const DigitFn& fn,
+                    const ShuffleDest& dst) {
   if (rin)
-    launch_scatter_t<K, true, RANGE, REMOTE>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_base, ctr,
-                                             kout, rout, fn, dst);
+    launch_scatter_t<K, true, RANGE, REMOTE>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_base,
+                                             tile_st, ctr, kout, rout, fn, dst);
   else
-    launch_scatter_t<K, false, RANGE, REMOTE>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_base, ctr,
-                                              kout, rout, fn, dst);
+    launch_scatter_t<K, false, RANGE, REMOTE>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_base,
+                                              tile_st, ctr, kout, rout, fn, dst);
 }
 
 // chunk_base[s] = first chunk of segment s (exclusive scan of the segments' chunk
@@ -679,10 +689,11 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
     exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
     uint4* tdesc = static_cast<uint4*>(ws(ctx, "part.tdesc", (ntiles + 1) * sizeof(uint4)));
     uint32_t* ctr = static_cast<uint32_t*>(ws(ctx, "part.tile_ctr", sizeof(uint32_t)));
+    uint32_t* tile_st = static_cast<uint32_t*>(ws(ctx, "part.tile_st", ntiles * D * sizeof(uint32_t)));
     launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, seg_off,
-           (const uint32_t*)chunk_base, nseg, bits, (const uint32_t*)hist, tile_pref, tdesc, ctr);
-    launch_scatter<K, RANGE, false>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, tile_pref, ctr, kout,
-                                    rout, fn, ShuffleDest{});
+           (const uint32_t*)chunk_base, nseg, bits, (const uint32_t*)hist, tile_pref, tile_st, tdesc, ctr);
+    launch_scatter<K, RANGE, false>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, tile_pref, tile_st, ctr,
+                                    kout, rout, fn, ShuffleDest{});
     const uint32_t P = nseg << bits;
     uint32_t* off = static_cast<uint32_t*>(ws(ctx, (ps + ".off").c_str(), (P + 1) * sizeof(uint32_t)));
     launch(ctx, "extract_off", extract_off, dim3((P + 1 + 255) / 256), dim3(256), 0, (const uint32_t*)hist,
@@ -724,8 +735,9 @@ ShufflePass shuffle_prepare_impl(gj_ctx* ctx, const gj_rel& X, uint32_t g, const
   exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
   uint4* tdesc = static_cast<uint4*>(ws(ctx, (t + ".stdesc").c_str(), (sp.ntiles + 1) * sizeof(uint4)));
   uint32_t* ctr = static_cast<uint32_t*>(ws(ctx, (t + ".sctr").c_str(), sizeof(uint32_t)));
+  uint32_t* tile_st = static_cast<uint32_t*>(ws(ctx, (t + ".sst").c_str(), sp.ntiles * D * sizeof(uint32_t) + 4));
   launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, (const uint32_t*)nullptr,
-         (const uint32_t*)nullptr, 1u, g, (const uint32_t*)hist, tile_pref, tdesc, ctr);
+         (const uint32_t*)nullptr, 1u, g, (const uint32_t*)hist, tile_pref, tile_st, tdesc, ctr);
   uint32_t* off = static_cast<uint32_t*>(ws(ctx, (t + ".soff").c_str(), (D + 1) * sizeof(uint32_t)));
   launch(ctx, "extract_off", extract_off, dim3((D + 1 + 255) / 256), dim3(256), 0, (const uint32_t*)hist,
          (const uint32_t*)nullptr,
@@ -733,6 +745,7 @@ ShufflePass shuffle_prepare_impl(gj_ctx* ctx, const gj_rel& X, uint32_t g, const
   sp.hist = hist;
   sp.tile_pref = tile_pref;
   sp.tdesc = tdesc;
+  sp.tile_st = tile_st;
   sp.ctr = ctr;
   sp.off = off;
   return sp;
@@ -765,12 +778,12 @@ void shuffle_scatter(gj_ctx* ctx, const gj_rel& X, const ShufflePass& sp, const 
   if (X.n == 0) return;
   if (X.key_type == GJ_I32)
     launch_scatter<int32_t, false, true>(ctx, static_cast<const int32_t*>(X.key), X.rid, X.rid_base, X.n, sp.tdesc,
-                                         sp.ntiles, 32 - sp.g, sp.g, sp.tile_pref, sp.ctr, nullptr, nullptr, DigitFn{},
-                                         dst);
+                                         sp.ntiles, 32 - sp.g, sp.g, sp.tile_pref, sp.tile_st, sp.ctr, nullptr,
+                                         nullptr, DigitFn{}, dst);
   else
     launch_scatter<int64_t, false, true>(ctx, static_cast<const int64_t*>(X.key), X.rid, X.rid_base, X.n, sp.tdesc,
-                                         sp.ntiles, 32 - sp.g, sp.g, sp.tile_pref, sp.ctr, nullptr, nullptr, DigitFn{},
-                                         dst);
+                                         sp.ntiles, 32 - sp.g, sp.g, sp.tile_pref, sp.tile_st, sp.ctr, nullptr,
+                                         nullptr, DigitFn{}, dst);
 }
 
 }  // namespace gj

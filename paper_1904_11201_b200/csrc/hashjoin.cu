@@ -717,23 +717,27 @@ __global__ void __launch_bounds__(HT) hj_write_kernel(HJArgs a, const uint8_t* _
 // unit is written.  Warp w writes the probe rows of its count-pass range (the key
 // vectors [w*vpw, (w+1)*vpw)) at its scanned offset, one row per lane per step; a
 // row has at most one match here, so the ranks are a ballot + popc.
-// Windows hold the first WCAP rows of a unit (rows beyond are read from global
-// memory): 2 x 51 KB per CTA, so 4 CTAs (32 warps) fit an SM; the planner's units
-// are ~2048 rows.
-constexpr uint32_t WCAP = 2560;
+// Windows hold the first WCAP_B build / WP probe rows of a unit (rows beyond are read
+// from global memory).  Build chunks are ~2048 rows; probe chunks reach 4096 when the
+// probe side is larger (configs[2]: 4 probe rows per build row), so two window sizes:
+// WP = 2560 (2 x 51 KB per CTA, 4 CTAs = 32 warps per SM) when the partitions average
+// <= 2048 probe rows, else WP = 4096 (2 x 68 KB, 3 CTAs per SM).
+constexpr uint32_t WCAP_B = 2560;
+template <uint32_t WP>
 struct WBuf {
-  uint32_t br[WCAP + 4];
-  uint32_t pr[WCAP + 4];
-  uint16_t st[WCAP + 8];
+  uint32_t br[WCAP_B + 4];
+  uint32_t pr[WP + 4];
+  uint16_t st[WP + 8];
 };
-static_assert(sizeof(WBuf) % 16 == 0, "16-byte aligned buffers");
+static_assert(sizeof(WBuf<2560>) % 16 == 0 && sizeof(WBuf<PCH_MAX>) % 16 == 0, "16-byte aligned buffers");
 
-__device__ __forceinline__ void wf_issue(WBuf& B, uint64_t* bar, const uint4 d, const HJArgs& a,
+template <uint32_t WP>
+__device__ __forceinline__ void wf_issue(WBuf<WP>& B, uint64_t* bar, const uint4 d, const HJArgs& a,
                                          const uint16_t* stage) {
   fence_proxy_async();  // generic reads of this buffer (previous unit) before the async writes
-  const Win wb = a.brid ? bulk_window(a.brid, d.x, min(d.y, WCAP), 4, a.nb) : Win{nullptr, 0, 0, 0};
-  const Win wp = a.prid ? bulk_window(a.prid, d.z, min(d.w, WCAP), 4, a.np) : Win{nullptr, 0, 0, 0};
-  const Win ws = bulk_window(stage, d.z, min(d.w, WCAP), 2, a.np);
+  const Win wb = a.brid ? bulk_window(a.brid, d.x, min(d.y, WCAP_B), 4, a.nb) : Win{nullptr, 0, 0, 0};
+  const Win wp = a.prid ? bulk_window(a.prid, d.z, min(d.w, WP), 4, a.np) : Win{nullptr, 0, 0, 0};
+  const Win ws = bulk_window(stage, d.z, min(d.w, WP), 2, a.np);
   const uint32_t bytes = wb.bytes + wp.bytes + ws.bytes;
   if (!bytes) {
     mbar_arrive(bar);
@@ -745,13 +749,14 @@ __device__ __forceinline__ void wf_issue(WBuf& B, uint64_t* bar, const uint4 d, 
   if (ws.bytes) bulk_g2s(B.st, ws.src, ws.bytes, bar);
 }
 
-template <typename K>
+template <typename K, uint32_t WP>
 __global__ void __launch_bounds__(HT) hj_write_fast(HJArgs a, const uint16_t* __restrict__ stage,
                                                     const uint8_t* __restrict__ multi) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr uint32_t N = KVec<K>::N;
-  WBuf* B = reinterpret_cast<WBuf*>(smem);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * sizeof(WBuf));
+  using Buf = WBuf<WP>;
+  Buf* B = reinterpret_cast<Buf*>(smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * sizeof(Buf));
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
   const uint32_t G = gridDim.x;
   uint32_t u = blockIdx.x;
@@ -770,10 +775,10 @@ __global__ void __launch_bounds__(HT) hj_write_fast(HJArgs a, const uint16_t* __
     const bool full = multi[u] != 0;
     mbar_wait(bar + b, (it >> 1) & 1);
     if (!full) {
-      const Win wb = a.brid ? bulk_window(a.brid, d.x, min(d.y, WCAP), 4, a.nb) : Win{nullptr, 0, 0, 0};
-      const Win wp = a.prid ? bulk_window(a.prid, d.z, min(d.w, WCAP), 4, a.np) : Win{nullptr, 0, 0, 0};
-      const Win ws = bulk_window(stage, d.z, min(d.w, WCAP), 2, a.np);
-      const WBuf& Bb = B[b];
+      const Win wb = a.brid ? bulk_window(a.brid, d.x, min(d.y, WCAP_B), 4, a.nb) : Win{nullptr, 0, 0, 0};
+      const Win wp = a.prid ? bulk_window(a.prid, d.z, min(d.w, WP), 4, a.np) : Win{nullptr, 0, 0, 0};
+      const Win ws = bulk_window(stage, d.z, min(d.w, WP), 2, a.np);
+      const Buf& Bb = B[b];
       // this warp's rows: those of its count-pass key vectors
       const Span sp = span16(a.pkey, d.z, d.w, sizeof(K));
       uint32_t vb, ve;
@@ -982,10 +987,15 @@ void write_impl(gj_ctx* ctx, uint32_t* out) {
   // units rebuild their table and re-probe
   a.nb = Bld.n;
   a.np = Prb.n;
-  const size_t fsmem = 2 * sizeof(WBuf) + 16;
-  set_smem(ctx, hj_write_fast<K>, fsmem);
-  launch(ctx, "hj_write", hj_write_fast<K>, dim3(hj_grid(ctx, hj_write_fast<K>, fsmem, a.U)), dim3(HT), fsmem, a,
-         (const uint16_t*)jc.stage, (const uint8_t*)jc.multi);
+  auto fast = [&](auto kern, size_t fsmem) {
+    set_smem(ctx, kern, fsmem);
+    launch(ctx, "hj_write", kern, dim3(hj_grid(ctx, kern, fsmem, a.U)), dim3(HT), fsmem, a,
+           (const uint16_t*)jc.stage, (const uint8_t*)jc.multi);
+  };
+  if (Prb.n / std::max<uint32_t>(jc.P, 1) <= 2048 || jc.pchunk <= 2560)
+    fast(hj_write_fast<K, 2560>, 2 * sizeof(WBuf<2560>) + 16);
+  else
+    fast(hj_write_fast<K, PCH_MAX>, 2 * sizeof(WBuf<PCH_MAX>) + 16);
   if (jc.nmulti == 0) return;
   const size_t smem = MultiSmem<K>::bytes;
   set_smem(ctx, hj_write_kernel<K>, smem);

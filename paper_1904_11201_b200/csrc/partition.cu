@@ -109,8 +109,9 @@ __global__ void __launch_bounds__(PT, sizeof(K) == 4 ? 4 : 3) part_hist(const K*
                                                 const uint32_t* __restrict__ chunk_base,
                                                 uint32_t nseg, uint32_t shift, uint32_t bits,
                                                 uint32_t* __restrict__ hist, uint32_t* __restrict__ tile_pref,
-                                                DigitFn fn) {
+                                                uint32_t* __restrict__ tile_st, DigitFn fn) {
   __shared__ uint32_t h[(1 << MAX_BITS) + 1];
+  __shared__ uint32_t wsum[PT / 32];
   const uint32_t D = 1u << bits, mask = D - 1;
   const uint32_t c = blockIdx.x;
   const ChunkLoc L = locate(c, n, seg_off, chunk_base, nseg);
@@ -122,6 +123,31 @@ __global__ void __launch_bounds__(PT, sizeof(K) == 4 ? 4 : 3) part_hist(const K*
   const uint32_t w = threadIdx.x >> 5, lane = lane_id();
   const uint32_t len = (uint32_t)(L.end - L.beg);
   const uint32_t ntiles = (len + TILE - 1) / TILE;
+  // after counting tile t (h = in-chunk counts through tile t): thread i owns digits
+  // 2i, 2i+1 (D <= 2 PT), stores their in-chunk prefix before tile t (kept in
+  // registers) and the tile-local digit starts (exclusive scan of the tile's counts
+  // over the digits), then keeps h as the next tile's prefix
+  const uint32_t d0 = 2 * threadIdx.x;
+  uint32_t prev0 = 0, prev1 = 0;
+  auto tile_rows = [&](uint32_t t) {
+    const uint32_t now0 = d0 < D ? h[d0] : 0u, now1 = d0 + 1 < D ? h[d0 + 1] : 0u;
+    const uint32_t x0 = now0 - prev0, x1 = now1 - prev1;
+    const uint32_t inc = warp_incl_scan(x0 + x1);
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();  // also: every h read done before the next tile's counting
+    uint32_t ex = inc - (x0 + x1);
+    for (uint32_t ww = 0; ww < w; ++ww) ex += wsum[ww];
+    const uint64_t r = ((uint64_t)c * TPC + t) * D;
+    if (d0 + 1 < D) {
+      *reinterpret_cast<uint2*>(tile_pref + r + d0) = make_uint2(prev0, prev1);
+      *reinterpret_cast<uint2*>(tile_st + r + d0) = make_uint2(ex, ex + x0);
+    } else if (d0 < D) {
+      tile_pref[r + d0] = prev0;
+      tile_st[r + d0] = ex;
+    }
+    prev0 = now0;
+    prev1 = now1;
+  };
   if (sizeof(K) == 4) {
     // int32: each thread reads its part of a tile as 16-byte vectors (absolute-address
     // windows: the chunk may start anywhere); the counting order does not matter
@@ -156,9 +182,6 @@ __global__ void __launch_bounds__(PT, sizeof(K) == 4 ? 4 : 3) part_hist(const K*
         for (uint32_t i = 0; i < VPT; ++i)
           vn[i] = threadIdx.x + i * PT < nvn ? __ldg(p + threadIdx.x + i * PT) : uint4{};
       }
-      uint32_t* row = tile_pref + ((uint64_t)c * TPC + t) * D;
-      for (uint32_t d = threadIdx.x; d < D; d += PT) row[d] = h[d];
-      __syncthreads();
       auto count4 = [&](const uint4 x, uint32_t vi) {
         const uint32_t j0 = vi * 4 - sc.x;  // wraps below the tile
         const int32_t kk[4] = {(int32_t)x.x, (int32_t)x.y, (int32_t)x.z, (int32_t)x.w};
@@ -170,6 +193,7 @@ __global__ void __launch_bounds__(PT, sizeof(K) == 4 ? 4 : 3) part_hist(const K*
       for (uint32_t i = 0; i < VPT; ++i) count4(v[i], threadIdx.x + i * PT);  // padding vectors hit bin D
       for (uint32_t vi = threadIdx.x + VPT * PT; vi < nv; vi += PT) count4(__ldg(vec_ptr(t) + vi), vi);
       __syncthreads();
+      tile_rows(t);
 #pragma unroll
       for (uint32_t i = 0; i < VPT; ++i) v[i] = vn[i];
     }
@@ -186,14 +210,12 @@ __global__ void __launch_bounds__(PT, sizeof(K) == 4 ? 4 : 3) part_hist(const K*
     if (t + 1 < ntiles)
       load_tile<K, false>(key, nullptr, L.beg + (uint64_t)(t + 1) * TILE, min(len - (t + 1) * TILE, (uint32_t)TILE),
                           w, lane, kn, r0);
-    uint32_t* row = tile_pref + ((uint64_t)c * TPC + t) * D;
-    for (uint32_t d = threadIdx.x; d < D; d += PT) row[d] = h[d];
-    __syncthreads();
     // branch-free: padding items count into the dummy bin D
 #pragma unroll
     for (int i = 0; i < PI; ++i)
       atomicAdd(&h[(w * PI + i) * 32 + lane < cnt ? digit_of<RANGE>(k[i], shift, mask, fn) : D], 1u);
     __syncthreads();
+    tile_rows(t);
 #pragma unroll
     for (int i = 0; i < PI; ++i) k[i] = kn[i];
   }
@@ -514,10 +536,8 @@ __global__ void __launch_bounds__(PT, SCATTER_MINB) part_scatter(
 __global__ void __launch_bounds__(PT) tile_base_kernel(uint64_t n, const uint32_t* __restrict__ seg_off,
                                                        const uint32_t* __restrict__ chunk_base, uint32_t nseg,
                                                        uint32_t bits, const uint32_t* __restrict__ scanned,
-                                                       uint32_t* __restrict__ tile_pref, uint32_t* __restrict__ tile_st,
-                                                       uint4* __restrict__ tdesc, uint32_t* __restrict__ tile_ctr) {
-  __shared__ uint32_t cnt_s[1 << MAX_BITS];
-  __shared__ uint32_t wsum[PT / 32];
+                                                       uint32_t* __restrict__ tile_pref, uint4* __restrict__ tdesc,
+                                                       uint32_t* __restrict__ tile_ctr) {
   const uint32_t c = blockIdx.x, D = 1u << bits;
   if (c == 0 && threadIdx.x == 0) *tile_ctr = 0;
   const ChunkLoc L = locate(c, n, seg_off, chunk_base, nseg);
@@ -530,32 +550,19 @@ __global__ void __launch_bounds__(PT) tile_base_kernel(uint64_t n, const uint32_
   }
   if (c >= L.total) return;
   const uint32_t nt = (len + TILE - 1) / TILE;
+  // thread i: digits 2i, 2i+1 (D <= 2 PT); the chunk's bases read once
+  const uint32_t d0 = 2 * threadIdx.x;
+  if (d0 >= D) return;
+  const uint64_t i0 = (uint64_t)L.cb * D + (uint64_t)d0 * L.nc + (c - L.cb);
+  const uint32_t b0 = scanned[i0], b1 = d0 + 1 < D ? scanned[i0 + L.nc] : 0u;
   for (uint32_t t = 0; t < nt; ++t) {
     uint32_t* row = tile_pref + ((uint64_t)c * TPC + t) * D;
-    for (uint32_t d = threadIdx.x; d < D; d += PT) {
-      const uint64_t idx = (uint64_t)L.cb * D + (uint64_t)d * L.nc + (c - L.cb);
-      const uint32_t base = scanned[idx], pre = row[d];
-      // digit d's count in tile t: the next tile's in-chunk prefix (still unmodified),
-      // or the chunk's total for the last tile (consecutive entries of the scanned
-      // (segment, digit, chunk) matrix; the scan also wrote the grand total at the end)
-      const uint32_t next = t + 1 < nt ? row[D + d] : scanned[idx + 1] - base;
-      cnt_s[d] = next - pre;
-      row[d] = base + pre;
+    if (d0 + 1 < D) {
+      uint2 v = *reinterpret_cast<const uint2*>(row + d0);
+      *reinterpret_cast<uint2*>(row + d0) = make_uint2(v.x + b0, v.y + b1);
+    } else {
+      row[d0] += b0;
     }
-    __syncthreads();
-    // tile-local digit starts: exclusive scan of the tile's D digit counts (each thread
-    // two consecutive digits)
-    const uint32_t d0 = 2 * threadIdx.x;
-    const uint32_t x0 = d0 < D ? cnt_s[d0] : 0u, x1 = d0 + 1 < D ? cnt_s[d0 + 1] : 0u;
-    const uint32_t inc = warp_incl_scan(x0 + x1);
-    if (lane_id() == 31) wsum[threadIdx.x >> 5] = inc;
-    __syncthreads();
-    uint32_t ex = inc - (x0 + x1);
-    for (uint32_t ww = 0; ww < (threadIdx.x >> 5); ++ww) ex += wsum[ww];
-    uint32_t* st = tile_st + ((uint64_t)c * TPC + t) * D;
-    if (d0 < D) st[d0] = ex;
-    if (d0 + 1 < D) st[d0 + 1] = ex + x0;
-    __syncthreads();
   }
 }
 
@@ -684,14 +691,14 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
     uint32_t* hist = static_cast<uint32_t*>(ws(ctx, (t + ".hist").c_str(), (hn + 1) * sizeof(uint32_t)));
     const uint64_t ntiles = max_chunks * TPC;
     uint32_t* tile_pref = static_cast<uint32_t*>(ws(ctx, "part.tile_pref", ntiles * D * sizeof(uint32_t)));
+    uint32_t* tile_st = static_cast<uint32_t*>(ws(ctx, "part.tile_st", ntiles * D * sizeof(uint32_t)));
     launch(ctx, "part_hist", part_hist<K, RANGE>, dim3((unsigned)max_chunks), dim3(PT), 0, kin, n, seg_off,
-           (const uint32_t*)chunk_base, nseg, shift, bits, hist, tile_pref, fn);
+           (const uint32_t*)chunk_base, nseg, shift, bits, hist, tile_pref, tile_st, fn);
     exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
     uint4* tdesc = static_cast<uint4*>(ws(ctx, "part.tdesc", (ntiles + 1) * sizeof(uint4)));
     uint32_t* ctr = static_cast<uint32_t*>(ws(ctx, "part.tile_ctr", sizeof(uint32_t)));
-    uint32_t* tile_st = static_cast<uint32_t*>(ws(ctx, "part.tile_st", ntiles * D * sizeof(uint32_t)));
     launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, seg_off,
-           (const uint32_t*)chunk_base, nseg, bits, (const uint32_t*)hist, tile_pref, tile_st, tdesc, ctr);
+           (const uint32_t*)chunk_base, nseg, bits, (const uint32_t*)hist, tile_pref, tdesc, ctr);
     launch_scatter<K, RANGE, false>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, tile_pref, tile_st, ctr,
                                     kout, rout, fn, ShuffleDest{});
     const uint32_t P = nseg << bits;
@@ -729,15 +736,15 @@ ShufflePass shuffle_prepare_impl(gj_ctx* ctx, const gj_rel& X, uint32_t g, const
   sp.ntiles = max_chunks * TPC;
   uint32_t* tile_pref = static_cast<uint32_t*>(ws(ctx, (t + ".stp").c_str(), sp.ntiles * D * sizeof(uint32_t) + 4));
   const uint32_t shift = 32 - g;
+  uint32_t* tile_st = static_cast<uint32_t*>(ws(ctx, (t + ".sst").c_str(), sp.ntiles * D * sizeof(uint32_t) + 4));
   launch(ctx, "part_hist", part_hist<K, false>, dim3((unsigned)std::max<uint64_t>(max_chunks, 1)), dim3(PT), 0,
          static_cast<const K*>(X.key), n, (const uint32_t*)nullptr, (const uint32_t*)nullptr, 1u, shift, g, hist,
-         tile_pref, DigitFn{});
+         tile_pref, tile_st, DigitFn{});
   exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
   uint4* tdesc = static_cast<uint4*>(ws(ctx, (t + ".stdesc").c_str(), (sp.ntiles + 1) * sizeof(uint4)));
   uint32_t* ctr = static_cast<uint32_t*>(ws(ctx, (t + ".sctr").c_str(), sizeof(uint32_t)));
-  uint32_t* tile_st = static_cast<uint32_t*>(ws(ctx, (t + ".sst").c_str(), sp.ntiles * D * sizeof(uint32_t) + 4));
   launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, (const uint32_t*)nullptr,
-         (const uint32_t*)nullptr, 1u, g, (const uint32_t*)hist, tile_pref, tile_st, tdesc, ctr);
+         (const uint32_t*)nullptr, 1u, g, (const uint32_t*)hist, tile_pref, tdesc, ctr);
   uint32_t* off = static_cast<uint32_t*>(ws(ctx, (t + ".soff").c_str(), (D + 1) * sizeof(uint32_t)));
   launch(ctx, "extract_off", extract_off, dim3((D + 1 + 255) / 256), dim3(256), 0, (const uint32_t*)hist,
          (const uint32_t*)nullptr,

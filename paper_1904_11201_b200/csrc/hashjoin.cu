@@ -375,7 +375,11 @@ __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __rest
 // computed once, together with its register prefetch.
 constexpr uint32_t EMPTY_KEY = 0x80000000u;  // INT32_MIN
 constexpr uint32_t KT = 8192;                // key slots (load <= 1/4 at 2048 build rows, <= 1/2 at 4096)
-constexpr size_t I32_SMEM = KT * 4 + KT * 2 + BCH_MAX * 2;
+constexpr uint32_t DB = 32;                  // unit descriptors per cp.async batch (2 batches in flight)
+// key slots, row per slot, the side-list head (a probe for EMPTY_KEY needs the first
+// side row only: several are a MULTI row, re-probed by hj_write_kernel), descriptors
+constexpr size_t I32_OFF_DESC = KT * 4 + KT * 2 + 16;
+constexpr size_t I32_SMEM = I32_OFF_DESC + 2 * DB * 16;
 
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   uint32_t v;
@@ -419,9 +423,9 @@ __device__ __forceinline__ UnitPlan plan_unit(const HJArgs& a, const uint4 d, ui
 // insert key k (row j); returns true if an equal key was met (a duplicate)
 __device__ __forceinline__ bool insert1(const I32Tab& t, uint32_t s, uint32_t tmask, uint32_t k, uint32_t j,
                                         uint32_t old, uint32_t* side_n) {
-  if (k == EMPTY_KEY) {  // the empty marker itself: side list
+  if (k == EMPTY_KEY) {  // the empty marker itself: side list (count + first row)
     const uint32_t at = atomicAdd(side_n, 1u);
-    sts16(t.side + 2 * at, j);
+    if (at == 0) sts16(t.side, j);
     return at > 0;
   }
   bool dup = false;
@@ -524,6 +528,17 @@ __device__ __forceinline__ void probe4(const I32Tab& t, uint4 x, uint32_t v, uin
   }
 }
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// CTA b owns the contiguous unit range [b U / G, (b+1) U / G): the descriptors stream
+// into a 2 x 32-entry shared ring by cp.async (a batch is requested 32 units before
+// it is read, so the descriptor -> key-vector dependency never waits on DRAM), and
+// consecutive units of one partition (probe chunks of a partition whose build side is
+// one chunk) share their build chunk: the table is built once and kept.
 __global__ void __launch_bounds__(HT, 4) hj_count_i32(HJArgs a, uint16_t* __restrict__ stage,
                                                       uint8_t* __restrict__ multi,
                                                       unsigned long long* __restrict__ nmulti) {
@@ -531,41 +546,65 @@ __global__ void __launch_bounds__(HT, 4) hj_count_i32(HJArgs a, uint16_t* __rest
   __shared__ uint32_t s_dup, s_side;
   const uint32_t tb = saddr(smem);
   const I32Tab t{tb, tb + KT * 4, tb + KT * 6};
+  const uint4* ring = reinterpret_cast<const uint4*>(smem + I32_OFF_DESC);
+  const uint32_t ring_a = tb + (uint32_t)I32_OFF_DESC;
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = lane_id();
   const uint32_t G = gridDim.x;
   const uint32_t U = (uint32_t)(a.meta[3] / HW);
-  uint32_t u = blockIdx.x;
-  if (u >= U) return;
+  const uint32_t u0 = (uint32_t)((uint64_t)U * blockIdx.x / G), u1 = (uint32_t)((uint64_t)U * (blockIdx.x + 1) / G);
+  const uint32_t n = u1 - u0;
+  if (n == 0) return;
+  // batch k (units u0 + 32k ..) -> ring slot k & 1; one commit group per batch
+  auto fetch = [&](uint32_t k) {
+    if (tid < DB) {
+      const uint32_t i = k * DB + tid;
+      if (i < n) cp_async16(ring_a + 16 * ((k & 1) * DB + tid), a.desc + u0 + i);
+    }
+    cp_async_commit();
+  };
+  fetch(0);
+  fetch(1);
   for (uint32_t i = tid; i < KT / 4; i += HT) sts128(t.key + 16 * i, EMPTY_KEY);
+  if (tid == 0) s_dup = s_side = 0;
+  cp_async_wait1();  // batch 0 landed (this thread's part)
+  __syncthreads();
   const bool vec = reinterpret_cast<uint64_t>(stage) % 8 == 0 && reinterpret_cast<uint64_t>(a.pkey) % 16 == 0;
   const uint4 zero = make_uint4(0, 0, 0, 0);
-  uint4 d = a.desc[u];
+  uint4 d = ring[0];
   UnitPlan P = plan_unit(a, d, w);
   // register prefetch: two build and two probe vectors per thread (all of a ~2040-row
   // unit; the few extra vectors of larger units are loaded when needed)
   uint4 bv0 = tid < P.sb.nv ? ldv(P.sb, tid) : zero, bv1 = tid + HT < P.sb.nv ? ldv(P.sb, tid + HT) : zero;
   uint4 pv0 = P.vb + lane < P.ve ? ldv(P.sp, P.vb + lane) : zero;
   uint4 pv1 = P.vb + lane + 32 < P.ve ? ldv(P.sp, P.vb + lane + 32) : zero;
-  for (; u < U; u += G) {
-    const uint4 dn = u + G < U ? a.desc[u + G] : zero;
+  bool built = false;  // the table holds d's build chunk
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t u = u0 + i;
+    if (((i + 1) & (DB - 1)) == 0 && i + 1 < n) {  // CTA-uniform: the next unit opens batch (i+1)/32
+      cp_async_wait1();
+      __syncthreads();  // batch visible to all; every read of the slot refilled below is done
+      fetch((i + 1) / DB + 1);
+    }
+    const uint4 dn = i + 1 < n ? ring[((i + 1) & (2 * DB - 1))] : zero;
+    const bool keep = dn.y != 0 && dn.x == d.x && dn.y == d.y;  // next unit: same build chunk
     const UnitPlan PN = plan_unit(a, dn, w);
-    const uint4 nb0 = tid < PN.sb.nv ? ldv(PN.sb, tid) : zero;
-    const uint4 nb1 = tid + HT < PN.sb.nv ? ldv(PN.sb, tid + HT) : zero;
+    const uint4 nb0 = !keep && tid < PN.sb.nv ? ldv(PN.sb, tid) : zero;
+    const uint4 nb1 = !keep && tid + HT < PN.sb.nv ? ldv(PN.sb, tid + HT) : zero;
     const uint4 np0 = PN.vb + lane < PN.ve ? ldv(PN.sp, PN.vb + lane) : zero;
     const uint4 np1 = PN.vb + lane + 32 < PN.ve ? ldv(PN.sp, PN.vb + lane + 32) : zero;
 
     const uint32_t bn = d.y, pn = d.w;
     const uint32_t logT = min(max(32 - __clz(4 * bn - 1), 5u), 13u);  // ~4 slots per build row
     const uint32_t T = 1u << logT, tmask = T - 1, tshift = 32 - logT;
-    if (tid == 0) s_dup = s_side = 0;
-    __syncthreads();  // table cleared, flags reset
-    bool dup = false;
-    if (tid < P.sb.nv) dup |= build4(t, bv0, tid, P.sb.shift, bn, tmask, tshift, &s_side);
-    if (tid + HT < P.sb.nv) dup |= build4(t, bv1, tid + HT, P.sb.shift, bn, tmask, tshift, &s_side);
-    for (uint32_t v = tid + 2 * HT; v < P.sb.nv; v += HT)
-      dup |= build4(t, ldv(P.sb, v), v, P.sb.shift, bn, tmask, tshift, &s_side);
-    if (__any_sync(FULL, dup) && lane == 0) s_dup = 1;
-    __syncthreads();
+    if (!built) {  // CTA-uniform
+      bool dup = false;
+      if (tid < P.sb.nv) dup |= build4(t, bv0, tid, P.sb.shift, bn, tmask, tshift, &s_side);
+      if (tid + HT < P.sb.nv) dup |= build4(t, bv1, tid + HT, P.sb.shift, bn, tmask, tshift, &s_side);
+      for (uint32_t v = tid + 2 * HT; v < P.sb.nv; v += HT)
+        dup |= build4(t, ldv(P.sb, v), v, P.sb.shift, bn, tmask, tshift, &s_side);
+      if (__any_sync(FULL, dup) && lane == 0) s_dup = 1;
+      __syncthreads();
+    }
     const bool unique = s_dup == 0;  // no duplicate build key: stop each probe at its first match
     const uint32_t side_n = s_side;
     uint16_t* st = stage + d.z;
@@ -583,12 +622,19 @@ __global__ void __launch_bounds__(HT, 4) hj_count_i32(HJArgs a, uint16_t* __rest
       multi[u] = 1;
       atomicAdd(nmulti, 1ull);  // > 0 tells the host to launch the MULTI write pass
     }
-    __syncthreads();  // every probe of this unit is done: clear the key slots it used
-    for (uint32_t i = tid; i < T / 4; i += HT) sts128(t.key + 16 * i, EMPTY_KEY);
+    if (!keep) {  // CTA-uniform
+      __syncthreads();  // every probe of this unit is done: clear the key slots it used
+      for (uint32_t i2 = tid; i2 < T / 4; i2 += HT) sts128(t.key + 16 * i2, EMPTY_KEY);
+      if (tid == 0) s_dup = s_side = 0;
+      __syncthreads();  // table cleared, flags reset
+    }
+    built = keep;
     d = dn;
     P = PN;
-    bv0 = nb0, bv1 = nb1, pv0 = np0, pv1 = np1;
+    if (!keep) bv0 = nb0, bv1 = nb1;
+    pv0 = np0, pv1 = np1;
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");  // no copy outstanding at exit
 }
 
 // Write pass for units with a MULTI row (duplicate build keys) or a partition split

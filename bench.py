@@ -449,14 +449,15 @@ def run_ours(args, world, rank, local):
         # The NLJ compares the pairs of the cells the region matrix keeps (all n_R x n_S
         # with theta_regions=0): INT ALU roofline, 1.5 ALU-pipe instr per pair-compare
         # (band: + 1 FMA-pipe IMAD), DESIGN.md §5.  The write pass also stores 8 B per
-        # pair: its bound is whichever of the two floors is higher.
+        # pair: its bound is whichever of the two floors is higher (the band's write
+        # pass, mostly Green cross products, is HBM-bound).
         pairs, cross = ctx.theta_stats()
         d = per_kernel[dom]
         sm = sampler.summary().get("sm_mhz") or 1965
         alu_peak = 148 * 64 * sm * 1e6 / 1.5 / 1e12  # T pair-compares/s the ALU pipe allows
         t = d["ms_per_launch"] * 1e-3
         t_alu = pairs / (alu_peak * 1e12)
-        t_hbm = (8 * info["n_out"] / (hbm * 1e9)) if dom == "nlj_write" else 0.0
+        t_hbm = (8 * info["n_out"] / (hbm * 1e9)) if dom in ("nlj_write", "band_write", "cross_rect") else 0.0
         if t_hbm > t_alu:
             ach = 8 * info["n_out"] / t / 1e9
             roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",

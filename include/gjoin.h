@@ -201,9 +201,10 @@ gj_status join_materialize(gj_ctx* ctx, gj_rel R, gj_rel S, uint32_t* out, uint6
  * PAPER.md:302 §4.2).  By default (GJ_OPT_THETA_REGIONS = 1) both relations are
  * range-partitioned into equal-width key buckets and only the region matrix's Red
  * cells (gj_region_classify) are compared -- R tiles held in registers, S tiles
- * staged into shared memory by 1-D TMA bulk copies -- Green cells are written as
- * cross products and White cells skipped; with GJ_OPT_THETA_REGIONS = 0 every
- * (R, S) pair is compared once per pass.
+ * staged into shared memory by 1-D TMA bulk copies; for GJ_BAND one warp per R row
+ * over its Red buckets -- Green cells are written as cross products and White cells
+ * skipped; with GJ_OPT_THETA_REGIONS = 0 every (R, S) pair is compared once per
+ * pass.
  * op in gj_op; eps used only by GJ_BAND.
  * theta_join_count: *n_out = |J(R,S,op)|; synchronises; caches per-unit offsets.
  * theta_join_materialize: writes |J| pairs (same cache/ERANGE rules as above). */
@@ -217,11 +218,13 @@ gj_status theta_join_materialize(gj_ctx* ctx, gj_rel R, gj_rel S, int op, uint64
  * (R bucket x, S bucket y) for R.key OP S.key: 0 White (no pair can match; skipped),
  * 1 Red (compared by the tiled NLJ), 2 Green (every pair matches; written as a cross
  * product).  <, <=: x < y Green, x == y Red, x > y White; >, >=: mirrored; !=:
- * off-diagonal Green; =: diagonal Red, rest White; GJ_BAND: |x - y| <= m Red, rest
- * White, where m = ceil(eps / bucket width) (m is ignored for the other ops).
- * GJ_EINVAL for an unknown op, k = 0, k > 4096 or cls == NULL. */
+ * off-diagonal Green; =: diagonal Red, rest White; GJ_BAND (bucket width w): |x - y|
+ * <= g Green, else |x - y| <= m Red, rest White, where m = ceil(eps / w) and
+ * g = floor((eps + 1) / w) - 1 (-1 = no Green cell); m and g are ignored for the
+ * other ops.  The band join uses w ~ eps / 8, so its output is mostly Green.
+ * GJ_EINVAL for an unknown op, k = 0, k > 4096, g < -1 or cls == NULL. */
 enum { GJ_CELL_WHITE = 0, GJ_CELL_RED = 1, GJ_CELL_GREEN = 2 };
-gj_status gj_region_classify(int op, uint32_t k, uint64_t m, uint8_t* cls);
+gj_status gj_region_classify(int op, uint32_t k, uint64_t m, int64_t g, uint8_t* cls);
 
 /* ---------------------------------------------------------------- pre-filter
  * Approximation of the paper's two-round common-key pre-filter (PAPER.md:78-82

@@ -103,7 +103,7 @@ def _load():
     L.prefilter_dist.argtypes = [vp, vp, _Rel, _Rel, u32, i32, u64, ctypes.c_double, vp, vp, pu64, vp, vp, pu64]
     L.theta_join_dist_count.argtypes = [vp, vp, _Rel, _Rel, i32, u64, pu64, pu64]
     L.theta_join_dist_materialize.argtypes = [vp, vp, _Rel, _Rel, i32, u64, vp, u64, pu64]
-    L.gj_region_classify.argtypes = [i32, u32, u64, vp]
+    L.gj_region_classify.argtypes = [i32, u32, u64, ctypes.c_int64, vp]
     L.gj_region_classify.restype = i32
     L.gj_dist_plan.argtypes = [pu64, i32, i32, i32, ctypes.POINTER(u32), ctypes.POINTER(u32), pu64]
     for f in ("gj_ctx_create", "gj_ctx_set_stream", "gj_ctx_set_allocator", "gj_ctx_set_option", "join_count", "join_materialize",
@@ -380,12 +380,13 @@ def join_host_batch(ctx: Context, batches):
 
 # ---------------------------------------------------------------- multi-GPU (NCCL)
 
-def region_classify(op: str, k: int, m: int = 0):
+def region_classify(op: str, k: int, m: int = 0, g: int = -1):
     """Region-matrix cell classes (gj_region_classify, §4.2 Fig. 9): a (k, k)
-    uint8 array, [x, y] = class of (R bucket x, S bucket y): 0 White, 1 Red, 2 Green."""
+    uint8 array, [x, y] = class of (R bucket x, S bucket y): 0 White, 1 Red, 2 Green.
+    band: m = Red radius ceil(eps / w), g = Green radius floor((eps + 1) / w) - 1."""
     import numpy as np
     out = np.zeros(k * k, dtype=np.uint8)
-    _check(lib.gj_region_classify(OPS[op], k, m, out.ctypes.data_as(ctypes.c_void_p)))
+    _check(lib.gj_region_classify(OPS[op], k, m, g, out.ctypes.data_as(ctypes.c_void_p)))
     return out.reshape(k, k)
 
 

@@ -544,14 +544,15 @@ NLJArgs make_args(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, const ThetaCach
 // rectangles start exactly where V ends, so every pair is produced once.
 // Class of cell (x, y) = (R bucket x, S bucket y) for R.key OP S.key (Fig. 9,
 // Alg.3 Reduce): GREEN = every pair satisfies the predicate (written as a cross
-// product), RED = must be compared (sent to the NLJ), WHITE = no pair can match
-// (skipped).  Buckets are equal-width and ascending, so for <, <=: x < y is Green,
-// x > y White; >, >=: mirrored; !=: off-diagonal Green; =: off-diagonal White; the
-// diagonal is Red (bucket ties).  Band: cells within m = ceil(eps / w) buckets can
-// hold a pair and are Red (the NLJ evaluates them; they are not split further into
-// Green), the rest White.
+// product), RED = must be compared, WHITE = no pair can match (skipped).  Buckets
+// are equal-width and ascending, so for <, <=: x < y is Green, x > y White; >, >=:
+// mirrored; !=: off-diagonal Green; =: off-diagonal White; the diagonal is Red
+// (bucket ties).  Band (width w): the largest distance of a pair in cell (x, y) is
+// (|x - y| + 1) w - 1 and the smallest (|x - y| - 1) w + 1, so |x - y| <= g =
+// floor((eps + 1) / w) - 1 is Green (g < 0: none), |x - y| <= m = ceil(eps / w) Red,
+// the rest White.
 enum { CELL_WHITE = 0, CELL_RED = 1, CELL_GREEN = 2 };
-int region_class(int op, uint64_t x, uint64_t y, uint64_t m) {
+int region_class(int op, uint64_t x, uint64_t y, uint64_t m, int64_t g) {
   switch (op) {
     case GJ_EQ: return x == y ? CELL_RED : CELL_WHITE;
     case GJ_NE: return x == y ? CELL_RED : CELL_GREEN;
@@ -559,7 +560,131 @@ int region_class(int op, uint64_t x, uint64_t y, uint64_t m) {
     case GJ_LE: return x < y ? CELL_GREEN : (x == y ? CELL_RED : CELL_WHITE);
     case GJ_GT:
     case GJ_GE: return x > y ? CELL_GREEN : (x == y ? CELL_RED : CELL_WHITE);
-    default: return (x > y ? x - y : y - x) <= m ? CELL_RED : CELL_WHITE;
+    default: {
+      const uint64_t d = x > y ? x - y : y - x;
+      return g >= 0 && d <= (uint64_t)g ? CELL_GREEN : (d <= m ? CELL_RED : CELL_WHITE);
+    }
+  }
+}
+
+// Band join over the region matrix (Alg.3 with the band's Green cells).  Both
+// relations are range-partitioned into P equal-width buckets of width w = 2^sh,
+// w ~ eps / 8, so the Green cells (all pairs match) carry most of the output and the
+// Red ones are a thin rim: for the R row r in bucket x the S rows of buckets
+// [x - m, x + m] are one contiguous run of the partitioned S, the Green buckets
+// [x - g, x + g] one contiguous run inside it.  One warp per R row: the count pass
+// adds the Green run's length to the Red rows' matches (exact predicate, ballots of
+// 32 S keys); the write pass emits the row's pairs in partitioned-S order -- left
+// Red matches (ballot ranks), the Green run as coalesced 8-byte stores, right Red
+// matches -- at the row's scanned offset.
+__device__ __forceinline__ int32_t shfl_key(int32_t v, uint32_t q) { return __shfl_sync(FULL, v, q); }
+__device__ __forceinline__ int64_t shfl_key(int64_t v, uint32_t q) {
+  return (int64_t)__shfl_sync(FULL, (long long)v, q);
+}
+
+template <typename K>
+struct BandArgs {
+  const K* rkey;
+  const uint32_t* rrid;
+  uint64_t nR;
+  const K* skey;
+  const uint32_t* srid;
+  const uint32_t* so;  // P + 1 S bucket starts
+  uint32_t P, sh, m;
+  int32_t g;
+  unsigned long long lo;
+  uint64_t eps;
+  uint32_t* cnt;                   // count: per R row
+  unsigned long long* stats;       // count: [0] Red pairs compared, [1] Green pairs
+  const uint64_t* off;             // write: per R row
+  uint2* out;
+};
+
+template <typename K, bool WRITE>
+__global__ void __launch_bounds__(256) band_cells_kernel(BandArgs<K> a) {
+  const uint32_t lane = lane_id();
+  const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  unsigned long long red_n = 0, green_n = 0;
+  // a warp takes 32 consecutive R rows: lane l fetches row l's key, rid, offset and
+  // bucket bounds (one dependent-load chain for 32 rows), then the warp walks the rows
+  for (uint64_t row0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; row0 < a.nR;
+       row0 += nwarps * 32) {
+    const uint64_t myrow = row0 + lane;
+    const bool have = myrow < a.nR;
+    K mykey = have ? a.rkey[myrow] : K(0);
+    uint32_t rb = 0, gb = 0, ge = 0, re = 0;  // Red [rb, gb) and [ge, re), Green [gb, ge)
+    if (have) {
+      const uint64_t x = (uint64_t)(KeyT<K>::bias(mykey) - a.lo) >> a.sh;
+      const uint64_t yl = x >= a.m ? x - a.m : 0, yh = min(x + a.m, (uint64_t)a.P - 1);
+      rb = a.so[yl];
+      re = a.so[yh + 1];
+      if (a.g >= 0) {
+        const uint64_t g = (uint64_t)a.g;
+        gb = a.so[x >= g ? x - g : 0];
+        ge = a.so[min(x + g, (uint64_t)a.P - 1) + 1];
+      } else {
+        gb = ge = a.so[x];
+      }
+    }
+    uint32_t myrid = 0;
+    uint64_t myoff = 0;
+    if (WRITE && have) {
+      myrid = a.rrid[myrow];
+      myoff = a.off[myrow];
+    }
+    const uint32_t nr = (uint32_t)min((uint64_t)32, a.nR - row0);
+    uint32_t mycnt = 0;
+    for (uint32_t q = 0; q < nr; ++q) {
+      const K r = shfl_key(mykey, q);
+      const uint32_t qrb = __shfl_sync(FULL, rb, q), qgb = __shfl_sync(FULL, gb, q);
+      const uint32_t qge = __shfl_sync(FULL, ge, q), qre = __shfl_sync(FULL, re, q);
+      if (!WRITE) {
+        uint32_t c = 0;
+        auto red = [&](uint32_t b, uint32_t e) {
+#pragma unroll 4
+          for (uint32_t j0 = b; j0 < e; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            c += __popc(__ballot_sync(FULL, j < e && theta_exact<K, GJ_BAND>(r, a.skey[j], a.eps)));
+          }
+        };
+        red(qrb, qgb);
+        red(qge, qre);
+        if (lane == q) mycnt = c + (qge - qgb);
+        if (lane == 0) {
+          red_n += (qgb - qrb) + (qre - qge);
+          green_n += qge - qgb;
+        }
+      } else {
+        const uint32_t rr = __shfl_sync(FULL, myrid, q);
+        uint64_t o = __shfl_sync(FULL, myoff, q);
+        auto red = [&](uint32_t b, uint32_t e) {
+          for (uint32_t j0 = b; j0 < e; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            const bool p = j < e && theta_exact<K, GJ_BAND>(r, a.skey[j], a.eps);
+            const uint32_t bal = __ballot_sync(FULL, p);
+            if (p) a.out[o + __popc(bal & lanemask_lt())] = make_uint2(rr, a.srid[j]);
+            o += __popc(bal);
+          }
+        };
+        red(qrb, qgb);
+        const uint32_t gn = qge - qgb;
+        uint2* go = a.out + o;
+        const uint32_t* gs = a.srid + qgb;
+#pragma unroll 4
+        for (uint32_t i = lane; i < gn; i += 32) go[i] = make_uint2(rr, gs[i]);
+        o += gn;
+        red(qge, qre);
+      }
+    }
+    if (!WRITE && have) a.cnt[myrow] = mycnt;
+  }
+  if (!WRITE) {
+    red_n = warp_sum(red_n);
+    green_n = warp_sum(green_n);
+    if (lane == 0 && (red_n | green_n)) {
+      atomicAdd(&a.stats[0], red_n);
+      atomicAdd(&a.stats[1], green_n);
+    }
   }
 }
 
@@ -606,16 +731,16 @@ void region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, int op, uint64_
       ylo = x1 > m ? x1 - m : 0;
       yhi = std::min<uint64_t>(P - 1, x2 + m);
     }
-    while (ylo > 0 && region_class(op, x1, ylo - 1, m) == CELL_RED) --ylo;
-    while (yhi + 1 < P && region_class(op, x2, yhi + 1, m) == CELL_RED) ++yhi;
+    while (ylo > 0 && region_class(op, x1, ylo - 1, m, -1) == CELL_RED) --ylo;
+    while (yhi + 1 < P && region_class(op, x2, yhi + 1, m, -1) == CELL_RED) ++yhi;
     const uint64_t vb = so[ylo] / al * al, ve = std::min<uint64_t>(nS, (so[yhi + 1] + al - 1) / al * al);
     tv[t] = {vb, ve};
     visit += ve - vb;
     // outside V a row's cells are Green or White as a whole side: Green after V when
     // the tile's last row x2 sees bucket yhi + 1 Green (then every row does), before V
     // when its first row x1 sees bucket ylo - 1 Green
-    const bool after = yhi + 1 < P && region_class(op, x2, yhi + 1, m) == CELL_GREEN;
-    const bool before = ylo > 0 && region_class(op, x1, ylo - 1, m) == CELL_GREEN;
+    const bool after = yhi + 1 < P && region_class(op, x2, yhi + 1, m, -1) == CELL_GREEN;
+    const bool before = ylo > 0 && region_class(op, x1, ylo - 1, m, -1) == CELL_GREEN;
     if (after && ve < nS) tc.rects.push_back(make_uint4((uint32_t)r0, (uint32_t)rn, (uint32_t)ve, (uint32_t)(nS - ve)));
     if (before && vb > 0) tc.rects.push_back(make_uint4((uint32_t)r0, (uint32_t)rn, 0u, (uint32_t)vb));
   }
@@ -666,6 +791,91 @@ void region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, int op, uint64_
   tc.cross_pairs = cross;
 }
 
+// Band join on the region matrix with Green cells (band_cells_kernel): buckets of
+// width 2^sh ~ eps / 8 (at most 2^18 of them), so ~90% of a row's pairs fall in Green
+// cells when the keys are spread over the buckets (configs[3]: w = 4096, g = 12,
+// m = 14 -- 25 Green and 4 Red S buckets per R row).
+template <typename K>
+void band_region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint64_t eps, unsigned long long lo,
+                       unsigned long long hi) {
+  ThetaCache& tc = ctx->tc;
+  const unsigned long long span = hi - lo;
+  const uint32_t L = span ? 64 - (uint32_t)__builtin_clzll(span) : 1;
+  uint32_t sh = 0;
+  while (sh < 63 && (2ull << sh) <= eps / 8) ++sh;  // largest 2^sh <= eps / 8
+  if (L > 18 && sh < L - 18) sh = L - 18;           // at most 2^18 buckets
+  const uint32_t Bb = L > sh ? L - sh : 1;
+  const uint32_t P = 1u << Bb;
+  const Partitioned PR = range_partition(ctx, R, Bb, lo, sh, "tR");
+  const Partitioned PS = range_partition(ctx, S, Bb, lo, sh, "tS");
+  const unsigned __int128 w = (unsigned __int128)1 << sh;
+  const unsigned __int128 mm = ((unsigned __int128)eps + w - 1) / w;
+  const uint32_t m = mm > P ? P : (uint32_t)mm;
+  const unsigned __int128 gg = ((unsigned __int128)eps + 1) / w;
+  const int32_t g = gg == 0 ? -1 : (int32_t)std::min<unsigned __int128>(gg - 1, P);
+  tc.regions = true;
+  tc.band = true;
+  tc.PR = gj_rel{PR.key, PR.rid, R.n, R.key_type, 0};
+  tc.PS = gj_rel{PS.key, PS.rid, S.n, S.key_type, 0};
+  tc.band_so = PS.off;
+  tc.band_P = P;
+  tc.band_sh = sh;
+  tc.band_m = m;
+  tc.band_g = g;
+  tc.band_lo = lo;
+  uint32_t* cnt = static_cast<uint32_t*>(ws(ctx, "band.cnt", (R.n + 1) * sizeof(uint32_t)));
+  uint64_t* off = static_cast<uint64_t*>(ws(ctx, "band.off", (R.n + 1) * sizeof(uint64_t)));
+  unsigned long long* st = static_cast<unsigned long long*>(ws(ctx, "band.stats", 4 * sizeof(unsigned long long)));
+  GJ_CUDA(cudaMemsetAsync(st, 0, 2 * sizeof(unsigned long long), ctx->stream));
+  BandArgs<K> a{};
+  a.rkey = static_cast<const K*>(PR.key);
+  a.rrid = PR.rid;
+  a.nR = R.n;
+  a.skey = static_cast<const K*>(PS.key);
+  a.srid = PS.rid;
+  a.so = PS.off;
+  a.P = P;
+  a.sh = sh;
+  a.m = m;
+  a.g = g;
+  a.lo = lo;
+  a.eps = eps;
+  a.cnt = cnt;
+  a.stats = st;
+  const unsigned grid = (unsigned)std::min<uint64_t>((R.n + 255) / 256, (uint64_t)ctx->num_sms * 8);
+  launch(ctx, "band_count", band_cells_kernel<K, false>, dim3(grid), dim3(256), 0, a);
+  exclusive_scan<uint32_t, uint64_t>(ctx, cnt, off, R.n, off + R.n);
+  GJ_CUDA(cudaMemcpyAsync(st + 2, off + R.n, sizeof(uint64_t), cudaMemcpyDeviceToDevice, ctx->stream));
+  unsigned long long h[3];
+  d2h_sync(ctx, h, st, sizeof(h));
+  tc.band_off = off;
+  tc.total = h[2];
+  tc.nlj_pairs = h[0];
+  tc.cross_pairs = h[1];
+}
+
+template <typename K>
+void band_region_write(gj_ctx* ctx, uint32_t* out) {
+  const ThetaCache& tc = ctx->tc;
+  BandArgs<K> a{};
+  a.rkey = static_cast<const K*>(tc.PR.key);
+  a.rrid = tc.PR.rid;
+  a.nR = tc.PR.n;
+  a.skey = static_cast<const K*>(tc.PS.key);
+  a.srid = tc.PS.rid;
+  a.so = tc.band_so;
+  a.P = tc.band_P;
+  a.sh = tc.band_sh;
+  a.m = tc.band_m;
+  a.g = tc.band_g;
+  a.lo = tc.band_lo;
+  a.eps = tc.eps;
+  a.off = tc.band_off;
+  a.out = reinterpret_cast<uint2*>(out);
+  const unsigned grid = (unsigned)std::min<uint64_t>((a.nR + 255) / 256, (uint64_t)ctx->num_sms * 8);
+  launch(ctx, "band_write", band_cells_kernel<K, true>, dim3(grid), dim3(256), 0, a);
+}
+
 template <typename K>
 void theta_count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S0, int op, uint64_t eps) {
   ThetaCache& tc = ctx->tc;
@@ -684,6 +894,7 @@ void theta_count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S0, int op, ui
   }
   tc.S = S;
   tc.regions = false;
+  tc.band = false;
   tc.nlj_pairs = tc.cross_pairs = 0;
   bool fast = (sizeof(K) == 4) && !ctx->force_slow_band;
   const bool regions = ctx->theta_regions != 0 && R.n < (1ull << 32) && S.n < (1ull << 32);
@@ -708,6 +919,7 @@ void theta_count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S0, int op, ui
     if (!(span + eps < (1ull << 32) && 2 * eps < (1ull << 32) - 1)) fast = false;
     if (ctx->force_slow_band) fast = false;
   }
+  if (regions && op == GJ_BAND) return band_region_count<K>(ctx, R, S, eps, lo, hi);
   if (regions) return region_count<K>(ctx, R, S, op, eps, lo, hi, fast);
   tc.mode = fast ? 1 : 0;
   tc.nlj_pairs = R.n * S.n;
@@ -741,6 +953,7 @@ void theta_write_impl(gj_ctx* ctx, uint32_t* out) {
   ThetaCache& tc = ctx->tc;
   if (tc.total == 0) return;
   if (tc.all_pairs) return cross_write(ctx, tc.R, tc.S, out);
+  if (tc.band) return band_region_write<K>(ctx, out);
   if (tc.regions) {
     if (tc.nlj_total) {
       uint32_t* work = static_cast<uint32_t*>(ws(ctx, "nlj.work", 16));
@@ -807,12 +1020,12 @@ void theta_write(gj_ctx* ctx, uint32_t* out) {
 
 }  // namespace gj
 
-extern "C" gj_status gj_region_classify(int op, uint32_t k, uint64_t m, uint8_t* cls) {
-  if (op < GJ_EQ || op > GJ_BAND || k == 0 || k > 4096 || !cls) {
+extern "C" gj_status gj_region_classify(int op, uint32_t k, uint64_t m, int64_t g, uint8_t* cls) {
+  if (op < GJ_EQ || op > GJ_BAND || k == 0 || k > 4096 || !cls || g < -1) {
     gj::set_last_error("gj_region_classify: bad arguments");
     return GJ_EINVAL;
   }
   for (uint64_t x = 0; x < k; ++x)
-    for (uint64_t y = 0; y < k; ++y) cls[x * k + y] = (uint8_t)gj::region_class(op, x, y, m);
+    for (uint64_t y = 0; y < k; ++y) cls[x * k + y] = (uint8_t)gj::region_class(op, x, y, m, g);
   return GJ_OK;
 }

@@ -84,6 +84,13 @@ struct ThetaCache {
   uint64_t nlj_pairs = 0, cross_pairs = 0;  // work of the count (gj_theta_stats)
   std::vector<uint4> rects;
   std::vector<uint64_t> rect_base;
+  // band on the region matrix (band_cells_kernel): bucket geometry, per-R-row offsets
+  bool band = false;
+  const uint32_t* band_so = nullptr;  // P + 1 S bucket starts
+  uint32_t band_P = 0, band_sh = 0, band_m = 0;
+  int32_t band_g = -1;
+  unsigned long long band_lo = 0;
+  const uint64_t* band_off = nullptr;
 };
 
 // Per-stream state of the single-pass scan: status words + ticket counter, the

@@ -65,13 +65,35 @@ def test_classes_are_sound_by_brute_force(op):
     S = rng.integers(0, k << sh, 500)
     eps = 11
     m = -(-eps // (1 << sh))
-    cls = gj.region_classify(op, k, m)
+    g = (eps + 1) // (1 << sh) - 1
+    cls = gj.region_classify(op, k, m, g)
     pred = {"eq": np.equal, "ne": np.not_equal, "lt": np.less, "le": np.less_equal, "gt": np.greater,
             "ge": np.greater_equal, "band": lambda a, b: np.abs(a - b) <= eps}[op]
     P = pred(R[:, None], S[None, :])
     cell = cls[(R >> sh)[:, None], (S >> sh)[None, :]]
     assert P[cell == GREEN].all()
     assert not P[cell == W].any()
+
+
+def test_band_green_cells():
+    """Band Green cells: with width w the farthest pair of cell (x, y) is
+    (|x-y| + 1) w - 1 apart, so |x - y| <= g = floor((eps + 1) / w) - 1 is all-match;
+    the nearest is (|x-y| - 1) w + 1, so |x - y| <= m = ceil(eps / w) can match.
+    configs[3]'s geometry (w = 4096, eps = 53687): g = 12, m = 14."""
+    w, eps = 4096, 53687
+    g, m = (eps + 1) // w - 1, -(-eps // w)
+    assert (g, m) == (12, 14)
+    b = gj.region_classify("band", 40, m=m, g=g)
+    assert list(b[20, 20 - 14:20 + 15]) == [RED, RED] + [GREEN] * 25 + [RED, RED]
+    assert b[20, 5] == W and b[20, 35] == W
+    # extreme pairs at the cell edges, brute force over every key of two buckets
+    for d, cls in ((12, GREEN), (13, RED), (14, RED), (15, W)):
+        lo_r, lo_s = 0, d * w
+        dmax = (lo_s + w - 1) - lo_r
+        dmin = lo_s - (lo_r + w - 1)
+        assert (cls == GREEN) == (dmax <= eps)
+        assert (cls == W) == (dmin > eps)
+    assert counts(gj.region_classify("band", 6, m=1, g=0)) == {"green": 6, "red": 10, "white": 20}
 
 
 def test_errors():

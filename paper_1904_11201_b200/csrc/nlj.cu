@@ -572,11 +572,11 @@ int region_class(int op, uint64_t x, uint64_t y, uint64_t m, int64_t g) {
 // w ~ eps / 8, so the Green cells (all pairs match) carry most of the output and the
 // Red ones are a thin rim: for the R row r in bucket x the S rows of buckets
 // [x - m, x + m] are one contiguous run of the partitioned S, the Green buckets
-// [x - g, x + g] one contiguous run inside it.  One warp per R row: the count pass
-// adds the Green run's length to the Red rows' matches (exact predicate, ballots of
-// 32 S keys); the write pass emits the row's pairs in partitioned-S order -- left
-// Red matches (ballot ranks), the Green run as coalesced 8-byte stores, right Red
-// matches -- at the row's scanned offset.
+// [x - g, x + g] one contiguous run inside it.  A warp handles one R row at a time:
+// the count pass adds the Green run's length to the Red rows' matches (exact
+// predicate, ballots of 32 S keys); the write pass emits the row's pairs in
+// partitioned-S order -- left Red matches (ballot ranks), the Green run as
+// coalesced 8-byte stores, right Red matches -- at the row's scanned offset.
 __device__ __forceinline__ int32_t shfl_key(int32_t v, uint32_t q) { return __shfl_sync(FULL, v, q); }
 __device__ __forceinline__ int64_t shfl_key(int64_t v, uint32_t q) {
   return (int64_t)__shfl_sync(FULL, (long long)v, q);
@@ -600,91 +600,134 @@ struct BandArgs {
   uint2* out;
 };
 
-template <typename K, bool WRITE>
-__global__ void __launch_bounds__(256) band_cells_kernel(BandArgs<K> a) {
+// S runs of the R row with key r (bucket x): Red [rb, gb) and [ge, re), Green [gb, ge)
+template <typename K>
+__device__ __forceinline__ void band_bounds(const BandArgs<K>& a, K r, uint32_t& rb, uint32_t& gb, uint32_t& ge,
+                                            uint32_t& re) {
+  const uint64_t x = (uint64_t)(KeyT<K>::bias(r) - a.lo) >> a.sh;
+  const uint64_t yl = x >= a.m ? x - a.m : 0, yh = min(x + a.m, (uint64_t)a.P - 1);
+  rb = a.so[yl];
+  re = a.so[yh + 1];
+  if (a.g >= 0) {
+    const uint64_t g = (uint64_t)a.g;
+    gb = a.so[x >= g ? x - g : 0];
+    ge = a.so[min(x + g, (uint64_t)a.P - 1) + 1];
+  } else {
+    gb = ge = a.so[x];
+  }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(256) band_count_kernel(BandArgs<K> a) {
   const uint32_t lane = lane_id();
   const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
   unsigned long long red_n = 0, green_n = 0;
-  // a warp takes 32 consecutive R rows: lane l fetches row l's key, rid, offset and
-  // bucket bounds (one dependent-load chain for 32 rows), then the warp walks the rows
+  // a warp takes 32 consecutive R rows: lane l fetches row l's key and bucket bounds
+  // (one dependent-load chain for 32 rows), then the warp walks the rows
   for (uint64_t row0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; row0 < a.nR;
        row0 += nwarps * 32) {
     const uint64_t myrow = row0 + lane;
     const bool have = myrow < a.nR;
     K mykey = have ? a.rkey[myrow] : K(0);
     uint32_t rb = 0, gb = 0, ge = 0, re = 0;  // Red [rb, gb) and [ge, re), Green [gb, ge)
-    if (have) {
-      const uint64_t x = (uint64_t)(KeyT<K>::bias(mykey) - a.lo) >> a.sh;
-      const uint64_t yl = x >= a.m ? x - a.m : 0, yh = min(x + a.m, (uint64_t)a.P - 1);
-      rb = a.so[yl];
-      re = a.so[yh + 1];
-      if (a.g >= 0) {
-        const uint64_t g = (uint64_t)a.g;
-        gb = a.so[x >= g ? x - g : 0];
-        ge = a.so[min(x + g, (uint64_t)a.P - 1) + 1];
-      } else {
-        gb = ge = a.so[x];
-      }
-    }
-    uint32_t myrid = 0;
-    uint64_t myoff = 0;
-    if (WRITE && have) {
-      myrid = a.rrid[myrow];
-      myoff = a.off[myrow];
-    }
+    if (have) band_bounds(a, mykey, rb, gb, ge, re);
     const uint32_t nr = (uint32_t)min((uint64_t)32, a.nR - row0);
     uint32_t mycnt = 0;
     for (uint32_t q = 0; q < nr; ++q) {
       const K r = shfl_key(mykey, q);
       const uint32_t qrb = __shfl_sync(FULL, rb, q), qgb = __shfl_sync(FULL, gb, q);
       const uint32_t qge = __shfl_sync(FULL, ge, q), qre = __shfl_sync(FULL, re, q);
-      if (!WRITE) {
-        uint32_t c = 0;
-        auto red = [&](uint32_t b, uint32_t e) {
+      uint32_t c = 0;
+      auto red = [&](uint32_t b, uint32_t e) {
 #pragma unroll 4
-          for (uint32_t j0 = b; j0 < e; j0 += 32) {
-            const uint32_t j = j0 + lane;
-            c += __popc(__ballot_sync(FULL, j < e && theta_exact<K, GJ_BAND>(r, a.skey[j], a.eps)));
-          }
-        };
-        red(qrb, qgb);
-        red(qge, qre);
-        if (lane == q) mycnt = c + (qge - qgb);
-        if (lane == 0) {
-          red_n += (qgb - qrb) + (qre - qge);
-          green_n += qge - qgb;
+        for (uint32_t j0 = b; j0 < e; j0 += 32) {
+          const uint32_t j = j0 + lane;
+          c += __popc(__ballot_sync(FULL, j < e && theta_exact<K, GJ_BAND>(r, a.skey[j], a.eps)));
         }
+      };
+      red(qrb, qgb);
+      red(qge, qre);
+      if (lane == q) mycnt = c + (qge - qgb);
+      if (lane == 0) {
+        red_n += (qgb - qrb) + (qre - qge);
+        green_n += qge - qgb;
+      }
+    }
+    if (have) a.cnt[myrow] = mycnt;
+  }
+  red_n = warp_sum(red_n);
+  green_n = warp_sum(green_n);
+  if (lane == 0 && (red_n | green_n)) {
+    atomicAdd(&a.stats[0], red_n);
+    atomicAdd(&a.stats[1], green_n);
+  }
+}
+
+// Write pass: a CTA takes 256 consecutive R rows (8 warps x 32); their S windows
+// are nested intervals of the partitioned S (bucket order), so the batch's Green
+// runs all lie in [rb of its first row, re of its last row) -- ~5.9K S rows at
+// configs[3] -- whose rids are staged in shared memory once (coalesced loads), and
+// the Green loop reads them there: without it every S rid was fetched from L2 by
+// ~100 R rows and, evicted by the streaming output, ~18 times from DRAM.  A batch
+// whose window exceeds BW_CAP (skewed keys) reads the rids from global memory.
+constexpr uint32_t BW_ROWS = 256, BW_CAP = 6144;
+template <typename K>
+__global__ void __launch_bounds__(BW_ROWS) band_write_kernel(BandArgs<K> a) {
+  __shared__ uint32_t s_rid[BW_CAP];
+  __shared__ uint32_t s_win[2];
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+  for (uint64_t row0 = (uint64_t)blockIdx.x * BW_ROWS; row0 < a.nR; row0 += (uint64_t)gridDim.x * BW_ROWS) {
+    const uint64_t myrow = row0 + threadIdx.x;
+    const bool have = myrow < a.nR;
+    K mykey = have ? a.rkey[myrow] : K(0);
+    uint32_t rb = 0, gb = 0, ge = 0, re = 0, myrid = 0;
+    uint64_t myoff = 0;
+    if (have) {
+      band_bounds(a, mykey, rb, gb, ge, re);
+      myrid = a.rrid[myrow];
+      myoff = a.off[myrow];
+    }
+    const uint32_t nrows = (uint32_t)min((uint64_t)BW_ROWS, a.nR - row0);
+    if (threadIdx.x == 0) s_win[0] = gb;                // Green runs: nondecreasing starts
+    if (threadIdx.x == nrows - 1) s_win[1] = ge;        // ... and ends
+    __syncthreads();
+    const uint32_t wlo = s_win[0], wn = s_win[1] - s_win[0];
+    const bool staged = wn <= BW_CAP;  // CTA-uniform
+    if (staged)
+      for (uint32_t i = threadIdx.x; i < wn; i += BW_ROWS) s_rid[i] = a.srid[wlo + i];
+    __syncthreads();
+    const uint32_t nr = min(32u, nrows > 32 * w ? nrows - 32 * w : 0u);
+    for (uint32_t q = 0; q < nr; ++q) {
+      const K r = shfl_key(mykey, q);
+      const uint32_t qrb = __shfl_sync(FULL, rb, q), qgb = __shfl_sync(FULL, gb, q);
+      const uint32_t qge = __shfl_sync(FULL, ge, q), qre = __shfl_sync(FULL, re, q);
+      const uint32_t rr = __shfl_sync(FULL, myrid, q);
+      uint64_t o = __shfl_sync(FULL, myoff, q);
+      auto red = [&](uint32_t b, uint32_t e) {
+        for (uint32_t j0 = b; j0 < e; j0 += 32) {
+          const uint32_t j = j0 + lane;
+          const bool p = j < e && theta_exact<K, GJ_BAND>(r, a.skey[j], a.eps);
+          const uint32_t bal = __ballot_sync(FULL, p);
+          if (p) a.out[o + __popc(bal & lanemask_lt())] = make_uint2(rr, a.srid[j]);
+          o += __popc(bal);
+        }
+      };
+      red(qrb, qgb);
+      const uint32_t gn = qge - qgb;
+      uint2* go = a.out + o;
+      if (staged) {
+        const uint32_t* gs = s_rid + (qgb - wlo);
+#pragma unroll 4
+        for (uint32_t i = lane; i < gn; i += 32) go[i] = make_uint2(rr, gs[i]);
       } else {
-        const uint32_t rr = __shfl_sync(FULL, myrid, q);
-        uint64_t o = __shfl_sync(FULL, myoff, q);
-        auto red = [&](uint32_t b, uint32_t e) {
-          for (uint32_t j0 = b; j0 < e; j0 += 32) {
-            const uint32_t j = j0 + lane;
-            const bool p = j < e && theta_exact<K, GJ_BAND>(r, a.skey[j], a.eps);
-            const uint32_t bal = __ballot_sync(FULL, p);
-            if (p) a.out[o + __popc(bal & lanemask_lt())] = make_uint2(rr, a.srid[j]);
-            o += __popc(bal);
-          }
-        };
-        red(qrb, qgb);
-        const uint32_t gn = qge - qgb;
-        uint2* go = a.out + o;
         const uint32_t* gs = a.srid + qgb;
 #pragma unroll 4
         for (uint32_t i = lane; i < gn; i += 32) go[i] = make_uint2(rr, gs[i]);
-        o += gn;
-        red(qge, qre);
       }
+      o += gn;
+      red(qge, qre);
     }
-    if (!WRITE && have) a.cnt[myrow] = mycnt;
-  }
-  if (!WRITE) {
-    red_n = warp_sum(red_n);
-    green_n = warp_sum(green_n);
-    if (lane == 0 && (red_n | green_n)) {
-      atomicAdd(&a.stats[0], red_n);
-      atomicAdd(&a.stats[1], green_n);
-    }
+    __syncthreads();  // the window is refilled by the next batch
   }
 }
 
@@ -791,7 +834,7 @@ void region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, int op, uint64_
   tc.cross_pairs = cross;
 }
 
-// Band join on the region matrix with Green cells (band_cells_kernel): buckets of
+// Band join on the region matrix with Green cells (band_count_kernel, band_write_kernel): buckets of
 // width 2^sh ~ eps / 8 (at most 2^18 of them), so ~90% of a row's pairs fall in Green
 // cells when the keys are spread over the buckets (configs[3]: w = 4096, g = 12,
 // m = 14 -- 25 Green and 4 Red S buckets per R row).
@@ -843,7 +886,7 @@ void band_region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint64_t e
   a.cnt = cnt;
   a.stats = st;
   const unsigned grid = (unsigned)std::min<uint64_t>((R.n + 255) / 256, (uint64_t)ctx->num_sms * 8);
-  launch(ctx, "band_count", band_cells_kernel<K, false>, dim3(grid), dim3(256), 0, a);
+  launch(ctx, "band_count", band_count_kernel<K>, dim3(grid), dim3(256), 0, a);
   exclusive_scan<uint32_t, uint64_t>(ctx, cnt, off, R.n, off + R.n);
   GJ_CUDA(cudaMemcpyAsync(st + 2, off + R.n, sizeof(uint64_t), cudaMemcpyDeviceToDevice, ctx->stream));
   unsigned long long h[3];
@@ -872,8 +915,8 @@ void band_region_write(gj_ctx* ctx, uint32_t* out) {
   a.eps = tc.eps;
   a.off = tc.band_off;
   a.out = reinterpret_cast<uint2*>(out);
-  const unsigned grid = (unsigned)std::min<uint64_t>((a.nR + 255) / 256, (uint64_t)ctx->num_sms * 8);
-  launch(ctx, "band_write", band_cells_kernel<K, true>, dim3(grid), dim3(256), 0, a);
+  const unsigned grid = (unsigned)std::min<uint64_t>((a.nR + BW_ROWS - 1) / BW_ROWS, (uint64_t)ctx->num_sms * 8);
+  launch(ctx, "band_write", band_write_kernel<K>, dim3(grid), dim3(BW_ROWS), 0, a);
 }
 
 template <typename K>

@@ -600,6 +600,18 @@ struct BandArgs {
   uint2* out;
 };
 
+// |r - s| <= eps.  FAST (int32, span + eps < 2^32, 2 eps < 2^32 - 1 -- DESIGN.md
+// reading R5): t = (r + eps) - s mod 2^32 on biased keys, match <=> t <= 2 eps (two
+// ALU ops); else the exact 64-bit difference.
+template <typename K, bool FAST>
+__device__ __forceinline__ bool band_match(K r, K s, uint64_t eps) {
+  if constexpr (FAST && sizeof(K) == 4) {
+    return (KeyT<K>::bias(r) + (uint32_t)eps) - KeyT<K>::bias(s) <= 2u * (uint32_t)eps;
+  } else {
+    return theta_exact<K, GJ_BAND>(r, s, eps);
+  }
+}
+
 // S runs of the R row with key r (bucket x): Red [rb, gb) and [ge, re), Green [gb, ge)
 template <typename K>
 __device__ __forceinline__ void band_bounds(const BandArgs<K>& a, K r, uint32_t& rb, uint32_t& gb, uint32_t& ge,
@@ -617,7 +629,7 @@ __device__ __forceinline__ void band_bounds(const BandArgs<K>& a, K r, uint32_t&
   }
 }
 
-template <typename K>
+template <typename K, bool FAST>
 __global__ void __launch_bounds__(256) band_count_kernel(BandArgs<K> a) {
   const uint32_t lane = lane_id();
   const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
@@ -642,7 +654,7 @@ __global__ void __launch_bounds__(256) band_count_kernel(BandArgs<K> a) {
 #pragma unroll 4
         for (uint32_t j0 = b; j0 < e; j0 += 32) {
           const uint32_t j = j0 + lane;
-          c += __popc(__ballot_sync(FULL, j < e && theta_exact<K, GJ_BAND>(r, a.skey[j], a.eps)));
+          c += __popc(__ballot_sync(FULL, j < e && band_match<K, FAST>(r, a.skey[j], a.eps)));
         }
       };
       red(qrb, qgb);
@@ -663,17 +675,23 @@ __global__ void __launch_bounds__(256) band_count_kernel(BandArgs<K> a) {
   }
 }
 
-// Write pass: a CTA takes 256 consecutive R rows (8 warps x 32); their S windows
-// are nested intervals of the partitioned S (bucket order), so the batch's Green
-// runs all lie in [rb of its first row, re of its last row) -- ~5.9K S rows at
-// configs[3] -- whose rids are staged in shared memory once (coalesced loads), and
-// the Green loop reads them there: without it every S rid was fetched from L2 by
-// ~100 R rows and, evicted by the streaming output, ~18 times from DRAM.  A batch
-// whose window exceeds BW_CAP (skewed keys) reads the rids from global memory.
+// Write pass: a CTA takes 256 consecutive R rows (8 warps x 32).  Their S runs are
+// nested intervals of the partitioned S (bucket order), so the batch reads only S
+// rows [rb of its first row, re of its last row) -- ~5.9K at configs[3] -- whose keys
+// and rids are staged in shared memory once (coalesced loads); the rows' Red
+// compares and Green copies then read shared memory only.  Without it every S rid
+// was fetched by ~100 R rows from L2 and, evicted by the streaming output, ~18 times
+// from DRAM.  A batch whose window exceeds BW_CAP (skewed keys) reads global memory.
+// Green runs leave as 16-byte stores (two pairs per lane).
 constexpr uint32_t BW_ROWS = 256, BW_CAP = 6144;
 template <typename K>
+constexpr size_t band_write_smem() { return (size_t)BW_CAP * (sizeof(K) + 4); }
+
+template <typename K, bool FAST>
 __global__ void __launch_bounds__(BW_ROWS) band_write_kernel(BandArgs<K> a) {
-  __shared__ uint32_t s_rid[BW_CAP];
+  extern __shared__ __align__(16) uint8_t smem[];
+  K* s_key = reinterpret_cast<K*>(smem);
+  uint32_t* s_rid = reinterpret_cast<uint32_t*>(smem + (size_t)BW_CAP * sizeof(K));
   __shared__ uint32_t s_win[2];
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
   for (uint64_t row0 = (uint64_t)blockIdx.x * BW_ROWS; row0 < a.nR; row0 += (uint64_t)gridDim.x * BW_ROWS) {
@@ -688,15 +706,21 @@ __global__ void __launch_bounds__(BW_ROWS) band_write_kernel(BandArgs<K> a) {
       myoff = a.off[myrow];
     }
     const uint32_t nrows = (uint32_t)min((uint64_t)BW_ROWS, a.nR - row0);
-    if (threadIdx.x == 0) s_win[0] = gb;                // Green runs: nondecreasing starts
-    if (threadIdx.x == nrows - 1) s_win[1] = ge;        // ... and ends
+    if (threadIdx.x == 0) s_win[0] = rb;          // S runs: nondecreasing starts
+    if (threadIdx.x == nrows - 1) s_win[1] = re;  // ... and ends
     __syncthreads();
     const uint32_t wlo = s_win[0], wn = s_win[1] - s_win[0];
     const bool staged = wn <= BW_CAP;  // CTA-uniform
     if (staged)
-      for (uint32_t i = threadIdx.x; i < wn; i += BW_ROWS) s_rid[i] = a.srid[wlo + i];
+      for (uint32_t i = threadIdx.x; i < wn; i += BW_ROWS) {
+        s_key[i] = a.skey[wlo + i];
+        s_rid[i] = a.srid[wlo + i];
+      }
     __syncthreads();
     const uint32_t nr = min(32u, nrows > 32 * w ? nrows - 32 * w : 0u);
+    // kk, rd: the window-relative shared arrays, or the global ones -- two inlined
+    // copies, so the staged loads compile to LDS, not generic loads
+    auto rows = [&](const K* kk, const uint32_t* rd) {
     for (uint32_t q = 0; q < nr; ++q) {
       const K r = shfl_key(mykey, q);
       const uint32_t qrb = __shfl_sync(FULL, rb, q), qgb = __shfl_sync(FULL, gb, q);
@@ -706,27 +730,30 @@ __global__ void __launch_bounds__(BW_ROWS) band_write_kernel(BandArgs<K> a) {
       auto red = [&](uint32_t b, uint32_t e) {
         for (uint32_t j0 = b; j0 < e; j0 += 32) {
           const uint32_t j = j0 + lane;
-          const bool p = j < e && theta_exact<K, GJ_BAND>(r, a.skey[j], a.eps);
+          const bool p = j < e && band_match<K, FAST>(r, kk[j], a.eps);
           const uint32_t bal = __ballot_sync(FULL, p);
-          if (p) a.out[o + __popc(bal & lanemask_lt())] = make_uint2(rr, a.srid[j]);
+          if (p) a.out[o + __popc(bal & lanemask_lt())] = make_uint2(rr, rd[j]);
           o += __popc(bal);
         }
       };
       red(qrb, qgb);
       const uint32_t gn = qge - qgb;
       uint2* go = a.out + o;
-      if (staged) {
-        const uint32_t* gs = s_rid + (qgb - wlo);
+      const uint32_t* gs = rd + qgb;
+      // head element up to the 16-byte boundary (out is 8-byte aligned), pairs, tail
+      const uint32_t head = min(gn, (uint32_t)(reinterpret_cast<uintptr_t>(go) >> 3) & 1u);
+      const uint32_t n2 = (gn - head) >> 1;
+      if (lane == 0 && head) go[0] = make_uint2(rr, gs[0]);
+      uint4* g4 = reinterpret_cast<uint4*>(go + head);
 #pragma unroll 4
-        for (uint32_t i = lane; i < gn; i += 32) go[i] = make_uint2(rr, gs[i]);
-      } else {
-        const uint32_t* gs = a.srid + qgb;
-#pragma unroll 4
-        for (uint32_t i = lane; i < gn; i += 32) go[i] = make_uint2(rr, gs[i]);
-      }
+      for (uint32_t i = lane; i < n2; i += 32) g4[i] = make_uint4(rr, gs[head + 2 * i], rr, gs[head + 2 * i + 1]);
+      if (lane == 0 && head + 2 * n2 < gn) go[gn - 1] = make_uint2(rr, gs[gn - 1]);
       o += gn;
       red(qge, qre);
     }
+    };
+    if (staged) rows(s_key - wlo, s_rid - wlo);
+    else rows(a.skey, a.srid);
     __syncthreads();  // the window is refilled by the next batch
   }
 }
@@ -840,7 +867,7 @@ void region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, int op, uint64_
 // m = 14 -- 25 Green and 4 Red S buckets per R row).
 template <typename K>
 void band_region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint64_t eps, unsigned long long lo,
-                       unsigned long long hi) {
+                       unsigned long long hi, bool fast) {
   ThetaCache& tc = ctx->tc;
   const unsigned long long span = hi - lo;
   const uint32_t L = span ? 64 - (uint32_t)__builtin_clzll(span) : 1;
@@ -858,6 +885,7 @@ void band_region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint64_t e
   const int32_t g = gg == 0 ? -1 : (int32_t)std::min<unsigned __int128>(gg - 1, P);
   tc.regions = true;
   tc.band = true;
+  tc.mode = fast ? 1 : 0;
   tc.PR = gj_rel{PR.key, PR.rid, R.n, R.key_type, 0};
   tc.PS = gj_rel{PS.key, PS.rid, S.n, S.key_type, 0};
   tc.band_so = PS.off;
@@ -886,7 +914,10 @@ void band_region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint64_t e
   a.cnt = cnt;
   a.stats = st;
   const unsigned grid = (unsigned)std::min<uint64_t>((R.n + 255) / 256, (uint64_t)ctx->num_sms * 8);
-  launch(ctx, "band_count", band_count_kernel<K>, dim3(grid), dim3(256), 0, a);
+  if (fast)
+    launch(ctx, "band_count", band_count_kernel<K, true>, dim3(grid), dim3(256), 0, a);
+  else
+    launch(ctx, "band_count", band_count_kernel<K, false>, dim3(grid), dim3(256), 0, a);
   exclusive_scan<uint32_t, uint64_t>(ctx, cnt, off, R.n, off + R.n);
   GJ_CUDA(cudaMemcpyAsync(st + 2, off + R.n, sizeof(uint64_t), cudaMemcpyDeviceToDevice, ctx->stream));
   unsigned long long h[3];
@@ -916,7 +947,14 @@ void band_region_write(gj_ctx* ctx, uint32_t* out) {
   a.off = tc.band_off;
   a.out = reinterpret_cast<uint2*>(out);
   const unsigned grid = (unsigned)std::min<uint64_t>((a.nR + BW_ROWS - 1) / BW_ROWS, (uint64_t)ctx->num_sms * 8);
-  launch(ctx, "band_write", band_write_kernel<K>, dim3(grid), dim3(BW_ROWS), 0, a);
+  const size_t smem = band_write_smem<K>();
+  if (tc.mode == 1) {
+    set_smem(ctx, band_write_kernel<K, true>, smem);
+    launch(ctx, "band_write", band_write_kernel<K, true>, dim3(grid), dim3(BW_ROWS), smem, a);
+  } else {
+    set_smem(ctx, band_write_kernel<K, false>, smem);
+    launch(ctx, "band_write", band_write_kernel<K, false>, dim3(grid), dim3(BW_ROWS), smem, a);
+  }
 }
 
 template <typename K>
@@ -962,7 +1000,7 @@ void theta_count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S0, int op, ui
     if (!(span + eps < (1ull << 32) && 2 * eps < (1ull << 32) - 1)) fast = false;
     if (ctx->force_slow_band) fast = false;
   }
-  if (regions && op == GJ_BAND) return band_region_count<K>(ctx, R, S, eps, lo, hi);
+  if (regions && op == GJ_BAND) return band_region_count<K>(ctx, R, S, eps, lo, hi, fast);
   if (regions) return region_count<K>(ctx, R, S, op, eps, lo, hi, fast);
   tc.mode = fast ? 1 : 0;
   tc.nlj_pairs = R.n * S.n;

@@ -45,6 +45,7 @@ sys.path.insert(0, ROOT)
 S_BITS_C4 = 24  # set from --c4-s-bits
 C5_BITS = 28  # set from --c5-bits
 C3_WEAK = False  # set from --c3-weak
+C2_SPARSE = False  # set from --c2-sparse
 METRIC = "join input & output tuples/s at 1/2/4/8 B200; % of HBM/INT roofline"
 
 
@@ -159,11 +160,16 @@ def make_workload(name, device, rank=0, world=1):
     g = max(world.bit_length() - 1, 0)
     if name == "c2":
         n = 1 << 27  # per GPU
-        b = 27 + g
-        R = gd.perm_range(n, b, seed, offset=rank * n, device=device)
-        S = gd.pkfk_S(n, b, seed, offset=rank * n, device=device)
+        if C2_SPARSE:  # R = 2^27 x N distinct keys drawn from a permutation of [0, 2^31)
+            b = 31
+            R = gd.perm_range(n, b, seed, offset=rank * n, device=device)
+            S = gd.pkfk_S(n, b, seed, offset=rank * n, device=device, domain=n * world)
+        else:  # R = a permutation of [0, 2^(27 + log2 N)) (dense keys)
+            b = 27 + g
+            R = gd.perm_range(n, b, seed, offset=rank * n, device=device)
+            S = gd.pkfk_S(n, b, seed, offset=rank * n, device=device)
         desc = ("configs[1]: equi hash join 2^27 x 2^27 8-byte tuples (int32 key+payload, payload not read), "
-                "PK-FK unique R keys")
+                "PK-FK unique R keys" + (" drawn from [0, 2^31) (--c2-sparse)" if C2_SPARSE else ""))
         if world > 1:
             desc += f"; weak scaling: {world} ranks x (2^27 x 2^27) block shards, NCCL hash shuffle + local join"
         return dict(kind="equi", R=R, S=S, desc=desc, rid_base_R=rank * n, rid_base=rank * n, n_out_expected=n)
@@ -626,6 +632,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--c3-weak", action="store_true", help="c3: 2^25 x 2^27 per GPU (weak) instead of 2^28 x 2^30 total")
+    ap.add_argument("--c2-sparse", action="store_true",
+                    help="c2: R keys drawn from a permutation of [0, 2^31) instead of [0, 2^(27+log2 N))")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-sample-bits", type=int, default=23)
@@ -634,10 +642,11 @@ def main():
     ap.add_argument("--c5-bits", type=int, default=28, help="log2 |R| per GPU for c5 (|S| = 2|R|; 28 at N=8 = configs[4])")
     ap.add_argument("--opt", action="append", default=[], help="ctx option name=value (tuning sweeps)")
     args = ap.parse_args()
-    global S_BITS_C4, C5_BITS, C3_WEAK
+    global S_BITS_C4, C5_BITS, C3_WEAK, C2_SPARSE
     S_BITS_C4 = args.c4_s_bits
     C5_BITS = args.c5_bits
     C3_WEAK = args.c3_weak
+    C2_SPARSE = args.c2_sparse
     world, rank, local = dist_setup(args)
 
     if args.impl == "reference":

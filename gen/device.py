@@ -65,10 +65,13 @@ def perm_range(n, b, seed, offset=0, mult=1, dtype=torch.int32, device="cuda"):
     return out
 
 
-def pkfk_S(n, b, seed, offset=0, device="cuda"):
+def pkfk_S(n, b, seed, offset=0, device="cuda", domain=None):
+    """S FK draws: perm_b(rank), rank uniform in [0, domain) (default 2^b, i.e. the
+    keys of perm_range(2^b, b)); domain = |R| for R = perm_range(|R|, b) with b > log2|R|."""
     out = torch.empty(n, dtype=torch.int32, device=device)
     mask, sh, c = _perm(b, seed)
-    _ok(lib().gjgen_pkfk(ctypes.c_void_p(out.data_ptr()), n, mask, sh, c, 1 << b, int(stream_key(seed, 1)),
+    D = (1 << b) if domain is None else domain
+    _ok(lib().gjgen_pkfk(ctypes.c_void_p(out.data_ptr()), n, mask, sh, c, D, int(stream_key(seed, 1)),
                          offset, _stream()))
     return out
 

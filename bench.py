@@ -46,6 +46,7 @@ S_BITS_C4 = 24  # set from --c4-s-bits
 C5_BITS = 28  # set from --c5-bits
 C3_WEAK = False  # set from --c3-weak
 C2_SPARSE = False  # set from --c2-sparse
+C4_SKEW = False  # set from --c4-skew
 METRIC = "join input & output tuples/s at 1/2/4/8 B200; % of HBM/INT roofline"
 
 
@@ -197,13 +198,29 @@ def make_workload(name, device, rank=0, world=1):
     if name == "c4":
         nr = (1 << 20) // world  # R (2^20) is block-sharded and replicated by the join
         ns = 1 << S_BITS_C4      # per GPU (2^24 = configs[3]; smaller only for ncu captures)
-        R = gd.uniform(nr, 1 << 30, seed, 0, offset=rank * nr, device=device)
-        S = gd.uniform(ns, 1 << 30, seed, 1, offset=rank * ns, device=device)
-        desc = (f"configs[3]: band join |R.a-S.b|<=53687, 2^20 x 2^{S_BITS_C4} uniform int32 in [0,2^30), "
-                "count+scan+write; region matrix (PAPER.md §4.2 Alg.3) unless --opt theta_regions=0")
+        if C4_SKEW:
+            # skewed keys: cluster z ~ Zipf(1) over 4096 clusters (permuted ids) spaced
+            # 2^18 apart in [0, 2^30), key = 2^18 z + uniform [0, 2^15); eps = 16 keeps
+            # the output near 3.7e8 pairs.  The hot cluster (11% of each side) packs
+            # ~235K S rows into one 4096-wide bucket: equal-width buckets (reading R15)
+            # stop pruning there.
+            zt = gd.zipf_table_device(1 << 12, device=device)
+            R = gd.zipf_S(nr, 12, zt, seed, offset=rank * nr, device=device) * (1 << 18) + \
+                gd.uniform(nr, 1 << 15, seed, 2, offset=rank * nr, device=device)
+            S = gd.zipf_S(ns, 12, zt, seed + 1, offset=rank * ns, device=device) * (1 << 18) + \
+                gd.uniform(ns, 1 << 15, seed, 3, offset=rank * ns, device=device)
+            eps = 16
+            desc = (f"configs[3] shape, skewed (--c4-skew): band join |R.a-S.b|<=16, 2^20 x 2^{S_BITS_C4} int32 "
+                    "keys in Zipf(1)-weighted clusters (4096 clusters 2^18 apart, 2^15 wide), count+scan+write")
+        else:
+            R = gd.uniform(nr, 1 << 30, seed, 0, offset=rank * nr, device=device)
+            S = gd.uniform(ns, 1 << 30, seed, 1, offset=rank * ns, device=device)
+            eps = gen.C4_EPS
+            desc = (f"configs[3]: band join |R.a-S.b|<=53687, 2^20 x 2^{S_BITS_C4} uniform int32 in [0,2^30), "
+                    "count+scan+write; region matrix (PAPER.md §4.2 Alg.3) unless --opt theta_regions=0")
         if world > 1:
             desc += f"; weak scaling: R (2^20) all-gathered, {world} x 2^24 S shards"
-        return dict(kind="band", R=R, S=S, eps=gen.C4_EPS, desc=desc, rid_base_R=rank * nr, rid_base=rank * ns)
+        return dict(kind="band", R=R, S=S, eps=eps, desc=desc, rid_base_R=rank * nr, rid_base=rank * ns)
     if name == "c5":
         nr, ns = 1 << C5_BITS, 1 << (C5_BITS + 1)  # per GPU; 2^28 x 2^29 at N=8 = 2^31 x 2^32 = configs[4]
         b = C5_BITS + g
@@ -632,6 +649,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--c3-weak", action="store_true", help="c3: 2^25 x 2^27 per GPU (weak) instead of 2^28 x 2^30 total")
+    ap.add_argument("--c4-skew", action="store_true", help="c4: Zipf-clustered keys, eps = 16 (a perf point)")
     ap.add_argument("--c2-sparse", action="store_true",
                     help="c2: R keys drawn from a permutation of [0, 2^31) instead of [0, 2^(27+log2 N))")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -642,11 +660,12 @@ def main():
     ap.add_argument("--c5-bits", type=int, default=28, help="log2 |R| per GPU for c5 (|S| = 2|R|; 28 at N=8 = configs[4])")
     ap.add_argument("--opt", action="append", default=[], help="ctx option name=value (tuning sweeps)")
     args = ap.parse_args()
-    global S_BITS_C4, C5_BITS, C3_WEAK, C2_SPARSE
+    global S_BITS_C4, C5_BITS, C3_WEAK, C2_SPARSE, C4_SKEW
     S_BITS_C4 = args.c4_s_bits
     C5_BITS = args.c5_bits
     C3_WEAK = args.c3_weak
     C2_SPARSE = args.c2_sparse
+    C4_SKEW = args.c4_skew
     world, rank, local = dist_setup(args)
 
     if args.impl == "reference":

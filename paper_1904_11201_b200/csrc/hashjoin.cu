@@ -575,8 +575,6 @@ __global__ void __launch_bounds__(HT, 4) hj_count_i32(HJArgs a, uint16_t* __rest
   // register prefetch: two build and two probe vectors per thread (all of a ~2040-row
   // unit; the few extra vectors of larger units are loaded when needed)
   uint4 bv0 = tid < P.sb.nv ? ldv(P.sb, tid) : zero, bv1 = tid + HT < P.sb.nv ? ldv(P.sb, tid + HT) : zero;
-  uint4 pv0 = P.vb + lane < P.ve ? ldv(P.sp, P.vb + lane) : zero;
-  uint4 pv1 = P.vb + lane + 32 < P.ve ? ldv(P.sp, P.vb + lane + 32) : zero;
   bool built = false;  // the table holds d's build chunk
   for (uint32_t i = 0; i < n; ++i) {
     const uint32_t u = u0 + i;
@@ -590,9 +588,10 @@ __global__ void __launch_bounds__(HT, 4) hj_count_i32(HJArgs a, uint16_t* __rest
     const UnitPlan PN = plan_unit(a, dn, w);
     const uint4 nb0 = !keep && tid < PN.sb.nv ? ldv(PN.sb, tid) : zero;
     const uint4 nb1 = !keep && tid + HT < PN.sb.nv ? ldv(PN.sb, tid + HT) : zero;
-    const uint4 np0 = PN.vb + lane < PN.ve ? ldv(PN.sp, PN.vb + lane) : zero;
-    const uint4 np1 = PN.vb + lane + 32 < PN.ve ? ldv(PN.sp, PN.vb + lane + 32) : zero;
 
+    // this unit's first two probe vectors per lane: in flight while the table is built
+    const uint4 pv0 = P.vb + lane < P.ve ? ldv(P.sp, P.vb + lane) : zero;
+    const uint4 pv1 = P.vb + lane + 32 < P.ve ? ldv(P.sp, P.vb + lane + 32) : zero;
     const uint32_t bn = d.y, pn = d.w;
     const uint32_t logT = min(max(32 - __clz(4 * bn - 1), 5u), 13u);  // ~4 slots per build row
     const uint32_t T = 1u << logT, tmask = T - 1, tshift = 32 - logT;
@@ -632,7 +631,6 @@ __global__ void __launch_bounds__(HT, 4) hj_count_i32(HJArgs a, uint16_t* __rest
     d = dn;
     P = PN;
     if (!keep) bv0 = nb0, bv1 = nb1;
-    pv0 = np0, pv1 = np1;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");  // no copy outstanding at exit
 }

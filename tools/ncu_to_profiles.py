@@ -35,6 +35,8 @@ TAGS = [
     (r"hj_write_fast", "hj_write"),
     (r"hj_write_kernel", "hj_write_multi"),
     (r"cross_rect", "cross_rect"),
+    (r"band_write_kernel", "band_write"),
+    (r"band_count_kernel", "band_count"),
     (r"nlj_kernel<[^>]*, (true|1)>", "nlj_write"),
     (r"nlj_kernel<[^>]*, (false|0)>", "nlj_count"),
     (r"pf_count", "pf_count"),

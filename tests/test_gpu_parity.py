@@ -691,6 +691,42 @@ def test_theta_regions_all_ops(gj, ctx, kind, op):
         check_theta(gj, ctx, R, S, op, eps, materialize=True)
 
 
+@pytest.mark.parametrize("eps", [0, 1, 7, 8, 9, 63, 4096, 100_000, 2**24])
+def test_band_region_geometry(gj, ctx, eps):
+    """The band's region-matrix path (bucket width ~eps/8: Green radius g, Red radius
+    m, reading R17) over widths from 1 (eps < 8) to Green runs spanning many buckets:
+    every pair vs the oracle, int32 keys over a 2^25 range with a dense cluster."""
+    rng = np.random.default_rng(100 + eps % 97)
+    R = np.concatenate([rng.integers(-2**24, 2**24, 6000), rng.integers(0, 3000, 1500)]).astype(np.int32)
+    S = np.concatenate([rng.integers(-2**24, 2**24, 14000), rng.integers(0, 3000, 4000)]).astype(np.int32)
+    ctx.set_option("theta_regions", 1)
+    n = check_theta(gj, ctx, R, S, "band", eps, materialize=False)
+    if n <= 40_000_000:
+        check_theta(gj, ctx, R, S, "band", eps, materialize=True)
+
+
+def test_band_write_unstaged_window(gj, ctx):
+    """A 256-row batch of the band write pass whose S window exceeds the shared staging
+    capacity (6144 rows: here all of S sits in a few buckets next to every R row)
+    reads S from global memory -- same pairs as the oracle."""
+    rng = np.random.default_rng(77)
+    R = rng.integers(1000, 1040, 700).astype(np.int32)
+    S = rng.integers(990, 1050, 20000).astype(np.int32)
+    S[:5] = [-2**20, 2**20, 0, 5000, -5000]  # widen the span so the buckets are narrow
+    ctx.set_option("theta_regions", 1)
+    check_theta(gj, ctx, R, S, "band", 3, materialize=True)
+
+
+@pytest.mark.parametrize("eps", [0, 5, 2**33])
+def test_band_region_int64(gj, ctx, eps):
+    """int64 keys take the band path with the exact 64-bit predicate."""
+    rng = np.random.default_rng(55)
+    R = rng.integers(-2**40, 2**40, 3000).astype(np.int64)
+    S = np.concatenate([rng.integers(-2**40, 2**40, 9000), R[:2000] + rng.integers(-9, 9, 2000)]).astype(np.int64)
+    ctx.set_option("theta_regions", 1)
+    check_theta(gj, ctx, R, S, "band", eps, materialize=True)
+
+
 @pytest.mark.parametrize("op", OPS)
 def test_theta_plain_nlj_all_ops(gj, ctx, op):
     """The plain NLJ over all pairs (GJ_OPT_THETA_REGIONS = 0) stays exact."""

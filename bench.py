@@ -290,16 +290,17 @@ def algorithmic_bytes(w, info):
             ab["part_scatter"] = ((nR + nS) * 2 * (w["R"].element_size() + 4) * info["passes"], 2 * info["passes"])
         return ab
     if w["kind"] == "pf_equi":
-        # a probed row costs its 8 B key + one 32 B Bloom sector (+ 1
-        # flag bit); the write pass reads the flags and each survivor's key (8 B) and
-        # writes key + rid (12 B); a filter insert 8 B key + a 32 B sector; then the
-        # hash join on the survivors with 8-byte keys.  (N=1 row counts: R and S each
-        # compacted once.)
+        # a probed row costs its 8 B key + one 32 B DRAM sector of the
+        # filter (its 8-byte block; + 1 flag bit); the write pass reads the flags and
+        # each survivor's key (8 B) and writes key + rid (12 B); then the hash join on
+        # the survivors with 8-byte keys.  (N=1 row counts: R and S each compacted once.)
         kR, kS = w["kept"]
         pf = info["pf_launches"]
         ab = join_bytes(kR, kS, nout, info["passes"], 8, False)
         ab["pf_count"] = (40 * (nR + nS) + (nR + nS) // 8, pf)
         ab["pf_write"] = ((nR + nS) // 8 + 20 * (kR + kS), pf)
+        # a filter insert reads its 8 B key once (multi-slice filters: after a slice
+        # partition of the keys, counted with part_scatter) and updates one 32 B sector
         ab["bloom_build"] = (40 * (nR + kS), info["bloom_launches"])
         return ab
     # band: NLJ is ALU-bound; bytes are tiny

@@ -230,9 +230,10 @@ gj_status gj_region_classify(int op, uint32_t k, uint64_t m, int64_t g, uint8_t*
  * Approximation of the paper's two-round common-key pre-filter (PAPER.md:78-82
  * §3.1, Alg.1 lines 1-13: keep only tuples whose join key occurs in both tables,
  * filtering BOTH tables).  GJ_PF_RANGE keeps keys in [max(minR,minS)-eps,
- * min(maxR,maxS)+eps] (saturating); GJ_PF_BLOOM builds a sector-blocked Bloom
- * filter of R's surviving keys (bloom_bits_per_key bits per key, 8 probes inside
- * one 32-byte sector) and drops S tuples whose key is absent; GJ_PF_TWO_SIDED then
+ * min(maxR,maxS)+eps] (saturating); GJ_PF_BLOOM builds a blocked Bloom filter of
+ * R's surviving keys (bloom_bits_per_key bits per key; 4 bits per key inside one
+ * 64-bit block: one atomic per insert, one 8-byte load per probe) and drops S
+ * tuples whose key is absent; GJ_PF_TWO_SIDED then
  * builds a filter of S's survivors and filters R the same way.  With op = GJ_BAND
  * and eps > 0 only the range stage applies (a Bloom filter cannot answer range
  * membership).  GJ_PF_EXACT (op = GJ_EQ, or GJ_BAND with eps = 0; replaces the

@@ -29,6 +29,22 @@ template <> struct KeyT<int64_t> {
 // Partition = top B bits (the multi-GPU shuffle takes the top log2(G) bits first);
 // the in-partition hash-table slot uses an independent hash.  Raw low key bits are
 // NOT used: configs[4]'s R keys are all even.
+// Bloom-filter hash (prefilter.cu): the filter block is its top bits; the radix
+// partitioner can bucket keys by the same bits (DigitFn::kind = DIGIT_BLOOM), so a
+// filter slice's keys are read once.
+__device__ __forceinline__ uint64_t bloom_hash(int32_t k) {
+  uint64_t h = (uint64_t)(uint32_t)k * 0xC2B2AE3D27D4EB4Full;
+  h ^= h >> 29;
+  h *= 0x165667B19E3779F9ull;
+  return h ^ (h >> 32);
+}
+__device__ __forceinline__ uint64_t bloom_hash(int64_t k) {
+  uint64_t h = (uint64_t)k * 0xC2B2AE3D27D4EB4Full;
+  h ^= h >> 29;
+  h *= 0x165667B19E3779F9ull;
+  return h ^ (h >> 32);
+}
+
 __device__ __forceinline__ uint32_t khash(int32_t k) {
   return (uint32_t)(((uint64_t)(uint32_t)k * 0x9E3779B97F4A7C15ull) >> 32);
 }

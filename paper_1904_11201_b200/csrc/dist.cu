@@ -371,7 +371,7 @@ void dist_equi_count_filtered(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj
     for (int p = 0; p < G; ++p) {
       sspec.logb[p] = pf_log_blocks(o.need[p][0], bpk);
       sspec.woff[p] = total;
-      total += 8ull << sspec.logb[p];
+      total += (uint64_t)BLOOM_BLOCK_WORDS << sspec.logb[p];
     }
     uint32_t* words = static_cast<uint32_t*>(ws(ctx, "dpf.filters", total * 4));
     pf_bloom_into(ctx, RL, words + sspec.woff[me], sspec.logb[me]);
@@ -379,7 +379,7 @@ void dist_equi_count_filtered(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj
       RegionScope rs(ctx, "nccl_allgather_bloom");
       GJ_NCCL(ncclGroupStart());
       for (int p = 0; p < G; ++p)
-        GJ_NCCL(ncclBroadcast(words + sspec.woff[p], words + sspec.woff[p], 8ull << sspec.logb[p], ncclUint32, p,
+        GJ_NCCL(ncclBroadcast(words + sspec.woff[p], words + sspec.woff[p], (uint64_t)BLOOM_BLOCK_WORDS << sspec.logb[p], ncclUint32, p,
                               c->comm, ctx->stream));
       GJ_NCCL(ncclGroupEnd());
     }
@@ -403,7 +403,7 @@ void dist_equi_count_filtered(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj
   if ((flags & GJ_PF_TWO_SIDED) && (flags & GJ_PF_BLOOM)) {
     PfSpec rspec;
     rspec.logb[0] = pf_log_blocks(SL.n, bpk);
-    uint32_t* w = static_cast<uint32_t*>(ws(ctx, "dpf.filterS", (8ull << rspec.logb[0]) * 4));
+    uint32_t* w = static_cast<uint32_t*>(ws(ctx, "dpf.filterS", ((uint64_t)BLOOM_BLOCK_WORDS << rspec.logb[0]) * 4));
     pf_bloom_into(ctx, SL, w, rspec.logb[0]);
     rspec.words = w;
     rspec.nfilt = 1;
@@ -506,7 +506,7 @@ void dist_prefilter(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S, u
   auto union_filters = [&](const gj_rel& X, uint64_t total, const char* tag) -> PfSpec {
     PfSpec f = spec;
     const uint32_t lb = pf_log_blocks((total + G - 1) / G, bpk);
-    const uint64_t fw = 8ull << lb;  // words per filter
+    const uint64_t fw = (uint64_t)BLOOM_BLOCK_WORDS << lb;  // words per filter
     for (int p = 0; p < G; ++p) {
       f.woff[p] = (uint64_t)p * fw;
       f.logb[p] = lb;

@@ -79,7 +79,8 @@ __device__ __forceinline__ uint32_t digit_of(K k, uint32_t shift, uint32_t mask)
 template <bool RANGE, typename K>
 __device__ __forceinline__ uint32_t digit_of(K k, uint32_t shift, uint32_t mask, const DigitFn& f) {
   if (!RANGE) return digit_of(k, shift, mask);
-  const uint32_t w = (uint32_t)(((unsigned long long)KeyT<K>::bias(k) - f.lo) >> f.sh) << f.up;
+  const uint32_t w = f.kind == DIGIT_BLOOM ? (uint32_t)(bloom_hash(k) >> 32)
+                                           : (uint32_t)(((unsigned long long)KeyT<K>::bias(k) - f.lo) >> f.sh) << f.up;
   return (w >> shift) & mask;
 }
 
@@ -772,6 +773,14 @@ Partitioned range_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, unsigned l
                             const char* tag) {
   if (B == 0 || B > 18) throw Error(GJ_EINVAL, "range partition needs 1..18 bucket bits");
   const DigitFn fn{lo, sh, 32 - B};
+  if (X.key_type == GJ_I32) return partition_impl<int32_t, true>(ctx, X, B, tag, 0, nullptr, 1, fn);
+  return partition_impl<int64_t, true>(ctx, X, B, tag, 0, nullptr, 1, fn);
+}
+
+Partitioned bloom_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char* tag) {
+  if (B == 0 || B > 18) throw Error(GJ_EINVAL, "bloom partition needs 1..18 bits");
+  DigitFn fn{};
+  fn.kind = DIGIT_BLOOM;
   if (X.key_type == GJ_I32) return partition_impl<int32_t, true>(ctx, X, B, tag, 0, nullptr, 1, fn);
   return partition_impl<int64_t, true>(ctx, X, B, tag, 0, nullptr, 1, fn);
 }

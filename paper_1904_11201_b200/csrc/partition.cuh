@@ -31,10 +31,12 @@ Partitioned radix_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char
                             const uint32_t* seg_off0 = nullptr, uint32_t nseg0 = 1);
 
 // Key -> partition word for range partitioning: ((bias(key) - lo) >> sh) << up.
+enum { DIGIT_RANGE = 0, DIGIT_BLOOM = 1 };
 struct DigitFn {
   unsigned long long lo = 0;
   uint32_t sh = 0;
   uint32_t up = 0;
+  uint32_t kind = DIGIT_RANGE;  // RANGE-mode partitions: key range, or the Bloom hash's top bits
 };
 // Range-partition X into 2^B equal-width key buckets: bucket(key) =
 // (bias(key) - lo) >> sh (bias = order-preserving signed -> unsigned map; every
@@ -43,6 +45,9 @@ struct DigitFn {
 // PAPER.md:258-266 §4.2).  Stable; off[p] as for radix_partition.
 Partitioned range_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, unsigned long long lo, uint32_t sh,
                             const char* tag);
+// Partition X by the top B bits of bloom_hash(key) (1 <= B <= 18): partition p holds
+// the keys whose Bloom blocks lie in the p-th 2^-B of the filter.  Stable.
+Partitioned bloom_partition(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char* tag);
 
 // ---- multi-GPU shuffle fused into the partition scatter
 constexpr int MAX_RANKS = 8;

@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "nlj.cuh"
+#include "partition.cuh"
 #include "prefilter.cuh"
 #include "runtime.h"
 #include "scan.cuh"
@@ -95,26 +96,16 @@ __global__ void set_build(const K* __restrict__ key, uint64_t n, Filt range, voi
   }
 }
 
-__device__ __forceinline__ uint64_t bloom_hash(int32_t k) {
-  uint64_t h = (uint64_t)(uint32_t)k * 0xC2B2AE3D27D4EB4Full;
-  h ^= h >> 29;
-  h *= 0x165667B19E3779F9ull;
-  return h ^ (h >> 32);
-}
-__device__ __forceinline__ uint64_t bloom_hash(int64_t k) {
-  uint64_t h = (uint64_t)k * 0xC2B2AE3D27D4EB4Full;
-  h ^= h >> 29;
-  h *= 0x165667B19E3779F9ull;
-  return h ^ (h >> 32);
-}
 
-// Split-block Bloom filter: the block index from the top bits of the hash, then ONE
-// bit in each of the block's 8 words (bit positions from a remix), so a key sets 8
-// bits inside one 32-byte sector, its mask costs 8 shifts, an insert is 4 64-bit
-// atomicOr and a probe one 32-byte sector read.
+// Blocked Bloom filter (register-blocked): the block -- one 64-bit word -- from the
+// top bits of the hash, then k = 4 bit positions inside it from a remix, so an insert
+// is ONE 64-bit atomicOr and a probe one 8-byte load.  At 8 bits per key (8 keys per
+// block on average) the false-positive rate E_j[(1 - (63/64)^(4j))^4], j ~ Poisson(8),
+// is 3.26% -- the same as a 256-bit split block with 8 bits (3.32%), whose 4 atomics
+// per insert made the build L2-atomic bound.
 struct BloomSlot {
   uint32_t block;
-  uint32_t mask[8];
+  unsigned long long mask;
 };
 template <typename K>
 __device__ __forceinline__ BloomSlot bloom_slot(K k, uint32_t log_blocks) {
@@ -122,8 +113,8 @@ __device__ __forceinline__ BloomSlot bloom_slot(K k, uint32_t log_blocks) {
   const uint64_t h = bloom_hash(k);
   b.block = log_blocks ? (uint32_t)(h >> (64 - log_blocks)) : 0u;
   const uint64_t h2 = (h ^ (h >> 31)) * 0x9E3779B97F4A7C15ull;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) b.mask[w] = 1u << ((uint32_t)(h2 >> (24 + 5 * w)) & 31u);
+  b.mask = (1ull << ((h2 >> 40) & 63u)) | (1ull << ((h2 >> 46) & 63u)) | (1ull << ((h2 >> 52) & 63u)) |
+           (1ull << ((h2 >> 58) & 63u));
   return b;
 }
 
@@ -143,12 +134,10 @@ __device__ __forceinline__ bool keep(K k, const Filt& f) {
       lb = f.logb[d];
     }
     const BloomSlot s = bloom_slot(k, lb);
-    if (ok) {  // predicated sector read: out-of-range keys cost no probe
-      const uint4* p = reinterpret_cast<const uint4*>(words + (uint64_t)s.block * 8);
-      const uint4 a = __ldg(p), c = __ldg(p + 1);
-      ok = ((a.x & s.mask[0]) != 0) & ((a.y & s.mask[1]) != 0) & ((a.z & s.mask[2]) != 0) &
-           ((a.w & s.mask[3]) != 0) & ((c.x & s.mask[4]) != 0) & ((c.y & s.mask[5]) != 0) &
-           ((c.z & s.mask[6]) != 0) & ((c.w & s.mask[7]) != 0);
+    if (ok) {  // predicated load: out-of-range keys cost no probe
+      const unsigned long long v =
+          __ldg(reinterpret_cast<const unsigned long long*>(words + (uint64_t)s.block * BLOOM_BLOCK_WORDS));
+      ok = (v & s.mask) == s.mask;
     }
   }
   if (f.set && ok) ok = set_contains(k, f);
@@ -159,19 +148,23 @@ __device__ __forceinline__ bool keep(K k, const Filt& f) {
 // the filter in L2-sized block ranges, so every 64-bit atomicOr hits a line that
 // stays in L2 instead of a DRAM read-modify-write of a random sector (a 256 MB
 // filter does not fit the 126 MB L2); the keys are re-read once per range.
+// With `off` (keys partitioned by their slice: bloom_partition), slice p's keys are
+// key[off[p], off[p+1]) and every one of them falls in the slice.
 template <typename K>
 __global__ void bloom_build(const K* __restrict__ key, uint64_t n, Filt range, uint32_t* __restrict__ bloom,
-                            uint32_t log_blocks, uint32_t blk_lo, uint32_t blk_hi) {
+                            uint32_t log_blocks, uint32_t blk_lo, uint32_t blk_hi, const uint32_t* __restrict__ off,
+                            uint32_t p) {
+  if (off) {
+    key += off[p];
+    n = off[p + 1] - off[p];
+  }
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const K k = key[i];
     const uint32_t blk = log_blocks ? (uint32_t)(bloom_hash(k) >> (64 - log_blocks)) : 0u;
     if (blk < blk_lo || blk >= blk_hi) continue;
     if (!keep(k, range)) continue;
     const BloomSlot s = bloom_slot(k, log_blocks);
-    unsigned long long* bw = reinterpret_cast<unsigned long long*>(bloom + (uint64_t)s.block * 8);
-#pragma unroll
-    for (int w = 0; w < 4; ++w)
-      atomicOr(&bw[w], (unsigned long long)s.mask[2 * w] | ((unsigned long long)s.mask[2 * w + 1] << 32));
+    atomicOr(reinterpret_cast<unsigned long long*>(bloom + (uint64_t)s.block * BLOOM_BLOCK_WORDS), s.mask);
   }
 }
 
@@ -185,10 +178,8 @@ __global__ void bloom_build_dest(const K* __restrict__ key, uint64_t n, Filt ran
     if (!keep(k, range)) continue;
     const uint32_t d = range.g ? khash(k) >> (32 - range.g) : 0u;
     const BloomSlot s = bloom_slot(k, range.logb[d]);
-    unsigned long long* bw = reinterpret_cast<unsigned long long*>(words + range.woff[d] + (uint64_t)s.block * 8);
-#pragma unroll
-    for (int w = 0; w < 4; ++w)
-      atomicOr(&bw[w], (unsigned long long)s.mask[2 * w] | ((unsigned long long)s.mask[2 * w + 1] << 32));
+    atomicOr(reinterpret_cast<unsigned long long*>(words + range.woff[d] + (uint64_t)s.block * BLOOM_BLOCK_WORDS),
+             s.mask);
   }
 }
 
@@ -301,21 +292,42 @@ uint64_t compact(gj_ctx* ctx, const gj_rel& X, const Filt& f, void* kout, uint32
   return h;
 }
 
-// Filter block ranges of at most ~48 MB (L2 holds them while every key is
-// streamed past): f(b0, b1) per range; one range for filters that already fit.
-template <typename F>
-void for_block_ranges(uint32_t log_blocks, F f) {
-  // 48 MB measured best at the configs[4] shape (96 MB: 25.0 ms/step, 24 MB 29.7, 48 MB 24.3)
-  constexpr uint64_t slice_bytes = 48ull << 20;
-  const uint64_t nblk = 1ull << log_blocks, per = std::max<uint64_t>(1, slice_bytes / 32);
-  for (uint64_t b = 0; b < nblk; b += per) f((uint32_t)b, (uint32_t)std::min<uint64_t>(nblk, b + per));
-}
+// Filter slices of at most 48 MB: L2 holds a slice's lines while its keys' atomics
+// land (48 MB measured best at the configs[4] shape with round 1's 4-atomic split
+// blocks: 96 MB 25.0 ms/step, 24 MB 29.7, 48 MB 24.3).
+constexpr uint64_t BLOOM_SLICE_BYTES = 48ull << 20;
 
 uint32_t log_blocks_for(uint64_t n, double bpk) {
-  const double bits = std::max(256.0, (double)n * bpk);
+  const double bits = std::max(256.0, (double)n * bpk);  // >= 4 blocks (bloom_or works on 16-byte groups)
   uint32_t lb = 0;
-  while ((256.0 * (double)(1ull << lb)) < bits && lb < 40) ++lb;
+  while ((32.0 * BLOOM_BLOCK_WORDS * (double)(1ull << lb)) < bits && lb < 40) ++lb;
   return lb;
+}
+
+// Fills the 2^lb-block filter at `bloom` (zeroed here) with X's keys that pass
+// `range`, one L2-sized slice at a time.  A filter of several slices first has its
+// keys partitioned by slice (bloom_partition: one radix pass on the Bloom hash's top
+// bits), so each slice launch reads only its own keys instead of all of them (at
+// configs[4]'s shape the 6 re-reads of R cost more than the inserts).
+template <typename K>
+void fill_bloom(gj_ctx* ctx, const gj_rel& X, const Filt& range, uint32_t* bloom, uint32_t lb) {
+  const uint64_t words = (uint64_t)BLOOM_BLOCK_WORDS << lb;
+  GJ_CUDA(cudaMemsetAsync(bloom, 0, words * sizeof(uint32_t), ctx->stream));
+  if (X.n == 0) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((X.n + 255) / 256, (uint64_t)ctx->num_sms * 16);
+  uint32_t B = 0;  // slices = 2^B
+  while (B < 9 && B < lb && (words * 4 >> B) > BLOOM_SLICE_BYTES) ++B;
+  if (B) {
+    const gj_rel Xr{X.key, nullptr, X.n, X.key_type, 0};
+    const Partitioned P = bloom_partition(ctx, Xr, B, "bl");
+    const uint32_t per = 1u << (lb - B);
+    for (uint32_t p = 0; p < (1u << B); ++p)
+      launch(ctx, "bloom_build", bloom_build<K>, dim3(grid), dim3(256), 0, static_cast<const K*>(P.key), X.n, range,
+             bloom, lb, p * per, (p + 1) * per, P.off, p);
+    return;
+  }
+  launch(ctx, "bloom_build", bloom_build<K>, dim3(grid), dim3(256), 0, static_cast<const K*>(X.key), X.n, range,
+         bloom, lb, 0u, (uint32_t)(1ull << lb), (const uint32_t*)nullptr, 0u);
 }
 
 template <typename K>
@@ -323,16 +335,8 @@ const uint32_t* build_bloom(gj_ctx* ctx, const gj_rel& X, const Filt& range, dou
                             const char* tag) {
   const uint32_t lb = log_blocks_for(X.n, bpk);
   *log_blocks = lb;
-  const uint64_t words = (1ull << lb) * 8;
-  uint32_t* bloom = static_cast<uint32_t*>(ws(ctx, tag, words * sizeof(uint32_t)));
-  GJ_CUDA(cudaMemsetAsync(bloom, 0, words * sizeof(uint32_t), ctx->stream));
-  if (X.n) {
-    const unsigned grid = (unsigned)std::min<uint64_t>((X.n + 255) / 256, (uint64_t)ctx->num_sms * 16);
-    for_block_ranges(lb, [&](uint32_t b0, uint32_t b1) {
-      launch(ctx, "bloom_build", bloom_build<K>, dim3(grid), dim3(256), 0, static_cast<const K*>(X.key), X.n, range,
-             bloom, lb, b0, b1);
-    });
-  }
+  uint32_t* bloom = static_cast<uint32_t*>(ws(ctx, tag, ((uint64_t)BLOOM_BLOCK_WORDS << lb) * sizeof(uint32_t)));
+  fill_bloom<K>(ctx, X, range, bloom, lb);
   return bloom;
 }
 
@@ -444,20 +448,11 @@ Filt to_filt(const PfSpec& p) {
 uint32_t pf_log_blocks(uint64_t n, double bpk) { return log_blocks_for(n, bpk); }
 
 void pf_bloom_into(gj_ctx* ctx, const gj_rel& X, uint32_t* words, uint32_t logb) {
-  GJ_CUDA(cudaMemsetAsync(words, 0, (8ull << logb) * sizeof(uint32_t), ctx->stream));
-  if (X.n == 0) return;
   Filt none{};
   none.lo = 0;
   none.hi = ~0ull;
-  const unsigned grid = (unsigned)std::min<uint64_t>((X.n + 255) / 256, (uint64_t)ctx->num_sms * 16);
-  for_block_ranges(logb, [&](uint32_t b0, uint32_t b1) {
-    if (X.key_type == GJ_I32)
-      launch(ctx, "bloom_build", bloom_build<int32_t>, dim3(grid), dim3(256), 0, static_cast<const int32_t*>(X.key),
-             X.n, none, words, logb, b0, b1);
-    else
-      launch(ctx, "bloom_build", bloom_build<int64_t>, dim3(grid), dim3(256), 0, static_cast<const int64_t*>(X.key),
-             X.n, none, words, logb, b0, b1);
-  });
+  if (X.key_type == GJ_I32) fill_bloom<int32_t>(ctx, X, none, words, logb);
+  else fill_bloom<int64_t>(ctx, X, none, words, logb);
 }
 
 uint64_t pf_compact(gj_ctx* ctx, const gj_rel& X, const PfSpec& spec, void* kout, uint32_t* rout, const char* tag) {

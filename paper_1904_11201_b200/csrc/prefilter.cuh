@@ -21,9 +21,11 @@ struct PfSpec {
   uint32_t logb[MAX_RANKS] = {};
 };
 
-// log2 of the number of 256-bit blocks of a filter for n keys at bpk bits per key.
+// Blocked Bloom filter: 64-bit blocks (2 uint32 words), 4 bits per key in one block.
+constexpr uint32_t BLOOM_BLOCK_WORDS = 2;
+// log2 of the number of blocks of a filter for n keys at bpk bits per key.
 uint32_t pf_log_blocks(uint64_t n, double bpk);
-// Bloom filter of X's keys into `words` (8 << logb uint32, zeroed here).
+// Bloom filter of X's keys into `words` (BLOOM_BLOCK_WORDS << logb uint32, zeroed here).
 void pf_bloom_into(gj_ctx* ctx, const gj_rel& X, uint32_t* words, uint32_t logb);
 // Stable compaction of X by the spec into kout / rout (X.n entries each); returns
 // the number of survivors (synchronises the stream).  Survivors keep their rids.

@@ -482,16 +482,16 @@ def test_prefilter_no_false_negatives(gj, ctx, flags):
     p = p[np.lexsort((p[:, 1], p[:, 0]))]
     assert np.array_equal(p, oracle.hash_equi(R, S)[1])
     if flags & 2:
-        # Bloom FPR within 2x of the split-block formula at 8 bits/key: a block holds
-        # Poisson(256/8 = 32) keys, each setting one bit in each of the 8 32-bit words a
-        # probe tests, so FPR = E_j[(1 - (31/32)^j)^8] = 0.0332 (an upper bound: the
-        # filter never gets fewer than 8 bits per inserted key)
+        # Bloom FPR within 2x of the blocked-filter formula at 8 bits/key: a 64-bit
+        # block holds Poisson(64/8 = 8) keys, each setting 4 bits (with repetition), and
+        # a probe tests 4 bits of one block, so FPR = E_j[(1 - (63/64)^(4j))^4] = 0.0326
+        # (an upper bound: the filter never gets fewer than 8 bits per inserted key)
         import math
-        p, fpr = math.exp(-32.0), 0.0
+        p, fpr = math.exp(-8.0), 0.0
         for j in range(200):
             if j:
-                p *= 32.0 / j
-            fpr += p * (1 - (31 / 32) ** j) ** 8
+                p *= 8.0 / j
+            fpr += p * (1 - (63 / 64) ** (4 * j)) ** 4
         lo, hi = max(R.min(), S.min()), min(R.max(), S.max())
         cand = np.ones(len(S), bool)
         cand[list(keepS)] = False  # true non-members ...

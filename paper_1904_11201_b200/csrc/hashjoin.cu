@@ -539,7 +539,10 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // it is read, so the descriptor -> key-vector dependency never waits on DRAM), and
 // consecutive units of one partition (probe chunks of a partition whose build side is
 // one chunk) share their build chunk: the table is built once and kept.
-__global__ void __launch_bounds__(HT, 4) hj_count_i32(HJArgs a, uint16_t* __restrict__ stage,
+#ifndef GJ_HJ_MINB
+#define GJ_HJ_MINB 4  // CTAs per SM the register budget targets (4: 64 registers)
+#endif
+__global__ void __launch_bounds__(HT, GJ_HJ_MINB) hj_count_i32(HJArgs a, uint16_t* __restrict__ stage,
                                                       uint8_t* __restrict__ multi,
                                                       unsigned long long* __restrict__ nmulti) {
   extern __shared__ __align__(16) uint8_t smem[];

@@ -157,7 +157,7 @@ void trace_mark(const char* label) {
   last = now;
 }
 
-RegionScope::RegionScope(gj_ctx* c, const char* t) : ctx(c), tag(t) {
+RegionScope::RegionScope(gj_ctx* c, const char* t) : ctx(c), tag(t), nvtx(t) {
   if (ctx->profile) {
     a = get_event(ctx);
     GJ_CUDA(cudaEventRecord(a, ctx->stream));
@@ -260,7 +260,7 @@ static void do_join_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S) {
 
 using namespace gj;
 
-#define API_BEGIN try {
+#define API_BEGIN try { gj::NvtxRange nvtx_range_(__func__);
 #define API_END                                            \
   }                                                        \
   catch (const gj::Error& e) {                             \

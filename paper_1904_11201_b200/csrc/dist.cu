@@ -693,7 +693,7 @@ void dist_theta_count(gj_ctx* ctx, gj_comm* c, const gj_rel& R, const gj_rel& S,
 
 using namespace gj;
 
-#define DAPI_BEGIN try {
+#define DAPI_BEGIN try { gj::NvtxRange nvtx_range_(__func__);
 #define DAPI_END                                                  \
   }                                                               \
   catch (const gj::Error& e) {                                    \

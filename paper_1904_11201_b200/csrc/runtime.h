@@ -2,6 +2,7 @@
 // accounting and per-kernel CUDA-event timing.  Product code only.
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -181,11 +182,22 @@ struct LaunchScope {
 void trace_mark(const char* label);
 void trace_sync(gj_ctx* ctx, const char* label);  // GJ_TRACE=2: stream sync first
 
+// NVTX range for the lifetime of the object (every C-ABI entry point and every
+// RegionScope): timeline tools (nsys, ncu --nvtx) see the library's phases; without
+// an attached tool the NVTX3 calls are no-ops.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // Times a non-kernel stream region (e.g. an NCCL exchange) under GJ_OPT_PROFILE;
 // not counted as a kernel launch.
 struct RegionScope {
   gj_ctx* ctx;
   const char* tag;
+  NvtxRange nvtx;
   cudaEvent_t a = nullptr;
   RegionScope(gj_ctx* c, const char* t);
   ~RegionScope();

@@ -438,6 +438,11 @@ __device__ __forceinline__ bool insert1(const I32Tab& t, uint32_t s, uint32_t tm
   return dup;
 }
 
+// element q (0..3) of a 4-register array, q dynamic: three selects, no local memory
+__device__ __forceinline__ uint32_t pick4(const uint32_t (&a)[4], uint32_t q) {
+  return q == 0 ? a[0] : (q == 1 ? a[1] : (q == 2 ? a[2] : a[3]));
+}
+
 __device__ __forceinline__ bool build4(const I32Tab& t, uint4 x, uint32_t v, uint32_t shift, uint32_t bn,
                                        uint32_t tmask, uint32_t tshift, uint32_t* side_n) {
   const uint32_t k[4] = {x.x, x.y, x.z, x.w};
@@ -456,10 +461,19 @@ __device__ __forceinline__ bool build4(const I32Tab& t, uint4 x, uint32_t v, uin
 #pragma unroll
       for (int q = 0; q < 4; ++q) sts16(t.row + 2 * s[q], j0 + q);
     } else {
+      // collisions (keys that are not a dense range: ~12% at load 1/4) are walked one
+      // pending key per round, rounds = the lane's collisions -- not one divergent
+      // walk per key position q whenever any lane's q-th key collided
+      uint32_t pm = 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         if (o[q] == EMPTY_KEY) sts16(t.row + 2 * s[q], j0 + q);
-        else dup |= insert1(t, s[q], tmask, k[q], j0 + q, o[q], side_n);
+        pm |= (uint32_t)(o[q] != EMPTY_KEY) << q;
+      }
+      while (pm) {
+        const uint32_t q = __ffs(pm) - 1;
+        pm &= pm - 1;
+        dup |= insert1(t, pick4(s, q), tmask, pick4(k, q), j0 + q, pick4(o, q), side_n);
       }
     }
   } else {

@@ -25,10 +25,6 @@ template <> struct KeyT<int64_t> {
   __host__ __device__ static __forceinline__ U bias(int64_t k) { return (U)k ^ 0x8000000000000000ull; }
 };
 
-// Multiplicative hash (Fibonacci hashing): the high 32 bits of key * 2^64/phi.
-// Partition = top B bits (the multi-GPU shuffle takes the top log2(G) bits first);
-// the in-partition hash-table slot uses an independent hash.  Raw low key bits are
-// NOT used: configs[4]'s R keys are all even.
 // Bloom-filter hash (prefilter.cu): the filter block is its top bits; the radix
 // partitioner can bucket keys by the same bits (DigitFn::kind = DIGIT_BLOOM), so a
 // filter slice's keys are read once.
@@ -45,6 +41,10 @@ __device__ __forceinline__ uint64_t bloom_hash(int64_t k) {
   return h ^ (h >> 32);
 }
 
+// Multiplicative hash (Fibonacci hashing): the high 32 bits of key * 2^64/phi.
+// Partition = top B bits (the multi-GPU shuffle takes the top log2(G) bits first);
+// the in-partition hash-table slot uses an independent hash.  Raw low key bits are
+// NOT used: configs[4]'s R keys are all even.
 __device__ __forceinline__ uint32_t khash(int32_t k) {
   return (uint32_t)(((uint64_t)(uint32_t)k * 0x9E3779B97F4A7C15ull) >> 32);
 }

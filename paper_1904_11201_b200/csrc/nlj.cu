@@ -695,7 +695,9 @@ __global__ void __launch_bounds__(BW_ROWS) band_write_kernel(BandArgs<K> a) {
   __shared__ uint32_t s_win[2];
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
   for (uint64_t row0 = (uint64_t)blockIdx.x * BW_ROWS; row0 < a.nR; row0 += (uint64_t)gridDim.x * BW_ROWS) {
-    const uint64_t myrow = row0 + threadIdx.x;
+    // rows interleaved over the warps (warp w: rows w, w + 8, ..., its lane l holds
+    // row 8 l + w), so the CTA's concurrent output regions are adjacent rows'
+    const uint64_t myrow = row0 + lane * 8 + w;
     const bool have = myrow < a.nR;
     K mykey = have ? a.rkey[myrow] : K(0);
     uint32_t rb = 0, gb = 0, ge = 0, re = 0, myrid = 0;
@@ -706,8 +708,8 @@ __global__ void __launch_bounds__(BW_ROWS) band_write_kernel(BandArgs<K> a) {
       myoff = a.off[myrow];
     }
     const uint32_t nrows = (uint32_t)min((uint64_t)BW_ROWS, a.nR - row0);
-    if (threadIdx.x == 0) s_win[0] = rb;          // S runs: nondecreasing starts
-    if (threadIdx.x == nrows - 1) s_win[1] = re;  // ... and ends
+    if (threadIdx.x == 0) s_win[0] = rb;                // S runs: nondecreasing starts
+    if (lane * 8 + w == nrows - 1) s_win[1] = re;       // ... and ends
     __syncthreads();
     const uint32_t wlo = s_win[0], wn = s_win[1] - s_win[0];
     const bool staged = wn <= BW_CAP;  // CTA-uniform
@@ -717,7 +719,7 @@ __global__ void __launch_bounds__(BW_ROWS) band_write_kernel(BandArgs<K> a) {
         s_rid[i] = a.srid[wlo + i];
       }
     __syncthreads();
-    const uint32_t nr = min(32u, nrows > 32 * w ? nrows - 32 * w : 0u);
+    const uint32_t nr = nrows > w ? (nrows - w + 7) / 8 : 0u;  // this warp's rows
     // kk, rd: the window-relative shared arrays, or the global ones -- two inlined
     // copies, so the staged loads compile to LDS, not generic loads
     auto rows = [&](const K* kk, const uint32_t* rd) {

@@ -675,23 +675,25 @@ __global__ void __launch_bounds__(256) band_count_kernel(BandArgs<K> a) {
   }
 }
 
-// Write pass: a CTA takes 256 consecutive R rows (8 warps x 32).  Their S runs are
-// nested intervals of the partitioned S (bucket order), so the batch reads only S
-// rows [rb of its first row, re of its last row) -- ~5.9K at configs[3] -- whose keys
-// and rids are staged in shared memory once (coalesced loads); the rows' Red
-// compares and Green copies then read shared memory only.  Without it every S rid
-// was fetched by ~100 R rows from L2 and, evicted by the streaming output, ~18 times
-// from DRAM.  A batch whose window exceeds BW_CAP (skewed keys) reads global memory.
-// Green runs leave as 16-byte stores (two pairs per lane).
+// Write pass: a CTA takes 256 consecutive R rows (8 warps x 32, interleaved).  Their
+// S runs are nested intervals of the partitioned S (bucket order), so the batch's
+// Green runs all lie in [rb of its first row, re of its last row) -- ~5.9K rows at
+// configs[3] -- whose rids are staged in shared memory once (coalesced loads); the
+// Green copies then read shared memory, the Red compares (~256 keys per row) read
+// L2.  Without the staging every S rid was fetched by ~100 R rows from L2 and,
+// evicted by the streaming output, ~18 times from DRAM; staging the keys as well
+// measured slower (48 KB per CTA: 4 CTAs/SM instead of 5).  A batch whose window
+// exceeds BW_CAP (skewed keys) reads global memory.  Green runs leave as 16-byte
+// stores (two pairs per lane).
 constexpr uint32_t BW_ROWS = 256, BW_CAP = 6144;
-template <typename K>
-constexpr size_t band_write_smem() { return (size_t)BW_CAP * (sizeof(K) + 4); }
+constexpr size_t BW_SMEM = (size_t)BW_CAP * 4;
 
+#ifndef GJ_BW_MINB
+#define GJ_BW_MINB 6  // 40 registers: 6 CTAs (48 warps) per SM (8: 32 registers spill, slower)
+#endif
 template <typename K, bool FAST>
-__global__ void __launch_bounds__(BW_ROWS) band_write_kernel(BandArgs<K> a) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  K* s_key = reinterpret_cast<K*>(smem);
-  uint32_t* s_rid = reinterpret_cast<uint32_t*>(smem + (size_t)BW_CAP * sizeof(K));
+__global__ void __launch_bounds__(BW_ROWS, GJ_BW_MINB) band_write_kernel(BandArgs<K> a) {
+  extern __shared__ __align__(16) uint32_t s_rid[];  // BW_CAP
   __shared__ uint32_t s_win[2];
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
   for (uint64_t row0 = (uint64_t)blockIdx.x * BW_ROWS; row0 < a.nR; row0 += (uint64_t)gridDim.x * BW_ROWS) {
@@ -714,15 +716,12 @@ __global__ void __launch_bounds__(BW_ROWS) band_write_kernel(BandArgs<K> a) {
     const uint32_t wlo = s_win[0], wn = s_win[1] - s_win[0];
     const bool staged = wn <= BW_CAP;  // CTA-uniform
     if (staged)
-      for (uint32_t i = threadIdx.x; i < wn; i += BW_ROWS) {
-        s_key[i] = a.skey[wlo + i];
-        s_rid[i] = a.srid[wlo + i];
-      }
+      for (uint32_t i = threadIdx.x; i < wn; i += BW_ROWS) s_rid[i] = a.srid[wlo + i];
     __syncthreads();
     const uint32_t nr = nrows > w ? (nrows - w + 7) / 8 : 0u;  // this warp's rows
-    // kk, rd: the window-relative shared arrays, or the global ones -- two inlined
-    // copies, so the staged loads compile to LDS, not generic loads
-    auto rows = [&](const K* kk, const uint32_t* rd) {
+    // rd: the window-relative shared rids, or the global ones -- two inlined copies,
+    // so the staged loads compile to LDS, not generic loads
+    auto rows = [&](const uint32_t* rd) {
     for (uint32_t q = 0; q < nr; ++q) {
       const K r = shfl_key(mykey, q);
       const uint32_t qrb = __shfl_sync(FULL, rb, q), qgb = __shfl_sync(FULL, gb, q);
@@ -732,7 +731,7 @@ __global__ void __launch_bounds__(BW_ROWS) band_write_kernel(BandArgs<K> a) {
       auto red = [&](uint32_t b, uint32_t e) {
         for (uint32_t j0 = b; j0 < e; j0 += 32) {
           const uint32_t j = j0 + lane;
-          const bool p = j < e && band_match<K, FAST>(r, kk[j], a.eps);
+          const bool p = j < e && band_match<K, FAST>(r, a.skey[j], a.eps);
           const uint32_t bal = __ballot_sync(FULL, p);
           if (p) a.out[o + __popc(bal & lanemask_lt())] = make_uint2(rr, rd[j]);
           o += __popc(bal);
@@ -754,8 +753,8 @@ __global__ void __launch_bounds__(BW_ROWS) band_write_kernel(BandArgs<K> a) {
       red(qge, qre);
     }
     };
-    if (staged) rows(s_key - wlo, s_rid - wlo);
-    else rows(a.skey, a.srid);
+    if (staged) rows(s_rid - wlo);
+    else rows(a.srid);
     __syncthreads();  // the window is refilled by the next batch
   }
 }
@@ -949,7 +948,7 @@ void band_region_write(gj_ctx* ctx, uint32_t* out) {
   a.off = tc.band_off;
   a.out = reinterpret_cast<uint2*>(out);
   const unsigned grid = (unsigned)std::min<uint64_t>((a.nR + BW_ROWS - 1) / BW_ROWS, (uint64_t)ctx->num_sms * 8);
-  const size_t smem = band_write_smem<K>();
+  const size_t smem = BW_SMEM;
   if (tc.mode == 1) {
     set_smem(ctx, band_write_kernel<K, true>, smem);
     launch(ctx, "band_write", band_write_kernel<K, true>, dim3(grid), dim3(BW_ROWS), smem, a);

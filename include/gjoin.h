@@ -158,9 +158,10 @@ void gj_ctx_reset_stats(gj_ctx* ctx);
 int gj_ctx_kernel_times(gj_ctx* ctx, const char** names, double* ms, uint64_t* launches,
                         int max_tags);
 /* Work of the last theta_join_count on this ctx (host outputs, either may be NULL):
- * nlj_pairs = (r, s) pairs the tiled NLJ compares (n_R * n_S without the region
- * matrix; the visited cells with it, §4.2), cross_pairs = pairs written
- * as Green cross products without a compare (0, 0 before any theta count). */
+ * nlj_pairs = (r, s) pairs compared (n_R * n_S without the region matrix; the
+ * visited cells with it, §4.2 -- for GJ_BAND the Red cells' pairs),
+ * cross_pairs = pairs written as Green cross products without a compare (0, 0
+ * before any theta count). */
 gj_status gj_theta_stats(gj_ctx* ctx, uint64_t* nlj_pairs, uint64_t* cross_pairs);
 /* Of the last join_count (or join_dist_count: this rank's local join) on this ctx,
  * host outputs, any may be NULL: rsize_eq8 = the paper's result-size estimate Eq.8

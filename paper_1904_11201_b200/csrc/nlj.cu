@@ -160,6 +160,7 @@ struct NLJArgs {
   uint2* out;
   const uint4* udesc;  // region mode: unit u = R rows [x, x + y) x S rows [z, z + w); else a uniform grid
   uint32_t dense;      // write pass: matches are dense (>= 1 per 256 compared pairs): no screening
+  uint32_t band_pad, band_pad_ok;  // band: a register key that matches no S key (see nlj_kernel)
 };
 
 // Write pass, a screened group of 4 S keys holding a match: each lane builds its
@@ -234,7 +235,12 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
       slen = send > sbeg ? send - sbeg : 0;
     }
     const uint32_t ntiles = (uint32_t)((slen + TS - 1) / TS);
-    const bool full = r0 + RT <= rend;
+    // a ragged R tile still takes the fast path for the band when its empty register
+    // slots can hold a key that matches no S key (a.band_pad: biased max key + 3 eps + 1,
+    // valid while span + 3 eps + 1 < 2^32): those slots then count as rows that never
+    // match
+    const bool pad = OP == GJ_BAND && a.band_pad_ok;
+    const bool full = r0 + RT <= rend || pad;
 
     K rk[KR];
     uint32_t rf[KR], rr[KR];
@@ -249,7 +255,7 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
       if (WRITE) rr[i] = v ? (a.rrid ? a.rrid[row] : a.rrid_base + (uint32_t)row) : 0u;
       if (FAST) {
         uint32_t b = (uint32_t)rk[i] ^ 0x80000000u;
-        rf[i] = (OP == GJ_BAND) ? b + (uint32_t)a.eps : b;
+        rf[i] = (OP == GJ_BAND) ? (v ? b + (uint32_t)a.eps : a.band_pad) : b;
       }
       if (WRITE) rrs[i * NT + tid] = rr[i];  // read back only by this thread
     }
@@ -419,7 +425,7 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
     g += ntiles;
     if (!WRITE) {
       uint64_t c = tot;
-      if (FAST && full && !direct(OP)) c = (uint64_t)nvalid * slen - tot;
+      if (FAST && full && !direct(OP)) c = (uint64_t)(pad ? KR : nvalid) * slen - tot;
       c = warp_sum(c);
       if (lane == 0) a.wcnt[(uint64_t)u * NWARP + w] = c;
     }
@@ -525,6 +531,13 @@ NLJArgs make_args(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, const ThetaCach
   a.nsplit = tc.nsplit;
   a.SR = tc.SR;
   a.U = tc.U;
+  // band pad key (nlj_kernel): biased max + 3 eps + 1 stays above every S key by more
+  // than 2 eps without wrapping iff span + 3 eps + 1 < 2^32
+  if (tc.op == GJ_BAND && R.key_type == GJ_I32 && tc.key_hi >= tc.key_lo &&
+      (unsigned __int128)(tc.key_hi - tc.key_lo) + 3 * (unsigned __int128)tc.eps + 1 < ((unsigned __int128)1 << 32)) {
+    a.band_pad = (uint32_t)(tc.key_hi + 3 * tc.eps + 1);
+    a.band_pad_ok = 1;
+  }
   return a;
 }
 
@@ -612,20 +625,66 @@ __device__ __forceinline__ bool band_match(K r, K s, uint64_t eps) {
   }
 }
 
-// S runs of the R row with key r (bucket x): Red [rb, gb) and [ge, re), Green [gb, ge)
+// Red rims of more than RED_HEAVY S rows per R row (skewed keys: a hot S bucket next
+// to a row) are not compared row by row: those buckets' Red cells go to the tiled
+// NLJ (register-blocked R tiles x S chunks, band_heavy_* below), the band kernels
+// write only their Green runs.
+constexpr uint32_t RED_HEAVY = 4096;
+
+// S runs of bucket x's R rows: Red [rb, gb) and [ge, re), Green [gb, ge)
+__device__ __forceinline__ void bucket_bounds(const uint32_t* __restrict__ so, uint32_t P, uint32_t m, int32_t g,
+                                              uint64_t x, uint32_t& rb, uint32_t& gb, uint32_t& ge, uint32_t& re) {
+  const uint64_t yl = x >= m ? x - m : 0, yh = min(x + m, (uint64_t)P - 1);
+  rb = so[yl];
+  re = so[yh + 1];
+  if (g >= 0) {
+    const uint64_t gg = (uint64_t)g;
+    gb = so[x >= gg ? x - gg : 0];
+    ge = so[min(x + gg, (uint64_t)P - 1) + 1];
+  } else {
+    gb = ge = so[x];
+  }
+}
+
+// The middle of a heavy Red run that the NLJ takes: its 16-byte aligned interior
+// (the NLJ stages S by TMA), [up(b), down(e)) -- the band kernels keep the <= 3-row
+// head and tail.  Empty (x, x) when the run is not heavy.
+template <typename K>
+__device__ __forceinline__ void nlj_middle(bool heavy, uint32_t b, uint32_t e, uint32_t& mb, uint32_t& me) {
+  constexpr uint32_t al = 16 / sizeof(K);
+  mb = heavy ? min((b + al - 1) & ~(al - 1), e) : e;
+  me = heavy ? max(e & ~(al - 1), mb) : e;
+}
+
+// The bounds for the R row with key r: Red [rb, gb) and [ge, re) minus the NLJ's
+// middles [l0, l1) and [h0, h1) of a heavy bucket, Green [gb, ge)
 template <typename K>
 __device__ __forceinline__ void band_bounds(const BandArgs<K>& a, K r, uint32_t& rb, uint32_t& gb, uint32_t& ge,
-                                            uint32_t& re) {
-  const uint64_t x = (uint64_t)(KeyT<K>::bias(r) - a.lo) >> a.sh;
-  const uint64_t yl = x >= a.m ? x - a.m : 0, yh = min(x + a.m, (uint64_t)a.P - 1);
-  rb = a.so[yl];
-  re = a.so[yh + 1];
-  if (a.g >= 0) {
-    const uint64_t g = (uint64_t)a.g;
-    gb = a.so[x >= g ? x - g : 0];
-    ge = a.so[min(x + g, (uint64_t)a.P - 1) + 1];
-  } else {
-    gb = ge = a.so[x];
+                                            uint32_t& re, uint32_t& l0, uint32_t& l1, uint32_t& h0, uint32_t& h1) {
+  bucket_bounds(a.so, a.P, a.m, a.g, (uint64_t)(KeyT<K>::bias(r) - a.lo) >> a.sh, rb, gb, ge, re);
+  const bool heavy = (gb - rb) + (re - ge) > RED_HEAVY;
+  nlj_middle<K>(heavy, rb, gb, l0, l1);
+  nlj_middle<K>(heavy, ge, re, h0, h1);
+}
+
+// Heavy buckets (R rows present, Red rim > RED_HEAVY): their index, R rows and Red
+// runs, appended to hb[] (count in *nh): the host turns them into NLJ units.
+template <typename K>
+__global__ void band_heavy_kernel(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ so, uint32_t P,
+                                  uint32_t m, int32_t g, uint4* __restrict__ hb, uint32_t* __restrict__ nh,
+                                  uint32_t cap) {
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < P; x += gridDim.x * blockDim.x) {
+    if (ro[x + 1] == ro[x]) continue;
+    uint32_t rb, gb, ge, re, l0, l1, h0, h1;
+    bucket_bounds(so, P, m, g, x, rb, gb, ge, re);
+    if ((gb - rb) + (re - ge) <= RED_HEAVY) continue;
+    nlj_middle<K>(true, rb, gb, l0, l1);
+    nlj_middle<K>(true, ge, re, h0, h1);
+    const uint32_t i = atomicAdd(nh, 1u);
+    if (i < cap) {
+      hb[2 * i] = make_uint4(ro[x], ro[x + 1] - ro[x], l0, l1 - l0);      // left Red middle
+      hb[2 * i + 1] = make_uint4(ro[x], ro[x + 1] - ro[x], h0, h1 - h0);  // right Red middle
+    }
   }
 }
 
@@ -642,13 +701,16 @@ __global__ void __launch_bounds__(256) band_count_kernel(BandArgs<K> a) {
     const bool have = myrow < a.nR;
     K mykey = have ? a.rkey[myrow] : K(0);
     uint32_t rb = 0, gb = 0, ge = 0, re = 0;  // Red [rb, gb) and [ge, re), Green [gb, ge)
-    if (have) band_bounds(a, mykey, rb, gb, ge, re);
+    uint32_t l0 = 0, l1 = 0, h0 = 0, h1 = 0;  // the NLJ's middles of a heavy bucket's Red runs
+    if (have) band_bounds(a, mykey, rb, gb, ge, re, l0, l1, h0, h1);
     const uint32_t nr = (uint32_t)min((uint64_t)32, a.nR - row0);
     uint32_t mycnt = 0;
     for (uint32_t q = 0; q < nr; ++q) {
       const K r = shfl_key(mykey, q);
       const uint32_t qrb = __shfl_sync(FULL, rb, q), qgb = __shfl_sync(FULL, gb, q);
       const uint32_t qge = __shfl_sync(FULL, ge, q), qre = __shfl_sync(FULL, re, q);
+      const uint32_t ql0 = __shfl_sync(FULL, l0, q), ql1 = __shfl_sync(FULL, l1, q);
+      const uint32_t qh0 = __shfl_sync(FULL, h0, q), qh1 = __shfl_sync(FULL, h1, q);
       uint32_t c = 0;
       auto red = [&](uint32_t b, uint32_t e) {
 #pragma unroll 4
@@ -657,11 +719,13 @@ __global__ void __launch_bounds__(256) band_count_kernel(BandArgs<K> a) {
           c += __popc(__ballot_sync(FULL, j < e && band_match<K, FAST>(r, a.skey[j], a.eps)));
         }
       };
-      red(qrb, qgb);
-      red(qge, qre);
+      red(qrb, ql0);
+      red(ql1, qgb);
+      red(qge, qh0);
+      red(qh1, qre);
       if (lane == q) mycnt = c + (qge - qgb);
       if (lane == 0) {
-        red_n += (qgb - qrb) + (qre - qge);
+        red_n += (qgb - qrb) + (qre - qge) - (ql1 - ql0) - (qh1 - qh0);
         green_n += qge - qgb;
       }
     }
@@ -702,10 +766,10 @@ __global__ void __launch_bounds__(BW_ROWS, GJ_BW_MINB) band_write_kernel(BandArg
     const uint64_t myrow = row0 + lane * 8 + w;
     const bool have = myrow < a.nR;
     K mykey = have ? a.rkey[myrow] : K(0);
-    uint32_t rb = 0, gb = 0, ge = 0, re = 0, myrid = 0;
+    uint32_t rb = 0, gb = 0, ge = 0, re = 0, myrid = 0, l0 = 0, l1 = 0, h0 = 0, h1 = 0;
     uint64_t myoff = 0;
     if (have) {
-      band_bounds(a, mykey, rb, gb, ge, re);
+      band_bounds(a, mykey, rb, gb, ge, re, l0, l1, h0, h1);
       myrid = a.rrid[myrow];
       myoff = a.off[myrow];
     }
@@ -726,6 +790,8 @@ __global__ void __launch_bounds__(BW_ROWS, GJ_BW_MINB) band_write_kernel(BandArg
       const K r = shfl_key(mykey, q);
       const uint32_t qrb = __shfl_sync(FULL, rb, q), qgb = __shfl_sync(FULL, gb, q);
       const uint32_t qge = __shfl_sync(FULL, ge, q), qre = __shfl_sync(FULL, re, q);
+      const uint32_t ql0 = __shfl_sync(FULL, l0, q), ql1 = __shfl_sync(FULL, l1, q);
+      const uint32_t qh0 = __shfl_sync(FULL, h0, q), qh1 = __shfl_sync(FULL, h1, q);
       const uint32_t rr = __shfl_sync(FULL, myrid, q);
       uint64_t o = __shfl_sync(FULL, myoff, q);
       auto red = [&](uint32_t b, uint32_t e) {
@@ -737,7 +803,8 @@ __global__ void __launch_bounds__(BW_ROWS, GJ_BW_MINB) band_write_kernel(BandArg
           o += __popc(bal);
         }
       };
-      red(qrb, qgb);
+      red(qrb, ql0);
+      red(ql1, qgb);
       const uint32_t gn = qge - qgb;
       uint2* go = a.out + o;
       const uint32_t* gs = rd + qgb;
@@ -750,7 +817,8 @@ __global__ void __launch_bounds__(BW_ROWS, GJ_BW_MINB) band_write_kernel(BandArg
       for (uint32_t i = lane; i < n2; i += 32) g4[i] = make_uint4(rr, gs[head + 2 * i], rr, gs[head + 2 * i + 1]);
       if (lane == 0 && head + 2 * n2 < gn) go[gn - 1] = make_uint2(rr, gs[gn - 1]);
       o += gn;
-      red(qge, qre);
+      red(qge, qh0);
+      red(qh1, qre);
     }
     };
     if (staged) rows(s_rid - wlo);
@@ -915,18 +983,74 @@ void band_region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint64_t e
   a.cnt = cnt;
   a.stats = st;
   const unsigned grid = (unsigned)std::min<uint64_t>((R.n + 255) / 256, (uint64_t)ctx->num_sms * 8);
+  // heavy buckets first (their list is read back only when there is one)
+  const uint32_t hcap = 1u << 16;
+  uint32_t* nh = static_cast<uint32_t*>(ws(ctx, "band.nheavy", 16));
+  uint4* hb = static_cast<uint4*>(ws(ctx, "band.heavy", 2ull * hcap * sizeof(uint4)));
+  GJ_CUDA(cudaMemsetAsync(nh, 0, sizeof(uint32_t), ctx->stream));
+  launch(ctx, "band_heavy", band_heavy_kernel<K>, dim3(std::min<uint32_t>((P + 255) / 256, ctx->num_sms * 4)),
+         dim3(256), 0, PR.off, PS.off, P, m, g, hb, nh, hcap);
   if (fast)
     launch(ctx, "band_count", band_count_kernel<K, true>, dim3(grid), dim3(256), 0, a);
   else
     launch(ctx, "band_count", band_count_kernel<K, false>, dim3(grid), dim3(256), 0, a);
   exclusive_scan<uint32_t, uint64_t>(ctx, cnt, off, R.n, off + R.n);
   GJ_CUDA(cudaMemcpyAsync(st + 2, off + R.n, sizeof(uint64_t), cudaMemcpyDeviceToDevice, ctx->stream));
-  unsigned long long h[3];
+  GJ_CUDA(cudaMemsetAsync(st + 3, 0, sizeof(unsigned long long), ctx->stream));
+  GJ_CUDA(cudaMemcpyAsync(st + 3, nh, sizeof(uint32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+  unsigned long long h[4];  // Red pairs compared, Green pairs, band pairs, heavy buckets
   d2h_sync(ctx, h, st, sizeof(h));
   tc.band_off = off;
-  tc.total = h[2];
+  tc.band_total = h[2];
   tc.nlj_pairs = h[0];
   tc.cross_pairs = h[1];
+  tc.U = 0;
+  tc.nlj_total = 0;
+  tc.band_nlj_pairs = 0;
+  const uint32_t nheavy = (uint32_t)std::min<unsigned long long>(h[3], hcap);
+  if (h[3] > hcap) throw Error(GJ_EINVAL, "band join: more than 65536 heavy key buckets");
+  if (nheavy) {
+    // the heavy buckets' Red cells: tiles of RT R rows x S chunks of SR rows
+    std::vector<uint4> runs(2ull * nheavy), ud;
+    d2h_sync(ctx, runs.data(), hb, runs.size() * sizeof(uint4));
+    // bucket order (the list was appended in atomic order): deterministic positions
+    std::sort(runs.begin(), runs.end(),
+              [](const uint4& u, const uint4& v) { return u.x != v.x ? u.x < v.x : u.z < v.z; });
+    const uint64_t SR = 16 * TS;
+    uint64_t pairs = 0;
+    for (const uint4& q : runs)
+      for (uint64_t r0 = q.x; r0 < (uint64_t)q.x + q.y; r0 += RT)
+        for (uint64_t s0 = q.z; s0 < (uint64_t)q.z + q.w; s0 += SR) {
+          const uint32_t rn = (uint32_t)std::min<uint64_t>(RT, (uint64_t)q.x + q.y - r0);
+          const uint32_t sn = (uint32_t)std::min<uint64_t>(SR, (uint64_t)q.z + q.w - s0);
+          ud.push_back(make_uint4((uint32_t)r0, rn, (uint32_t)s0, sn));
+          pairs += (uint64_t)rn * sn;
+        }
+    tc.U = (uint32_t)ud.size();
+    if (tc.U) {
+      uint4* udev = static_cast<uint4*>(ws(ctx, "nlj.udesc", ud.size() * sizeof(uint4)));
+      GJ_CUDA(cudaMemcpyAsync(udev, ud.data(), ud.size() * sizeof(uint4), cudaMemcpyHostToDevice, ctx->stream));
+      tc.udesc = udev;
+      tc.nsplit = 1;
+      tc.SR = SR;
+      const uint64_t nw = (uint64_t)tc.U * NWARP;
+      uint64_t* wcnt = static_cast<uint64_t*>(ws(ctx, "nlj.wcnt", (nw + 1) * sizeof(uint64_t)));
+      uint64_t* woff = static_cast<uint64_t*>(ws(ctx, "nlj.woff", (nw + 1) * sizeof(uint64_t)));
+      uint32_t* work = static_cast<uint32_t*>(ws(ctx, "nlj.work", 16));
+      GJ_CUDA(cudaMemsetAsync(work, 0, sizeof(uint32_t), ctx->stream));
+      NLJArgs na = make_args(ctx, tc.PR, tc.PS, tc);
+      na.work = work;
+      na.wcnt = wcnt;
+      na.udesc = udev;
+      dispatch<K>(ctx, na, GJ_BAND, fast, false);
+      exclusive_scan<uint64_t, uint64_t>(ctx, wcnt, woff, nw, woff + nw);
+      tc.woff = woff;
+      d2h_sync(ctx, &tc.nlj_total, woff + nw, sizeof(uint64_t));  // also orders the udesc copy before ud dies
+      tc.nlj_pairs += pairs;
+      tc.band_nlj_pairs = pairs;
+    }
+  }
+  tc.total = tc.band_total + tc.nlj_total;
 }
 
 template <typename K>
@@ -955,6 +1079,17 @@ void band_region_write(gj_ctx* ctx, uint32_t* out) {
   } else {
     set_smem(ctx, band_write_kernel<K, false>, smem);
     launch(ctx, "band_write", band_write_kernel<K, false>, dim3(grid), dim3(BW_ROWS), smem, a);
+  }
+  if (tc.nlj_total) {  // the heavy buckets' Red pairs, after the band kernel's
+    uint32_t* work = static_cast<uint32_t*>(ws(ctx, "nlj.work", 16));
+    GJ_CUDA(cudaMemsetAsync(work, 0, sizeof(uint32_t), ctx->stream));
+    NLJArgs na = make_args(ctx, tc.PR, tc.PS, tc);
+    na.work = work;
+    na.woff = tc.woff;
+    na.out = reinterpret_cast<uint2*>(out) + tc.band_total;
+    na.udesc = tc.udesc;
+    na.dense = tc.nlj_total * 256 >= tc.band_nlj_pairs;
+    dispatch<K>(ctx, na, GJ_BAND, tc.mode == 1, true);
   }
 }
 
@@ -990,6 +1125,8 @@ void theta_count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S0, int op, ui
     lo = std::min(h[0], h[2]);
     hi = std::max(h[1], h[3]);
   }
+  tc.key_lo = lo;
+  tc.key_hi = hi;
   if (op == GJ_BAND) {
     const unsigned long long span = hi - lo;  // exact: biased keys are order-preserving
     if (eps >= span) {

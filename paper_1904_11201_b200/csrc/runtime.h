@@ -92,6 +92,9 @@ struct ThetaCache {
   int32_t band_g = -1;
   unsigned long long band_lo = 0;
   const uint64_t* band_off = nullptr;
+  uint64_t band_total = 0;  // pairs of the band kernels; the heavy buckets' NLJ pairs follow
+  uint64_t band_nlj_pairs = 0;  // pairs the NLJ compares for the heavy buckets
+  unsigned long long key_lo = 1, key_hi = 0;  // biased key range of the last band / region count (lo > hi: unknown)
 };
 
 // Per-stream state of the single-pass scan: status words + ticket counter, the

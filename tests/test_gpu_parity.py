@@ -717,6 +717,22 @@ def test_band_write_unstaged_window(gj, ctx):
     check_theta(gj, ctx, R, S, "band", 3, materialize=True)
 
 
+def test_band_heavy_buckets_deterministic(gj, ctx):
+    """Skewed band join: most R rows sit next to a hot S bucket whose Red rim exceeds
+    the per-row limit, so those buckets' Red cells go to the tiled NLJ after the band
+    kernels' pairs -- same pairs as the oracle, same positions on a rerun."""
+    rng = np.random.default_rng(78)
+    R = np.concatenate([rng.integers(1000, 1040, 3000), rng.integers(-2**20, 2**20, 500)]).astype(np.int32)
+    S = np.concatenate([rng.integers(990, 1050, 30000), rng.integers(-2**20, 2**20, 2000)]).astype(np.int32)
+    ctx.set_option("theta_regions", 1)
+    n = check_theta(gj, ctx, R, S, "band", 3, materialize=True)
+    nlj_pairs, cross = ctx.theta_stats()
+    assert nlj_pairs > 0
+    a = gj.theta_join_materialize(ctx, dev(R), dev(S), "band", 3, n).cpu().numpy()
+    b = gj.theta_join_materialize(ctx, dev(R), dev(S), "band", 3, n).cpu().numpy()
+    assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("eps", [0, 5, 2**33])
 def test_band_region_int64(gj, ctx, eps):
     """int64 keys take the band path with the exact 64-bit predicate."""

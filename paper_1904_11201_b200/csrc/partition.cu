@@ -327,14 +327,20 @@ __global__ void __launch_bounds__(PT, SCATTER_MINB) part_scatter(
     const uint32_t b = it & 1;
     t = s_tile[b];
     if (t >= ntiles) break;  // CTA-uniform
+    // the next tile: claimed now, its TMA load issued into buffer b ^ 1 right after
+    // this tile's first barrier (every thread is then past the previous tile, the
+    // last user of b ^ 1) -- so no end-of-tile barrier is needed
+    uint32_t tn = 0;
     if (threadIdx.x == 0) {
-      const uint32_t tn = G + atomicAdd(tile_ctr, 1u);
+      tn = G + atomicAdd(tile_ctr, 1u);
       s_tile[b ^ 1] = tn;
-      if (tn < ntiles) {
+    }
+    auto issue_next = [&]() {
+      if (threadIdx.x == 0 && tn < ntiles) {
         if (bulk) bulk_wait_read();  // the previous tile's bulk stores have read buffer b ^ 1
         issue(b ^ 1, tdesc[tn]);
       }
-    }
+    };
     const uint4 d = tdesc[t];
     uint32_t g0a = 0, g0b = 0;  // global run starts of my two digits in this tile
     uint32_t sta = 0, stb = 0;  // their tile-local starts (tile_base_kernel's per-tile digit scan)
@@ -352,6 +358,7 @@ __global__ void __launch_bounds__(PT, SCATTER_MINB) part_scatter(
     if (cnt == 0) {  // CTA-uniform
       mbar_wait(bars + b, (it >> 1) & 1);
       __syncthreads();
+      issue_next();
       continue;
     }
     {
@@ -396,6 +403,7 @@ __global__ void __launch_bounds__(PT, SCATTER_MINB) part_scatter(
     for (int i = 0; i < PI; ++i)
       rr[i] = HAS_RID ? rbuf[ro + (w * PI + i) * 32 + lane] : rid_base + d.x + (w * PI + i) * 32 + lane;
     __syncthreads();  // inputs are in registers: the buffer becomes the staging area
+    issue_next();
     {  // staging positions: thread i owns digits i and i + H -- the warps' exclusive
        // column prefix on top of the digit's tile-local start (precomputed per tile by
        // tile_base_kernel, so no cross-warp scan and no extra barrier here)
@@ -522,7 +530,6 @@ __global__ void __launch_bounds__(PT, SCATTER_MINB) part_scatter(
         }
       }
     }
-    __syncthreads();  // the buffer may be refilled by the next iteration's issue
   }
   if (bulk && threadIdx.x == 0) bulk_wait_all();  // bulk stores complete
   if (REMOTE) __threadfence_system();  // peer writes performed before the kernel retires

@@ -159,7 +159,7 @@ struct NLJArgs {
   const uint64_t* woff;
   uint2* out;
   const uint4* udesc;  // region mode: unit u = R rows [x, x + y) x S rows [z, z + w); else a uniform grid
-  uint32_t dense;      // write pass: matches are dense (>= 1 per 256 compared pairs): no screening
+  uint32_t dense;      // write pass: >= 1 match per 1024 compared pairs (~1 per warp step): no screening
   uint32_t band_pad, band_pad_ok;  // band: a register key that matches no S key (see nlj_kernel)
 };
 
@@ -1088,7 +1088,7 @@ void band_region_write(gj_ctx* ctx, uint32_t* out) {
     na.woff = tc.woff;
     na.out = reinterpret_cast<uint2*>(out) + tc.band_total;
     na.udesc = tc.udesc;
-    na.dense = tc.nlj_total * 256 >= tc.band_nlj_pairs;
+    na.dense = tc.nlj_total * 1024 >= tc.band_nlj_pairs;
     dispatch<K>(ctx, na, GJ_BAND, tc.mode == 1, true);
   }
 }
@@ -1182,7 +1182,7 @@ void theta_write_impl(gj_ctx* ctx, uint32_t* out) {
       a.woff = tc.woff;
       a.out = reinterpret_cast<uint2*>(out);
       a.udesc = tc.udesc;
-      a.dense = tc.nlj_total * 256 >= tc.nlj_pairs;
+      a.dense = tc.nlj_total * 1024 >= tc.nlj_pairs;
       dispatch<K>(ctx, a, tc.op, tc.mode == 1, true);
     }
     if (!tc.rects.empty()) {
@@ -1202,7 +1202,7 @@ void theta_write_impl(gj_ctx* ctx, uint32_t* out) {
   a.work = work;
   a.woff = tc.woff;
   a.out = reinterpret_cast<uint2*>(out);
-  a.dense = tc.total * 256 >= tc.nlj_pairs;
+  a.dense = tc.total * 1024 >= tc.nlj_pairs;
   dispatch<K>(ctx, a, tc.op, tc.mode == 1, true);
 }
 

@@ -984,7 +984,7 @@ void band_region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint64_t e
   a.stats = st;
   const unsigned grid = (unsigned)std::min<uint64_t>((R.n + 255) / 256, (uint64_t)ctx->num_sms * 8);
   // heavy buckets first (their list is read back only when there is one)
-  const uint32_t hcap = 1u << 16;
+  const uint32_t hcap = P;  // every bucket could be heavy
   uint32_t* nh = static_cast<uint32_t*>(ws(ctx, "band.nheavy", 16));
   uint4* hb = static_cast<uint4*>(ws(ctx, "band.heavy", 2ull * hcap * sizeof(uint4)));
   GJ_CUDA(cudaMemsetAsync(nh, 0, sizeof(uint32_t), ctx->stream));
@@ -1008,7 +1008,6 @@ void band_region_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint64_t e
   tc.nlj_total = 0;
   tc.band_nlj_pairs = 0;
   const uint32_t nheavy = (uint32_t)std::min<unsigned long long>(h[3], hcap);
-  if (h[3] > hcap) throw Error(GJ_EINVAL, "band join: more than 65536 heavy key buckets");
   if (nheavy) {
     // the heavy buckets' Red cells: tiles of RT R rows x S chunks of SR rows
     std::vector<uint4> runs(2ull * nheavy), ud;

@@ -563,6 +563,16 @@ __global__ void __launch_bounds__(PT) tile_base_kernel(uint64_t n, const uint32_
   if (d0 >= D) return;
   const uint64_t i0 = (uint64_t)L.cb * D + (uint64_t)d0 * L.nc + (c - L.cb);
   const uint32_t b0 = scanned[i0], b1 = d0 + 1 < D ? scanned[i0 + L.nc] : 0u;
+  if (d0 + 1 < D && nt == TPC) {  // a full chunk: all 16 rows' loads in flight at once
+    uint2 v[TPC];
+#pragma unroll
+    for (uint32_t t = 0; t < TPC; ++t)
+      v[t] = *reinterpret_cast<const uint2*>(tile_pref + ((uint64_t)c * TPC + t) * D + d0);
+#pragma unroll
+    for (uint32_t t = 0; t < TPC; ++t)
+      *reinterpret_cast<uint2*>(tile_pref + ((uint64_t)c * TPC + t) * D + d0) = make_uint2(v[t].x + b0, v[t].y + b1);
+    return;
+  }
   for (uint32_t t = 0; t < nt; ++t) {
     uint32_t* row = tile_pref + ((uint64_t)c * TPC + t) * D;
     if (d0 + 1 < D) {

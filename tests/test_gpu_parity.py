@@ -733,6 +733,27 @@ def test_band_heavy_buckets_deterministic(gj, ctx):
     assert np.array_equal(a, b)
 
 
+def test_band_heavy_buckets_int64_and_rid_maps(gj, ctx):
+    """The heavy-bucket NLJ path with int64 keys (exact predicate, 2-key alignment)
+    and with caller rid maps on both sides: pairs are the oracle's positional pairs
+    mapped through the rid arrays."""
+    rng = np.random.default_rng(79)
+    R = np.concatenate([rng.integers(2**40, 2**40 + 64, 2500), rng.integers(-2**45, 2**45, 300)]).astype(np.int64)
+    S = np.concatenate([rng.integers(2**40 - 8, 2**40 + 72, 20000), rng.integers(-2**45, 2**45, 900)]).astype(np.int64)
+    rR = rng.permutation(10**6)[: len(R)].astype(np.uint32)
+    rS = rng.permutation(10**6)[: len(S)].astype(np.uint32)
+    ctx.set_option("theta_regions", 1)
+    tR, tS = gj.Rel(dev(R), dev(rR.view(np.int32))), gj.Rel(dev(S), dev(rS.view(np.int32)))
+    n = gj.theta_join_count(ctx, tR, tS, "band", 2)
+    assert n == oracle.theta_count_sorted(R, S, "band", 2)
+    assert ctx.theta_stats()[0] > 0
+    out = canon_gpu(gj.theta_join_materialize(ctx, tR, tS, "band", 2, n))
+    _, cp = oracle.nlj(R, S, "band", 2)
+    cp = np.stack([rR[cp[:, 0]], rS[cp[:, 1]]], 1).astype(np.uint32)
+    cp = cp[np.lexsort((cp[:, 1], cp[:, 0]))]
+    assert np.array_equal(out.astype(np.uint32), cp)
+
+
 @pytest.mark.parametrize("eps", [0, 5, 2**33])
 def test_band_region_int64(gj, ctx, eps):
     """int64 keys take the band path with the exact 64-bit predicate."""

@@ -535,6 +535,29 @@ __global__ void __launch_bounds__(PT, SCATTER_MINB) part_scatter(
   if (REMOTE) __threadfence_system();  // peer writes performed before the kernel retires
 }
 
+// off[p] = start of output partition p (p = segment << bits | digit), off[P] = n:
+// the scanned matrix's first chunk entry of (segment, digit)
+__device__ __forceinline__ void extract_one(uint32_t p, const uint32_t* __restrict__ scanned,
+                                            const uint32_t* __restrict__ seg_off,
+                                            const uint32_t* __restrict__ chunk_base, uint32_t nseg, uint32_t bits,
+                                            uint64_t n, uint32_t* __restrict__ off) {
+  const uint32_t P = nseg << bits;
+  if (p > P) return;
+  if (p == P) { off[P] = (uint32_t)n; return; }
+  uint32_t seg = p >> bits, d = p & ((1u << bits) - 1);
+  uint32_t cb, nc, start;
+  if (chunk_base == nullptr) {
+    cb = 0;
+    nc = (uint32_t)((n + CHUNK - 1) / CHUNK);
+    start = 0;
+  } else {
+    cb = chunk_base[seg];
+    nc = chunk_base[seg + 1] - cb;
+    start = seg_off[seg];
+  }
+  off[p] = nc ? scanned[(uint64_t)cb * (1u << bits) + (uint64_t)d * nc] : start;
+}
+
 // Plans one scatter, one CTA per chunk: turns the in-chunk prefix rows of part_hist
 // into absolute run starts (every tile's row gets its chunk's scanned (segment,
 // digit, chunk) offsets added, so the scatter reads one contiguous row per tile --
@@ -545,9 +568,12 @@ __global__ void __launch_bounds__(PT) tile_base_kernel(uint64_t n, const uint32_
                                                        const uint32_t* __restrict__ chunk_base, uint32_t nseg,
                                                        uint32_t bits, const uint32_t* __restrict__ scanned,
                                                        uint32_t* __restrict__ tile_pref, uint4* __restrict__ tdesc,
-                                                       uint32_t* __restrict__ tile_ctr) {
+                                                       uint32_t* __restrict__ tile_ctr, uint32_t* __restrict__ off) {
   const uint32_t c = blockIdx.x, D = 1u << bits;
   if (c == 0 && threadIdx.x == 0) *tile_ctr = 0;
+  // the pass's output partition starts (folded in here: one launch fewer per pass)
+  for (uint32_t p = c * PT + threadIdx.x; p <= (nseg << bits); p += gridDim.x * PT)
+    extract_one(p, scanned, seg_off, chunk_base, nseg, bits, n, off);
   const ChunkLoc L = locate(c, n, seg_off, chunk_base, nseg);
   const uint32_t len = c < L.total ? (uint32_t)(L.end - L.beg) : 0u;
   if (threadIdx.x < TPC) {
@@ -638,27 +664,6 @@ __global__ void __launch_bounds__(1024) chunk_base_kernel(const uint32_t* __rest
   if (threadIdx.x == 0) cb[nseg] = carry;
 }
 
-__global__ void extract_off(const uint32_t* __restrict__ scanned, const uint32_t* __restrict__ seg_off,
-                            const uint32_t* __restrict__ chunk_base, uint32_t nseg, uint32_t bits,
-                            uint64_t n, uint32_t* __restrict__ off) {
-  const uint32_t P = nseg << bits;
-  uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p > P) return;
-  if (p == P) { off[P] = (uint32_t)n; return; }
-  uint32_t seg = p >> bits, d = p & ((1u << bits) - 1);
-  uint32_t cb, nc, start;
-  if (chunk_base == nullptr) {
-    cb = 0;
-    nc = (uint32_t)((n + CHUNK - 1) / CHUNK);
-    start = 0;
-  } else {
-    cb = chunk_base[seg];
-    nc = chunk_base[seg + 1] - cb;
-    start = seg_off[seg];
-  }
-  off[p] = nc ? scanned[(uint64_t)cb * (1u << bits) + (uint64_t)d * nc] : start;
-}
-
 __global__ void fill_off2(uint32_t* off, uint64_t n) {
   off[0] = 0;
   off[1] = (uint32_t)n;
@@ -715,14 +720,12 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
     exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
     uint4* tdesc = static_cast<uint4*>(ws(ctx, "part.tdesc", (ntiles + 1) * sizeof(uint4)));
     uint32_t* ctr = static_cast<uint32_t*>(ws(ctx, "part.tile_ctr", sizeof(uint32_t)));
-    launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, seg_off,
-           (const uint32_t*)chunk_base, nseg, bits, (const uint32_t*)hist, tile_pref, tdesc, ctr);
-    launch_scatter<K, RANGE, false>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, tile_pref, tile_st, ctr,
-                                    kout, rout, fn, ShuffleDest{});
     const uint32_t P = nseg << bits;
     uint32_t* off = static_cast<uint32_t*>(ws(ctx, (ps + ".off").c_str(), (P + 1) * sizeof(uint32_t)));
-    launch(ctx, "extract_off", extract_off, dim3((P + 1 + 255) / 256), dim3(256), 0, (const uint32_t*)hist,
-           seg_off, (const uint32_t*)chunk_base, nseg, bits, n, off);
+    launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, seg_off,
+           (const uint32_t*)chunk_base, nseg, bits, (const uint32_t*)hist, tile_pref, tdesc, ctr, off);
+    launch_scatter<K, RANGE, false>(ctx, kin, rin, X.rid_base, n, tdesc, ntiles, shift, bits, tile_pref, tile_st, ctr,
+                                    kout, rout, fn, ShuffleDest{});
     kin = kout;
     rin = rout;
     seg_off = off;
@@ -761,12 +764,9 @@ ShufflePass shuffle_prepare_impl(gj_ctx* ctx, const gj_rel& X, uint32_t g, const
   exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
   uint4* tdesc = static_cast<uint4*>(ws(ctx, (t + ".stdesc").c_str(), (sp.ntiles + 1) * sizeof(uint4)));
   uint32_t* ctr = static_cast<uint32_t*>(ws(ctx, (t + ".sctr").c_str(), sizeof(uint32_t)));
-  launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, (const uint32_t*)nullptr,
-         (const uint32_t*)nullptr, 1u, g, (const uint32_t*)hist, tile_pref, tdesc, ctr);
   uint32_t* off = static_cast<uint32_t*>(ws(ctx, (t + ".soff").c_str(), (D + 1) * sizeof(uint32_t)));
-  launch(ctx, "extract_off", extract_off, dim3((D + 1 + 255) / 256), dim3(256), 0, (const uint32_t*)hist,
-         (const uint32_t*)nullptr,
-         (const uint32_t*)nullptr, 1u, g, n, off);
+  launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, (const uint32_t*)nullptr,
+         (const uint32_t*)nullptr, 1u, g, (const uint32_t*)hist, tile_pref, tdesc, ctr, off);
   sp.hist = hist;
   sp.tile_pref = tile_pref;
   sp.tdesc = tdesc;

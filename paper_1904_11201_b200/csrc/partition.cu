@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(PT, sizeof(K) == 4 ? 4 : 3) part_hist(const K*
                                                 const uint32_t* __restrict__ chunk_base,
                                                 uint32_t nseg, uint32_t shift, uint32_t bits,
                                                 uint32_t* __restrict__ hist, uint32_t* __restrict__ tile_pref,
-                                                uint32_t* __restrict__ tile_st, DigitFn fn) {
+                                                uint16_t* __restrict__ tile_st, DigitFn fn) {
   __shared__ uint32_t h[(1 << MAX_BITS) + 1];
   __shared__ uint32_t wsum[PT / 32];
   const uint32_t D = 1u << bits, mask = D - 1;
@@ -141,10 +141,10 @@ __global__ void __launch_bounds__(PT, sizeof(K) == 4 ? 4 : 3) part_hist(const K*
     const uint64_t r = ((uint64_t)c * TPC + t) * D;
     if (d0 + 1 < D) {
       *reinterpret_cast<uint2*>(tile_pref + r + d0) = make_uint2(prev0, prev1);
-      *reinterpret_cast<uint2*>(tile_st + r + d0) = make_uint2(ex, ex + x0);
+      *reinterpret_cast<uint32_t*>(tile_st + r + d0) = ex | (ex + x0) << 16;  // starts < 4096
     } else if (d0 < D) {
       tile_pref[r + d0] = prev0;
-      tile_st[r + d0] = ex;
+      tile_st[r + d0] = (uint16_t)ex;
     }
     prev0 = now0;
     prev1 = now1;
@@ -271,7 +271,7 @@ template <typename K, bool HAS_RID, bool RANGE, bool REMOTE>
 __global__ void __launch_bounds__(PT, SCATTER_MINB) part_scatter(
     const K* __restrict__ key_in, const uint32_t* __restrict__ rid_in, uint32_t rid_base, uint64_t n,
     const uint4* __restrict__ tdesc, uint32_t ntiles, uint32_t shift, uint32_t bits,
-    const uint32_t* __restrict__ tile_base, const uint32_t* __restrict__ tile_st, K* __restrict__ key_out,
+    const uint32_t* __restrict__ tile_base, const uint16_t* __restrict__ tile_st, K* __restrict__ key_out,
     uint32_t* __restrict__ rid_out, uint32_t* __restrict__ tile_ctr, DigitFn fn, ShuffleDest dst) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using L = ScatterLayout<K>;
@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(PT) tile_base_kernel(uint64_t n, const uint32_
 template <typename K, bool HAS_RID, bool RANGE, bool REMOTE>
 void launch_scatter_t(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
                       const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* tile_base,
-                      const uint32_t* tile_st, uint32_t* ctr, K* kout, uint32_t* rout, const DigitFn& fn,
+                      const uint16_t* tile_st, uint32_t* ctr, K* kout, uint32_t* rout, const DigitFn& fn,
                       const ShuffleDest& dst) {
   auto kern = part_scatter<K, HAS_RID, RANGE, REMOTE>;
   const size_t smem = ScatterLayout<K>::bytes(1u << bits);
@@ -629,7 +629,7 @@ void launch_scatter_t(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t r
 template <typename K, bool RANGE, bool REMOTE>
 void launch_scatter(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid_base, uint64_t n,
                     const uint4* tdesc, uint64_t ntiles, uint32_t shift, uint32_t bits, const uint32_t* tile_base,
-                    const uint32_t* tile_st, uint32_t* ctr, K* kout, uint32_t* rout, const DigitFn& fn,
+                    const uint16_t* tile_st, uint32_t* ctr, K* kout, uint32_t* rout, const DigitFn& fn,
                     const ShuffleDest& dst) {
   if (rin)
     launch_scatter_t<K, true, RANGE, REMOTE>(ctx, kin, rin, rid_base, n, tdesc, ntiles, shift, bits, tile_base,
@@ -714,7 +714,7 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
     uint32_t* hist = static_cast<uint32_t*>(ws(ctx, (t + ".hist").c_str(), (hn + 1) * sizeof(uint32_t)));
     const uint64_t ntiles = max_chunks * TPC;
     uint32_t* tile_pref = static_cast<uint32_t*>(ws(ctx, "part.tile_pref", ntiles * D * sizeof(uint32_t)));
-    uint32_t* tile_st = static_cast<uint32_t*>(ws(ctx, "part.tile_st", ntiles * D * sizeof(uint32_t)));
+    uint16_t* tile_st = static_cast<uint16_t*>(ws(ctx, "part.tile_st", ntiles * D * sizeof(uint16_t)));
     launch(ctx, "part_hist", part_hist<K, RANGE>, dim3((unsigned)max_chunks), dim3(PT), 0, kin, n, seg_off,
            (const uint32_t*)chunk_base, nseg, shift, bits, hist, tile_pref, tile_st, fn);
     exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
@@ -757,7 +757,7 @@ ShufflePass shuffle_prepare_impl(gj_ctx* ctx, const gj_rel& X, uint32_t g, const
   sp.ntiles = max_chunks * TPC;
   uint32_t* tile_pref = static_cast<uint32_t*>(ws(ctx, (t + ".stp").c_str(), sp.ntiles * D * sizeof(uint32_t) + 4));
   const uint32_t shift = 32 - g;
-  uint32_t* tile_st = static_cast<uint32_t*>(ws(ctx, (t + ".sst").c_str(), sp.ntiles * D * sizeof(uint32_t) + 4));
+  uint16_t* tile_st = static_cast<uint16_t*>(ws(ctx, (t + ".sst").c_str(), sp.ntiles * D * sizeof(uint16_t) + 4));
   launch(ctx, "part_hist", part_hist<K, false>, dim3((unsigned)std::max<uint64_t>(max_chunks, 1)), dim3(PT), 0,
          static_cast<const K*>(X.key), n, (const uint32_t*)nullptr, (const uint32_t*)nullptr, 1u, shift, g, hist,
          tile_pref, tile_st, DigitFn{});

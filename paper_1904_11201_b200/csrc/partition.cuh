@@ -63,7 +63,7 @@ struct ShufflePass {
   const uint32_t* hist = nullptr;
   const uint32_t* tile_pref = nullptr;
   const uint4* tdesc = nullptr;
-  const uint32_t* tile_st = nullptr;  // per (tile, digit): tile-local run start
+  const uint16_t* tile_st = nullptr;  // per (tile, digit): tile-local run start (< 4096)
   uint32_t* ctr = nullptr;        // the scatter's tile counter (reset by the planning kernel)
   const uint32_t* off = nullptr;  // device, 2^g + 1 run starts (local digit order)
 };

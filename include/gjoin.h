@@ -131,7 +131,11 @@ const char* gj_last_error(void);
  *                          hash of its arguments and options (op, eps, flags, key type,
  *                          bloom bits, radix / shuffle / grid options); if the ranks
  *                          disagree, every rank returns GJ_EINVAL (SURVEY §8(b)'s debug
- *                          check; one tiny NCCL all-reduce and a sync per call). */
+ *                          check; one tiny NCCL all-reduce and a sync per call).
+ *  GJ_OPT_OVERLAP_PARTITIONS  single-GPU equi join: 1 (default) = S is radix-partitioned
+ *                          on a second ctx-owned stream beside R (each relation's kernels
+ *                          fill the other's partial last waves); 0 = one after the other
+ *                          on the ctx stream.  Same result either way. */
 enum {
   GJ_OPT_PART_BITS = 1,
   GJ_OPT_BUILD_CHUNK = 2,
@@ -144,7 +148,8 @@ enum {
   GJ_OPT_THETA_REGIONS = 9,
   GJ_OPT_THETA_GRID_ROWS = 10,
   GJ_OPT_SHUFFLE_CTAS = 11,
-  GJ_OPT_CHECK_ARGS = 12
+  GJ_OPT_CHECK_ARGS = 12,
+  GJ_OPT_OVERLAP_PARTITIONS = 13
 };
 gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t value);
 

@@ -243,11 +243,36 @@ void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t ski
   // the build side to the duplicate-heavy FK relation on random size fluctuations.
   const bool swap = ctx->build_side == 2 || (ctx->build_side == 0 && S.n * 10 < R.n * 9);
   const uint32_t B = std::max(b0, std::min<uint32_t>(auto_bits(ctx, swap ? S.n : R.n), 32 - skip));
-  Partitioned PR = radix_partition(ctx, R, B - b0, "R", skip + b0, b0 ? segR : nullptr, 1u << b0);
-  // S may still be arriving (multi-GPU: its shuffle runs on a second stream while R
-  // is partitioned here)
-  if (s_ready) GJ_CUDA(cudaStreamWaitEvent(ctx->stream, s_ready, 0));
-  Partitioned PS = radix_partition(ctx, S, B - b0, "S", skip + b0, b0 ? segS : nullptr, 1u << b0);
+  Partitioned PR, PS;
+  if (!s_ready && ctx->overlap_partitions) {
+    // single GPU: S is partitioned on the ctx's second stream beside R, so each
+    // relation's kernels fill the other's tails (partial last waves); separate scratch
+    // per relation ("R.*", "S.*"), scan state per stream
+    if (!ctx->aux) {
+      GJ_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+      for (auto& e : ctx->aux_ev) GJ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaStream_t main_stream = ctx->stream;
+    GJ_CUDA(cudaEventRecord(ctx->aux_ev[0], main_stream));
+    GJ_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev[0], 0));
+    ctx->stream = ctx->aux;
+    try {
+      PS = radix_partition(ctx, S, B - b0, "S", skip + b0, b0 ? segS : nullptr, 1u << b0);
+    } catch (...) {
+      ctx->stream = main_stream;
+      throw;
+    }
+    GJ_CUDA(cudaEventRecord(ctx->aux_ev[1], ctx->aux));
+    ctx->stream = main_stream;
+    PR = radix_partition(ctx, R, B - b0, "R", skip + b0, b0 ? segR : nullptr, 1u << b0);
+    GJ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));
+  } else {
+    PR = radix_partition(ctx, R, B - b0, "R", skip + b0, b0 ? segR : nullptr, 1u << b0);
+    // S may still be arriving (multi-GPU: its shuffle runs on a second stream while R
+    // is partitioned here)
+    if (s_ready) GJ_CUDA(cudaStreamWaitEvent(ctx->stream, s_ready, 0));
+    PS = radix_partition(ctx, S, B - b0, "S", skip + b0, b0 ? segS : nullptr, 1u << b0);
+  }
   hash_join_count(ctx, R, S, B, swap, PR, PS);
   jc.valid = true;
 }
@@ -372,6 +397,7 @@ gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t v) {
       ctx->theta_grid_rows = (uint32_t)v;
       break;
     case GJ_OPT_CHECK_ARGS: ctx->check_args = v != 0; break;
+    case GJ_OPT_OVERLAP_PARTITIONS: ctx->overlap_partitions = v != 0; break;
     case GJ_OPT_SHUFFLE_CTAS:
       if (v < -1 || v > 1 << 20) throw Error(GJ_EINVAL, "shuffle_ctas must be -1, 0 or a CTA count");
       ctx->shuffle_ctas = (int)v;

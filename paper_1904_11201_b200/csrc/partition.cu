@@ -713,13 +713,13 @@ Partitioned partition_impl(gj_ctx* ctx, const gj_rel& X, uint32_t B, const char*
     const uint64_t hn = max_chunks * D;
     uint32_t* hist = static_cast<uint32_t*>(ws(ctx, (t + ".hist").c_str(), (hn + 1) * sizeof(uint32_t)));
     const uint64_t ntiles = max_chunks * TPC;
-    uint32_t* tile_pref = static_cast<uint32_t*>(ws(ctx, "part.tile_pref", ntiles * D * sizeof(uint32_t)));
-    uint16_t* tile_st = static_cast<uint16_t*>(ws(ctx, "part.tile_st", ntiles * D * sizeof(uint16_t)));
+    uint32_t* tile_pref = static_cast<uint32_t*>(ws(ctx, (t + ".tile_pref").c_str(), ntiles * D * sizeof(uint32_t)));
+    uint16_t* tile_st = static_cast<uint16_t*>(ws(ctx, (t + ".tile_st").c_str(), ntiles * D * sizeof(uint16_t)));
     launch(ctx, "part_hist", part_hist<K, RANGE>, dim3((unsigned)max_chunks), dim3(PT), 0, kin, n, seg_off,
            (const uint32_t*)chunk_base, nseg, shift, bits, hist, tile_pref, tile_st, fn);
     exclusive_scan<uint32_t, uint32_t>(ctx, hist, hist, hn, hist + hn);
-    uint4* tdesc = static_cast<uint4*>(ws(ctx, "part.tdesc", (ntiles + 1) * sizeof(uint4)));
-    uint32_t* ctr = static_cast<uint32_t*>(ws(ctx, "part.tile_ctr", sizeof(uint32_t)));
+    uint4* tdesc = static_cast<uint4*>(ws(ctx, (t + ".tdesc").c_str(), (ntiles + 1) * sizeof(uint4)));
+    uint32_t* ctr = static_cast<uint32_t*>(ws(ctx, (t + ".tile_ctr").c_str(), sizeof(uint32_t)));
     const uint32_t P = nseg << bits;
     uint32_t* off = static_cast<uint32_t*>(ws(ctx, (ps + ".off").c_str(), (P + 1) * sizeof(uint32_t)));
     launch(ctx, "tile_base", tile_base_kernel, dim3((unsigned)max_chunks), dim3(PT), 0, n, seg_off,

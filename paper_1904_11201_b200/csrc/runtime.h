@@ -133,6 +133,10 @@ struct gj_ctx {
   int build_side = 0;
   uint32_t hj_unit_cap = 0;  // hash-join unit arrays: capacity the last joins needed
   int shuffle_bits = 0;
+#ifndef GJ_OVERLAP_PARTITIONS
+#define GJ_OVERLAP_PARTITIONS 1
+#endif
+  bool overlap_partitions = GJ_OVERLAP_PARTITIONS;  // 1 GPU: partition S on `aux` beside R
   // workspace (optionally from the caller's allocator hook)
   std::map<std::string, gj::Buf> bufs;
   gj_alloc_fn alloc_fn = nullptr;

@@ -266,6 +266,21 @@ void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t ski
     ctx->stream = main_stream;
     PR = radix_partition(ctx, R, B - b0, "R", skip + b0, b0 ? segR : nullptr, 1u << b0);
     GJ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));
+  } else if (s_ready && ctx->aux && ctx->overlap_partitions) {
+    // multi-GPU: S's shuffle ran on `aux` (s_ready recorded there after its barrier);
+    // its local passes follow it on `aux` while R's run here
+    cudaStream_t main_stream = ctx->stream;
+    ctx->stream = ctx->aux;
+    try {
+      PS = radix_partition(ctx, S, B - b0, "S", skip + b0, b0 ? segS : nullptr, 1u << b0);
+    } catch (...) {
+      ctx->stream = main_stream;
+      throw;
+    }
+    GJ_CUDA(cudaEventRecord(ctx->aux_ev[1], ctx->aux));
+    ctx->stream = main_stream;
+    PR = radix_partition(ctx, R, B - b0, "R", skip + b0, b0 ? segR : nullptr, 1u << b0);
+    GJ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));
   } else {
     PR = radix_partition(ctx, R, B - b0, "R", skip + b0, b0 ? segR : nullptr, 1u << b0);
     // S may still be arriving (multi-GPU: its shuffle runs on a second stream while R

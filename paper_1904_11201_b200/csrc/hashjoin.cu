@@ -553,6 +553,9 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // it is read, so the descriptor -> key-vector dependency never waits on DRAM), and
 // consecutive units of one partition (probe chunks of a partition whose build side is
 // one chunk) share their build chunk: the table is built once and kept.
+#ifndef GJ_HJ_SLOTS
+#define GJ_HJ_SLOTS 4  // key slots per build row (rounded up to a power of two)
+#endif
 #ifndef GJ_HJ_MINB
 #define GJ_HJ_MINB 4  // CTAs per SM the register budget targets (4: 64 registers)
 #endif
@@ -610,7 +613,7 @@ __global__ void __launch_bounds__(HT, GJ_HJ_MINB) hj_count_i32(HJArgs a, uint16_
     const uint4 pv0 = P.vb + lane < P.ve ? ldv(P.sp, P.vb + lane) : zero;
     const uint4 pv1 = P.vb + lane + 32 < P.ve ? ldv(P.sp, P.vb + lane + 32) : zero;
     const uint32_t bn = d.y, pn = d.w;
-    const uint32_t logT = min(max(32 - __clz(4 * bn - 1), 5u), 13u);  // ~4 slots per build row
+    const uint32_t logT = min(max(32 - __clz(GJ_HJ_SLOTS * bn - 1), 5u), 13u);  // ~4 slots per build row
     const uint32_t T = 1u << logT, tmask = T - 1, tshift = 32 - logT;
     if (!built) {  // CTA-uniform
       bool dup = false;

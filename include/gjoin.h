@@ -135,7 +135,12 @@ const char* gj_last_error(void);
  *  GJ_OPT_OVERLAP_PARTITIONS  single-GPU equi join: 1 (default) = S is radix-partitioned
  *                          on a second ctx-owned stream beside R (each relation's kernels
  *                          fill the other's partial last waves); 0 = one after the other
- *                          on the ctx stream.  Same result either way. */
+ *                          on the ctx stream.  Same result either way.
+ *  GJ_OPT_FIB_SLOTS        int32 equi join: 1 (default) = a key's shared-memory table
+ *                          slot is the khash bits right below the ones the partitioning
+ *                          consumed (Fibonacci hashing continued; keys from a dense
+ *                          range then never collide inside a partition) whenever those
+ *                          bits suffice; 0 = a second multiplicative hash.  Same result. */
 enum {
   GJ_OPT_PART_BITS = 1,
   GJ_OPT_BUILD_CHUNK = 2,
@@ -149,7 +154,8 @@ enum {
   GJ_OPT_THETA_GRID_ROWS = 10,
   GJ_OPT_SHUFFLE_CTAS = 11,
   GJ_OPT_CHECK_ARGS = 12,
-  GJ_OPT_OVERLAP_PARTITIONS = 13
+  GJ_OPT_OVERLAP_PARTITIONS = 13,
+  GJ_OPT_FIB_SLOTS = 14
 };
 gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t value);
 

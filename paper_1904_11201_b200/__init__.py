@@ -37,7 +37,7 @@ RANGE, BLOOM, TWO_SIDED, EXACT = 1, 2, 4, 8
 OPT = {"part_bits": 1, "build_chunk": 2, "probe_chunk": 3, "profile": 4, "nlj_split": 5,
        "force_slow_band": 6, "build_side": 7, "shuffle_bits": 8, "theta_regions": 9,
        "theta_grid_rows": 10, "shuffle_ctas": 11, "check_args": 12,
-       "overlap_partitions": 13}
+       "overlap_partitions": 13, "fib_slots": 14}
 STATUS = {0: "GJ_OK", 1: "GJ_EINVAL", 2: "GJ_ENOMEM", 3: "GJ_ERANGE", 4: "GJ_ESTATE", 5: "GJ_ECUDA",
           6: "GJ_ENCCL"}
 I32, I64 = 0, 1

@@ -288,7 +288,7 @@ void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t ski
     if (s_ready) GJ_CUDA(cudaStreamWaitEvent(ctx->stream, s_ready, 0));
     PS = radix_partition(ctx, S, B - b0, "S", skip + b0, b0 ? segS : nullptr, 1u << b0);
   }
-  hash_join_count(ctx, R, S, B, swap, PR, PS);
+  hash_join_count(ctx, R, S, skip, B, swap, PR, PS);
   jc.valid = true;
 }
 
@@ -413,6 +413,7 @@ gj_status gj_ctx_set_option(gj_ctx* ctx, int option, int64_t v) {
       break;
     case GJ_OPT_CHECK_ARGS: ctx->check_args = v != 0; break;
     case GJ_OPT_OVERLAP_PARTITIONS: ctx->overlap_partitions = v != 0; break;
+    case GJ_OPT_FIB_SLOTS: ctx->fib_slots = v != 0; break;
     case GJ_OPT_SHUFFLE_CTAS:
       if (v < -1 || v > 1 << 20) throw Error(GJ_EINVAL, "shuffle_ctas must be -1, 0 or a CTA count");
       ctx->shuffle_ctas = (int)v;

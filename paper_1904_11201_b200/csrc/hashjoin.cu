@@ -69,6 +69,7 @@ struct HJArgs {
   uint2* out;
   int swap;
   uint64_t nb, np;  // build / probe array lengths (bulk-copy windows are clamped to them)
+  uint2 slot_c;     // hj_count_i32's slot constant (slot32)
 };
 
 // The 16-byte vectors covering elements [first, first + cnt) of an array, on absolute
@@ -402,7 +403,15 @@ __device__ __forceinline__ uint32_t cas32(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void sts128(uint32_t a, uint32_t x) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(a), "r"(x) : "memory");
 }
-__device__ __forceinline__ uint32_t slot32(uint32_t k, uint32_t tshift) { return slot_hash((int32_t)k) >> tshift; }
+// Slot of key k in a 2^(32 - tshift)-slot table: the top bits of hi32(k * c), c a
+// 64-bit odd constant given per launch (c.x low word, c.y high word; two IMADs).
+// count_impl passes c = khash's constant << hbits when the partitioning consumed
+// hbits <= 19 hash bits: the slot is then the khash bits right below the consumed
+// ones (Fibonacci hashing continued: keys from a dense range get distinct slots
+// inside a partition, three-distance theorem); else slot_hash's constant.
+__device__ __forceinline__ uint32_t slot32(uint32_t k, uint2 c, uint32_t tshift) {
+  return (k * c.y + __umulhi(k, c.x)) >> tshift;
+}
 
 struct I32Tab {
   uint32_t key, row, side;  // shared addresses: key slots, row per slot, side list
@@ -444,14 +453,14 @@ __device__ __forceinline__ uint32_t pick4(const uint32_t (&a)[4], uint32_t q) {
 }
 
 __device__ __forceinline__ bool build4(const I32Tab& t, uint4 x, uint32_t v, uint32_t shift, uint32_t bn,
-                                       uint32_t tmask, uint32_t tshift, uint32_t* side_n) {
+                                       uint32_t tmask, uint2 sc, uint32_t tshift, uint32_t* side_n) {
   const uint32_t k[4] = {x.x, x.y, x.z, x.w};
   const uint32_t j0 = v * 4 - shift;
   bool dup = false;
   if (j0 < bn && j0 + 3 < bn) {  // all four rows in the unit: straight line
     uint32_t s[4], o[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) s[q] = slot32(k[q], tshift);
+    for (int q = 0; q < 4; ++q) s[q] = slot32(k[q], sc, tshift);
 #pragma unroll
     for (int q = 0; q < 4; ++q) o[q] = k[q] != EMPTY_KEY ? cas32(t.key + 4 * s[q], k[q]) : 0u;
     bool clean = true;
@@ -480,7 +489,7 @@ __device__ __forceinline__ bool build4(const I32Tab& t, uint4 x, uint32_t v, uin
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (j0 + q < bn) {
-        const uint32_t s = slot32(k[q], tshift);
+        const uint32_t s = slot32(k[q], sc, tshift);
         const uint32_t o = k[q] != EMPTY_KEY ? cas32(t.key + 4 * s, k[q]) : 0u;
         if (o == EMPTY_KEY) sts16(t.row + 2 * s, j0 + q);
         else dup |= insert1(t, s, tmask, k[q], j0 + q, o, side_n);
@@ -509,14 +518,14 @@ __device__ __forceinline__ uint32_t probe_walk(const I32Tab& t, uint32_t s, uint
 }
 
 __device__ __forceinline__ void probe4(const I32Tab& t, uint4 x, uint32_t v, uint32_t shift, uint32_t pn,
-                                       uint32_t tmask, uint32_t tshift, bool unique, uint32_t side_n,
+                                       uint32_t tmask, uint2 sc, uint32_t tshift, bool unique, uint32_t side_n,
                                        uint16_t* __restrict__ st, bool vec, uint32_t& c, bool& many) {
   const uint32_t k[4] = {x.x, x.y, x.z, x.w};
   const uint32_t j0 = v * 4 - shift;
   const bool full = j0 < pn && j0 + 3 < pn;
   uint32_t s[4], e[4], r[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) s[q] = slot32(k[q], tshift);
+  for (int q = 0; q < 4; ++q) s[q] = slot32(k[q], sc, tshift);
 #pragma unroll
   for (int q = 0; q < 4; ++q) e[q] = (full || j0 + q < pn) ? lds32(t.key + 4 * s[q]) : EMPTY_KEY;
 #pragma unroll
@@ -617,10 +626,10 @@ __global__ void __launch_bounds__(HT, GJ_HJ_MINB) hj_count_i32(HJArgs a, uint16_
     const uint32_t T = 1u << logT, tmask = T - 1, tshift = 32 - logT;
     if (!built) {  // CTA-uniform
       bool dup = false;
-      if (tid < P.sb.nv) dup |= build4(t, bv0, tid, P.sb.shift, bn, tmask, tshift, &s_side);
-      if (tid + HT < P.sb.nv) dup |= build4(t, bv1, tid + HT, P.sb.shift, bn, tmask, tshift, &s_side);
+      if (tid < P.sb.nv) dup |= build4(t, bv0, tid, P.sb.shift, bn, tmask, a.slot_c, tshift, &s_side);
+      if (tid + HT < P.sb.nv) dup |= build4(t, bv1, tid + HT, P.sb.shift, bn, tmask, a.slot_c, tshift, &s_side);
       for (uint32_t v = tid + 2 * HT; v < P.sb.nv; v += HT)
-        dup |= build4(t, ldv(P.sb, v), v, P.sb.shift, bn, tmask, tshift, &s_side);
+        dup |= build4(t, ldv(P.sb, v), v, P.sb.shift, bn, tmask, a.slot_c, tshift, &s_side);
       if (__any_sync(FULL, dup) && lane == 0) s_dup = 1;
       __syncthreads();
     }
@@ -630,11 +639,11 @@ __global__ void __launch_bounds__(HT, GJ_HJ_MINB) hj_count_i32(HJArgs a, uint16_
     uint32_t c = 0;
     bool many = false;
     if (P.vb + lane < P.ve)
-      probe4(t, pv0, P.vb + lane, P.sp.shift, pn, tmask, tshift, unique, side_n, st, vec, c, many);
+      probe4(t, pv0, P.vb + lane, P.sp.shift, pn, tmask, a.slot_c, tshift, unique, side_n, st, vec, c, many);
     if (P.vb + lane + 32 < P.ve)
-      probe4(t, pv1, P.vb + lane + 32, P.sp.shift, pn, tmask, tshift, unique, side_n, st, vec, c, many);
+      probe4(t, pv1, P.vb + lane + 32, P.sp.shift, pn, tmask, a.slot_c, tshift, unique, side_n, st, vec, c, many);
     for (uint32_t v = P.vb + lane + 64; v < P.ve; v += 32)
-      probe4(t, ldv(P.sp, v), v, P.sp.shift, pn, tmask, tshift, unique, side_n, st, vec, c, many);
+      probe4(t, ldv(P.sp, v), v, P.sp.shift, pn, tmask, a.slot_c, tshift, unique, side_n, st, vec, c, many);
     c = warp_sum(c);
     if (lane == 0) a.wcnt[(uint64_t)u * HW + w] = c;
     if (__any_sync(FULL, many) && lane == 0) {
@@ -933,7 +942,7 @@ uint32_t hj_grid(gj_ctx* ctx, Kern k, size_t smem, uint32_t U) {
 }
 
 template <typename K>
-void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool swap,
+void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t skip, uint32_t B, bool swap,
                 const Partitioned& PR, const Partitioned& PS) {
   JoinCache& jc = ctx->jc;
   const gj_rel& Bld = swap ? S : R;
@@ -997,6 +1006,11 @@ void count_impl(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool 
     a.meta = meta;
     a.wcnt = wcnt;
     a.swap = swap;
+    // slot constant: khash's << the consumed hash bits while 13 (the largest table)
+    // more bits remain below them, else slot_hash's
+    const uint32_t hbits = skip + B;
+    const uint64_t sc = ctx->fib_slots && hbits + 13 <= 32 ? 0x9E3779B97F4A7C15ull << hbits : 0xD6E8FEB86659FD93ull;
+    a.slot_c = make_uint2((uint32_t)sc, (uint32_t)(sc >> 32));
     const size_t smem = sizeof(K) == 4 ? I32_SMEM : hj_smem<K, false>();
     if (sizeof(K) == 4) {
       set_smem(ctx, hj_count_i32, smem);
@@ -1069,10 +1083,10 @@ void write_impl(gj_ctx* ctx, uint32_t* out) {
 
 }  // namespace
 
-void hash_join_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t B, bool swap,
+void hash_join_count(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t skip, uint32_t B, bool swap,
                      const Partitioned& PR, const Partitioned& PS) {
-  if (R.key_type == GJ_I32) count_impl<int32_t>(ctx, R, S, B, swap, PR, PS);
-  else count_impl<int64_t>(ctx, R, S, B, swap, PR, PS);
+  if (R.key_type == GJ_I32) count_impl<int32_t>(ctx, R, S, skip, B, swap, PR, PS);
+  else count_impl<int64_t>(ctx, R, S, skip, B, swap, PR, PS);
 }
 
 void hash_join_write(gj_ctx* ctx, uint32_t* out) {

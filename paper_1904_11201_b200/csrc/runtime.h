@@ -137,6 +137,10 @@ struct gj_ctx {
 #define GJ_OVERLAP_PARTITIONS 1
 #endif
   bool overlap_partitions = GJ_OVERLAP_PARTITIONS;  // 1 GPU: partition S on `aux` beside R
+#ifndef GJ_FIB_SLOTS
+#define GJ_FIB_SLOTS 1
+#endif
+  bool fib_slots = GJ_FIB_SLOTS;  // int32 hash table: slots from the next khash bits
   // workspace (optionally from the caller's allocator hook)
   std::map<std::string, gj::Buf> bufs;
   gj_alloc_fn alloc_fn = nullptr;

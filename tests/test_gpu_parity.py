@@ -142,6 +142,19 @@ def test_equi_planner_variants(gj, ctx, bits, chunk, pchunk):
     check_equi(gj, ctx, R, S)
 
 
+@pytest.mark.parametrize("fib,bits", [(1, 4), (1, 19), (1, 20), (0, 4), (0, 19)])
+def test_equi_slot_constants(gj, ctx, fib, bits):
+    """hj_count_i32's table slots: the khash bits below the consumed ones (fib, while
+    hbits + 13 <= 32; bits = 20 falls back) or slot_hash -- dense keys (no collisions
+    under fib), duplicates and a ragged tail both ways."""
+    ctx.set_option("fib_slots", fib)
+    ctx.set_option("part_bits", bits)
+    rng = np.random.default_rng(7)
+    R = rng.permutation(40_009).astype(np.int32)
+    S = np.concatenate([rng.integers(0, 40_009, 50_003), np.full(300, 17)]).astype(np.int32)
+    check_equi(gj, ctx, R, S)
+
+
 @pytest.mark.parametrize("side", [1, 2])
 def test_equi_build_side(gj, ctx, side):
     ctx.set_option("build_side", side)

@@ -130,7 +130,7 @@ LaunchScope::~LaunchScope() noexcept(false) {
   if (ctx->profile) {
     cudaEvent_t b = get_event(ctx);
     GJ_CUDA(cudaEventRecord(b, ctx->stream));
-    ctx->pending.push_back({tag, a, b});
+    ctx->pending.push_back({tag, a, b, ctx->stream});
   }
 }
 
@@ -144,7 +144,7 @@ static int trace_level() {
 
 // GJ_TRACE=2: synchronise the stream first, so the mark times the GPU work of the phase
 void trace_sync(gj_ctx* ctx, const char* label) {
-  if (trace_level() >= 2) cudaStreamSynchronize(ctx->stream);
+  if (trace_level() == 2) cudaStreamSynchronize(ctx->stream);
   trace_mark(label);
 }
 
@@ -167,13 +167,23 @@ RegionScope::RegionScope(gj_ctx* c, const char* t) : ctx(c), tag(t), nvtx(t) {
 RegionScope::~RegionScope() {
   if (ctx->profile && a) {
     cudaEvent_t b = get_event(ctx);
-    if (cudaEventRecord(b, ctx->stream) == cudaSuccess) ctx->pending.push_back({tag, a, b});
+    if (cudaEventRecord(b, ctx->stream) == cudaSuccess) ctx->pending.push_back({tag, a, b, ctx->stream});
   }
 }
 
 static void flush_prof(gj_ctx* ctx) {
   if (ctx->pending.empty()) return;
   GJ_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (trace_level() >= 3) {  // timeline of this API call: start offset, duration, stream
+    const cudaEvent_t t0 = ctx->pending.front().a;
+    for (auto& p : ctx->pending) {
+      float st = 0.f, ms = 0.f;
+      GJ_CUDA(cudaEventElapsedTime(&st, t0, p.a));
+      GJ_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+      std::fprintf(stderr, "[gj tl %d] %-22s %s %8.4f +%7.4f ms\n", (int)getpid(), p.tag,
+                   p.s == ctx->aux && ctx->aux ? "aux " : "main", st, ms);
+    }
+  }
   for (auto& p : ctx->pending) {
     float ms = 0.f;
     GJ_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));

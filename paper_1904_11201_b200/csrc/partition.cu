@@ -36,7 +36,10 @@ namespace {
 constexpr int PT = 256;          // threads per CTA
 constexpr int PI = GJ_SCATTER_PI;  // items per thread per tile
 constexpr int TILE = PT * PI;    // 4096 tuples per tile
-constexpr int CHUNK = 65536;     // tuples per chunk
+#ifndef GJ_PART_CHUNK
+#define GJ_PART_CHUNK 65536
+#endif
+constexpr int CHUNK = GJ_PART_CHUNK;  // tuples per chunk (one part_hist CTA)
 constexpr int TPC = CHUNK / TILE;  // tiles per chunk
 constexpr int NW = PT / 32;
 constexpr int MAX_BITS = 9;      // digits per pass <= 512

@@ -109,6 +109,7 @@ struct ScanState {
 struct ProfRec {
   const char* tag;
   cudaEvent_t a, b;
+  cudaStream_t s;  // the stream both events were recorded on (GJ_TRACE=3 timeline)
 };
 
 }  // namespace gj
@@ -124,7 +125,10 @@ struct gj_ctx {
   bool profile = false;
   uint32_t nlj_split = 0;
   bool force_slow_band = false;
-  bool overlap_shuffle = true;   // multi-GPU equi: S shuffle on a 2nd stream beside R's local passes
+#ifndef GJ_OVERLAP_SHUFFLE
+#define GJ_OVERLAP_SHUFFLE 1
+#endif
+  bool overlap_shuffle = GJ_OVERLAP_SHUFFLE;  // multi-GPU equi: S shuffle on a 2nd stream beside R's local passes
   bool check_args = false;       // collective calls verify the ranks agree on their arguments
   int shuffle_ctas = 0;          // CTAs of that S shuffle scatter (0 = half the resident CTAs, -1 = all)
   int shuffle_grid_cap = 0;      // set by the dist code for the launch in flight (0 = no cap)
@@ -190,6 +194,8 @@ struct LaunchScope {
 };
 
 // Host-side phase trace (env GJ_TRACE=1): wall-clock ms since the previous mark, to stderr.
+// GJ_TRACE=3 with the profile option: per API call, every launch / region with its
+// start offset, duration and stream (main / aux), from the profiling events.
 void trace_mark(const char* label);
 void trace_sync(gj_ctx* ctx, const char* label);  // GJ_TRACE=2: stream sync first
 

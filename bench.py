@@ -332,7 +332,9 @@ def run_ours(args, world, rank, local):
         out = torch.empty((max(int(n * 1.2) + 1024, 1), 2), dtype=torch.int32, device=dev)
 
         def step():
-            if comm is None:
+            if comm is None and not args.two_call_step:  # count -> scan -> write in one C-ABI call
+                m = gj.join_count_materialize(ctx, R, S, out).shape[0]
+            elif comm is None:
                 m = gj.join_count(ctx, R, S)
                 gj.join_materialize(ctx, R, S, m, out=out)
             else:
@@ -356,6 +358,9 @@ def run_ours(args, world, rank, local):
         out = torch.empty((max(int(n * 1.2) + 1024, 1), 2), dtype=torch.int32, device=dev)
 
         def step():
+            if comm is None and not args.two_call_step:
+                kR, rR, kS, rS = gj.prefilter(ctx, R, S, PF, "eq", 0, 8.0)
+                return gj.join_count_materialize(ctx, gj.Rel(kR, rR), gj.Rel(kS, rS), out).shape[0]
             m, (R2, S2), _ = pf_step_count()
             if comm is None:
                 gj.join_materialize(ctx, R2, S2, m, out=out)
@@ -672,6 +677,9 @@ def main():
     ap.add_argument("--c4-skew", action="store_true", help="c4: Zipf-clustered keys, eps = 16 (a perf point)")
     ap.add_argument("--c2-sparse", action="store_true",
                     help="c2: R keys drawn from a permutation of [0, 2^31) instead of [0, 2^(27+log2 N))")
+    ap.add_argument("--two-call-step", action="store_true",
+                    help="1-GPU equi step as join_count + join_materialize (two C-ABI calls) instead of "
+                         "join_count_materialize (A/B of the host round trip between count and write)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-sample-bits", type=int, default=23)

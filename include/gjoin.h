@@ -203,10 +203,17 @@ gj_status gj_join_local_sizes(gj_ctx* ctx, uint64_t* n_R, uint64_t* n_S);
  * join_materialize: writes |J| pairs to out[0 .. 2*|J|) (device uint32, caller-
  *   allocated, `capacity` pairs).  Reuses the cache of the immediately preceding
  *   join_count on the same R, S (same pointers, sizes, types, rid bases); else
- *   recomputes.  *n_written = |J| (host).  GJ_ERANGE if capacity < |J|. */
+ *   recomputes.  *n_written = |J| (host).  GJ_ERANGE if capacity < |J|.
+ * join_count_materialize: join_count followed by join_materialize in one call
+ *   (always counts afresh): the write pass is launched as soon as the count's one
+ *   host read-back returns, with no return to the caller in between.  *n_written =
+ *   |J|; GJ_ERANGE (nothing written, *n_written = |J|, the count cached for a
+ *   join_materialize into a larger buffer) if capacity < |J|. */
 gj_status join_count(gj_ctx* ctx, gj_rel R, gj_rel S, uint64_t* n_out);
 gj_status join_materialize(gj_ctx* ctx, gj_rel R, gj_rel S, uint32_t* out, uint64_t capacity,
                            uint64_t* n_written);
+gj_status join_count_materialize(gj_ctx* ctx, gj_rel R, gj_rel S, uint32_t* out, uint64_t capacity,
+                                 uint64_t* n_written);
 
 /* ---------------------------------------------------------------- theta join
  * Tiled nested-loop join (§3.3.1; theta = NLJ with a predicate,

@@ -89,6 +89,7 @@ def _load():
     L.gj_ctx_kernel_times.restype = i32
     L.join_count.argtypes = [vp, _Rel, _Rel, pu64]
     L.join_materialize.argtypes = [vp, _Rel, _Rel, vp, u64, pu64]
+    L.join_count_materialize.argtypes = [vp, _Rel, _Rel, vp, u64, pu64]
     L.theta_join_count.argtypes = [vp, _Rel, _Rel, i32, u64, pu64]
     L.theta_join_materialize.argtypes = [vp, _Rel, _Rel, i32, u64, vp, u64, pu64]
     L.prefilter.argtypes = [vp, _Rel, _Rel, u32, i32, u64, ctypes.c_double, vp, vp, pu64, vp, vp, pu64]
@@ -108,7 +109,7 @@ def _load():
     L.gj_region_classify.restype = i32
     L.gj_dist_plan.argtypes = [pu64, i32, i32, i32, ctypes.POINTER(u32), ctypes.POINTER(u32), pu64]
     for f in ("gj_ctx_create", "gj_ctx_set_stream", "gj_ctx_set_allocator", "gj_ctx_set_option", "join_count", "join_materialize",
-              "theta_join_count", "theta_join_materialize", "prefilter", "join_host", "join_host_batch",
+              "join_count_materialize", "theta_join_count", "theta_join_materialize", "prefilter", "join_host", "join_host_batch",
               "gj_comm_unique_id",
               "gj_comm_init", "join_dist_count", "join_dist_count_filtered", "join_dist_materialize", "prefilter_dist",
               "theta_join_dist_count", "theta_join_dist_materialize", "gj_dist_plan"):
@@ -122,8 +123,8 @@ lib = _load()
 ABI_SYMBOLS = ("gj_ctx_create", "gj_ctx_destroy", "gj_ctx_set_stream", "gj_ctx_set_allocator", "gj_last_error", "gj_ctx_set_option",
                "gj_ctx_launch_count", "gj_ctx_reset_stats", "gj_ctx_kernel_times", "gj_theta_stats", "gj_join_stats",
                "gj_join_local_sizes", "gj_gather_payloads", "join_count",
-               "join_materialize", "theta_join_count", "theta_join_materialize", "prefilter", "join_host",
-               "join_host_batch",
+               "join_materialize", "join_count_materialize", "theta_join_count", "theta_join_materialize",
+               "prefilter", "join_host", "join_host_batch",
                "gj_comm_unique_id", "gj_comm_init", "gj_comm_destroy", "join_dist_count", "join_dist_count_filtered",
                "join_dist_materialize", "prefilter_dist", "theta_join_dist_count", "theta_join_dist_materialize",
                "gj_dist_plan",
@@ -276,6 +277,17 @@ def join_materialize(ctx: Context, R, S, n: Optional[int] = None, out: Optional[
     w = ctypes.c_uint64()
     _check(lib.join_materialize(ctx.h, _rel(R), _rel(S), ctypes.c_void_p(buf.data_ptr()), buf.shape[0],
                                 ctypes.byref(w)))
+    return buf[: w.value]
+
+
+def join_count_materialize(ctx: Context, R, S, out: torch.Tensor):
+    """Count and write in one C-ABI call (the write launched right after the count's
+    host read-back); out = a (capacity, 2) 32-bit CUDA tensor.  Returns the (|J|, 2)
+    view; raises GJ_ERANGE if capacity < |J|."""
+    buf = _out(0, out, None)
+    w = ctypes.c_uint64()
+    _check(lib.join_count_materialize(ctx.h, _rel(R), _rel(S), ctypes.c_void_p(buf.data_ptr()), buf.shape[0],
+                                      ctypes.byref(w)))
     return buf[: w.value]
 
 

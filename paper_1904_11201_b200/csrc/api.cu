@@ -546,6 +546,24 @@ gj_status join_materialize(gj_ctx* ctx, gj_rel R, gj_rel S, uint32_t* out, uint6
   API_END
 }
 
+gj_status join_count_materialize(gj_ctx* ctx, gj_rel R, gj_rel S, uint32_t* out, uint64_t capacity,
+                                 uint64_t* n_written) {
+  API_BEGIN
+  if (!ctx || !n_written) throw Error(GJ_EINVAL, "join_count_materialize: NULL ctx or n_written");
+  check_pair(R, S);
+  if (reinterpret_cast<uintptr_t>(out) % 8)
+    throw Error(GJ_EINVAL, "join_count_materialize: out must be 8-byte aligned");
+  do_join_count(ctx, R, S);
+  const JoinCache& jc = ctx->jc;
+  *n_written = jc.total;
+  if (capacity < jc.total)
+    throw Error(GJ_ERANGE, "join_count_materialize: capacity " + std::to_string(capacity) + " < |J| = " +
+                               std::to_string(jc.total));
+  if (jc.total && !out) throw Error(GJ_EINVAL, "join_count_materialize: out is NULL");
+  hash_join_write(ctx, out);
+  API_END
+}
+
 gj_status theta_join_count(gj_ctx* ctx, gj_rel R, gj_rel S, int op, uint64_t eps, uint64_t* n_out) {
   API_BEGIN
   if (!ctx || !n_out) throw Error(GJ_EINVAL, "theta_join_count: NULL ctx or n_out");

@@ -155,6 +155,29 @@ def test_equi_slot_constants(gj, ctx, fib, bits):
     check_equi(gj, ctx, R, S)
 
 
+def test_join_count_materialize(gj, ctx):
+    """The fused call equals count + materialize (same pairs at the same positions),
+    counts afresh every call, and reports GJ_ERANGE with nothing written when short."""
+    import torch
+    rng = np.random.default_rng(11)
+    R = dev(rng.integers(0, 3000, 20_011).astype(np.int32))
+    S = dev(rng.integers(0, 3000, 30_007).astype(np.int32))
+    n = gj.join_count(ctx, R, S)
+    ref = gj.join_materialize(ctx, R, S, n).clone()
+    out = torch.full((n + 5, 2), -1, dtype=torch.int32, device="cuda")
+    got = gj.join_count_materialize(ctx, R, S, out)
+    assert got.shape[0] == n and torch.equal(got, ref)
+    assert int((out[n:] == -1).sum()) == 10
+    S[0] = S[1]  # same pointers, new contents: the fused call must not reuse the cache
+    n2 = gj.join_count(ctx, R, S)
+    got2 = gj.join_count_materialize(ctx, R, S, out)
+    assert got2.shape[0] == n2 and np.array_equal(canon_gpu(got2), canon_gpu(gj.join_materialize(ctx, R, S, n2)))
+    small = torch.full((n2 - 1, 2), -1, dtype=torch.int32, device="cuda")
+    with pytest.raises(gj.GJError, match="GJ_ERANGE"):
+        gj.join_count_materialize(ctx, R, S, small)
+    assert int((small == -1).sum()) == small.numel()
+
+
 @pytest.mark.parametrize("side", [1, 2])
 def test_equi_build_side(gj, ctx, side):
     ctx.set_option("build_side", side)

@@ -177,8 +177,34 @@ void fused_shuffle(gj_ctx* ctx, gj_comm* c, const gj_rel* const X[2], uint32_t b
   const uint32_t G1 = g + b1, D1 = 1u << G1, L1 = 1u << b1;
   trace_sync(ctx, "fused: start");
   ShufflePass SP[2];
-  for (int rel = 0; rel < 2; ++rel)
-    if (X[rel]) SP[rel] = shuffle_prepare(ctx, *X[rel], G1, rel ? "sS" : "sR");
+#ifndef GJ_OVERLAP_SHUFFLE_PREP
+#define GJ_OVERLAP_SHUFFLE_PREP 1
+#endif
+  if (GJ_OVERLAP_SHUFFLE_PREP && s_ready && X[0] && X[1]) {
+    // the two relations' shuffle histograms / plans side by side: S's on the second
+    // stream (its own scratch "sS.*"), so each fills the other's partial last wave
+    if (!ctx->aux) {
+      GJ_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+      for (auto& e : ctx->aux_ev) GJ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaStream_t main_stream = ctx->stream;
+    GJ_CUDA(cudaEventRecord(ctx->aux_ev[0], main_stream));
+    GJ_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev[0], 0));
+    ctx->stream = ctx->aux;
+    try {
+      SP[1] = shuffle_prepare(ctx, *X[1], G1, "sS");
+    } catch (...) {
+      ctx->stream = main_stream;
+      throw;
+    }
+    GJ_CUDA(cudaEventRecord(ctx->aux_ev[1], ctx->aux));
+    ctx->stream = main_stream;
+    SP[0] = shuffle_prepare(ctx, *X[0], G1, "sR");
+    GJ_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));
+  } else {
+    for (int rel = 0; rel < 2; ++rel)
+      if (X[rel]) SP[rel] = shuffle_prepare(ctx, *X[rel], G1, rel ? "sS" : "sR");
+  }
   trace_sync(ctx, "fused: shuffle hist");
   // per rank: 2 x D1 run counts + its key width (all ranks must agree on it)
   const size_t row = 2 * (size_t)D1 + 1;

@@ -219,6 +219,18 @@ static bool same_rel(const gj_rel& a, const gj_rel& b) {
   return a.key == b.key && a.rid == b.rid && a.n == b.n && a.key_type == b.key_type && a.rid_base == b.rid_base;
 }
 
+#ifndef GJ_AUX_PRIORITY
+#define GJ_AUX_PRIORITY 0  // 1: the second stream at the device's greatest priority, -1: least
+#endif
+void ensure_aux(gj_ctx* ctx) {
+  if (ctx->aux) return;
+  int least = 0, greatest = 0;
+  GJ_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  const int prio = GJ_AUX_PRIORITY > 0 ? greatest : (GJ_AUX_PRIORITY < 0 ? least : 0);
+  GJ_CUDA(cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, prio));
+  for (auto& e : ctx->aux_ev) GJ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
 uint32_t auto_bits(gj_ctx* ctx, uint64_t nb) {
   if (ctx->part_bits >= 0) return (uint32_t)ctx->part_bits;
   // mean build tuples per partition within [target/sqrt2, target*sqrt2]: B rounds
@@ -258,10 +270,7 @@ void join_count_core(gj_ctx* ctx, const gj_rel& R, const gj_rel& S, uint32_t ski
     // single GPU: S is partitioned on the ctx's second stream beside R, so each
     // relation's kernels fill the other's tails (partial last waves); separate scratch
     // per relation ("R.*", "S.*"), scan state per stream
-    if (!ctx->aux) {
-      GJ_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
-      for (auto& e : ctx->aux_ev) GJ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
+    ensure_aux(ctx);
     cudaStream_t main_stream = ctx->stream;
     GJ_CUDA(cudaEventRecord(ctx->aux_ev[0], main_stream));
     GJ_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev[0], 0));

@@ -183,10 +183,7 @@ void fused_shuffle(gj_ctx* ctx, gj_comm* c, const gj_rel* const X[2], uint32_t b
   if (GJ_OVERLAP_SHUFFLE_PREP && s_ready && X[0] && X[1]) {
     // the two relations' shuffle histograms / plans side by side: S's on the second
     // stream (its own scratch "sS.*"), so each fills the other's partial last wave
-    if (!ctx->aux) {
-      GJ_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
-      for (auto& e : ctx->aux_ev) GJ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
+    ensure_aux(ctx);
     cudaStream_t main_stream = ctx->stream;
     GJ_CUDA(cudaEventRecord(ctx->aux_ev[0], main_stream));
     GJ_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev[0], 0));
@@ -285,10 +282,7 @@ void fused_shuffle(gj_ctx* ctx, gj_comm* c, const gj_rel* const X[2], uint32_t b
     if (!X[rel]) continue;
     if (overlap && rel == 1) {
       barrier("shuffle_barrier");
-      if (!ctx->aux) {
-        GJ_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
-        for (auto& e : ctx->aux_ev) GJ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      }
+      ensure_aux(ctx);
       GJ_CUDA(cudaEventRecord(ctx->aux_ev[0], main_stream));
       GJ_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev[0], 0));
       ctx->stream = ctx->aux;

@@ -197,6 +197,8 @@ struct LaunchScope {
 // GJ_TRACE=3 with the profile option: per API call, every launch / region with its
 // start offset, duration and stream (main / aux), from the profiling events.
 void trace_mark(const char* label);
+// creates the ctx's second stream (and its events) on first use
+void ensure_aux(gj_ctx* ctx);
 void trace_sync(gj_ctx* ctx, const char* label);  // GJ_TRACE=2: stream sync first
 
 // NVTX range for the lifetime of the object (every C-ABI entry point and every

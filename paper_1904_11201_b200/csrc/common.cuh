@@ -80,6 +80,11 @@ __device__ __forceinline__ T warp_sum(T v) {
 
 // ------------------------------------------------- 1-D TMA (bulk copy) + mbarrier
 __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// First statement of every library kernel: with programmatic dependent launch
+// (runtime.h launch()) a kernel's CTAs may be dispatched before the previous kernel
+// in the stream has completed; this waits for it (and its memory) before any access.
+// A no-op for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
 }

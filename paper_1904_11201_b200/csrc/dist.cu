@@ -81,13 +81,16 @@ namespace gj {
 namespace {
 
 __global__ void bucket_counts(const uint32_t* __restrict__ off, uint32_t G, unsigned long long* __restrict__ out) {
+  pdl_wait();
   const uint32_t p = threadIdx.x;
   if (p < G) out[p] = off[p + 1] - off[p];
 }
 __global__ void run_counts(const uint32_t* __restrict__ off, uint32_t D, uint32_t* __restrict__ out) {
+  pdl_wait();
   for (uint32_t d = threadIdx.x; d < D; d += blockDim.x) out[d] = off[d + 1] - off[d];
 }
 __global__ void fill_rids(uint32_t* __restrict__ out, uint64_t n, uint32_t base) {
+  pdl_wait();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     out[i] = base + (uint32_t)i;
 }

@@ -20,6 +20,7 @@ template <int W32>
 __global__ void gather_kernel(const uint2* __restrict__ pairs, uint64_t n, const uint32_t* __restrict__ pR,
                               uint32_t baseR, const uint32_t* __restrict__ pS, uint32_t baseS, uint32_t* __restrict__ oR,
                               uint32_t* __restrict__ oS, uint32_t wR, uint32_t wS) {
+  pdl_wait();
   const uint32_t wr = W32 ? (uint32_t)W32 : wR, ws_ = W32 ? (uint32_t)W32 : wS;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint2 p = pairs[i];

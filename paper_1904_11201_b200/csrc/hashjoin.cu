@@ -284,6 +284,7 @@ template <typename K>
 __global__ void __launch_bounds__(HT) hj_count_kernel(HJArgs a, uint16_t* __restrict__ stage,
                                                       uint8_t* __restrict__ multi,
                                                       unsigned long long* __restrict__ nmulti) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_dup;
   Table<K> tab;
@@ -571,6 +572,7 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 __global__ void __launch_bounds__(HT, GJ_HJ_MINB) hj_count_i32(HJArgs a, uint16_t* __restrict__ stage,
                                                       uint8_t* __restrict__ multi,
                                                       unsigned long long* __restrict__ nmulti) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_dup, s_side;
   const uint32_t tb = saddr(smem);
@@ -683,6 +685,7 @@ struct MultiSmem {
 
 template <typename K>
 __global__ void __launch_bounds__(HT) hj_write_kernel(HJArgs a, const uint8_t* __restrict__ multi) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t smem[];
   using L = MultiSmem<K>;
   K* bk = reinterpret_cast<K*>(smem);
@@ -825,6 +828,7 @@ __device__ __forceinline__ void wf_issue(WBuf<WP>& B, uint64_t* bar, const uint4
 template <typename K, uint32_t WP>
 __global__ void __launch_bounds__(HT) hj_write_fast(HJArgs a, const uint16_t* __restrict__ stage,
                                                     const uint8_t* __restrict__ multi) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr uint32_t N = KVec<K>::N;
   using Buf = WBuf<WP>;
@@ -885,6 +889,7 @@ __global__ void __launch_bounds__(HT) hj_write_fast(HJArgs a, const uint16_t* __
 __global__ void hj_units(const uint32_t* __restrict__ boff, const uint32_t* __restrict__ poff, uint32_t P,
                          uint32_t bchunk, uint32_t pchunk, unsigned long long* __restrict__ nunits,
                          unsigned long long* __restrict__ eq8) {
+  pdl_wait();
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long prod = 0;
   if (p < P) {
@@ -908,6 +913,7 @@ __global__ void hj_unit_desc(const unsigned long long* __restrict__ unit_off, co
                              const uint32_t* __restrict__ poff, uint32_t P, uint32_t cap, uint32_t bchunk,
                              uint32_t pchunk, uint4* __restrict__ desc, uint8_t* __restrict__ multi,
                              unsigned long long* __restrict__ meta) {
+  pdl_wait();
   const unsigned long long U = unit_off[P];
   const uint32_t Ue = U <= cap ? (uint32_t)U : 0u;
   if (blockIdx.x == 0 && threadIdx.x == 0) {

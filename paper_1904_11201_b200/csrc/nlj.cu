@@ -201,6 +201,7 @@ __device__ __noinline__ uint64_t emit_group(const uint32_t* rf, const uint32_t* 
 
 template <typename K, int OP, bool FAST, bool WRITE>
 __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
   K* sbuf = reinterpret_cast<K*>(smem);  // STG * TS keys
   __shared__ __align__(8) uint64_t bar[STG];
@@ -435,6 +436,7 @@ __global__ void __launch_bounds__(NT) nlj_kernel(NLJArgs a) {
 
 template <typename K>
 __global__ void minmax_kernel(const K* __restrict__ key, uint64_t n, unsigned long long* mm) {
+  pdl_wait();
   unsigned long long lo = ~0ull, hi = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     unsigned long long b = (unsigned long long)KeyT<K>::bias(key[i]);
@@ -452,12 +454,14 @@ __global__ void minmax_kernel(const K* __restrict__ key, uint64_t n, unsigned lo
   }
 }
 __global__ void minmax_init(unsigned long long* mm) {
+  pdl_wait();
   mm[0] = ~0ull;
   mm[1] = 0;
 }
 
 __global__ void cross_kernel(const uint32_t* __restrict__ rrid, uint32_t rbase, uint64_t nR,
                              const uint32_t* __restrict__ srid, uint32_t sbase, uint64_t nS, uint2* out) {
+  pdl_wait();
   const uint64_t total = nR * nS;
   for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = x / nS, j = x - i * nS;
@@ -470,6 +474,7 @@ __global__ void cross_kernel(const uint32_t* __restrict__ rrid, uint32_t rbase, 
 // base[b].  CTAs stride over the pairs of every rectangle in turn.
 __global__ void cross_rect_kernel(const uint4* __restrict__ rect, const uint64_t* __restrict__ base, uint32_t nrect,
                                   const uint32_t* __restrict__ rrid, const uint32_t* __restrict__ srid, uint2* out) {
+  pdl_wait();
   for (uint32_t b = 0; b < nrect; ++b) {
     const uint4 q = rect[b];
     const uint64_t total = (uint64_t)q.y * q.w, o = base[b];
@@ -673,6 +678,7 @@ template <typename K>
 __global__ void band_heavy_kernel(const uint32_t* __restrict__ ro, const uint32_t* __restrict__ so, uint32_t P,
                                   uint32_t m, int32_t g, uint4* __restrict__ hb, uint32_t* __restrict__ nh,
                                   uint32_t cap) {
+  pdl_wait();
   for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < P; x += gridDim.x * blockDim.x) {
     if (ro[x + 1] == ro[x]) continue;
     uint32_t rb, gb, ge, re, l0, l1, h0, h1;
@@ -690,6 +696,7 @@ __global__ void band_heavy_kernel(const uint32_t* __restrict__ ro, const uint32_
 
 template <typename K, bool FAST>
 __global__ void __launch_bounds__(256) band_count_kernel(BandArgs<K> a) {
+  pdl_wait();
   const uint32_t lane = lane_id();
   const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
   unsigned long long red_n = 0, green_n = 0;
@@ -757,6 +764,7 @@ constexpr size_t BW_SMEM = (size_t)BW_CAP * 4;
 #endif
 template <typename K, bool FAST>
 __global__ void __launch_bounds__(BW_ROWS, GJ_BW_MINB) band_write_kernel(BandArgs<K> a) {
+  pdl_wait();
   extern __shared__ __align__(16) uint32_t s_rid[];  // BW_CAP
   __shared__ uint32_t s_win[2];
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;

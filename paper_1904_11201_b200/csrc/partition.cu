@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(PT, sizeof(K) == 4 ? 4 : 3) part_hist(const K*
                                                 uint32_t nseg, uint32_t shift, uint32_t bits,
                                                 uint32_t* __restrict__ hist, uint32_t* __restrict__ tile_pref,
                                                 uint16_t* __restrict__ tile_st, DigitFn fn) {
+  pdl_wait();
   __shared__ uint32_t h[(1 << MAX_BITS) + 1];
   __shared__ uint32_t wsum[PT / 32];
   const uint32_t D = 1u << bits, mask = D - 1;
@@ -276,6 +277,7 @@ __global__ void __launch_bounds__(PT, SCATTER_MINB) part_scatter(
     const uint4* __restrict__ tdesc, uint32_t ntiles, uint32_t shift, uint32_t bits,
     const uint32_t* __restrict__ tile_base, const uint16_t* __restrict__ tile_st, K* __restrict__ key_out,
     uint32_t* __restrict__ rid_out, uint32_t* __restrict__ tile_ctr, DigitFn fn, ShuffleDest dst) {
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   using L = ScatterLayout<K>;
   constexpr bool ILV = sizeof(K) == 4 && !REMOTE;  // int32 local: one (key, rid) uint2 per staging slot
@@ -572,6 +574,7 @@ __global__ void __launch_bounds__(PT) tile_base_kernel(uint64_t n, const uint32_
                                                        uint32_t bits, const uint32_t* __restrict__ scanned,
                                                        uint32_t* __restrict__ tile_pref, uint4* __restrict__ tdesc,
                                                        uint32_t* __restrict__ tile_ctr, uint32_t* __restrict__ off) {
+  pdl_wait();
   const uint32_t c = blockIdx.x, D = 1u << bits;
   if (c == 0 && threadIdx.x == 0) *tile_ctr = 0;
   // the pass's output partition starts (folded in here: one launch fewer per pass)
@@ -646,6 +649,7 @@ void launch_scatter(gj_ctx* ctx, const K* kin, const uint32_t* rin, uint32_t rid
 // counts), chunk_base[nseg] = total chunks: one CTA.
 __global__ void __launch_bounds__(1024) chunk_base_kernel(const uint32_t* __restrict__ seg_off, uint32_t nseg,
                                                           uint32_t* __restrict__ cb) {
+  pdl_wait();
   __shared__ uint32_t wsum[32];
   __shared__ uint32_t carry;
   if (threadIdx.x == 0) carry = 0;
@@ -668,6 +672,7 @@ __global__ void __launch_bounds__(1024) chunk_base_kernel(const uint32_t* __rest
 }
 
 __global__ void fill_off2(uint32_t* off, uint64_t n) {
+  pdl_wait();
   off[0] = 0;
   off[1] = (uint32_t)n;
 }

@@ -73,6 +73,7 @@ __device__ __forceinline__ bool set_contains(K k, const Filt& f) {
 template <typename K>
 __global__ void set_build(const K* __restrict__ key, uint64_t n, Filt range, void* set, uint32_t lg,
                           uint32_t* has_top) {
+  pdl_wait();
   using U = typename KeyT<K>::U;
   U* t = static_cast<U*>(set);
   const uint64_t mask = (1ull << lg) - 1;
@@ -154,6 +155,7 @@ template <typename K>
 __global__ void bloom_build(const K* __restrict__ key, uint64_t n, Filt range, uint32_t* __restrict__ bloom,
                             uint32_t log_blocks, uint32_t blk_lo, uint32_t blk_hi, const uint32_t* __restrict__ off,
                             uint32_t p) {
+  pdl_wait();
   if (off) {
     key += off[p];
     n = off[p + 1] - off[p];
@@ -173,6 +175,7 @@ __global__ void bloom_build(const K* __restrict__ key, uint64_t n, Filt range, u
 // filters of one rank's shard, before the ranks OR them together (prefilter_dist).
 template <typename K>
 __global__ void bloom_build_dest(const K* __restrict__ key, uint64_t n, Filt range, uint32_t* __restrict__ words) {
+  pdl_wait();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const K k = key[i];
     if (!keep(k, range)) continue;
@@ -185,6 +188,7 @@ __global__ void bloom_build_dest(const K* __restrict__ key, uint64_t n, Filt ran
 
 // dst[i] = OR over the G pieces src[g * nw + i] (the owner's view of everyone's filter)
 __global__ void bloom_or(const uint4* __restrict__ src, uint64_t nw4, uint32_t G, uint4* __restrict__ dst) {
+  pdl_wait();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw4; i += (uint64_t)gridDim.x * blockDim.x) {
     uint4 a = src[i];
     for (uint32_t g = 1; g < G; ++g) {
@@ -201,6 +205,7 @@ __global__ void bloom_or(const uint4* __restrict__ src, uint64_t nw4, uint32_t G
 template <typename K>
 __global__ void __launch_bounds__(FT) pf_count(const K* __restrict__ key, uint64_t n, Filt f,
                                                uint32_t* __restrict__ flags, uint32_t* __restrict__ tile_cnt) {
+  pdl_wait();
   const uint32_t w = threadIdx.x >> 5, lane = lane_id();
   const uint64_t wb = (uint64_t)blockIdx.x * FTILE + (uint64_t)w * 32 * FI;
   uint32_t c = 0;
@@ -239,6 +244,7 @@ __global__ void __launch_bounds__(FT) pf_write(const K* __restrict__ key, const 
                                                uint32_t rid_base, uint64_t n, const uint32_t* __restrict__ flags,
                                                const uint32_t* __restrict__ tile_off, K* __restrict__ kout,
                                                uint32_t* __restrict__ rout) {
+  pdl_wait();
   __shared__ uint32_t woff[FT / 32];
   const uint32_t w = threadIdx.x >> 5, lane = lane_id();
   const uint64_t wb = (uint64_t)blockIdx.x * FTILE + (uint64_t)w * 32 * FI;

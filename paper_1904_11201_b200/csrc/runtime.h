@@ -145,6 +145,10 @@ struct gj_ctx {
 #define GJ_FIB_SLOTS 1
 #endif
   bool fib_slots = GJ_FIB_SLOTS;  // int32 hash table: slots from the next khash bits
+#ifndef GJ_PDL
+#define GJ_PDL 1
+#endif
+  bool pdl = GJ_PDL;  // launch with programmatic stream serialization
   // workspace (optionally from the caller's allocator hook)
   std::map<std::string, gj::Buf> bufs;
   gj_alloc_fn alloc_fn = nullptr;
@@ -229,7 +233,23 @@ inline void launch(gj_ctx* ctx, const char* tag, void (*k)(KArgs...), dim3 grid,
                    size_t smem, Args... args) {
   if (grid.x == 0 || grid.y == 0 || grid.z == 0) return;
   LaunchScope ls(ctx, tag);
-  k<<<grid, block, smem, ctx->stream>>>(static_cast<KArgs>(args)...);
+  if (ctx->pdl) {
+    // programmatic dependent launch: the kernel may be dispatched while the previous
+    // one in the stream drains (every kernel starts with pdl_wait())
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+  } else {
+    k<<<grid, block, smem, ctx->stream>>>(static_cast<KArgs>(args)...);
+  }
 }
 
 // Opt a kernel into > 48 KB dynamic shared memory.  The attribute belongs to the

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(SCAN_T) scan_lookback(const TIn* in, TOut* out
                                                         typename TileStatus<TOut>::W* __restrict__ status,
                                                         unsigned long long* __restrict__ ticket,
                                                         unsigned long long ticket_base, uint32_t epoch) {
+  pdl_wait();
   using S = TileStatus<TOut>;
   __shared__ uint32_t s_tile;
   __shared__ TOut s_prefix, s_tot;

@@ -124,7 +124,8 @@ LaunchScope::LaunchScope(gj_ctx* c, const char* t) : ctx(c), tag(t) {
 }
 
 LaunchScope::~LaunchScope() noexcept(false) {
-  cudaError_t e = cudaGetLastError();
+  const cudaError_t last = cudaGetLastError();  // also clears a launch error it reports
+  const cudaError_t e = err != cudaSuccess ? err : last;
   if (e != cudaSuccess) throw Error(GJ_ECUDA, std::string("launch ") + tag + ": " + cudaGetErrorString(e));
   ++ctx->launches;
   if (ctx->profile) {

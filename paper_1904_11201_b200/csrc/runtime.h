@@ -193,6 +193,7 @@ struct LaunchScope {
   gj_ctx* ctx;
   const char* tag;
   cudaEvent_t a = nullptr;
+  cudaError_t err = cudaSuccess;  // the launch call's own status (cudaLaunchKernelEx)
   LaunchScope(gj_ctx* c, const char* t);
   ~LaunchScope() noexcept(false);
 };
@@ -246,7 +247,7 @@ inline void launch(gj_ctx* ctx, const char* tag, void (*k)(KArgs...), dim3 grid,
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+    ls.err = cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
   } else {
     k<<<grid, block, smem, ctx->stream>>>(static_cast<KArgs>(args)...);
   }

@@ -108,7 +108,10 @@ __device__ __forceinline__ void load_tile(const K* __restrict__ key, const uint3
 // int32: a 4-CTA/SM register budget (64 registers) measured 0.1228 vs 0.1248 ms at
 // configs[1] (6 CTAs/SM: 40 registers + spills, 0.1307 ms); int64 keeps 3 (80).
 template <typename K, bool RANGE>
-__global__ void __launch_bounds__(PT, sizeof(K) == 4 ? 4 : 3) part_hist(const K* __restrict__ key, uint64_t n,
+#ifndef GJ_HIST_MINB
+#define GJ_HIST_MINB 4
+#endif
+__global__ void __launch_bounds__(PT, sizeof(K) == 4 ? GJ_HIST_MINB : 3) part_hist(const K* __restrict__ key, uint64_t n,
                                                 const uint32_t* __restrict__ seg_off,
                                                 const uint32_t* __restrict__ chunk_base,
                                                 uint32_t nseg, uint32_t shift, uint32_t bits,
